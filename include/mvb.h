@@ -1,0 +1,217 @@
+/*
+ * mvb.h -- C ABI of libmvb.so, the B200 (sm_100a) moving-source synthesis
+ * library (arXiv 2508.03065 hot path).  Drop-in boundary for the reference
+ * package `moverb` (paths below are relative to /root/reference/pkg/src/moverb/).
+ *
+ * Conventions
+ *   - every entry point returns int: MVB_OK (0) or a negative MVB_E* code;
+ *     mvb_last_error() returns the message of the calling thread's last
+ *     failure.  No C++ exception crosses the ABI.
+ *   - pointers named d_* are DEVICE pointers owned by the caller (e.g. torch
+ *     tensors); h_* are host pointers read synchronously during the call.
+ *   - every launch is ordered on the caller's `stream` (a cudaStream_t, NULL =
+ *     legacy default stream); calls never synchronize the device unless they
+ *     say so.  No global mutable state.
+ *   - there is no CPU implementation behind any of these symbols.
+ */
+#ifndef MVB_H
+#define MVB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MVB_ABI_VERSION 1
+
+#define MVB_OK 0
+#define MVB_EINVAL (-1) /* bad argument (size, null pointer, range)           */
+#define MVB_ECUDA (-2)  /* CUDA launch/runtime error, or no sm_100 device     */
+
+int mvb_abi_version(void);
+const char* mvb_last_error(void);
+/* Fills SM count and compute capability of the current device. */
+int mvb_device_info(int* h_sm_count, int* h_cc_major, int* h_cc_minor);
+/* sizeof of the structs below as compiled into the library (for bindings
+ * that pack them by hand): image, job, work, coef32. */
+int mvb_struct_sizes(int* h_image, int* h_job, int* h_work, int* h_coef32);
+
+/* ------------------------------------------------------------------------
+ * 1. Operator boundary: the reference's kernel swap point (_kernels.py:21-31).
+ *    Same semantics and fp64 arithmetic order as the numba kernels -- results
+ *    are bit-identical to the reference on identical inputs.
+ * --------------------------------------------------------------------- */
+
+/* _kernels.py:65-78 distance_streams: d_out (S,T) = |offset + sign*pos - mic| */
+int mvb_distance_streams(const double* d_offset, const double* d_sign, const double* d_mic,
+                         const double* d_pos, int64_t S, int64_t T, double* d_out,
+                         void* stream);
+
+/* _kernels.py:126-136 accumulate_images: mutates d_out (out_len,) in place.
+ * d_streams (n_branches, stream_len); d_tau, d_amp (S, out_len). */
+int mvb_accumulate_images(double* d_out, int64_t out_len, const double* d_streams,
+                          int64_t n_branches, int64_t stream_len, const double* d_tau,
+                          const double* d_amp, int64_t S, int64_t offset, int64_t d0,
+                          void* stream);
+
+/* _kernels.py:184-190 upsample_stream, batched over `rows` coarse sequences:
+ * d_coarse (rows, n_coarse), d_table (factor, n_taps) row-major as the
+ * reference's _phase_table, d_out (rows, out_len). */
+int mvb_upsample_streams(const double* d_coarse, int64_t rows, int64_t n_coarse,
+                         const double* d_table, int64_t factor, int64_t n_taps,
+                         int64_t out_len, double* d_out, void* stream);
+
+/* farrow.py:214-229 branch_filter: d_out (n_branches, T+L-1) = x (*) c_k,
+ * sequential fp64 sums (equal to np.convolve within rounding). */
+int mvb_branch_filter(const double* d_x, int64_t T, const double* d_branches,
+                      int64_t n_branches, int64_t L, double* d_out, void* stream);
+
+/* ------------------------------------------------------------------------
+ * 2. Image lattice (room.py:98-143 enumerate_images, room.py:175-187
+ *    as_arrays), one thread per image, canonical (order, lattice, parity)
+ *    order.  Batched over n_rooms rooms of the same max_order; every output
+ *    is (n_rooms, S, ...) and may be NULL.
+ * --------------------------------------------------------------------- */
+
+int64_t mvb_image_count(int max_order);
+int mvb_enumerate(const double* d_dims, const double* d_walls, int64_t n_rooms,
+                  int max_order, int32_t* d_lattice, int32_t* d_parity,
+                  int32_t* d_order, double* d_beta, double* d_offset, double* d_sign,
+                  void* stream);
+
+/* ------------------------------------------------------------------------
+ * 3. Fused moving-source render (synth.py:194-294 generalised to any tier
+ *    list, fixed or moving receiver, batches of scenes/channels).  A batch
+ *    is a job table (one job = one (scene, channel) output), one image
+ *    table holding every job's images, and one fp64 `paths` buffer of
+ *    (x, y, z) rows holding every source path, receiver path/position and
+ *    decimated path.  Every kernel below covers the whole batch per launch.
+ *
+ *    Call order: coarse_distances -> track_bounds -> track_max (-> host:
+ *    out_len = len(s) + ceil(rate*dmax/c) + L, synth.py:211-212) ->
+ *      fast:  branch_records_f32, track_coeffs, sort_keys, rank,
+ *             synthesize_f32 [, reduce_partials_f32]
+ *      exact: branch_filter (per signal), synthesize_f64
+ * --------------------------------------------------------------------- */
+
+/* One image of one job (96 B). */
+typedef struct mvb_image {
+    double off[3];    /* 2*lattice*dims                                     */
+    double beta;      /* product of wall reflection coefficients            */
+    float sign[3];    /* +-1 per axis                                        */
+    float amp_num;    /* beta / (4 pi), fast path                            */
+    int32_t factor;   /* decimation N of the image's tier (1 = per sample)   */
+    int32_t n_coarse; /* K = ceil(T / N) for factor > 1                       */
+    int64_t coarse;   /* first of its K coarse distances (factor > 1)        */
+    int64_t coef;     /* first of its K fast-path interval records            */
+    int64_t table;    /* first element of the factor's (65, N) transposed table */
+    int64_t cpath;    /* first row of its coarse source path in `paths`; with a
+                         moving receiver the K coarse receiver rows follow     */
+    int32_t job;      /* owning job                                           */
+    int32_t fit;      /* index of the factor's (9, 65) refit block            */
+} mvb_image;
+
+/* One (scene, channel) render. */
+typedef struct mvb_job {
+    int64_t out_off, out_len; /* slice of the flat output                       */
+    int64_t part_off;         /* slice of the partial buffer (n_chunks > 1)     */
+    int64_t rec_base;         /* record / stream index of branch sample 0       */
+    int64_t ls;               /* branch stream length len(s) + L - 1            */
+    int64_t img_off, n_img;   /* slice of the image table                       */
+    int64_t pos_off, mic_off; /* first row of the source path / receiver in paths */
+    int32_t T, mic_moving;    /* track length len(traj); receiver path has T rows */
+    int32_t L, d0;            /* branch length (= delay shift) and D0           */
+    int32_t n_chunks, nb;     /* image chunks; branches per record / stream     */
+    double rate, c, d_min, kappa; /* kappa = rate / c                           */
+} mvb_job;
+
+/* One CTA of the fast synthesis grid: samples [32U*tile, 32U*(tile+1)) of
+ * `job`, images [img_begin, img_end) of its (delay-sorted) image slice. */
+typedef struct mvb_work {
+    int32_t job, tile, img_begin, img_end, chunk, pad0, pad1, pad2;
+} mvb_work;
+
+/* Fast-path interval record: the reference's upsampled track on coarse
+ * interval k (samples kN .. kN+N-1) refit as a degree-8 polynomial in
+ * u = 2 r / N - 1, anchored and pre-split in fp64 (48 B). */
+typedef struct mvb_coef32 {
+    int32_t B;   /* floor(kappa*g0 + L - D0)                                  */
+    float f;     /* kappa*g0 + L - D0 - B - 1/2                               */
+    float d_mid; /* g0 (metres, the track at u = 0)                           */
+    float pad;
+    float g[8];  /* kappa * g_p, p = 1..8                                     */
+} mvb_coef32;
+
+/* Coarse distances of the n_sel images d_sel (factor > 1) on their coarse
+ * paths -> d_coarse[image.coarse + k], k < K.  _kernels.py:54-62 arithmetic:
+ * bitwise equal to distance_streams on decimate(traj, N).positions. */
+int mvb_coarse_distances(const mvb_image* d_images, const int32_t* d_sel, int64_t n_sel,
+                         const mvb_job* d_jobs, const double* d_paths, double* d_coarse,
+                         void* stream);
+
+/* Per-image bounds of the track maximum over t < T (synth.py:201):
+ * factor 1 images listed in d_full_sel: exact per-sample max (lb = ub);
+ * others: lb = largest coarse sample (attained), ub = rigorous bound of the
+ * band-limited reconstruction, window max + negsum * window range. */
+int mvb_track_bounds(const mvb_image* d_images, int64_t n_img, const int32_t* d_full_sel,
+                     int64_t n_full, const mvb_job* d_jobs, const double* d_paths,
+                     const double* d_coarse, double negsum, double* d_lb, double* d_ub,
+                     void* stream);
+
+/* Exact track max of every job (d_dmax[n_jobs]): the reference's 65-tap
+ * upsample is evaluated at every t < T only for the images whose ub reaches
+ * the job's largest lb.  d_scratch: n_img + n_jobs int32. */
+int mvb_track_max(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jobs,
+                  const double* d_coarse, const double* d_tables, const double* d_lb,
+                  const double* d_ub, int32_t* d_scratch, double* d_dmax, void* stream);
+
+/* Fast-path interval records of the images d_sel (factor > 1):
+ * d_coef[image.coef + k] for k < K, from the coarse distances and the
+ * factor's refit block d_fits[image.fit * 585]. */
+int mvb_track_coeffs(const mvb_image* d_images, const int32_t* d_sel, int64_t n_sel,
+                     const mvb_job* d_jobs, const double* d_coarse, const double* d_fits,
+                     mvb_coef32* d_coef, void* stream);
+
+/* Delay-sort key of every image: its distance at the middle of its job's
+ * path (coarse sample for factor > 1). */
+int mvb_sort_keys(const mvb_image* d_images, int64_t n_img, const mvb_job* d_jobs,
+                  const double* d_paths, const double* d_coarse, double* d_key, void* stream);
+
+/* Stable rank of each key inside its job's image slice (ties by index):
+ * d_rank[img_off + i] = #{j in job : k_j < k_i or (k_j == k_i and j < i)}. */
+int mvb_rank(const double* d_key, const mvb_job* d_jobs, int64_t n_jobs, int64_t max_n_img,
+             int32_t* d_rank, void* stream);
+
+/* Fast path: interleaved fp32 branch records rec[(pad + m) * nb + k] for
+ * m < T + L - 1 (v'_k = x (*) c'_k, d_cbranch (M1, L) fp64 in the centred
+ * basis (mu - 1/2)^k, zero branches k >= M1); other rows are left as the
+ * caller zeroed them.  L <= 128. */
+int mvb_branch_records_f32(const float* d_x, int64_t T, const double* d_cbranch, int M1,
+                           int L, int nb, int64_t pad, float* d_rec, void* stream);
+
+/* Fast synthesis (fp32 I/O, fp64 anchors), one CTA per work item; jobs
+ * with n_chunks > 1 write d_part[part_off + chunk*out_len + n]. */
+int mvb_synthesize_f32(const mvb_job* d_jobs, const mvb_work* d_work, int64_t n_work,
+                       const mvb_image* d_images, const mvb_coef32* d_coef,
+                       const float* d_rec, const double* d_paths, float* d_out,
+                       float* d_part, int nb, void* stream);
+
+/* Fixed-order sum of the n_chunks partial rows of every job. */
+int mvb_reduce_partials_f32(const mvb_job* d_jobs, int64_t n_jobs, int64_t max_out_len,
+                            const float* d_part, float* d_out, void* stream);
+
+/* Exact synthesis (fp64): per-sample reference arithmetic (exact or 65-tap
+ * upsampled distance, tau = (rate*d)/c, gain, floor split, Horner in mu)
+ * in the reference's summation order (32-image blocks of the canonical
+ * order, then the pairwise block tree).  d_streams holds each job's
+ * (nb, ls) branch streams at rec_base. */
+int mvb_synthesize_f64(const mvb_job* d_jobs, int64_t n_jobs, int64_t max_out_len,
+                       const mvb_image* d_images, const double* d_coarse,
+                       const double* d_tables, const double* d_streams,
+                       const double* d_paths, double* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MVB_H */

@@ -1,13 +1,25 @@
 """B200-native moving-source synthesis (arXiv 2508.03065 hot path).
 
-Drop-in for the reference package `moverb`'s render path: the public names
-mirror moverb (render, prepare_streams, synthesize, SynthesisConfig, Room,
-MicPosition, Trajectory, FarrowFilter, enumerate_images, ...), while every
-computation runs in hand-written sm_100a CUDA kernels behind the C ABI in
-include/mvb.h (libmvb.so).  There is no CPU fallback: calling a compute
-entry point without the built library or without a GPU raises.
+Drop-in for the render path of the reference package `moverb`: the public
+names mirror moverb (render, prepare_streams, synthesize, SynthesisConfig,
+Room, MicPosition, Trajectory, FarrowFilter, enumerate_images, ...), and
+every computation runs in hand-written sm_100a CUDA kernels behind the C ABI
+in include/mvb.h (libmvb.so).  There is no CPU fallback: a compute entry
+point called without the built library or without a GPU raises.
 """
 
+from ._lib import MvbError
 from .farrow import FarrowFilter, hann_sinc, split_delay
+from .room import ImageSourceSpec, MicPosition, Room, enumerate_images, image_count
+from .synth import (BudgetError, DelayStreams, SynthesisConfig, cost_report,
+                    full_rate_moving_oracle, prepare_streams, render, render_jobs, synthesize)
+from .trajectory import Trajectory, bandlimited_upsample, decimate
 
 __version__ = "0.1.0"
+
+__all__ = [
+    "BudgetError", "DelayStreams", "FarrowFilter", "ImageSourceSpec", "MicPosition", "MvbError",
+    "Room", "SynthesisConfig", "Trajectory", "bandlimited_upsample", "cost_report", "decimate",
+    "enumerate_images", "full_rate_moving_oracle", "hann_sinc", "image_count", "prepare_streams",
+    "render", "render_jobs", "split_delay", "synthesize", "__version__",
+]

@@ -1,0 +1,103 @@
+"""ctypes binding of libmvb.so (include/mvb.h).
+
+The library is the only compute backend.  Loading fails loudly when the
+shared object is missing, and every call checks that a CUDA device is
+present; there is no CPU path behind any function of this package.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmvb.so")
+
+_lock = threading.Lock()
+_lib = None
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+I32 = ctypes.c_int32
+INT = ctypes.c_int
+DBL = ctypes.c_double
+
+# name -> argtypes (all return int status unless listed in _RESTYPE)
+_SIGS = {
+    "mvb_abi_version": [],
+    "mvb_last_error": [],
+    "mvb_device_info": [P, P, P],
+    "mvb_struct_sizes": [P, P, P, P],
+    "mvb_distance_streams": [P, P, P, P, I64, I64, P, P],
+    "mvb_accumulate_images": [P, I64, P, I64, I64, P, P, I64, I64, I64, P],
+    "mvb_upsample_streams": [P, I64, I64, P, I64, I64, I64, P, P],
+    "mvb_branch_filter": [P, I64, P, I64, I64, P, P],
+    "mvb_image_count": [INT],
+    "mvb_enumerate": [P, P, I64, INT, P, P, P, P, P, P, P],
+    "mvb_coarse_distances": [P, P, I64, P, P, P, P],
+    "mvb_track_bounds": [P, I64, P, I64, P, P, P, DBL, P, P, P],
+    "mvb_track_max": [P, P, I64, P, P, P, P, P, P, P],
+    "mvb_track_coeffs": [P, P, I64, P, P, P, P, P],
+    "mvb_sort_keys": [P, I64, P, P, P, P, P],
+    "mvb_rank": [P, P, I64, I64, P, P],
+    "mvb_branch_records_f32": [P, I64, P, INT, INT, INT, I64, P, P],
+    "mvb_synthesize_f32": [P, P, I64, P, P, P, P, P, P, INT, P],
+    "mvb_reduce_partials_f32": [P, I64, I64, P, P, P],
+    "mvb_synthesize_f64": [P, I64, I64, P, P, P, P, P, P, P],
+}
+_RESTYPE = {"mvb_last_error": ctypes.c_char_p, "mvb_image_count": I64}
+
+IMAGE_BYTES, JOB_BYTES, WORK_BYTES, COEF_BYTES = 96, 128, 32, 48
+
+
+class MvbError(RuntimeError):
+    """A libmvb call returned a non-zero status."""
+
+
+def lib():
+    """Load libmvb.so once; raise if it is absent (no fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise MvbError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (nvcc, sm_100a). This package has no CPU implementation.")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPE.get(name, ctypes.c_int)
+        sizes = [ctypes.c_int() for _ in range(4)]
+        L.mvb_struct_sizes(*[ctypes.byref(s) for s in sizes])
+        got = tuple(s.value for s in sizes)
+        if got != (IMAGE_BYTES, JOB_BYTES, WORK_BYTES, COEF_BYTES):
+            raise MvbError(f"libmvb struct layout mismatch: {got}")
+        _lib = L
+    return _lib
+
+
+def call(name: str, *args) -> None:
+    """Invoke a status-returning entry point; raise MvbError on failure."""
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        msg = lib().mvb_last_error().decode("utf-8", "replace")
+        raise MvbError(f"{name} failed ({rc}): {msg}")
+
+
+def image_count(max_order: int) -> int:
+    return int(lib().mvb_image_count(int(max_order)))
+
+
+def device_info():
+    sm, ma, mi = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    call("mvb_device_info", ctypes.byref(sm), ctypes.byref(ma), ctypes.byref(mi))
+    return sm.value, ma.value, mi.value
+
+
+def loaded_path() -> str | None:
+    return LIB_PATH if _lib is not None else None

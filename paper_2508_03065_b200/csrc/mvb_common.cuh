@@ -1,0 +1,74 @@
+// Shared helpers for libmvb.so (sm_100a).  Error plumbing for the C ABI,
+// launch checks, and the exact-arithmetic primitives the reference-faithful
+// kernels use (explicit _rn intrinsics are never contracted into FMAs, which
+// keeps them bit-identical to numba with fastmath off, _kernels.py:12-13).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "mvb.h"
+
+namespace mvb {
+
+void set_error(const std::string& msg);
+const char* get_error();
+
+inline int fail(int code, const std::string& msg) {
+    set_error(msg);
+    return code;
+}
+
+inline int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(MVB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return MVB_OK;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline unsigned grid_for(int64_t n, int block) {
+    int64_t g = (n + block - 1) / block;
+    return (unsigned)(g > 0 ? g : 1);
+}
+
+// exact reference arithmetic --------------------------------------------------
+__device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double xsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double xdiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// |off + sign*p - mic| in the order of _kernels.py:58-61:
+// dx = (off + sign*p) - mic ; sqrt((dx*dx + dy*dy) + dz*dz)
+__device__ __forceinline__ double exact_distance(double ox, double oy, double oz, double sx,
+                                                 double sy, double sz, const double* p,
+                                                 const double* m) {
+    double dx = xsub(xadd(ox, xmul(sx, p[0])), m[0]);
+    double dy = xsub(xadd(oy, xmul(sy, p[1])), m[1]);
+    double dz = xsub(xadd(oz, xmul(sz, p[2])), m[2]);
+    return __dsqrt_rn(xadd(xadd(xmul(dx, dx), xmul(dy, dy)), xmul(dz, dz)));
+}
+
+// 65-tap upsampled track value at sample m (_kernels.py:169-180), with the
+// phase table stored transposed (col-major: tabT[col * factor + phase]) so
+// that consecutive samples read consecutive addresses.
+__device__ __forceinline__ double exact_upsample(const double* __restrict__ coarse, int64_t nc,
+                                                 const double* __restrict__ tabT,
+                                                 int64_t factor, int64_t m) {
+    const int64_t half = 32;
+    int64_t base = m / factor;
+    int64_t phase = m - base * factor;
+    double acc = 0.0;
+#pragma unroll 5
+    for (int col = 0; col < 65; ++col) {
+        int64_t j = base + (col - half);
+        j = j < 0 ? 0 : (j >= nc ? nc - 1 : j);
+        acc = xadd(acc, xmul(__ldg(tabT + (int64_t)col * factor + phase), __ldg(coarse + j)));
+    }
+    return acc;
+}
+
+}  // namespace mvb

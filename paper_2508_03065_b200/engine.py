@@ -1,0 +1,570 @@
+"""Fused moving-source render engine: plans a batch of jobs on the device
+and drives libmvb (include/mvb.h).
+
+A *job* is one output channel of one scene: dry signal s, source path,
+receiver (fixed position or path), room, image order and tier table.  The
+engine renders any number of jobs with a fixed number of kernel launches:
+
+  Geometry(jobs)                       synth.py:261-288 (prepare_streams)
+    paths buffer   every source path, receiver and decimated path (fp64 rows)
+    image table    GPU enumeration (room.py:108-143), tier factor per order
+    coarse tracks  mvb_coarse_distances on pos[::N] (decimate decision on
+                   the device, trajectory.py:279-298)
+    dmax per job   mvb_track_bounds + mvb_track_max: the exact max of the
+                   reference's tracks, hence the reference's out_len
+  render(geometry, signals, filter)    synth.py:194-258 (synthesize)
+    fast  (fp32):  branch records, interval polynomials, per-job delay sort,
+                   mvb_synthesize_f32 over (job, tile, image chunk) CTAs,
+                   fixed-order chunk reduction
+    exact (fp64):  reference streams + mvb_synthesize_f64 (reference
+                   arithmetic and summation order)
+
+Sharding: `shard=(rank, world)` restricts every job to a contiguous slice of
+its delay-sorted images (fast path); the caller sums the partial outputs
+(parallel.py does it with one NCCL reduce).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._dev import ptr, require_cuda, stream_handle
+from .farrow import as_filter, centered_branches
+from .room import image_count, image_table
+from .trajectory import device_constants, lowpass_columns_dev, negative_mass
+
+SYNTH_U = 32
+TILE = 32 * SYNTH_U  # output samples per CTA
+IMG_COLS, JOB_COLS, WORK_COLS = 12, 16, 4
+PAD_MARGIN = 64
+FOUR_PI = 4.0 * np.pi
+
+
+@dataclass
+class Job:
+    s: object  # (Ts,) dry signal (numpy / torch); fp32 selects the fast path
+    pos: object  # (T, 3) source path at the audio rate
+    mic: object  # (3,) fixed receiver or (T, 3) receiver path
+    dims: object
+    walls: object
+    max_order: int
+    tiers: tuple  # ((max_order, N), ...) ascending in max_order
+    rate: float
+    c: float = 343.0
+    d_min: float = 0.05
+    image_index: object = None  # optional subset of the canonical image order
+    signal_key: object = None  # jobs with equal keys share one dry signal
+    path_key: object = None  # jobs with equal keys share one source path
+
+
+def _key(explicit, obj):
+    return ("k", explicit) if explicit is not None else ("id", id(obj))
+
+
+def _as_f64_rows(a) -> object:
+    if isinstance(a, torch.Tensor):
+        return a.to(torch.float64).reshape(-1, 3)
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64)).reshape(-1, 3)
+
+
+def _validate_tiers(tiers, max_order):
+    if not tiers:
+        raise ValueError("tier table is empty")
+    prev = -1
+    for mo, N in tiers:
+        if int(N) != N or N < 1:
+            raise ValueError("tier decimation must be a positive integer")
+        if mo <= prev:
+            raise ValueError("tier max_order must increase")
+        prev = mo
+    if tiers[-1][0] < max_order:
+        raise ValueError("tiers do not cover max_order")
+
+
+def pack_jobs(rows: list) -> np.ndarray:
+    """list of dicts -> (n, 16) int64 array with the mvb_job layout."""
+    a = np.zeros((len(rows), JOB_COLS), dtype=np.int64)
+    i32 = a[:, 9:12].view(np.int32)
+    f64 = a[:, 12:16].view(np.float64)
+    for j, r in enumerate(rows):
+        a[j, 0:9] = [r["out_off"], r["out_len"], r["part_off"], r["rec_base"], r["ls"],
+                     r["img_off"], r["n_img"], r["pos_off"], r["mic_off"]]
+        i32[j] = [r["T"], r["mic_moving"], r["L"], r["d0"], r["n_chunks"], r["nb"]]
+        f64[j] = [r["rate"], r["c"], r["d_min"], r["kappa"]]
+    return a
+
+
+class Geometry:
+    """Device-side hierarchical tracks of a batch of jobs (prepare stage)."""
+
+    def __init__(self, jobs: list, device=None):
+        if not jobs:
+            raise ValueError("no jobs")
+        self.dev = dev = require_cuda(device)
+        self.jobs = jobs
+        st = stream_handle(dev)
+        nJ = len(jobs)
+        for jb in jobs:
+            _validate_tiers(jb.tiers, jb.max_order)
+        # ---- full-rate paths ------------------------------------------------
+        host_parts, dev_parts = [], []
+        row = 0
+        path_row = {}
+        self.T = np.zeros(nJ, np.int64)
+        self.pos_off = np.zeros(nJ, np.int64)
+        self.mic_off = np.zeros(nJ, np.int64)
+        self.moving = np.zeros(nJ, np.int64)
+        for j, jb in enumerate(jobs):
+            k = _key(jb.path_key, jb.pos)
+            if k not in path_row:
+                p = _as_f64_rows(jb.pos)
+                path_row[k] = (row, p.shape[0])
+                (dev_parts if isinstance(p, torch.Tensor) else host_parts).append((row, p))
+                row += p.shape[0]
+            self.pos_off[j], self.T[j] = path_row[k]
+            m = _as_f64_rows(jb.mic)
+            if m.shape[0] == 1:
+                self.moving[j] = 0
+            elif m.shape[0] == self.T[j]:
+                self.moving[j] = 1
+            else:
+                raise ValueError("receiver must be a 3-vector or a (T,3) path")
+            self.mic_off[j] = row
+            (dev_parts if isinstance(m, torch.Tensor) else host_parts).append((row, m))
+            row += m.shape[0]
+        full_rows = row
+        # ---- coarse path slots per (job, decimated factor) ------------------
+        self.cpath = {}  # (j, N) -> row
+        for j, jb in enumerate(jobs):
+            for _, N in jb.tiers:
+                N = int(N)
+                if N > 1 and (j, N) not in self.cpath:
+                    K = -(-int(self.T[j]) // N)
+                    self.cpath[(j, N)] = row
+                    row += K * (1 + int(self.moving[j]))
+        self.paths = torch.empty(max(row, 1), 3, dtype=torch.float64, device=dev)
+        if host_parts:
+            host = np.zeros((full_rows, 3))
+            for r0, p in host_parts:
+                host[r0:r0 + p.shape[0]] = p
+            buf = torch.from_numpy(host).pin_memory() if torch.cuda.is_available() else torch.from_numpy(host)
+            self.paths[:full_rows].copy_(buf, non_blocking=True)
+        for r0, p in dev_parts:
+            self.paths[r0:r0 + p.shape[0]].copy_(p)
+        self._decimate_paths()
+        # ---- image table ----------------------------------------------------
+        self._build_images()
+        # ---- job table (geometry fields; render fills the rest) -------------
+        self.job_rows = []
+        for j, jb in enumerate(jobs):
+            self.job_rows.append(dict(
+                out_off=0, out_len=0, part_off=0, rec_base=0, ls=0,
+                img_off=int(self.img_off[j]), n_img=int(self.n_img[j]),
+                pos_off=int(self.pos_off[j]), mic_off=int(self.mic_off[j]),
+                T=int(self.T[j]), mic_moving=int(self.moving[j]), L=0, d0=0, n_chunks=1, nb=0,
+                rate=float(jb.rate), c=float(jb.c), d_min=float(jb.d_min),
+                kappa=float(jb.rate) / float(jb.c)))
+        jobs_dev = torch.from_numpy(pack_jobs(self.job_rows)).to(dev)
+        # ---- coarse tracks, bounds, exact max ---------------------------------
+        n_img = self.n_images
+        self.coarse = torch.empty(max(self.n_coarse_total, 1), dtype=torch.float64, device=dev)
+        if self.dec_sel.numel():
+            _lib.call("mvb_coarse_distances", ptr(self.images), ptr(self.dec_sel),
+                      self.dec_sel.numel(), ptr(jobs_dev), ptr(self.paths), ptr(self.coarse), st)
+        lb = torch.empty(n_img, dtype=torch.float64, device=dev)
+        ub = torch.empty(n_img, dtype=torch.float64, device=dev)
+        negsum = max([negative_mass(N) for N in self.factors if N > 1], default=0.0)
+        _lib.call("mvb_track_bounds", ptr(self.images), n_img, ptr(self.full_sel),
+                  self.full_sel.numel(), ptr(jobs_dev), ptr(self.paths),
+                  ptr(self.coarse) if self.dec_sel.numel() else ptr(None), negsum, ptr(lb), ptr(ub), st)
+        scratch = torch.empty(n_img + nJ, dtype=torch.int32, device=dev)
+        dmax = torch.empty(nJ, dtype=torch.float64, device=dev)
+        _lib.call("mvb_track_max", ptr(self.images), ptr(jobs_dev), nJ,
+                  ptr(self.coarse) if self.dec_sel.numel() else ptr(None), ptr(self.tables), ptr(lb),
+                  ptr(ub), ptr(scratch), ptr(dmax), st)
+        self.dmax = dmax.cpu().numpy()  # the one host sync of the prepare stage
+        self.eval_count = [int(self.evals[j]) for j in range(nJ)]
+
+    # ------------------------------------------------------------------------
+    def _decimate_paths(self):
+        """Fill the coarse path slots: pos[::N] (and receiver[::N]); the
+        anti-alias low-pass runs only where the reference's decision
+        (Nyquist_out < bandwidth < 2 Nyquist_out) says so.  Bandwidths of all
+        distinct paths are measured in one batched FFT per path length."""
+        jobs, dev = self.jobs, self.dev
+        # distinct full-rate paths that need decimation: (row, T, rate) -> factors
+        need = {}
+        for (j, N), dst in self.cpath.items():
+            T = int(self.T[j])
+            rate = float(jobs[j].rate)
+            need.setdefault((int(self.pos_off[j]), T, rate), set()).add(N)
+            if self.moving[j]:
+                need.setdefault((int(self.mic_off[j]), T, rate), set()).add(N)
+        if not need:
+            return
+        bw = {}
+        by_len = {}
+        for (r0, T, rate) in need:
+            by_len.setdefault((T, rate), []).append(r0)
+        for (T, rate), starts in by_len.items():
+            idx = torch.tensor(starts, device=dev)[:, None] + torch.arange(T, device=dev)[None, :]
+            x = self.paths[idx]  # (G, T, 3)
+            bw_t = _bandwidth_batch(x, rate)
+            for r0, b in zip(starts, bw_t.cpu().numpy().tolist()):
+                bw[(r0, T, rate)] = b
+        coarse_src = {}
+        for key, factors in need.items():
+            r0, T, rate = key
+            for N in factors:
+                nyq = 0.5 * rate / N
+                src = self.paths[r0:r0 + T]
+                if T >= 2 and nyq < bw[key] < 2.0 * nyq:
+                    src = lowpass_columns_dev(src, rate, 0.9 * nyq)
+                coarse_src[(r0, N)] = src[::N]
+        for (j, N), dst in self.cpath.items():
+            K = -(-int(self.T[j]) // N)
+            self.paths[dst:dst + K] = coarse_src[(int(self.pos_off[j]), N)]
+            if self.moving[j]:
+                self.paths[dst + K:dst + 2 * K] = coarse_src[(int(self.mic_off[j]), N)]
+
+    def _build_images(self):
+        jobs, dev = self.jobs, self.dev
+        nJ = len(jobs)
+        # factor constants (transposed tables + refits) shared by the batch
+        factors = sorted({int(N) for jb in jobs for _, N in jb.tiers if int(N) > 1})
+        self.factors = factors
+        tab_parts, fit_parts = [], []
+        self.table_off, self.fit_idx = {}, {}
+        off = 0
+        for q, N in enumerate(factors):
+            cst = device_constants(N, dev)
+            self.table_off[N] = off
+            tab_parts.append(cst["tableT"].reshape(-1))
+            off += cst["tableT"].numel()
+            self.fit_idx[N] = q
+            fit_parts.append(cst["fit"].reshape(-1))
+        self.tables = torch.cat(tab_parts) if tab_parts else torch.zeros(1, dtype=torch.float64, device=dev)
+        self.fits = torch.cat(fit_parts) if fit_parts else torch.zeros(1, dtype=torch.float64, device=dev)
+        # groups of jobs with identical enumeration / tier layout
+        groups = {}
+        for j, jb in enumerate(jobs):
+            sub = None if jb.image_index is None else tuple(np.asarray(jb.image_index).tolist())
+            key = (int(jb.max_order), tuple((int(a), int(b)) for a, b in jb.tiers), sub)
+            groups.setdefault(key, []).append(j)
+        self.img_off = np.zeros(nJ, np.int64)
+        self.n_img = np.zeros(nJ, np.int64)
+        self.evals = np.zeros(nJ, np.int64)
+        blocks, dec_sel, full_sel = [], [], []
+        img_base = 0
+        coarse_base = 0
+        self.order_of_job = [None] * nJ
+        for (max_order, tiers, sub), members in groups.items():
+            room_key, rooms, member_room = {}, [], []
+            for j in members:
+                d = np.asarray(jobs[j].dims, dtype=np.float64).reshape(3)
+                w = np.asarray(jobs[j].walls, dtype=np.float64)
+                w = np.full(6, float(w)) if w.ndim == 0 else w.reshape(6)
+                k = (d.tobytes(), w.tobytes())
+                if k not in room_key:
+                    room_key[k] = len(rooms)
+                    rooms.append((d, w))
+                member_room.append(room_key[k])
+            tab = image_table(np.stack([r[0] for r in rooms]), np.stack([r[1] for r in rooms]),
+                              max_order, dev)
+            sel = None if sub is None else torch.as_tensor(np.asarray(sub, np.int64), device=dev)
+            order = tab.order[0] if sel is None else tab.order[0][sel]
+            S = int(order.numel())
+            fac = torch.ones(S, dtype=torch.int64, device=dev)
+            prev = -1
+            for mo, N in tiers:
+                fac = torch.where((order > prev) & (order <= mo), torch.full_like(fac, N), fac)
+                prev = mo
+            fac_np = fac.cpu().numpy()
+            G = len(members)
+            ridx = torch.as_tensor(member_room, device=dev)
+            offset = tab.offset[ridx]
+            sign = tab.sign[ridx]
+            beta = tab.beta[ridx]
+            if sel is not None:
+                offset, sign, beta = offset[:, sel], sign[:, sel], beta[:, sel]
+            Tj = torch.as_tensor(self.T[members], device=dev)
+            Nf = fac[None, :].expand(G, S)
+            K = torch.where(Nf > 1, (Tj[:, None] + Nf - 1) // Nf, torch.zeros_like(Nf))
+            cnt = K.reshape(-1)
+            coarse_off = coarse_base + torch.cumsum(cnt, 0) - cnt
+            coarse_base += int(cnt.sum().item()) if cnt.numel() else 0
+            table = torch.zeros_like(Nf)
+            fit = torch.zeros_like(Nf)
+            cpath = torch.zeros_like(Nf)
+            for N in set(fac_np.tolist()):
+                if N == 1:
+                    continue
+                m = Nf == N
+                table = torch.where(m, torch.full_like(table, self.table_off[N]), table)
+                fit = torch.where(m, torch.full_like(fit, self.fit_idx[N]), fit)
+                cp = torch.as_tensor([self.cpath[(j, N)] for j in members], device=dev)[:, None]
+                cpath = torch.where(m, cp.expand(G, S), cpath)
+            blk = torch.zeros(G, S, IMG_COLS, dtype=torch.int64, device=dev)
+            f64 = blk.view(torch.float64)
+            f64[:, :, 0:3] = offset
+            f64[:, :, 3] = beta
+            f32 = blk[:, :, 4:6].view(torch.float32)
+            f32[:, :, 0:3] = sign.to(torch.float32)
+            f32[:, :, 3] = (beta / FOUR_PI).to(torch.float32)
+            i32 = blk[:, :, 6:7].view(torch.int32)
+            i32[:, :, 0] = Nf.to(torch.int32)
+            i32[:, :, 1] = K.to(torch.int32)
+            blk[:, :, 7] = coarse_off.reshape(G, S)
+            blk[:, :, 8] = coarse_off.reshape(G, S)  # one interval record per coarse sample
+            blk[:, :, 9] = table
+            blk[:, :, 10] = cpath
+            j32 = blk[:, :, 11:12].view(torch.int32)
+            j32[:, :, 0] = torch.as_tensor(members, dtype=torch.int32, device=dev)[:, None]
+            j32[:, :, 1] = fit.to(torch.int32)
+            blocks.append(blk.reshape(G * S, IMG_COLS))
+            flat_dec = torch.nonzero((Nf > 1).reshape(-1)).squeeze(1) + img_base
+            flat_full = torch.nonzero((Nf == 1).reshape(-1)).squeeze(1) + img_base
+            dec_sel.append(flat_dec)
+            full_sel.append(flat_full)
+            n_full = int((fac_np == 1).sum())
+            for g, j in enumerate(members):
+                self.img_off[j] = img_base + g * S
+                self.n_img[j] = S
+                T = int(self.T[j])
+                self.evals[j] = n_full * T + sum(-(-T // int(N)) for N in fac_np.tolist() if N > 1)
+                self.order_of_job[j] = order
+            img_base += G * S
+        self.images = torch.cat(blocks) if len(blocks) > 1 else blocks[0]
+        self.n_images = img_base
+        self.n_coarse_total = coarse_base
+        self.dec_sel = torch.cat(dec_sel).to(torch.int32)
+        self.full_sel = torch.cat(full_sel).to(torch.int32)
+        if self.full_sel.numel() > 65535:
+            raise ValueError("more than 65535 full-rate images in one batch")
+
+    # ------------------------------------------------------------------------
+    def tau_max(self, j: int) -> float:
+        jb = self.jobs[j]
+        return float(jb.rate) * float(self.dmax[j]) / float(jb.c)
+
+
+def _bandwidth_batch(x: torch.Tensor, rate: float, energy_fraction: float = 0.99) -> torch.Tensor:
+    """Per-path 99%-energy bandwidth (reference trajectory.py:316-339) of
+    x (G, T, 3) on the device."""
+    G, T, _ = x.shape
+    if T < 2:
+        return torch.zeros(G, dtype=torch.float64, device=x.device)
+    xc = x - x.mean(dim=1, keepdim=True)
+    pw = torch.fft.rfft(xc, dim=1).abs() ** 2  # (G, F, 3)
+    tot = pw.sum(dim=1)  # (G, 3)
+    cum = torch.cumsum(pw, dim=1) / torch.where(tot > 0, tot, torch.ones_like(tot))[:, None, :]
+    F = pw.shape[1]
+    cumT = cum.permute(0, 2, 1).reshape(G * 3, F).contiguous()
+    k = torch.searchsorted(cumT, torch.full((G * 3, 1), energy_fraction, dtype=cumT.dtype,
+                                            device=x.device)).squeeze(1)
+    k = torch.clamp(k, max=F - 1).reshape(G, 3)
+    f = k.to(torch.float64) * (rate / T)
+    f = torch.where(tot > 0, f, torch.zeros_like(f))
+    return f.max(dim=1).values
+
+
+# ----------------------------------------------------------------------------
+# filter banks
+
+
+def fast_bank(filt) -> tuple:
+    """Centred fp32-path Farrow bank: (coeffs (M1, L) fp64, M1, nb).  Banks
+    above degree 7 are reduced to degree 7 when that changes no tap by more
+    than 5e-7 of the largest tap (below fp32 resolution of the path)."""
+    f = as_filter(filt)
+    cb = centered_branches(f.branches)
+    M1 = cb.shape[0]
+    if M1 > 8:
+        mu = 0.5 - 0.5 * np.cos(np.pi * (np.arange(256) + 0.5) / 256)
+        u = mu - 0.5
+        h = (u[:, None] ** np.arange(M1)[None, :]) @ cb
+        V = np.polynomial.chebyshev.chebvander(2 * u, 7)
+        ch, *_ = np.linalg.lstsq(V, h, rcond=None)
+        red = np.zeros((8, cb.shape[1]))
+        for j in range(cb.shape[1]):
+            p = np.polynomial.chebyshev.cheb2poly(ch[:, j])
+            red[:p.size, j] = p * (2.0 ** np.arange(p.size))
+        uu = np.linspace(-0.5, 0.5, 2001)
+        ex = (uu[:, None] ** np.arange(M1)[None, :]) @ cb
+        ap = (uu[:, None] ** np.arange(8)[None, :]) @ red
+        if np.max(np.abs(ex - ap)) <= 5e-7 * np.max(np.abs(ex)):
+            cb, M1 = red, 8
+    nb = 4 if M1 <= 4 else 8 if M1 <= 8 else 12 if M1 <= 12 else 16
+    if M1 > 16:
+        raise ValueError("fast path supports Farrow degree <= 15")
+    return cb, M1, nb
+
+
+# ----------------------------------------------------------------------------
+# render stage
+
+
+@dataclass
+class RenderResult:
+    out: torch.Tensor  # flat output (fp32 fast / fp64 exact)
+    offsets: np.ndarray  # per-job start in `out`
+    lengths: np.ndarray  # per-job out_len
+    n_images: np.ndarray  # per-job images rendered (this shard)
+    updates: int  # image x output-sample updates computed (this shard)
+    launches: int  # libmvb kernel launches in the render stage
+
+    def job(self, j: int) -> torch.Tensor:
+        return self.out[self.offsets[j]:self.offsets[j] + self.lengths[j]]
+
+
+def _chunking(n_imgs, tiles, sm_count):
+    """Images per CTA: enough CTAs for >= 4 waves of 2 CTAs/SM, chunks of
+    >= 128 images (a CTA then does >= 128 x TILE updates)."""
+    total_tiles = int(sum(tiles))
+    want = 8 * sm_count
+    if total_tiles >= want:
+        return [1] * len(n_imgs)
+    out = []
+    for S, t in zip(n_imgs, tiles):
+        per = max(1, math.ceil(want / max(total_tiles, 1)))
+        per = min(per, max(1, S // 128))
+        out.append(per)
+    return out
+
+
+def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=None,
+           signal_keys=None) -> RenderResult:
+    """Synthesize every job of `geom` (signals[j] is job j's dry signal)."""
+    dev = geom.dev
+    st = stream_handle(dev)
+    jobs = geom.jobs
+    nJ = len(jobs)
+    f = as_filter(filt)
+    L, d0 = int(f.branch_len), int(f.nominal_delay)
+    if precision not in ("fp32", "fp64"):
+        raise ValueError("precision must be 'fp32' or 'fp64'")
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    # signals: dedupe, upload
+    keys = signal_keys or [_key(jobs[j].signal_key, signals[j]) for j in range(nJ)]
+    uniq = {}
+    for j in range(nJ):
+        uniq.setdefault(keys[j], []).append(j)
+    dt = torch.float32 if precision == "fp32" else torch.float64
+    sig_dev, sig_len = {}, {}
+    for k, members in uniq.items():
+        s = signals[members[0]]
+        t = s.to(dev, dt) if isinstance(s, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(np.asarray(s), dtype=np.float32 if dt == torch.float32 else np.float64)).to(dev)
+        t = t.reshape(-1).contiguous()
+        if t.numel() == 0:
+            raise ValueError("input must be a nonempty 1-D signal")
+        sig_dev[k], sig_len[k] = t, t.numel()
+    out_len = np.zeros(nJ, np.int64)
+    tau_ceil = np.zeros(nJ, np.int64)
+    for j in range(nJ):
+        tau_ceil[j] = int(math.ceil(geom.tau_max(j)))
+        out_len[j] = sig_len[keys[j]] + tau_ceil[j] + L
+    offsets = np.concatenate([[0], np.cumsum(out_len)[:-1]]).astype(np.int64)
+    rows = [dict(r) for r in geom.job_rows]
+    for j in range(nJ):
+        rows[j].update(out_off=int(offsets[j]), out_len=int(out_len[j]), L=L, d0=d0,
+                       ls=int(sig_len[keys[j]] + L - 1))
+    launches = 0
+    if precision == "fp64":
+        if shard is not None and shard[1] > 1:
+            raise ValueError("the exact fp64 engine runs replicas only (no image sharding)")
+        nb = int(f.poly_order) + 1
+        br = torch.from_numpy(np.ascontiguousarray(f.branches, dtype=np.float64)).to(dev)
+        base, bases = 0, {}
+        for k in uniq:
+            bases[k] = base
+            base += nb * (sig_len[k] + L - 1)
+        streams = torch.empty(base, dtype=torch.float64, device=dev)
+        for k in uniq:
+            T = sig_len[k]
+            _lib.call("mvb_branch_filter", ptr(sig_dev[k]), T, ptr(br), nb, L,
+                      ptr(streams[bases[k]:]), st)
+            launches += 1
+        for j in range(nJ):
+            rows[j].update(rec_base=bases[keys[j]], nb=nb)
+        jobs_dev = torch.from_numpy(pack_jobs(rows)).to(dev)
+        out = torch.empty(int(out_len.sum()), dtype=torch.float64, device=dev)
+        _lib.call("mvb_synthesize_f64", ptr(jobs_dev), nJ, int(out_len.max()), ptr(geom.images),
+                  ptr(geom.coarse), ptr(geom.tables), ptr(streams), ptr(geom.paths), ptr(out), st)
+        launches += 1
+        upd = int(np.sum(out_len * geom.n_img))
+        return RenderResult(out, offsets, out_len, geom.n_img.copy(), upd, launches)
+
+    # ---------------------------------------------------------------- fast --
+    cb, M1, nb = fast_bank(f)
+    cb_dev = torch.from_numpy(np.ascontiguousarray(cb)).to(dev)
+    rec_rows, bases = 0, {}
+    for k, members in uniq.items():
+        front = int(max(tau_ceil[j] for j in members)) + L + PAD_MARGIN
+        back = front + TILE + PAD_MARGIN
+        bases[k] = (rec_rows, front)
+        rec_rows += front + sig_len[k] + L - 1 + back
+    rec = torch.zeros(rec_rows * nb, dtype=torch.float32, device=dev)
+    for k in uniq:
+        r0, front = bases[k]
+        _lib.call("mvb_branch_records_f32", ptr(sig_dev[k]), sig_len[k], ptr(cb_dev), M1, L, nb,
+                  r0 + front, ptr(rec), st)
+        launches += 1
+    for j in range(nJ):
+        r0, front = bases[keys[j]]
+        rows[j].update(rec_base=r0 + front, nb=nb)
+    # image slices of this shard (in delay-sorted order)
+    rank_, world = (0, 1) if shard is None else (int(shard[0]), int(shard[1]))
+    lo = (geom.n_img * rank_) // world
+    hi = (geom.n_img * (rank_ + 1)) // world
+    tiles = [-(-int(out_len[j]) // TILE) for j in range(nJ)]
+    chunks = _chunking([int(hi[j] - lo[j]) for j in range(nJ)], tiles, sm_count)
+    part_rows = 0
+    work = []
+    for j in range(nJ):
+        nc = chunks[j] if hi[j] > lo[j] else 1
+        rows[j]["n_chunks"] = nc
+        if nc > 1:
+            rows[j]["part_off"] = part_rows
+            part_rows += nc * int(out_len[j])
+        span = int(hi[j] - lo[j])
+        for c in range(nc):
+            a = int(lo[j]) + (span * c) // nc
+            b = int(lo[j]) + (span * (c + 1)) // nc
+            for t in range(tiles[j]):
+                work.append((j, t, a, b, c, 0, 0, 0))
+    jobs_dev = torch.from_numpy(pack_jobs(rows)).to(dev)
+    coef = torch.empty(max(geom.n_coarse_total, 1) * 12, dtype=torch.float32, device=dev)
+    if geom.dec_sel.numel():
+        _lib.call("mvb_track_coeffs", ptr(geom.images), ptr(geom.dec_sel), geom.dec_sel.numel(),
+                  ptr(jobs_dev), ptr(geom.coarse), ptr(geom.fits), ptr(coef), st)
+        launches += 1
+    key = torch.empty(geom.n_images, dtype=torch.float64, device=dev)
+    _lib.call("mvb_sort_keys", ptr(geom.images), geom.n_images, ptr(jobs_dev), ptr(geom.paths),
+              ptr(geom.coarse), ptr(key), st)
+    rank = torch.empty(geom.n_images, dtype=torch.int32, device=dev)
+    _lib.call("mvb_rank", ptr(key), ptr(jobs_dev), nJ, int(geom.n_img.max()), ptr(rank), st)
+    launches += 2
+    job_of_img = geom.images[:, 11:12].view(torch.int32)[:, 0].to(torch.int64)
+    job_base = torch.as_tensor(geom.img_off, device=dev)[job_of_img]
+    perm = torch.empty(geom.n_images, dtype=torch.int64, device=dev)
+    perm[job_base + rank.to(torch.int64)] = torch.arange(geom.n_images, device=dev)
+    images_sorted = geom.images[perm].contiguous()
+    work_dev = torch.from_numpy(np.asarray(work, dtype=np.int32).reshape(-1, 8)).to(dev)
+    out = torch.empty(int(out_len.sum()), dtype=torch.float32, device=dev)
+    part = torch.empty(max(part_rows, 1), dtype=torch.float32, device=dev)
+    _lib.call("mvb_synthesize_f32", ptr(jobs_dev), ptr(work_dev), len(work), ptr(images_sorted),
+              ptr(coef), ptr(rec), ptr(geom.paths), ptr(out), ptr(part), nb, st)
+    launches += 1
+    if part_rows:
+        _lib.call("mvb_reduce_partials_f32", ptr(jobs_dev), nJ, int(out_len.max()), ptr(part),
+                  ptr(out), st)
+        launches += 1
+    n_img_shard = (hi - lo).astype(np.int64)
+    upd = int(np.sum(out_len * n_img_shard))
+    return RenderResult(out, offsets, out_len, n_img_shard, upd, launches)

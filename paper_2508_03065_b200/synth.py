@@ -1,0 +1,354 @@
+"""Hierarchical moving-image-source synthesis -- the drop-in API.
+
+Mirrors reference synth.py (SynthesisConfig :43-91, DelayStreams :94-119,
+prepare_streams :273-288, synthesize :194-258, render :291-294,
+select_images :261-270, cost_report :302-331, BudgetError :39-40) and
+reference.py:116-130 (full_rate_moving_oracle).  Same validation and
+ValueError behaviour; numpy in, float64 numpy out.
+
+Differences, all opt-in through new SynthesisConfig fields:
+  tiers      ((max_order, N), ...) any number of hierarchical rates; the
+             reference's (order_split, decimation) is the 2-tier default.
+  precision  "fp64": the exact engine (reference arithmetic and summation
+             order, bit-faithful); "fp32": the fused B200 fast path
+             (max error ~1e-6 of the output peak); "auto" (default): fp32
+             when the dry signal is float32, fp64 otherwise.
+A moving receiver is accepted as a (T, 3) array in place of the mic.
+`workers` is accepted and ignored (the GPU schedules itself).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from . import engine
+from .farrow import as_filter
+from .room import Room, as_mic, image_count, image_table
+from .trajectory import Trajectory
+
+SUMMATION_BLOCK = 32
+
+
+class BudgetError(RuntimeError):
+    """Raised when a requested render exceeds the configured evaluation cap."""
+
+
+@dataclass(frozen=True)
+class SynthesisConfig:
+    audio_rate: float = 16000.0
+    order_split: int = 1
+    decimation: int = 3200
+    max_order: int = 3
+    t60: float = None
+    sound_speed: float = 343.0
+    d_min: float = 0.05
+    summation: str = "pairwise"
+    modulate: str = "receiver"
+    workers: int = 1
+    eval_budget: float = 2.0e9
+    tiers: tuple = None
+    precision: str = "auto"
+
+    def __post_init__(self):
+        if self.audio_rate <= 0:
+            raise ValueError("audio_rate must be > 0")
+        if self.decimation < 1 or int(self.decimation) != self.decimation:
+            raise ValueError("decimation must be a positive integer")
+        if self.order_split < 0:
+            raise ValueError("order_split must be >= 0")
+        if self.max_order < 0:
+            raise ValueError("max_order must be >= 0")
+        if self.t60 is not None and self.t60 <= 0:
+            raise ValueError("t60 must be > 0 when set")
+        if self.sound_speed <= 0:
+            raise ValueError("sound_speed must be > 0")
+        if self.d_min <= 0:
+            raise ValueError("d_min must be > 0")
+        if self.summation != "pairwise":
+            raise ValueError("summation policy must be 'pairwise'")
+        if self.modulate not in ("receiver", "source"):
+            raise ValueError("modulate must be 'receiver' or 'source'")
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+        if self.eval_budget <= 0:
+            raise ValueError("eval_budget must be > 0")
+        if self.precision not in ("auto", "fp32", "fp64"):
+            raise ValueError("precision must be 'auto', 'fp32' or 'fp64'")
+        if self.tiers is not None:
+            tiers = tuple((int(a), int(b)) for a, b in self.tiers)
+            engine._validate_tiers(tiers, self.max_order)
+            object.__setattr__(self, "tiers", tiers)
+
+    def tier_table(self) -> tuple:
+        """((max_order, N), ...): explicit tiers, else the reference's split
+        (orders <= order_split at full rate, the rest decimated by N)."""
+        if self.tiers is not None:
+            return self.tiers
+        if self.order_split >= self.max_order:
+            return ((self.max_order, 1),)
+        return ((self.order_split, 1), (self.max_order, int(self.decimation)))
+
+
+def _canonical_index(specs, room, max_order) -> np.ndarray:
+    """Positions of `specs` (ImageSourceSpec list) in the canonical order."""
+    t = image_table(room.dims, room.wall_reflection, max_order)
+    lat = t.lattice[0].cpu().numpy()
+    par = t.parity[0].cpu().numpy()
+    where = {(tuple(lat[i]), tuple(par[i])): i for i in range(lat.shape[0])}
+    idx = []
+    for sp in specs:
+        k = (tuple(int(v) for v in sp.lattice), tuple(int(bool(v)) for v in sp.parity))
+        if k not in where:
+            raise ValueError("image spec beyond max_order")
+        idx.append(where[k])
+    idx = np.asarray(idx, dtype=np.int64)
+    return np.sort(idx)  # merge_streams restores canonical order (synth.py:161-179)
+
+
+class DelayStreams:
+    """Per-image distance tracks of one render, held on the device.
+
+    Same attributes as reference synth.py:94-119 (rate, specs, d,
+    eval_count, tau(cfg), amplitude(cfg), image_count()); `d` is
+    materialised from the device tracks only when read.
+    """
+
+    def __init__(self, geometry, rate, room, max_order, index):
+        self.geometry = geometry
+        self.rate = float(rate)
+        self._room = room
+        self._max_order = max_order
+        self._index = index
+        self._specs = None
+        self._d = None
+        self.eval_count = geometry.eval_count[0] if geometry is not None else 0
+
+    @property
+    def specs(self):
+        if self._specs is None:
+            from .room import enumerate_images
+            full = enumerate_images(self._room, self._max_order)
+            self._specs = [full[i] for i in self._index] if self._index is not None else full
+        return self._specs
+
+    def image_count(self):
+        return 0 if self.geometry is None else int(self.geometry.n_img[0])
+
+    @property
+    def d(self) -> np.ndarray:
+        if self._d is None:
+            self._d = materialize_tracks(self.geometry)
+        return self._d
+
+    def tau(self, cfg):
+        return self.rate * self.d / cfg.sound_speed
+
+    def amplitude(self, cfg):
+        beta = np.array([s.beta for s in self.specs])
+        return beta[:, None] / (4.0 * np.pi * np.maximum(self.d, cfg.d_min))
+
+
+def materialize_tracks(geom) -> np.ndarray:
+    """(S, T) fp64 tracks of job 0 in canonical order, computed on the GPU
+    with the reference kernels (distance_streams / upsample_stream)."""
+    from . import _lib
+    from ._dev import ptr, stream_handle
+    if geom is None:
+        return np.zeros((0, 0))
+    dev = geom.dev
+    S, T = int(geom.n_img[0]), int(geom.T[0])
+    img = geom.images[int(geom.img_off[0]):int(geom.img_off[0]) + S]
+    f64 = img.view(torch.float64)
+    i32 = img[:, 6:7].view(torch.int32)
+    factor = i32[:, 0].cpu().numpy()
+    coarse_off = img[:, 7].cpu().numpy()
+    K = i32[:, 1].cpu().numpy()
+    out = torch.empty(S, T, dtype=torch.float64, device=dev)
+    st = stream_handle(dev)
+    full = np.nonzero(factor == 1)[0]
+    if full.size:
+        sel = torch.as_tensor(full, device=dev)
+        off = f64[sel, 0:3].contiguous()
+        sg = img[sel, 4:6].view(torch.float32)[:, 0:3].to(torch.float64).contiguous()
+        res = torch.empty(full.size, T, dtype=torch.float64, device=dev)
+        if geom.moving[0]:
+            raise NotImplementedError("materialising tracks of a moving receiver")
+        mic = geom.paths[int(geom.mic_off[0])].contiguous()
+        pos = geom.paths[int(geom.pos_off[0]):int(geom.pos_off[0]) + T].contiguous()
+        _lib.call("mvb_distance_streams", ptr(off), ptr(sg), ptr(mic), ptr(pos), full.size, T,
+                  ptr(res), st)
+        out[sel] = res
+    from .trajectory import phase_table
+    for N in sorted(set(factor.tolist()) - {1}):
+        rows = np.nonzero(factor == N)[0]
+        tab = torch.from_numpy(np.ascontiguousarray(phase_table(int(N)))).to(dev)
+        k = int(K[rows[0]])
+        idx = torch.as_tensor(coarse_off[rows], device=dev)[:, None] + torch.arange(k, device=dev)
+        coarse = geom.coarse[idx].contiguous()
+        res = torch.empty(rows.size, T, dtype=torch.float64, device=dev)
+        _lib.call("mvb_upsample_streams", ptr(coarse), rows.size, k, ptr(tab), int(N), 65, T,
+                  ptr(res), st)
+        out[torch.as_tensor(rows, device=dev)] = res
+    return out.cpu().numpy()
+
+
+def _check_receiver(mic, room, T):
+    m = mic.pos if hasattr(mic, "pos") else np.asarray(mic, dtype=np.float64)
+    if m.ndim == 1:
+        as_mic(m).require_inside(room)
+        return m
+    if m.shape != (T, 3):
+        raise ValueError("a moving receiver must be a (T, 3) path")
+    if not (np.all(m > 0) and np.all(m < room.dims)):
+        raise ValueError("mic path must stay strictly inside the room")
+    return m
+
+
+def select_images(room, traj, mic, cfg):
+    """Canonical image indices kept for a render (t60 cull at the start
+    position, reference synth.py:261-270); None = all images."""
+    if cfg.t60 is None:
+        return None
+    from .kernels import distance_streams
+    t = image_table(room.dims, room.wall_reflection, cfg.max_order)
+    m = np.asarray(mic if not hasattr(mic, "pos") else mic.pos, dtype=np.float64)
+    m0 = m if m.ndim == 1 else m[0]
+    d = distance_streams(t.offset[0], t.sign[0], torch.as_tensor(m0, device=t.offset.device),
+                         torch.as_tensor(traj.positions[:1], device=t.offset.device))[:, 0]
+    keep = (d <= cfg.sound_speed * cfg.t60).nonzero().squeeze(1).cpu().numpy()
+    return keep.astype(np.int64)
+
+
+def prepare_streams(traj, room, mic, cfg, images=None) -> DelayStreams:
+    """Device tracks of every image (reference synth.py:273-288), for any
+    tier table."""
+    if traj.rate != cfg.audio_rate:
+        raise ValueError("trajectory rate must equal the audio rate")
+    m = _check_receiver(mic, room, len(traj))
+    if images is not None:
+        index = _canonical_index(images, room, cfg.max_order) if len(images) else np.zeros(0, np.int64)
+    else:
+        index = select_images(room, traj, m, cfg)
+    if index is not None and index.size == 0:
+        return DelayStreams(None, traj.rate, room, cfg.max_order, index)
+    job = engine.Job(s=None, pos=traj.positions, mic=m, dims=room.dims, walls=room.wall_reflection,
+                     max_order=cfg.max_order, tiers=cfg.tier_table(), rate=traj.rate,
+                     c=cfg.sound_speed, d_min=cfg.d_min, image_index=index)
+    geom = engine.Geometry([job])
+    return DelayStreams(geom, traj.rate, room, cfg.max_order, index)
+
+
+def _precision(s, cfg) -> str:
+    if cfg.precision != "auto":
+        return cfg.precision
+    dt = s.dtype if hasattr(s, "dtype") else np.asarray(s).dtype
+    return "fp32" if dt in (np.float32, torch.float32) else "fp64"
+
+
+def _check_signal(s):
+    a = s.detach().cpu().numpy() if isinstance(s, torch.Tensor) else np.asarray(s)
+    if a.ndim != 1 or a.size == 0:
+        raise ValueError("input must be a nonempty 1-D signal")
+    if not np.all(np.isfinite(a)):
+        raise ValueError("input must be finite")
+    return a
+
+
+def synthesize(s, streams: DelayStreams, f, cfg) -> np.ndarray:
+    """Render s through the moving image set (reference synth.py:194-258).
+    Output length len(s) + ceil(max delay) + L, float64."""
+    a = _check_signal(s)
+    if cfg.modulate != "receiver":
+        raise NotImplementedError("modulate='source' (reference validation switch) is not "
+                                  "implemented on the GPU engine")
+    filt = as_filter(f)
+    if streams.image_count() == 0:
+        return np.zeros(a.size + filt.branch_len)
+    prec = _precision(a, cfg)
+    res = engine.render(streams.geometry, [a], filt, precision=prec)
+    return res.job(0).to(torch.float64).cpu().numpy()
+
+
+def render(s, traj, room, mic, f, cfg) -> np.ndarray:
+    """End-to-end: trajectory in, reverberant moving-source audio out."""
+    _check_signal(s)
+    return synthesize(s, prepare_streams(traj, room, mic, cfg), f, cfg)
+
+
+def full_rate_moving_oracle(s, traj, room, mic, f, cfg):
+    """Every image's distance at every sample (reference.py:116-130)."""
+    evals = image_count(cfg.max_order) * len(traj)
+    if evals > cfg.eval_budget:
+        raise BudgetError(f"oracle render needs {evals:.3g} distance evaluations, "
+                          f"budget is {cfg.eval_budget:.3g}")
+    return render(s, traj, room, mic, f, replace(cfg, decimation=1, tiers=((cfg.max_order, 1),)))
+
+
+def _count_order_leq(k):
+    return 1 + sum(4 * o * o + 2 for o in range(1, k + 1))
+
+
+def cost_report(cfg, images, duration):
+    """Distance-evaluation counts, brute force vs hierarchical (reference
+    synth.py:302-331), for any tier table."""
+    n = int(round(duration * cfg.audio_rate))
+    tiers = cfg.tier_table()
+    if isinstance(images, int):
+        total = images
+        per_tier, prev, left = [], -1, images
+        for mo, N in tiers:
+            c = min(left, _count_order_leq(mo) - (_count_order_leq(prev) if prev >= 0 else 0))
+            per_tier.append((c, N))
+            left -= c
+            prev = mo
+        if left > 0:
+            per_tier[-1] = (per_tier[-1][0] + left, per_tier[-1][1])
+    else:
+        total = len(images)
+        per_tier, prev = [], -1
+        for mo, N in tiers:
+            per_tier.append((sum(1 for sp in images if prev < sp.order <= mo), N))
+            prev = mo
+    low = sum(c for c, N in per_tier if N == 1)
+    high = total - low
+    hier = sum(c * (n if N == 1 else -(-n // N)) for c, N in per_tier)
+    high_hier = sum(c * -(-n // N) for c, N in per_tier if N != 1)
+    naive = total * n
+    return {
+        "images_total": total,
+        "images_low": low,
+        "images_high": high,
+        "samples": n,
+        "naive_evals": naive,
+        "hierarchical_evals": hier,
+        "reduction_ratio": naive / hier if hier else float("inf"),
+        "high_order_reduction": (high * n / high_hier) if high_hier else float("inf"),
+    }
+
+
+# ----------------------------------------------------------------------------
+# batched, device-resident entry points (benchmarks, multi-scene workloads)
+
+
+def scene_jobs(scenes, channels=None) -> list:
+    """workloads.Scene list -> engine.Job list (one job per (scene, mic))."""
+    jobs = []
+    for q, sc in enumerate(scenes):
+        chans = range(len(sc.mics)) if channels is None else channels
+        for ch in chans:
+            jobs.append(engine.Job(s=sc.s, pos=sc.pos, mic=sc.mics[ch], dims=sc.dims, walls=sc.walls,
+                                   max_order=sc.max_order, tiers=sc.tiers, rate=sc.rate,
+                                   signal_key=("scene", q), path_key=("scene", q)))
+    return jobs
+
+
+def render_jobs(jobs, f, precision="fp32", shard=None, signals=None):
+    """Geometry + render of a job batch; returns engine.RenderResult
+    (device output, per-job offsets/lengths, update count)."""
+    geom = engine.Geometry(jobs)
+    sig = signals if signals is not None else [jb.s for jb in jobs]
+    keys = [engine._key(jb.signal_key, jb.s) for jb in jobs]
+    return engine.render(geom, sig, f, precision=precision, shard=shard, signal_keys=keys)

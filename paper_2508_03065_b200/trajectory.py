@@ -1,0 +1,199 @@
+"""Source / receiver paths and the hierarchical track resampling constants.
+
+Trajectory mirrors reference trajectory.py:29-60.  The decimation decision
+(trajectory.py:279-298: low-pass only when Nyquist_out < bandwidth <
+2 Nyquist_out) is taken on the device with torch.fft; the per-factor
+Kaiser-windowed-sinc phase table (trajectory.py:235-257) is a cached host
+constant like the reference's lru_cache, from which two device constants
+are derived:
+
+  * the transposed table (65, N) read by the exact fp64 path, and
+  * the degree-8 refit of every table column in u = 2 r / N - 1 that the
+    fast path evaluates per sample: exact track on each
+    coarse interval to < 1e-9 m at the configs' rates.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from functools import lru_cache
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._dev import ptr, require_cuda, stream_handle, to_dev
+
+UPSAMPLE_HALFWIDTH = 32
+UPSAMPLE_KAISER_BETA = 7.857
+FIT_DEGREE = 8
+
+
+@dataclass(frozen=True)
+class Trajectory:
+    """rate: positions per second; positions (T, 3) metres."""
+
+    rate: float
+    positions: np.ndarray
+
+    def __post_init__(self):
+        if self.rate <= 0:
+            raise ValueError("trajectory rate must be > 0")
+        p = np.asarray(self.positions, dtype=np.float64)
+        if p.ndim != 2 or p.shape[1] != 3 or p.shape[0] < 1:
+            raise ValueError("positions must be a (T, 3) array with T >= 1")
+        if not np.all(np.isfinite(p)):
+            raise ValueError("positions must be finite")
+        p = p.copy()
+        p.flags.writeable = False
+        object.__setattr__(self, "positions", p)
+        object.__setattr__(self, "rate", float(self.rate))
+
+    def __len__(self):
+        return self.positions.shape[0]
+
+    @property
+    def duration(self):
+        return len(self) / self.rate
+
+
+@lru_cache(maxsize=16)
+def phase_table(factor: int) -> np.ndarray:
+    """(factor, 65) Kaiser(7.857)-windowed sinc rows at r/factor - i, each
+    normalised to sum 1 (constant input passes exactly)."""
+    hw = UPSAMPLE_HALFWIDTH
+    offs = np.arange(-hw, hw + 1, dtype=np.float64)
+    tab = np.empty((factor, offs.size))
+    i0b = np.i0(UPSAMPLE_KAISER_BETA)
+    for r in range(factor):
+        arg = r / factor - offs
+        inside = np.abs(arg) <= hw
+        win = np.zeros_like(arg)
+        z = np.clip(arg / hw, -1.0, 1.0)
+        win[inside] = np.i0(UPSAMPLE_KAISER_BETA * np.sqrt(1.0 - z[inside] ** 2)) / i0b
+        row = np.sinc(arg) * win
+        tab[r] = row / row.sum()
+    tab.flags.writeable = False
+    return tab
+
+
+@lru_cache(maxsize=16)
+def phase_fit(factor: int) -> np.ndarray:
+    """(FIT_DEGREE+1, 65): table[r, c] ~= sum_p fit[p, c] u^p, u = 2r/N - 1."""
+    tab = phase_table(factor)
+    u = 2.0 * np.arange(factor) / factor - 1.0
+    V = u[:, None] ** np.arange(FIT_DEGREE + 1)[None, :]
+    fit, *_ = np.linalg.lstsq(V, tab, rcond=None)
+    fit.flags.writeable = False
+    return fit
+
+
+@lru_cache(maxsize=16)
+def negative_mass(factor: int) -> float:
+    """max over phases of the summed negative weights (overshoot bound)."""
+    tab = phase_table(factor)
+    return float(np.max(np.sum(np.where(tab < 0, -tab, 0.0), axis=1)))
+
+
+_DEV_CONST: dict = {}
+
+
+def device_constants(factor: int, device) -> dict:
+    """Transposed table and polynomial refit of `factor` on `device` (cached)."""
+    key = (int(factor), str(device))
+    c = _DEV_CONST.get(key)
+    if c is None:
+        c = {
+            "tableT": to_dev(np.ascontiguousarray(phase_table(factor).T), torch.float64, device),
+            "fit": to_dev(phase_fit(factor), torch.float64, device),
+            "negsum": negative_mass(factor),
+        }
+        _DEV_CONST[key] = c
+    return c
+
+
+def bandwidth_estimate_dev(pos: torch.Tensor, rate: float, energy_fraction: float = 0.99) -> float:
+    """Largest per-axis frequency holding `energy_fraction` of the
+    mean-removed displacement power (reference trajectory.py:316-339)."""
+    n = pos.shape[0]
+    if n < 2:
+        return 0.0
+    x = pos - pos.mean(dim=0, keepdim=True)
+    pw = torch.fft.rfft(x, dim=0).abs() ** 2
+    tot = pw.sum(dim=0)
+    cum = torch.cumsum(pw, dim=0) / torch.where(tot > 0, tot, torch.ones_like(tot))
+    k = torch.searchsorted(cum.T.contiguous(), torch.full((3, 1), energy_fraction, dtype=cum.dtype,
+                                                          device=cum.device)).squeeze(1)
+    k = torch.clamp(k, max=pw.shape[0] - 1)
+    freqs = k.to(torch.float64) * (rate / n)
+    freqs = torch.where(tot > 0, freqs, torch.zeros_like(freqs))
+    return float(freqs.max().item())
+
+
+def lowpass_columns_dev(x: torch.Tensor, rate: float, cutoff: float) -> torch.Tensor:
+    """Raised-cosine-edged FFT low-pass with odd reflection padding
+    (reference trajectory.py:214-232), on the device."""
+    n = x.shape[0]
+    pad = min(n - 1, max(16, n // 4))
+    head = 2 * x[:1] - torch.flip(x[1:pad + 1], dims=[0])
+    tail = 2 * x[-1:] - torch.flip(x[-pad - 1:-1], dims=[0])
+    ext = torch.cat([head, x, tail], dim=0)
+    m = ext.shape[0]
+    f = torch.arange(m // 2 + 1, device=x.device, dtype=torch.float64) * (rate / m)
+    lo, hi = 0.8 * cutoff, cutoff
+    g = torch.ones_like(f)
+    band = (f > lo) & (f <= hi)
+    g = torch.where(band, 0.5 * (1 + torch.cos(np.pi * (f - lo) / (hi - lo))), g)
+    g = torch.where(f > hi, torch.zeros_like(g), g)
+    y = torch.fft.irfft(torch.fft.rfft(ext, dim=0) * g[:, None], n=m, dim=0)
+    return y[pad:pad + n].contiguous()
+
+
+def decimate_dev(pos: torch.Tensor, rate: float, factor: int) -> torch.Tensor:
+    """Coarse path pos[::N] (device), low-passed first when the measured
+    bandwidth lies in (Nyquist_out, 2 Nyquist_out)."""
+    factor = int(factor)
+    if factor < 1:
+        raise ValueError("decimation factor must be a positive integer")
+    if factor == 1:
+        return pos
+    nyq = 0.5 * rate / factor
+    src = pos
+    if pos.shape[0] >= 2:
+        bw = bandwidth_estimate_dev(pos, rate)
+        if nyq < bw < 2.0 * nyq:
+            src = lowpass_columns_dev(pos, rate, 0.9 * nyq)
+    return src[::factor].contiguous()
+
+
+def decimate(traj: Trajectory, factor: int) -> Trajectory:
+    """Reference-API decimate (trajectory.py:279-298), computed on the GPU."""
+    if int(factor) != factor or factor < 1:
+        raise ValueError("decimation factor must be a positive integer")
+    if factor == 1:
+        return traj
+    dev = require_cuda()
+    p = decimate_dev(to_dev(traj.positions, torch.float64, dev), traj.rate, int(factor))
+    return Trajectory(rate=traj.rate / factor, positions=p.cpu().numpy())
+
+
+def bandlimited_upsample(samples, factor: int, out_len: int) -> np.ndarray:
+    """Windowed-sinc interpolation by `factor` (trajectory.py:260-276) on
+    the GPU (mvb_upsample_streams); exact on constants, endpoints hold."""
+    x = np.asarray(samples, dtype=np.float64)
+    if x.ndim != 1 or x.size == 0:
+        raise ValueError("samples must be a nonempty 1-D sequence")
+    if factor < 1 or int(factor) != factor:
+        raise ValueError("factor must be a positive integer")
+    factor = int(factor)
+    if factor == 1:
+        if out_len <= x.size:
+            return x[:out_len].copy()
+        return np.concatenate([x, np.full(out_len - x.size, x[-1])])
+    dev = require_cuda()
+    xc = to_dev(x, torch.float64, dev)
+    tab = to_dev(phase_table(factor), torch.float64, dev)
+    out = torch.empty(out_len, dtype=torch.float64, device=dev)
+    _lib.call("mvb_upsample_streams", ptr(xc), 1, x.size, ptr(tab), factor, tab.shape[1], out_len,
+              ptr(out), stream_handle(dev))
+    return out.cpu().numpy()

@@ -1,0 +1,119 @@
+"""CPU-only checks of the host layer and the C ABI library (no GPU)."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "mvb.h")
+LIB = os.path.join(ROOT, "paper_2508_03065_b200", "libmvb.so")
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^(?:int|int64_t|const char\*)\s+(mvb_\w+)\(", txt, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    if not os.path.exists(LIB):
+        import __graft_entry__
+        __graft_entry__.build()
+    lib = ctypes.CDLL(LIB)
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(lib, s), s
+
+
+def test_struct_layout_matches_binding():
+    from paper_2508_03065_b200 import _lib
+    _lib.lib()  # raises on mismatch
+
+
+def test_abi_version_and_counts():
+    from paper_2508_03065_b200 import _lib
+    assert _lib.lib().mvb_abi_version() == 1
+    for o in (0, 1, 5, 20):
+        assert _lib.image_count(o) == 1 + sum(4 * k * k + 2 for k in range(1, o + 1))
+
+
+def test_product_refuses_to_run_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2508_03065_b200 import MvbError, Room, SynthesisConfig, Trajectory, hann_sinc, render
+    room = Room(dims=np.array([5.0, 6.0, 4.0]), wall_reflection=0.9)
+    tr = Trajectory(rate=16000.0, positions=np.tile([2.0, 3.0, 2.0], (100, 1)))
+    with pytest.raises(MvbError):
+        render(np.ones(100), tr, room, [1.0, 1.0, 1.0], hann_sinc(32), SynthesisConfig(max_order=1))
+
+
+def test_config_validation():
+    from paper_2508_03065_b200 import SynthesisConfig
+    for kw in [{"audio_rate": 0.0}, {"decimation": 0}, {"order_split": -1}, {"max_order": -1},
+               {"sound_speed": 0.0}, {"d_min": 0.0}, {"workers": 0}, {"eval_budget": 0.0},
+               {"modulate": "both"}, {"t60": -1.0}, {"precision": "fp16"},
+               {"tiers": ((2, 1), (1, 4))}, {"max_order": 5, "tiers": ((2, 1), (4, 8))}]:
+        with pytest.raises(ValueError):
+            SynthesisConfig(**kw)
+    c = SynthesisConfig()
+    assert c.tier_table() == ((1, 1), (3, 3200))
+    assert SynthesisConfig(max_order=1, order_split=1).tier_table() == ((1, 1),)
+
+
+def test_cost_report_matches_reference_numbers():
+    from paper_2508_03065_b200 import SynthesisConfig, cost_report
+    cfg = SynthesisConfig(audio_rate=16000.0, order_split=1, decimation=3200)
+    rep = cost_report(cfg, 45000, 1.0)
+    assert rep["naive_evals"] == 45000 * 16000
+    assert rep["images_low"] == 7 and rep["images_high"] == 45000 - 7
+    assert rep["high_order_reduction"] >= 100.0
+    assert rep["hierarchical_evals"] == 7 * 16000 + (45000 - 7) * 5
+
+
+def test_fast_bank_reduction():
+    from paper_2508_03065_b200.engine import fast_bank
+    from paper_2508_03065_b200.farrow import hann_sinc
+    cb, M1, nb = fast_bank(hann_sinc(64, 14))
+    assert (M1, nb) == (8, 8)
+    mu = np.linspace(0, 1, 501)
+    h = ((mu - 0.5)[:, None] ** np.arange(8)[None, :]) @ cb
+    from oracle.oracle import hann_sinc_taps
+    assert np.max(np.abs(h - hann_sinc_taps(64, mu))) < 6e-7
+
+
+def test_farrow_centering_is_exact():
+    from paper_2508_03065_b200.farrow import centered_branches, hann_sinc
+    f = hann_sinc(32, 14)
+    cb = centered_branches(f.branches)
+    mu = np.linspace(0, 1, 101)
+    a = (mu[:, None] ** np.arange(15)[None, :]) @ f.branches
+    b = ((mu - 0.5)[:, None] ** np.arange(15)[None, :]) @ cb
+    assert np.max(np.abs(a - b)) < 1e-13
+
+
+def test_track_fit_accuracy_against_oracle_upsampler():
+    """The fast path's degree-8 interval polynomials reproduce the
+    reference's 65-tap upsampled tracks."""
+    from oracle import oracle as orc
+    from paper_2508_03065_b200.trajectory import phase_fit, phase_table
+    from paper_2508_03065_b200 import workloads
+    sc = workloads.make_scenes("c3", duration=1.0)[0]
+    dims = sc.dims
+    for N in (32, 256):
+        cpos = sc.pos[::N]
+        off = 2 * np.array([3.0, -2.0, 5.0]) * dims
+        sg = np.array([1.0, -1.0, 1.0])
+        coarse = orc.distance_streams(off[None], sg[None], dims / 2, cpos)[0]
+        ref = orc.upsample_stream(coarse, phase_table(N), N, sc.T)
+        fit = phase_fit(N)
+        K = coarse.size
+        idx = np.clip(np.arange(K)[:, None] + np.arange(65)[None, :] - 32, 0, K - 1)
+        g = coarse[idx] @ fit.T  # (K, 9)
+        u = 2 * np.arange(N) / N - 1
+        d = (g @ (u[None, :] ** np.arange(9)[:, None])).reshape(-1)[:sc.T]
+        assert np.max(np.abs(d - ref)) < 2e-9

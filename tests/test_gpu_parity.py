@@ -1,0 +1,150 @@
+"""GPU parity: libmvb (through its C ABI) against the CPU oracle and the
+golden vectors the reference produced.  Needs a B200 (marker `gpu`).
+
+Bars (north_star): fp64 (exact engine) max |err| <= 1e-10 of the output
+peak -- in practice bit-identical to the oracle; fp32 fast path <= 1e-5 of
+the peak.  Integer/index work (enumeration, out_len) is exact.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_err
+from oracle import oracle as orc
+from paper_2508_03065_b200 import workloads
+from paper_2508_03065_b200.farrow import hann_sinc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU box
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2508_03065_b200 import kernels, room as mroom  # noqa: E402
+from paper_2508_03065_b200.synth import render_jobs, scene_jobs  # noqa: E402
+
+FP32_TOL = 1e-5
+FP64_TOL = 1e-10
+
+
+# ---------------------------------------------------------------- operators
+def test_kernel_trio_bitwise(kernels_golden):
+    g = kernels_golden
+    d = kernels.distance_streams(g["dist_offset"], g["dist_sign"], g["dist_mic"], g["dist_pos"])
+    assert np.array_equal(d, g["dist_out"])
+    out = np.zeros(g["acc_out"].size)
+    kernels.accumulate_images(out, g["acc_streams"], g["acc_tau"], g["acc_amp"], 8, 3)
+    assert np.array_equal(out, g["acc_out"])
+    for N in (16, 64):
+        up = kernels.upsample_stream(g[f"up{N}_coarse"], g[f"table{N}"], N, g[f"up{N}_out"].size)
+        assert np.array_equal(up, g[f"up{N}_out"])
+
+
+def test_branch_filter_matches_oracle(kernels_golden):
+    g = kernels_golden
+    v = kernels.branch_filter(g["acc_x"], g["design_3_8_08"])
+    assert np.array_equal(v, orc.branch_filter(g["acc_x"], g["design_3_8_08"]))
+    assert rel_err(v, g["acc_streams"]) < 1e-15
+
+
+@pytest.mark.parametrize("tag", ["a", "b", "c"])
+def test_enumeration(kernels_golden, tag):
+    g = kernels_golden
+    t = mroom.image_table(g[f"enum_{tag}_dims"], g[f"enum_{tag}_walls"], int(g[f"enum_{tag}_order"]))
+    assert np.array_equal(t.order[0].cpu().numpy(), g[f"enum_{tag}_ord"])
+    assert np.array_equal(t.lattice[0].cpu().numpy(), g[f"enum_{tag}_lattice"])
+    assert np.array_equal(t.parity[0].cpu().numpy(), g[f"enum_{tag}_parity"])
+    assert np.array_equal(t.offset[0].cpu().numpy(), g[f"enum_{tag}_offset"])
+    assert np.array_equal(t.sign[0].cpu().numpy(), g[f"enum_{tag}_sign"])
+    np.testing.assert_allclose(t.beta[0].cpu().numpy(), g[f"enum_{tag}_beta"], rtol=4e-16, atol=0)
+
+
+def test_enumeration_batch_and_large_order():
+    rng = np.random.default_rng(0)
+    dims = rng.uniform(3, 10, size=(5, 3))
+    walls = rng.uniform(0.6, 0.95, size=(5, 6))
+    t = mroom.image_table(dims, walls, 12)
+    for r in range(5):
+        im = orc.enumerate_images(dims[r], walls[r], 12)
+        assert np.array_equal(t.offset[r].cpu().numpy(), im.offset)
+        assert np.array_equal(t.order[r].cpu().numpy(), im.order)
+        np.testing.assert_allclose(t.beta[r].cpu().numpy(), im.beta, rtol=4e-16)
+    t = mroom.image_table([20.0, 15.0, 8.0], 0.9, 40)
+    im = orc.enumerate_images([20.0, 15.0, 8.0], np.full(6, 0.9), 40)
+    assert np.array_equal(t.lattice[0].cpu().numpy(), im.lattice)
+    assert np.array_equal(t.parity[0].cpu().numpy(), im.parity)
+
+
+# ---------------------------------------------------------------- renders
+CASES = {
+    "c1": ("c1", dict()),
+    "c1_refdesign": ("c1", dict(tiers=((1, 1), (3, 32)))),
+    "c2": ("c2", dict(duration=0.25)),
+    "c3": ("c3", dict(duration=0.1, max_order=8, tiers=((2, 1), (5, 32), (8, 256)))),
+    "c4": ("c4", dict(duration=0.25, max_order=6, n_scenes=3)),
+    "c5": ("c5", dict(duration=0.1, max_order=6, n_channels=4, tiers=((2, 1), (4, 32), (6, 256)))),
+}
+
+
+def _scenes(case):
+    wl, over = CASES[case]
+    g = golden(f"render_{case}.npz")
+    scenes = workloads.make_scenes(wl, **over)
+    chans = [int(c) for c in g["channels"]] if wl == "c5" else None
+    return g, scenes, chans
+
+
+def _filter_of(g, L):
+    from paper_2508_03065_b200.farrow import FarrowFilter
+    b = g["branches"]
+    return FarrowFilter(b.shape[0] - 1, b.shape[1], b, (b.shape[1] - 1) // 2, 1.0)
+
+
+def _oracle(scenes, chans, branches):
+    ys = []
+    for sc in scenes:
+        for ch in (chans if chans is not None else range(len(sc.mics))):
+            ys.append(orc.OracleScene(sc.s, sc.pos, sc.mics[ch], sc.dims, sc.walls, sc.max_order,
+                                      sc.tiers, branches, sc.rate).render())
+    return ys
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_exact_engine_matches_oracle_and_reference(case):
+    g, scenes, chans = _scenes(case)
+    f = _filter_of(g, scenes[0].fd_taps)
+    res = render_jobs(scene_jobs(scenes, chans), f, precision="fp64")
+    ys = [res.job(j).cpu().numpy() for j in range(len(res.lengths))]
+    assert [y.size for y in ys] == [int(v) for v in g["lens"]]
+    y = np.concatenate(ys)
+    assert rel_err(y, g["y"]) <= FP64_TOL
+    ref = np.concatenate(_oracle(scenes, chans, g["branches"]))
+    # same arithmetic and order as the oracle: bit-identical (the reference
+    # itself differs from both by np.convolve's summation order, ~1e-15)
+    assert rel_err(y, ref) <= 1e-15
+
+
+@pytest.mark.parametrize("case", ["c2", "c3", "c4", "c5", "c1"])
+def test_fast_engine_matches_oracle(case):
+    g, scenes, chans = _scenes(case)
+    f = _filter_of(g, scenes[0].fd_taps)
+    res = render_jobs(scene_jobs(scenes, chans), f, precision="fp32")
+    ys = [res.job(j).double().cpu().numpy() for j in range(len(res.lengths))]
+    assert [y.size for y in ys] == [int(v) for v in g["lens"]]
+    for y, ref in zip(ys, _oracle(scenes, chans, g["branches"])):
+        assert rel_err(y, ref) <= FP32_TOL
+
+
+def test_fast_engine_reference_design_filter():
+    """The reference's own default filter design(3, 8, 0.8) on the fast
+    path (Farrow M=3, 16-byte records)."""
+    g, scenes, chans = _scenes("c1_refdesign")
+    f = _filter_of(g, 8)
+    sc = scenes[0]
+    s32 = sc.s.astype(np.float32)
+    res = render_jobs(scene_jobs(scenes), f, precision="fp32", signals=[s32])
+    y = res.job(0).double().cpu().numpy()
+    ref = orc.OracleScene(s32.astype(np.float64), sc.pos, sc.mics[0], sc.dims, sc.walls,
+                          sc.max_order, sc.tiers, g["branches"], sc.rate).render()
+    assert y.size == ref.size
+    assert rel_err(y, ref) <= FP32_TOL
