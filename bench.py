@@ -1,0 +1,489 @@
+#!/usr/bin/env python
+"""Benchmark of the moving-source synthesis hot path (BASELINE.json metric:
+image x output-sample updates per second; real-time factor alongside).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
+    python bench.py --impl reference ...   # CPU oracle port on the host cores
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step is one complete render of the workload from device-resident inputs:
+GPU image enumeration, decimation decisions, coarse tracks, exact out_len,
+branch records, interval polynomials, delay sort and the fused synthesis
+(+ the NCCL reduce of image shards for N > 1).  `value` = all updates
+processed by all ranks / max-over-ranks device time.  `e2e` = the same
+metric through the public API `render(s, traj, room, mic, f, cfg)` with host
+numpy buffers (H2D of s/path/mic and D2H of the output inside the timing).
+Default workload: c3 (20x15x8 m hall, order 20, 10 s at 48 kHz, 11521
+images, 64-tap Hann-sinc) -- the largest single-scene config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU work of the cpu_baseline / reference sample")
+    ap.add_argument("--profile", action="store_true",
+                    help="ncu mode: warmup+steps renders only, no probes/e2e/cpu")
+    return ap.parse_args()
+
+
+METRIC = "image x output-sample updates/sec"
+
+
+def workload_note(name):
+    from paper_2508_03065_b200 import workloads
+    w = workloads.WORKLOADS[name]
+    return w
+
+
+# ----------------------------------------------------------------------------
+# clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.file, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.file.flush()
+        self.file.seek(0)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.file.read().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(n)
+        os.unlink(self.file.name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# workload
+
+
+def build_workload(name, rank, world):
+    """Scenes, the jobs this rank renders, and the sharding mode."""
+    from paper_2508_03065_b200 import workloads
+    scenes = workloads.make_scenes(name)
+    w = workloads.WORKLOADS[name]
+    if world == 1:
+        return scenes, scenes, None, "single"
+    if name in ("c3", "c5"):
+        return scenes, scenes, (rank, world), f"image-shard x{world} + NCCL reduce"
+    if name == "c4":
+        mine = [sc for q, sc in enumerate(scenes) if q % world == rank]
+        return scenes, mine, None, f"scene-shard x{world} (no collective)"
+    return scenes, scenes, None, f"replicas x{world}"
+
+
+def device_jobs(scenes, dev):
+    """engine.Job list with every input already resident on the device."""
+    import torch
+    from paper_2508_03065_b200 import engine
+    jobs = []
+    for q, sc in enumerate(scenes):
+        s = torch.from_numpy(np.ascontiguousarray(sc.s)).to(dev)
+        pos = torch.from_numpy(np.ascontiguousarray(sc.pos)).to(dev)
+        for ch, m in enumerate(sc.mics):
+            mic = torch.from_numpy(np.ascontiguousarray(m, dtype=np.float64)).to(dev)
+            jobs.append(engine.Job(s=s, pos=pos, mic=mic, dims=sc.dims, walls=sc.walls,
+                                   max_order=sc.max_order, tiers=sc.tiers, rate=sc.rate,
+                                   signal_key=("s", q), path_key=("p", q)))
+    return jobs
+
+
+# ----------------------------------------------------------------------------
+# CPU oracle sample
+
+
+_ORACLE_CACHE = {}
+
+
+def cpu_sample(name, target_s, nthreads):
+    """Time the oracle port on a bounded slice of the workload: all images of
+    the first scene/channel, output samples [n0, n0 + W) with W calibrated to
+    ~target_s seconds.  Returns (updates/s, description, threads)."""
+    from oracle import oracle as orc
+    from paper_2508_03065_b200 import hann_sinc, workloads
+    if name not in _ORACLE_CACHE:
+        sc = workloads.make_scenes(name, n_scenes=1 if name == "c4" else None,
+                                   n_channels=1 if name == "c5" else None)[0]
+        f = hann_sinc(sc.fd_taps, 14)
+        _ORACLE_CACHE[name] = (sc, orc.OracleScene(sc.s, sc.pos, sc.mics[0], sc.dims, sc.walls,
+                                                   sc.max_order, sc.tiers, f.branches, sc.rate))
+    sc, o = _ORACLE_CACHE[name]
+    S = len(o.images)
+    n0 = sc.T // 2
+    w = 64
+    t = time.perf_counter()
+    o.render_window(n0, n0 + w, nthreads)
+    dt = max(time.perf_counter() - t, 1e-6)
+    w = int(max(64, min(sc.T // 2, w * target_s / dt)))
+    t = time.perf_counter()
+    o.render_window(n0, n0 + w, nthreads)
+    dt = time.perf_counter() - t
+    desc = (f"{name} scene 0 ch 0: all {S} images x output samples [{n0}, {n0 + w}) "
+            f"(oracle C port, Farrow M=14 Hann-sinc L={sc.fd_taps}, per-sample 65-tap tracks)")
+    return S * w / dt, desc, nthreads, S * w, dt
+
+
+# ----------------------------------------------------------------------------
+
+
+def measured_peaks(dev):
+    """FP32 FFMA TFLOP/s and L1-hit load GB/s on this GPU (CUDA events)."""
+    import torch
+    from paper_2508_03065_b200 import _lib
+    from paper_2508_03065_b200._dev import ptr, stream_handle
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sink = torch.zeros(sms * 64, dtype=torch.float32, device=dev)
+    buf = torch.randn(64 * 16 * 1024 // 4, dtype=torch.float32, device=dev)
+    st = stream_handle(dev)
+    out = {}
+    for name, blocks, iters, work in (
+            ("ffma", sms * 8, 4000, lambda b, it: b * 256 * it * 128 * 2),
+            ("l1", sms * 8, 4000, lambda b, it: b * 256 * it * 4 * 16)):
+        best = 0.0
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            if name == "ffma":
+                _lib.call("mvb_peak_ffma", blocks, iters, ptr(sink), st)
+            else:
+                _lib.call("mvb_peak_l1", blocks, iters, ptr(buf), ptr(sink), st)
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, work(blocks, iters) / (e0.elapsed_time(e1) * 1e-3))
+        out[name] = best
+    return out["ffma"] / 1e12, out["l1"] / 1e9
+
+
+def load_traffic(name):
+    p = os.path.join(ROOT, "profiles", f"ncu_synth_{name}.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except (OSError, ValueError):
+            return None
+    return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2508_03065_b200 import (Room, SynthesisConfig, Trajectory, hann_sinc, render,
+                                       workloads)
+    from paper_2508_03065_b200.synth import render_jobs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    name = args.config
+    w = workloads.WORKLOADS[name]
+    scenes, mine, shard, mode = build_workload(name, rank, world)
+    f = hann_sinc(w.fd_taps, 14)
+    jobs = device_jobs(mine, dev)
+    timing = []
+
+    def step(record=False):
+        tl = timing if record else None
+        res = render_jobs(jobs, f, precision="fp32", shard=shard, timing=tl)
+        if shard is not None:
+            dist.reduce(res.out, dst=0, op=dist.ReduceOp.SUM)
+        return res
+
+    if not args.profile:
+        ffma_tf, l1_gbs = measured_peaks(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    barrier()
+    if args.profile:
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        return
+    clocks = ClockSampler(local)
+    clocks.start()
+    total_ms = 0.0
+    updates = 0
+    launches = 0
+    timing.clear()
+    for k in range(args.steps):
+        flush.fill_(float(k))  # L2 flush between timed steps (256 MiB write)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = step(record=True)
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        total_ms += e0.elapsed_time(e1)
+        updates += res.updates
+        launches += res.launches
+    clk = clocks.stop()
+    kern_ms = [a.elapsed_time(b) for a, b in timing]
+    t = torch.tensor([total_ms, float(updates), sum(kern_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        total_ms_all, updates_all = float(tmax[0]), float(tsum[1])
+        if name in ("c1", "c2"):
+            updates_all = float(tsum[1])  # replicas: every rank's work counts
+    else:
+        total_ms_all, updates_all = total_ms, float(updates)
+    value = updates_all / (total_ms_all * 1e-3)
+    ms_step = total_ms_all / args.steps
+    audio_s = sum(sc.T / sc.rate * len(sc.mics) for sc in scenes)
+    if name in ("c1", "c2") and world > 1:
+        audio_s *= world
+    rtf = audio_s * args.steps / (total_ms_all * 1e-3)
+
+    # ---- end to end through the public API with host buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        if world == 1 and len(scenes) == 1 and len(scenes[0].mics) == 1:
+            sc = scenes[0]
+            room = Room(dims=sc.dims, wall_reflection=sc.walls)
+            traj = Trajectory(rate=sc.rate, positions=sc.pos)
+            cfg = SynthesisConfig(audio_rate=sc.rate, max_order=sc.max_order, tiers=sc.tiers,
+                                  precision="fp32")
+            s32 = np.ascontiguousarray(sc.s, dtype=np.float32)
+            y = render(s32, traj, room, sc.mics[0], f, cfg)  # warm
+            tt = 0.0
+            for _ in range(args.steps):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                y = render(s32, traj, room, sc.mics[0], f, cfg)
+                torch.cuda.synchronize()
+                tt += time.perf_counter() - t0
+            e2e_upd = res.updates * args.steps
+            h2d = s32.nbytes + traj.positions.nbytes + np.asarray(sc.mics[0]).nbytes
+            e2e = {"value": e2e_upd / tt, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
+                   "d2h_bytes_per_step": int(y.size * 4), "api": "paper_2508_03065_b200.render"}
+        else:
+            # batch / multi-rank: host numpy in, device render (+ reduce), host out
+            from paper_2508_03065_b200.synth import scene_jobs
+            host_jobs = scene_jobs(mine)
+            tt = 0.0
+            upd = 0
+            h2d = sum(sc.s.nbytes + sc.pos.nbytes + sum(np.asarray(m).nbytes for m in sc.mics)
+                      for sc in mine)
+            d2h = 0
+            for _ in range(args.steps):
+                torch.cuda.synchronize()
+                barrier()
+                t0 = time.perf_counter()
+                r = render_jobs(host_jobs, f, precision="fp32", shard=shard)
+                if shard is not None:
+                    dist.reduce(r.out, dst=0, op=dist.ReduceOp.SUM)
+                out_h = r.out.cpu() if (shard is None or rank == 0) else None
+                torch.cuda.synchronize()
+                barrier()
+                tt += time.perf_counter() - t0
+                upd += r.updates
+                d2h = 0 if out_h is None else out_h.numel() * 4
+            tt_t = torch.tensor([tt, float(upd)], dtype=torch.float64, device=dev)
+            if world > 1:
+                tmax = tt_t.clone()
+                dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+                dist.all_reduce(tt_t, op=dist.ReduceOp.SUM)
+                tt, upd = float(tmax[0]), float(tt_t[1])
+            e2e = {"value": upd / tt, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
+                   "d2h_bytes_per_step": int(d2h), "api": "paper_2508_03065_b200.render_jobs"}
+
+    # ---- roofline of the dominant kernel (fused synthesis) --------------------
+    kern_avg_ms = float(np.mean(kern_ms)) if kern_ms else float("nan")
+    upd_per_launch = res.updates  # one synthesis launch per step
+    flops = upd_per_launch * w.fd_taps * 2.0  # taps x FMA (north_star roofline)
+    achieved = flops / (kern_avg_ms * 1e-3) / 1e12
+    traffic = load_traffic(name)
+    roof = {
+        "kernel": "k_synth_f32 (mvb_synthesize_f32)",
+        "bound": "fp32",
+        "achieved": achieved,
+        "peak": ffma_tf,
+        "unit": "TFLOP/s",
+        "frac": achieved / ffma_tf,
+        "traffic": None if traffic is None else traffic.get("dram_bytes_per_launch"),
+        "peak_source": "measured on this GPU by bench.py (mvb_peak_ffma, best of 3)",
+        "algorithmic": f"{upd_per_launch} updates x {w.fd_taps} taps x 2 flop per launch "
+                       f"(SURVEY 8d: L FMAs per update)",
+        "kernel_ms": kern_avg_ms,
+        "kernel_share_of_step": kern_avg_ms / ms_step if ms_step else None,
+        "executed": {
+            "algorithm": "Farrow (paper Eq. 5): 32 B record gather + 8 FMA Horner per update",
+            "l1_bytes_per_update": 32,
+            "achieved_l1_gbs": upd_per_launch * 32 / (kern_avg_ms * 1e-3) / 1e9,
+            "peak_l1_gbs": l1_gbs,
+            "frac_l1": upd_per_launch * 32 / (kern_avg_ms * 1e-3) / 1e9 / l1_gbs,
+        },
+    }
+
+    # ---- CPU baseline (rank 0, N = 1) -----------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import oracle as orc
+        nth = orc.default_threads()
+        v, desc, th, n_upd, dt = cpu_sample(name, args.cpu_seconds, nth)
+        cpu = {"value": v, "unit": "updates/s", "cores": th, "kind": "port", "sample": desc,
+               "seconds": dt}
+
+    if rank == 0:
+        gsize = {"c1": 1, "c2": 1, "c3": 1, "c4": 256, "c5": 1}[name]
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "updates/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "strong" if (world > 1 and name in ("c3", "c5")) else "weak",
+            "vs_baseline": None,
+            "dtype": "f32 (fp64 delay anchors)",
+            "data": "synthetic (seeded white Gaussian dry signal, seeded paths; SURVEY 8d)",
+            "config": {
+                "workload": name,
+                "scenes": gsize,
+                "channels": len(scenes[0].mics),
+                "images_per_job": int(res.n_images.max()) if world == 1 else None,
+                "out_len": [int(v) for v in res.lengths[:4]],
+                "tiers": [list(t) for t in w.tiers],
+                "fd": f"{w.fd_taps}-tap Hann-windowed sinc (Farrow fit, fp32 path degree 7)",
+                "rate": w.rate,
+                "duration_s": w.duration,
+                "parallelism": mode,
+                "l2": "flushed between timed steps (256 MiB write); per-step working set >L2",
+            },
+            "rtf": rtf,
+            "clocks": clk,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+    nth = orc.default_threads()
+    name = args.config
+    total_upd, total_s = 0, 0.0
+    per = max(2.0, args.cpu_seconds / max(1, args.steps))
+    cpu_sample(name, 0.5, nth)  # warm-up: oracle setup (streams, tracks) + one slice
+    desc = None
+    for _ in range(args.steps):
+        v, desc, th, n_upd, dt = cpu_sample(name, per, nth)
+        total_upd += n_upd
+        total_s += dt
+    value = total_upd / total_s
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": "updates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_s / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded, same generators as the GPU arm)",
+        "config": {"workload": name, "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": nth, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

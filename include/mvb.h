@@ -211,6 +211,16 @@ int mvb_synthesize_f64(const mvb_job* d_jobs, int64_t n_jobs, int64_t max_out_le
                        const double* d_tables, const double* d_streams,
                        const double* d_paths, double* d_out, void* stream);
 
+/* ------------------------------------------------------------------------
+ * 4. Roofline probes (measurement only): FP32 FFMA throughput
+ *    (blocks x 256 threads x iters x 128 FFMA) and L1-hit 16-byte load
+ *    bandwidth (blocks x 256 threads x iters x 4 x 16 B).  Time them with
+ *    CUDA events on `stream`.
+ * --------------------------------------------------------------------- */
+int mvb_peak_ffma(int blocks, int iters, float* d_sink, void* stream);
+int mvb_peak_l1(int blocks, int iters, const float* d_buf /* 1 MiB */, float* d_sink,
+                void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,8 @@ _SIGS = {
     "mvb_synthesize_f32": [P, P, I64, P, P, P, P, P, P, INT, P],
     "mvb_reduce_partials_f32": [P, I64, I64, P, P, P],
     "mvb_synthesize_f64": [P, I64, I64, P, P, P, P, P, P, P],
+    "mvb_peak_ffma": [INT, INT, P, P],
+    "mvb_peak_l1": [INT, INT, P, P, P],
 }
 _RESTYPE = {"mvb_last_error": ctypes.c_char_p, "mvb_image_count": I64}
 

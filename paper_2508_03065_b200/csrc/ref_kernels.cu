@@ -114,6 +114,30 @@ __device__ __forceinline__ void decode_triple(int o, int idx, int& jx, int& jy, 
 
 __device__ __forceinline__ int pydiv2(int a) { return a >= 0 ? a / 2 : -((-a + 1) / 2); }
 
+// x^n for integer n >= 0, carried in double-double (error-free products via
+// FMA) and rounded once: the correctly rounded power, which is what the
+// reference's `float ** int` (glibc pow) returns.
+__device__ double ipow_rn(double x, int n) {
+    double rh = 1.0, rl = 0.0;  // result
+    double bh = x, bl = 0.0;    // base^(2^k)
+    while (n > 0) {
+        if (n & 1) {
+            double p = rh * bh;
+            double e = fma(rh, bh, -p) + (rh * bl + rl * bh);
+            rh = p + e;
+            rl = e - (rh - p);
+        }
+        n >>= 1;
+        if (n) {
+            double p = bh * bh;
+            double e = fma(bh, bh, -p) + 2.0 * bh * bl;
+            bh = p + e;
+            bl = e - (bh - p);
+        }
+    }
+    return rh + rl;
+}
+
 __global__ void k_enumerate(const double* __restrict__ dims, const double* __restrict__ walls,
                             int max_order, int64_t S, int32_t* __restrict__ lattice,
                             int32_t* __restrict__ parity, int32_t* __restrict__ order,
@@ -158,7 +182,7 @@ __global__ void k_enumerate(const double* __restrict__ dims, const double* __res
             int hm, hp;  // room.py:98-105
             if (j >= 0) { hm = j / 2; hp = (j + 1) / 2; }
             else { hm = (-j + 1) / 2; hp = (-j) / 2; }
-            b = xmul(b, xmul(pow(wl[2 * k], (double)hm), pow(wl[2 * k + 1], (double)hp)));
+            b = xmul(b, xmul(ipow_rn(wl[2 * k], hm), ipow_rn(wl[2 * k + 1], hp)));
             if (lattice) lattice[3 * row + k] = l;
             if (parity) parity[3 * row + k] = q;
             if (offset) offset[3 * row + k] = xmul(xmul(2.0, (double)l), dm[k]);

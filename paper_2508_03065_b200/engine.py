@@ -188,6 +188,8 @@ class Geometry:
                   ptr(self.coarse) if self.dec_sel.numel() else ptr(None), ptr(self.tables), ptr(lb),
                   ptr(ub), ptr(scratch), ptr(dmax), st)
         self.dmax = dmax.cpu().numpy()  # the one host sync of the prepare stage
+        self.launches = self.n_enum_launches + 2 + (1 if self.dec_sel.numel() else 0) \
+            + (1 if self.full_sel.numel() else 0) + (2 if self.dec_sel.numel() else 1)
         self.eval_count = [int(self.evals[j]) for j in range(nJ)]
 
     # ------------------------------------------------------------------------
@@ -263,6 +265,7 @@ class Geometry:
         img_base = 0
         coarse_base = 0
         self.order_of_job = [None] * nJ
+        self.n_enum_launches = len(groups)
         for (max_order, tiers, sub), members in groups.items():
             room_key, rooms, member_room = {}, [], []
             for j in members:
@@ -409,6 +412,21 @@ def fast_bank(filt) -> tuple:
 # render stage
 
 
+def _events(timing):
+    if timing is None:
+        return None
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
+def _events_end(timing, e0):
+    if timing is not None:
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        timing.append((e0, e1))
+
+
 @dataclass
 class RenderResult:
     out: torch.Tensor  # flat output (fp32 fast / fp64 exact)
@@ -438,8 +456,10 @@ def _chunking(n_imgs, tiles, sm_count):
 
 
 def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=None,
-           signal_keys=None) -> RenderResult:
-    """Synthesize every job of `geom` (signals[j] is job j's dry signal)."""
+           signal_keys=None, timing: list | None = None) -> RenderResult:
+    """Synthesize every job of `geom` (signals[j] is job j's dry signal).
+    `timing`, if a list, receives (start, end) CUDA events recorded on the
+    launch stream around the synthesis kernel."""
     dev = geom.dev
     st = stream_handle(dev)
     jobs = geom.jobs
@@ -494,8 +514,10 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
             rows[j].update(rec_base=bases[keys[j]], nb=nb)
         jobs_dev = torch.from_numpy(pack_jobs(rows)).to(dev)
         out = torch.empty(int(out_len.sum()), dtype=torch.float64, device=dev)
+        ev = _events(timing)
         _lib.call("mvb_synthesize_f64", ptr(jobs_dev), nJ, int(out_len.max()), ptr(geom.images),
                   ptr(geom.coarse), ptr(geom.tables), ptr(streams), ptr(geom.paths), ptr(out), st)
+        _events_end(timing, ev)
         launches += 1
         upd = int(np.sum(out_len * geom.n_img))
         return RenderResult(out, offsets, out_len, geom.n_img.copy(), upd, launches)
@@ -558,8 +580,10 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
     work_dev = torch.from_numpy(np.asarray(work, dtype=np.int32).reshape(-1, 8)).to(dev)
     out = torch.empty(int(out_len.sum()), dtype=torch.float32, device=dev)
     part = torch.empty(max(part_rows, 1), dtype=torch.float32, device=dev)
+    ev = _events(timing)
     _lib.call("mvb_synthesize_f32", ptr(jobs_dev), ptr(work_dev), len(work), ptr(images_sorted),
               ptr(coef), ptr(rec), ptr(geom.paths), ptr(out), ptr(part), nb, st)
+    _events_end(timing, ev)
     launches += 1
     if part_rows:
         _lib.call("mvb_reduce_partials_f32", ptr(jobs_dev), nJ, int(out_len.max()), ptr(part),

@@ -345,10 +345,13 @@ def scene_jobs(scenes, channels=None) -> list:
     return jobs
 
 
-def render_jobs(jobs, f, precision="fp32", shard=None, signals=None):
+def render_jobs(jobs, f, precision="fp32", shard=None, signals=None, timing=None):
     """Geometry + render of a job batch; returns engine.RenderResult
-    (device output, per-job offsets/lengths, update count)."""
+    (device output, per-job offsets/lengths, update count, launches)."""
     geom = engine.Geometry(jobs)
     sig = signals if signals is not None else [jb.s for jb in jobs]
     keys = [engine._key(jb.signal_key, jb.s) for jb in jobs]
-    return engine.render(geom, sig, f, precision=precision, shard=shard, signal_keys=keys)
+    res = engine.render(geom, sig, f, precision=precision, shard=shard, signal_keys=keys,
+                        timing=timing)
+    res.launches += geom.launches
+    return res
