@@ -124,6 +124,9 @@ typedef struct mvb_job {
     int32_t L, d0;            /* branch length (= delay shift) and D0           */
     int32_t n_chunks, nb;     /* image chunks; branches per record / stream     */
     double rate, c, d_min, kappa; /* kappa = rate / c                           */
+    int64_t rec_front;        /* fast path: zero rows before branch sample 0, so
+                                 row index rec_base - rec_front + (idx + rec_front)
+                                 is never negative                              */
 } mvb_job;
 
 /* One CTA of the fast synthesis grid: samples [32U*tile, 32U*(tile+1)) of
@@ -183,15 +186,19 @@ int mvb_sort_keys(const mvb_image* d_images, int64_t n_img, const mvb_job* d_job
 int mvb_rank(const double* d_key, const mvb_job* d_jobs, int64_t n_jobs, int64_t max_n_img,
              int32_t* d_rank, void* stream);
 
-/* Fast path: interleaved fp32 branch records rec[(pad + m) * nb + k] for
- * m < T + L - 1 (v'_k = x (*) c'_k, d_cbranch (M1, L) fp64 in the centred
- * basis (mu - 1/2)^k, zero branches k >= M1); other rows are left as the
- * caller zeroed them.  L <= 128. */
+/* Fast path: fp32 branch records v'_k = x (*) c'_k (d_cbranch (M1, L) fp64
+ * in the centred basis (mu - 1/2)^k, zero branches k >= M1) for input
+ * samples m < T + L - 1, written to global rows row0 + m.  Layout: rows in
+ * blocks of 64; block b holds nb/4 planes of 64 float4 (plane p = branches
+ * 4p..4p+3), i.e. row r plane p is float4 number r + (nb/4 - 1)(r & ~63) +
+ * 64 p.  Rows outside are left as the caller zeroed them.  L <= 128;
+ * row0 + T + L < 2^31. */
 int mvb_branch_records_f32(const float* d_x, int64_t T, const double* d_cbranch, int M1,
-                           int L, int nb, int64_t pad, float* d_rec, void* stream);
+                           int L, int nb, int64_t row0, float* d_rec, void* stream);
 
 /* Fast synthesis (fp32 I/O, fp64 anchors), one CTA per work item; jobs
- * with n_chunks > 1 write d_part[part_off + chunk*out_len + n]. */
+ * with n_chunks > 1 write d_part[part_off + chunk*out_len + n].  Gather rows
+ * are rec_base + n + L - D (global, never negative: front zero pad). */
 int mvb_synthesize_f32(const mvb_job* d_jobs, const mvb_work* d_work, int64_t n_work,
                        const mvb_image* d_images, const mvb_coef32* d_coef,
                        const float* d_rec, const double* d_paths, float* d_out,

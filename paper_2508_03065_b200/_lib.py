@@ -50,7 +50,7 @@ _SIGS = {
 }
 _RESTYPE = {"mvb_last_error": ctypes.c_char_p, "mvb_image_count": I64}
 
-IMAGE_BYTES, JOB_BYTES, WORK_BYTES, COEF_BYTES = 96, 128, 32, 48
+IMAGE_BYTES, JOB_BYTES, WORK_BYTES, COEF_BYTES = 96, 136, 32, 48
 
 
 class MvbError(RuntimeError):

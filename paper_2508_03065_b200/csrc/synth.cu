@@ -1,20 +1,29 @@
 // Fractional-delay synthesis (synth.py:194-258 + _kernels.py:90-136).
 //
 // Fast path (fp32 I/O, the B200 roofline path)
-//   k_branch_records_f32  v'_k = x (*) c'_k for the centred Farrow bank,
-//                         stored interleaved: one 32-byte record (8 floats)
-//                         per input sample, zero-padded on both sides so the
-//                         gather needs no bounds test (the reference's
-//                         `valid` window reads zeros outside [0, ls)).
+//   k_branch_records_f32  v'_k = x (*) c'_k for the centred Farrow bank.
+//                         Record layout: rows (input samples, zero-padded on
+//                         both sides so the gather needs no bounds test --
+//                         the reference's `valid` window reads zeros) in
+//                         blocks of 64; a block stores plane 0 (branches
+//                         0..3, one float4 per row) for its 64 rows, then
+//                         plane 1 (branches 4..7), ...  A warp's gather of 32
+//                         consecutive rows is one coalesced 512-byte load per
+//                         plane, and plane p sits at an immediate +1 KiB*p
+//                         from plane 0, so one IMAD.WIDE addresses a row.
 //   k_synth_f32           one CTA per (job, 32*U-sample tile, image chunk);
 //                         8 warps walk the chunk's delay-sorted images, lane
 //                         l of a warp owns samples n0 + 32u + l, u < U.  Per
 //                         update: the interval polynomial of the track (fp32
 //                         around an fp64 anchor), the (D, mu) split, one
-//                         2x16-byte coalesced record gather (L1), Horner in
-//                         mu - 1/2, gain 1/(4 pi d) and one FMA into a register
-//                         accumulator.  Warps are reduced in fixed order in
-//                         shared memory, then written coalesced.
+//                         coalesced 16-byte load per plane (L1), an even/odd
+//                         Horner in mu - 1/2 on paired FMAs (FFMA2), gain
+//                         1/(4 pi d) and one FMA into a register accumulator.
+//                         Decimated tiers with N | 1024 run an N-templated
+//                         body whose interval reloads sit at compile-time
+//                         steps, so the 32 unrolled steps are straight-line
+//                         code and overlap.  Warps reduce in fixed order in
+//                         shared memory, then write coalesced.
 //   k_reduce_f32          fixed-order sum of chunk partials.
 //
 // Exact path (fp64): k_synth_f64 repeats the reference arithmetic for every
@@ -27,21 +36,38 @@
 namespace mvb {
 
 // ---------------------------------------------------------------------------
-// branch records
+// record layout
 
-template <int NB>
+constexpr int REC_BLOCK = 64;  // rows per block
+
+// float4 index of plane 0 of row r (plane p adds REC_BLOCK * p)
+template <int NP>
+__host__ __device__ __forceinline__ unsigned rec_index(unsigned r) {
+    return r + (NP - 1) * (r & ~(unsigned)(REC_BLOCK - 1));
+}
+
+// &base[rec_index(r)] as one IMAD.WIDE.U32
+template <int NP>
+__device__ __forceinline__ const float4* rec_row(const float4* base, unsigned r) {
+    const float4* p;
+    asm("mad.wide.u32 %0, %1, 16, %2;" : "=l"(p) : "r"(rec_index<NP>(r)), "l"(base));
+    return p;
+}
+
+template <int NP>
 __global__ void k_branch_records_f32(const float* __restrict__ x, int64_t T,
-                                     const double* __restrict__ cb, int M1, int L, int64_t pad,
+                                     const double* __restrict__ cb, int M1, int L, int64_t row0,
                                      float* __restrict__ rec) {
+    constexpr int NB = 4 * NP;
     extern __shared__ float sx[];  // [blockDim.x + L - 1]
     __shared__ float sc[NB * 128];
     const int64_t m0 = (int64_t)blockIdx.x * blockDim.x;
-    for (int t = threadIdx.x; t < NB * L && t < NB * 128; t += blockDim.x) {
-        int k = t / L, j = t - (t / L) * L;
+    for (int t = threadIdx.x; t < NB * L; t += blockDim.x) {
+        const int k = t / L, j = t - (t / L) * L;
         sc[k * L + j] = k < M1 ? (float)cb[k * L + j] : 0.f;
     }
     for (int t = threadIdx.x; t < (int)blockDim.x + L - 1; t += blockDim.x) {
-        int64_t q = m0 - (L - 1) + t;
+        const int64_t q = m0 - (L - 1) + t;
         sx[t] = (q >= 0 && q < T) ? x[q] : 0.f;
     }
     __syncthreads();
@@ -50,49 +76,117 @@ __global__ void k_branch_records_f32(const float* __restrict__ x, int64_t T,
     float acc[NB];
 #pragma unroll
     for (int k = 0; k < NB; ++k) acc[k] = 0.f;
-    // v_k[m] = sum_j c_k[j] x[m - j]; sx[threadIdx.x + L-1 - j] = x[m - j]
+    // v_k[m] = sum_j c_k[j] x[m - j];  sx[threadIdx.x + L-1 - j] = x[m - j]
     for (int j = 0; j < L; ++j) {
-        float xv = sx[threadIdx.x + L - 1 - j];
+        const float xv = sx[threadIdx.x + L - 1 - j];
 #pragma unroll
         for (int k = 0; k < NB; ++k) acc[k] = fmaf(sc[k * L + j], xv, acc[k]);
     }
-    float4* o = reinterpret_cast<float4*>(rec + (pad + m) * NB);
+    float4* o = reinterpret_cast<float4*>(rec) + rec_index<NP>((unsigned)(row0 + m));
 #pragma unroll
-    for (int q = 0; q < NB / 4; ++q) o[q] = make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+    for (int p = 0; p < NP; ++p)
+        o[REC_BLOCK * p] = make_float4(acc[4 * p], acc[4 * p + 1], acc[4 * p + 2], acc[4 * p + 3]);
 }
 
 // ---------------------------------------------------------------------------
-// fast synthesis
+// fast synthesis helpers
 
-template <int NB>
-__device__ __forceinline__ float gather_horner(const float4* __restrict__ R, int64_t idx, float mc) {
-    const float4* p = R + idx * (NB / 4);
-    float h;
-    if constexpr (NB == 4) {
-        float4 a = __ldg(p);
-        h = fmaf(fmaf(fmaf(a.w, mc, a.z), mc, a.y), mc, a.x);
-    } else if constexpr (NB == 8) {
-        float4 a = __ldg(p), b = __ldg(p + 1);
-        h = b.w;
-        h = fmaf(h, mc, b.z);
-        h = fmaf(h, mc, b.y);
-        h = fmaf(h, mc, b.x);
-        h = fmaf(h, mc, a.w);
-        h = fmaf(h, mc, a.z);
-        h = fmaf(h, mc, a.y);
-        h = fmaf(h, mc, a.x);
-    } else {
-        float v[NB];
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+// Even/odd Horner with paired FMAs (SASS FFMA2):  sum_k v_k x^k =
+// E(x^2) + x O(x^2); the (even, odd) coefficient pairs are adjacent floats
+// of the records, i.e. ready-made float2 operands.
+template <int NP>
+__device__ __forceinline__ float gather_horner(const float4* __restrict__ R, unsigned row,
+                                               float mc) {
+    const float y = mc * mc;
+    const float2 yy = f2(y, y);
+    const float4* a = rec_row<NP>(R, row);
+    float4 v[NP];
 #pragma unroll
-        for (int q = 0; q < NB / 4; ++q) {
-            float4 a = __ldg(p + q);
-            v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
-        }
-        h = v[NB - 1];
+    for (int p = 0; p < NP; ++p) v[p] = __ldg(a + REC_BLOCK * p);
+    float2 q = f2(v[NP - 1].z, v[NP - 1].w);
+    q = __ffma2_rn(q, yy, f2(v[NP - 1].x, v[NP - 1].y));
 #pragma unroll
-        for (int k = NB - 2; k >= 0; --k) h = fmaf(h, mc, v[k]);
+    for (int p = NP - 2; p >= 0; --p) {
+        q = __ffma2_rn(q, yy, f2(v[p].z, v[p].w));
+        q = __ffma2_rn(q, yy, f2(v[p].x, v[p].y));
     }
-    return h;
+    return fmaf(mc, q.y, q.x);
+}
+
+// Track residual kappa*(d(u) - g0) = u * sum_{p=1..8} g_p u^(p-1), same
+// even/odd pairing over the record's (g1,g2), (g3,g4), (g5,g6), (g7,g8).
+__device__ __forceinline__ float track_residual(const float4& c1, const float4& c2, float uu) {
+    const float y = uu * uu;
+    const float2 yy = f2(y, y);
+    float2 q = f2(c2.z, c2.w);
+    q = __ffma2_rn(q, yy, f2(c2.x, c2.y));
+    q = __ffma2_rn(q, yy, f2(c1.z, c1.w));
+    q = __ffma2_rn(q, yy, f2(c1.x, c1.y));
+    return fmaf(uu, q.y, q.x) * uu;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// predicated 16-byte read-only load: v keeps its value when !pred
+__device__ __forceinline__ void ldg4_if(float4& v, const float4* p, bool pred) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+        "@q ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];\n\t}"
+        : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
+        : "l"(p), "r"((int)pred));
+}
+
+// rint via the 1.5*2^23 trick: v = t + MAGIC holds rint(t) in its low
+// mantissa bits (|t| < 2^22): bits(v) = 0x4B400000 + rint(t).
+constexpr float MAGIC_F = 12582912.0f;
+constexpr int MAGIC_I = 0x4B400000;
+
+// One decimated-image step given the interval record (c0, c1, c2):
+// nlB = rec_base + n0 + lane + L + MAGIC_I - B.  Returns the contribution.
+template <int NP>
+__device__ __forceinline__ float dec_step(const float4& c0, const float4& c1, const float4& c2,
+                                          float uu, int rowbase, const float4* __restrict__ R,
+                                          float an, float invk, float dmin) {
+    const float res = track_residual(c1, c2, uu);  // kappa * (d - g0)
+    const float t = c0.y + res;
+    const float v = t + MAGIC_F;
+    const float mc = t - (v - MAGIC_F);
+    const unsigned row = (unsigned)(rowbase - __float_as_int(v));
+    const float d = fmaf(res, invk, c0.z);
+    const float A = an * rcp_approx(fmaxf(d, dmin));
+    return A * gather_horner<NP>(R, row, mc);
+}
+
+// Decimated image on a tile wholly inside [0, T) with TILE % NT == 0: the
+// tile starts on an interval boundary, interval q covers steps
+// [q*SPI, (q+1)*SPI) and u = 2r/N - 1 is a per-step constant plus a lane
+// term -- no per-step bookkeeping, straight-line steps.
+template <int U, int NP, int NT>
+__device__ __forceinline__ void dec_static(float (&acc)[U], const float4* __restrict__ cf4,
+                                           const float4* __restrict__ R, int n0, int lane,
+                                           int nl, float an, float invk, float dmin) {
+    constexpr int SPI = NT / 32;  // steps per coarse interval
+    const unsigned k0 = (unsigned)(n0 / NT);
+    const float lt = (float)lane * (2.0f / NT);
+    float4 c0, c1, c2;
+    int nlB = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (u % SPI == 0) {
+            const float4* c = cf4 + 3u * (k0 + (unsigned)(u / SPI));
+            c0 = __ldg(c);
+            c1 = __ldg(c + 1);
+            c2 = __ldg(c + 2);
+            nlB = nl - __float_as_int(c0.x);
+        }
+        const float uu = lt + ((float)((u % SPI) * 32) * (2.0f / NT) - 1.0f);
+        acc[u] += dec_step<NP>(c0, c1, c2, uu, nlB + 32 * u, R, an, invk, dmin);
+    }
 }
 
 constexpr int SYNTH_WARPS = 8;
@@ -103,7 +197,7 @@ constexpr int SYNTH_WARPS = 8;
 #define SYNTH_MINB 2
 #endif
 
-template <int U, int NB, int MINB>
+template <int U, int NP, int MINB>
 __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     const mvb_job* __restrict__ jobs, const mvb_work* __restrict__ work,
     const mvb_image* __restrict__ images, const mvb_coef32* __restrict__ coef,
@@ -115,17 +209,23 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     const int img_begin = wp->img_begin, img_end = wp->img_end;
     const mvb_job* Jp = jobs + wp->job;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t n0 = (int64_t)wp->tile * TN;
+    const int n0 = wp->tile * TN;
     const int T = Jp->T;
     const int Lsh = Jp->L;
-    const float4* __restrict__ R = reinterpret_cast<const float4*>(rec) + Jp->rec_base * (NB / 4);
+    // rows are indexed globally: row = rec_base + (n + L - D) >= 0 thanks to
+    // the zero front pad of every signal's region
+    const int rb = (int)Jp->rec_base;
+    const float4* __restrict__ R = reinterpret_cast<const float4*>(rec);
     const mvb_image* __restrict__ imgs = images + Jp->img_off;
+    const float invk = (float)(1.0 / Jp->kappa);
+    const float dmin = (float)Jp->d_min;
     float* __restrict__ row = red[warp];
 #pragma unroll
     for (int u = 0; u < U; ++u) row[32 * u + lane] = 0.f;
     float acc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) acc[u] = 0.f;
+    const bool inside = n0 + TN <= T;  // no hold-extension inside this tile
 
     for (int i = img_begin + warp; i < img_end; i += SYNTH_WARPS) {
         const mvb_image* ip = imgs + i;
@@ -136,7 +236,6 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
             // accumulated in the warp's own shared-memory row
             const double kappa = Jp->kappa;
             const double sL = (double)(Lsh - Jp->d0);
-            const float dmin = (float)Jp->d_min;
             const double ox = ip->off[0], oy = ip->off[1], oz = ip->off[2];
             const double sx = ip->sign[0], sy = ip->sign[1], sz = ip->sign[2];
             const double* P = paths + 3 * Jp->pos_off;
@@ -144,38 +243,68 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
             const double* Q = paths + 3 * Jp->mic_off;
 #pragma unroll 1
             for (int u = 0; u < U; ++u) {
-                const int64_t n = n0 + 32 * u + lane;
-                const int64_t m = n < T ? n : T - 1;
-                const double* p = P + 3 * m;
-                const double* q = moving ? Q + 3 * m : Q;
-                double dx = ox + sx * p[0] - q[0];
-                double dy = oy + sy * p[1] - q[1];
-                double dz = oz + sz * p[2] - q[2];
-                double d = sqrt(dx * dx + dy * dy + dz * dz);
-                double s = fma(d, kappa, sL);
-                double D = floor(s);
-                float mc = (float)(s - D) - 0.5f;
-                int64_t idx = n + Lsh - (int64_t)D;
-                float A = __fdividef(an, fmaxf((float)d, dmin));
-                row[32 * u + lane] = fmaf(A, gather_horner<NB>(R, idx, mc), row[32 * u + lane]);
+                const int n = n0 + 32 * u + lane;
+                const int m = n < T ? n : T - 1;
+                const double* p = P + 3 * (int64_t)m;
+                const double* q = moving ? Q + 3 * (int64_t)m : Q;
+                const double dx = ox + sx * p[0] - q[0];
+                const double dy = oy + sy * p[1] - q[1];
+                const double dz = oz + sz * p[2] - q[2];
+                const double d = sqrt(dx * dx + dy * dy + dz * dz);
+                const double s = fma(d, kappa, sL);
+                const double D = floor(s);
+                const float mc = (float)(s - D) - 0.5f;
+                const unsigned r = (unsigned)(rb + n + Lsh - (int)D);
+                const float A = an * rcp_approx(fmaxf((float)d, dmin));
+                row[32 * u + lane] = fmaf(A, gather_horner<NP>(R, r, mc), row[32 * u + lane]);
+            }
+            continue;
+        }
+        const float4* __restrict__ cf4 = reinterpret_cast<const float4*>(coef + ip->coef);
+        const int nl = rb + n0 + lane + Lsh + MAGIC_I;
+        if (inside && (N == 32 || N == 64 || N == 128 || N == 256)) {
+            switch (N) {
+                case 32: dec_static<U, NP, 32>(acc, cf4, R, n0, lane, nl, an, invk, dmin); break;
+                case 64: dec_static<U, NP, 64>(acc, cf4, R, n0, lane, nl, an, invk, dmin); break;
+                case 128: dec_static<U, NP, 128>(acc, cf4, R, n0, lane, nl, an, invk, dmin); break;
+                default: dec_static<U, NP, 256>(acc, cf4, R, n0, lane, nl, an, invk, dmin); break;
+            }
+        } else if (inside && (N & 31) == 0) {
+            // ---- warp-uniform intervals, predicated reloads ----
+            const float twoInvN = 2.0f / (float)N;
+            unsigned k = (unsigned)(n0 / N);
+            int r0 = n0 - (int)k * N;  // multiple of 32
+            float4 c0 = __ldg(cf4 + 3u * k), c1 = __ldg(cf4 + 3u * k + 1), c2 = __ldg(cf4 + 3u * k + 2);
+            const float lanef = (float)lane;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (u > 0) {
+                    r0 += 32;
+                    const bool w = r0 == N;
+                    r0 = w ? 0 : r0;
+                    k += w;
+                    const float4* c = cf4 + 3u * k;
+                    ldg4_if(c0, c, w);
+                    ldg4_if(c1, c + 1, w);
+                    ldg4_if(c2, c + 2, w);
+                }
+                const float uu = fmaf((float)r0 + lanef, twoInvN, -1.f);
+                acc[u] += dec_step<NP>(c0, c1, c2, uu, nl - __float_as_int(c0.x) + 32 * u, R, an,
+                                       invk, dmin);
             }
         } else {
-            const mvb_coef32* __restrict__ cf = coef + ip->coef;
+            // ---- generic: per-lane intervals (N % 32 != 0, or the tile
+            // reaches the hold-extended tail n >= T) ----
             const float twoInvN = 2.0f / (float)N;
-            const float invk = (float)(1.0 / Jp->kappa);
-            const float dmin = (float)Jp->d_min;
-            // (k, r) of each lane's first sample, then advanced by 32 per step
-            const int mfirst = (int)(n0 + lane < T ? n0 + lane : T - 1);
+            const int mfirst = n0 + lane < T ? n0 + lane : T - 1;
             int k = mfirst / N;
             int r = mfirst - k * N;
             const int kT = (T - 1) / N, rT = (T - 1) - kT * N;
             int kc = -1;
-            int B = 0;
-            float f = 0.f, dm = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f,
-                  g6 = 0.f, g7 = 0.f;
+            float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0, c2 = c0;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int64_t n = n0 + 32 * u + lane;
+                const int n = n0 + 32 * u + lane;
                 if (u > 0) {
                     if (n < T) {
                         r += 32;
@@ -186,31 +315,13 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
                     }
                 }
                 if (k != kc) {
-                    const float4* c4 = reinterpret_cast<const float4*>(cf + k);
-                    float4 h0 = __ldg(c4), h1 = __ldg(c4 + 1), h2 = __ldg(c4 + 2);
-                    B = __float_as_int(h0.x);
-                    f = h0.y; dm = h0.z;
-                    g0 = h1.x; g1 = h1.y; g2 = h1.z; g3 = h1.w;
-                    g4 = h2.x; g5 = h2.y; g6 = h2.z; g7 = h2.w;
+                    const float4* c = cf4 + 3u * (unsigned)k;
+                    c0 = __ldg(c); c1 = __ldg(c + 1); c2 = __ldg(c + 2);
                     kc = k;
                 }
                 const float uu = fmaf((float)r, twoInvN, -1.f);
-                float t = g7;
-                t = fmaf(t, uu, g6);
-                t = fmaf(t, uu, g5);
-                t = fmaf(t, uu, g4);
-                t = fmaf(t, uu, g3);
-                t = fmaf(t, uu, g2);
-                t = fmaf(t, uu, g1);
-                t = fmaf(t, uu, g0);
-                const float res = t * uu;  // kappa * (d - g0)
-                t = f + res;
-                const float rt = rintf(t);
-                const float mc = t - rt;
-                const int idx = (int)n + Lsh - B - (int)rt;
-                const float d = fmaf(res, invk, dm);
-                const float A = __fdividef(an, fmaxf(d, dmin));
-                acc[u] = fmaf(A, gather_horner<NB>(R, idx, mc), acc[u]);
+                acc[u] += dec_step<NP>(c0, c1, c2, uu, nl - __float_as_int(c0.x) + 32 * u, R, an,
+                                       invk, dmin);
             }
         }
     }
@@ -224,7 +335,7 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
         float s = red[0][t];
 #pragma unroll
         for (int q = 1; q < SYNTH_WARPS; ++q) s += red[q][t];
-        const int64_t n = n0 + t;
+        const int64_t n = (int64_t)n0 + t;
         if (n < out_len) dst[n] = s;
     }
 }
@@ -309,19 +420,19 @@ using namespace mvb;
 extern "C" {
 
 int mvb_branch_records_f32(const float* x, int64_t T, const double* cb, int M1, int L, int nb,
-                           int64_t pad, float* rec, void* stream) {
-    if (T < 1 || L < 1 || M1 < 1 || M1 > nb || pad < 0) return fail(MVB_EINVAL, "branch_records: sizes");
+                           int64_t row0, float* rec, void* stream) {
+    if (T < 1 || L < 1 || L > 128 || M1 < 1 || M1 > nb || row0 < 0 || row0 + T + L > 0x7fffffffLL)
+        return fail(MVB_EINVAL, "branch_records: sizes");
     if (!x || !cb || !rec) return fail(MVB_EINVAL, "branch_records: null");
-    if (nb * L > nb * 128) return fail(MVB_EINVAL, "branch_records: L > 128");
     const int block = 256;
-    size_t smem = sizeof(float) * (block + L - 1);
-    unsigned g = grid_for(T + L - 1, block);
+    const size_t smem = sizeof(float) * (block + L - 1);
+    const unsigned g = grid_for(T + L - 1, block);
     cudaStream_t s = as_stream(stream);
     switch (nb) {
-        case 4: k_branch_records_f32<4><<<g, block, smem, s>>>(x, T, cb, M1, L, pad, rec); break;
-        case 8: k_branch_records_f32<8><<<g, block, smem, s>>>(x, T, cb, M1, L, pad, rec); break;
-        case 12: k_branch_records_f32<12><<<g, block, smem, s>>>(x, T, cb, M1, L, pad, rec); break;
-        case 16: k_branch_records_f32<16><<<g, block, smem, s>>>(x, T, cb, M1, L, pad, rec); break;
+        case 4: k_branch_records_f32<1><<<g, block, smem, s>>>(x, T, cb, M1, L, row0, rec); break;
+        case 8: k_branch_records_f32<2><<<g, block, smem, s>>>(x, T, cb, M1, L, row0, rec); break;
+        case 12: k_branch_records_f32<3><<<g, block, smem, s>>>(x, T, cb, M1, L, row0, rec); break;
+        case 16: k_branch_records_f32<4><<<g, block, smem, s>>>(x, T, cb, M1, L, row0, rec); break;
         default: return fail(MVB_EINVAL, "branch_records: nb must be 4, 8, 12 or 16");
     }
     return check_launch("branch_records_f32");
@@ -337,13 +448,16 @@ int mvb_synthesize_f32(const mvb_job* jobs, const mvb_work* work, int64_t n_work
     cudaStream_t s = as_stream(stream);
     const unsigned g = (unsigned)n_work;
     const int block = SYNTH_WARPS * 32;
+#define MVB_SYNTH(NP) k_synth_f32<SYNTH_U, NP, SYNTH_MINB><<<g, block, 0, s>>>( \
+        jobs, work, images, coef, rec, paths, out, part)
     switch (nb) {
-        case 4: k_synth_f32<SYNTH_U, 4, SYNTH_MINB><<<g, block, 0, s>>>(jobs, work, images, coef, rec, paths, out, part); break;
-        case 8: k_synth_f32<SYNTH_U, 8, SYNTH_MINB><<<g, block, 0, s>>>(jobs, work, images, coef, rec, paths, out, part); break;
-        case 12: k_synth_f32<SYNTH_U, 12, SYNTH_MINB><<<g, block, 0, s>>>(jobs, work, images, coef, rec, paths, out, part); break;
-        case 16: k_synth_f32<SYNTH_U, 16, SYNTH_MINB><<<g, block, 0, s>>>(jobs, work, images, coef, rec, paths, out, part); break;
+        case 4: MVB_SYNTH(1); break;
+        case 8: MVB_SYNTH(2); break;
+        case 12: MVB_SYNTH(3); break;
+        case 16: MVB_SYNTH(4); break;
         default: return fail(MVB_EINVAL, "synthesize_f32: nb must be 4, 8, 12 or 16");
     }
+#undef MVB_SYNTH
     return check_launch("synthesize_f32");
 }
 

@@ -36,11 +36,11 @@ from . import _lib
 from ._dev import ptr, require_cuda, stream_handle
 from .farrow import as_filter, centered_branches
 from .room import image_count, image_table
-from .trajectory import device_constants, lowpass_columns_dev, negative_mass
+from .trajectory import bandwidth_batch, device_constants, lowpass_columns_dev, negative_mass
 
 SYNTH_U = 32
 TILE = 32 * SYNTH_U  # output samples per CTA
-IMG_COLS, JOB_COLS, WORK_COLS = 12, 16, 4
+IMG_COLS, JOB_COLS, WORK_COLS = 12, 17, 4
 PAD_MARGIN = 64
 FOUR_PI = 4.0 * np.pi
 
@@ -96,6 +96,7 @@ def pack_jobs(rows: list) -> np.ndarray:
                      r["img_off"], r["n_img"], r["pos_off"], r["mic_off"]]
         i32[j] = [r["T"], r["mic_moving"], r["L"], r["d0"], r["n_chunks"], r["nb"]]
         f64[j] = [r["rate"], r["c"], r["d_min"], r["kappa"]]
+        a[j, 16] = r.get("rec_front", 0)
     return a
 
 
@@ -216,7 +217,7 @@ class Geometry:
         for (T, rate), starts in by_len.items():
             idx = torch.tensor(starts, device=dev)[:, None] + torch.arange(T, device=dev)[None, :]
             x = self.paths[idx]  # (G, T, 3)
-            bw_t = _bandwidth_batch(x, rate)
+            bw_t = bandwidth_batch(x, rate)
             for r0, b in zip(starts, bw_t.cpu().numpy().tolist()):
                 bw[(r0, T, rate)] = b
         coarse_src = {}
@@ -354,26 +355,6 @@ class Geometry:
     def tau_max(self, j: int) -> float:
         jb = self.jobs[j]
         return float(jb.rate) * float(self.dmax[j]) / float(jb.c)
-
-
-def _bandwidth_batch(x: torch.Tensor, rate: float, energy_fraction: float = 0.99) -> torch.Tensor:
-    """Per-path 99%-energy bandwidth (reference trajectory.py:316-339) of
-    x (G, T, 3) on the device."""
-    G, T, _ = x.shape
-    if T < 2:
-        return torch.zeros(G, dtype=torch.float64, device=x.device)
-    xc = x - x.mean(dim=1, keepdim=True)
-    pw = torch.fft.rfft(xc, dim=1).abs() ** 2  # (G, F, 3)
-    tot = pw.sum(dim=1)  # (G, 3)
-    cum = torch.cumsum(pw, dim=1) / torch.where(tot > 0, tot, torch.ones_like(tot))[:, None, :]
-    F = pw.shape[1]
-    cumT = cum.permute(0, 2, 1).reshape(G * 3, F).contiguous()
-    k = torch.searchsorted(cumT, torch.full((G * 3, 1), energy_fraction, dtype=cumT.dtype,
-                                            device=x.device)).squeeze(1)
-    k = torch.clamp(k, max=F - 1).reshape(G, 3)
-    f = k.to(torch.float64) * (rate / T)
-    f = torch.where(tot > 0, f, torch.zeros_like(f))
-    return f.max(dim=1).values
 
 
 # ----------------------------------------------------------------------------
@@ -531,6 +512,9 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
         back = front + TILE + PAD_MARGIN
         bases[k] = (rec_rows, front)
         rec_rows += front + sig_len[k] + L - 1 + back
+    rec_rows = -(-rec_rows // 64) * 64  # whole 64-row blocks (mvb.h record layout)
+    if rec_rows + int(out_len.max()) + L >= 2**31 - 0x4B400000:
+        raise ValueError("batch too large for 32-bit record rows; split it")
     rec = torch.zeros(rec_rows * nb, dtype=torch.float32, device=dev)
     for k in uniq:
         r0, front = bases[k]
@@ -539,7 +523,7 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
         launches += 1
     for j in range(nJ):
         r0, front = bases[keys[j]]
-        rows[j].update(rec_base=r0 + front, nb=nb)
+        rows[j].update(rec_base=r0 + front, rec_front=front, nb=nb)
     # image slices of this shard (in delay-sorted order)
     rank_, world = (0, 1) if shard is None else (int(shard[0]), int(shard[1]))
     lo = (geom.n_img * rank_) // world
