@@ -169,11 +169,12 @@ int mvb_track_max(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jo
                   const double* d_coarse, const double* d_tables, const double* d_lb,
                   const double* d_ub, int32_t* d_scratch, double* d_dmax, void* stream);
 
-/* Fast-path interval records of the images d_sel (factor > 1):
- * d_coef[image.coef + k] for k < K, from the coarse distances and the
- * factor's refit block d_fits[image.fit * 585]. */
+/* Fast-path interval records of the images d_sel, all of one decimation
+ * factor N: d_coef[image.coef + k] for k < K, from the coarse distances and
+ * h_fit, the factor's (9, 65) refit of its phase-table columns in
+ * u = 2r/N - 1 (HOST pointer; passed to the kernel by value). */
 int mvb_track_coeffs(const mvb_image* d_images, const int32_t* d_sel, int64_t n_sel,
-                     const mvb_job* d_jobs, const double* d_coarse, const double* d_fits,
+                     const mvb_job* d_jobs, const double* d_coarse, const double* h_fit,
                      mvb_coef32* d_coef, void* stream);
 
 /* Delay-sort key of every image: its distance at the middle of its job's
@@ -196,13 +197,14 @@ int mvb_rank(const double* d_key, const mvb_job* d_jobs, int64_t n_jobs, int64_t
 int mvb_branch_records_f32(const float* d_x, int64_t T, const double* d_cbranch, int M1,
                            int L, int nb, int64_t row0, float* d_rec, void* stream);
 
-/* Fast synthesis (fp32 I/O, fp64 anchors), one CTA per work item; jobs
- * with n_chunks > 1 write d_part[part_off + chunk*out_len + n].  Gather rows
- * are rec_base + n + L - D (global, never negative: front zero pad). */
+/* Fast synthesis (fp32 I/O, fp64 anchors), one CTA per work item covering
+ * 32*u_steps output samples (u_steps 16 or 32); jobs with n_chunks > 1 write
+ * d_part[part_off + chunk*out_len + n].  Gather rows are rec_base + n + L - D
+ * (global, never negative: front zero pad). */
 int mvb_synthesize_f32(const mvb_job* d_jobs, const mvb_work* d_work, int64_t n_work,
                        const mvb_image* d_images, const mvb_coef32* d_coef,
                        const float* d_rec, const double* d_paths, float* d_out,
-                       float* d_part, int nb, void* stream);
+                       float* d_part, int nb, int u_steps, void* stream);
 
 /* Fixed-order sum of the n_chunks partial rows of every job. */
 int mvb_reduce_partials_f32(const mvb_job* d_jobs, int64_t n_jobs, int64_t max_out_len,

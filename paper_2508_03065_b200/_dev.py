@@ -37,5 +37,6 @@ def to_dev(a, dtype, device) -> torch.Tensor:
     """numpy / torch -> contiguous device tensor of dtype (no copy if already)."""
     if isinstance(a, torch.Tensor):
         return a.to(device=device, dtype=dtype).contiguous()
-    arr = np.ascontiguousarray(np.asarray(a), dtype=torch.empty((), dtype=dtype).numpy().dtype)
-    return torch.from_numpy(arr).to(device, non_blocking=False)
+    arr = np.array(np.asarray(a), dtype=torch.empty((), dtype=dtype).numpy().dtype, order="C")
+    # pinned staging + async copy: no host/stream serialisation
+    return torch.from_numpy(arr).pin_memory().to(device, non_blocking=True)

@@ -42,7 +42,7 @@ _SIGS = {
     "mvb_sort_keys": [P, I64, P, P, P, P, P],
     "mvb_rank": [P, P, I64, I64, P, P],
     "mvb_branch_records_f32": [P, I64, P, INT, INT, INT, I64, P, P],
-    "mvb_synthesize_f32": [P, P, I64, P, P, P, P, P, P, INT, P],
+    "mvb_synthesize_f32": [P, P, I64, P, P, P, P, P, P, INT, INT, P],
     "mvb_reduce_partials_f32": [P, I64, I64, P, P, P],
     "mvb_synthesize_f64": [P, I64, I64, P, P, P, P, P, P, P],
     "mvb_peak_ffma": [INT, INT, P, P],

@@ -190,12 +190,6 @@ __device__ __forceinline__ void dec_static(float (&acc)[U], const float4* __rest
 }
 
 constexpr int SYNTH_WARPS = 8;
-#ifndef SYNTH_U
-#define SYNTH_U 32
-#endif
-#ifndef SYNTH_MINB
-#define SYNTH_MINB 2
-#endif
 
 template <int U, int NP, int MINB>
 __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
@@ -440,23 +434,33 @@ int mvb_branch_records_f32(const float* x, int64_t T, const double* cb, int M1, 
 
 int mvb_synthesize_f32(const mvb_job* jobs, const mvb_work* work, int64_t n_work,
                        const mvb_image* images, const mvb_coef32* coef, const float* rec,
-                       const double* paths, float* out, float* part, int nb, void* stream) {
+                       const double* paths, float* out, float* part, int nb, int u_steps,
+                       void* stream) {
     if (n_work < 0 || n_work > 0x7fffffff) return fail(MVB_EINVAL, "synthesize_f32: n_work");
     if (n_work == 0) return MVB_OK;
     if (!jobs || !work || !images || !rec || !paths || !out)
         return fail(MVB_EINVAL, "synthesize_f32: null");
+    if (u_steps != 16 && u_steps != 32) return fail(MVB_EINVAL, "synthesize_f32: u_steps 16 or 32");
     cudaStream_t s = as_stream(stream);
     const unsigned g = (unsigned)n_work;
     const int block = SYNTH_WARPS * 32;
-#define MVB_SYNTH(NP) k_synth_f32<SYNTH_U, NP, SYNTH_MINB><<<g, block, 0, s>>>( \
+    // U = 32 (1024-sample tiles, 2 CTAs/SM) or U = 16 (512-sample tiles, 3 CTAs/SM)
+#define MVB_SYNTH(U, NP, MB) k_synth_f32<U, NP, MB><<<g, block, 0, s>>>( \
         jobs, work, images, coef, rec, paths, out, part)
-    switch (nb) {
-        case 4: MVB_SYNTH(1); break;
-        case 8: MVB_SYNTH(2); break;
-        case 12: MVB_SYNTH(3); break;
-        case 16: MVB_SYNTH(4); break;
-        default: return fail(MVB_EINVAL, "synthesize_f32: nb must be 4, 8, 12 or 16");
+#define MVB_SYNTH_NB(U, MB)                         \
+    switch (nb) {                                   \
+        case 4: MVB_SYNTH(U, 1, MB); break;         \
+        case 8: MVB_SYNTH(U, 2, MB); break;         \
+        case 12: MVB_SYNTH(U, 3, MB); break;        \
+        case 16: MVB_SYNTH(U, 4, MB); break;        \
+        default: return fail(MVB_EINVAL, "synthesize_f32: nb must be 4, 8, 12 or 16"); \
     }
+    if (u_steps == 32) {
+        MVB_SYNTH_NB(32, 2)
+    } else {
+        MVB_SYNTH_NB(16, 3)
+    }
+#undef MVB_SYNTH_NB
 #undef MVB_SYNTH
     return check_launch("synthesize_f32");
 }

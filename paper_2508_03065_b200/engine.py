@@ -26,6 +26,7 @@ its delay-sorted images (fast path); the caller sums the partial outputs
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, field
 
@@ -36,9 +37,11 @@ from . import _lib
 from ._dev import ptr, require_cuda, stream_handle
 from .farrow import as_filter, centered_branches
 from .room import image_count, image_table
-from .trajectory import bandwidth_batch, device_constants, lowpass_columns_dev, negative_mass
+from .trajectory import decimate_batch, device_constants, negative_mass, phase_fit
 
-SYNTH_U = 32
+import os
+
+SYNTH_U = int(os.environ.get("MVB_SYNTH_U", "16"))  # 16 or 32 steps per lane
 TILE = 32 * SYNTH_U  # output samples per CTA
 IMG_COLS, JOB_COLS, WORK_COLS = 12, 17, 4
 PAD_MARGIN = 64
@@ -60,6 +63,12 @@ class Job:
     image_index: object = None  # optional subset of the canonical image order
     signal_key: object = None  # jobs with equal keys share one dry signal
     path_key: object = None  # jobs with equal keys share one source path
+
+
+def h2d(a: np.ndarray, dev) -> torch.Tensor:
+    """Host array -> device through pinned memory, without a host sync."""
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    return t.pin_memory().to(dev, non_blocking=True)
 
 
 def _key(explicit, obj):
@@ -170,7 +179,7 @@ class Geometry:
                 T=int(self.T[j]), mic_moving=int(self.moving[j]), L=0, d0=0, n_chunks=1, nb=0,
                 rate=float(jb.rate), c=float(jb.c), d_min=float(jb.d_min),
                 kappa=float(jb.rate) / float(jb.c)))
-        jobs_dev = torch.from_numpy(pack_jobs(self.job_rows)).to(dev)
+        jobs_dev = h2d(pack_jobs(self.job_rows), dev)
         # ---- coarse tracks, bounds, exact max ---------------------------------
         n_img = self.n_images
         self.coarse = torch.empty(max(self.n_coarse_total, 1), dtype=torch.float64, device=dev)
@@ -188,52 +197,56 @@ class Geometry:
         _lib.call("mvb_track_max", ptr(self.images), ptr(jobs_dev), nJ,
                   ptr(self.coarse) if self.dec_sel.numel() else ptr(None), ptr(self.tables), ptr(lb),
                   ptr(ub), ptr(scratch), ptr(dmax), st)
-        self.dmax = dmax.cpu().numpy()  # the one host sync of the prepare stage
+        # dmax reaches the host through a pinned copy + event: the render stage
+        # queues its out_len-independent kernels before it waits (dmax_host)
+        self._dmax_host = torch.empty(nJ, dtype=torch.float64, pin_memory=True)
+        self._dmax_host.copy_(dmax, non_blocking=True)
+        self._dmax_ready = torch.cuda.Event()
+        self._dmax_ready.record()
+        self._dmax = None
         self.launches = self.n_enum_launches + 2 + (1 if self.dec_sel.numel() else 0) \
             + (1 if self.full_sel.numel() else 0) + (2 if self.dec_sel.numel() else 1)
         self.eval_count = [int(self.evals[j]) for j in range(nJ)]
 
+    @property
+    def dmax(self) -> np.ndarray:
+        """Per-job exact track maximum (waits for the geometry kernels only)."""
+        if self._dmax is None:
+            self._dmax_ready.synchronize()
+            self._dmax = self._dmax_host.numpy().copy()
+        return self._dmax
+
     # ------------------------------------------------------------------------
     def _decimate_paths(self):
-        """Fill the coarse path slots: pos[::N] (and receiver[::N]); the
-        anti-alias low-pass runs only where the reference's decision
-        (Nyquist_out < bandwidth < 2 Nyquist_out) says so.  Bandwidths of all
-        distinct paths are measured in one batched FFT per path length."""
+        """Fill the coarse path slots with pos[::N] (and receiver[::N]).  The
+        reference's anti-alias decision (low-pass only when Nyquist_out <
+        bandwidth < 2 Nyquist_out, trajectory.py:279-298) is taken and applied
+        on the device for all paths of one length at once (decimate_batch):
+        no host round trip, one index_copy per (length, factor)."""
         jobs, dev = self.jobs, self.dev
-        # distinct full-rate paths that need decimation: (row, T, rate) -> factors
-        need = {}
+        groups = {}  # (T, rate) -> {row0: position}
+        uses = {}  # (T, rate, N) -> list of (position, destination row)
         for (j, N), dst in self.cpath.items():
-            T = int(self.T[j])
-            rate = float(jobs[j].rate)
-            need.setdefault((int(self.pos_off[j]), T, rate), set()).add(N)
+            T, rate = int(self.T[j]), float(jobs[j].rate)
+            g = groups.setdefault((T, rate), {})
+            K = -(-T // N)
+            srcs = [(int(self.pos_off[j]), dst)]
             if self.moving[j]:
-                need.setdefault((int(self.mic_off[j]), T, rate), set()).add(N)
-        if not need:
-            return
-        bw = {}
-        by_len = {}
-        for (r0, T, rate) in need:
-            by_len.setdefault((T, rate), []).append(r0)
-        for (T, rate), starts in by_len.items():
-            idx = torch.tensor(starts, device=dev)[:, None] + torch.arange(T, device=dev)[None, :]
-            x = self.paths[idx]  # (G, T, 3)
-            bw_t = bandwidth_batch(x, rate)
-            for r0, b in zip(starts, bw_t.cpu().numpy().tolist()):
-                bw[(r0, T, rate)] = b
-        coarse_src = {}
-        for key, factors in need.items():
-            r0, T, rate = key
-            for N in factors:
-                nyq = 0.5 * rate / N
-                src = self.paths[r0:r0 + T]
-                if T >= 2 and nyq < bw[key] < 2.0 * nyq:
-                    src = lowpass_columns_dev(src, rate, 0.9 * nyq)
-                coarse_src[(r0, N)] = src[::N]
-        for (j, N), dst in self.cpath.items():
-            K = -(-int(self.T[j]) // N)
-            self.paths[dst:dst + K] = coarse_src[(int(self.pos_off[j]), N)]
-            if self.moving[j]:
-                self.paths[dst + K:dst + 2 * K] = coarse_src[(int(self.mic_off[j]), N)]
+                srcs.append((int(self.mic_off[j]), dst + K))
+            for r0, d in srcs:
+                pos = g.setdefault(r0, len(g))
+                uses.setdefault((T, rate, N), []).append((pos, d))
+        for (T, rate), rows in groups.items():
+            starts = sorted(rows, key=rows.get)
+            x = torch.stack([self.paths[r0:r0 + T] for r0 in starts])  # (G, T, 3)
+            for (T2, rate2, N), lst in uses.items():
+                if (T2, rate2) != (T, rate):
+                    continue
+                coarse = decimate_batch(x, rate, N)  # (G, K, 3)
+                K = coarse.shape[1]
+                info = h2d(np.asarray(lst, dtype=np.int64), dev)
+                dst = (info[:, 1:2] + torch.arange(K, device=dev)[None, :]).reshape(-1)
+                self.paths.index_copy_(0, dst, coarse[info[:, 0]].reshape(-1, 3))
 
     def _build_images(self):
         jobs, dev = self.jobs, self.dev
@@ -263,6 +276,7 @@ class Geometry:
         self.n_img = np.zeros(nJ, np.int64)
         self.evals = np.zeros(nJ, np.int64)
         blocks, dec_sel, full_sel = [], [], []
+        by_factor = {}
         img_base = 0
         coarse_base = 0
         self.order_of_job = [None] * nJ
@@ -280,28 +294,36 @@ class Geometry:
                 member_room.append(room_key[k])
             tab = image_table(np.stack([r[0] for r in rooms]), np.stack([r[1] for r in rooms]),
                               max_order, dev)
-            sel = None if sub is None else torch.as_tensor(np.asarray(sub, np.int64), device=dev)
+            sel = None if sub is None else h2d(np.asarray(sub, np.int64), dev)
+            # canonical order is sorted by reflection order, 4o^2+2 images per
+            # order: tiers and interval counts follow on the host, no sync
+            order_np = np.repeat(np.arange(max_order + 1),
+                                 [1] + [4 * o * o + 2 for o in range(1, max_order + 1)])
+            if sub is not None:
+                order_np = order_np[np.asarray(sub, np.int64)]
             order = tab.order[0] if sel is None else tab.order[0][sel]
-            S = int(order.numel())
-            fac = torch.ones(S, dtype=torch.int64, device=dev)
+            S = int(order_np.size)
+            fac_np = np.ones(S, np.int64)
             prev = -1
             for mo, N in tiers:
-                fac = torch.where((order > prev) & (order <= mo), torch.full_like(fac, N), fac)
+                fac_np[(order_np > prev) & (order_np <= mo)] = N
                 prev = mo
-            fac_np = fac.cpu().numpy()
             G = len(members)
-            ridx = torch.as_tensor(member_room, device=dev)
+            ridx = h2d(np.asarray(member_room, np.int64), dev)
             offset = tab.offset[ridx]
             sign = tab.sign[ridx]
             beta = tab.beta[ridx]
             if sel is not None:
                 offset, sign, beta = offset[:, sel], sign[:, sel], beta[:, sel]
-            Tj = torch.as_tensor(self.T[members], device=dev)
+            K_np = np.where(fac_np[None, :] > 1,
+                            -(-self.T[members][:, None] // fac_np[None, :]), 0)  # (G, S)
+            cnt_np = K_np.reshape(-1)
+            coarse_off_np = coarse_base + np.cumsum(cnt_np) - cnt_np
+            coarse_base += int(cnt_np.sum())
+            fac = h2d(fac_np, dev)
             Nf = fac[None, :].expand(G, S)
-            K = torch.where(Nf > 1, (Tj[:, None] + Nf - 1) // Nf, torch.zeros_like(Nf))
-            cnt = K.reshape(-1)
-            coarse_off = coarse_base + torch.cumsum(cnt, 0) - cnt
-            coarse_base += int(cnt.sum().item()) if cnt.numel() else 0
+            K = h2d(K_np, dev)
+            coarse_off = h2d(coarse_off_np, dev)
             table = torch.zeros_like(Nf)
             fit = torch.zeros_like(Nf)
             cpath = torch.zeros_like(Nf)
@@ -311,7 +333,7 @@ class Geometry:
                 m = Nf == N
                 table = torch.where(m, torch.full_like(table, self.table_off[N]), table)
                 fit = torch.where(m, torch.full_like(fit, self.fit_idx[N]), fit)
-                cp = torch.as_tensor([self.cpath[(j, N)] for j in members], device=dev)[:, None]
+                cp = h2d(np.asarray([self.cpath[(j, N)] for j in members], np.int64), dev)[:, None]
                 cpath = torch.where(m, cp.expand(G, S), cpath)
             blk = torch.zeros(G, S, IMG_COLS, dtype=torch.int64, device=dev)
             f64 = blk.view(torch.float64)
@@ -328,25 +350,31 @@ class Geometry:
             blk[:, :, 9] = table
             blk[:, :, 10] = cpath
             j32 = blk[:, :, 11:12].view(torch.int32)
-            j32[:, :, 0] = torch.as_tensor(members, dtype=torch.int32, device=dev)[:, None]
+            j32[:, :, 0] = h2d(np.asarray(members, np.int32), dev)[:, None]
             j32[:, :, 1] = fit.to(torch.int32)
             blocks.append(blk.reshape(G * S, IMG_COLS))
-            flat_dec = torch.nonzero((Nf > 1).reshape(-1)).squeeze(1) + img_base
-            flat_full = torch.nonzero((Nf == 1).reshape(-1)).squeeze(1) + img_base
+            tiled = np.tile(fac_np, G)
+            flat_dec = h2d(np.nonzero(tiled > 1)[0].astype(np.int32) + img_base, dev)
+            flat_full = h2d(np.nonzero(tiled == 1)[0].astype(np.int32) + img_base, dev)
+            for N in set(fac_np.tolist()) - {1}:
+                by_factor.setdefault(int(N), []).append(
+                    np.nonzero(tiled == N)[0].astype(np.int32) + img_base)
             dec_sel.append(flat_dec)
             full_sel.append(flat_full)
-            n_full = int((fac_np == 1).sum())
+            facs, cnts = np.unique(fac_np, return_counts=True)
             for g, j in enumerate(members):
                 self.img_off[j] = img_base + g * S
                 self.n_img[j] = S
                 T = int(self.T[j])
-                self.evals[j] = n_full * T + sum(-(-T // int(N)) for N in fac_np.tolist() if N > 1)
+                self.evals[j] = int(sum(c * (T if N == 1 else -(-T // int(N)))
+                                        for N, c in zip(facs.tolist(), cnts.tolist())))
                 self.order_of_job[j] = order
             img_base += G * S
         self.images = torch.cat(blocks) if len(blocks) > 1 else blocks[0]
         self.n_images = img_base
         self.n_coarse_total = coarse_base
         self.dec_sel = torch.cat(dec_sel).to(torch.int32)
+        self.sel_by_factor = {N: h2d(np.concatenate(v), dev) for N, v in by_factor.items()}
         self.full_sel = torch.cat(full_sel).to(torch.int32)
         if self.full_sel.numel() > 65535:
             raise ValueError("more than 65535 full-rate images in one batch")
@@ -361,7 +389,18 @@ class Geometry:
 # filter banks
 
 
+_BANKS: dict = {}
+
+
 def fast_bank(filt) -> tuple:
+    f = as_filter(filt)
+    key = (f.branches.shape, f.branches.tobytes())
+    if key not in _BANKS:
+        _BANKS[key] = _fast_bank(f)
+    return _BANKS[key]
+
+
+def _fast_bank(filt) -> tuple:
     """Centred fp32-path Farrow bank: (coeffs (M1, L) fp64, M1, nb).  Banks
     above degree 7 are reduced to degree 7 when that changes no tap by more
     than 5e-7 of the largest tap (below fp32 resolution of the path)."""
@@ -459,41 +498,47 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
     sig_dev, sig_len = {}, {}
     for k, members in uniq.items():
         s = signals[members[0]]
-        t = s.to(dev, dt) if isinstance(s, torch.Tensor) else torch.from_numpy(
-            np.ascontiguousarray(np.asarray(s), dtype=np.float32 if dt == torch.float32 else np.float64)).to(dev)
+        t = s.to(dev, dt) if isinstance(s, torch.Tensor) else h2d(
+            np.asarray(s, dtype=np.float32 if dt == torch.float32 else np.float64), dev)
         t = t.reshape(-1).contiguous()
         if t.numel() == 0:
             raise ValueError("input must be a nonempty 1-D signal")
         sig_dev[k], sig_len[k] = t, t.numel()
-    out_len = np.zeros(nJ, np.int64)
-    tau_ceil = np.zeros(nJ, np.int64)
-    for j in range(nJ):
-        tau_ceil[j] = int(math.ceil(geom.tau_max(j)))
-        out_len[j] = sig_len[keys[j]] + tau_ceil[j] + L
-    offsets = np.concatenate([[0], np.cumsum(out_len)[:-1]]).astype(np.int64)
-    rows = [dict(r) for r in geom.job_rows]
-    for j in range(nJ):
-        rows[j].update(out_off=int(offsets[j]), out_len=int(out_len[j]), L=L, d0=d0,
-                       ls=int(sig_len[keys[j]] + L - 1))
     launches = 0
+    base_rows = [dict(r, L=L, d0=d0) for r in geom.job_rows]
+
+    def finish_rows():
+        """out_len needs the exact track max (waits for the geometry kernels)."""
+        out_len = np.zeros(nJ, np.int64)
+        tau_ceil = np.zeros(nJ, np.int64)
+        for j in range(nJ):
+            tau_ceil[j] = int(math.ceil(geom.tau_max(j)))
+            out_len[j] = sig_len[keys[j]] + tau_ceil[j] + L
+        offsets = np.concatenate([[0], np.cumsum(out_len)[:-1]]).astype(np.int64)
+        rows = [dict(r) for r in base_rows]
+        for j in range(nJ):
+            rows[j].update(out_off=int(offsets[j]), out_len=int(out_len[j]),
+                           ls=int(sig_len[keys[j]] + L - 1))
+        return out_len, tau_ceil, offsets, rows
+
     if precision == "fp64":
         if shard is not None and shard[1] > 1:
             raise ValueError("the exact fp64 engine runs replicas only (no image sharding)")
         nb = int(f.poly_order) + 1
-        br = torch.from_numpy(np.ascontiguousarray(f.branches, dtype=np.float64)).to(dev)
+        br = h2d(np.asarray(f.branches, dtype=np.float64), dev)
         base, bases = 0, {}
         for k in uniq:
             bases[k] = base
             base += nb * (sig_len[k] + L - 1)
         streams = torch.empty(base, dtype=torch.float64, device=dev)
         for k in uniq:
-            T = sig_len[k]
-            _lib.call("mvb_branch_filter", ptr(sig_dev[k]), T, ptr(br), nb, L,
+            _lib.call("mvb_branch_filter", ptr(sig_dev[k]), sig_len[k], ptr(br), nb, L,
                       ptr(streams[bases[k]:]), st)
             launches += 1
+        out_len, _, offsets, rows = finish_rows()
         for j in range(nJ):
             rows[j].update(rec_base=bases[keys[j]], nb=nb)
-        jobs_dev = torch.from_numpy(pack_jobs(rows)).to(dev)
+        jobs_dev = h2d(pack_jobs(rows), dev)
         out = torch.empty(int(out_len.sum()), dtype=torch.float64, device=dev)
         ev = _events(timing)
         _lib.call("mvb_synthesize_f64", ptr(jobs_dev), nJ, int(out_len.max()), ptr(geom.images),
@@ -504,8 +549,30 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
         return RenderResult(out, offsets, out_len, geom.n_img.copy(), upd, launches)
 
     # ---------------------------------------------------------------- fast --
+    # 1. work that does not depend on out_len: interval records and the
+    #    per-job delay sort (queued before the host waits for dmax)
     cb, M1, nb = fast_bank(f)
-    cb_dev = torch.from_numpy(np.ascontiguousarray(cb)).to(dev)
+    cb_dev = h2d(np.ascontiguousarray(cb), dev)
+    pre_dev = h2d(pack_jobs(base_rows), dev)
+    coef = torch.empty(max(geom.n_coarse_total, 1) * 12, dtype=torch.float32, device=dev)
+    for N, sel in geom.sel_by_factor.items():
+        fit = np.ascontiguousarray(phase_fit(N), dtype=np.float64)
+        _lib.call("mvb_track_coeffs", ptr(geom.images), ptr(sel), sel.numel(), ptr(pre_dev),
+                  ptr(geom.coarse), fit.ctypes.data_as(ctypes.c_void_p), ptr(coef), st)
+        launches += 1
+    key = torch.empty(geom.n_images, dtype=torch.float64, device=dev)
+    _lib.call("mvb_sort_keys", ptr(geom.images), geom.n_images, ptr(pre_dev), ptr(geom.paths),
+              ptr(geom.coarse), ptr(key), st)
+    rank = torch.empty(geom.n_images, dtype=torch.int32, device=dev)
+    _lib.call("mvb_rank", ptr(key), ptr(pre_dev), nJ, int(geom.n_img.max()), ptr(rank), st)
+    launches += 2
+    job_of_img = geom.images[:, 11:12].view(torch.int32)[:, 0].to(torch.int64)
+    job_base = h2d(geom.img_off, dev)[job_of_img]
+    perm = torch.empty(geom.n_images, dtype=torch.int64, device=dev)
+    perm[job_base + rank.to(torch.int64)] = torch.arange(geom.n_images, device=dev)
+    images_sorted = geom.images[perm]
+    # 2. out_len, zero-padded branch records, work list, synthesis
+    out_len, tau_ceil, offsets, rows = finish_rows()
     rec_rows, bases = 0, {}
     for k, members in uniq.items():
         front = int(max(tau_ceil[j] for j in members)) + L + PAD_MARGIN
@@ -531,7 +598,7 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
     tiles = [-(-int(out_len[j]) // TILE) for j in range(nJ)]
     chunks = _chunking([int(hi[j] - lo[j]) for j in range(nJ)], tiles, sm_count)
     part_rows = 0
-    work = []
+    blocks = []
     for j in range(nJ):
         nc = chunks[j] if hi[j] > lo[j] else 1
         rows[j]["n_chunks"] = nc
@@ -539,34 +606,22 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
             rows[j]["part_off"] = part_rows
             part_rows += nc * int(out_len[j])
         span = int(hi[j] - lo[j])
-        for c in range(nc):
-            a = int(lo[j]) + (span * c) // nc
-            b = int(lo[j]) + (span * (c + 1)) // nc
-            for t in range(tiles[j]):
-                work.append((j, t, a, b, c, 0, 0, 0))
-    jobs_dev = torch.from_numpy(pack_jobs(rows)).to(dev)
-    coef = torch.empty(max(geom.n_coarse_total, 1) * 12, dtype=torch.float32, device=dev)
-    if geom.dec_sel.numel():
-        _lib.call("mvb_track_coeffs", ptr(geom.images), ptr(geom.dec_sel), geom.dec_sel.numel(),
-                  ptr(jobs_dev), ptr(geom.coarse), ptr(geom.fits), ptr(coef), st)
-        launches += 1
-    key = torch.empty(geom.n_images, dtype=torch.float64, device=dev)
-    _lib.call("mvb_sort_keys", ptr(geom.images), geom.n_images, ptr(jobs_dev), ptr(geom.paths),
-              ptr(geom.coarse), ptr(key), st)
-    rank = torch.empty(geom.n_images, dtype=torch.int32, device=dev)
-    _lib.call("mvb_rank", ptr(key), ptr(jobs_dev), nJ, int(geom.n_img.max()), ptr(rank), st)
-    launches += 2
-    job_of_img = geom.images[:, 11:12].view(torch.int32)[:, 0].to(torch.int64)
-    job_base = torch.as_tensor(geom.img_off, device=dev)[job_of_img]
-    perm = torch.empty(geom.n_images, dtype=torch.int64, device=dev)
-    perm[job_base + rank.to(torch.int64)] = torch.arange(geom.n_images, device=dev)
-    images_sorted = geom.images[perm].contiguous()
-    work_dev = torch.from_numpy(np.asarray(work, dtype=np.int32).reshape(-1, 8)).to(dev)
+        cs = np.arange(nc)
+        blk = np.zeros((nc, tiles[j], 8), dtype=np.int32)  # mvb_work rows
+        blk[:, :, 0] = j
+        blk[:, :, 1] = np.arange(tiles[j])[None, :]
+        blk[:, :, 2] = (int(lo[j]) + (span * cs) // nc)[:, None]
+        blk[:, :, 3] = (int(lo[j]) + (span * (cs + 1)) // nc)[:, None]
+        blk[:, :, 4] = cs[:, None]
+        blocks.append(blk.reshape(-1, 8))
+    work = np.concatenate(blocks)
+    jobs_dev = h2d(pack_jobs(rows), dev)
+    work_dev = h2d(work, dev)
     out = torch.empty(int(out_len.sum()), dtype=torch.float32, device=dev)
     part = torch.empty(max(part_rows, 1), dtype=torch.float32, device=dev)
     ev = _events(timing)
     _lib.call("mvb_synthesize_f32", ptr(jobs_dev), ptr(work_dev), len(work), ptr(images_sorted),
-              ptr(coef), ptr(rec), ptr(geom.paths), ptr(out), ptr(part), nb, st)
+              ptr(coef), ptr(rec), ptr(geom.paths), ptr(out), ptr(part), nb, SYNTH_U, st)
     _events_end(timing, ev)
     launches += 1
     if part_rows:

@@ -137,23 +137,42 @@ def bandwidth_estimate_dev(pos: torch.Tensor, rate: float, energy_fraction: floa
     return float(bandwidth_batch(pos[None], rate, energy_fraction)[0].item())
 
 
-def lowpass_columns_dev(x: torch.Tensor, rate: float, cutoff: float) -> torch.Tensor:
+def lowpass_batch(x: torch.Tensor, rate: float, cutoff: float) -> torch.Tensor:
     """Raised-cosine-edged FFT low-pass with odd reflection padding
-    (reference trajectory.py:214-232), on the device."""
-    n = x.shape[0]
+    (reference trajectory.py:214-232) of x (G, T, 3) on the device."""
+    n = x.shape[1]
     pad = min(n - 1, max(16, n // 4))
-    head = 2 * x[:1] - torch.flip(x[1:pad + 1], dims=[0])
-    tail = 2 * x[-1:] - torch.flip(x[-pad - 1:-1], dims=[0])
-    ext = torch.cat([head, x, tail], dim=0)
-    m = ext.shape[0]
+    head = 2 * x[:, :1] - torch.flip(x[:, 1:pad + 1], dims=[1])
+    tail = 2 * x[:, -1:] - torch.flip(x[:, -pad - 1:-1], dims=[1])
+    ext = torch.cat([head, x, tail], dim=1).permute(0, 2, 1).contiguous()  # (G, 3, m)
+    m = ext.shape[2]
     f = torch.arange(m // 2 + 1, device=x.device, dtype=torch.float64) * (rate / m)
     lo, hi = 0.8 * cutoff, cutoff
     g = torch.ones_like(f)
     band = (f > lo) & (f <= hi)
     g = torch.where(band, 0.5 * (1 + torch.cos(np.pi * (f - lo) / (hi - lo))), g)
     g = torch.where(f > hi, torch.zeros_like(g), g)
-    y = torch.fft.irfft(torch.fft.rfft(ext, dim=0) * g[:, None], n=m, dim=0)
-    return y[pad:pad + n].contiguous()
+    y = torch.fft.irfft(torch.fft.rfft(ext, dim=2) * g, n=m, dim=2)
+    return y[:, :, pad:pad + n].permute(0, 2, 1)
+
+
+def lowpass_columns_dev(x: torch.Tensor, rate: float, cutoff: float) -> torch.Tensor:
+    return lowpass_batch(x[None], rate, cutoff)[0].contiguous()
+
+
+def decimate_batch(x: torch.Tensor, rate: float, factor: int) -> torch.Tensor:
+    """Coarse paths x[:, ::N] of x (G, T, 3), each low-passed first when its
+    measured bandwidth lies in (Nyquist_out, 2 Nyquist_out) -- decided and
+    applied on the device without a host round trip (the low-passed variant
+    is computed for every path and selected per path)."""
+    raw = x[:, ::factor]
+    if x.shape[1] < 2 or factor == 1:
+        return raw
+    nyq = 0.5 * rate / factor
+    bw = bandwidth_batch(x, rate)
+    use = ((bw > nyq) & (bw < 2.0 * nyq))[:, None, None]
+    lp = lowpass_batch(x, rate, 0.9 * nyq)[:, ::factor]
+    return torch.where(use, lp, raw)
 
 
 def decimate_dev(pos: torch.Tensor, rate: float, factor: int) -> torch.Tensor:
