@@ -169,11 +169,12 @@ def cpu_sample(name, target_s, nthreads):
     sc, o = _ORACLE_CACHE[name]
     S = len(o.images)
     n0 = sc.T // 2
-    w = 64
-    t = time.perf_counter()
-    o.render_window(n0, n0 + w, nthreads)
-    dt = max(time.perf_counter() - t, 1e-6)
-    w = int(max(64, min(sc.T // 2, w * target_s / dt)))
+    w = 256
+    for _ in range(2):  # calibrate the slice to ~target_s of CPU work
+        t = time.perf_counter()
+        o.render_window(n0, n0 + w, nthreads)
+        dt = max(time.perf_counter() - t, 1e-6)
+        w = int(max(256, min(sc.T // 2, w * min(target_s / dt, 64.0))))
     t = time.perf_counter()
     o.render_window(n0, n0 + w, nthreads)
     dt = time.perf_counter() - t

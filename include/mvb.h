@@ -124,15 +124,17 @@ typedef struct mvb_job {
     int32_t L, d0;            /* branch length (= delay shift) and D0           */
     int32_t n_chunks, nb;     /* image chunks; branches per record / stream     */
     double rate, c, d_min, kappa; /* kappa = rate / c                           */
-    int64_t rec_front;        /* fast path: zero rows before branch sample 0, so
-                                 row index rec_base - rec_front + (idx + rec_front)
-                                 is never negative                              */
+    int32_t img_stride;       /* fast path: images per sort segment in the
+                                 delay-sorted table (segment s of this job
+                                 starts at img_off + s * img_stride)            */
+    int32_t pad;
 } mvb_job;
 
 /* One CTA of the fast synthesis grid: samples [32U*tile, 32U*(tile+1)) of
- * `job`, images [img_begin, img_end) of its (delay-sorted) image slice. */
+ * `job`, images [img_begin, img_end) of the job's image table sorted by
+ * delay at the centre of sort segment `seg`. */
 typedef struct mvb_work {
-    int32_t job, tile, img_begin, img_end, chunk, pad0, pad1, pad2;
+    int32_t job, tile, img_begin, img_end, chunk, seg, pad1, pad2;
 } mvb_work;
 
 /* Fast-path interval record: the reference's upsampled track on coarse
@@ -170,22 +172,20 @@ int mvb_track_max(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jo
                   const double* d_ub, int32_t* d_scratch, double* d_dmax, void* stream);
 
 /* Fast-path interval records of the images d_sel, all of one decimation
- * factor N: d_coef[image.coef + k] for k < K, from the coarse distances and
- * h_fit, the factor's (9, 65) refit of its phase-table columns in
- * u = 2r/N - 1 (HOST pointer; passed to the kernel by value). */
+ * factor N: d_coef[image.coef + k] for k < K (K <= max_K), from the coarse
+ * distances and h_fit, the factor's (9, 65) refit of its phase-table
+ * columns in u = 2r/N - 1 (HOST pointer; passed to the kernel by value). */
 int mvb_track_coeffs(const mvb_image* d_images, const int32_t* d_sel, int64_t n_sel,
-                     const mvb_job* d_jobs, const double* d_coarse, const double* h_fit,
-                     mvb_coef32* d_coef, void* stream);
+                     int64_t max_K, const mvb_job* d_jobs, const double* d_coarse,
+                     const double* h_fit, mvb_coef32* d_coef, void* stream);
 
-/* Delay-sort key of every image: its distance at the middle of its job's
- * path (coarse sample for factor > 1). */
-int mvb_sort_keys(const mvb_image* d_images, int64_t n_img, const mvb_job* d_jobs,
+/* Delay-sort keys: d_key[(j * max_n_seg + s) * max_n_img + i] = distance of
+ * image i of job j at the centre of segment s (samples [s*seg_len,
+ * (s+1)*seg_len), clamped to the track), coarse sample for factor > 1.
+ * Entries beyond a job's images / segments are not written. */
+int mvb_sort_keys(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jobs,
+                  int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
                   const double* d_paths, const double* d_coarse, double* d_key, void* stream);
-
-/* Stable rank of each key inside its job's image slice (ties by index):
- * d_rank[img_off + i] = #{j in job : k_j < k_i or (k_j == k_i and j < i)}. */
-int mvb_rank(const double* d_key, const mvb_job* d_jobs, int64_t n_jobs, int64_t max_n_img,
-             int32_t* d_rank, void* stream);
 
 /* Fast path: fp32 branch records v'_k = x (*) c'_k (d_cbranch (M1, L) fp64
  * in the centred basis (mu - 1/2)^k, zero branches k >= M1) for input

@@ -210,7 +210,8 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     // the zero front pad of every signal's region
     const int rb = (int)Jp->rec_base;
     const float4* __restrict__ R = reinterpret_cast<const float4*>(rec);
-    const mvb_image* __restrict__ imgs = images + Jp->img_off;
+    // this tile's delay-sorted image table (sort segment wp->seg)
+    const mvb_image* __restrict__ imgs = images + Jp->img_off + (int64_t)wp->seg * Jp->img_stride;
     const float invk = (float)(1.0 / Jp->kappa);
     const float dmin = (float)Jp->d_min;
     float* __restrict__ row = red[warp];

@@ -11,7 +11,7 @@
 //   k_coeffs           fast-path interval records: the 65-tap Kaiser
 //                      upsampler refit per coarse interval as a degree-8
 //                      polynomial in u, anchored in fp64, pre-split (B, f)
-//   k_sort_keys/k_rank per-job delay sort (L1 locality of the gather)
+//   k_sort_keys        per-(job, time segment) delay-sort keys (L1 locality)
 #include <cfloat>
 
 #include "mvb_common.cuh"
@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
     const int64_t K = im.n_coarse;
     const double* c = coarse + im.coarse;
     const int e0 = COEF_KI * threadIdx.x;
-    for (int64_t k0 = 0; k0 < K; k0 += COEF_SPAN) {
+    // blockIdx.y-th span of 512 intervals (grid.y = max spans over images)
+    for (int64_t k0 = (int64_t)blockIdx.y * COEF_SPAN; k0 < K; k0 += (int64_t)gridDim.y * COEF_SPAN) {
         __syncthreads();
         for (int t = threadIdx.x; t < COEF_SPAN + 64; t += blockDim.x) {
             int64_t q = k0 - 32 + t;
@@ -247,45 +248,26 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
     }
 }
 
-__global__ void k_sort_keys(const mvb_image* __restrict__ images, int64_t n_img,
-                            const mvb_job* __restrict__ jobs, const double* __restrict__ paths,
-                            const double* __restrict__ coarse, double* __restrict__ key) {
+__global__ void k_sort_keys(const mvb_image* __restrict__ images, const mvb_job* __restrict__ jobs,
+                            int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
+                            const double* __restrict__ paths, const double* __restrict__ coarse,
+                            double* __restrict__ key) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n_img) return;
-    const mvb_image im = images[i];
-    const mvb_job& J = jobs[im.job];
-    const int64_t t = (J.T - 1) / 2;
+    const int64_t s = blockIdx.y, j = blockIdx.z;
+    const mvb_job& J = jobs[j];
+    if (i >= J.n_img || s * seg_len >= J.T) return;
+    const mvb_image im = images[J.img_off + i];
+    int64_t t = s * seg_len + seg_len / 2;
+    if (t > J.T - 1) t = J.T - 1;
+    double k;
     if (im.factor == 1) {
-        key[i] = image_distance(im, paths + 3 * (J.pos_off + t), mic_row(J, paths, t));
+        k = image_distance(im, paths + 3 * (J.pos_off + t), mic_row(J, paths, t));
     } else {
-        int64_t k = t / im.factor;
-        if (k >= im.n_coarse) k = im.n_coarse - 1;
-        key[i] = coarse[im.coarse + k];
+        int64_t c = t / im.factor;
+        if (c >= im.n_coarse) c = im.n_coarse - 1;
+        k = coarse[im.coarse + c];
     }
-}
-
-__global__ void k_rank(const double* __restrict__ key, const mvb_job* __restrict__ jobs,
-                       int32_t* __restrict__ rank) {
-    __shared__ double tile[256];
-    const mvb_job& J = jobs[blockIdx.y];
-    const int64_t n = J.n_img;
-    const double* kk = key + J.img_off;
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if ((int64_t)blockIdx.x * blockDim.x >= n) return;
-    const double mine = i < n ? kk[i] : 0.0;
-    int r = 0;
-    for (int64_t t0 = 0; t0 < n; t0 += 256) {
-        const int64_t t = t0 + threadIdx.x;
-        tile[threadIdx.x] = t < n ? kk[t] : DBL_MAX;
-        __syncthreads();
-        const int lim = n - t0 < 256 ? (int)(n - t0) : 256;
-        for (int q = 0; q < lim; ++q) {
-            const double v = tile[q];
-            r += (v < mine) || (v == mine && t0 + q < i);
-        }
-        __syncthreads();
-    }
-    if (i < n) rank[J.img_off + i] = r;
+    key[(j * max_n_seg + s) * max_n_img + i] = k;
 }
 
 }  // namespace mvb
@@ -336,36 +318,34 @@ int mvb_track_max(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
 }
 
 int mvb_track_coeffs(const mvb_image* images, const int32_t* sel, int64_t n_sel,
-                     const mvb_job* jobs, const double* coarse, const double* h_fit,
-                     mvb_coef32* coef, void* stream) {
+                     int64_t max_K, const mvb_job* jobs, const double* coarse,
+                     const double* h_fit, mvb_coef32* coef, void* stream) {
     if (n_sel < 0 || n_sel > 0x7fffffff) return fail(MVB_EINVAL, "track_coeffs: n_sel");
     if (n_sel == 0) return MVB_OK;
     if (!images || !sel || !jobs || !coarse || !h_fit || !coef)
         return fail(MVB_EINVAL, "track_coeffs: null");
+    if (max_K < 1) return fail(MVB_EINVAL, "track_coeffs: max_K");
     FitParam fp;
     for (int i = 0; i < 9 * 65; ++i) fp.v[i] = h_fit[i];
-    k_coeffs<<<(unsigned)n_sel, COEF_BLOCK, 0, as_stream(stream)>>>(fp, images, sel, jobs, coarse, coef);
+    int64_t spans = (max_K + COEF_SPAN - 1) / COEF_SPAN;
+    if (spans > 65535) spans = 65535;
+    k_coeffs<<<dim3((unsigned)n_sel, (unsigned)spans), COEF_BLOCK, 0, as_stream(stream)>>>(
+        fp, images, sel, jobs, coarse, coef);
     return check_launch("track_coeffs");
 }
 
-int mvb_sort_keys(const mvb_image* images, int64_t n_img, const mvb_job* jobs,
-                  const double* paths, const double* coarse, double* key, void* stream) {
-    if (n_img < 0) return fail(MVB_EINVAL, "sort_keys: n_img");
-    if (n_img == 0) return MVB_OK;
+int mvb_sort_keys(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs, int64_t max_n_img,
+                  int64_t max_n_seg, int64_t seg_len, const double* paths, const double* coarse,
+                  double* key, void* stream) {
+    if (n_jobs < 0 || n_jobs > 65535 || max_n_img < 0 || max_n_seg < 0 || max_n_seg > 65535 ||
+        seg_len < 1)
+        return fail(MVB_EINVAL, "sort_keys: sizes");
+    if (n_jobs == 0 || max_n_img == 0 || max_n_seg == 0) return MVB_OK;
     if (!images || !jobs || !paths || !key) return fail(MVB_EINVAL, "sort_keys: null");
-    k_sort_keys<<<grid_for(n_img, 256), 256, 0, as_stream(stream)>>>(images, n_img, jobs, paths,
-                                                                     coarse, key);
+    dim3 g(grid_for(max_n_img, 256), (unsigned)max_n_seg, (unsigned)n_jobs);
+    k_sort_keys<<<g, 256, 0, as_stream(stream)>>>(images, jobs, max_n_img, max_n_seg, seg_len, paths,
+                                                  coarse, key);
     return check_launch("sort_keys");
-}
-
-int mvb_rank(const double* key, const mvb_job* jobs, int64_t n_jobs, int64_t max_n_img,
-             int32_t* rank, void* stream) {
-    if (n_jobs < 0 || n_jobs > 65535 || max_n_img < 0) return fail(MVB_EINVAL, "rank: sizes");
-    if (n_jobs == 0 || max_n_img == 0) return MVB_OK;
-    if (!key || !jobs || !rank) return fail(MVB_EINVAL, "rank: null");
-    k_rank<<<dim3(grid_for(max_n_img, 256), (unsigned)n_jobs), 256, 0, as_stream(stream)>>>(key, jobs,
-                                                                                          rank);
-    return check_launch("rank");
 }
 
 }  // extern "C"

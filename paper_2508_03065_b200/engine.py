@@ -43,6 +43,7 @@ import os
 
 SYNTH_U = int(os.environ.get("MVB_SYNTH_U", "16"))  # 16 or 32 steps per lane
 TILE = 32 * SYNTH_U  # output samples per CTA
+SEG_LEN = 32 * TILE  # samples per delay-sort segment
 IMG_COLS, JOB_COLS, WORK_COLS = 12, 17, 4
 PAD_MARGIN = 64
 FOUR_PI = 4.0 * np.pi
@@ -105,7 +106,7 @@ def pack_jobs(rows: list) -> np.ndarray:
                      r["img_off"], r["n_img"], r["pos_off"], r["mic_off"]]
         i32[j] = [r["T"], r["mic_moving"], r["L"], r["d0"], r["n_chunks"], r["nb"]]
         f64[j] = [r["rate"], r["c"], r["d_min"], r["kappa"]]
-        a[j, 16] = r.get("rec_front", 0)
+        a[j, 16:17].view(np.int32)[:] = [r.get("img_stride", 0), 0]
     return a
 
 
@@ -557,20 +558,23 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
     coef = torch.empty(max(geom.n_coarse_total, 1) * 12, dtype=torch.float32, device=dev)
     for N, sel in geom.sel_by_factor.items():
         fit = np.ascontiguousarray(phase_fit(N), dtype=np.float64)
-        _lib.call("mvb_track_coeffs", ptr(geom.images), ptr(sel), sel.numel(), ptr(pre_dev),
+        max_K = -(-int(geom.T.max()) // N)
+        _lib.call("mvb_track_coeffs", ptr(geom.images), ptr(sel), sel.numel(), max_K, ptr(pre_dev),
                   ptr(geom.coarse), fit.ctypes.data_as(ctypes.c_void_p), ptr(coef), st)
         launches += 1
-    key = torch.empty(geom.n_images, dtype=torch.float64, device=dev)
-    _lib.call("mvb_sort_keys", ptr(geom.images), geom.n_images, ptr(pre_dev), ptr(geom.paths),
-              ptr(geom.coarse), ptr(key), st)
-    rank = torch.empty(geom.n_images, dtype=torch.int32, device=dev)
-    _lib.call("mvb_rank", ptr(key), ptr(pre_dev), nJ, int(geom.n_img.max()), ptr(rank), st)
-    launches += 2
-    job_of_img = geom.images[:, 11:12].view(torch.int32)[:, 0].to(torch.int64)
-    job_base = h2d(geom.img_off, dev)[job_of_img]
-    perm = torch.empty(geom.n_images, dtype=torch.int64, device=dev)
-    perm[job_base + rank.to(torch.int64)] = torch.arange(geom.n_images, device=dev)
-    images_sorted = geom.images[perm]
+    # delay sort per (job, time segment of SEG_LEN samples): keys by our
+    # kernel, one batched argsort (padding keys +inf sort last)
+    n_seg = [-(-int(geom.T[j]) // SEG_LEN) for j in range(nJ)]
+    max_seg, max_img = max(n_seg), int(geom.n_img.max())
+    key = torch.full((nJ, max_seg, max_img), float("inf"), dtype=torch.float64, device=dev)
+    _lib.call("mvb_sort_keys", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg, SEG_LEN,
+              ptr(geom.paths), ptr(geom.coarse), ptr(key), st)
+    launches += 1
+    order = torch.argsort(key, dim=2)  # (nJ, max_seg, max_img)
+    base = h2d(geom.img_off, dev)[:, None, None]
+    nimg_dev = h2d(geom.n_img, dev)[:, None, None]
+    gidx = base + torch.minimum(order, nimg_dev - 1)  # padded slots: any own image
+    images_sorted = geom.images[gidx.reshape(-1)]  # layout (job, segment, max_img)
     # 2. out_len, zero-padded branch records, work list, synthesis
     out_len, tau_ceil, offsets, rows = finish_rows()
     rec_rows, bases = 0, {}
@@ -590,7 +594,8 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
         launches += 1
     for j in range(nJ):
         r0, front = bases[keys[j]]
-        rows[j].update(rec_base=r0 + front, rec_front=front, nb=nb)
+        rows[j].update(rec_base=r0 + front, nb=nb, img_off=j * max_seg * max_img,
+                       img_stride=max_img)
     # image slices of this shard (in delay-sorted order)
     rank_, world = (0, 1) if shard is None else (int(shard[0]), int(shard[1]))
     lo = (geom.n_img * rank_) // world
@@ -613,6 +618,7 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
         blk[:, :, 2] = (int(lo[j]) + (span * cs) // nc)[:, None]
         blk[:, :, 3] = (int(lo[j]) + (span * (cs + 1)) // nc)[:, None]
         blk[:, :, 4] = cs[:, None]
+        blk[:, :, 5] = np.minimum(np.arange(tiles[j]) * TILE // SEG_LEN, n_seg[j] - 1)[None, :]
         blocks.append(blk.reshape(-1, 8))
     work = np.concatenate(blocks)
     jobs_dev = h2d(pack_jobs(rows), dev)

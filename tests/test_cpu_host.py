@@ -117,3 +117,25 @@ def test_track_fit_accuracy_against_oracle_upsampler():
         u = 2 * np.arange(N) / N - 1
         d = (g @ (u[None, :] ** np.arange(9)[:, None])).reshape(-1)[:sc.T]
         assert np.max(np.abs(d - ref)) < 2e-9
+
+
+def test_pack_jobs_matches_c_layout():
+    """engine.pack_jobs writes the exact byte layout of mvb_job (mvb.h)."""
+    from paper_2508_03065_b200.engine import pack_jobs
+
+    class Job(ctypes.Structure):
+        _fields_ = [(n, ctypes.c_int64) for n in
+                    ("out_off", "out_len", "part_off", "rec_base", "ls", "img_off", "n_img",
+                     "pos_off", "mic_off")] + \
+                   [(n, ctypes.c_int32) for n in ("T", "mic_moving", "L", "d0", "n_chunks", "nb")] + \
+                   [(n, ctypes.c_double) for n in ("rate", "c", "d_min", "kappa")] + \
+                   [("img_stride", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+    assert ctypes.sizeof(Job) == 136
+    row = dict(out_off=1, out_len=2, part_off=3, rec_base=4, ls=5, img_off=6, n_img=7, pos_off=8,
+               mic_off=9, T=10, mic_moving=1, L=64, d0=31, n_chunks=3, nb=8, rate=48000.0,
+               c=343.0, d_min=0.05, kappa=48000.0 / 343.0, img_stride=11521)
+    raw = pack_jobs([row]).tobytes()
+    j = Job.from_buffer_copy(raw)
+    for k, v in row.items():
+        assert getattr(j, k) == v, k
