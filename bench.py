@@ -118,16 +118,20 @@ class ClockSampler:
 
 def build_workload(name, rank, world):
     """Scenes, the jobs this rank renders, and the sharding mode."""
-    from paper_2508_03065_b200 import workloads
+    from paper_2508_03065_b200 import parallel, workloads
+    from paper_2508_03065_b200.room import image_count
     scenes = workloads.make_scenes(name)
-    w = workloads.WORKLOADS[name]
-    if world == 1:
+    mode = parallel.shard_mode(name, world)
+    if mode == "single":
         return scenes, scenes, None, "single"
-    if name in ("c3", "c5"):
+    if mode == "images":
         return scenes, scenes, (rank, world), f"image-shard x{world} + NCCL reduce"
-    if name == "c4":
-        mine = [sc for q, sc in enumerate(scenes) if q % world == rank]
-        return scenes, mine, None, f"scene-shard x{world} (no collective)"
+    if mode == "scenes":
+        # LPT by update count ~ images x (T + max delay of the room's reach)
+        cost = [image_count(sc.max_order) * len(sc.mics) *
+                (sc.T + sc.max_order * float(np.max(sc.dims)) * sc.rate / 343.0) for sc in scenes]
+        mine = [scenes[i] for i in parallel.lpt_assign(cost, world)[rank]]
+        return scenes, mine, None, f"scene-shard x{world} LPT (no collective)"
     return scenes, scenes, None, f"replicas x{world}"
 
 
@@ -227,8 +231,8 @@ def load_traffic(name):
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    from paper_2508_03065_b200 import (Room, SynthesisConfig, Trajectory, hann_sinc, render,
-                                       workloads)
+    from paper_2508_03065_b200 import (Room, SynthesisConfig, Trajectory, hann_sinc, parallel,
+                                       render, workloads)
     from paper_2508_03065_b200.synth import render_jobs
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -249,12 +253,13 @@ def run_ours(args):
     f = hann_sinc(w.fd_taps, 14)
     jobs = device_jobs(mine, dev)
     timing = []
+    precision = "fp64" if w.dtype == "f64" else "fp32"  # c1 is an fp64 config
 
     def step(record=False):
         tl = timing if record else None
-        res = render_jobs(jobs, f, precision="fp32", shard=shard, timing=tl)
+        res = render_jobs(jobs, f, precision=precision, shard=shard, timing=tl)
         if shard is not None:
-            dist.reduce(res.out, dst=0, op=dist.ReduceOp.SUM)
+            parallel.reduce_to_root(res.out)
         return res
 
     if not args.profile:
@@ -296,9 +301,9 @@ def run_ours(args):
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         tsum = t.clone()
         dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        # every rank's updates count: image shards and scene shards split the
+        # work, replicas each do all of it (value = N x one replica)
         total_ms_all, updates_all = float(tmax[0]), float(tsum[1])
-        if name in ("c1", "c2"):
-            updates_all = float(tsum[1])  # replicas: every rank's work counts
     else:
         total_ms_all, updates_all = total_ms, float(updates)
     value = updates_all / (total_ms_all * 1e-3)
@@ -316,8 +321,8 @@ def run_ours(args):
             room = Room(dims=sc.dims, wall_reflection=sc.walls)
             traj = Trajectory(rate=sc.rate, positions=sc.pos)
             cfg = SynthesisConfig(audio_rate=sc.rate, max_order=sc.max_order, tiers=sc.tiers,
-                                  precision="fp32")
-            s32 = np.ascontiguousarray(sc.s, dtype=np.float32)
+                                  precision=precision)
+            s32 = np.ascontiguousarray(sc.s)
             y = render(s32, traj, room, sc.mics[0], f, cfg)  # warm
             tt = 0.0
             for _ in range(args.steps):
@@ -343,9 +348,9 @@ def run_ours(args):
                 torch.cuda.synchronize()
                 barrier()
                 t0 = time.perf_counter()
-                r = render_jobs(host_jobs, f, precision="fp32", shard=shard)
+                r = render_jobs(host_jobs, f, precision=precision, shard=shard)
                 if shard is not None:
-                    dist.reduce(r.out, dst=0, op=dist.ReduceOp.SUM)
+                    parallel.reduce_to_root(r.out)
                 out_h = r.out.cpu() if (shard is None or rank == 0) else None
                 torch.cuda.synchronize()
                 barrier()
@@ -411,7 +416,7 @@ def run_ours(args):
             "higher_is_better": True,
             "scaling": "strong" if (world > 1 and name in ("c3", "c5")) else "weak",
             "vs_baseline": None,
-            "dtype": "f32 (fp64 delay anchors)",
+            "dtype": "f64" if precision == "fp64" else "f32 (fp64 delay anchors)",
             "data": "synthetic (seeded white Gaussian dry signal, seeded paths; SURVEY 8d)",
             "config": {
                 "workload": name,

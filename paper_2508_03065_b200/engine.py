@@ -36,6 +36,7 @@ import torch
 from . import _lib
 from ._dev import ptr, require_cuda, stream_handle
 from .farrow import as_filter, centered_branches
+from .parallel import image_slice
 from .room import image_count, image_table
 from .trajectory import decimate_batch, device_constants, negative_mass, phase_fit
 
@@ -598,8 +599,9 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
                        img_stride=max_img)
     # image slices of this shard (in delay-sorted order)
     rank_, world = (0, 1) if shard is None else (int(shard[0]), int(shard[1]))
-    lo = (geom.n_img * rank_) // world
-    hi = (geom.n_img * (rank_ + 1)) // world
+    sl = [image_slice(int(n), rank_, world) for n in geom.n_img]
+    lo = np.array([a for a, _ in sl], dtype=np.int64)
+    hi = np.array([b for _, b in sl], dtype=np.int64)
     tiles = [-(-int(out_len[j]) // TILE) for j in range(nJ)]
     chunks = _chunking([int(hi[j] - lo[j]) for j in range(nJ)], tiles, sm_count)
     part_rows = 0
