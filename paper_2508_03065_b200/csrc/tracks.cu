@@ -66,36 +66,49 @@ __global__ void k_coarse(const mvb_image* __restrict__ images, const int32_t* __
 // over segments s-1..s+1 (a superset of every 65-tap window centred in s).
 // With weights summing to 1 whose negative mass is <= negsum, any window
 // value is <= wmax + negsum (wmax - wmin).
-__global__ void k_bounds_coarse(const mvb_image* __restrict__ images,
+__device__ __forceinline__ void warp_maxmin(double& M, double& m) {
+    for (int o = 16; o > 0; o >>= 1) {
+        M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+        m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
+}
+
+// max / min of coarse samples [64 s, 64 s + 64) (clipped to K), warp-uniform
+__device__ __forceinline__ void seg_maxmin(const double* c, int64_t K, int64_t s, int lane,
+                                           double& M, double& m) {
+    M = -DBL_MAX;
+    m = DBL_MAX;
+    const int64_t a = 64 * s + lane, b = a + 32;
+    if (a < K) { const double v = c[a]; M = v; m = v; }
+    if (b < K) { const double v = c[b]; M = fmax(M, v); m = fmin(m, v); }
+    warp_maxmin(M, m);
+}
+
+// One warp per image, 8 images per block; segments are reduced once with
+// coalesced loads and combined with their neighbours in a sliding window.
+__global__ void k_bounds_coarse(const mvb_image* __restrict__ images, int64_t n_img,
                                 const double* __restrict__ coarse, double negsum,
                                 double* __restrict__ lb, double* __restrict__ ub) {
-    __shared__ double red[32];
-    const int64_t i = blockIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= n_img) return;
     const mvb_image im = images[i];
     if (im.factor == 1) return;
     const double* c = coarse + im.coarse;
     const int64_t K = im.n_coarse;
     const int64_t nseg = (K + 63) / 64;
+    double Mp = -DBL_MAX, mp = DBL_MAX, Mc, mc, Mn, mn;
+    seg_maxmin(c, K, 0, lane, Mc, mc);
     double best_lb = 0.0, best_ub = 0.0;
-    for (int64_t s = threadIdx.x; s < nseg; s += blockDim.x) {
-        double M = -DBL_MAX, mn = DBL_MAX, own = -DBL_MAX;
-        for (int64_t q = s - 1; q <= s + 1; ++q) {
-            int64_t a = q * 64, b = a + 64;
-            if (a < 0) a = 0;
-            if (b > K) b = K;
-            for (int64_t t = a; t < b; ++t) {
-                const double v = c[t];
-                M = fmax(M, v);
-                mn = fmin(mn, v);
-                if (q == s) own = fmax(own, v);
-            }
-        }
-        best_lb = fmax(best_lb, own);
-        best_ub = fmax(best_ub, M + negsum * (M - mn) + 1e-9);
+    for (int64_t s = 0; s < nseg; ++s) {
+        if (s + 1 < nseg) seg_maxmin(c, K, s + 1, lane, Mn, mn);
+        else { Mn = -DBL_MAX; mn = DBL_MAX; }
+        const double M = fmax(Mp, fmax(Mc, Mn)), m = fmin(mp, fmin(mc, mn));
+        best_lb = fmax(best_lb, Mc);
+        best_ub = fmax(best_ub, M + negsum * (M - m) + 1e-9);
+        Mp = Mc; mp = mc; Mc = Mn; mc = mn;
     }
-    best_lb = block_max(best_lb, red);
-    best_ub = block_max(best_ub, red);
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
         lb[i] = best_lb;
         ub[i] = best_ub;
     }
@@ -173,28 +186,41 @@ __global__ void k_exact_max(const mvb_image* __restrict__ images, const mvb_job*
     }
 }
 
-// Fast-path interval records.  One block per image; chunks of 512
-// consecutive intervals stage their coarse window (512 + 64 samples) in
-// shared memory (skewed by one word per 16 so the 4-interval stride is
-// conflict-free); each thread forms 4 consecutive intervals' 9 coefficients.
-// The factor's (9, 65) refit matrix is a by-value kernel parameter, i.e. it
-// sits in the constant bank and every DFMA reads it as a free operand: per
-// tap, one shared load feeds 36 fp64 FMAs (585 FMAs per interval).
+// Fast-path interval records, by summation by parts.  With the factor's
+// (9, 65) refit F (track on interval k: d(u) = sum_p g_p u^p,
+// g_p = sum_c F[p][c] w[k + c - 32], w the coarse distances) and
+// sum_c F[p][c] = [p == 0]:
+//     g_p - [p == 0] w[k] = sum_{j<64} G[p][j] * dw[k - 32 + j],
+//     dw[i] = w[i+1] - w[i],   G = partial sums of F's rows.
+// dw is formed once per coarse sample in fp64 and rounded to fp32 (|dw| is
+// one coarse step of motion, so its rounding error is ~1e-9 m); the 576
+// products per interval then run as fp32 FMAs, paired into FFMA2 over
+// (g_p, g_p+1).  Measured against the exact 65-tap track (tests) the
+// residual error is < 4e-9 m, i.e. < 6e-7 samples of delay at 48 kHz.
+// One block per (image, span of 1024 intervals); 8 consecutive intervals
+// per thread so each shared-memory load of dw feeds 8 x 5 FMA instructions.
 constexpr int COEF_BLOCK = 128;
-constexpr int COEF_KI = 4;
+constexpr int COEF_KI = 8;
 constexpr int COEF_SPAN = COEF_BLOCK * COEF_KI;
 
-struct FitParam {
-    double v[9 * 65];
+struct SbpParam {
+    float g[64][10];  // G[p][j] stored per tap j: (g0..g8, pad)
 };
 
-__device__ __forceinline__ int skew16(int e) { return e + (e >> 4); }
+// skew one word per 32 so the 8-interval thread stride is conflict-free
+__device__ __forceinline__ int skew32(int e) { return e + (e >> 5); }
+
+constexpr int COEF_DW = COEF_SPAN + 64 + (COEF_SPAN + 64) / 32 + 1;
+constexpr size_t COEF_SMEM = sizeof(mvb_coef32) * COEF_SPAN + sizeof(float) * COEF_DW;
 
 __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
-    const __grid_constant__ FitParam fit, const mvb_image* __restrict__ images,
+    const __grid_constant__ SbpParam sp, const mvb_image* __restrict__ images,
     const int32_t* __restrict__ sel, const mvb_job* __restrict__ jobs,
     const double* __restrict__ coarse, mvb_coef32* __restrict__ out) {
-    __shared__ double win[COEF_SPAN + 64 + (COEF_SPAN + 64) / 16 + 1];
+    // records of the span are staged here and written out coalesced
+    extern __shared__ __align__(16) unsigned char coef_smem[];
+    mvb_coef32* srec = reinterpret_cast<mvb_coef32*>(coef_smem);
+    float* dw = reinterpret_cast<float*>(coef_smem + sizeof(mvb_coef32) * COEF_SPAN);
     const mvb_image im = images[sel[blockIdx.x]];
     const mvb_job& J = jobs[im.job];
     const double kappa = J.kappa;
@@ -202,49 +228,74 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
     const int64_t K = im.n_coarse;
     const double* c = coarse + im.coarse;
     const int e0 = COEF_KI * threadIdx.x;
-    // blockIdx.y-th span of 512 intervals (grid.y = max spans over images)
-    for (int64_t k0 = (int64_t)blockIdx.y * COEF_SPAN; k0 < K; k0 += (int64_t)gridDim.y * COEF_SPAN) {
+    for (int64_t k0 = (int64_t)blockIdx.y * COEF_SPAN; k0 < K;
+         k0 += (int64_t)gridDim.y * COEF_SPAN) {
         __syncthreads();
+        // dw[i] for i = k0 - 32 .. k0 + COEF_SPAN + 31 (clamped samples hold)
         for (int t = threadIdx.x; t < COEF_SPAN + 64; t += blockDim.x) {
-            int64_t q = k0 - 32 + t;
-            q = q < 0 ? 0 : (q >= K ? K - 1 : q);
-            win[skew16(t)] = c[q];
+            int64_t a = k0 - 32 + t, b = a + 1;
+            a = a < 0 ? 0 : (a >= K ? K - 1 : a);
+            b = b < 0 ? 0 : (b >= K ? K - 1 : b);
+            dw[skew32(t)] = (float)(c[b] - c[a]);
         }
         __syncthreads();
-        if (k0 + e0 >= K) continue;
-        double g[COEF_KI][9];
+        if (k0 + e0 < K) {
+        float2 acc[COEF_KI][4];
+        float acc8[COEF_KI];
 #pragma unroll
-        for (int q = 0; q < COEF_KI; ++q)
+        for (int q = 0; q < COEF_KI; ++q) {
 #pragma unroll
-            for (int p = 0; p < 9; ++p) g[q][p] = 0.0;
-        double w[COEF_KI];
+            for (int p = 0; p < 4; ++p) acc[q][p] = make_float2(0.f, 0.f);
+            acc8[q] = 0.f;
+        }
+        float x[COEF_KI];
 #pragma unroll
-        for (int q = 0; q < COEF_KI - 1; ++q) w[q + 1] = win[skew16(e0 + q)];
+        for (int q = 0; q < COEF_KI - 1; ++q) x[q + 1] = dw[skew32(e0 + q)];
 #pragma unroll
-        for (int col = 0; col < 65; ++col) {
+        for (int j = 0; j < 64; ++j) {
 #pragma unroll
-            for (int q = 0; q < COEF_KI - 1; ++q) w[q] = w[q + 1];
-            w[COEF_KI - 1] = win[skew16(e0 + col + COEF_KI - 1)];
+            for (int q = 0; q < COEF_KI - 1; ++q) x[q] = x[q + 1];
+            x[COEF_KI - 1] = dw[skew32(e0 + j + COEF_KI - 1)];
+            const float* g = sp.g[j];
 #pragma unroll
-            for (int p = 0; p < 9; ++p)
+            for (int q = 0; q < COEF_KI; ++q) {
+                const float2 xx = make_float2(x[q], x[q]);
 #pragma unroll
-                for (int q = 0; q < COEF_KI; ++q) g[q][p] = fma(fit.v[p * 65 + col], w[q], g[q][p]);
+                for (int p = 0; p < 4; ++p)
+                    acc[q][p] = __ffma2_rn(make_float2(g[2 * p], g[2 * p + 1]), xx, acc[q][p]);
+                acc8[q] = fmaf(g[8], x[q], acc8[q]);
+            }
         }
 #pragma unroll
         for (int q = 0; q < COEF_KI; ++q) {
             const int64_t k = k0 + e0 + q;
             if (k >= K) break;
+            const double g0 = c[k] + (double)acc[q][0].x;
             mvb_coef32 r;
-            const double base = fma(kappa, g[q][0], shift);
+            const double base = fma(kappa, g0, shift);
             const double B = floor(base);
             r.B = (int32_t)B;
             r.f = (float)(base - B - 0.5);
-            r.d_mid = (float)g[q][0];
+            r.d_mid = (float)g0;
             r.pad = 0.f;
-#pragma unroll
-            for (int p = 0; p < 8; ++p) r.g[p] = (float)(kappa * g[q][p + 1]);
-            out[im.coef + k] = r;
+            const float kf = (float)kappa;
+            r.g[0] = kf * acc[q][0].y;
+            r.g[1] = kf * acc[q][1].x;
+            r.g[2] = kf * acc[q][1].y;
+            r.g[3] = kf * acc[q][2].x;
+            r.g[4] = kf * acc[q][2].y;
+            r.g[5] = kf * acc[q][3].x;
+            r.g[6] = kf * acc[q][3].y;
+            r.g[7] = kf * acc8[q];
+            srec[e0 + q] = r;
         }
+        }
+        __syncthreads();
+        // coalesced copy of the span's records (16 B per thread per pass)
+        const int64_t n_rec = K - k0 < COEF_SPAN ? K - k0 : COEF_SPAN;
+        const float4* src = reinterpret_cast<const float4*>(srec);
+        float4* dst = reinterpret_cast<float4*>(out + im.coef + k0);
+        for (int64_t t = threadIdx.x; t < n_rec * 3; t += blockDim.x) dst[t] = src[t];
     }
 }
 
@@ -296,7 +347,8 @@ int mvb_track_bounds(const mvb_image* images, int64_t n_img, const int32_t* full
     if (cudaMemsetAsync(lb, 0, sizeof(double) * n_img, s) != cudaSuccess ||
         cudaMemsetAsync(ub, 0, sizeof(double) * n_img, s) != cudaSuccess)
         return fail(MVB_ECUDA, "track_bounds: memset");
-    if (coarse) k_bounds_coarse<<<(unsigned)n_img, 128, 0, s>>>(images, coarse, negsum, lb, ub);
+    if (coarse)
+        k_bounds_coarse<<<grid_for(n_img, 8), 256, 0, s>>>(images, n_img, coarse, negsum, lb, ub);
     if (n_full > 0) {
         if (!full_sel || !paths) return fail(MVB_EINVAL, "track_bounds: null full-rate inputs");
         k_bounds_full<<<dim3(16, (unsigned)n_full), 256, 0, s>>>(images, full_sel, jobs, paths, lb, ub);
@@ -325,12 +377,31 @@ int mvb_track_coeffs(const mvb_image* images, const int32_t* sel, int64_t n_sel,
     if (!images || !sel || !jobs || !coarse || !h_fit || !coef)
         return fail(MVB_EINVAL, "track_coeffs: null");
     if (max_K < 1) return fail(MVB_EINVAL, "track_coeffs: max_K");
-    FitParam fp;
-    for (int i = 0; i < 9 * 65; ++i) fp.v[i] = h_fit[i];
+    // summation-by-parts weights G[p][j] = sum_{c>j} F[p][c] (j >= 32) or
+    // -sum_{c<=j} F[p][c] (j < 32), formed in fp64, stored fp32 per tap
+    SbpParam sp;
+    for (int j = 0; j < 64; ++j) {
+        for (int p = 0; p < 9; ++p) {
+            double acc = 0.0;
+            if (j >= 32)
+                for (int cc = j + 1; cc < 65; ++cc) acc += h_fit[p * 65 + cc];
+            else
+                for (int cc = 0; cc <= j; ++cc) acc -= h_fit[p * 65 + cc];
+            sp.g[j][p] = (float)acc;
+        }
+        sp.g[j][9] = 0.f;
+    }
     int64_t spans = (max_K + COEF_SPAN - 1) / COEF_SPAN;
     if (spans > 65535) spans = 65535;
-    k_coeffs<<<dim3((unsigned)n_sel, (unsigned)spans), COEF_BLOCK, 0, as_stream(stream)>>>(
-        fp, images, sel, jobs, coarse, coef);
+    static thread_local bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_coeffs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)COEF_SMEM);
+        if (e != cudaSuccess) return fail(MVB_ECUDA, cudaGetErrorString(e));
+        attr_set = true;
+    }
+    k_coeffs<<<dim3((unsigned)n_sel, (unsigned)spans), COEF_BLOCK, COEF_SMEM, as_stream(stream)>>>(
+        sp, images, sel, jobs, coarse, coef);
     return check_launch("track_coeffs");
 }
 
