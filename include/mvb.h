@@ -198,7 +198,7 @@ int mvb_branch_records_f32(const float* d_x, int64_t T, const double* d_cbranch,
                            int L, int nb, int64_t row0, float* d_rec, void* stream);
 
 /* Fast synthesis (fp32 I/O, fp64 anchors), one CTA per work item covering
- * 32*u_steps output samples (u_steps 16 or 32); jobs with n_chunks > 1 write
+ * 32*u_steps output samples (u_steps = 16); jobs with n_chunks > 1 write
  * d_part[part_off + chunk*out_len + n].  Gather rows are rec_base + n + L - D
  * (global, never negative: front zero pad). */
 int mvb_synthesize_f32(const mvb_job* d_jobs, const mvb_work* d_work, int64_t n_work,

@@ -162,26 +162,26 @@ __device__ __forceinline__ float dec_step(const float4& c0, const float4& c1, co
     return A * gather_horner<NP>(R, row, mc);
 }
 
-// Decimated image on a tile wholly inside [0, T) with TILE % NT == 0: the
+// Decimated image on a tile wholly inside [0, T) with TILE % NT == 0 (its
+// records staged in shared memory by the warp's cp.async pipeline): the
 // tile starts on an interval boundary, interval q covers steps
 // [q*SPI, (q+1)*SPI) and u = 2r/N - 1 is a per-step constant plus a lane
 // term -- no per-step bookkeeping, straight-line steps.
 template <int U, int NP, int NT>
-__device__ __forceinline__ void dec_static(float (&acc)[U], const float4* __restrict__ cf4,
-                                           const float4* __restrict__ R, int n0, int lane,
-                                           int nl, float an, float invk, float dmin) {
+__device__ __forceinline__ void dec_static(float (&acc)[U], const float4* __restrict__ cs,
+                                           const float4* __restrict__ R, int lane, int nl,
+                                           float an, float invk, float dmin) {
     constexpr int SPI = NT / 32;  // steps per coarse interval
-    const unsigned k0 = (unsigned)(n0 / NT);
     const float lt = (float)lane * (2.0f / NT);
     float4 c0, c1, c2;
     int nlB = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        if (u % SPI == 0) {
-            const float4* c = cf4 + 3u * (k0 + (unsigned)(u / SPI));
-            c0 = __ldg(c);
-            c1 = __ldg(c + 1);
-            c2 = __ldg(c + 2);
+        if (u % SPI == 0) {  // interval records staged in shared memory
+            const float4* c = cs + 3 * (u / SPI);
+            c0 = c[0];
+            c1 = c[1];
+            c2 = c[2];
             nlB = nl - __float_as_int(c0.x);
         }
         const float uu = lt + ((float)((u % SPI) * 32) * (2.0f / NT) - 1.0f);
@@ -191,6 +191,58 @@ __device__ __forceinline__ void dec_static(float (&acc)[U], const float4* __rest
 
 constexpr int SYNTH_WARPS = 8;
 
+// 16-byte asynchronous global -> shared copy (LDGSTS), L2-only caching
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Per-warp staging area: image structs for the current, next and next-next
+// image of the warp, and the interval records of the current and next image
+// over this tile (only for factors N >= 32, at most TN/32 + 1 records).
+template <int U>
+struct alignas(16) WarpStage {
+    static constexpr int RMAX = U + 1;
+    mvb_image img[3];
+    mvb_coef32 rec[2][RMAX];
+    int k0[2];
+    int cnt[2];
+};
+
+// issue the copies of image q's interval records over [n0, n0+TN) into slot
+// `dst` (lane-parallel 16-byte chunks); the records exist only for factor >= 32
+template <int U>
+__device__ __forceinline__ void stage_records(WarpStage<U>& st, int slot, const mvb_image& q,
+                                              const mvb_coef32* __restrict__ coef, int n0, int T,
+                                              int lane) {
+    constexpr int TN = 32 * U;
+    const int N = q.factor;
+    int cnt = 0, k0 = 0;
+    if (N >= 32) {
+        k0 = n0 / N;
+        const int last = (n0 + TN - 1 < T - 1 ? n0 + TN - 1 : T - 1) / N;
+        cnt = last - k0 + 1;
+        if (cnt > WarpStage<U>::RMAX) cnt = 0;  // cannot happen for N >= 32
+        const char* src = reinterpret_cast<const char*>(coef + q.coef + k0);
+        char* dst = reinterpret_cast<char*>(st.rec[slot]);
+        for (int c = lane; c < 3 * cnt; c += 32) cp_async16(dst + 16 * c, src + 16 * c);
+    }
+    if (lane == 0) {
+        st.k0[slot] = k0;
+        st.cnt[slot] = cnt;
+    }
+}
+
+template <int U>
+__device__ __forceinline__ void stage_image(WarpStage<U>& st, int slot, const mvb_image* src,
+                                            int lane) {
+    if (lane < (int)(sizeof(mvb_image) / 16))
+        cp_async16(reinterpret_cast<char*>(&st.img[slot]) + 16 * lane,
+                   reinterpret_cast<const char*>(src) + 16 * lane);
+}
+
 template <int U, int NP, int MINB>
 __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     const mvb_job* __restrict__ jobs, const mvb_work* __restrict__ work,
@@ -199,6 +251,7 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     float* __restrict__ part) {
     constexpr int TN = 32 * U;
     __shared__ float red[SYNTH_WARPS][TN];
+    __shared__ WarpStage<U> stage[SYNTH_WARPS];
     const mvb_work* wp = work + blockIdx.x;
     const int img_begin = wp->img_begin, img_end = wp->img_end;
     const mvb_job* Jp = jobs + wp->job;
@@ -215,6 +268,7 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     const float invk = (float)(1.0 / Jp->kappa);
     const float dmin = (float)Jp->d_min;
     float* __restrict__ row = red[warp];
+    WarpStage<U>& st = stage[warp];
 #pragma unroll
     for (int u = 0; u < U; ++u) row[32 * u + lane] = 0.f;
     float acc[U];
@@ -222,17 +276,40 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     for (int u = 0; u < U; ++u) acc[u] = 0.f;
     const bool inside = n0 + TN <= T;  // no hold-extension inside this tile
 
-    for (int i = img_begin + warp; i < img_end; i += SYNTH_WARPS) {
-        const mvb_image* ip = imgs + i;
-        const int N = ip->factor;
-        const float an = ip->amp_num;
+    // prologue of the staging pipeline: structs of the first two images, then
+    // the first image's records
+    const int i0 = img_begin + warp;
+    if (i0 < img_end) stage_image(st, 0, imgs + i0, lane);
+    if (i0 + SYNTH_WARPS < img_end) stage_image(st, 1, imgs + i0 + SYNTH_WARPS, lane);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+    if (i0 < img_end) stage_records(st, 0, st.img[0], coef, n0, T, lane);
+    cp_async_commit();
+
+    int t = 0;
+    for (int i = i0; i < img_end; i += SYNTH_WARPS, ++t) {
+        const int cur = t % 3, rcur = t & 1;
+        // everything issued one image ago has landed: records(i), struct(i+8)
+        cp_async_wait_all();
+        __syncwarp();
+        // stream the next image's records and the struct after it while
+        // this image is processed
+        if (i + SYNTH_WARPS < img_end)
+            stage_records(st, rcur ^ 1, st.img[(t + 1) % 3], coef, n0, T, lane);
+        if (i + 2 * SYNTH_WARPS < img_end) stage_image(st, (t + 2) % 3, imgs + i + 2 * SYNTH_WARPS, lane);
+        cp_async_commit();
+
+        const mvb_image& im = st.img[cur];
+        const int N = im.factor;
+        const float an = im.amp_num;
         if (N == 1) {
             // near images (full-rate tier): exact fp64 distance per sample,
             // accumulated in the warp's own shared-memory row
             const double kappa = Jp->kappa;
             const double sL = (double)(Lsh - Jp->d0);
-            const double ox = ip->off[0], oy = ip->off[1], oz = ip->off[2];
-            const double sx = ip->sign[0], sy = ip->sign[1], sz = ip->sign[2];
+            const double ox = im.off[0], oy = im.off[1], oz = im.off[2];
+            const double sx = im.sign[0], sy = im.sign[1], sz = im.sign[2];
             const double* P = paths + 3 * Jp->pos_off;
             const int moving = Jp->mic_moving;
             const double* Q = paths + 3 * Jp->mic_off;
@@ -255,41 +332,20 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
             }
             continue;
         }
-        const float4* __restrict__ cf4 = reinterpret_cast<const float4*>(coef + ip->coef);
         const int nl = rb + n0 + lane + Lsh + MAGIC_I;
+        const float4* __restrict__ cs = reinterpret_cast<const float4*>(st.rec[rcur]);
         if (inside && (N == 32 || N == 64 || N == 128 || N == 256)) {
+            // staged records: slot j = interval n0/N + j
             switch (N) {
-                case 32: dec_static<U, NP, 32>(acc, cf4, R, n0, lane, nl, an, invk, dmin); break;
-                case 64: dec_static<U, NP, 64>(acc, cf4, R, n0, lane, nl, an, invk, dmin); break;
-                case 128: dec_static<U, NP, 128>(acc, cf4, R, n0, lane, nl, an, invk, dmin); break;
-                default: dec_static<U, NP, 256>(acc, cf4, R, n0, lane, nl, an, invk, dmin); break;
-            }
-        } else if (inside && (N & 31) == 0) {
-            // ---- warp-uniform intervals, predicated reloads ----
-            const float twoInvN = 2.0f / (float)N;
-            unsigned k = (unsigned)(n0 / N);
-            int r0 = n0 - (int)k * N;  // multiple of 32
-            float4 c0 = __ldg(cf4 + 3u * k), c1 = __ldg(cf4 + 3u * k + 1), c2 = __ldg(cf4 + 3u * k + 2);
-            const float lanef = (float)lane;
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (u > 0) {
-                    r0 += 32;
-                    const bool w = r0 == N;
-                    r0 = w ? 0 : r0;
-                    k += w;
-                    const float4* c = cf4 + 3u * k;
-                    ldg4_if(c0, c, w);
-                    ldg4_if(c1, c + 1, w);
-                    ldg4_if(c2, c + 2, w);
-                }
-                const float uu = fmaf((float)r0 + lanef, twoInvN, -1.f);
-                acc[u] += dec_step<NP>(c0, c1, c2, uu, nl - __float_as_int(c0.x) + 32 * u, R, an,
-                                       invk, dmin);
+                case 32: dec_static<U, NP, 32>(acc, cs, R, lane, nl, an, invk, dmin); break;
+                case 64: dec_static<U, NP, 64>(acc, cs, R, lane, nl, an, invk, dmin); break;
+                case 128: dec_static<U, NP, 128>(acc, cs, R, lane, nl, an, invk, dmin); break;
+                default: dec_static<U, NP, 256>(acc, cs, R, lane, nl, an, invk, dmin); break;
             }
         } else {
-            // ---- generic: per-lane intervals (N % 32 != 0, or the tile
-            // reaches the hold-extended tail n >= T) ----
+            // ---- generic: per-lane intervals (other factors, or the tile
+            // reaches the hold-extended tail n >= T); records from global ----
+            const float4* __restrict__ cf4 = reinterpret_cast<const float4*>(coef + im.coef);
             const float twoInvN = 2.0f / (float)N;
             const int mfirst = n0 + lane < T ? n0 + lane : T - 1;
             int k = mfirst / N;
@@ -320,17 +376,20 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
             }
         }
     }
+    cp_async_wait_all();
 #pragma unroll
     for (int u = 0; u < U; ++u) row[32 * u + lane] += acc[u];
     __syncthreads();
     const int64_t out_len = Jp->out_len;
     const int n_chunks = Jp->n_chunks;
     float* dst = n_chunks == 1 ? out + Jp->out_off : part + Jp->part_off + (int64_t)wp->chunk * out_len;
-    for (int t = threadIdx.x; t < TN; t += blockDim.x) {
-        float s = red[0][t];
 #pragma unroll
-        for (int q = 1; q < SYNTH_WARPS; ++q) s += red[q][t];
-        const int64_t n = (int64_t)n0 + t;
+    for (int q = 0; q < TN / (SYNTH_WARPS * 32); ++q) {
+        const int t2 = q * SYNTH_WARPS * 32 + threadIdx.x;
+        float s = red[0][t2];
+#pragma unroll
+        for (int w = 1; w < SYNTH_WARPS; ++w) s += red[w][t2];
+        const int64_t n = (int64_t)n0 + t2;
         if (n < out_len) dst[n] = s;
     }
 }
@@ -441,11 +500,11 @@ int mvb_synthesize_f32(const mvb_job* jobs, const mvb_work* work, int64_t n_work
     if (n_work == 0) return MVB_OK;
     if (!jobs || !work || !images || !rec || !paths || !out)
         return fail(MVB_EINVAL, "synthesize_f32: null");
-    if (u_steps != 16 && u_steps != 32) return fail(MVB_EINVAL, "synthesize_f32: u_steps 16 or 32");
+    if (u_steps != 16) return fail(MVB_EINVAL, "synthesize_f32: u_steps must be 16");
     cudaStream_t s = as_stream(stream);
     const unsigned g = (unsigned)n_work;
     const int block = SYNTH_WARPS * 32;
-    // U = 32 (1024-sample tiles, 2 CTAs/SM) or U = 16 (512-sample tiles, 3 CTAs/SM)
+    // U = 16: 512-sample tiles, 3 CTAs/SM
 #define MVB_SYNTH(U, NP, MB) k_synth_f32<U, NP, MB><<<g, block, 0, s>>>( \
         jobs, work, images, coef, rec, paths, out, part)
 #define MVB_SYNTH_NB(U, MB)                         \
@@ -456,11 +515,7 @@ int mvb_synthesize_f32(const mvb_job* jobs, const mvb_work* work, int64_t n_work
         case 16: MVB_SYNTH(U, 4, MB); break;        \
         default: return fail(MVB_EINVAL, "synthesize_f32: nb must be 4, 8, 12 or 16"); \
     }
-    if (u_steps == 32) {
-        MVB_SYNTH_NB(32, 2)
-    } else {
-        MVB_SYNTH_NB(16, 3)
-    }
+    MVB_SYNTH_NB(16, 3)
 #undef MVB_SYNTH_NB
 #undef MVB_SYNTH
     return check_launch("synthesize_f32");

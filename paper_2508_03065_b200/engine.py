@@ -42,7 +42,7 @@ from .trajectory import decimate_batch, device_constants, negative_mass, phase_f
 
 import os
 
-SYNTH_U = int(os.environ.get("MVB_SYNTH_U", "16"))  # 16 or 32 steps per lane
+SYNTH_U = 16  # steps per lane (mvb_synthesize_f32 u_steps)
 TILE = 32 * SYNTH_U  # output samples per CTA
 SEG_LEN = 32 * TILE  # samples per delay-sort segment
 IMG_COLS, JOB_COLS, WORK_COLS = 12, 17, 4
