@@ -171,6 +171,12 @@ int mvb_track_max(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jo
                   const double* d_coarse, const double* d_tables, const double* d_lb,
                   const double* d_ub, int32_t* d_scratch, double* d_dmax, void* stream);
 
+/* Decimation decision helper (trajectory.py:316-339): for each of `rows`
+ * power-spectrum rows of length F (fp64, contiguous), the first index whose
+ * cumulative energy reaches fraction * row total; -1 for an all-zero row. */
+int mvb_energy_index(const double* d_power, int64_t rows, int64_t F, double fraction,
+                     int64_t* d_index, void* stream);
+
 /* Fast-path interval records of the images d_sel, all of one decimation
  * factor N: d_coef[image.coef + k] for k < K (K <= max_K), from the coarse
  * distances and h_fit, the factor's (9, 65) refit of its phase-table

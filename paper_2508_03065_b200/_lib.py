@@ -44,6 +44,7 @@ _SIGS = {
     "mvb_synthesize_f32": [P, P, I64, P, P, P, P, P, P, INT, INT, P],
     "mvb_reduce_partials_f32": [P, I64, I64, P, P, P],
     "mvb_synthesize_f64": [P, I64, I64, P, P, P, P, P, P, P],
+    "mvb_energy_index": [P, I64, I64, DBL, P, P],
     "mvb_peak_ffma": [INT, INT, P, P],
     "mvb_peak_l1": [INT, INT, P, P, P],
 }

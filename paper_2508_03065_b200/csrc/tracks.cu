@@ -420,3 +420,72 @@ int mvb_sort_keys(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs, 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// decimation decision (trajectory.py:316-339 bandwidth_estimate): per power
+// spectrum row, the first index whose cumulative energy reaches `fraction`
+// of the row total (searchsorted-left on cumsum/total), -1 for an empty row.
+// One block per row: block reduction for the total, then a chunked block scan
+// that stops at the first crossing.
+
+namespace mvb {
+
+__global__ void __launch_bounds__(256) k_energy_index(const double* __restrict__ pw, int64_t F,
+                                                      double fraction, int64_t* __restrict__ out) {
+    __shared__ double wsum[8];
+    __shared__ double carry_s;
+    __shared__ int found_s;
+    const double* p = pw + (int64_t)blockIdx.x * F;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double s = 0.0;
+    for (int64_t f = threadIdx.x; f < F; f += 256) s += p[f];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) wsum[w] = s;
+    __syncthreads();
+    double tot = 0.0;
+    for (int q = 0; q < 8; ++q) tot += wsum[q];
+    if (!(tot > 0.0)) {
+        if (threadIdx.x == 0) out[blockIdx.x] = -1;
+        return;
+    }
+    const double thr = fraction * tot;
+    if (threadIdx.x == 0) { carry_s = 0.0; found_s = 0x7fffffff; }
+    __syncthreads();
+    for (int64_t base = 0; base < F; base += 256) {
+        const int64_t f = base + threadIdx.x;
+        double v = f < F ? p[f] : 0.0;
+        // inclusive warp scan, then across warps
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        __syncthreads();
+        if (lane == 31) wsum[w] = v;
+        __syncthreads();
+        double pre = carry_s;
+        for (int q = 0; q < w; ++q) pre += wsum[q];
+        const double cum = pre + v;
+        if (f < F && cum >= thr) atomicMin(&found_s, (int)(f - base));
+        __syncthreads();
+        if (found_s != 0x7fffffff) {
+            if (threadIdx.x == 0) out[blockIdx.x] = base + found_s;
+            return;
+        }
+        if (threadIdx.x == 255) carry_s = cum;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[blockIdx.x] = F - 1;
+}
+
+}  // namespace mvb
+
+extern "C" int mvb_energy_index(const double* pw, int64_t rows, int64_t F, double fraction,
+                                int64_t* out, void* stream) {
+    using namespace mvb;
+    if (rows < 0 || rows > 0x7fffffff || F < 1 || !(fraction > 0.0 && fraction < 1.0))
+        return fail(MVB_EINVAL, "energy_index: args");
+    if (rows == 0) return MVB_OK;
+    if (!pw || !out) return fail(MVB_EINVAL, "energy_index: null");
+    k_energy_index<<<(unsigned)rows, 256, 0, as_stream(stream)>>>(pw, F, fraction, out);
+    return check_launch("energy_index");
+}

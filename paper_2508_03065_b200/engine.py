@@ -38,7 +38,8 @@ from ._dev import ptr, require_cuda, stream_handle
 from .farrow import as_filter, centered_branches
 from .parallel import image_slice
 from .room import image_count, image_table
-from .trajectory import decimate_batch, device_constants, negative_mass, phase_fit
+from .trajectory import (bandwidth_batch, decimate_batch, device_constants, negative_mass,
+                         phase_fit)
 
 import os
 
@@ -241,10 +242,11 @@ class Geometry:
         for (T, rate), rows in groups.items():
             starts = sorted(rows, key=rows.get)
             x = torch.stack([self.paths[r0:r0 + T] for r0 in starts])  # (G, T, 3)
+            bw = bandwidth_batch(x, rate)  # once for all factors
             for (T2, rate2, N), lst in uses.items():
                 if (T2, rate2) != (T, rate):
                     continue
-                coarse = decimate_batch(x, rate, N)  # (G, K, 3)
+                coarse = decimate_batch(x, rate, N, bw)  # (G, K, 3)
                 K = coarse.shape[1]
                 info = h2d(np.asarray(lst, dtype=np.int64), dev)
                 dst = (info[:, 1:2] + torch.arange(K, device=dev)[None, :]).reshape(-1)

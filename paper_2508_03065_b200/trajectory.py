@@ -115,22 +115,19 @@ def device_constants(factor: int, device) -> dict:
 def bandwidth_batch(x: torch.Tensor, rate: float, energy_fraction: float = 0.99) -> torch.Tensor:
     """Per-path smallest frequency holding `energy_fraction` of the
     mean-removed displacement power, max over axes (reference
-    trajectory.py:316-339), for x (G, T, 3) on the device -> (G,)."""
+    trajectory.py:316-339), for x (G, T, 3) on the device -> (G,).  The FFT
+    is cuFFT (torch.fft); the energy search is libmvb's mvb_energy_index."""
     G, T, _ = x.shape
     if T < 2:
         return torch.zeros(G, dtype=torch.float64, device=x.device)
     xc = (x - x.mean(dim=1, keepdim=True)).permute(0, 2, 1).contiguous()  # (G, 3, T)
-    pw = torch.fft.rfft(xc, dim=2).abs() ** 2  # (G, 3, F)
-    tot = pw.sum(dim=2)  # (G, 3)
-    # scan along the contiguous axis (an outer-dim cumsum costs ~40 ms at T=480k)
-    cum = torch.cumsum(pw, dim=2) / torch.where(tot > 0, tot, torch.ones_like(tot))[:, :, None]
+    pw = (torch.fft.rfft(xc, dim=2).abs() ** 2).contiguous()  # (G, 3, F)
     F = pw.shape[2]
-    k = torch.searchsorted(cum.reshape(G * 3, F), torch.full((G * 3, 1), energy_fraction,
-                                                             dtype=cum.dtype, device=x.device))
-    k = torch.clamp(k.squeeze(1), max=F - 1).reshape(G, 3)
-    f = k.to(torch.float64) * (rate / T)
-    f = torch.where(tot > 0, f, torch.zeros_like(f))
-    return f.max(dim=1).values
+    k = torch.empty(G * 3, dtype=torch.int64, device=x.device)
+    _lib.call("mvb_energy_index", ptr(pw), G * 3, F, float(energy_fraction), ptr(k),
+              stream_handle(x.device))
+    f = k.reshape(G, 3).to(torch.float64) * (rate / T)  # empty rows (-1) -> negative
+    return torch.clamp(f, min=0.0).max(dim=1).values
 
 
 def bandwidth_estimate_dev(pos: torch.Tensor, rate: float, energy_fraction: float = 0.99) -> float:
@@ -160,16 +157,19 @@ def lowpass_columns_dev(x: torch.Tensor, rate: float, cutoff: float) -> torch.Te
     return lowpass_batch(x[None], rate, cutoff)[0].contiguous()
 
 
-def decimate_batch(x: torch.Tensor, rate: float, factor: int) -> torch.Tensor:
+def decimate_batch(x: torch.Tensor, rate: float, factor: int, bw: torch.Tensor | None = None
+                   ) -> torch.Tensor:
     """Coarse paths x[:, ::N] of x (G, T, 3), each low-passed first when its
     measured bandwidth lies in (Nyquist_out, 2 Nyquist_out) -- decided and
     applied on the device without a host round trip (the low-passed variant
-    is computed for every path and selected per path)."""
+    is computed for every path and selected per path).  `bw` may carry the
+    paths' bandwidths (bandwidth_batch) when several factors are needed."""
     raw = x[:, ::factor]
     if x.shape[1] < 2 or factor == 1:
         return raw
     nyq = 0.5 * rate / factor
-    bw = bandwidth_batch(x, rate)
+    if bw is None:
+        bw = bandwidth_batch(x, rate)
     use = ((bw > nyq) & (bw < 2.0 * nyq))[:, None, None]
     lp = lowpass_batch(x, rate, 0.9 * nyq)[:, ::factor]
     return torch.where(use, lp, raw)

@@ -151,3 +151,16 @@ def test_fast_engine_reference_design_filter():
                           sc.max_order, sc.tiers, g["branches"], sc.rate).render()
     assert y.size == ref.size
     assert rel_err(y, ref) <= FP32_TOL
+
+
+@pytest.mark.parametrize("tag", ["slow", "fast"])
+def test_decimate_on_device_matches_reference(kernels_golden, tag):
+    """Bandwidth decision (cuFFT + mvb_energy_index) and the anti-alias
+    low-pass (trajectory.py:279-298); 'fast' triggers the low-pass."""
+    from paper_2508_03065_b200.trajectory import Trajectory, bandwidth_estimate_dev, decimate
+    g = kernels_golden
+    pos = g[f"dec_{tag}_in"]
+    tr = decimate(Trajectory(rate=1000.0, positions=pos), int(g[f"dec_{tag}_N"]))
+    np.testing.assert_allclose(tr.positions, g[f"dec_{tag}_out"], rtol=0, atol=1e-12)
+    bw = bandwidth_estimate_dev(torch.as_tensor(pos, device="cuda"), 1000.0)
+    assert bw == orc.bandwidth_estimate(pos, 1000.0)
