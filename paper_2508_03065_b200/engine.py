@@ -68,10 +68,51 @@ class Job:
     path_key: object = None  # jobs with equal keys share one source path
 
 
+class _PinnedRing:
+    """Persistent pinned staging ring for the planner's small uploads.
+
+    Arrays are copied into the ring and sent with an asynchronous
+    stream-ordered copy (no host sync, no per-call cudaHostAlloc).  Before
+    the ring wraps, the event recorded after the last copy of the previous
+    lap is awaited, so no staged bytes are overwritten before their copy ran.
+    """
+
+    ALIGN = 256
+
+    def __init__(self, nbytes: int = 16 << 20):
+        self.cap = nbytes
+        self.buf = None
+        self.off = 0
+        self.fence = None
+
+    def put(self, a: np.ndarray, dev) -> torch.Tensor:
+        a = np.ascontiguousarray(a)
+        n = a.nbytes
+        if n > self.cap // 4:  # large arrays: one-off pinned copy
+            return torch.from_numpy(np.array(a)).pin_memory().to(dev, non_blocking=True)
+        if self.buf is None:
+            self.buf = torch.empty(self.cap, dtype=torch.uint8, pin_memory=True)
+            self.host = self.buf.numpy()
+        if self.off + n > self.cap:
+            if self.fence is not None:
+                self.fence.synchronize()
+            self.off = 0
+        self.host[self.off:self.off + n] = a.reshape(-1).view(np.uint8)
+        src = self.buf[self.off:self.off + n].view(torch.from_numpy(a[:0].reshape(-1)).dtype)
+        out = src.reshape(a.shape).to(dev, non_blocking=True)
+        self.off += -(-max(n, 1) // self.ALIGN) * self.ALIGN
+        if self.fence is None:
+            self.fence = torch.cuda.Event()
+        self.fence.record()
+        return out
+
+
+_RING = _PinnedRing()
+
+
 def h2d(a: np.ndarray, dev) -> torch.Tensor:
-    """Host array -> device through pinned memory, without a host sync."""
-    t = torch.from_numpy(np.ascontiguousarray(a))
-    return t.pin_memory().to(dev, non_blocking=True)
+    """Host array -> device without a host sync (pinned ring staging)."""
+    return _RING.put(np.asarray(a), dev)
 
 
 def _key(explicit, obj):
@@ -132,6 +173,8 @@ class Geometry:
         self.pos_off = np.zeros(nJ, np.int64)
         self.mic_off = np.zeros(nJ, np.int64)
         self.moving = np.zeros(nJ, np.int64)
+        # all source paths first (equal-length paths of a batch then form one
+        # strided view for the decimation decision), receivers after them
         for j, jb in enumerate(jobs):
             k = _key(jb.path_key, jb.pos)
             if k not in path_row:
@@ -140,6 +183,7 @@ class Geometry:
                 (dev_parts if isinstance(p, torch.Tensor) else host_parts).append((row, p))
                 row += p.shape[0]
             self.pos_off[j], self.T[j] = path_row[k]
+        for j, jb in enumerate(jobs):
             m = _as_f64_rows(jb.mic)
             if m.shape[0] == 1:
                 self.moving[j] = 0
@@ -241,7 +285,11 @@ class Geometry:
                 uses.setdefault((T, rate, N), []).append((pos, d))
         for (T, rate), rows in groups.items():
             starts = sorted(rows, key=rows.get)
-            x = torch.stack([self.paths[r0:r0 + T] for r0 in starts])  # (G, T, 3)
+            G = len(starts)
+            if all(starts[q] == starts[0] + q * T for q in range(G)):
+                x = self.paths[starts[0]:starts[0] + G * T].view(G, T, 3)  # contiguous run
+            else:
+                x = torch.stack([self.paths[r0:r0 + T] for r0 in starts])  # (G, T, 3)
             bw = bandwidth_batch(x, rate)  # once for all factors
             for (T2, rate2, N), lst in uses.items():
                 if (T2, rate2) != (T, rate):
@@ -319,26 +367,26 @@ class Geometry:
             beta = tab.beta[ridx]
             if sel is not None:
                 offset, sign, beta = offset[:, sel], sign[:, sel], beta[:, sel]
-            K_np = np.where(fac_np[None, :] > 1,
-                            -(-self.T[members][:, None] // fac_np[None, :]), 0)  # (G, S)
-            cnt_np = K_np.reshape(-1)
-            coarse_off_np = coarse_base + np.cumsum(cnt_np) - cnt_np
-            coarse_base += int(cnt_np.sum())
-            fac = h2d(fac_np, dev)
+            # per-image (S) host arrays, per-job (G) arrays; (G, S) fields are
+            # formed on the device by broadcasting (no per-image H2D of G*S)
+            facs = sorted(set(fac_np.tolist()))
+            fidx_np = np.searchsorted(np.asarray(facs), fac_np)
+            table_np = np.asarray([self.table_off.get(N, 0) for N in facs], np.int64)[fidx_np]
+            fit_np = np.asarray([self.fit_idx.get(N, 0) for N in facs], np.int64)[fidx_np]
+            cpath_np = np.asarray([[self.cpath.get((j, N), 0) for N in facs] for j in members],
+                                  np.int64)  # (G, nF)
+            Tj_np = self.T[members]
+            s_info = h2d(np.stack([fac_np, table_np, fit_np, fidx_np]), dev)  # (4, S)
+            fac, table, fit, fidx = s_info[0], s_info[1], s_info[2], s_info[3]
+            g_info = h2d(np.concatenate([Tj_np, np.asarray(members, np.int64)]), dev)
+            Tj, jid = g_info[:G], g_info[G:]
+            cpath = h2d(cpath_np, dev)[:, fidx]  # (G, S)
             Nf = fac[None, :].expand(G, S)
-            K = h2d(K_np, dev)
-            coarse_off = h2d(coarse_off_np, dev)
-            table = torch.zeros_like(Nf)
-            fit = torch.zeros_like(Nf)
-            cpath = torch.zeros_like(Nf)
-            for N in set(fac_np.tolist()):
-                if N == 1:
-                    continue
-                m = Nf == N
-                table = torch.where(m, torch.full_like(table, self.table_off[N]), table)
-                fit = torch.where(m, torch.full_like(fit, self.fit_idx[N]), fit)
-                cp = h2d(np.asarray([self.cpath[(j, N)] for j in members], np.int64), dev)[:, None]
-                cpath = torch.where(m, cp.expand(G, S), cpath)
+            K = torch.where(Nf > 1, (Tj[:, None] + Nf - 1) // Nf, torch.zeros_like(Nf))
+            cnt = K.reshape(-1)
+            coarse_off = coarse_base + torch.cumsum(cnt, 0) - cnt
+            counts = {N: int((fac_np == N).sum()) for N in facs}
+            coarse_base += int(sum(c * int(np.sum(-(-Tj_np // N))) for N, c in counts.items() if N > 1))
             blk = torch.zeros(G, S, IMG_COLS, dtype=torch.int64, device=dev)
             f64 = blk.view(torch.float64)
             f64[:, :, 0:3] = offset
@@ -351,34 +399,37 @@ class Geometry:
             i32[:, :, 1] = K.to(torch.int32)
             blk[:, :, 7] = coarse_off.reshape(G, S)
             blk[:, :, 8] = coarse_off.reshape(G, S)  # one interval record per coarse sample
-            blk[:, :, 9] = table
+            blk[:, :, 9] = table[None, :]
             blk[:, :, 10] = cpath
             j32 = blk[:, :, 11:12].view(torch.int32)
-            j32[:, :, 0] = h2d(np.asarray(members, np.int32), dev)[:, None]
-            j32[:, :, 1] = fit.to(torch.int32)
+            j32[:, :, 0] = jid.to(torch.int32)[:, None]
+            j32[:, :, 1] = fit.to(torch.int32)[None, :]
             blocks.append(blk.reshape(G * S, IMG_COLS))
-            tiled = np.tile(fac_np, G)
-            flat_dec = h2d(np.nonzero(tiled > 1)[0].astype(np.int32) + img_base, dev)
-            flat_full = h2d(np.nonzero(tiled == 1)[0].astype(np.int32) + img_base, dev)
-            for N in set(fac_np.tolist()) - {1}:
-                by_factor.setdefault(int(N), []).append(
-                    np.nonzero(tiled == N)[0].astype(np.int32) + img_base)
-            dec_sel.append(flat_dec)
-            full_sel.append(flat_full)
-            facs, cnts = np.unique(fac_np, return_counts=True)
+            # selections: image positions of one factor, for every job of the group
+            jbase = img_base + S * torch.arange(G, device=dev, dtype=torch.int64)[:, None]
+
+            def positions(mask):
+                idx = h2d(np.nonzero(mask)[0].astype(np.int64), dev)
+                return (jbase + idx[None, :]).reshape(-1).to(torch.int32)
+
+            dec_sel.append(positions(fac_np > 1))
+            full_sel.append(positions(fac_np == 1))
+            for N in facs:
+                if N > 1:
+                    by_factor.setdefault(int(N), []).append(positions(fac_np == N))
             for g, j in enumerate(members):
                 self.img_off[j] = img_base + g * S
                 self.n_img[j] = S
                 T = int(self.T[j])
                 self.evals[j] = int(sum(c * (T if N == 1 else -(-T // int(N)))
-                                        for N, c in zip(facs.tolist(), cnts.tolist())))
+                                        for N, c in counts.items()))
                 self.order_of_job[j] = order
             img_base += G * S
         self.images = torch.cat(blocks) if len(blocks) > 1 else blocks[0]
         self.n_images = img_base
         self.n_coarse_total = coarse_base
         self.dec_sel = torch.cat(dec_sel).to(torch.int32)
-        self.sel_by_factor = {N: h2d(np.concatenate(v), dev) for N, v in by_factor.items()}
+        self.sel_by_factor = {N: torch.cat(v) for N, v in by_factor.items()}
         self.full_sel = torch.cat(full_sel).to(torch.int32)
         if self.full_sel.numel() > 65535:
             raise ValueError("more than 65535 full-rate images in one batch")
