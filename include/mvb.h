@@ -194,14 +194,17 @@ int mvb_sort_keys(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jo
                   const double* d_paths, const double* d_coarse, double* d_key, void* stream);
 
 /* Fast path: fp32 branch records v'_k = x (*) c'_k (d_cbranch (M1, L) fp64
- * in the centred basis (mu - 1/2)^k, zero branches k >= M1) for input
- * samples m < T + L - 1, written to global rows row0 + m.  Layout: rows in
- * blocks of 64; block b holds nb/4 planes of 64 float4 (plane p = branches
- * 4p..4p+3), i.e. row r plane p is float4 number r + (nb/4 - 1)(r & ~63) +
- * 64 p.  Rows outside are left as the caller zeroed them.  L <= 128;
- * row0 + T + L < 2^31. */
-int mvb_branch_records_f32(const float* d_x, int64_t T, const double* d_cbranch, int M1,
-                           int L, int nb, int64_t row0, float* d_rec, void* stream);
+ * in the centred basis (mu - 1/2)^k, zero branches k >= M1) of n_sig dry
+ * signals in one launch: signal q is d_x_all[sig_off[q] ..] of length
+ * sig_len[q] (<= max_len), its sample m < len + L - 1 goes to global row
+ * sig_row0[q] + m (device arrays).  Layout: rows in blocks of 64; block b
+ * holds nb/4 planes of 64 float4 (plane p = branches 4p..4p+3), i.e. row r
+ * plane p is float4 number r + (nb/4 - 1)(r & ~63) + 64 p.  Rows outside
+ * are left as the caller zeroed them.  L <= 128; rows < 2^31. */
+int mvb_branch_records_f32(const float* d_x_all, const int64_t* d_sig_off,
+                           const int64_t* d_sig_len, const int64_t* d_sig_row0, int64_t n_sig,
+                           int64_t max_len, const double* d_cbranch, int M1, int L, int nb,
+                           float* d_rec, void* stream);
 
 /* Fast synthesis (fp32 I/O, fp64 anchors), one CTA per work item covering
  * 32*u_steps output samples (u_steps = 16); jobs with n_chunks > 1 write

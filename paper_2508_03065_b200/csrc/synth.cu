@@ -54,14 +54,23 @@ __device__ __forceinline__ const float4* rec_row(const float4* base, unsigned r)
     return p;
 }
 
+// One launch for every distinct dry signal of a batch: blockIdx.y selects
+// the signal (x_all + off[y], length len[y], record rows from row0[y]).
 template <int NP>
-__global__ void k_branch_records_f32(const float* __restrict__ x, int64_t T,
-                                     const double* __restrict__ cb, int M1, int L, int64_t row0,
+__global__ void k_branch_records_f32(const float* __restrict__ x_all,
+                                     const int64_t* __restrict__ sig_off,
+                                     const int64_t* __restrict__ sig_len,
+                                     const int64_t* __restrict__ sig_row0,
+                                     const double* __restrict__ cb, int M1, int L,
                                      float* __restrict__ rec) {
     constexpr int NB = 4 * NP;
     extern __shared__ float sx[];  // [blockDim.x + L - 1]
     __shared__ float sc[NB * 128];
+    const int64_t T = sig_len[blockIdx.y];
     const int64_t m0 = (int64_t)blockIdx.x * blockDim.x;
+    if (m0 >= T + L - 1) return;
+    const float* __restrict__ x = x_all + sig_off[blockIdx.y];
+    const int64_t row0 = sig_row0[blockIdx.y];
     for (int t = threadIdx.x; t < NB * L; t += blockDim.x) {
         const int k = t / L, j = t - (t / L) * L;
         sc[k * L + j] = k < M1 ? (float)cb[k * L + j] : 0.f;
@@ -473,22 +482,28 @@ using namespace mvb;
 
 extern "C" {
 
-int mvb_branch_records_f32(const float* x, int64_t T, const double* cb, int M1, int L, int nb,
-                           int64_t row0, float* rec, void* stream) {
-    if (T < 1 || L < 1 || L > 128 || M1 < 1 || M1 > nb || row0 < 0 || row0 + T + L > 0x7fffffffLL)
+int mvb_branch_records_f32(const float* x_all, const int64_t* sig_off, const int64_t* sig_len,
+                           const int64_t* sig_row0, int64_t n_sig, int64_t max_len,
+                           const double* cb, int M1, int L, int nb, float* rec, void* stream) {
+    if (n_sig < 0 || n_sig > 65535 || max_len < 1 || L < 1 || L > 128 || M1 < 1 || M1 > nb)
         return fail(MVB_EINVAL, "branch_records: sizes");
-    if (!x || !cb || !rec) return fail(MVB_EINVAL, "branch_records: null");
+    if (n_sig == 0) return MVB_OK;
+    if (!x_all || !sig_off || !sig_len || !sig_row0 || !cb || !rec)
+        return fail(MVB_EINVAL, "branch_records: null");
     const int block = 256;
     const size_t smem = sizeof(float) * (block + L - 1);
-    const unsigned g = grid_for(T + L - 1, block);
+    const dim3 g(grid_for(max_len + L - 1, block), (unsigned)n_sig);
     cudaStream_t s = as_stream(stream);
+#define MVB_BR(NP) k_branch_records_f32<NP><<<g, block, smem, s>>>(x_all, sig_off, sig_len, \
+                                                                   sig_row0, cb, M1, L, rec)
     switch (nb) {
-        case 4: k_branch_records_f32<1><<<g, block, smem, s>>>(x, T, cb, M1, L, row0, rec); break;
-        case 8: k_branch_records_f32<2><<<g, block, smem, s>>>(x, T, cb, M1, L, row0, rec); break;
-        case 12: k_branch_records_f32<3><<<g, block, smem, s>>>(x, T, cb, M1, L, row0, rec); break;
-        case 16: k_branch_records_f32<4><<<g, block, smem, s>>>(x, T, cb, M1, L, row0, rec); break;
+        case 4: MVB_BR(1); break;
+        case 8: MVB_BR(2); break;
+        case 12: MVB_BR(3); break;
+        case 16: MVB_BR(4); break;
         default: return fail(MVB_EINVAL, "branch_records: nb must be 4, 8, 12 or 16");
     }
+#undef MVB_BR
     return check_launch("branch_records_f32");
 }
 

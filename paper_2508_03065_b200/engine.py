@@ -641,11 +641,14 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
     if rec_rows + int(out_len.max()) + L >= 2**31 - 0x4B400000:
         raise ValueError("batch too large for 32-bit record rows; split it")
     rec = torch.zeros(rec_rows * nb, dtype=torch.float32, device=dev)
-    for k in uniq:
-        r0, front = bases[k]
-        _lib.call("mvb_branch_records_f32", ptr(sig_dev[k]), sig_len[k], ptr(cb_dev), M1, L, nb,
-                  r0 + front, ptr(rec), st)
-        launches += 1
+    ukeys = list(uniq)
+    x_all = sig_dev[ukeys[0]] if len(ukeys) == 1 else torch.cat([sig_dev[k] for k in ukeys])
+    lens = np.asarray([sig_len[k] for k in ukeys], np.int64)
+    sig_tab = h2d(np.stack([np.concatenate([[0], np.cumsum(lens)[:-1]]), lens,
+                            np.asarray([bases[k][0] + bases[k][1] for k in ukeys], np.int64)]), dev)
+    _lib.call("mvb_branch_records_f32", ptr(x_all), ptr(sig_tab[0]), ptr(sig_tab[1]),
+              ptr(sig_tab[2]), len(ukeys), int(lens.max()), ptr(cb_dev), M1, L, nb, ptr(rec), st)
+    launches += 1
     for j in range(nJ):
         r0, front = bases[keys[j]]
         rows[j].update(rec_base=r0 + front, nb=nb, img_off=j * max_seg * max_img,
