@@ -214,6 +214,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int U>
 struct alignas(16) WarpStage {
     static constexpr int RMAX = U + 1;
+    static_assert(3 * RMAX <= 64, "stage_records copies at most two 16-byte chunks per lane");
     mvb_image img[3];
     mvb_coef32 rec[2][RMAX];
     int k0[2];
@@ -230,13 +231,22 @@ __device__ __forceinline__ void stage_records(WarpStage<U>& st, int slot, const 
     const int N = q.factor;
     int cnt = 0, k0 = 0;
     if (N >= 32) {
-        k0 = n0 / N;
-        const int last = (n0 + TN - 1 < T - 1 ? n0 + TN - 1 : T - 1) / N;
-        cnt = last - k0 + 1;
-        if (cnt > WarpStage<U>::RMAX) cnt = 0;  // cannot happen for N >= 32
+        const int nlast = n0 + TN - 1 < T - 1 ? n0 + TN - 1 : T - 1;
+        int last;
+        if ((N & (N - 1)) == 0) {  // power of two: shifts, not divisions
+            const int sh = __ffs(N) - 1;
+            k0 = n0 >> sh;
+            last = nlast >> sh;
+        } else {
+            k0 = n0 / N;
+            last = nlast / N;
+        }
+        cnt = last - k0 + 1;  // <= U + 1 for N >= 32
         const char* src = reinterpret_cast<const char*>(coef + q.coef + k0);
         char* dst = reinterpret_cast<char*>(st.rec[slot]);
-        for (int c = lane; c < 3 * cnt; c += 32) cp_async16(dst + 16 * c, src + 16 * c);
+        // 3*cnt <= 3*(U+1) 16-byte chunks: at most two per lane, no loop
+        if (lane < 3 * cnt) cp_async16(dst + 16 * lane, src + 16 * lane);
+        if (lane + 32 < 3 * cnt) cp_async16(dst + 16 * (lane + 32), src + 16 * (lane + 32));
     }
     if (lane == 0) {
         st.k0[slot] = k0;
