@@ -437,7 +437,7 @@ class OracleScene:
 
     def out_len(self, nthreads: int = 0) -> int:
         tau_max = self.rate * self.track_max(nthreads) / self.c
-        return self.T + int(math.ceil(tau_max)) + self.L
+        return self.s.size + int(math.ceil(tau_max)) + self.L  # synth.py:211-212: len(s)
 
     def render_window(self, n0: int, n1: int, nthreads: int = 0) -> np.ndarray:
         out = np.empty(max(0, n1 - n0))

@@ -88,8 +88,8 @@ class _PinnedRing:
     def put(self, a: np.ndarray, dev) -> torch.Tensor:
         a = np.ascontiguousarray(a)
         n = a.nbytes
-        if n > self.cap // 4:  # large arrays: one-off pinned copy
-            return torch.from_numpy(np.array(a)).pin_memory().to(dev, non_blocking=True)
+        if n > self.cap // 4:  # large arrays: one-off pinned copy (own writable copy)
+            return torch.from_numpy(np.array(a, copy=True)).pin_memory().to(dev, non_blocking=True)
         if self.buf is None:
             self.buf = torch.empty(self.cap, dtype=torch.uint8, pin_memory=True)
             self.host = self.buf.numpy()
@@ -98,7 +98,7 @@ class _PinnedRing:
                 self.fence.synchronize()
             self.off = 0
         self.host[self.off:self.off + n] = a.reshape(-1).view(np.uint8)
-        src = self.buf[self.off:self.off + n].view(torch.from_numpy(a[:0].reshape(-1)).dtype)
+        src = self.buf[self.off:self.off + n].view(_TORCH_DTYPE[a.dtype.str[1:]])
         out = src.reshape(a.shape).to(dev, non_blocking=True)
         self.off += -(-max(n, 1) // self.ALIGN) * self.ALIGN
         if self.fence is None:
@@ -107,6 +107,8 @@ class _PinnedRing:
         return out
 
 
+_TORCH_DTYPE = {"f8": torch.float64, "f4": torch.float32, "i8": torch.int64, "i4": torch.int32,
+                "u1": torch.uint8, "b1": torch.bool}
 _RING = _PinnedRing()
 
 

@@ -216,8 +216,8 @@ def select_images(room, traj, mic, cfg):
     t = image_table(room.dims, room.wall_reflection, cfg.max_order)
     m = np.asarray(mic if not hasattr(mic, "pos") else mic.pos, dtype=np.float64)
     m0 = m if m.ndim == 1 else m[0]
-    d = distance_streams(t.offset[0], t.sign[0], torch.as_tensor(m0, device=t.offset.device),
-                         torch.as_tensor(traj.positions[:1], device=t.offset.device))[:, 0]
+    d = distance_streams(t.offset[0], t.sign[0], torch.tensor(np.array(m0), device=t.offset.device),
+                         torch.tensor(np.array(traj.positions[:1]), device=t.offset.device))[:, 0]
     keep = (d <= cfg.sound_speed * cfg.t60).nonzero().squeeze(1).cpu().numpy()
     return keep.astype(np.int64)
 
