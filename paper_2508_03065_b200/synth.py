@@ -9,6 +9,8 @@ ValueError behaviour; numpy in, float64 numpy out.
 Differences, all opt-in through new SynthesisConfig fields:
   tiers      ((max_order, N), ...) any number of hierarchical rates; the
              reference's (order_split, decimation) is the 2-tier default.
+  modulate   "receiver" (default) on both engines; "source" (the reference's
+             validation switch) on the exact path, one branch pass per image.
   precision  "fp64": the exact engine (reference arithmetic and summation
              order, bit-faithful); "fp32": the fused B200 fast path
              (max error ~1e-6 of the output peak); "auto" (default): fp32
@@ -152,12 +154,17 @@ class DelayStreams:
 
 
 def materialize_tracks(geom) -> np.ndarray:
+    """(S, T) fp64 tracks of job 0 in canonical order (numpy)."""
+    if geom is None:
+        return np.zeros((0, 0))
+    return materialize_tracks_dev(geom).cpu().numpy()
+
+
+def materialize_tracks_dev(geom) -> torch.Tensor:
     """(S, T) fp64 tracks of job 0 in canonical order, computed on the GPU
     with the reference kernels (distance_streams / upsample_stream)."""
     from . import _lib
     from ._dev import ptr, stream_handle
-    if geom is None:
-        return np.zeros((0, 0))
     dev = geom.dev
     S, T = int(geom.n_img[0]), int(geom.T[0])
     img = geom.images[int(geom.img_off[0]):int(geom.img_off[0]) + S]
@@ -192,7 +199,7 @@ def materialize_tracks(geom) -> np.ndarray:
         _lib.call("mvb_upsample_streams", ptr(coarse), rows.size, k, ptr(tab), int(N), 65, T,
                   ptr(res), st)
         out[torch.as_tensor(rows, device=dev)] = res
-    return out.cpu().numpy()
+    return out
 
 
 def _check_receiver(mic, room, T):
@@ -261,15 +268,52 @@ def synthesize(s, streams: DelayStreams, f, cfg) -> np.ndarray:
     """Render s through the moving image set (reference synth.py:194-258).
     Output length len(s) + ceil(max delay) + L, float64."""
     a = _check_signal(s)
-    if cfg.modulate != "receiver":
-        raise NotImplementedError("modulate='source' (reference validation switch) is not "
-                                  "implemented on the GPU engine")
     filt = as_filter(f)
     if streams.image_count() == 0:
         return np.zeros(a.size + filt.branch_len)
+    if cfg.modulate == "source":
+        return _synthesize_source(a, streams, filt, cfg)
     prec = _precision(a, cfg)
     res = engine.render(streams.geometry, [a], filt, precision=prec)
     return res.job(0).to(torch.float64).cpu().numpy()
+
+
+def _synthesize_source(x, streams, f, cfg) -> np.ndarray:
+    """modulate="source" (reference synth.py:228-242, its validation switch):
+    the gain is applied at emission time, so every image filters its own
+    gain-modulated input -- one branch pass per image.  fp64, reference
+    arithmetic and block/pairwise order, on the device with the operator
+    trio (kernels.branch_filter / accumulate_images); materialises (S, out_len)
+    tracks like the reference, so it is meant for validation-size renders."""
+    from . import kernels
+    geom = streams.geometry
+    dev = geom.dev
+    d = materialize_tracks_dev(geom)
+    S, T = d.shape
+    xs = torch.from_numpy(np.array(x, dtype=np.float64)).to(dev)
+    tau_max = streams.rate * float(d.max().item()) / cfg.sound_speed
+    out_len = x.size + int(np.ceil(tau_max)) + f.branch_len
+    d_ext = torch.cat([d, d[:, -1:].expand(S, out_len - T)], dim=1) if T < out_len else d[:, :out_len]
+    d_ext = d_ext.contiguous()
+    tau = streams.rate * d_ext / cfg.sound_speed
+    img = geom.images[int(geom.img_off[0]):int(geom.img_off[0]) + S]
+    beta = img.view(torch.float64)[:, 3]
+    amp = beta[:, None] / (4.0 * np.pi * torch.clamp_min(d_ext, cfg.d_min))
+    ones = torch.ones(1, out_len, dtype=torch.float64, device=dev)
+    branches = torch.from_numpy(np.array(f.branches)).to(dev)
+    buffers = []
+    for b0 in range(0, S, SUMMATION_BLOCK):
+        buf = torch.zeros(out_len, dtype=torch.float64, device=dev)
+        for i in range(b0, min(b0 + SUMMATION_BLOCK, S)):
+            v = kernels.branch_filter((xs * amp[i, :x.size]).contiguous(), branches)
+            kernels.accumulate_images(buf, v, tau[i:i + 1], ones, f.branch_len, f.nominal_delay)
+        buffers.append(buf)
+    while len(buffers) > 1:  # synth.py:182-191
+        merged = [buffers[k] + buffers[k + 1] for k in range(0, len(buffers) - 1, 2)]
+        if len(buffers) % 2:
+            merged.append(buffers[-1])
+        buffers = merged
+    return buffers[0].cpu().numpy()
 
 
 def render(s, traj, room, mic, f, cfg) -> np.ndarray:

@@ -180,6 +180,28 @@ def kernel_cases():
     print("kernels.npz written")
 
 
+def source_modulation_case():
+    """synth.py:228-242: gain applied at emission time (validation switch)."""
+    from dataclasses import replace
+    sc = workloads.make_scenes("c1", duration=0.25, tiers=((1, 1), (3, 32)))[0]
+    f = rfarrow.design(3, 8, 0.8)
+    room = Room(dims=sc.dims, wall_reflection=sc.walls)
+    images = enumerate_images(room, sc.max_order)
+    traj = Trajectory(rate=sc.rate, positions=sc.pos)
+    streams = tier_streams(images, traj, MicPosition(pos=sc.mics[0]), room, sc.tiers)
+    cfg = SynthesisConfig(audio_rate=sc.rate, max_order=sc.max_order, modulate="source")
+    y = synthesize(np.asarray(sc.s, dtype=np.float64), streams, f, cfg)
+    np.savez_compressed(os.path.join(HERE, "render_c1_source.npz"), y=y,
+                        branches=np.asarray(f.branches),
+                        inputs_sha=np.array(digest(sc.s, sc.pos, sc.mics[0])))
+    print("c1_source out_len", y.size)
+
+
 if __name__ == "__main__":
-    kernel_cases()
-    render_cases()
+    import sys as _sys
+    if "--source-only" in _sys.argv:
+        source_modulation_case()
+    else:
+        kernel_cases()
+        render_cases()
+        source_modulation_case()

@@ -215,3 +215,25 @@ def test_moving_receiver_exact_engine():
     y = mvb.render(x, tr, ROOM, mic_path, f, cfg)
     ref = oracle_render(x, tr, mic_path, f, cfg)
     assert y.size == ref.size and rel_err(y, ref) <= 1e-13
+
+
+def test_source_modulation_matches_reference_golden():
+    """modulate='source' (synth.py:228-242) against the reference's own
+    output (tests/golden/render_c1_source.npz), and close to receiver
+    modulation for slow motion (reference test_synth.py:263-277)."""
+    from paper_2508_03065_b200 import workloads
+    g = golden("render_c1_source.npz")
+    sc = workloads.make_scenes("c1", duration=0.25, tiers=((1, 1), (3, 32)))[0]
+    f = FarrowFilter(3, 8, g["branches"], 3, 0.8)
+    room = mvb.Room(dims=sc.dims, wall_reflection=sc.walls)
+    tr = mvb.Trajectory(rate=sc.rate, positions=sc.pos)
+    cfg = mvb.SynthesisConfig(audio_rate=sc.rate, max_order=sc.max_order, tiers=sc.tiers,
+                              modulate="source")
+    y = mvb.render(sc.s, tr, room, sc.mics[0], f, cfg)
+    assert y.size == g["y"].size
+    assert rel_err(y, g["y"]) <= 1e-12
+    from dataclasses import replace
+    y_rx = mvb.render(sc.s, tr, room, sc.mics[0], f, replace(cfg, modulate="receiver"))
+    m = min(y.size, y_rx.size)
+    err = y[200:m - 200] - y_rx[200:m - 200]
+    assert 10 * np.log10(np.sum(y_rx[200:m - 200] ** 2) / np.sum(err ** 2)) >= 30.0
