@@ -230,7 +230,43 @@ int mvb_synthesize_f64(const mvb_job* d_jobs, int64_t n_jobs, int64_t max_out_le
                        const double* d_paths, double* d_out, void* stream);
 
 /* ------------------------------------------------------------------------
- * 4. Roofline probes (measurement only): FP32 FFMA throughput
+ * 4. Static responses and the splice baseline (reference.py:49-187), fp64.
+ *    Sequence: mvb_static_taps -> sort each row of d_base (stable) ->
+ *    mvb_static_gather -> mvb_block_convolve [-> mvb_splice_sum].
+ * --------------------------------------------------------------------- */
+/* reference.py:67-93 for B source positions d_src (B,3) and the S images
+ * (d_offset (S,3), d_sign (S,3), d_beta (S,)): d_base (B,S) = floor(tau),
+ * d_tau (B,S) = rate*d/c, d_kernel (B,S,65) = beta/(4 pi max(d,d_min)) *
+ * Kaiser(7.857)-windowed sinc at (i - 32) - frac (reference.py:49-64). */
+int mvb_static_taps(const double* d_offset, const double* d_sign, const double* d_beta,
+                    int64_t S, const double* d_src, int64_t B, const double* d_mic,
+                    double rate, double c, double d_min, int64_t* d_base, double* d_tau,
+                    double* d_kernel, void* stream);
+/* reference.py:94-100 (scatter-add into the tap train, clipped to
+ * [0, n_taps)) as a gather: d_taps (B, tap_stride), row b zero beyond
+ * d_n_taps[b].  d_base_sorted / d_perm: each row of d_base sorted ascending
+ * and the image index of every sorted entry. */
+int mvb_static_gather(const int64_t* d_base_sorted, const int64_t* d_perm, const double* d_kernel,
+                      int64_t S, int64_t B, const int64_t* d_n_taps, int64_t tap_stride,
+                      double* d_taps, void* stream);
+/* Direct convolution of block b's windowed support of x (n,) with tap row
+ * b: d_pieces (n_blocks, piece_stride), row b = (x * w_b)[lo_b:hi_b] (*)
+ * taps_b, length (hi_b - lo_b) + n_taps_b - 1 <= max_piece.  Blocks and
+ * windows as splice_baseline (reference.py:145-165; lo_b = b*hop, windowed
+ * = 1); static_render (reference.py:103-117) is n_blocks = 1, hop = n,
+ * crossfade = 0, windowed = 0. */
+int mvb_block_convolve(const double* d_x, int64_t n, int64_t hop, int64_t crossfade,
+                       int64_t n_blocks, int windowed, const double* d_taps,
+                       const int64_t* d_n_taps, int64_t tap_stride, int64_t max_piece,
+                       double* d_pieces, int64_t piece_stride, void* stream);
+/* reference.py:180-186: d_out[i] = sum over blocks in order of the pieces
+ * covering output sample i (max_span = longest piece). */
+int mvb_splice_sum(const double* d_pieces, int64_t piece_stride, int64_t n, int64_t hop,
+                   int64_t crossfade, int64_t n_blocks, const int64_t* d_n_taps,
+                   int64_t max_span, double* d_out, int64_t out_len, void* stream);
+
+/* ------------------------------------------------------------------------
+ * 5. Roofline probes (measurement only): FP32 FFMA throughput
  *    (blocks x 256 threads x iters x 128 FFMA) and L1-hit 16-byte load
  *    bandwidth (blocks x 256 threads x iters x 4 x 16 B).  Time them with
  *    CUDA events on `stream`.

@@ -454,3 +454,70 @@ class OracleScene:
         lib().orc_hann_sinc_gather(ctypes.byref(sc), _p(self.s), self.s.size, self.L,
                                    int(n0), int(n1), _p(out), nthreads)
         return out
+
+
+# ---------------------------------------------------------------------------
+# static responses and the splice baseline (reference.py:49-187)
+def sinc_kernels(frac) -> np.ndarray:
+    """(n, 65) Kaiser(7.857)-windowed sinc rows at offsets (i - 32) - frac
+    (reference.py:49-64), vectorised over frac (n,)."""
+    hw = UPSAMPLE_HALFWIDTH
+    arg = np.arange(-hw, hw + 1, dtype=np.float64)[None, :] - np.asarray(frac, np.float64)[:, None]
+    z = np.clip(arg / hw, -1.0, 1.0)
+    win = np.where(np.abs(arg) <= hw, np.i0(7.857 * np.sqrt(np.maximum(0.0, 1.0 - z * z))), 0.0)
+    return np.sinc(arg) * (win / np.i0(7.857))
+
+
+def static_rir_taps(dims, walls, src, mic, rate: float, max_order: int, c: float = 343.0,
+                    d_min: float = 0.05) -> np.ndarray:
+    """Tap train of a frozen source (reference.py:67-100): every image's
+    windowed sinc scaled by beta/(4 pi max(d, d_min)) and added at
+    floor(tau) - 32 in canonical image order, clipped to [0, n_taps)."""
+    im = enumerate_images(dims, walls, max_order)
+    p = im.offset + im.sign * np.asarray(src, np.float64)[None, :]
+    d = np.linalg.norm(p - np.asarray(mic, np.float64)[None, :], axis=1)
+    tau = rate * d / c
+    n_taps = int(np.ceil(tau.max())) + UPSAMPLE_HALFWIDTH + 2
+    base = np.floor(tau)
+    rows = (im.beta / (4.0 * np.pi * np.maximum(d, d_min)))[:, None] * sinc_kernels(tau - base)
+    idx = base.astype(np.int64)[:, None] - UPSAMPLE_HALFWIDTH + np.arange(rows.shape[1])[None, :]
+    keep = (idx >= 0) & (idx < n_taps)
+    taps = np.zeros(n_taps)
+    np.add.at(taps, idx[keep], rows[keep])  # image-major: canonical order per tap
+    return taps
+
+
+def splice_windows(n: int, hop: int, crossfade: int):
+    """(start, stop-of-support, window values) of every block
+    (reference.py:145-165)."""
+    nb = max(1, -(-n // hop))
+    out = []
+    for b in range(nb):
+        start, stop = b * hop, min(n, (b + 1) * hop)
+        end = min(n, stop + crossfade) if (crossfade > 0 and b < nb - 1) else stop
+        w = np.ones(end - start)
+        if crossfade > 0:
+            k = np.arange(start, end)
+            fade_in = (k < stop) & (k < start + crossfade) & (b > 0)
+            w[fade_in] = (k[fade_in] - start + 0.5) / crossfade
+            fade_out = k >= stop
+            w[fade_out] = np.maximum(0.0, 1.0 - (k[fade_out] - stop + 0.5) / crossfade)
+        out.append((start, end, w))
+    return out
+
+
+def splice_baseline(s, pos, dims, walls, mic, rate: float, max_order: int, hop: int,
+                    crossfade: int, c: float = 343.0, d_min: float = 0.05) -> np.ndarray:
+    """Block-frozen render (reference.py:133-187): source frozen at each
+    block start, windowed blocks convolved (direct) with their responses and
+    overlap-added in block order."""
+    s = np.asarray(s, np.float64)
+    pieces = []
+    for start, end, w in splice_windows(s.size, hop, crossfade):
+        taps = static_rir_taps(dims, walls, pos[min(start, len(pos) - 1)], mic, rate, max_order,
+                               c, d_min)
+        pieces.append((start, np.convolve(s[start:end] * w, taps), s.size + taps.size - 1))
+    out = np.zeros(max(p[2] for p in pieces))
+    for start, y, _ in pieces:
+        out[start:start + y.size] += y
+    return out

@@ -45,6 +45,10 @@ _SIGS = {
     "mvb_reduce_partials_f32": [P, I64, I64, P, P, P],
     "mvb_synthesize_f64": [P, I64, I64, P, P, P, P, P, P, P],
     "mvb_energy_index": [P, I64, I64, DBL, P, P],
+    "mvb_static_taps": [P, P, P, I64, P, I64, P, DBL, DBL, DBL, P, P, P, P],
+    "mvb_static_gather": [P, P, P, I64, I64, P, I64, P, P],
+    "mvb_block_convolve": [P, I64, I64, I64, I64, INT, P, P, I64, I64, P, I64, P],
+    "mvb_splice_sum": [P, I64, I64, I64, I64, I64, P, I64, P, I64, P],
     "mvb_peak_ffma": [INT, INT, P, P],
     "mvb_peak_l1": [INT, INT, P, P, P],
 }

@@ -197,11 +197,61 @@ def source_modulation_case():
     print("c1_source out_len", y.size)
 
 
+def static_cases():
+    """reference.py:67-251: static_rir, static_render (direct and FFT
+    branches), splice_baseline (butt-joined, cross-faded, short last block)
+    and compare, on the reference test suite's room and mic."""
+    from moverb import reference as rref
+    room = Room(dims=np.array([5.0, 6.0, 4.0]), wall_reflection=np.full(6, 0.9))
+    mic = MicPosition(pos=np.array([1.25, 2.6, 2.75]))
+    rate = 16000.0
+    out = {}
+    srcs = {"far": np.array([2.0, 3.5, 2.0]), "near": np.array([1.5, 2.8, 2.5]),
+            "corner": np.array([0.3, 5.6, 0.4])}
+    for tag, src in srcs.items():
+        for order in (0, 2, 3):
+            r = rref.static_rir(room, src, mic, rate, order)
+            out[f"rir_{tag}_{order}"] = r.taps
+            out[f"rir_{tag}_{order}_count"] = np.array(r.image_count)
+    rng = np.random.default_rng(11)
+    x_small = rng.standard_normal(1600)   # 1600 * 638 < 5e6: np.convolve
+    x_large = rng.standard_normal(16000)  # > 5e6 products: fftconvolve
+    out["x_small"], out["x_large"] = x_small, x_large
+    rir = rref.static_rir(room, srcs["far"], mic, rate, 2)
+    out["render_small"] = rref.static_render(x_small, rir)
+    out["render_large"] = rref.static_render(x_large, rir)
+    n = 4000
+    t = np.arange(n) / rate
+    pos = np.stack([1.0 + 0.9 * t, np.full(n, 3.0), np.full(n, 2.0)], axis=1)
+    traj = Trajectory(rate=rate, positions=pos)
+    x = np.sin(2 * np.pi * 700.0 * t) + 0.3 * rng.standard_normal(n)
+    out["splice_x"], out["splice_pos"] = x, pos
+    cfg = SynthesisConfig(max_order=2, decimation=1)
+    for hop, cf in ((640, 0), (640, 128), (640, 200), (600, 100), (1000, 1000)):
+        out[f"splice_{hop}_{cf}"] = rref.splice_baseline(x, traj, room, mic, hop, cf, cfg)
+    a = out["splice_640_0"]
+    b = out["splice_640_128"]
+    for tag, (u, v, kw) in {"ab": (a, b, dict(passband=0.8, rate=rate, interior=0.05)),
+                            "aa": (a, a, dict(passband=1.0, rate=rate, interior=0.1)),
+                            "noisy": (b + 1e-3 * rng.standard_normal(b.size), b,
+                                      dict(passband=0.9, rate=rate, interior=0.0))}.items():
+        rep = rref.compare(u, v, **kw)
+        out[f"cmp_{tag}_a"], out[f"cmp_{tag}_b"] = u, v
+        out[f"cmp_{tag}_snr"] = np.array(rep.snr_db)
+        out[f"cmp_{tag}_jump"] = np.array(rep.envelope_max_jump)
+        out[f"cmp_{tag}_track"] = rep.inst_freq_track
+    np.savez_compressed(os.path.join(HERE, "static.npz"), **out)
+    print("static.npz written")
+
+
 if __name__ == "__main__":
     import sys as _sys
     if "--source-only" in _sys.argv:
         source_modulation_case()
+    elif "--static-only" in _sys.argv:
+        static_cases()
     else:
+        static_cases()
         kernel_cases()
         render_cases()
         source_modulation_case()

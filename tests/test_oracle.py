@@ -104,3 +104,30 @@ def test_oracle_render_matches_reference(case):
     # same tracks and streams up to np.convolve's summation order (and, for
     # c5, the reference's moving-mic source transform): ~1e-15 relative
     assert rel_err(y, g["y"]) < 1e-12
+
+
+# ---------------------------------------------------------------- static row
+ROOM_DIMS, ROOM_WALLS = np.array([5.0, 6.0, 4.0]), np.full(6, 0.9)
+MIC_STD = np.array([1.25, 2.6, 2.75])
+STATIC_SRCS = {"far": [2.0, 3.5, 2.0], "near": [1.5, 2.8, 2.5], "corner": [0.3, 5.6, 0.4]}
+
+
+def test_oracle_static_rir_matches_reference():
+    g = golden("static.npz")
+    for tag, src in STATIC_SRCS.items():
+        for order in (0, 2, 3):
+            ref = g[f"rir_{tag}_{order}"]
+            taps = orc.static_rir_taps(ROOM_DIMS, ROOM_WALLS, src, MIC_STD, 16000.0, order)
+            assert taps.size == ref.size
+            assert np.max(np.abs(taps - ref)) <= 1e-13 * np.max(np.abs(ref))
+            assert int(g[f"rir_{tag}_{order}_count"]) == orc.image_count(order)
+
+
+def test_oracle_splice_matches_reference():
+    g = golden("static.npz")
+    for hop, cf in ((640, 0), (640, 128), (640, 200), (600, 100), (1000, 1000)):
+        ref = g[f"splice_{hop}_{cf}"]
+        y = orc.splice_baseline(g["splice_x"], g["splice_pos"], ROOM_DIMS, ROOM_WALLS, MIC_STD,
+                                16000.0, 2, hop, cf)
+        assert y.size == ref.size
+        assert np.max(np.abs(y - ref)) <= 1e-12 * np.max(np.abs(ref))
