@@ -351,12 +351,12 @@ def run_ours(args):
                 r = render_jobs(host_jobs, f, precision=precision, shard=shard)
                 if shard is not None:
                     parallel.reduce_to_root(r.out)
-                out_h = r.out.cpu() if (shard is None or rank == 0) else None
+                out_h = r.host() if (shard is None or rank == 0) else None
                 torch.cuda.synchronize()
                 barrier()
                 tt += time.perf_counter() - t0
                 upd += r.updates
-                d2h = 0 if out_h is None else out_h.numel() * 4
+                d2h = 0 if out_h is None else out_h.nbytes
             tt_t = torch.tensor([tt, float(upd)], dtype=torch.float64, device=dev)
             if world > 1:
                 tmax = tt_t.clone()

@@ -217,8 +217,6 @@ struct alignas(16) WarpStage {
     static_assert(3 * RMAX <= 64, "stage_records copies at most two 16-byte chunks per lane");
     mvb_image img[3];
     mvb_coef32 rec[2][RMAX];
-    int k0[2];
-    int cnt[2];
 };
 
 // issue the copies of image q's interval records over [n0, n0+TN) into slot
@@ -229,28 +227,24 @@ __device__ __forceinline__ void stage_records(WarpStage<U>& st, int slot, const 
                                               int lane) {
     constexpr int TN = 32 * U;
     const int N = q.factor;
-    int cnt = 0, k0 = 0;
-    if (N >= 32) {
+    // tiles past the track end (n0 >= T) read the held record directly: cnt <= 0
+    if (N >= 32 && n0 < T) {
         const int nlast = n0 + TN - 1 < T - 1 ? n0 + TN - 1 : T - 1;
-        int last;
+        int k0, last;
         if ((N & (N - 1)) == 0) {  // power of two: shifts, not divisions
-            const int sh = __ffs(N) - 1;
+            const int sh = 31 - __clz(N);
             k0 = n0 >> sh;
             last = nlast >> sh;
         } else {
             k0 = n0 / N;
             last = nlast / N;
         }
-        cnt = last - k0 + 1;  // <= U + 1 for N >= 32
-        const char* src = reinterpret_cast<const char*>(coef + q.coef + k0);
+        const int chunks = 3 * (last - k0 + 1);  // <= 3 (U + 1) for N >= 32
+        const char* src = reinterpret_cast<const char*>(coef + q.coef) + 48 * k0;
         char* dst = reinterpret_cast<char*>(st.rec[slot]);
-        // 3*cnt <= 3*(U+1) 16-byte chunks: at most two per lane, no loop
-        if (lane < 3 * cnt) cp_async16(dst + 16 * lane, src + 16 * lane);
-        if (lane + 32 < 3 * cnt) cp_async16(dst + 16 * (lane + 32), src + 16 * (lane + 32));
-    }
-    if (lane == 0) {
-        st.k0[slot] = k0;
-        st.cnt[slot] = cnt;
+        // at most two 16-byte chunks per lane, no loop
+        if (lane < chunks) cp_async16(dst + 16 * lane, src + 16 * lane);
+        if (lane + 32 < chunks) cp_async16(dst + 16 * (lane + 32), src + 16 * (lane + 32));
     }
 }
 
@@ -294,6 +288,7 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
 #pragma unroll
     for (int u = 0; u < U; ++u) acc[u] = 0.f;
     const bool inside = n0 + TN <= T;  // no hold-extension inside this tile
+    const bool tail = n0 >= T;         // wholly hold-extended: one delay per image
 
     // prologue of the staging pipeline: structs of the first two images, then
     // the first image's records
@@ -306,22 +301,55 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     if (i0 < img_end) stage_records(st, 0, st.img[0], coef, n0, T, lane);
     cp_async_commit();
 
-    int t = 0;
-    for (int i = i0; i < img_end; i += SYNTH_WARPS, ++t) {
-        const int cur = t % 3, rcur = t & 1;
+    // staging slots rotate: struct slots (cur, nx1, nx2), record slot rcur
+    int cur = 0, nx1 = 1, nx2 = 2, rcur = 0, rot;
+    for (int i = i0; i < img_end;
+         i += SYNTH_WARPS, rot = cur, cur = nx1, nx1 = nx2, nx2 = rot, rcur ^= 1) {
         // everything issued one image ago has landed: records(i), struct(i+8)
         cp_async_wait_all();
         __syncwarp();
         // stream the next image's records and the struct after it while
         // this image is processed
-        if (i + SYNTH_WARPS < img_end)
-            stage_records(st, rcur ^ 1, st.img[(t + 1) % 3], coef, n0, T, lane);
-        if (i + 2 * SYNTH_WARPS < img_end) stage_image(st, (t + 2) % 3, imgs + i + 2 * SYNTH_WARPS, lane);
+        if (i + SYNTH_WARPS < img_end) stage_records(st, rcur ^ 1, st.img[nx1], coef, n0, T, lane);
+        if (i + 2 * SYNTH_WARPS < img_end) stage_image(st, nx2, imgs + i + 2 * SYNTH_WARPS, lane);
         cp_async_commit();
 
         const mvb_image& im = st.img[cur];
         const int N = im.factor;
         const float an = im.amp_num;
+        if (tail) {
+            // hold-extended tile (synth.py:213-216): every sample sees the
+            // track value at T-1, so the delay split and the gain are one
+            // warp-uniform computation; per step only the gather remains
+            float mc, A;
+            int row0;
+            if (N == 1) {
+                const double* p = paths + 3 * (Jp->pos_off + (int64_t)(T - 1));
+                const double* q = paths + 3 * (Jp->mic_off + (Jp->mic_moving ? (int64_t)(T - 1) : 0));
+                const double dx = im.off[0] + im.sign[0] * p[0] - q[0];
+                const double dy = im.off[1] + im.sign[1] * p[1] - q[1];
+                const double dz = im.off[2] + im.sign[2] * p[2] - q[2];
+                const double d = sqrt(dx * dx + dy * dy + dz * dz);
+                const double sv = fma(d, Jp->kappa, (double)(Lsh - Jp->d0));
+                const double D = floor(sv);
+                mc = (float)(sv - D) - 0.5f;
+                row0 = rb + n0 + lane + Lsh - (int)D;
+                A = an * rcp_approx(fmaxf((float)d, dmin));
+            } else {
+                const int kT = (T - 1) / N, rT = (T - 1) - kT * N;
+                const float4* c = reinterpret_cast<const float4*>(coef + im.coef) + 3u * (unsigned)kT;
+                const float4 c0 = __ldg(c), c1 = __ldg(c + 1), c2 = __ldg(c + 2);
+                const float res = track_residual(c1, c2, fmaf((float)rT, 2.0f / (float)N, -1.f));
+                const float tq = c0.y + res;
+                const float v = tq + MAGIC_F;
+                mc = tq - (v - MAGIC_F);
+                row0 = rb + n0 + lane + Lsh + MAGIC_I - __float_as_int(c0.x) - __float_as_int(v);
+                A = an * rcp_approx(fmaxf(fmaf(res, invk, c0.z), dmin));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[u] += A * gather_horner<NP>(R, (unsigned)(row0 + 32 * u), mc);
+            continue;
+        }
         if (N == 1) {
             // near images (full-rate tier): exact fp64 distance per sample,
             // accumulated in the warp's own shared-memory row

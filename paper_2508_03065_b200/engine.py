@@ -117,6 +117,112 @@ def h2d(a: np.ndarray, dev) -> torch.Tensor:
     return _RING.put(np.asarray(a), dev)
 
 
+_POOL = None
+
+
+def _copy_pool():
+    global _POOL
+    if _POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1)),
+                                   thread_name_prefix="mvb-stage")
+    return _POOL
+
+
+def parallel_copy(pairs, chunk_bytes: int = 4 << 20) -> None:
+    """np.copyto(dst, src) for every (dst, src) pair, split into chunks
+    along axis 0 and run on a thread pool (numpy releases the GIL for plain
+    copies, so host memory bandwidth, not one core, bounds bulk staging)."""
+    tasks = []
+    total = 0
+    for dst, src in pairs:
+        n = dst.shape[0] if dst.ndim else 1
+        row = max(1, dst.nbytes // max(n, 1))
+        step = max(1, chunk_bytes // row)
+        for r in range(0, max(n, 1), step):
+            tasks.append((dst[r:r + step], src[r:r + step]) if dst.ndim else (dst, src))
+        total += dst.nbytes
+    if total < (8 << 20) or len(tasks) == 1:
+        for d, s_ in tasks:
+            np.copyto(d, s_, casting="unsafe")
+        return
+    pool = _copy_pool()
+    nw = pool._max_workers
+    groups = [tasks[i::nw] for i in range(nw)]
+
+    def run(group):
+        for d, s_ in group:
+            np.copyto(d, s_, casting="unsafe")
+
+    for fut in [pool.submit(run, g) for g in groups if g]:
+        fut.result()
+
+
+class _BulkStager:
+    """Persistent pinned slabs for bulk uploads (paths, signals): parts are
+    copied straight into a slab (parallel_copy) and sent with ONE
+    asynchronous copy; a slab is reused once the event recorded after its
+    copy has completed, so no per-call cudaHostAlloc and no host sync."""
+
+    MAX_SLABS = 4
+
+    def __init__(self):
+        self.slabs = []  # [pinned uint8 tensor, event | None]
+
+    def _acquire(self, nbytes: int):
+        for sl in self.slabs:
+            if sl[0].numel() >= nbytes and (sl[1] is None or sl[1].query()):
+                return sl
+        cap = 1 << max(20, (max(nbytes, 1) - 1).bit_length())
+        sl = [torch.empty(cap, dtype=torch.uint8, pin_memory=True), None]
+        self.slabs.append(sl)
+        if len(self.slabs) > self.MAX_SLABS:  # drop the smallest idle slab
+            idle = [x for x in self.slabs if x is not sl and (x[1] is None or x[1].query())]
+            if idle:
+                self.slabs.remove(min(idle, key=lambda x: x[0].numel()))
+        return sl
+
+    def upload(self, parts, out: torch.Tensor) -> None:
+        """parts: [(row0, host array)] written into rows of `out` (a device
+        tensor whose trailing dims match the parts); one H2D copy of the
+        covered rows [0, max row)."""
+        if not parts:
+            return
+        np_dt = torch.empty((), dtype=out.dtype).numpy().dtype
+        row_elems = int(np.prod(out.shape[1:])) if out.dim() > 1 else 1
+        rows = max(r0 + (p.shape[0] if np.ndim(p) else 1) for r0, p in parts)
+        nbytes = rows * row_elems * np_dt.itemsize
+        sl = self._acquire(nbytes)
+        host = sl[0][:nbytes].numpy().view(np_dt).reshape((rows,) + tuple(out.shape[1:]))
+        covered = np.zeros(rows, bool)
+        pairs = []
+        for r0, p in parts:
+            p = np.asarray(p)
+            n = p.shape[0]
+            pairs.append((host[r0:r0 + n], p.reshape((n,) + tuple(out.shape[1:]))))
+            covered[r0:r0 + n] = True
+        if not covered.all():
+            host[~covered] = 0
+        parallel_copy(pairs)
+        out[:rows].copy_(sl[0][:nbytes].view(out.dtype).view((rows,) + tuple(out.shape[1:])),
+                         non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        sl[1] = ev
+
+
+_STAGER = _BulkStager()
+
+
+def d2h(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> numpy through pinned memory (caching host
+    allocator), waiting only for the producing stream."""
+    host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    host.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return host.numpy()
+
+
 def _key(explicit, obj):
     return ("k", explicit) if explicit is not None else ("id", id(obj))
 
@@ -208,11 +314,7 @@ class Geometry:
                     row += K * (1 + int(self.moving[j]))
         self.paths = torch.empty(max(row, 1), 3, dtype=torch.float64, device=dev)
         if host_parts:
-            host = np.zeros((full_rows, 3))
-            for r0, p in host_parts:
-                host[r0:r0 + p.shape[0]] = p
-            buf = torch.from_numpy(host).pin_memory() if torch.cuda.is_available() else torch.from_numpy(host)
-            self.paths[:full_rows].copy_(buf, non_blocking=True)
+            _STAGER.upload(host_parts, self.paths)
         for r0, p in dev_parts:
             self.paths[r0:r0 + p.shape[0]].copy_(p)
         self._decimate_paths()
@@ -516,6 +618,10 @@ class RenderResult:
     def job(self, j: int) -> torch.Tensor:
         return self.out[self.offsets[j]:self.offsets[j] + self.lengths[j]]
 
+    def host(self) -> np.ndarray:
+        """The flat output as numpy (pinned D2H, waits for the render)."""
+        return d2h(self.out)
+
 
 def _chunking(n_imgs, tiles, sm_count):
     """Images per CTA: enough CTAs for >= 4 waves of 2 CTAs/SM, chunks of
@@ -553,14 +659,24 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
         uniq.setdefault(keys[j], []).append(j)
     dt = torch.float32 if precision == "fp32" else torch.float64
     sig_dev, sig_len = {}, {}
+    host_sigs, n_host = [], 0
     for k, members in uniq.items():
         s = signals[members[0]]
-        t = s.to(dev, dt) if isinstance(s, torch.Tensor) else h2d(
-            np.asarray(s, dtype=np.float32 if dt == torch.float32 else np.float64), dev)
-        t = t.reshape(-1).contiguous()
-        if t.numel() == 0:
+        if isinstance(s, torch.Tensor):
+            t = s.to(dev, dt).reshape(-1).contiguous()
+            sig_dev[k], sig_len[k] = t, t.numel()
+        else:
+            a = np.asarray(s).reshape(-1)
+            host_sigs.append((k, n_host, a))
+            sig_len[k] = a.size
+            n_host += a.size
+        if sig_len[k] == 0:
             raise ValueError("input must be a nonempty 1-D signal")
-        sig_dev[k], sig_len[k] = t, t.numel()
+    if host_sigs:  # all host signals: one bulk upload, device views per key
+        sig_all = torch.empty(n_host, dtype=dt, device=dev)
+        _STAGER.upload([(r0, a) for _, r0, a in host_sigs], sig_all)
+        for k, r0, a in host_sigs:
+            sig_dev[k] = sig_all[r0:r0 + a.size]
     launches = 0
     base_rows = [dict(r, L=L, d0=d0) for r in geom.job_rows]
 
@@ -644,8 +760,13 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
         raise ValueError("batch too large for 32-bit record rows; split it")
     rec = torch.zeros(rec_rows * nb, dtype=torch.float32, device=dev)
     ukeys = list(uniq)
-    x_all = sig_dev[ukeys[0]] if len(ukeys) == 1 else torch.cat([sig_dev[k] for k in ukeys])
     lens = np.asarray([sig_len[k] for k in ukeys], np.int64)
+    if len(ukeys) == 1:
+        x_all = sig_dev[ukeys[0]]
+    elif host_sigs and len(host_sigs) == len(ukeys):
+        x_all = sig_all  # already concatenated in key order
+    else:
+        x_all = torch.cat([sig_dev[k] for k in ukeys])
     sig_tab = h2d(np.stack([np.concatenate([[0], np.cumsum(lens)[:-1]]), lens,
                             np.asarray([bases[k][0] + bases[k][1] for k in ukeys], np.int64)]), dev)
     _lib.call("mvb_branch_records_f32", ptr(x_all), ptr(sig_tab[0]), ptr(sig_tab[1]),

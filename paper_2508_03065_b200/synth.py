@@ -275,7 +275,8 @@ def synthesize(s, streams: DelayStreams, f, cfg) -> np.ndarray:
         return _synthesize_source(a, streams, filt, cfg)
     prec = _precision(a, cfg)
     res = engine.render(streams.geometry, [a], filt, precision=prec)
-    return res.job(0).to(torch.float64).cpu().numpy()
+    from .engine import d2h
+    return d2h(res.job(0)).astype(np.float64)
 
 
 def _synthesize_source(x, streams, f, cfg) -> np.ndarray:

@@ -150,3 +150,15 @@ def test_pack_jobs_matches_c_layout():
     j = Job.from_buffer_copy(raw)
     for k, v in row.items():
         assert getattr(j, k) == v, k
+
+
+def test_parallel_copy_chunks_and_casts():
+    from paper_2508_03065_b200.engine import parallel_copy
+    rng = np.random.default_rng(0)
+    big = rng.standard_normal((3_000_000, 3))           # 72 MB: thread pool, many chunks
+    small = rng.standard_normal(1000).astype(np.float32)
+    dst_big = np.empty_like(big)
+    dst_small = np.empty(1000, np.float64)
+    parallel_copy([(dst_big, big), (dst_small, small)], chunk_bytes=1 << 20)
+    assert np.array_equal(dst_big, big)
+    assert np.array_equal(dst_small, small.astype(np.float64))
