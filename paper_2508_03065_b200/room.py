@@ -175,3 +175,19 @@ def image_position(spec, source_pos, room):
 
 def image_distance(spec, source_pos, mic, room):
     return float(np.linalg.norm(image_position(spec, source_pos, room) - as_mic(mic).pos))
+
+
+def estimate_image_count(room, t60, c=343.0) -> int:
+    """Lattice points m (room-centred source and mic) with path length
+    |(m_x Lx, m_y Ly, m_z Lz)| <= c * t60: the cost-budget estimate of
+    reference room.py:190-209 (not an enumeration)."""
+    if t60 <= 0:
+        raise ValueError("t60 must be > 0")
+    r = c * t60
+    lx, ly, lz = (float(v) for v in room.dims)
+    mx = np.arange(-int(r // lx), int(r // lx) + 1, dtype=np.float64)
+    my = np.arange(-int(r // ly), int(r // ly) + 1, dtype=np.float64)
+    rest = r * r - (mx[:, None] * lx) ** 2 - (my[None, :] * ly) ** 2
+    inside = rest >= 0.0
+    half = np.floor(np.sqrt(np.where(inside, rest, 0.0)) / lz)
+    return int(np.sum(np.where(inside, 2.0 * half + 1.0, 0.0)))

@@ -191,7 +191,7 @@ def materialize_tracks_dev(geom) -> torch.Tensor:
     from .trajectory import phase_table
     for N in sorted(set(factor.tolist()) - {1}):
         rows = np.nonzero(factor == N)[0]
-        tab = torch.from_numpy(np.ascontiguousarray(phase_table(int(N)))).to(dev)
+        tab = torch.from_numpy(np.array(phase_table(int(N)))).to(dev)
         k = int(K[rows[0]])
         idx = torch.as_tensor(coarse_off[rows], device=dev)[:, None] + torch.arange(k, device=dev)
         coarse = geom.coarse[idx].contiguous()

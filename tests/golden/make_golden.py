@@ -244,13 +244,57 @@ def static_cases():
     print("static.npz written")
 
 
+def cli_cases():
+    """reference cli.py simulate (4 modes, --dump-image) and compare, run
+    through the reference's own main() on files written here; inputs and
+    outputs land in tests/golden/cli/."""
+    import shutil
+    import tempfile
+    from moverb import cli as rcli, io_formats as rio
+    out_dir = os.path.join(HERE, "cli")
+    os.makedirs(out_dir, exist_ok=True)
+    rate = 16000.0
+    n = 4000
+    t = np.arange(n) / rate
+    pos = np.stack([1.0 + 0.8 * t, 3.0 + 0.3 * t, np.full(n, 2.0)], axis=1)
+    rng = np.random.default_rng(21)
+    x = (0.5 * np.sin(2 * np.pi * 440.0 * t) + 0.2 * rng.standard_normal(n)).astype(np.float32)
+    tmp = tempfile.mkdtemp()
+    rio.write_trajectory(os.path.join(tmp, "path.txt"), Trajectory(rate=rate, positions=pos))
+    rio.write_wav(os.path.join(tmp, "dry.wav"), rate, x)
+    cfg = ("room.dims = 5 6 4\nroom.reflection = 0.9\nmic.pos = 1.25 2.6 2.75\n"
+           "traj.file = {tmp}/path.txt\nsynth.rate = 16000\nsynth.N = 64\nsynth.K = 1\n"
+           "synth.max_order = 3\n")
+    with open(os.path.join(tmp, "run.cfg"), "w") as fh:
+        fh.write(cfg.format(tmp=tmp))
+    for mode, extra in (("hierarchical", ["--dump-image", "7", "--dump-csv",
+                                          os.path.join(tmp, "image7.csv")]),
+                        ("oracle", []), ("splice", ["--crossfade", "64"]), ("static", [])):
+        rc = rcli.main(["simulate", "--config", os.path.join(tmp, "run.cfg"), "--mode", mode,
+                        "--in", os.path.join(tmp, "dry.wav"),
+                        "--out", os.path.join(tmp, f"{mode}.wav")] + extra)
+        assert rc == 0, mode
+    rc = rcli.main(["compare", os.path.join(tmp, "hierarchical.wav"), os.path.join(tmp, "oracle.wav"),
+                    "--report", os.path.join(tmp, "report.txt")])
+    assert rc == 0
+    for name in ("path.txt", "dry.wav", "hierarchical.wav", "oracle.wav", "splice.wav",
+                 "static.wav", "image7.csv", "report.txt"):
+        shutil.copy(os.path.join(tmp, name), os.path.join(out_dir, name))
+    with open(os.path.join(out_dir, "run.cfg"), "w") as fh:
+        fh.write(cfg.replace("{tmp}", "{dir}"))
+    print("cli fixtures written")
+
+
 if __name__ == "__main__":
     import sys as _sys
     if "--source-only" in _sys.argv:
         source_modulation_case()
     elif "--static-only" in _sys.argv:
         static_cases()
+    elif "--cli-only" in _sys.argv:
+        cli_cases()
     else:
+        cli_cases()
         static_cases()
         kernel_cases()
         render_cases()
