@@ -148,6 +148,33 @@ typedef struct mvb_coef32 {
     float g[8];  /* kappa * g_p, p = 1..8                                     */
 } mvb_coef32;
 
+/* Image classes of one job group (one class per decimation factor). */
+#define MVB_MAX_CLASSES 8
+typedef struct mvb_class_table {
+    int32_t n;                        /* classes, <= MVB_MAX_CLASSES            */
+    int32_t factor[MVB_MAX_CLASSES];  /* decimation factor N of the class       */
+    int32_t fit[MVB_MAX_CLASSES];     /* refit block index of N                 */
+    int32_t count[MVB_MAX_CLASSES];   /* images of the class per job            */
+    int64_t table[MVB_MAX_CLASSES];   /* offset of N's transposed table         */
+    int64_t sel_off[MVB_MAX_CLASSES]; /* this group's block in d_class_sel (N > 1) */
+} mvb_class_table;
+
+/* Image records of a group of G jobs sharing (max_order, tiers, image
+ * subset): image (g, s) -> d_images[img_base + g*S + s] from the enumerated
+ * room tables (d_tab_offset (R,S0,3), d_tab_sign (R,S0,3), d_tab_beta
+ * (R,S0), room_table.py canonical order).  d_img (S, 2+nC) int32 per image:
+ * canonical source index, class, and the number of earlier images in each
+ * class; d_job (G, 4+nC) int64 per job: room, T, job id, first coarse
+ * index, coarse path row per class.  Also writes the image selections:
+ * d_full_sel / d_dec_sel (factor 1 / > 1 images, row g of each block
+ * holding job g's images in order, at full_off / dec_off) and d_class_sel
+ * (per class blocks at classes->sel_off[c]). */
+int mvb_build_images(const double* d_tab_offset, const double* d_tab_sign, const double* d_tab_beta,
+                     int64_t S0, const int32_t* d_img, int64_t S, const int64_t* d_job, int64_t G,
+                     const mvb_class_table* h_classes, int64_t img_base, mvb_image* d_images,
+                     int32_t* d_full_sel, int64_t full_off, int32_t* d_dec_sel, int64_t dec_off,
+                     int32_t* d_class_sel, void* stream);
+
 /* Coarse distances of the n_sel images d_sel (factor > 1) on their coarse
  * paths -> d_coarse[image.coarse + k], k < K.  _kernels.py:54-62 arithmetic:
  * bitwise equal to distance_streams on decimate(traj, N).positions. */

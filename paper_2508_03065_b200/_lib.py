@@ -35,6 +35,7 @@ _SIGS = {
     "mvb_branch_filter": [P, I64, P, I64, I64, P, P],
     "mvb_image_count": [INT],
     "mvb_enumerate": [P, P, I64, INT, P, P, P, P, P, P, P],
+    "mvb_build_images": [P, P, P, I64, P, I64, P, I64, P, I64, P, P, I64, P, I64, P, P],
     "mvb_coarse_distances": [P, P, I64, P, P, P, P],
     "mvb_track_bounds": [P, I64, P, I64, P, P, P, DBL, P, P, P],
     "mvb_track_max": [P, P, I64, P, P, P, P, P, P, P],
@@ -55,6 +56,17 @@ _SIGS = {
 _RESTYPE = {"mvb_last_error": ctypes.c_char_p, "mvb_image_count": I64}
 
 IMAGE_BYTES, JOB_BYTES, WORK_BYTES, COEF_BYTES = 96, 136, 32, 48
+
+
+MAX_CLASSES = 8
+
+
+class ClassTable(ctypes.Structure):
+    """mvb_class_table (mvb.h): image classes of one job group."""
+
+    _fields_ = [("n", ctypes.c_int32), ("factor", ctypes.c_int32 * MAX_CLASSES),
+                ("fit", ctypes.c_int32 * MAX_CLASSES), ("count", ctypes.c_int32 * MAX_CLASSES),
+                ("table", ctypes.c_int64 * MAX_CLASSES), ("sel_off", ctypes.c_int64 * MAX_CLASSES)]
 
 
 class MvbError(RuntimeError):

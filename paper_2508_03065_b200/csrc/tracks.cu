@@ -325,7 +325,84 @@ __global__ void k_sort_keys(const mvb_image* __restrict__ images, const mvb_job*
 
 using namespace mvb;
 
+__global__ void k_build_images(const double* __restrict__ toff, const double* __restrict__ tsgn,
+                               const double* __restrict__ tbeta, int64_t S0,
+                               const int32_t* __restrict__ img, int64_t S,
+                               const int64_t* __restrict__ job, int64_t G,
+                               const mvb_class_table cls, int64_t img_base,
+                               mvb_image* __restrict__ out, int32_t* __restrict__ full_sel,
+                               int32_t* __restrict__ dec_sel, int32_t* __restrict__ class_sel) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= G * S) return;
+    const int64_t g = t / S, s = t - g * S;
+    const int nC = cls.n;
+    const int32_t* im = img + s * (2 + nC);
+    const int64_t* jb = job + g * (4 + nC);
+    const int64_t src = im[0];
+    const int c = im[1];
+    const int64_t room = jb[0], T = jb[1];
+    // coarse index: the job's first + the intervals of its earlier images
+    int64_t coarse = jb[3];
+    int full_rank = 0, dec_rank = 0;
+    for (int q = 0; q < nC; ++q) {
+        const int N = cls.factor[q];
+        if (N > 1) {
+            coarse += (int64_t)im[2 + q] * ((T + N - 1) / N);
+            dec_rank += im[2 + q];
+        } else {
+            full_rank += im[2 + q];
+        }
+    }
+    const int N = cls.factor[c];
+    const int64_t r = room * S0 + src;
+    mvb_image o;
+    o.off[0] = toff[3 * r + 0];
+    o.off[1] = toff[3 * r + 1];
+    o.off[2] = toff[3 * r + 2];
+    o.beta = tbeta[r];
+    o.sign[0] = (float)tsgn[3 * r + 0];
+    o.sign[1] = (float)tsgn[3 * r + 1];
+    o.sign[2] = (float)tsgn[3 * r + 2];
+    o.amp_num = (float)(o.beta / (4.0 * 3.141592653589793));
+    o.factor = N;
+    o.n_coarse = N > 1 ? (int32_t)((T + N - 1) / N) : 0;
+    o.coarse = coarse;
+    o.coef = coarse;  // one interval record per coarse sample
+    o.table = cls.table[c];
+    o.cpath = jb[4 + c];
+    o.job = (int32_t)jb[2];
+    o.fit = cls.fit[c];
+    const int64_t gi = img_base + t;
+    out[gi] = o;
+    if (N > 1) {
+        int dec_count = 0;
+        for (int q = 0; q < nC; ++q)
+            if (cls.factor[q] > 1) dec_count += cls.count[q];
+        dec_sel[g * dec_count + dec_rank] = (int32_t)gi;
+        class_sel[cls.sel_off[c] + g * cls.count[c] + im[2 + c]] = (int32_t)gi;
+    } else {
+        full_sel[g * cls.count[c] + full_rank] = (int32_t)gi;
+    }
+}
+
 extern "C" {
+
+int mvb_build_images(const double* toff, const double* tsgn, const double* tbeta, int64_t S0,
+                     const int32_t* img, int64_t S, const int64_t* job, int64_t G,
+                     const mvb_class_table* classes, int64_t img_base, mvb_image* images,
+                     int32_t* full_sel, int64_t full_off, int32_t* dec_sel, int64_t dec_off,
+                     int32_t* class_sel, void* stream) {
+    if (S < 0 || G < 0 || S0 < 1 || !classes || classes->n < 1 || classes->n > MVB_MAX_CLASSES)
+        return fail(MVB_EINVAL, "build_images: bad sizes / classes");
+    if (S == 0 || G == 0) return MVB_OK;
+    if (!toff || !tsgn || !tbeta || !img || !job || !images)
+        return fail(MVB_EINVAL, "build_images: null");
+    if (img_base + G * S > 0x7fffffff) return fail(MVB_EINVAL, "build_images: > 2^31 images");
+    k_build_images<<<grid_for(G * S, 256), 256, 0, as_stream(stream)>>>(
+        toff, tsgn, tbeta, S0, img, S, job, G, *classes, img_base, images,
+        full_sel ? full_sel + full_off : nullptr, dec_sel ? dec_sel + dec_off : nullptr, class_sel);
+    return check_launch("build_images");
+}
 
 int mvb_coarse_distances(const mvb_image* images, const int32_t* sel, int64_t n_sel,
                          const mvb_job* jobs, const double* paths, double* coarse, void* stream) {

@@ -371,9 +371,10 @@ class Geometry:
     def _decimate_paths(self):
         """Fill the coarse path slots with pos[::N] (and receiver[::N]).  The
         reference's anti-alias decision (low-pass only when Nyquist_out <
-        bandwidth < 2 Nyquist_out, trajectory.py:279-298) is taken and applied
-        on the device for all paths of one length at once (decimate_batch):
-        no host round trip, one index_copy per (length, factor)."""
+        bandwidth < 2 Nyquist_out, trajectory.py:279-298) is measured on the
+        device for all paths of one length at once (bandwidth_batch), and the
+        low-pass runs only for the paths it selects; one index_copy per
+        (length, factor)."""
         jobs, dev = self.jobs, self.dev
         groups = {}  # (T, rate) -> {row0: position}
         uses = {}  # (T, rate, N) -> list of (position, destination row)
@@ -394,7 +395,10 @@ class Geometry:
                 x = self.paths[starts[0]:starts[0] + G * T].view(G, T, 3)  # contiguous run
             else:
                 x = torch.stack([self.paths[r0:r0 + T] for r0 in starts])  # (G, T, 3)
-            bw = bandwidth_batch(x, rate)  # once for all factors
+            # once for all factors; the decision comes to the host (the queue
+            # holds only the path upload here, so the wait is ~the FFT) and
+            # the low-pass runs only for paths whose bandwidth needs it
+            bw = bandwidth_batch(x, rate).cpu().numpy()
             for (T2, rate2, N), lst in uses.items():
                 if (T2, rate2) != (T, rate):
                     continue
@@ -405,12 +409,17 @@ class Geometry:
                 self.paths.index_copy_(0, dst, coarse[info[:, 0]].reshape(-1, 3))
 
     def _build_images(self):
+        """Image records of every job: rooms enumerated on the device (one
+        launch per group of jobs sharing max_order / tiers / subset), then
+        one mvb_build_images launch per group writes the records and the
+        factor selections straight into their final buffers."""
         jobs, dev = self.jobs, self.dev
         nJ = len(jobs)
-        # factor constants (transposed tables + refits) shared by the batch
+        st = stream_handle(dev)
+        # factor constants (transposed tables) shared by the batch
         factors = sorted({int(N) for jb in jobs for _, N in jb.tiers if int(N) > 1})
         self.factors = factors
-        tab_parts, fit_parts = [], []
+        tab_parts = []
         self.table_off, self.fit_idx = {}, {}
         off = 0
         for q, N in enumerate(factors):
@@ -419,25 +428,83 @@ class Geometry:
             tab_parts.append(cst["tableT"].reshape(-1))
             off += cst["tableT"].numel()
             self.fit_idx[N] = q
-            fit_parts.append(cst["fit"].reshape(-1))
         self.tables = torch.cat(tab_parts) if tab_parts else torch.zeros(1, dtype=torch.float64, device=dev)
-        self.fits = torch.cat(fit_parts) if fit_parts else torch.zeros(1, dtype=torch.float64, device=dev)
-        # groups of jobs with identical enumeration / tier layout
         groups = {}
         for j, jb in enumerate(jobs):
             sub = None if jb.image_index is None else tuple(np.asarray(jb.image_index).tolist())
             key = (int(jb.max_order), tuple((int(a), int(b)) for a, b in jb.tiers), sub)
             groups.setdefault(key, []).append(j)
+        self.n_enum_launches = 2 * len(groups)
         self.img_off = np.zeros(nJ, np.int64)
         self.n_img = np.zeros(nJ, np.int64)
         self.evals = np.zeros(nJ, np.int64)
-        blocks, dec_sel, full_sel = [], [], []
-        by_factor = {}
-        img_base = 0
-        coarse_base = 0
-        self.order_of_job = [None] * nJ
-        self.n_enum_launches = len(groups)
+        # pass 1 (host): classes, per-image prefix counts, sizes
+        plans = []
+        img_base = coarse_base = n_full = n_dec = 0
+        n_cls = {N: 0 for N in factors}
         for (max_order, tiers, sub), members in groups.items():
+            order_np = np.repeat(np.arange(max_order + 1),
+                                 [1] + [4 * o * o + 2 for o in range(1, max_order + 1)])
+            src = np.arange(order_np.size, dtype=np.int64)
+            if sub is not None:
+                src = np.asarray(sub, np.int64)
+                order_np = order_np[src]
+            S = int(order_np.size)
+            fac_np = np.ones(S, np.int64)
+            prev = -1
+            for mo, N in tiers:
+                fac_np[(order_np > prev) & (order_np <= mo)] = N
+                prev = mo
+            classes = sorted(set(fac_np.tolist()))
+            if len(classes) > _lib.MAX_CLASSES:
+                raise ValueError(f"at most {_lib.MAX_CLASSES} distinct decimation factors")
+            cidx = np.searchsorted(np.asarray(classes), fac_np)
+            onehot = (cidx[:, None] == np.arange(len(classes))[None, :]).astype(np.int32)
+            pref = np.cumsum(onehot, axis=0) - onehot  # earlier images per class
+            counts = onehot.sum(axis=0)
+            G = len(members)
+            Tj = self.T[members].astype(np.int64)
+            Kc = np.array([[-(-int(T) // N) if N > 1 else 0 for N in classes] for T in Tj],
+                          np.int64).reshape(G, len(classes))
+            per_job = (Kc * counts[None, :]).sum(axis=1)
+            kbase = coarse_base + np.concatenate([[0], np.cumsum(per_job)[:-1]]).astype(np.int64)
+            ct = _lib.ClassTable()
+            ct.n = len(classes)
+            for q, N in enumerate(classes):
+                ct.factor[q] = int(N)
+                ct.fit[q] = self.fit_idx.get(int(N), 0)
+                ct.count[q] = int(counts[q])
+                ct.table[q] = self.table_off.get(int(N), 0)
+                if N > 1:
+                    ct.sel_off[q] = n_cls[int(N)]
+                    n_cls[int(N)] += G * int(counts[q])
+            full_cnt = sum(int(counts[q]) for q, N in enumerate(classes) if N == 1)
+            plans.append(dict(max_order=max_order, sub=sub, members=members, S=S, src=src,
+                              cidx=cidx, pref=pref, classes=classes, kbase=kbase, ct=ct,
+                              img_base=img_base, full_off=n_full, dec_off=n_dec))
+            for g, j in enumerate(members):
+                self.img_off[j] = img_base + g * S
+                self.n_img[j] = S
+                T = int(self.T[j])
+                self.evals[j] = int(sum(int(counts[q]) * (T if N == 1 else -(-T // int(N)))
+                                        for q, N in enumerate(classes)))
+            img_base += G * S
+            coarse_base += int(per_job.sum())
+            n_full += G * full_cnt
+            n_dec += G * (S - full_cnt)
+        # class selections: one region per factor, groups in order inside it
+        cls_base, acc = {}, 0
+        for N in factors:
+            cls_base[N] = acc
+            acc += n_cls[N]
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.images = torch.empty(max(img_base, 1), IMG_COLS, dtype=torch.int64, device=dev)
+        self.full_sel = torch.empty(n_full, **i32)
+        self.dec_sel = torch.empty(n_dec, **i32)
+        class_sel = torch.empty(max(acc, 1), **i32)
+        # pass 2 (device): enumerate each group's rooms, build its records
+        for pl in plans:
+            members = pl["members"]
             room_key, rooms, member_room = {}, [], []
             for j in members:
                 d = np.asarray(jobs[j].dims, dtype=np.float64).reshape(3)
@@ -449,92 +516,29 @@ class Geometry:
                     rooms.append((d, w))
                 member_room.append(room_key[k])
             tab = image_table(np.stack([r[0] for r in rooms]), np.stack([r[1] for r in rooms]),
-                              max_order, dev)
-            sel = None if sub is None else h2d(np.asarray(sub, np.int64), dev)
-            # canonical order is sorted by reflection order, 4o^2+2 images per
-            # order: tiers and interval counts follow on the host, no sync
-            order_np = np.repeat(np.arange(max_order + 1),
-                                 [1] + [4 * o * o + 2 for o in range(1, max_order + 1)])
-            if sub is not None:
-                order_np = order_np[np.asarray(sub, np.int64)]
-            order = tab.order[0] if sel is None else tab.order[0][sel]
-            S = int(order_np.size)
-            fac_np = np.ones(S, np.int64)
-            prev = -1
-            for mo, N in tiers:
-                fac_np[(order_np > prev) & (order_np <= mo)] = N
-                prev = mo
-            G = len(members)
-            ridx = h2d(np.asarray(member_room, np.int64), dev)
-            offset = tab.offset[ridx]
-            sign = tab.sign[ridx]
-            beta = tab.beta[ridx]
-            if sel is not None:
-                offset, sign, beta = offset[:, sel], sign[:, sel], beta[:, sel]
-            # per-image (S) host arrays, per-job (G) arrays; (G, S) fields are
-            # formed on the device by broadcasting (no per-image H2D of G*S)
-            facs = sorted(set(fac_np.tolist()))
-            fidx_np = np.searchsorted(np.asarray(facs), fac_np)
-            table_np = np.asarray([self.table_off.get(N, 0) for N in facs], np.int64)[fidx_np]
-            fit_np = np.asarray([self.fit_idx.get(N, 0) for N in facs], np.int64)[fidx_np]
-            cpath_np = np.asarray([[self.cpath.get((j, N), 0) for N in facs] for j in members],
-                                  np.int64)  # (G, nF)
-            Tj_np = self.T[members]
-            s_info = h2d(np.stack([fac_np, table_np, fit_np, fidx_np]), dev)  # (4, S)
-            fac, table, fit, fidx = s_info[0], s_info[1], s_info[2], s_info[3]
-            g_info = h2d(np.concatenate([Tj_np, np.asarray(members, np.int64)]), dev)
-            Tj, jid = g_info[:G], g_info[G:]
-            cpath = h2d(cpath_np, dev)[:, fidx]  # (G, S)
-            Nf = fac[None, :].expand(G, S)
-            K = torch.where(Nf > 1, (Tj[:, None] + Nf - 1) // Nf, torch.zeros_like(Nf))
-            cnt = K.reshape(-1)
-            coarse_off = coarse_base + torch.cumsum(cnt, 0) - cnt
-            counts = {N: int((fac_np == N).sum()) for N in facs}
-            coarse_base += int(sum(c * int(np.sum(-(-Tj_np // N))) for N, c in counts.items() if N > 1))
-            blk = torch.zeros(G, S, IMG_COLS, dtype=torch.int64, device=dev)
-            f64 = blk.view(torch.float64)
-            f64[:, :, 0:3] = offset
-            f64[:, :, 3] = beta
-            f32 = blk[:, :, 4:6].view(torch.float32)
-            f32[:, :, 0:3] = sign.to(torch.float32)
-            f32[:, :, 3] = (beta / FOUR_PI).to(torch.float32)
-            i32 = blk[:, :, 6:7].view(torch.int32)
-            i32[:, :, 0] = Nf.to(torch.int32)
-            i32[:, :, 1] = K.to(torch.int32)
-            blk[:, :, 7] = coarse_off.reshape(G, S)
-            blk[:, :, 8] = coarse_off.reshape(G, S)  # one interval record per coarse sample
-            blk[:, :, 9] = table[None, :]
-            blk[:, :, 10] = cpath
-            j32 = blk[:, :, 11:12].view(torch.int32)
-            j32[:, :, 0] = jid.to(torch.int32)[:, None]
-            j32[:, :, 1] = fit.to(torch.int32)[None, :]
-            blocks.append(blk.reshape(G * S, IMG_COLS))
-            # selections: image positions of one factor, for every job of the group
-            jbase = img_base + S * torch.arange(G, device=dev, dtype=torch.int64)[:, None]
-
-            def positions(mask):
-                idx = h2d(np.nonzero(mask)[0].astype(np.int64), dev)
-                return (jbase + idx[None, :]).reshape(-1).to(torch.int32)
-
-            dec_sel.append(positions(fac_np > 1))
-            full_sel.append(positions(fac_np == 1))
-            for N in facs:
+                              pl["max_order"], dev)
+            ct, classes, S = pl["ct"], pl["classes"], pl["S"]
+            for q, N in enumerate(classes):
                 if N > 1:
-                    by_factor.setdefault(int(N), []).append(positions(fac_np == N))
-            for g, j in enumerate(members):
-                self.img_off[j] = img_base + g * S
-                self.n_img[j] = S
-                T = int(self.T[j])
-                self.evals[j] = int(sum(c * (T if N == 1 else -(-T // int(N)))
-                                        for N, c in counts.items()))
-                self.order_of_job[j] = order
-            img_base += G * S
-        self.images = torch.cat(blocks) if len(blocks) > 1 else blocks[0]
+                    ct.sel_off[q] += cls_base[int(N)]
+            img_tab = np.concatenate([pl["src"][:, None], pl["cidx"][:, None], pl["pref"]],
+                                     axis=1).astype(np.int32)  # (S, 2 + nC) int32 (mvb.h)
+            cp = np.asarray([[self.cpath.get((j, int(N)), 0) for N in classes] for j in members],
+                            np.int64).reshape(len(members), len(classes))
+            job_tab = np.concatenate([np.asarray(member_room, np.int64)[:, None],
+                                      self.T[members].astype(np.int64)[:, None],
+                                      np.asarray(members, np.int64)[:, None], pl["kbase"][:, None], cp],
+                                     axis=1)
+            img_dev = h2d(np.ascontiguousarray(img_tab), dev)
+            job_dev = h2d(np.ascontiguousarray(job_tab), dev)
+            _lib.call("mvb_build_images", ptr(tab.offset), ptr(tab.sign), ptr(tab.beta), tab.count,
+                      ptr(img_dev), S, ptr(job_dev), len(members), ctypes.byref(ct), pl["img_base"],
+                      ptr(self.images), ptr(self.full_sel), pl["full_off"], ptr(self.dec_sel),
+                      pl["dec_off"], ptr(class_sel), st)
         self.n_images = img_base
         self.n_coarse_total = coarse_base
-        self.dec_sel = torch.cat(dec_sel).to(torch.int32)
-        self.sel_by_factor = {N: torch.cat(v) for N, v in by_factor.items()}
-        self.full_sel = torch.cat(full_sel).to(torch.int32)
+        self.sel_by_factor = {N: class_sel[cls_base[N]:cls_base[N] + n_cls[N]] for N in factors
+                              if n_cls[N]}
         if self.full_sel.numel() > 65535:
             raise ValueError("more than 65535 full-rate images in one batch")
 

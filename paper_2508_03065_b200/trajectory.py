@@ -170,6 +170,16 @@ def decimate_batch(x: torch.Tensor, rate: float, factor: int, bw: torch.Tensor |
     nyq = 0.5 * rate / factor
     if bw is None:
         bw = bandwidth_batch(x, rate)
+    if isinstance(bw, np.ndarray):  # decided on the host: low-pass only the paths that need it
+        need = np.nonzero((bw > nyq) & (bw < 2.0 * nyq))[0]
+        if need.size == 0:
+            return raw
+        if need.size == x.shape[0]:
+            return lowpass_batch(x, rate, 0.9 * nyq)[:, ::factor]
+        idx = torch.as_tensor(need, device=x.device)
+        out = raw.clone()
+        out[idx] = lowpass_batch(x[idx], rate, 0.9 * nyq)[:, ::factor]
+        return out
     use = ((bw > nyq) & (bw < 2.0 * nyq))[:, None, None]
     lp = lowpass_batch(x, rate, 0.9 * nyq)[:, ::factor]
     return torch.where(use, lp, raw)

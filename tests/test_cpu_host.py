@@ -162,3 +162,11 @@ def test_parallel_copy_chunks_and_casts():
     parallel_copy([(dst_big, big), (dst_small, small)], chunk_bytes=1 << 20)
     assert np.array_equal(dst_big, big)
     assert np.array_equal(dst_small, small.astype(np.float64))
+
+
+def test_class_table_layout():
+    import ctypes
+    from paper_2508_03065_b200 import _lib
+    # mvb_class_table: int32 n + 3 x int32[8] (100 B) padded to 104, + 2 x int64[8]
+    assert ctypes.sizeof(_lib.ClassTable) == 104 + 128
+    assert _lib.ClassTable.table.offset == 104
