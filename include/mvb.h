@@ -224,10 +224,10 @@ int mvb_sort_keys(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jo
  * in the centred basis (mu - 1/2)^k, zero branches k >= M1) of n_sig dry
  * signals in one launch: signal q is d_x_all[sig_off[q] ..] of length
  * sig_len[q] (<= max_len), its sample m < len + L - 1 goes to global row
- * sig_row0[q] + m (device arrays).  Layout: rows in blocks of 64; block b
- * holds nb/4 planes of 64 float4 (plane p = branches 4p..4p+3), i.e. row r
- * plane p is float4 number r + (nb/4 - 1)(r & ~63) + 64 p.  Rows outside
- * are left as the caller zeroed them.  L <= 128; rows < 2^31. */
+ * sig_row0[q] + m (device arrays).  Layout: row r = the nb branch values
+ * contiguous, row stride 16 B for nb = 4, else 32 B * ceil(nb / 8) (nb = 12
+ * is padded to 16 floats); rows outside are left as the caller zeroed them.
+ * L <= 128; rows < 2^31. */
 int mvb_branch_records_f32(const float* d_x_all, const int64_t* d_sig_off,
                            const int64_t* d_sig_len, const int64_t* d_sig_row0, int64_t n_sig,
                            int64_t max_len, const double* d_cbranch, int M1, int L, int nb,

@@ -2,15 +2,13 @@
 //
 // Fast path (fp32 I/O, the B200 roofline path)
 //   k_branch_records_f32  v'_k = x (*) c'_k for the centred Farrow bank.
-//                         Record layout: rows (input samples, zero-padded on
-//                         both sides so the gather needs no bounds test --
-//                         the reference's `valid` window reads zeros) in
-//                         blocks of 64; a block stores plane 0 (branches
-//                         0..3, one float4 per row) for its 64 rows, then
-//                         plane 1 (branches 4..7), ...  A warp's gather of 32
-//                         consecutive rows is one coalesced 512-byte load per
-//                         plane, and plane p sits at an immediate +1 KiB*p
-//                         from plane 0, so one IMAD.WIDE addresses a row.
+//                         Record layout: one row per input sample (zero-padded
+//                         on both sides so the gather needs no bounds test --
+//                         the reference's `valid` window reads zeros), the
+//                         row's 4 NP branch values contiguous (32 B for the
+//                         8-branch bank): one IMAD.WIDE and one 256-bit load
+//                         (LDG.256) per update; a warp's 32 consecutive rows
+//                         are one coalesced 1 KiB access.
 //   k_synth_f32           one CTA per (job, 32*U-sample tile, image chunk);
 //                         8 warps walk the chunk's delay-sorted images, lane
 //                         l of a warp owns samples n0 + 32u + l, u < U.  Per
@@ -38,20 +36,25 @@ namespace mvb {
 // ---------------------------------------------------------------------------
 // record layout
 
-constexpr int REC_BLOCK = 64;  // rows per block
-
-// float4 index of plane 0 of row r (plane p adds REC_BLOCK * p)
+// a record row holds the nb = 4 NP branch values of one input sample,
+// contiguous and padded to a whole number of 32-byte units when NP > 1, so a
+// row is one (NP = 1) 16-byte or NP/2 (rounded up) 32-byte loads
 template <int NP>
-__host__ __device__ __forceinline__ unsigned rec_index(unsigned r) {
-    return r + (NP - 1) * (r & ~(unsigned)(REC_BLOCK - 1));
-}
+__host__ __device__ constexpr int row_f4() { return NP == 1 ? 1 : 2 * ((NP + 1) / 2); }
 
-// &base[rec_index(r)] as one IMAD.WIDE.U32
+// &base[row r] as one IMAD.WIDE.U32
 template <int NP>
 __device__ __forceinline__ const float4* rec_row(const float4* base, unsigned r) {
     const float4* p;
-    asm("mad.wide.u32 %0, %1, 16, %2;" : "=l"(p) : "r"(rec_index<NP>(r)), "l"(base));
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(r), "n"(16 * row_f4<NP>()), "l"(base));
     return p;
+}
+
+// 32-byte read-only load (sm_100 LDG.256)
+__device__ __forceinline__ void ldg8(float4& a, float4& b, const float4* p) {
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(p));
 }
 
 // One launch for every distinct dry signal of a batch: blockIdx.y selects
@@ -91,10 +94,10 @@ __global__ void k_branch_records_f32(const float* __restrict__ x_all,
 #pragma unroll
         for (int k = 0; k < NB; ++k) acc[k] = fmaf(sc[k * L + j], xv, acc[k]);
     }
-    float4* o = reinterpret_cast<float4*>(rec) + rec_index<NP>((unsigned)(row0 + m));
+    float4* o = reinterpret_cast<float4*>(rec) + (size_t)(row0 + m) * row_f4<NP>();
 #pragma unroll
     for (int p = 0; p < NP; ++p)
-        o[REC_BLOCK * p] = make_float4(acc[4 * p], acc[4 * p + 1], acc[4 * p + 2], acc[4 * p + 3]);
+        o[p] = make_float4(acc[4 * p], acc[4 * p + 1], acc[4 * p + 2], acc[4 * p + 3]);
 }
 
 // ---------------------------------------------------------------------------
@@ -112,8 +115,13 @@ __device__ __forceinline__ float gather_horner(const float4* __restrict__ R, uns
     const float2 yy = f2(y, y);
     const float4* a = rec_row<NP>(R, row);
     float4 v[NP];
+    if (NP == 1) {
+        v[0] = __ldg(a);
+    } else {
 #pragma unroll
-    for (int p = 0; p < NP; ++p) v[p] = __ldg(a + REC_BLOCK * p);
+        for (int p = 0; p + 1 < NP; p += 2) ldg8(v[p], v[p + 1], a + p);
+        if (NP % 2) v[NP - 1] = __ldg(a + NP - 1);
+    }
     float2 q = f2(v[NP - 1].z, v[NP - 1].w);
     q = __ffma2_rn(q, yy, f2(v[NP - 1].x, v[NP - 1].y));
 #pragma unroll

@@ -759,10 +759,10 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
         back = front + TILE + PAD_MARGIN
         bases[k] = (rec_rows, front)
         rec_rows += front + sig_len[k] + L - 1 + back
-    rec_rows = -(-rec_rows // 64) * 64  # whole 64-row blocks (mvb.h record layout)
     if rec_rows + int(out_len.max()) + L >= 2**31 - 0x4B400000:
         raise ValueError("batch too large for 32-bit record rows; split it")
-    rec = torch.zeros(rec_rows * nb, dtype=torch.float32, device=dev)
+    row_floats = 4 if nb == 4 else 8 * -(-nb // 8)  # mvb.h record layout
+    rec = torch.zeros(rec_rows * row_floats, dtype=torch.float32, device=dev)
     ukeys = list(uniq)
     lens = np.asarray([sig_len[k] for k in ukeys], np.int64)
     if len(ukeys) == 1:
