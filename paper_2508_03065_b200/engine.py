@@ -212,6 +212,16 @@ class _BulkStager:
 
 
 _STAGER = _BulkStager()
+_SIDE = {}
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    """Per-device side stream for input staging that must not queue behind
+    the current stream."""
+    key = str(dev)
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=dev)
+    return _SIDE[key]
 
 
 def d2h(t: torch.Tensor) -> np.ndarray:
@@ -264,7 +274,12 @@ def pack_jobs(rows: list) -> np.ndarray:
 class Geometry:
     """Device-side hierarchical tracks of a batch of jobs (prepare stage)."""
 
-    def __init__(self, jobs: list, device=None):
+    def __init__(self, jobs: list, device=None, inputs_ready=None):
+        """`inputs_ready`: optional CUDA event after which every device
+        tensor of `jobs` is final.  With it, the paths are staged and their
+        bandwidths measured on a side stream that waits only for that event,
+        so planning this batch does not queue behind earlier work on the
+        current stream (e.g. the previous batch's synthesis)."""
         if not jobs:
             raise ValueError("no jobs")
         self.dev = dev = require_cuda(device)
@@ -312,12 +327,21 @@ class Geometry:
                     K = -(-int(self.T[j]) // N)
                     self.cpath[(j, N)] = row
                     row += K * (1 + int(self.moving[j]))
-        self.paths = torch.empty(max(row, 1), 3, dtype=torch.float64, device=dev)
-        if host_parts:
-            _STAGER.upload(host_parts, self.paths)
-        for r0, p in dev_parts:
-            self.paths[r0:r0 + p.shape[0]].copy_(p)
-        self._decimate_paths()
+        main = torch.cuda.current_stream(dev)
+        side = _side_stream(dev) if inputs_ready is not None else main
+        if side is not main:
+            side.wait_event(inputs_ready)
+        with torch.cuda.stream(side):
+            self.paths = torch.empty(max(row, 1), 3, dtype=torch.float64, device=dev)
+            if host_parts:
+                _STAGER.upload(host_parts, self.paths)
+            for r0, p in dev_parts:
+                self.paths[r0:r0 + p.shape[0]].copy_(p)
+            path_groups, bws = self._path_bandwidths(main)  # host waits for `side` only
+        if side is not main:
+            main.wait_stream(side)
+            self.paths.record_stream(main)
+        self._decimate_paths(path_groups, bws)
         # ---- image table ----------------------------------------------------
         self._build_images()
         # ---- job table (geometry fields; render fills the rest) -------------
@@ -368,14 +392,11 @@ class Geometry:
         return self._dmax
 
     # ------------------------------------------------------------------------
-    def _decimate_paths(self):
-        """Fill the coarse path slots with pos[::N] (and receiver[::N]).  The
-        reference's anti-alias decision (low-pass only when Nyquist_out <
-        bandwidth < 2 Nyquist_out, trajectory.py:279-298) is measured on the
-        device for all paths of one length at once (bandwidth_batch), and the
-        low-pass runs only for the paths it selects; one index_copy per
-        (length, factor)."""
-        jobs, dev = self.jobs, self.dev
+    def _path_bandwidths(self, consumer):
+        """Paths that need decimation, grouped by (length, rate), and their
+        measured bandwidths (trajectory.py:316-339) on the host: one batched
+        FFT per group, one small device->host copy (the only wait)."""
+        jobs = self.jobs
         groups = {}  # (T, rate) -> {row0: position}
         uses = {}  # (T, rate, N) -> list of (position, destination row)
         for (j, N), dst in self.cpath.items():
@@ -388,6 +409,7 @@ class Geometry:
             for r0, d in srcs:
                 pos = g.setdefault(r0, len(g))
                 uses.setdefault((T, rate, N), []).append((pos, d))
+        out, bws = [], []
         for (T, rate), rows in groups.items():
             starts = sorted(rows, key=rows.get)
             G = len(starts)
@@ -395,10 +417,24 @@ class Geometry:
                 x = self.paths[starts[0]:starts[0] + G * T].view(G, T, 3)  # contiguous run
             else:
                 x = torch.stack([self.paths[r0:r0 + T] for r0 in starts])  # (G, T, 3)
-            # once for all factors; the decision comes to the host (the queue
-            # holds only the path upload here, so the wait is ~the FFT) and
-            # the low-pass runs only for paths whose bandwidth needs it
-            bw = bandwidth_batch(x, rate).cpu().numpy()
+                x.record_stream(consumer)  # read again by the decimation
+            out.append((T, rate, x, uses))
+            bws.append(bandwidth_batch(x, rate))
+        host = torch.cat(bws).cpu().numpy() if bws else np.zeros(0)
+        split, q = [], 0
+        for _, _, x, _ in out:
+            split.append(host[q:q + x.shape[0]])
+            q += x.shape[0]
+        return out, split
+
+    def _decimate_paths(self, path_groups, bws):
+        """Fill the coarse path slots with pos[::N] (and receiver[::N]).  The
+        reference's anti-alias decision (low-pass only when Nyquist_out <
+        bandwidth < 2 Nyquist_out, trajectory.py:279-298) uses the measured
+        bandwidths; the low-pass runs only for the paths it selects; one
+        index_copy per (length, factor)."""
+        dev = self.dev
+        for (T, rate, x, uses), bw in zip(path_groups, bws):
             for (T2, rate2, N), lst in uses.items():
                 if (T2, rate2) != (T, rate):
                     continue

@@ -390,10 +390,13 @@ def scene_jobs(scenes, channels=None) -> list:
     return jobs
 
 
-def render_jobs(jobs, f, precision="fp32", shard=None, signals=None, timing=None):
+def render_jobs(jobs, f, precision="fp32", shard=None, signals=None, timing=None,
+                inputs_ready=None):
     """Geometry + render of a job batch; returns engine.RenderResult
-    (device output, per-job offsets/lengths, update count, launches)."""
-    geom = engine.Geometry(jobs)
+    (device output, per-job offsets/lengths, update count, launches).
+    `inputs_ready` (optional CUDA event): the jobs' device tensors are final
+    once it completes -- lets planning overlap earlier work on the stream."""
+    geom = engine.Geometry(jobs, inputs_ready=inputs_ready)
     sig = signals if signals is not None else [jb.s for jb in jobs]
     keys = [engine._key(jb.signal_key, jb.s) for jb in jobs]
     res = engine.render(geom, sig, f, precision=precision, shard=shard, signal_keys=keys,
