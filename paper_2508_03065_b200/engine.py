@@ -28,6 +28,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -37,11 +38,9 @@ from . import _lib
 from ._dev import ptr, require_cuda, stream_handle
 from .farrow import as_filter, centered_branches
 from .parallel import image_slice
-from .room import image_count, image_table
+from .room import image_table
 from .trajectory import (bandwidth_batch, decimate_batch, device_constants, negative_mass,
                          phase_fit)
-
-import os
 
 SYNTH_U = 16  # steps per lane (mvb_synthesize_f32 u_steps)
 TILE = 32 * SYNTH_U  # output samples per CTA

@@ -28,8 +28,7 @@ import torch
 
 from . import engine
 from .farrow import as_filter
-from .room import Room, as_mic, image_count, image_table
-from .trajectory import Trajectory
+from .room import as_mic, image_count, image_table
 
 SUMMATION_BLOCK = 32
 

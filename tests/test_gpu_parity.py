@@ -12,7 +12,6 @@ import pytest
 from conftest import golden, rel_err
 from oracle import oracle as orc
 from paper_2508_03065_b200 import workloads
-from paper_2508_03065_b200.farrow import hann_sinc
 
 pytestmark = pytest.mark.gpu
 
