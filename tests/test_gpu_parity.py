@@ -12,6 +12,7 @@ import pytest
 from conftest import golden, rel_err
 from oracle import oracle as orc
 from paper_2508_03065_b200 import workloads
+from paper_2508_03065_b200.farrow import hann_sinc
 
 pytestmark = pytest.mark.gpu
 
@@ -163,3 +164,36 @@ def test_decimate_on_device_matches_reference(kernels_golden, tag):
     np.testing.assert_allclose(tr.positions, g[f"dec_{tag}_out"], rtol=0, atol=1e-12)
     bw = bandwidth_estimate_dev(torch.as_tensor(pos, device="cuda"), 1000.0)
     assert bw == orc.bandwidth_estimate(pos, 1000.0)
+
+
+def test_mixed_job_groups_in_one_batch():
+    """Jobs with different max_order / tiers / image subsets in one batch
+    (several enumeration groups, class selections at group offsets) render
+    like the oracle, each on both engines."""
+    import dataclasses
+    from paper_2508_03065_b200 import engine
+    base = workloads.make_scenes("c2", duration=0.1)[0]
+    f = hann_sinc(32, 14)
+    variants = [dict(max_order=4, tiers=((1, 1), (4, 32))),
+                dict(max_order=6, tiers=((2, 1), (4, 64), (6, 128))),
+                dict(max_order=3, tiers=((3, 1),)),
+                dict(max_order=4, tiers=((1, 1), (4, 32)), image_index=np.arange(5, 60, 3))]
+    for precision, tol in (("fp64", 1e-13), ("fp32", FP32_TOL)):
+        sig = base.s.astype(np.float64 if precision == "fp64" else np.float32)
+        jobs = [engine.Job(s=sig, pos=base.pos, mic=base.mics[0], dims=base.dims, walls=base.walls,
+                           rate=base.rate, **v) for v in variants]
+        res = render_jobs(jobs, f, precision=precision)
+        for j, v in enumerate(variants):
+            im = orc.enumerate_images(base.dims, base.walls, v["max_order"])
+            if "image_index" in v:
+                im = im.take(v["image_index"])
+            ref = orc.OracleScene(base.s, base.pos, base.mics[0], base.dims, base.walls,
+                                  v["max_order"], v["tiers"], f.branches, base.rate,
+                                  images=im).render()
+            if precision == "fp32":
+                ref = orc.OracleScene(sig.astype(np.float64), base.pos, base.mics[0], base.dims,
+                                      base.walls, v["max_order"], v["tiers"], f.branches,
+                                      base.rate, images=im).render()
+            y = res.job(j).double().cpu().numpy()
+            assert y.size == ref.size, (precision, j)
+            assert rel_err(y, ref) <= tol, (precision, j)
