@@ -177,26 +177,39 @@ int mvb_build_images(const double* d_tab_offset, const double* d_tab_sign, const
 
 /* Coarse distances of the n_sel images d_sel (factor > 1) on their coarse
  * paths -> d_coarse[image.coarse + k], k < K.  _kernels.py:54-62 arithmetic:
- * bitwise equal to distance_streams on decimate(traj, N).positions. */
+ * bitwise equal to distance_streams on decimate(traj, N).positions.  Unless
+ * d_lb / d_ub are NULL, also the bounds of each image's track maximum over
+ * t < T (synth.py:201): lb = largest coarse sample (attained), ub = rigorous
+ * bound of the band-limited reconstruction, window max + negsum * window
+ * range (negsum: the upsampler's negative tap mass); d_lb / d_ub must be
+ * zero-initialised (maxima of track chunks merge atomically).  max_K: the
+ * largest K of the selection. */
 int mvb_coarse_distances(const mvb_image* d_images, const int32_t* d_sel, int64_t n_sel,
-                         const mvb_job* d_jobs, const double* d_paths, double* d_coarse,
+                         int64_t max_K, const mvb_job* d_jobs, const double* d_paths,
+                         double negsum, double* d_coarse, double* d_lb, double* d_ub,
                          void* stream);
 
-/* Per-image bounds of the track maximum over t < T (synth.py:201):
- * factor 1 images listed in d_full_sel: exact per-sample max (lb = ub);
- * others: lb = largest coarse sample (attained), ub = rigorous bound of the
- * band-limited reconstruction, window max + negsum * window range. */
-int mvb_track_bounds(const mvb_image* d_images, int64_t n_img, const int32_t* d_full_sel,
-                     int64_t n_full, const mvb_job* d_jobs, const double* d_paths,
-                     const double* d_coarse, double negsum, double* d_lb, double* d_ub,
-                     void* stream);
+/* Bounds of the track maximum of the factor-1 images d_full_sel: lb =
+ * exact distance at the first / middle / last sample, ub = the largest
+ * distance between the bounding boxes of the image path and the receiver.
+ * d_bbox: n_jobs x 65 x 12 doubles of scratch (path bounding boxes and
+ * their partial reductions). */
+int mvb_track_bounds(const mvb_image* d_images, const int32_t* d_full_sel, int64_t n_full,
+                     const mvb_job* d_jobs, int64_t n_jobs, const double* d_paths,
+                     double* d_bbox, double* d_lb, double* d_ub, void* stream);
 
-/* Exact track max of every job (d_dmax[n_jobs]): the reference's 65-tap
- * upsample is evaluated at every t < T only for the images whose ub reaches
- * the job's largest lb.  d_scratch: n_img + n_jobs int32. */
+/* Exact track max of every job (d_dmax[n_jobs]): only the images whose ub
+ * reaches the job's largest lb are evaluated at every t < T (exact distance
+ * for factor 1, the reference's 65-tap upsample otherwise).  d_scratch:
+ * n_img + n_jobs int32. */
 int mvb_track_max(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jobs,
-                  const double* d_coarse, const double* d_tables, const double* d_lb,
-                  const double* d_ub, int32_t* d_scratch, double* d_dmax, void* stream);
+                  const double* d_coarse, const double* d_tables, const double* d_paths,
+                  const double* d_lb, const double* d_ub, int32_t* d_scratch, double* d_dmax,
+                  void* stream);
+
+/* d_out[q] = d_images[d_idx[q]], q < n (delay-sorted image tables). */
+int mvb_gather_images(const mvb_image* d_images, const int64_t* d_idx, int64_t n,
+                      mvb_image* d_out, void* stream);
 
 /* Decimation decision helper (trajectory.py:316-339): for each of `rows`
  * power-spectrum rows of length F (fp64, contiguous), the first index whose

@@ -36,9 +36,10 @@ _SIGS = {
     "mvb_image_count": [INT],
     "mvb_enumerate": [P, P, I64, INT, P, P, P, P, P, P, P],
     "mvb_build_images": [P, P, P, I64, P, I64, P, I64, P, I64, P, P, I64, P, I64, P, P],
-    "mvb_coarse_distances": [P, P, I64, P, P, P, P],
-    "mvb_track_bounds": [P, I64, P, I64, P, P, P, DBL, P, P, P],
-    "mvb_track_max": [P, P, I64, P, P, P, P, P, P, P],
+    "mvb_coarse_distances": [P, P, I64, I64, P, P, DBL, P, P, P, P],
+    "mvb_track_bounds": [P, P, I64, P, I64, P, P, P, P, P],
+    "mvb_track_max": [P, P, I64, P, P, P, P, P, P, P, P],
+    "mvb_gather_images": [P, P, I64, P, P],
     "mvb_track_coeffs": [P, P, I64, I64, P, P, P, P, P],
     "mvb_sort_keys": [P, P, I64, I64, I64, I64, P, P, P, P],
     "mvb_branch_records_f32": [P, P, P, P, I64, I64, P, INT, INT, INT, P, P],

@@ -3,10 +3,10 @@
 // jobs of a batch in one launch; an image finds its job, paths and tier
 // constants through the fields of mvb_image.
 //
-//   k_coarse           coarse distances per (image, coarse sample): the
-//                      reference's distance arithmetic on pos[::N]
-//   k_bounds_coarse    per-image lower/upper bound of the upsampled max
-//   k_bounds_full      exact per-sample max of full-rate images
+//   k_coarse_bounds    coarse distances per (image, coarse sample) -- the
+//                      reference's distance arithmetic on pos[::N] -- fused
+//                      with the per-image bounds of the upsampled max
+//   k_path_bbox / k_bounds_full  bounds of the full-rate images' max
 //   k_select/k_exact_max  exact max over the images that can hold it
 //   k_coeffs           fast-path interval records: the 65-tap Kaiser
 //                      upsampler refit per coarse interval as a degree-8
@@ -47,19 +47,6 @@ __device__ __forceinline__ double block_max(double v, double* red) {
     return v;
 }
 
-// one block per selected image
-__global__ void k_coarse(const mvb_image* __restrict__ images, const int32_t* __restrict__ sel,
-                         const mvb_job* __restrict__ jobs, const double* __restrict__ paths,
-                         double* __restrict__ coarse) {
-    const mvb_image im = images[sel[blockIdx.x]];
-    const mvb_job& J = jobs[im.job];
-    const int64_t K = im.n_coarse;
-    const double* src = paths + 3 * im.cpath;
-    const double* mic = J.mic_moving ? src + 3 * K : paths + 3 * J.mic_off;
-    for (int64_t k = threadIdx.x; k < K; k += blockDim.x)
-        coarse[im.coarse + k] = image_distance(im, src + 3 * k, mic + (J.mic_moving ? 3 * k : 0));
-}
-
 // Decimated images: lb = largest coarse sample (attained to ~1e-12 m: the
 // phase-0 row of the table is a unit impulse up to sinc(integer) rounding);
 // ub = max over 64-sample segments s of M + negsum (M - m), M/m the max/min
@@ -84,53 +71,149 @@ __device__ __forceinline__ void seg_maxmin(const double* c, int64_t K, int64_t s
     warp_maxmin(M, m);
 }
 
-// One warp per image, 8 images per block; segments are reduced once with
-// coalesced loads and combined with their neighbours in a sliding window.
-__global__ void k_bounds_coarse(const mvb_image* __restrict__ images, int64_t n_img,
-                                const double* __restrict__ coarse, double negsum,
-                                double* __restrict__ lb, double* __restrict__ ub) {
+// Coarse distances of the decimated images (the reference's distance
+// arithmetic on pos[::N]) fused with their track bounds: a warp handles
+// CB_SEGS 64-sample segments of one image (blockIdx.y = chunk), computes and
+// writes them in order, reduces each segment's max / min with shuffles and
+// keeps a sliding window of three segments (the neighbours just outside the
+// chunk are recomputed, not written), so the coarse array is written once
+// and never re-read for the bounds.  Chunk maxima merge atomically into the
+// zero-initialised lb / ub.
+constexpr int CB_SEGS = 16;
+
+__global__ void k_coarse_bounds(const mvb_image* __restrict__ images, const int32_t* __restrict__ sel,
+                                int64_t n_sel, const mvb_job* __restrict__ jobs,
+                                const double* __restrict__ paths, double negsum,
+                                double* __restrict__ coarse, double* __restrict__ lb,
+                                double* __restrict__ ub) {
     const int lane = threadIdx.x & 31;
-    const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (i >= n_img) return;
+    const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (w >= n_sel) return;
+    const int32_t i = sel[w];
     const mvb_image im = images[i];
-    if (im.factor == 1) return;
-    const double* c = coarse + im.coarse;
     const int64_t K = im.n_coarse;
     const int64_t nseg = (K + 63) / 64;
+    const int64_t s0 = (int64_t)blockIdx.y * CB_SEGS;
+    if (s0 >= nseg) return;
+    const int64_t s1 = s0 + CB_SEGS < nseg ? s0 + CB_SEGS : nseg;
+    const mvb_job& J = jobs[im.job];
+    const double* src = paths + 3 * im.cpath;
+    const double* mic = J.mic_moving ? src + 3 * K : paths + 3 * J.mic_off;
+    const int64_t mstep = J.mic_moving ? 3 : 0;
+    double* c = coarse + im.coarse;
+    auto segment = [&](int64_t s, bool write, double& M, double& m) {
+        M = -DBL_MAX;
+        m = DBL_MAX;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t k = 64 * s + 32 * h + lane;
+            if (k < K) {
+                const double v = image_distance(im, src + 3 * k, mic + mstep * k);
+                if (write) c[k] = v;
+                M = fmax(M, v);
+                m = fmin(m, v);
+            }
+        }
+        warp_maxmin(M, m);
+    };
     double Mp = -DBL_MAX, mp = DBL_MAX, Mc, mc, Mn, mn;
-    seg_maxmin(c, K, 0, lane, Mc, mc);
+    if (s0 > 0) segment(s0 - 1, false, Mp, mp);
+    segment(s0, true, Mc, mc);
     double best_lb = 0.0, best_ub = 0.0;
-    for (int64_t s = 0; s < nseg; ++s) {
-        if (s + 1 < nseg) seg_maxmin(c, K, s + 1, lane, Mn, mn);
+    for (int64_t s = s0; s < s1; ++s) {
+        if (s + 1 < nseg) segment(s + 1, s + 1 < s1, Mn, mn);
         else { Mn = -DBL_MAX; mn = DBL_MAX; }
         const double M = fmax(Mp, fmax(Mc, Mn)), m = fmin(mp, fmin(mc, mn));
         best_lb = fmax(best_lb, Mc);
         best_ub = fmax(best_ub, M + negsum * (M - m) + 1e-9);
         Mp = Mc; mp = mc; Mc = Mn; mc = mn;
     }
-    if (lane == 0) {
-        lb[i] = best_lb;
-        ub[i] = best_ub;
+    if (lb && lane == 0) {
+        atomic_max_pos(lb + i, best_lb);
+        atomic_max_pos(ub + i, best_ub);
     }
 }
 
-// Full-rate images: exact per-sample max, merged atomically (lb/ub zeroed).
-__global__ void k_bounds_full(const mvb_image* __restrict__ images, const int32_t* __restrict__ sel,
-                              const mvb_job* __restrict__ jobs, const double* __restrict__ paths,
-                              double* __restrict__ lb, double* __restrict__ ub) {
+// Axis-aligned bounding boxes of every job's source path and receiver
+// (moving or fixed): bbox[j] = (src lo xyz, src hi xyz, mic lo xyz, mic hi
+// xyz).  BBOX_PARTS blocks per job reduce row ranges in one pass over all
+// three axes (partials after the n_jobs final boxes), k_bbox_reduce folds them.
+constexpr int BBOX_PARTS = 64;
+constexpr int BBOX_WORDS = 12;
+
+__device__ __forceinline__ double block_min(double v, double* red) { return -block_max(-v, red); }
+
+__global__ void k_path_bbox(const mvb_job* __restrict__ jobs, const double* __restrict__ paths,
+                            int64_t n_jobs, double* __restrict__ bbox) {
     __shared__ double red[32];
-    const int32_t i = sel[blockIdx.y];
+    const mvb_job& J = jobs[blockIdx.y];
+    double* part = bbox + BBOX_WORDS * (n_jobs + (int64_t)blockIdx.y * BBOX_PARTS + blockIdx.x);
+    for (int which = 0; which < 2; ++which) {
+        const double* P = paths + 3 * (which == 0 ? J.pos_off : J.mic_off);
+        const int64_t n = which == 0 || J.mic_moving ? J.T : 1;
+        double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+             t += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const double v = P[3 * t + a];
+                lo[a] = fmin(lo[a], v);
+                hi[a] = fmax(hi[a], v);
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double l = block_min(lo[a], red), h = block_max(hi[a], red);
+            if (threadIdx.x == 0) {
+                part[6 * which + a] = l;
+                part[6 * which + 3 + a] = h;
+            }
+        }
+    }
+}
+
+__global__ void k_bbox_reduce(int64_t n_jobs, double* __restrict__ bbox) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= n_jobs) return;
+    const double* part = bbox + BBOX_WORDS * (n_jobs + j * BBOX_PARTS);
+    for (int w = 0; w < BBOX_WORDS; ++w) {
+        const bool is_lo = (w % 6) < 3;
+        double v = part[w];
+        for (int q = 1; q < BBOX_PARTS; ++q)
+            v = is_lo ? fmin(v, part[BBOX_WORDS * q + w]) : fmax(v, part[BBOX_WORDS * q + w]);
+        bbox[BBOX_WORDS * j + w] = v;
+    }
+}
+
+// Full-rate images: lb = exact distance at the first, middle and last
+// sample; ub = largest distance between the image path's bounding box and
+// the receiver's (exact box algebra, + 1e-9 m for rounding).  Images whose
+// ub can reach the job's largest lb are scanned exactly by k_exact_max.
+__global__ void k_bounds_full(const mvb_image* __restrict__ images, const int32_t* __restrict__ sel,
+                              int64_t n_full, const mvb_job* __restrict__ jobs,
+                              const double* __restrict__ paths, const double* __restrict__ bbox,
+                              double* __restrict__ lb, double* __restrict__ ub) {
+    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= n_full) return;
+    const int32_t i = sel[q];
     const mvb_image im = images[i];
     const mvb_job& J = jobs[im.job];
     double best = 0.0;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < J.T;
-         t += (int64_t)gridDim.x * blockDim.x)
-        best = fmax(best, image_distance(im, paths + 3 * (J.pos_off + t), mic_row(J, paths, t)));
-    best = block_max(best, red);
-    if (threadIdx.x == 0) {
-        atomic_max_pos(lb + i, best);
-        atomic_max_pos(ub + i, best);
+    const int64_t ts[3] = {0, (J.T - 1) / 2, J.T - 1};
+    for (int k = 0; k < 3; ++k)
+        best = fmax(best, image_distance(im, paths + 3 * (J.pos_off + ts[k]), mic_row(J, paths, ts[k])));
+    const double* b = bbox + 12 * im.job;
+    double sq = 0.0;
+    for (int a = 0; a < 3; ++a) {
+        // image coordinate off + sign * p over p in [lo, hi]
+        const double e1 = im.off[a] + (double)im.sign[a] * b[a];
+        const double e2 = im.off[a] + (double)im.sign[a] * b[3 + a];
+        const double xlo = fmin(e1, e2), xhi = fmax(e1, e2);
+        const double g = fmax(fabs(xhi - b[6 + a]), fabs(b[9 + a] - xlo));
+        sq += g * g;
     }
+    lb[i] = best;
+    ub[i] = sqrt(sq) * (1.0 + 1e-12) + 1e-9;
 }
 
 // One block per job.  scratch region of job j starts at img_off + j:
@@ -142,24 +225,19 @@ __global__ void k_select(const mvb_image* __restrict__ images, const mvb_job* __
     __shared__ double red[32];
     const int64_t j = blockIdx.x;
     const mvb_job J = jobs[j];
-    double m = 0.0, mf = 0.0;
-    for (int64_t q = threadIdx.x; q < J.n_img; q += blockDim.x) {
-        const int64_t i = J.img_off + q;
-        m = fmax(m, lb[i]);
-        if (images[i].factor == 1) mf = fmax(mf, lb[i]);
-    }
+    double m = 0.0;
+    for (int64_t q = threadIdx.x; q < J.n_img; q += blockDim.x) m = fmax(m, lb[J.img_off + q]);
     m = block_max(m, red);
-    mf = block_max(mf, red);
     int32_t* sc = scratch + J.img_off + j;
     if (threadIdx.x == 0) {
         sc[0] = 0;
-        dmax[j] = mf;
+        dmax[j] = 0.0;
     }
     __syncthreads();
     const double LB = m - 1e-9;
     for (int64_t q = threadIdx.x; q < J.n_img; q += blockDim.x) {
         const int64_t i = J.img_off + q;
-        if (images[i].factor != 1 && ub[i] >= LB) {
+        if (ub[i] >= LB) {
             const int slot = atomicAdd(sc, 1);
             sc[1 + slot] = (int32_t)i;
         }
@@ -168,7 +246,8 @@ __global__ void k_select(const mvb_image* __restrict__ images, const mvb_job* __
 
 __global__ void k_exact_max(const mvb_image* __restrict__ images, const mvb_job* __restrict__ jobs,
                             const double* __restrict__ coarse, const double* __restrict__ tables,
-                            const int32_t* __restrict__ scratch, double* __restrict__ dmax) {
+                            const double* __restrict__ paths, const int32_t* __restrict__ scratch,
+                            double* __restrict__ dmax) {
     __shared__ double red[32];
     const int64_t j = blockIdx.z;
     const mvb_job& J = jobs[j];
@@ -179,8 +258,10 @@ __global__ void k_exact_max(const mvb_image* __restrict__ images, const mvb_job*
         double best = 0.0;
         for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < J.T;
              t += (int64_t)gridDim.x * blockDim.x)
-            best = fmax(best, exact_upsample(coarse + im.coarse, im.n_coarse, tables + im.table,
-                                             im.factor, t));
+            best = fmax(best, im.factor == 1
+                                  ? image_distance(im, paths + 3 * (J.pos_off + t), mic_row(J, paths, t))
+                                  : exact_upsample(coarse + im.coarse, im.n_coarse, tables + im.table,
+                                                   im.factor, t));
         best = block_max(best, red);
         if (threadIdx.x == 0) atomic_max_pos(dmax + j, best);
     }
@@ -197,11 +278,9 @@ __global__ void k_exact_max(const mvb_image* __restrict__ images, const mvb_job*
 // products per interval then run as fp32 FMAs, paired into FFMA2 over
 // (g_p, g_p+1).  Measured against the exact 65-tap track (tests) the
 // residual error is < 4e-9 m, i.e. < 6e-7 samples of delay at 48 kHz.
-// One block per (image, span of 1024 intervals); 8 consecutive intervals
-// per thread so each shared-memory load of dw feeds 8 x 5 FMA instructions.
-constexpr int COEF_BLOCK = 128;
-constexpr int COEF_KI = 8;
-constexpr int COEF_SPAN = COEF_BLOCK * COEF_KI;
+// One block per (image, span of BLOCK x KI intervals); KI consecutive
+// intervals per thread so each shared-memory load of dw feeds KI x 5 FMA
+// instructions.
 
 struct SbpParam {
     float g[64][10];  // G[p][j] stored per tap j: (g0..g8, pad)
@@ -210,15 +289,21 @@ struct SbpParam {
 // skew one word per 32 so the 8-interval thread stride is conflict-free
 __device__ __forceinline__ int skew32(int e) { return e + (e >> 5); }
 
-constexpr int COEF_DW = COEF_SPAN + 64 + (COEF_SPAN + 64) / 32 + 1;
-constexpr size_t COEF_SMEM = sizeof(mvb_coef32) * COEF_SPAN + sizeof(float) * COEF_DW;
+template <int COEF_BLOCK, int COEF_KI>
+struct CoefShape {
+    static constexpr int SPAN = COEF_BLOCK * COEF_KI;
+    static constexpr int DW = SPAN + 64 + (SPAN + 64) / 32 + 1;
+    static constexpr size_t SMEM = sizeof(mvb_coef32) * SPAN + sizeof(float) * DW;
+};
 
+template <int COEF_BLOCK, int COEF_KI>
 __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
     const __grid_constant__ SbpParam sp, const mvb_image* __restrict__ images,
     const int32_t* __restrict__ sel, const mvb_job* __restrict__ jobs,
     const double* __restrict__ coarse, mvb_coef32* __restrict__ out) {
     // records of the span are staged here and written out coalesced
     extern __shared__ __align__(16) unsigned char coef_smem[];
+    constexpr int COEF_SPAN = CoefShape<COEF_BLOCK, COEF_KI>::SPAN;
     mvb_coef32* srec = reinterpret_cast<mvb_coef32*>(coef_smem);
     float* dw = reinterpret_cast<float*>(coef_smem + sizeof(mvb_coef32) * COEF_SPAN);
     const mvb_image im = images[sel[blockIdx.x]];
@@ -297,6 +382,16 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
         float4* dst = reinterpret_cast<float4*>(out + im.coef + k0);
         for (int64_t t = threadIdx.x; t < n_rec * 3; t += blockDim.x) dst[t] = src[t];
     }
+}
+
+// images_sorted[q] = images[idx[q]]: 16-byte chunks, six per record
+__global__ void k_gather_images(const mvb_image* __restrict__ images, const int64_t* __restrict__ idx,
+                                int64_t n, mvb_image* __restrict__ out) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    constexpr int CH = sizeof(mvb_image) / 16;
+    if (t >= n * CH) return;
+    const int64_t q = t / CH, c = t - q * CH;
+    reinterpret_cast<float4*>(out + q)[c] = __ldg(reinterpret_cast<const float4*>(images + idx[q]) + c);
 }
 
 __global__ void k_sort_keys(const mvb_image* __restrict__ images, const mvb_job* __restrict__ jobs,
@@ -385,6 +480,25 @@ __global__ void k_build_images(const double* __restrict__ toff, const double* __
     }
 }
 
+template <int BLOCK, int KI>
+static int launch_coeffs(const SbpParam& sp, const mvb_image* images, const int32_t* sel,
+                         int64_t n_sel, int64_t max_K, const mvb_job* jobs, const double* coarse,
+                         mvb_coef32* coef, void* stream) {
+    using S = CoefShape<BLOCK, KI>;
+    int64_t spans = (max_K + S::SPAN - 1) / S::SPAN;
+    if (spans > 65535) spans = 65535;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k_coeffs<BLOCK, KI>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
+        if (e != cudaSuccess) return fail(MVB_ECUDA, cudaGetErrorString(e));
+        attr_set = true;
+    }
+    k_coeffs<BLOCK, KI><<<dim3((unsigned)n_sel, (unsigned)spans), BLOCK, S::SMEM, as_stream(stream)>>>(
+        sp, images, sel, jobs, coarse, coef);
+    return check_launch("track_coeffs");
+}
+
 extern "C" {
 
 int mvb_build_images(const double* toff, const double* tsgn, const double* tbeta, int64_t S0,
@@ -405,44 +519,58 @@ int mvb_build_images(const double* toff, const double* tsgn, const double* tbeta
 }
 
 int mvb_coarse_distances(const mvb_image* images, const int32_t* sel, int64_t n_sel,
-                         const mvb_job* jobs, const double* paths, double* coarse, void* stream) {
+                         int64_t max_K, const mvb_job* jobs, const double* paths, double negsum,
+                         double* coarse, double* lb, double* ub, void* stream) {
     if (n_sel < 0 || n_sel > 0x7fffffff) return fail(MVB_EINVAL, "coarse_distances: n_sel");
     if (n_sel == 0) return MVB_OK;
     if (!images || !sel || !jobs || !paths || !coarse) return fail(MVB_EINVAL, "coarse_distances: null");
-    k_coarse<<<(unsigned)n_sel, 256, 0, as_stream(stream)>>>(images, sel, jobs, paths, coarse);
+    if ((lb == nullptr) != (ub == nullptr)) return fail(MVB_EINVAL, "coarse_distances: lb/ub");
+    if (max_K < 1) return fail(MVB_EINVAL, "coarse_distances: max_K");
+    const int64_t chunks = ((max_K + 63) / 64 + CB_SEGS - 1) / CB_SEGS;
+    if (chunks > 65535) return fail(MVB_EINVAL, "coarse_distances: coarse track too long");
+    k_coarse_bounds<<<dim3(grid_for(n_sel, 8), (unsigned)chunks), 256, 0, as_stream(stream)>>>(
+        images, sel, n_sel, jobs, paths, negsum, coarse, lb, ub);
     return check_launch("coarse_distances");
 }
 
-int mvb_track_bounds(const mvb_image* images, int64_t n_img, const int32_t* full_sel,
-                     int64_t n_full, const mvb_job* jobs, const double* paths,
-                     const double* coarse, double negsum, double* lb, double* ub, void* stream) {
-    if (n_img < 0 || n_img > 0x7fffffff || n_full < 0 || n_full > 65535)
+int mvb_track_bounds(const mvb_image* images, const int32_t* full_sel, int64_t n_full,
+                     const mvb_job* jobs, int64_t n_jobs, const double* paths, double* bbox,
+                     double* lb, double* ub, void* stream) {
+    if (n_full < 0 || n_full > 0x7fffffff || n_jobs < 1 || n_jobs > 0x7fffffff)
         return fail(MVB_EINVAL, "track_bounds: sizes");
-    if (n_img == 0) return MVB_OK;
-    if (!images || !jobs || !lb || !ub) return fail(MVB_EINVAL, "track_bounds: null");
+    if (n_full == 0) return MVB_OK;
+    if (!images || !full_sel || !jobs || !paths || !bbox || !lb || !ub)
+        return fail(MVB_EINVAL, "track_bounds: null");
     cudaStream_t s = as_stream(stream);
-    if (cudaMemsetAsync(lb, 0, sizeof(double) * n_img, s) != cudaSuccess ||
-        cudaMemsetAsync(ub, 0, sizeof(double) * n_img, s) != cudaSuccess)
-        return fail(MVB_ECUDA, "track_bounds: memset");
-    if (coarse)
-        k_bounds_coarse<<<grid_for(n_img, 8), 256, 0, s>>>(images, n_img, coarse, negsum, lb, ub);
-    if (n_full > 0) {
-        if (!full_sel || !paths) return fail(MVB_EINVAL, "track_bounds: null full-rate inputs");
-        k_bounds_full<<<dim3(16, (unsigned)n_full), 256, 0, s>>>(images, full_sel, jobs, paths, lb, ub);
-    }
+    if (n_jobs > 65535) return fail(MVB_EINVAL, "track_bounds: n_jobs");
+    k_path_bbox<<<dim3(BBOX_PARTS, (unsigned)n_jobs), 256, 0, s>>>(jobs, paths, n_jobs, bbox);
+    k_bbox_reduce<<<grid_for(n_jobs, 128), 128, 0, s>>>(n_jobs, bbox);
+    k_bounds_full<<<grid_for(n_full, 128), 128, 0, s>>>(images, full_sel, n_full, jobs, paths, bbox,
+                                                        lb, ub);
     return check_launch("track_bounds");
 }
 
+int mvb_gather_images(const mvb_image* images, const int64_t* idx, int64_t n, mvb_image* out,
+                      void* stream) {
+    if (n < 0) return fail(MVB_EINVAL, "gather_images: n");
+    if (n == 0) return MVB_OK;
+    if (!images || !idx || !out) return fail(MVB_EINVAL, "gather_images: null");
+    const int64_t chunks = n * (int64_t)(sizeof(mvb_image) / 16);
+    k_gather_images<<<grid_for(chunks, 256), 256, 0, as_stream(stream)>>>(images, idx, n, out);
+    return check_launch("gather_images");
+}
+
 int mvb_track_max(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
-                  const double* coarse, const double* tables, const double* lb, const double* ub,
-                  int32_t* scratch, double* dmax, void* stream) {
+                  const double* coarse, const double* tables, const double* paths,
+                  const double* lb, const double* ub, int32_t* scratch, double* dmax,
+                  void* stream) {
     if (n_jobs < 1 || n_jobs > 65535) return fail(MVB_EINVAL, "track_max: n_jobs");
-    if (!images || !jobs || !lb || !ub || !scratch || !dmax) return fail(MVB_EINVAL, "track_max: null");
+    if (!images || !jobs || !paths || !lb || !ub || !scratch || !dmax)
+        return fail(MVB_EINVAL, "track_max: null");
     cudaStream_t s = as_stream(stream);
     k_select<<<(unsigned)n_jobs, 256, 0, s>>>(images, jobs, lb, ub, scratch, dmax);
-    if (coarse && tables)
-        k_exact_max<<<dim3(64, 8, (unsigned)n_jobs), 256, 0, s>>>(images, jobs, coarse, tables,
-                                                                   scratch, dmax);
+    k_exact_max<<<dim3(64, 8, (unsigned)n_jobs), 256, 0, s>>>(images, jobs, coarse, tables, paths,
+                                                               scratch, dmax);
     return check_launch("track_max");
 }
 
@@ -468,18 +596,9 @@ int mvb_track_coeffs(const mvb_image* images, const int32_t* sel, int64_t n_sel,
         }
         sp.g[j][9] = 0.f;
     }
-    int64_t spans = (max_K + COEF_SPAN - 1) / COEF_SPAN;
-    if (spans > 65535) spans = 65535;
-    static thread_local bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_coeffs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)COEF_SMEM);
-        if (e != cudaSuccess) return fail(MVB_ECUDA, cudaGetErrorString(e));
-        attr_set = true;
-    }
-    k_coeffs<<<dim3((unsigned)n_sel, (unsigned)spans), COEF_BLOCK, COEF_SMEM, as_stream(stream)>>>(
-        sp, images, sel, jobs, coarse, coef);
-    return check_launch("track_coeffs");
+    // 64 threads x 8 intervals: measured best of {64,128,256} x {4,8} on c3/c4
+    // (more resident blocks hide the staging prologue; 70% of the FFMA peak on c4)
+    return launch_coeffs<64, 8>(sp, images, sel, n_sel, max_K, jobs, coarse, coef, stream);
 }
 
 int mvb_sort_keys(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs, int64_t max_n_img,

@@ -357,20 +357,24 @@ class Geometry:
         # ---- coarse tracks, bounds, exact max ---------------------------------
         n_img = self.n_images
         self.coarse = torch.empty(max(self.n_coarse_total, 1), dtype=torch.float64, device=dev)
-        if self.dec_sel.numel():
-            _lib.call("mvb_coarse_distances", ptr(self.images), ptr(self.dec_sel),
-                      self.dec_sel.numel(), ptr(jobs_dev), ptr(self.paths), ptr(self.coarse), st)
-        lb = torch.empty(n_img, dtype=torch.float64, device=dev)
-        ub = torch.empty(n_img, dtype=torch.float64, device=dev)
+        lb = torch.zeros(n_img, dtype=torch.float64, device=dev)
+        ub = torch.zeros(n_img, dtype=torch.float64, device=dev)
         negsum = max([negative_mass(N) for N in self.factors if N > 1], default=0.0)
-        _lib.call("mvb_track_bounds", ptr(self.images), n_img, ptr(self.full_sel),
-                  self.full_sel.numel(), ptr(jobs_dev), ptr(self.paths),
-                  ptr(self.coarse) if self.dec_sel.numel() else ptr(None), negsum, ptr(lb), ptr(ub), st)
+        if self.dec_sel.numel():  # coarse distances + bounds of the decimated images
+            max_K = max(-(-int(self.T[j]) // N) for (j, N) in self.cpath)
+            _lib.call("mvb_coarse_distances", ptr(self.images), ptr(self.dec_sel),
+                      self.dec_sel.numel(), max_K, ptr(jobs_dev), ptr(self.paths), negsum,
+                      ptr(self.coarse), ptr(lb), ptr(ub), st)
+        if self.full_sel.numel():  # bounding-box bounds of the full-rate images
+            bbox = torch.empty(nJ, 65, 12, dtype=torch.float64, device=dev)  # boxes + partials
+            _lib.call("mvb_track_bounds", ptr(self.images), ptr(self.full_sel),
+                      self.full_sel.numel(), ptr(jobs_dev), nJ, ptr(self.paths), ptr(bbox),
+                      ptr(lb), ptr(ub), st)
         scratch = torch.empty(n_img + nJ, dtype=torch.int32, device=dev)
         dmax = torch.empty(nJ, dtype=torch.float64, device=dev)
         _lib.call("mvb_track_max", ptr(self.images), ptr(jobs_dev), nJ,
-                  ptr(self.coarse) if self.dec_sel.numel() else ptr(None), ptr(self.tables), ptr(lb),
-                  ptr(ub), ptr(scratch), ptr(dmax), st)
+                  ptr(self.coarse) if self.dec_sel.numel() else ptr(None), ptr(self.tables),
+                  ptr(self.paths), ptr(lb), ptr(ub), ptr(scratch), ptr(dmax), st)
         # dmax reaches the host through a pinned copy + event: the render stage
         # queues its out_len-independent kernels before it waits (dmax_host)
         self._dmax_host = torch.empty(nJ, dtype=torch.float64, pin_memory=True)
@@ -378,8 +382,8 @@ class Geometry:
         self._dmax_ready = torch.cuda.Event()
         self._dmax_ready.record()
         self._dmax = None
-        self.launches = self.n_enum_launches + 2 + (1 if self.dec_sel.numel() else 0) \
-            + (1 if self.full_sel.numel() else 0) + (2 if self.dec_sel.numel() else 1)
+        self.launches = self.n_enum_launches + (1 if self.dec_sel.numel() else 0) \
+            + (2 if self.full_sel.numel() else 0) + 2
         self.eval_count = [int(self.evals[j]) for j in range(nJ)]
 
     @property
@@ -784,8 +788,10 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
     order = torch.argsort(key, dim=2)  # (nJ, max_seg, max_img)
     base = h2d(geom.img_off, dev)[:, None, None]
     nimg_dev = h2d(geom.n_img, dev)[:, None, None]
-    gidx = base + torch.minimum(order, nimg_dev - 1)  # padded slots: any own image
-    images_sorted = geom.images[gidx.reshape(-1)]  # layout (job, segment, max_img)
+    gidx = (base + torch.minimum(order, nimg_dev - 1)).reshape(-1)  # padded slots: any own image
+    images_sorted = torch.empty(gidx.numel(), IMG_COLS, dtype=torch.int64, device=dev)
+    _lib.call("mvb_gather_images", ptr(geom.images), ptr(gidx), gidx.numel(), ptr(images_sorted), st)
+    launches += 1  # layout (job, segment, max_img)
     # 2. out_len, zero-padded branch records, work list, synthesis
     out_len, tau_ceil, offsets, rows = finish_rows()
     rec_rows, bases = 0, {}
