@@ -237,3 +237,35 @@ def test_source_modulation_matches_reference_golden():
     m = min(y.size, y_rx.size)
     err = y[200:m - 200] - y_rx[200:m - 200]
     assert 10 * np.log10(np.sum(y_rx[200:m - 200] ** 2) / np.sum(err ** 2)) >= 30.0
+
+
+@pytest.mark.parametrize("case", ["single_position", "single_sample_signal", "order0_fast",
+                                  "factor_exceeds_T", "odd_factor_fast", "short_signal"])
+def test_edge_cases_match_oracle(case):
+    """Degenerate sizes the reference accepts: T = 1, len(s) = 1, no
+    reflections, N > T (one coarse sample), odd N on the fast engine, a
+    signal shorter than the filter."""
+    f = mvb.hann_sinc(32, 14)
+    rng = np.random.default_rng(11)
+    n, T = 2000, 2000
+    cfg = mvb.SynthesisConfig(max_order=3, order_split=1, decimation=32)
+    if case == "single_position":
+        T = 1
+    elif case == "single_sample_signal":
+        n = 1
+    elif case == "order0_fast":
+        cfg = mvb.SynthesisConfig(max_order=0, decimation=1)
+    elif case == "factor_exceeds_T":
+        T = 100
+        cfg = mvb.SynthesisConfig(max_order=3, order_split=1, decimation=256)
+    elif case == "odd_factor_fast":
+        cfg = mvb.SynthesisConfig(max_order=4, order_split=1, decimation=37)
+    elif case == "short_signal":
+        n = 20
+    tr = moving(T) if T > 1 else static([2.0, 3.0, 2.0], 1)
+    x = rng.standard_normal(n)
+    for xx, tol in ((x, 1e-13), (x.astype(np.float32), 1e-5)):
+        y = mvb.render(xx, tr, ROOM, MIC, f, cfg)
+        ref = oracle_render(np.asarray(xx, np.float64), tr, MIC, f, cfg)
+        assert y.size == ref.size, case
+        assert rel_err(y, ref) <= tol, case
