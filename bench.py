@@ -379,6 +379,18 @@ def run_ours(args):
     flops = upd_per_launch * w.fd_taps * 2.0  # taps x FMA (north_star roofline)
     achieved = flops / (kern_avg_ms * 1e-3) / 1e12
     traffic = load_traffic(name)
+    # the other leg of the north_star roofline: algorithmic HBM bytes of a
+    # render (dry signal + trajectory in, output out) at the
+    # measured HBM bandwidth -- the slower leg (FMA) is the bound
+    alg_bytes = sum(sc.s.itemsize * sc.T + 24 * sc.T * (1 + (np.ndim(sc.mics[0]) > 1) * len(sc.mics))
+                    for sc in mine) + 4 * int(np.sum(res.lengths))
+    hbm_gbs = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 7700.0
+    hbm_leg = {"algorithmic_bytes": int(alg_bytes),
+               "achieved_gbs": alg_bytes / (kern_avg_ms * 1e-3) / 1e9, "peak_gbs": hbm_gbs,
+               "frac": alg_bytes / (kern_avg_ms * 1e-3) / 1e9 / hbm_gbs,
+               "measured_dram_gbs": None if traffic is None else
+               traffic.get("dram_bytes_per_launch") / (kern_avg_ms * 1e-3) / 1e9}
     roof = {
         "kernel": "k_synth_f32 (mvb_synthesize_f32)",
         "bound": "fp32",
@@ -392,6 +404,7 @@ def run_ours(args):
                        f"(SURVEY 8d: L FMAs per update)",
         "kernel_ms": kern_avg_ms,
         "kernel_share_of_step": kern_avg_ms / ms_step if ms_step else None,
+        "hbm_leg": hbm_leg,
         "executed": {
             "algorithm": "Farrow (paper Eq. 5): 32 B record gather + 8 FMA Horner per update",
             "l1_bytes_per_update": 32,

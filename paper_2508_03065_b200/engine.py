@@ -30,6 +30,7 @@ import ctypes
 import math
 import os
 from dataclasses import dataclass, field
+from functools import lru_cache
 
 import numpy as np
 import torch
@@ -270,6 +271,47 @@ def pack_jobs(rows: list) -> np.ndarray:
     return a
 
 
+@lru_cache(maxsize=64)
+def _group_plan(max_order: int, tiers: tuple, sub: tuple | None):
+    """Host plan of one enumeration group (pure function of its key):
+    canonical source index, factor class and per-class prefix counts of
+    every image (the (S, 2+nC) int32 table mvb_build_images reads), the
+    classes and their image counts."""
+    order_np = np.repeat(np.arange(max_order + 1),
+                         [1] + [4 * o * o + 2 for o in range(1, max_order + 1)])
+    src = np.arange(order_np.size, dtype=np.int64)
+    if sub is not None:
+        src = np.asarray(sub, np.int64)
+        order_np = order_np[src]
+    fac_np = np.ones(order_np.size, np.int64)
+    prev = -1
+    for mo, N in tiers:
+        fac_np[(order_np > prev) & (order_np <= mo)] = N
+        prev = mo
+    classes = tuple(sorted(set(fac_np.tolist())))
+    if len(classes) > _lib.MAX_CLASSES:
+        raise ValueError(f"at most {_lib.MAX_CLASSES} distinct decimation factors")
+    cidx = np.searchsorted(np.asarray(classes), fac_np)
+    onehot = (cidx[:, None] == np.arange(len(classes))[None, :]).astype(np.int32)
+    pref = np.cumsum(onehot, axis=0) - onehot  # earlier images per class
+    img_tab = np.concatenate([src[:, None], cidx[:, None], pref], axis=1).astype(np.int32)
+    img_tab.flags.writeable = False
+    return classes, onehot.sum(axis=0), img_tab
+
+
+_DEV_CACHE: dict = {}
+
+
+def _cached_dev(key, make):
+    """Small read-only device tables reused across renders (bounded)."""
+    t = _DEV_CACHE.get(key)
+    if t is None:
+        if len(_DEV_CACHE) > 64:
+            _DEV_CACHE.clear()
+        t = _DEV_CACHE[key] = make()
+    return t
+
+
 class Geometry:
     """Device-side hierarchical tracks of a batch of jobs (prepare stage)."""
 
@@ -458,16 +500,16 @@ class Geometry:
         # factor constants (transposed tables) shared by the batch
         factors = sorted({int(N) for jb in jobs for _, N in jb.tiers if int(N) > 1})
         self.factors = factors
-        tab_parts = []
         self.table_off, self.fit_idx = {}, {}
         off = 0
         for q, N in enumerate(factors):
-            cst = device_constants(N, dev)
             self.table_off[N] = off
-            tab_parts.append(cst["tableT"].reshape(-1))
-            off += cst["tableT"].numel()
+            off += 65 * N
             self.fit_idx[N] = q
-        self.tables = torch.cat(tab_parts) if tab_parts else torch.zeros(1, dtype=torch.float64, device=dev)
+        self.tables = _cached_dev(
+            ("tables", tuple(factors), str(dev)),
+            lambda: torch.cat([device_constants(N, dev)["tableT"].reshape(-1) for N in factors])
+            if factors else torch.zeros(1, dtype=torch.float64, device=dev))
         groups = {}
         for j, jb in enumerate(jobs):
             sub = None if jb.image_index is None else tuple(np.asarray(jb.image_index).tolist())
@@ -482,25 +524,8 @@ class Geometry:
         img_base = coarse_base = n_full = n_dec = 0
         n_cls = {N: 0 for N in factors}
         for (max_order, tiers, sub), members in groups.items():
-            order_np = np.repeat(np.arange(max_order + 1),
-                                 [1] + [4 * o * o + 2 for o in range(1, max_order + 1)])
-            src = np.arange(order_np.size, dtype=np.int64)
-            if sub is not None:
-                src = np.asarray(sub, np.int64)
-                order_np = order_np[src]
-            S = int(order_np.size)
-            fac_np = np.ones(S, np.int64)
-            prev = -1
-            for mo, N in tiers:
-                fac_np[(order_np > prev) & (order_np <= mo)] = N
-                prev = mo
-            classes = sorted(set(fac_np.tolist()))
-            if len(classes) > _lib.MAX_CLASSES:
-                raise ValueError(f"at most {_lib.MAX_CLASSES} distinct decimation factors")
-            cidx = np.searchsorted(np.asarray(classes), fac_np)
-            onehot = (cidx[:, None] == np.arange(len(classes))[None, :]).astype(np.int32)
-            pref = np.cumsum(onehot, axis=0) - onehot  # earlier images per class
-            counts = onehot.sum(axis=0)
+            classes, counts, img_tab = _group_plan(max_order, tiers, sub)
+            S = img_tab.shape[0]
             G = len(members)
             Tj = self.T[members].astype(np.int64)
             Kc = np.array([[-(-int(T) // N) if N > 1 else 0 for N in classes] for T in Tj],
@@ -518,8 +543,8 @@ class Geometry:
                     ct.sel_off[q] = n_cls[int(N)]
                     n_cls[int(N)] += G * int(counts[q])
             full_cnt = sum(int(counts[q]) for q, N in enumerate(classes) if N == 1)
-            plans.append(dict(max_order=max_order, sub=sub, members=members, S=S, src=src,
-                              cidx=cidx, pref=pref, classes=classes, kbase=kbase, ct=ct,
+            plans.append(dict(key=(max_order, tiers, sub), max_order=max_order, members=members,
+                              S=S, img_tab=img_tab, classes=classes, kbase=kbase, ct=ct,
                               img_base=img_base, full_off=n_full, dec_off=n_dec))
             for g, j in enumerate(members):
                 self.img_off[j] = img_base + g * S
@@ -560,15 +585,15 @@ class Geometry:
             for q, N in enumerate(classes):
                 if N > 1:
                     ct.sel_off[q] += cls_base[int(N)]
-            img_tab = np.concatenate([pl["src"][:, None], pl["cidx"][:, None], pl["pref"]],
-                                     axis=1).astype(np.int32)  # (S, 2 + nC) int32 (mvb.h)
+
             cp = np.asarray([[self.cpath.get((j, int(N)), 0) for N in classes] for j in members],
                             np.int64).reshape(len(members), len(classes))
             job_tab = np.concatenate([np.asarray(member_room, np.int64)[:, None],
                                       self.T[members].astype(np.int64)[:, None],
                                       np.asarray(members, np.int64)[:, None], pl["kbase"][:, None], cp],
                                      axis=1)
-            img_dev = h2d(np.ascontiguousarray(img_tab), dev)
+            img_dev = _cached_dev(("img_tab", pl["key"], str(dev)),
+                                  lambda: h2d(pl["img_tab"], dev))  # (S, 2 + nC) int32 (mvb.h)
             job_dev = h2d(np.ascontiguousarray(job_tab), dev)
             _lib.call("mvb_build_images", ptr(tab.offset), ptr(tab.sign), ptr(tab.beta), tab.count,
                       ptr(img_dev), S, ptr(job_dev), len(members), ctypes.byref(ct), pl["img_base"],
