@@ -19,9 +19,11 @@ engine renders any number of jobs with a fixed number of kernel launches:
     exact (fp64):  reference streams + mvb_synthesize_f64 (reference
                    arithmetic and summation order)
 
-Sharding: `shard=(rank, world)` restricts every job to a contiguous slice of
-its delay-sorted images (fast path); the caller sums the partial outputs
-(parallel.py does it with one NCCL reduce).
+Sharding (synth.render_jobs): a rank renders a strided subset of every
+job's images (Job.image_index) with the batch-wide track maximum supplied by
+Geometry's `dmax_hook` (an all-reduce of the per-rank maxima), so every
+rank writes the reference's out_len and the partial outputs sum exactly
+(parallel.py: one NCCL reduce).
 """
 
 from __future__ import annotations
@@ -38,7 +40,6 @@ import torch
 from . import _lib
 from ._dev import ptr, require_cuda, stream_handle
 from .farrow import as_filter, centered_branches
-from .parallel import image_slice
 from .room import image_table
 from .trajectory import (bandwidth_batch, decimate_batch, device_constants, negative_mass,
                          phase_fit)
@@ -315,12 +316,14 @@ def _cached_dev(key, make):
 class Geometry:
     """Device-side hierarchical tracks of a batch of jobs (prepare stage)."""
 
-    def __init__(self, jobs: list, device=None, inputs_ready=None):
+    def __init__(self, jobs: list, device=None, inputs_ready=None, dmax_hook=None):
         """`inputs_ready`: optional CUDA event after which every device
         tensor of `jobs` is final.  With it, the paths are staged and their
         bandwidths measured on a side stream that waits only for that event,
         so planning this batch does not queue behind earlier work on the
-        current stream (e.g. the previous batch's synthesis)."""
+        current stream (e.g. the previous batch's synthesis).  `dmax_hook`:
+        optional callable applied in place to the device tensor of per-job
+        track maxima before it is read (image shards: all-reduce MAX)."""
         if not jobs:
             raise ValueError("no jobs")
         self.dev = dev = require_cuda(device)
@@ -417,6 +420,8 @@ class Geometry:
         _lib.call("mvb_track_max", ptr(self.images), ptr(jobs_dev), nJ,
                   ptr(self.coarse) if self.dec_sel.numel() else ptr(None), ptr(self.tables),
                   ptr(self.paths), ptr(lb), ptr(ub), ptr(scratch), ptr(dmax), st)
+        if dmax_hook is not None:
+            dmax_hook(dmax)
         # dmax reaches the host through a pinned copy + event: the render stage
         # queues its out_len-independent kernels before it waits (dmax_host)
         self._dmax_host = torch.empty(nJ, dtype=torch.float64, pin_memory=True)
@@ -679,8 +684,8 @@ class RenderResult:
     out: torch.Tensor  # flat output (fp32 fast / fp64 exact)
     offsets: np.ndarray  # per-job start in `out`
     lengths: np.ndarray  # per-job out_len
-    n_images: np.ndarray  # per-job images rendered (this shard)
-    updates: int  # image x output-sample updates computed (this shard)
+    n_images: np.ndarray  # per-job images rendered
+    updates: int  # image x output-sample updates computed
     launches: int  # libmvb kernel launches in the render stage
 
     def job(self, j: int) -> torch.Tensor:
@@ -706,7 +711,7 @@ def _chunking(n_imgs, tiles, sm_count):
     return out
 
 
-def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=None,
+def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
            signal_keys=None, timing: list | None = None) -> RenderResult:
     """Synthesize every job of `geom` (signals[j] is job j's dry signal).
     `timing`, if a list, receives (start, end) CUDA events recorded on the
@@ -763,8 +768,6 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
         return out_len, tau_ceil, offsets, rows
 
     if precision == "fp64":
-        if shard is not None and shard[1] > 1:
-            raise ValueError("the exact fp64 engine runs replicas only (no image sharding)")
         nb = int(f.poly_order) + 1
         br = h2d(np.asarray(f.branches, dtype=np.float64), dev)
         base, bases = 0, {}
@@ -846,11 +849,8 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
         r0, front = bases[keys[j]]
         rows[j].update(rec_base=r0 + front, nb=nb, img_off=j * max_seg * max_img,
                        img_stride=max_img)
-    # image slices of this shard (in delay-sorted order)
-    rank_, world = (0, 1) if shard is None else (int(shard[0]), int(shard[1]))
-    sl = [image_slice(int(n), rank_, world) for n in geom.n_img]
-    lo = np.array([a for a, _ in sl], dtype=np.int64)
-    hi = np.array([b for _, b in sl], dtype=np.int64)
+    lo = np.zeros(nJ, dtype=np.int64)
+    hi = geom.n_img.astype(np.int64)
     tiles = [-(-int(out_len[j]) // TILE) for j in range(nJ)]
     chunks = _chunking([int(hi[j] - lo[j]) for j in range(nJ)], tiles, sm_count)
     part_rows = 0
@@ -885,6 +885,5 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32", shard=N
         _lib.call("mvb_reduce_partials_f32", ptr(jobs_dev), nJ, int(out_len.max()), ptr(part),
                   ptr(out), st)
         launches += 1
-    n_img_shard = (hi - lo).astype(np.int64)
-    upd = int(np.sum(out_len * n_img_shard))
-    return RenderResult(out, offsets, out_len, n_img_shard, upd, launches)
+    upd = int(np.sum(out_len * hi))
+    return RenderResult(out, offsets, out_len, hi.copy(), upd, launches)

@@ -2,11 +2,16 @@
 
 One process per GPU (torchrun), torch.distributed for the plumbing:
 
-  image shards   c3, c5: every rank renders all output samples of every job
-                 from a contiguous slice of each time segment's delay-sorted
-                 image list (images are independent), then one
-                 reduce (sum) of the output buffers to rank 0 -- NCCL over
-                 NVLink on B200, ~2 MB (c3) / ~13 MB (c5) per render.
+  image shards   c3, c5: rank r renders all output samples of every job from
+                 the strided image subset r, r+W, r+2W, ... of its canonical
+                 list (images are independent; striding keeps
+                 every tier balanced), so enumeration-independent work --
+                 coarse tracks, bounds, interval records, sort, synthesis --
+                 divides by W.  Two exchanges: an all-reduce MAX of the
+                 per-job track maxima (a few bytes; every rank then writes the
+                 reference's out_len) and one reduce (sum) of the output
+                 buffers to rank 0 -- NCCL over NVLink on B200, ~2 MB (c3) /
+                 ~13 MB (c5) per render.
   scene shards   c4: independent scenes, longest-processing-time assignment
                  by update count; no collective.
   replicas       c1, c2: too small to split; every rank renders the job.
@@ -22,12 +27,23 @@ import heapq
 import numpy as np
 
 
-def image_slice(n_images: int, rank: int, world: int) -> tuple:
-    """[lo, hi) positions of a sorted image list owned by `rank`; the slices
-    of ranks 0..world-1 tile [0, n_images) exactly."""
+def image_subset(images, rank: int, world: int) -> np.ndarray:
+    """Canonical image positions owned by `rank`: every world-th entry of
+    `images` (an image count or an index list) starting at `rank`; the
+    subsets of ranks 0..world-1 partition it."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("need 0 <= rank < world")
-    return (n_images * rank) // world, (n_images * (rank + 1)) // world
+    idx = np.arange(int(images), dtype=np.int64) if np.ndim(images) == 0 \
+        else np.asarray(images, dtype=np.int64)
+    return idx[rank::world]
+
+
+def allreduce_max(t, group=None):
+    """In-place MAX over the ranks (no-op without a process group)."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t
 
 
 def lpt_assign(costs, world: int) -> list:

@@ -390,15 +390,32 @@ def scene_jobs(scenes, channels=None) -> list:
 
 
 def render_jobs(jobs, f, precision="fp32", shard=None, signals=None, timing=None,
-                inputs_ready=None):
+                inputs_ready=None, dmax_hook=None):
     """Geometry + render of a job batch; returns engine.RenderResult
     (device output, per-job offsets/lengths, update count, launches).
     `inputs_ready` (optional CUDA event): the jobs' device tensors are final
-    once it completes -- lets planning overlap earlier work on the stream."""
-    geom = engine.Geometry(jobs, inputs_ready=inputs_ready)
+    once it completes -- lets planning overlap earlier work on the stream.
+    `shard=(rank, world)`: render the strided image subset rank::world of
+    every job (parallel.image_subset; all per-image work divides by world),
+    with out_len from the batch-wide track maximum (all-reduce MAX over
+    the ranks, or `dmax_hook` when given) so the ranks' outputs sum to the
+    full render."""
+    if shard is not None and int(shard[1]) > 1:
+        if precision == "fp64":
+            raise ValueError("the exact fp64 engine runs replicas only (its summation order "
+                             "spans all images)")
+        from dataclasses import replace as _replace
+        from . import parallel
+        rank, world = int(shard[0]), int(shard[1])
+        jobs = [_replace(jb, image_index=parallel.image_subset(
+                    image_count(jb.max_order) if jb.image_index is None else jb.image_index,
+                    rank, world), signal_key=engine._key(jb.signal_key, jb.s),
+                    path_key=engine._key(jb.path_key, jb.pos)) for jb in jobs]
+        if dmax_hook is None:
+            dmax_hook = parallel.allreduce_max
+    geom = engine.Geometry(jobs, inputs_ready=inputs_ready, dmax_hook=dmax_hook)
     sig = signals if signals is not None else [jb.s for jb in jobs]
     keys = [engine._key(jb.signal_key, jb.s) for jb in jobs]
-    res = engine.render(geom, sig, f, precision=precision, shard=shard, signal_keys=keys,
-                        timing=timing)
+    res = engine.render(geom, sig, f, precision=precision, signal_keys=keys, timing=timing)
     res.launches += geom.launches
     return res

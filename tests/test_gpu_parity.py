@@ -197,3 +197,37 @@ def test_mixed_job_groups_in_one_batch():
             y = res.job(j).double().cpu().numpy()
             assert y.size == ref.size, (precision, j)
             assert rel_err(y, ref) <= tol, (precision, j)
+
+
+def test_image_shards_sum_to_full_render():
+    """Image shards (parallel.image_subset) rendered one after another on
+    this GPU: per-shard track maxima -> batch-wide maximum (the value the
+    all-reduce MAX produces across ranks, fed through dmax_hook) -> every
+    shard writes the full out_len and the shard outputs sum to the render
+    (no rank waits on another: the shards run sequentially)."""
+    import dataclasses
+    from paper_2508_03065_b200 import engine, parallel
+    g, scenes, chans = _scenes("c5")
+    f = _filter_of(g, scenes[0].fd_taps)
+    jobs = scene_jobs(scenes, chans)
+    world = 3
+    full = render_jobs(jobs, f, precision="fp32")
+    local = []
+    for r in range(world):
+        sub = [dataclasses.replace(jb, image_index=parallel.image_subset(
+            mroom.image_count(jb.max_order), r, world)) for jb in jobs]
+        local.append(engine.Geometry(sub).dmax)
+    gmax = np.max(np.stack(local), axis=0)
+
+    def hook(t):
+        t.copy_(torch.as_tensor(gmax, device=t.device))
+
+    parts = [render_jobs(jobs, f, precision="fp32", shard=(r, world), dmax_hook=hook)
+             for r in range(world)]
+    assert all(np.array_equal(p.lengths, full.lengths) for p in parts)
+    assert sum(p.updates for p in parts) == full.updates
+    total = sum(p.out.double() for p in parts).cpu().numpy()
+    ref = np.concatenate(_oracle(scenes, chans, g["branches"]))
+    assert rel_err(total, ref) <= FP32_TOL
+    with pytest.raises(ValueError):
+        render_jobs(jobs, f, precision="fp64", shard=(0, 2))

@@ -1,14 +1,15 @@
-"""Multi-GPU partitioning logic on CPU: image_slice / lpt_assign properties
-and a world_size-2 gloo run of the image-shard + reduce path, with the CPU
-oracle rendering each rank's shard (test infrastructure stands in for the
-GPU renderer; the partition and the collective are the product code)."""
+"""Multi-GPU partitioning logic on CPU: image_subset / lpt_assign properties
+and a world_size-2 gloo run of the image-shard path -- strided image
+subsets, the all-reduce MAX of the track maxima and the sum-reduce of the
+outputs -- with the CPU oracle rendering each rank's subset (test
+infrastructure stands in for the GPU renderer; the partition and the
+collectives are the product code)."""
 
 import os
 import socket
 import tempfile
 
 import numpy as np
-import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -16,13 +17,14 @@ import torch.multiprocessing as mp
 from paper_2508_03065_b200 import parallel
 
 
-def test_image_slices_tile_the_list():
+def test_image_subsets_partition_and_balance():
     for n in (0, 1, 7, 11521):
         for world in (1, 2, 3, 8):
-            got = [parallel.image_slice(n, r, world) for r in range(world)]
-            assert got[0][0] == 0 and got[-1][1] == n
-            assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
-            assert max(h - l for l, h in got) - min(h - l for l, h in got) <= 1
+            got = [parallel.image_subset(n, r, world) for r in range(world)]
+            assert np.array_equal(np.sort(np.concatenate(got)), np.arange(n))
+            assert max(g.size for g in got) - min(g.size for g in got) <= 1
+    sub = np.array([3, 5, 8, 13, 21])
+    assert parallel.image_subset(sub, 1, 2).tolist() == [5, 13]
 
 
 def test_lpt_assign_balances_and_covers():
@@ -42,53 +44,29 @@ def test_shard_modes():
     assert parallel.shard_mode("c3", 1) == "single"
 
 
-SEG = 2048  # samples per sort segment in this test
-
-
-def _scene():
+def _scene(images=None):
     from oracle import oracle as orc
     from paper_2508_03065_b200 import hann_sinc, workloads
     sc = workloads.make_scenes("c3", duration=0.06, max_order=5, tiers=((1, 1), (3, 32), (5, 256)))[0]
     f = hann_sinc(sc.fd_taps, 14)
+    im = None
+    if images is not None:
+        im = orc.enumerate_images(sc.dims, sc.walls, sc.max_order).take(images)
     return orc.OracleScene(sc.s, sc.pos, sc.mics[0], sc.dims, sc.walls, sc.max_order, sc.tiers,
-                           f.branches, sc.rate)
-
-
-def _segment_order(o, s):
-    """Delay-sort of the images at the centre of segment s (engine rule)."""
-    t = min(o.T - 1, s * SEG + SEG // 2)
-    key = np.empty(len(o.images))
-    for i in range(len(o.images)):
-        if o.factor[i] == 1:
-            d = o.images.offset[i] + o.images.sign[i] * o.pos[t] - o.mic
-            key[i] = np.sqrt(d @ d)
-        else:
-            k = min(t // o.factor[i], o.coarse_len[i] - 1)
-            key[i] = o.coarse[o.coarse_off[i] + k]
-    return np.argsort(key, kind="stable")
+                           f.branches, sc.rate, images=im)
 
 
 def _worker(rank, world, port, outdir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    o = _scene()
-    out_len = o.out_len()
-    part = np.zeros(out_len)
-    n_seg = -(-o.T // SEG)
-    for s in range(n_seg):
-        order = _segment_order(o, s)
-        lo, hi = parallel.image_slice(order.size, rank, world)
-        mine = np.sort(order[lo:hi])
-        n0 = s * SEG
-        n1 = out_len if s == n_seg - 1 else (s + 1) * SEG  # hold tail: last segment
-        sub = o._struct(mine)
-        import ctypes
-        from oracle.oracle import lib, _p
-        buf = np.empty(n1 - n0)
-        lib().orc_render_window(ctypes.byref(sub), n0, n1, _p(buf), 1)
-        part[n0:n1] = buf
-    t = torch.from_numpy(part)
+    full = _scene()
+    mine = parallel.image_subset(len(full.images), rank, world)
+    o = _scene(mine)
+    dmax = torch.tensor([o.track_max()], dtype=torch.float64)
+    parallel.allreduce_max(dmax)  # batch-wide maximum -> the reference's out_len
+    out_len = o.s.size + int(np.ceil(o.rate * float(dmax[0]) / o.c)) + o.L
+    t = torch.from_numpy(o.render_window(0, out_len))
     parallel.reduce_to_root(t)
     if rank == 0:
         np.save(os.path.join(outdir, "reduced.npy"), t.numpy())
