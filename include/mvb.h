@@ -199,17 +199,37 @@ int mvb_track_bounds(const mvb_image* d_images, const int32_t* d_full_sel, int64
                      double* d_bbox, double* d_lb, double* d_ub, void* stream);
 
 /* Exact track max of every job (d_dmax[n_jobs]): only the images whose ub
- * reaches the job's largest lb are evaluated at every t < T (exact distance
- * for factor 1, the reference's 65-tap upsample otherwise).  d_scratch:
- * n_img + n_jobs int32. */
+ * reaches the job's largest lb are evaluated (exact distance for factor 1,
+ * the reference's 65-tap upsample otherwise), in 2048-sample chunks; a
+ * decimated candidate's chunk whose coarse-window bound (negsum as in
+ * mvb_coarse_distances) stays below the running maximum is skipped.
+ * d_scratch: n_img + n_jobs int32. */
 int mvb_track_max(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jobs,
                   const double* d_coarse, const double* d_tables, const double* d_paths,
-                  const double* d_lb, const double* d_ub, int32_t* d_scratch, double* d_dmax,
-                  void* stream);
+                  double negsum, const double* d_lb, const double* d_ub, int32_t* d_scratch,
+                  double* d_dmax, void* stream);
 
 /* d_out[q] = d_images[d_idx[q]], q < n (delay-sorted image tables). */
 int mvb_gather_images(const mvb_image* d_images, const int64_t* d_idx, int64_t n,
                       mvb_image* d_out, void* stream);
+
+/* Coarse path rows (decimate's pos[::N], trajectory.py:279-298) for n
+ * paths: d_dst[d_rows[2q+1] + k] = d_src[d_rows[2q] + k*N], k < K (rows of
+ * 3 doubles; d_rows holds (source row, destination row) pairs). */
+int mvb_decimate_rows(const double* d_src, const int64_t* d_rows, int64_t n, int64_t K,
+                      int64_t N, double* d_dst, void* stream);
+
+/* Decimation decision (trajectory.py:316-339) around a cuFFT rFFT:
+ * mvb_center_paths: d_out = x - mean over T of each axis of the paths
+ * d_x (G, T, 3) (d_scratch: 3 G x 64 doubles; G <= 65535);
+ * mvb_spectrum_index: for the rFFT of the centred paths along T (d_spec =
+ * complex (G, F, 3), re/im interleaved), for each (path, axis) the first
+ * bin whose cumulative power |X|^2 (|X| = hypot) reaches fraction x total
+ * -> d_index[3g + a], -1 when all zero (d_scratch: 3 G x 64 doubles). */
+int mvb_center_paths(const double* d_x, int64_t G, int64_t T, double* d_scratch, double* d_out,
+                     void* stream);
+int mvb_spectrum_index(const double* d_spec, int64_t G, int64_t F, double fraction,
+                       double* d_scratch, int64_t* d_index, void* stream);
 
 /* Decimation decision helper (trajectory.py:316-339): for each of `rows`
  * power-spectrum rows of length F (fp64, contiguous), the first index whose

@@ -33,10 +33,55 @@ def stream_handle(device=None) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
+class _PinnedRing:
+    """Persistent pinned staging ring for the planner's small uploads.
+
+    Arrays are copied into the ring and sent with an asynchronous
+    stream-ordered copy (no host sync, no per-call cudaHostAlloc, no
+    per-call event).  A lap is ~16 MB (hundreds of renders); before the ring
+    wraps, the device is synchronised once, so no staged bytes are
+    overwritten before their copy ran, whatever stream issued it.
+    """
+
+    ALIGN = 256
+
+    def __init__(self, nbytes: int = 16 << 20):
+        self.cap = nbytes
+        self.buf = None
+        self.off = 0
+
+    def put(self, a: np.ndarray, dev) -> torch.Tensor:
+        a = np.ascontiguousarray(a)
+        n = a.nbytes
+        if n > self.cap // 4:  # large arrays: one-off pinned copy (own writable copy)
+            return torch.from_numpy(np.array(a, copy=True)).pin_memory().to(dev, non_blocking=True)
+        if self.buf is None:
+            self.buf = torch.empty(self.cap, dtype=torch.uint8, pin_memory=True)
+            self.host = self.buf.numpy()
+        if self.off + n > self.cap:
+            torch.cuda.synchronize()
+            self.off = 0
+        self.host[self.off:self.off + n] = a.reshape(-1).view(np.uint8)
+        src = self.buf[self.off:self.off + n].view(_TORCH_DTYPE[a.dtype.str[1:]])
+        out = src.reshape(a.shape).to(dev, non_blocking=True)
+        self.off += -(-max(n, 1) // self.ALIGN) * self.ALIGN
+        return out
+
+
+_TORCH_DTYPE = {"f8": torch.float64, "f4": torch.float32, "i8": torch.int64, "i4": torch.int32,
+                "u1": torch.uint8, "b1": torch.bool}
+_RING = _PinnedRing()
+
+
+def h2d(a: np.ndarray, dev) -> torch.Tensor:
+    """Host array -> device without a host sync (pinned ring staging)."""
+    return _RING.put(np.asarray(a), dev)
+
+
 def to_dev(a, dtype, device) -> torch.Tensor:
-    """numpy / torch -> contiguous device tensor of dtype (no copy if already)."""
+    """numpy / torch -> contiguous device tensor of dtype (no copy if already);
+    host arrays go through the pinned ring (asynchronous, no host sync)."""
     if isinstance(a, torch.Tensor):
         return a.to(device=device, dtype=dtype).contiguous()
     arr = np.array(np.asarray(a), dtype=torch.empty((), dtype=dtype).numpy().dtype, order="C")
-    # pinned staging + async copy: no host/stream serialisation
-    return torch.from_numpy(arr).pin_memory().to(device, non_blocking=True)
+    return h2d(arr, device)

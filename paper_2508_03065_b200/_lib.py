@@ -38,7 +38,7 @@ _SIGS = {
     "mvb_build_images": [P, P, P, I64, P, I64, P, I64, P, I64, P, P, I64, P, I64, P, P],
     "mvb_coarse_distances": [P, P, I64, I64, P, P, DBL, P, P, P, P],
     "mvb_track_bounds": [P, P, I64, P, I64, P, P, P, P, P],
-    "mvb_track_max": [P, P, I64, P, P, P, P, P, P, P, P],
+    "mvb_track_max": [P, P, I64, P, P, P, DBL, P, P, P, P, P],
     "mvb_gather_images": [P, P, I64, P, P],
     "mvb_track_coeffs": [P, P, I64, I64, P, P, P, P, P],
     "mvb_sort_keys": [P, P, I64, I64, I64, I64, P, P, P, P],
@@ -47,6 +47,9 @@ _SIGS = {
     "mvb_reduce_partials_f32": [P, I64, I64, P, P, P],
     "mvb_synthesize_f64": [P, I64, I64, P, P, P, P, P, P, P],
     "mvb_energy_index": [P, I64, I64, DBL, P, P],
+    "mvb_decimate_rows": [P, P, I64, I64, I64, P, P],
+    "mvb_spectrum_index": [P, I64, I64, DBL, P, P, P],
+    "mvb_center_paths": [P, I64, I64, P, P, P],
     "mvb_static_taps": [P, P, P, I64, P, I64, P, DBL, DBL, DBL, P, P, P, P],
     "mvb_static_gather": [P, P, P, I64, I64, P, I64, P, P],
     "mvb_block_convolve": [P, I64, I64, I64, I64, INT, P, P, I64, I64, P, I64, P],

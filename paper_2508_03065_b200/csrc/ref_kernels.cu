@@ -147,6 +147,9 @@ __global__ void k_enumerate(const double* __restrict__ dims, const double* __res
     const int o = blockIdx.x;
     const int64_t room = blockIdx.y;
     const int n = o == 0 ? 1 : 4 * o * o + 2;
+    // blockIdx.z: which 256-image chunk of the order this block ranks
+    const int c0 = blockIdx.z * blockDim.x;
+    if (c0 >= n) return;
     int64_t base = 0;
     if (o > 0) {
         base = 1;
@@ -167,7 +170,7 @@ __global__ void k_enumerate(const double* __restrict__ dims, const double* __res
     __syncthreads();
     const double* dm = dims + 3 * room;
     const double* wl = walls + 6 * room;
-    for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+    for (int idx = c0 + threadIdx.x; idx < n && idx < c0 + (int)blockDim.x; idx += blockDim.x) {
         int64_t mine = keys[idx];
         int rank = 0;
         for (int j = 0; j < n; ++j) rank += keys[j] < mine;
@@ -288,7 +291,7 @@ int mvb_enumerate(const double* dims, const double* walls, int64_t n_rooms, int 
                                              (int)smem);
         if (e != cudaSuccess) return fail(MVB_ECUDA, cudaGetErrorString(e));
     }
-    dim3 g((unsigned)(max_order + 1), (unsigned)n_rooms);
+    dim3 g((unsigned)(max_order + 1), (unsigned)n_rooms, (unsigned)((nmax + 255) / 256));
     k_enumerate<<<g, 256, smem, as_stream(stream)>>>(dims, walls, max_order, S, lattice, parity,
                                                     order, beta, offset, sign);
     return check_launch("enumerate");

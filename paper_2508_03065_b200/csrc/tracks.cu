@@ -229,12 +229,15 @@ __global__ void k_select(const mvb_image* __restrict__ images, const mvb_job* __
     for (int64_t q = threadIdx.x; q < J.n_img; q += blockDim.x) m = fmax(m, lb[J.img_off + q]);
     m = block_max(m, red);
     int32_t* sc = scratch + J.img_off + j;
+    const double LB = m - 1e-9;
     if (threadIdx.x == 0) {
         sc[0] = 0;
-        dmax[j] = 0.0;
+        // every lb is attained by its track to ~1e-12 m, so the exact max is
+        // >= LB: seeding dmax with LB is exact and lets k_exact_max skip
+        // sample chunks whose bound stays below the running maximum
+        dmax[j] = LB > 0.0 ? LB : 0.0;
     }
     __syncthreads();
-    const double LB = m - 1e-9;
     for (int64_t q = threadIdx.x; q < J.n_img; q += blockDim.x) {
         const int64_t i = J.img_off + q;
         if (ub[i] >= LB) {
@@ -244,26 +247,57 @@ __global__ void k_select(const mvb_image* __restrict__ images, const mvb_job* __
     }
 }
 
+// Exact maxima of the candidates over t < T, in chunks of EXACT_CHUNK
+// samples (blockIdx.x strides over chunks).  A decimated candidate's chunk
+// is skipped when the bound of its coarse window (max + negsum (max - min),
+// the window covering every 65-tap sum in the chunk) cannot exceed the
+// running maximum; dmax only grows, so skipping is exact.
+constexpr int EXACT_CHUNK = 2048;
+
 __global__ void k_exact_max(const mvb_image* __restrict__ images, const mvb_job* __restrict__ jobs,
                             const double* __restrict__ coarse, const double* __restrict__ tables,
-                            const double* __restrict__ paths, const int32_t* __restrict__ scratch,
-                            double* __restrict__ dmax) {
+                            const double* __restrict__ paths, double negsum,
+                            const int32_t* __restrict__ scratch, double* __restrict__ dmax) {
     __shared__ double red[32];
+    __shared__ int skip;
     const int64_t j = blockIdx.z;
     const mvb_job& J = jobs[j];
     const int32_t* sc = scratch + J.img_off + j;
     const int count = sc[0];
+    const int64_t n_chunks = (J.T + EXACT_CHUNK - 1) / EXACT_CHUNK;
     for (int slot = blockIdx.y; slot < count; slot += gridDim.y) {
         const mvb_image im = images[sc[1 + slot]];
-        double best = 0.0;
-        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < J.T;
-             t += (int64_t)gridDim.x * blockDim.x)
-            best = fmax(best, im.factor == 1
-                                  ? image_distance(im, paths + 3 * (J.pos_off + t), mic_row(J, paths, t))
-                                  : exact_upsample(coarse + im.coarse, im.n_coarse, tables + im.table,
-                                                   im.factor, t));
-        best = block_max(best, red);
-        if (threadIdx.x == 0) atomic_max_pos(dmax + j, best);
+        for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+            const int64_t t0 = ch * EXACT_CHUNK;
+            const int64_t t1 = t0 + EXACT_CHUNK < J.T ? t0 + EXACT_CHUNK : J.T;
+            if (im.factor != 1) {
+                // coarse window of the chunk: [t0/N - 32, (t1-1)/N + 32], clamped
+                const double* c = coarse + im.coarse;
+                const int64_t K = im.n_coarse;
+                int64_t k0 = t0 / im.factor - 32, k1 = (t1 - 1) / im.factor + 32;
+                k0 = k0 < 0 ? 0 : k0;
+                k1 = k1 > K - 1 ? K - 1 : k1;
+                double M = -DBL_MAX, m = DBL_MAX;
+                for (int64_t k = k0 + threadIdx.x; k <= k1; k += blockDim.x) {
+                    M = fmax(M, c[k]);
+                    m = fmin(m, c[k]);
+                }
+                M = block_max(M, red);
+                m = -block_max(-m, red);
+                if (threadIdx.x == 0)
+                    skip = M + negsum * (M - m) + 1e-9 < *(volatile double*)(dmax + j);
+                __syncthreads();
+                if (skip) continue;
+            }
+            double best = 0.0;
+            for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x)
+                best = fmax(best, im.factor == 1
+                                      ? image_distance(im, paths + 3 * (J.pos_off + t), mic_row(J, paths, t))
+                                      : exact_upsample(coarse + im.coarse, im.n_coarse, tables + im.table,
+                                                       im.factor, t));
+            best = block_max(best, red);
+            if (threadIdx.x == 0) atomic_max_pos(dmax + j, best);
+        }
     }
 }
 
@@ -416,6 +450,151 @@ __global__ void k_sort_keys(const mvb_image* __restrict__ images, const mvb_job*
     key[(j * max_n_seg + s) * max_n_img + i] = k;
 }
 
+// Coarse path rows: dst[dst_row[q] + k] = src[src_row[q] + k * N], k < K
+// (decimate: pos[::N], trajectory.py:279-298), 3 doubles per row.
+__global__ void k_decimate_rows(const double* __restrict__ src, const int64_t* __restrict__ rows,
+                                int64_t n, int64_t K, int64_t N, double* __restrict__ dst) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n * K * 3) return;
+    const int64_t a = t % 3, k = (t / 3) % K, q = t / (3 * K);
+    dst[3 * (rows[2 * q + 1] + k) + a] = src[3 * (rows[2 * q] + k * N) + a];
+}
+
+// Bandwidth decision helpers (trajectory.py:316-339) ----------------------
+// Mean removal of x (G, T, 3) along T (the reference's x - x.mean()), wide:
+// chunk sums, then every block of the subtraction folds the chunk sums of
+// its path in a fixed order (deterministic, identical in every block).
+constexpr int SPEC_PARTS = 64;
+
+__device__ __forceinline__ int64_t part_begin(int64_t F, int q) { return (F * q) / SPEC_PARTS; }
+
+__global__ void k_path_sums(const double* __restrict__ x, int64_t T, double* __restrict__ partial) {
+    __shared__ double red[3][32];
+    const int64_t g = blockIdx.y;
+    const int q = blockIdx.x;
+    const int64_t t0 = part_begin(T, q), t1 = part_begin(T, q + 1);
+    double s[3] = {0.0, 0.0, 0.0};
+    for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) s[a] += x[3 * (g * T + t) + a];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) s[a] += __shfl_xor_sync(0xffffffffu, s[a], o);
+        if (l == 0) red[a][w] = s[a];
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double t = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[threadIdx.x][k];
+        partial[(g * 3 + threadIdx.x) * SPEC_PARTS + q] = t;
+    }
+}
+
+__global__ void k_path_center(const double* __restrict__ x, int64_t T,
+                              const double* __restrict__ partial, double* __restrict__ out) {
+    __shared__ double mean[3];
+    const int64_t g = blockIdx.y;
+    if (threadIdx.x < 3) {
+        const double* p = partial + (g * 3 + threadIdx.x) * SPEC_PARTS;
+        double t = 0.0;
+        for (int q = 0; q < SPEC_PARTS; ++q) t += p[q];
+        mean[threadIdx.x] = t / (double)T;
+    }
+    __syncthreads();
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < 3 * T;
+         e += (int64_t)gridDim.x * blockDim.x)
+        out[3 * g * T + e] = x[3 * g * T + e] - mean[e % 3];
+}
+
+// Spectra of the centred paths as cuFFT returns them for (G, T, 3)
+// transformed along T: spec[(g F + f) 3 + a] (complex).  Row (g, a) power
+// |X_f|^2 with |X| = hypot (numpy.abs).
+__device__ __forceinline__ double spec_power(const double2* spec, int64_t F, int64_t row, int64_t f) {
+    const int64_t g = row / 3, a = row % 3;
+    const double2 v = spec[(g * F + f) * 3 + a];
+    const double m = hypot(v.x, v.y);
+    return m * m;
+}
+
+// partial[row][q] = power summed over bins [part_begin(q), part_begin(q+1))
+__global__ void k_spec_partial(const double2* __restrict__ spec, int64_t F, double* __restrict__ partial) {
+    __shared__ double red[32];
+    const int64_t row = blockIdx.y;
+    const int q = blockIdx.x;
+    const int64_t f0 = part_begin(F, q), f1 = part_begin(F, q + 1);
+    double s = 0.0;
+    for (int64_t f = f0 + threadIdx.x; f < f1; f += blockDim.x) s += spec_power(spec, F, row, f);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) red[w] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += red[k];
+        partial[row * SPEC_PARTS + q] = t;
+    }
+}
+
+// First bin whose cumulative power reaches fraction x total (-1: all zero):
+// prefix of the row's partials locates the part, a block scan of that part
+// (tiles of 256 bins) locates the bin.
+__global__ void __launch_bounds__(256) k_spec_find(const double2* __restrict__ spec, int64_t F,
+                                                   const double* __restrict__ partial,
+                                                   double fraction, int64_t* __restrict__ out) {
+    __shared__ double wsum[8];
+    __shared__ double carry;
+    __shared__ int part, found;
+    const int64_t row = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double thr = 0.0;
+    if (threadIdx.x == 0) {
+        const double* p = partial + row * SPEC_PARTS;
+        double tot = 0.0;
+        for (int q = 0; q < SPEC_PARTS; ++q) tot += p[q];
+        part = -1;
+        if (tot > 0.0) {
+            thr = fraction * tot;
+            double acc = 0.0;
+            int q = 0;
+            for (; q < SPEC_PARTS - 1 && acc + p[q] < thr; ++q) acc += p[q];
+            part = q;
+            carry = acc;
+            wsum[0] = thr;
+        }
+        found = 0x7fffffff;
+    }
+    __syncthreads();
+    if (part < 0) {
+        if (threadIdx.x == 0) out[row] = -1;
+        return;
+    }
+    thr = wsum[0];
+    __syncthreads();
+    const int64_t f0 = part_begin(F, part), f1 = part_begin(F, part + 1);
+    for (int64_t base = f0; base < f1; base += 256) {
+        const int64_t f = base + threadIdx.x;
+        double v = f < f1 ? spec_power(spec, F, row, f) : 0.0;
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        if (lane == 31) wsum[w] = v;
+        __syncthreads();
+        double pre = carry;
+        for (int q = 0; q < w; ++q) pre += wsum[q];
+        if (f < f1 && pre + v >= thr) atomicMin(&found, (int)(f - base));
+        __syncthreads();
+        if (found != 0x7fffffff) {
+            if (threadIdx.x == 0) out[row] = base + found;
+            return;
+        }
+        if (threadIdx.x == 255) carry = pre + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[row] = f1 - 1;  // rounding: the part's end reaches thr
+}
+
 }  // namespace mvb
 
 using namespace mvb;
@@ -561,7 +740,7 @@ int mvb_gather_images(const mvb_image* images, const int64_t* idx, int64_t n, mv
 }
 
 int mvb_track_max(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
-                  const double* coarse, const double* tables, const double* paths,
+                  const double* coarse, const double* tables, const double* paths, double negsum,
                   const double* lb, const double* ub, int32_t* scratch, double* dmax,
                   void* stream) {
     if (n_jobs < 1 || n_jobs > 65535) return fail(MVB_EINVAL, "track_max: n_jobs");
@@ -570,7 +749,7 @@ int mvb_track_max(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
     cudaStream_t s = as_stream(stream);
     k_select<<<(unsigned)n_jobs, 256, 0, s>>>(images, jobs, lb, ub, scratch, dmax);
     k_exact_max<<<dim3(64, 8, (unsigned)n_jobs), 256, 0, s>>>(images, jobs, coarse, tables, paths,
-                                                               scratch, dmax);
+                                                               negsum, scratch, dmax);
     return check_launch("track_max");
 }
 
@@ -674,6 +853,45 @@ __global__ void __launch_bounds__(256) k_energy_index(const double* __restrict__
 }
 
 }  // namespace mvb
+
+extern "C" int mvb_decimate_rows(const double* src, const int64_t* rows, int64_t n, int64_t K,
+                                 int64_t N, double* dst, void* stream) {
+    using namespace mvb;
+    if (n < 0 || K < 0 || N < 1) return fail(MVB_EINVAL, "decimate_rows: sizes");
+    if (n == 0 || K == 0) return MVB_OK;
+    if (!src || !rows || !dst) return fail(MVB_EINVAL, "decimate_rows: null");
+    k_decimate_rows<<<grid_for(n * K * 3, 256), 256, 0, as_stream(stream)>>>(src, rows, n, K, N, dst);
+    return check_launch("decimate_rows");
+}
+
+extern "C" int mvb_center_paths(const double* x, int64_t G, int64_t T, double* scratch,
+                                double* out, void* stream) {
+    using namespace mvb;
+    if (G < 0 || G > 65535 || T < 1) return fail(MVB_EINVAL, "center_paths: sizes");
+    if (G == 0) return MVB_OK;
+    if (!x || !scratch || !out) return fail(MVB_EINVAL, "center_paths: null");
+    cudaStream_t s = as_stream(stream);
+    k_path_sums<<<dim3(SPEC_PARTS, (unsigned)G), 256, 0, s>>>(x, T, scratch);
+    unsigned bx = grid_for(3 * T, 256);
+    if (bx > 256) bx = 256;
+    k_path_center<<<dim3(bx, (unsigned)G), 256, 0, s>>>(x, T, scratch, out);
+    return check_launch("center_paths");
+}
+
+extern "C" int mvb_spectrum_index(const double* spec, int64_t G, int64_t F, double fraction,
+                                  double* scratch, int64_t* out, void* stream) {
+    using namespace mvb;
+    if (G < 0 || G > 0x7fffffff / 3 || F < 1 || !(fraction > 0.0 && fraction < 1.0))
+        return fail(MVB_EINVAL, "spectrum_index: args");
+    if (G == 0) return MVB_OK;
+    if (!spec || !scratch || !out) return fail(MVB_EINVAL, "spectrum_index: null");
+    if (3 * G > 65535) return fail(MVB_EINVAL, "spectrum_index: too many paths per call");
+    cudaStream_t s = as_stream(stream);
+    const double2* sp = reinterpret_cast<const double2*>(spec);
+    k_spec_partial<<<dim3(SPEC_PARTS, (unsigned)(3 * G)), 256, 0, s>>>(sp, F, scratch);
+    k_spec_find<<<(unsigned)(3 * G), 256, 0, s>>>(sp, F, scratch, fraction, out);
+    return check_launch("spectrum_index");
+}
 
 extern "C" int mvb_energy_index(const double* pw, int64_t rows, int64_t F, double fraction,
                                 int64_t* out, void* stream) {

@@ -38,11 +38,21 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._dev import ptr, require_cuda, stream_handle
+from ._dev import h2d, ptr, require_cuda, stream_handle
 from .farrow import as_filter, centered_branches
 from .room import image_table
-from .trajectory import (bandwidth_batch, decimate_batch, device_constants, negative_mass,
+from .trajectory import (bandwidth_batch, device_constants, lowpass_batch, negative_mass,
                          phase_fit)
+
+_TRACE = [] if os.environ.get("MVB_TRACE_HOST") else None
+
+
+def _mark(name: str) -> None:
+    """Host-phase timestamps for profiling the planner (env MVB_TRACE_HOST)."""
+    if _TRACE is not None:
+        import time
+        _TRACE.append((name, time.perf_counter()))
+
 
 SYNTH_U = 16  # steps per lane (mvb_synthesize_f32 u_steps)
 TILE = 32 * SYNTH_U  # output samples per CTA
@@ -69,53 +79,6 @@ class Job:
     path_key: object = None  # jobs with equal keys share one source path
 
 
-class _PinnedRing:
-    """Persistent pinned staging ring for the planner's small uploads.
-
-    Arrays are copied into the ring and sent with an asynchronous
-    stream-ordered copy (no host sync, no per-call cudaHostAlloc).  Before
-    the ring wraps, the event recorded after the last copy of the previous
-    lap is awaited, so no staged bytes are overwritten before their copy ran.
-    """
-
-    ALIGN = 256
-
-    def __init__(self, nbytes: int = 16 << 20):
-        self.cap = nbytes
-        self.buf = None
-        self.off = 0
-        self.fence = None
-
-    def put(self, a: np.ndarray, dev) -> torch.Tensor:
-        a = np.ascontiguousarray(a)
-        n = a.nbytes
-        if n > self.cap // 4:  # large arrays: one-off pinned copy (own writable copy)
-            return torch.from_numpy(np.array(a, copy=True)).pin_memory().to(dev, non_blocking=True)
-        if self.buf is None:
-            self.buf = torch.empty(self.cap, dtype=torch.uint8, pin_memory=True)
-            self.host = self.buf.numpy()
-        if self.off + n > self.cap:
-            if self.fence is not None:
-                self.fence.synchronize()
-            self.off = 0
-        self.host[self.off:self.off + n] = a.reshape(-1).view(np.uint8)
-        src = self.buf[self.off:self.off + n].view(_TORCH_DTYPE[a.dtype.str[1:]])
-        out = src.reshape(a.shape).to(dev, non_blocking=True)
-        self.off += -(-max(n, 1) // self.ALIGN) * self.ALIGN
-        if self.fence is None:
-            self.fence = torch.cuda.Event()
-        self.fence.record()
-        return out
-
-
-_TORCH_DTYPE = {"f8": torch.float64, "f4": torch.float32, "i8": torch.int64, "i4": torch.int32,
-                "u1": torch.uint8, "b1": torch.bool}
-_RING = _PinnedRing()
-
-
-def h2d(a: np.ndarray, dev) -> torch.Tensor:
-    """Host array -> device without a host sync (pinned ring staging)."""
-    return _RING.put(np.asarray(a), dev)
 
 
 _POOL = None
@@ -300,6 +263,11 @@ def _group_plan(max_order: int, tiers: tuple, sub: tuple | None):
     return classes, onehot.sum(axis=0), img_tab
 
 
+@lru_cache(maxsize=16)
+def _sm_count(index: int) -> int:
+    return torch.cuda.get_device_properties(index).multi_processor_count
+
+
 _DEV_CACHE: dict = {}
 
 
@@ -371,6 +339,7 @@ class Geometry:
                     K = -(-int(self.T[j]) // N)
                     self.cpath[(j, N)] = row
                     row += K * (1 + int(self.moving[j]))
+        _mark("geom.setup")
         main = torch.cuda.current_stream(dev)
         side = _side_stream(dev) if inputs_ready is not None else main
         if side is not main:
@@ -385,8 +354,10 @@ class Geometry:
         if side is not main:
             main.wait_stream(side)
             self.paths.record_stream(main)
+        _mark("geom.bandwidth")
         self._decimate_paths(path_groups, bws)
         # ---- image table ----------------------------------------------------
+        _mark("geom.decimate")
         self._build_images()
         # ---- job table (geometry fields; render fills the rest) -------------
         self.job_rows = []
@@ -398,6 +369,7 @@ class Geometry:
                 T=int(self.T[j]), mic_moving=int(self.moving[j]), L=0, d0=0, n_chunks=1, nb=0,
                 rate=float(jb.rate), c=float(jb.c), d_min=float(jb.d_min),
                 kappa=float(jb.rate) / float(jb.c)))
+        _mark("geom.images")
         jobs_dev = h2d(pack_jobs(self.job_rows), dev)
         # ---- coarse tracks, bounds, exact max ---------------------------------
         n_img = self.n_images
@@ -419,7 +391,8 @@ class Geometry:
         dmax = torch.empty(nJ, dtype=torch.float64, device=dev)
         _lib.call("mvb_track_max", ptr(self.images), ptr(jobs_dev), nJ,
                   ptr(self.coarse) if self.dec_sel.numel() else ptr(None), ptr(self.tables),
-                  ptr(self.paths), ptr(lb), ptr(ub), ptr(scratch), ptr(dmax), st)
+                  ptr(self.paths), negsum, ptr(lb), ptr(ub), ptr(scratch), ptr(dmax), st)
+        _mark("geom.tracks")
         if dmax_hook is not None:
             dmax_hook(dmax)
         # dmax reaches the host through a pinned copy + event: the render stage
@@ -445,7 +418,7 @@ class Geometry:
     def _path_bandwidths(self, consumer):
         """Paths that need decimation, grouped by (length, rate), and their
         measured bandwidths (trajectory.py:316-339) on the host: one batched
-        FFT per group, one small device->host copy (the only wait)."""
+        FFT per group, one small device->host copy per group (the waits)."""
         jobs = self.jobs
         groups = {}  # (T, rate) -> {row0: position}
         uses = {}  # (T, rate, N) -> list of (position, destination row)
@@ -470,12 +443,7 @@ class Geometry:
                 x.record_stream(consumer)  # read again by the decimation
             out.append((T, rate, x, uses))
             bws.append(bandwidth_batch(x, rate))
-        host = torch.cat(bws).cpu().numpy() if bws else np.zeros(0)
-        split, q = [], 0
-        for _, _, x, _ in out:
-            split.append(host[q:q + x.shape[0]])
-            q += x.shape[0]
-        return out, split
+        return out, bws
 
     def _decimate_paths(self, path_groups, bws):
         """Fill the coarse path slots with pos[::N] (and receiver[::N]).  The
@@ -484,15 +452,29 @@ class Geometry:
         bandwidths; the low-pass runs only for the paths it selects; one
         index_copy per (length, factor)."""
         dev = self.dev
+        st = stream_handle(dev)
         for (T, rate, x, uses), bw in zip(path_groups, bws):
             for (T2, rate2, N), lst in uses.items():
                 if (T2, rate2) != (T, rate):
                     continue
-                coarse = decimate_batch(x, rate, N, bw)  # (G, K, 3)
-                K = coarse.shape[1]
-                info = h2d(np.asarray(lst, dtype=np.int64), dev)
-                dst = (info[:, 1:2] + torch.arange(K, device=dev)[None, :]).reshape(-1)
-                self.paths.index_copy_(0, dst, coarse[info[:, 0]].reshape(-1, 3))
+                K = -(-T // N)
+                nyq = 0.5 * rate / N
+                lp_rows = np.nonzero((bw > nyq) & (bw < 2.0 * nyq))[0] if N > 1 else np.zeros(0)
+                pos = np.asarray([p for p, _ in lst], np.int64)
+                dst = np.asarray([d for _, d in lst], np.int64)
+                raw = ~np.isin(pos, lp_rows)
+                if raw.any():  # straight pos[::N] from the full-rate rows (x is (G, T, 3) contiguous)
+                    rows = h2d(np.stack([pos[raw] * T, dst[raw]], axis=1), dev)
+                    _lib.call("mvb_decimate_rows", ptr(x), ptr(rows), int(raw.sum()), K, N,
+                              ptr(self.paths), st)
+                if (~raw).any():  # anti-alias low-pass first (trajectory.py:279-298)
+                    sel = np.unique(pos[~raw])
+                    lp = lowpass_batch(x[torch.as_tensor(sel, device=dev)], rate, 0.9 * nyq)
+                    lp = lp.contiguous()
+                    where = np.searchsorted(sel, pos[~raw])
+                    rows = h2d(np.stack([where * T, dst[~raw]], axis=1), dev)
+                    _lib.call("mvb_decimate_rows", ptr(lp), ptr(rows), int((~raw).sum()), K, N,
+                              ptr(self.paths), st)
 
     def _build_images(self):
         """Image records of every job: rooms enumerated on the device (one
@@ -697,10 +679,11 @@ class RenderResult:
 
 
 def _chunking(n_imgs, tiles, sm_count):
-    """Images per CTA: enough CTAs for >= 4 waves of 2 CTAs/SM, chunks of
-    >= 128 images (a CTA then does >= 128 x TILE updates)."""
+    """Image chunks per (job, tile): enough CTAs for ~12 waves of 3 CTAs/SM
+    (a partial last wave then costs little), chunks of >= 128 images (a CTA
+    then does >= 128 x TILE updates)."""
     total_tiles = int(sum(tiles))
-    want = 8 * sm_count
+    want = 36 * sm_count
     if total_tiles >= want:
         return [1] * len(n_imgs)
     out = []
@@ -724,7 +707,7 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     L, d0 = int(f.branch_len), int(f.nominal_delay)
     if precision not in ("fp32", "fp64"):
         raise ValueError("precision must be 'fp32' or 'fp64'")
-    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    sm_count = _sm_count(dev.index if dev.index is not None else torch.cuda.current_device())
     # signals: dedupe, upload
     keys = signal_keys or [_key(jobs[j].signal_key, signals[j]) for j in range(nJ)]
     uniq = {}
@@ -795,6 +778,7 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     # ---------------------------------------------------------------- fast --
     # 1. work that does not depend on out_len: interval records and the
     #    per-job delay sort (queued before the host waits for dmax)
+    _mark("render.signals")
     cb, M1, nb = fast_bank(f)
     cb_dev = h2d(np.ascontiguousarray(cb), dev)
     pre_dev = h2d(pack_jobs(base_rows), dev)
@@ -813,6 +797,7 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     _lib.call("mvb_sort_keys", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg, SEG_LEN,
               ptr(geom.paths), ptr(geom.coarse), ptr(key), st)
     launches += 1
+    _mark("render.coeffs_keys")
     order = torch.argsort(key, dim=2)  # (nJ, max_seg, max_img)
     base = h2d(geom.img_off, dev)[:, None, None]
     nimg_dev = h2d(geom.n_img, dev)[:, None, None]
@@ -821,7 +806,9 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     _lib.call("mvb_gather_images", ptr(geom.images), ptr(gidx), gidx.numel(), ptr(images_sorted), st)
     launches += 1  # layout (job, segment, max_img)
     # 2. out_len, zero-padded branch records, work list, synthesis
+    _mark("render.sorted")
     out_len, tau_ceil, offsets, rows = finish_rows()
+    _mark("render.dmax_wait")
     rec_rows, bases = 0, {}
     for k, members in uniq.items():
         front = int(max(tau_ceil[j] for j in members)) + L + PAD_MARGIN
@@ -871,12 +858,14 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         blk[:, :, 4] = cs[:, None]
         blk[:, :, 5] = np.minimum(np.arange(tiles[j]) * TILE // SEG_LEN, n_seg[j] - 1)[None, :]
         blocks.append(blk.reshape(-1, 8))
+    _mark("render.records_plan")
     work = np.concatenate(blocks)
     jobs_dev = h2d(pack_jobs(rows), dev)
     work_dev = h2d(work, dev)
     out = torch.empty(int(out_len.sum()), dtype=torch.float32, device=dev)
     part = torch.empty(max(part_rows, 1), dtype=torch.float32, device=dev)
     ev = _events(timing)
+    _mark("render.work_upload")
     _lib.call("mvb_synthesize_f32", ptr(jobs_dev), ptr(work_dev), len(work), ptr(images_sorted),
               ptr(coef), ptr(rec), ptr(geom.paths), ptr(out), ptr(part), nb, SYNTH_U, st)
     _events_end(timing, ev)
@@ -886,4 +875,5 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
                   ptr(out), st)
         launches += 1
     upd = int(np.sum(out_len * hi))
+    _mark("render.synth_launched")
     return RenderResult(out, offsets, out_len, hi.copy(), upd, launches)

@@ -112,26 +112,36 @@ def device_constants(factor: int, device) -> dict:
     return c
 
 
-def bandwidth_batch(x: torch.Tensor, rate: float, energy_fraction: float = 0.99) -> torch.Tensor:
+def bandwidth_batch(x: torch.Tensor, rate: float, energy_fraction: float = 0.99) -> np.ndarray:
     """Per-path smallest frequency holding `energy_fraction` of the
     mean-removed displacement power, max over axes (reference
-    trajectory.py:316-339), for x (G, T, 3) on the device -> (G,).  The FFT
-    is cuFFT (torch.fft); the energy search is libmvb's mvb_energy_index."""
+    trajectory.py:316-339), for x (G, T, 3) on the device -> host (G,).
+    libmvb removes each axis' mean, cuFFT (torch.fft) transforms the paths
+    along time, libmvb finds each axis' energy index; one small
+    device->host copy.
+    Frequencies follow numpy.fft.rfftfreq: k * (1 / (T * (1 / rate)))."""
     G, T, _ = x.shape
-    if T < 2:
-        return torch.zeros(G, dtype=torch.float64, device=x.device)
-    xc = (x - x.mean(dim=1, keepdim=True)).permute(0, 2, 1).contiguous()  # (G, 3, T)
-    pw = (torch.fft.rfft(xc, dim=2).abs() ** 2).contiguous()  # (G, 3, F)
-    F = pw.shape[2]
+    if T < 2 or G == 0:
+        return np.zeros(G)
+    x = x.contiguous()
+    st = stream_handle(x.device)
+    scratch = torch.empty(3 * G * 64, dtype=torch.float64, device=x.device)
+    xc = torch.empty_like(x)
+    _lib.call("mvb_center_paths", ptr(x), G, T, ptr(scratch), ptr(xc), st)
+    spec = torch.fft.rfft(xc, dim=1)  # (G, F, 3) complex128
+    if not spec.is_contiguous():
+        spec = spec.contiguous()
+    F = spec.shape[1]
     k = torch.empty(G * 3, dtype=torch.int64, device=x.device)
-    _lib.call("mvb_energy_index", ptr(pw), G * 3, F, float(energy_fraction), ptr(k),
-              stream_handle(x.device))
-    f = k.reshape(G, 3).to(torch.float64) * (rate / T)  # empty rows (-1) -> negative
-    return torch.clamp(f, min=0.0).max(dim=1).values
+    _lib.call("mvb_spectrum_index", ptr(spec), G, F, float(energy_fraction), ptr(scratch), ptr(k),
+              st)
+    kh = k.cpu().numpy().reshape(G, 3)
+    hz = np.minimum(kh, F - 1) * (1.0 / (T * (1.0 / rate)))
+    return np.where(kh < 0, 0.0, hz).max(axis=1)
 
 
 def bandwidth_estimate_dev(pos: torch.Tensor, rate: float, energy_fraction: float = 0.99) -> float:
-    return float(bandwidth_batch(pos[None], rate, energy_fraction)[0].item())
+    return float(bandwidth_batch(pos[None], rate, energy_fraction)[0])
 
 
 def lowpass_batch(x: torch.Tensor, rate: float, cutoff: float) -> torch.Tensor:
@@ -160,29 +170,24 @@ def lowpass_columns_dev(x: torch.Tensor, rate: float, cutoff: float) -> torch.Te
 def decimate_batch(x: torch.Tensor, rate: float, factor: int, bw: torch.Tensor | None = None
                    ) -> torch.Tensor:
     """Coarse paths x[:, ::N] of x (G, T, 3), each low-passed first when its
-    measured bandwidth lies in (Nyquist_out, 2 Nyquist_out) -- decided and
-    applied on the device without a host round trip (the low-passed variant
-    is computed for every path and selected per path).  `bw` may carry the
-    paths' bandwidths (bandwidth_batch) when several factors are needed."""
+    measured bandwidth lies in (Nyquist_out, 2 Nyquist_out); the low-pass
+    runs only for those paths.  `bw` may carry the paths' bandwidths
+    (bandwidth_batch, host) when several factors are needed."""
     raw = x[:, ::factor]
     if x.shape[1] < 2 or factor == 1:
         return raw
     nyq = 0.5 * rate / factor
     if bw is None:
         bw = bandwidth_batch(x, rate)
-    if isinstance(bw, np.ndarray):  # decided on the host: low-pass only the paths that need it
-        need = np.nonzero((bw > nyq) & (bw < 2.0 * nyq))[0]
-        if need.size == 0:
-            return raw
-        if need.size == x.shape[0]:
-            return lowpass_batch(x, rate, 0.9 * nyq)[:, ::factor]
-        idx = torch.as_tensor(need, device=x.device)
-        out = raw.clone()
-        out[idx] = lowpass_batch(x[idx], rate, 0.9 * nyq)[:, ::factor]
-        return out
-    use = ((bw > nyq) & (bw < 2.0 * nyq))[:, None, None]
-    lp = lowpass_batch(x, rate, 0.9 * nyq)[:, ::factor]
-    return torch.where(use, lp, raw)
+    need = np.nonzero((bw > nyq) & (bw < 2.0 * nyq))[0]  # low-pass only the paths that need it
+    if need.size == 0:
+        return raw
+    if need.size == x.shape[0]:
+        return lowpass_batch(x, rate, 0.9 * nyq)[:, ::factor]
+    idx = torch.as_tensor(need, device=x.device)
+    out = raw.clone()
+    out[idx] = lowpass_batch(x[idx], rate, 0.9 * nyq)[:, ::factor]
+    return out
 
 
 def decimate_dev(pos: torch.Tensor, rate: float, factor: int) -> torch.Tensor:
