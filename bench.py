@@ -291,15 +291,17 @@ def run_ours(args):
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    results = []
     for k in range(args.steps):
         flush.fill_(float(k))
         res = step(record=True)
-        updates += res.updates
+        results.append(res)  # lengths / update counts are read after the bracket
         launches += res.launches
     e1.record()
     torch.cuda.synchronize()
     barrier()
     total_ms = e0.elapsed_time(e1)
+    updates = sum(r.updates for r in results)
     clk = clocks.stop()
     kern_ms = [a.elapsed_time(b) for a, b in timing]
     t = torch.tensor([total_ms, float(updates), sum(kern_ms)], dtype=torch.float64, device=dev)

@@ -189,14 +189,20 @@ int mvb_coarse_distances(const mvb_image* d_images, const int32_t* d_sel, int64_
                          double negsum, double* d_coarse, double* d_lb, double* d_ub,
                          void* stream);
 
+/* Axis-aligned bounding boxes of every job's source path and receiver:
+ * d_rows (n_jobs, 4) int64 = (source first row, T, receiver first row,
+ * receiver moving); d_bbox: n_jobs x 65 x 12 doubles, the first n_jobs x 12
+ * being (src lo xyz, src hi xyz, mic lo xyz, mic hi xyz), the rest scratch. */
+int mvb_path_bbox(const int64_t* d_rows, int64_t n_jobs, const double* d_paths, double* d_bbox,
+                  void* stream);
+
 /* Bounds of the track maximum of the factor-1 images d_full_sel: lb =
  * exact distance at the first / middle / last sample, ub = the largest
- * distance between the bounding boxes of the image path and the receiver.
- * d_bbox: n_jobs x 65 x 12 doubles of scratch (path bounding boxes and
- * their partial reductions). */
+ * distance between the bounding boxes (d_bbox, mvb_path_bbox) of the image
+ * path and the receiver. */
 int mvb_track_bounds(const mvb_image* d_images, const int32_t* d_full_sel, int64_t n_full,
-                     const mvb_job* d_jobs, int64_t n_jobs, const double* d_paths,
-                     double* d_bbox, double* d_lb, double* d_ub, void* stream);
+                     const mvb_job* d_jobs, const double* d_paths, const double* d_bbox,
+                     double* d_lb, double* d_ub, void* stream);
 
 /* Exact track max of every job (d_dmax[n_jobs]): only the images whose ub
  * reaches the job's largest lb are evaluated (exact distance for factor 1,
@@ -208,6 +214,15 @@ int mvb_track_max(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jo
                   const double* d_coarse, const double* d_tables, const double* d_paths,
                   double negsum, const double* d_lb, const double* d_ub, int32_t* d_scratch,
                   double* d_dmax, void* stream);
+
+/* Exact output lengths on the device (synth.py:211-212): for every job,
+ * len(s) + ceil(rate * d_dmax[j] / c) + L with len(s) = ls - L + 1, written
+ * into d_jobs[j].out_len (which holds the host's capacity on entry; the
+ * render kernels mask by it) and d_lengths[j]; *d_err = 1 if a length
+ * exceeds its capacity.  Lets the host plan from an upper bound without
+ * waiting for the track maxima. */
+int mvb_finalize_lengths(mvb_job* d_jobs, int64_t n_jobs, const double* d_dmax,
+                         int64_t* d_lengths, int32_t* d_err, void* stream);
 
 /* d_out[q] = d_images[d_idx[q]], q < n (delay-sorted image tables). */
 int mvb_gather_images(const mvb_image* d_images, const int64_t* d_idx, int64_t n,

@@ -73,6 +73,32 @@ _TORCH_DTYPE = {"f8": torch.float64, "f4": torch.float32, "i8": torch.int64, "i4
 _RING = _PinnedRing()
 
 
+_PINNED: dict = {}
+
+
+def pinned_scratch(name: str, n: int, dtype) -> torch.Tensor:
+    """Persistent pinned host scratch `name` for small readbacks whose copy
+    the caller waits for before the next use.  Pinned (not pageable) so a
+    readback on a side stream waits only for that stream -- a pageable
+    device->host copy also waits for the legacy default stream -- and
+    persistent so no per-call cudaHostAlloc (which synchronises the device)."""
+    t = _PINNED.get(name)
+    if t is None or t.numel() < n or t.dtype != dtype:
+        t = _PINNED[name] = torch.empty(max(n, 1024), dtype=dtype, pin_memory=True)
+    return t[:n]
+
+
+def readback(t: torch.Tensor, name: str) -> np.ndarray:
+    """Small device tensor -> numpy through pinned scratch, waiting only for
+    the current stream's work up to here."""
+    host = pinned_scratch(name, t.numel(), t.dtype)
+    host.copy_(t.reshape(-1), non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record()
+    ev.synchronize()
+    return host.numpy().copy().reshape(t.shape)
+
+
 def h2d(a: np.ndarray, dev) -> torch.Tensor:
     """Host array -> device without a host sync (pinned ring staging)."""
     return _RING.put(np.asarray(a), dev)

@@ -37,7 +37,9 @@ _SIGS = {
     "mvb_enumerate": [P, P, I64, INT, P, P, P, P, P, P, P],
     "mvb_build_images": [P, P, P, I64, P, I64, P, I64, P, I64, P, P, I64, P, I64, P, P],
     "mvb_coarse_distances": [P, P, I64, I64, P, P, DBL, P, P, P, P],
-    "mvb_track_bounds": [P, P, I64, P, I64, P, P, P, P, P],
+    "mvb_track_bounds": [P, P, I64, P, P, P, P, P, P],
+    "mvb_path_bbox": [P, I64, P, P, P],
+    "mvb_finalize_lengths": [P, I64, P, P, P, P],
     "mvb_track_max": [P, P, I64, P, P, P, DBL, P, P, P, P, P],
     "mvb_gather_images": [P, P, I64, P, P],
     "mvb_track_coeffs": [P, P, I64, I64, P, P, P, P, P],

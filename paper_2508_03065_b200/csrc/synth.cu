@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     const mvb_job* Jp = jobs + wp->job;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int n0 = wp->tile * TN;
+    if (n0 >= Jp->out_len) return;  // tile planned for the length bound only
     const int T = Jp->T;
     const int Lsh = Jp->L;
     // rows are indexed globally: row = rec_base + (n + L - D) >= 0 thanks to

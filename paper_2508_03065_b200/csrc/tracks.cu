@@ -143,14 +143,15 @@ constexpr int BBOX_WORDS = 12;
 
 __device__ __forceinline__ double block_min(double v, double* red) { return -block_max(-v, red); }
 
-__global__ void k_path_bbox(const mvb_job* __restrict__ jobs, const double* __restrict__ paths,
+// rows[j] = (source path first row, T, receiver first row, receiver moving)
+__global__ void k_path_bbox(const int64_t* __restrict__ rows, const double* __restrict__ paths,
                             int64_t n_jobs, double* __restrict__ bbox) {
     __shared__ double red[32];
-    const mvb_job& J = jobs[blockIdx.y];
+    const int64_t* R = rows + 4 * blockIdx.y;
     double* part = bbox + BBOX_WORDS * (n_jobs + (int64_t)blockIdx.y * BBOX_PARTS + blockIdx.x);
     for (int which = 0; which < 2; ++which) {
-        const double* P = paths + 3 * (which == 0 ? J.pos_off : J.mic_off);
-        const int64_t n = which == 0 || J.mic_moving ? J.T : 1;
+        const double* P = paths + 3 * (which == 0 ? R[0] : R[2]);
+        const int64_t n = which == 0 || R[3] ? R[1] : 1;
         double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
         for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
              t += (int64_t)gridDim.x * blockDim.x) {
@@ -712,21 +713,54 @@ int mvb_coarse_distances(const mvb_image* images, const int32_t* sel, int64_t n_
     return check_launch("coarse_distances");
 }
 
+int mvb_path_bbox(const int64_t* rows, int64_t n_jobs, const double* paths, double* bbox,
+                  void* stream) {
+    if (n_jobs < 0 || n_jobs > 65535) return fail(MVB_EINVAL, "path_bbox: n_jobs");
+    if (n_jobs == 0) return MVB_OK;
+    if (!rows || !paths || !bbox) return fail(MVB_EINVAL, "path_bbox: null");
+    cudaStream_t s = as_stream(stream);
+    k_path_bbox<<<dim3(BBOX_PARTS, (unsigned)n_jobs), 256, 0, s>>>(rows, paths, n_jobs, bbox);
+    k_bbox_reduce<<<grid_for(n_jobs, 128), 128, 0, s>>>(n_jobs, bbox);
+    return check_launch("path_bbox");
+}
+
 int mvb_track_bounds(const mvb_image* images, const int32_t* full_sel, int64_t n_full,
-                     const mvb_job* jobs, int64_t n_jobs, const double* paths, double* bbox,
-                     double* lb, double* ub, void* stream) {
-    if (n_full < 0 || n_full > 0x7fffffff || n_jobs < 1 || n_jobs > 0x7fffffff)
-        return fail(MVB_EINVAL, "track_bounds: sizes");
+                     const mvb_job* jobs, const double* paths, const double* bbox, double* lb,
+                     double* ub, void* stream) {
+    if (n_full < 0 || n_full > 0x7fffffff) return fail(MVB_EINVAL, "track_bounds: sizes");
     if (n_full == 0) return MVB_OK;
     if (!images || !full_sel || !jobs || !paths || !bbox || !lb || !ub)
         return fail(MVB_EINVAL, "track_bounds: null");
-    cudaStream_t s = as_stream(stream);
-    if (n_jobs > 65535) return fail(MVB_EINVAL, "track_bounds: n_jobs");
-    k_path_bbox<<<dim3(BBOX_PARTS, (unsigned)n_jobs), 256, 0, s>>>(jobs, paths, n_jobs, bbox);
-    k_bbox_reduce<<<grid_for(n_jobs, 128), 128, 0, s>>>(n_jobs, bbox);
-    k_bounds_full<<<grid_for(n_full, 128), 128, 0, s>>>(images, full_sel, n_full, jobs, paths, bbox,
-                                                        lb, ub);
+    k_bounds_full<<<grid_for(n_full, 128), 128, 0, as_stream(stream)>>>(images, full_sel, n_full, jobs,
+                                                                       paths, bbox, lb, ub);
     return check_launch("track_bounds");
+}
+
+// out_len of every job from its exact track maximum, as synth.py:211-212:
+// len(s) + ceil(rate * dmax / c) + L, written into the job table (the
+// kernels mask by it); lengths[j] for the host; err = 1 if a length exceeds
+// the capacity the host planned (jobs[j].out_len on entry).
+__global__ void k_finalize_lengths(mvb_job* __restrict__ jobs, int64_t n_jobs,
+                                   const double* __restrict__ dmax, int64_t* __restrict__ lengths,
+                                   int32_t* __restrict__ err) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= n_jobs) return;
+    mvb_job& J = jobs[j];
+    const int64_t sig_len = J.ls - J.L + 1;
+    const int64_t len = sig_len + (int64_t)ceil(J.rate * dmax[j] / J.c) + J.L;
+    if (len > J.out_len) atomicExch(err, 1);
+    J.out_len = len < J.out_len ? len : J.out_len;
+    lengths[j] = len;
+}
+
+int mvb_finalize_lengths(mvb_job* jobs, int64_t n_jobs, const double* dmax, int64_t* lengths,
+                         int32_t* err, void* stream) {
+    if (n_jobs < 0) return fail(MVB_EINVAL, "finalize_lengths: n_jobs");
+    if (n_jobs == 0) return MVB_OK;
+    if (!jobs || !dmax || !lengths || !err) return fail(MVB_EINVAL, "finalize_lengths: null");
+    k_finalize_lengths<<<grid_for(n_jobs, 128), 128, 0, as_stream(stream)>>>(jobs, n_jobs, dmax,
+                                                                            lengths, err);
+    return check_launch("finalize_lengths");
 }
 
 int mvb_gather_images(const mvb_image* images, const int64_t* idx, int64_t n, mvb_image* out,

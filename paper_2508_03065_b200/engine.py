@@ -38,7 +38,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._dev import h2d, ptr, require_cuda, stream_handle
+from ._dev import h2d, pinned_scratch, ptr, require_cuda, stream_handle
 from .farrow import as_filter, centered_branches
 from .room import image_table
 from .trajectory import (bandwidth_batch, device_constants, lowpass_batch, negative_mass,
@@ -181,10 +181,12 @@ _SIDE = {}
 
 def _side_stream(dev) -> torch.cuda.Stream:
     """Per-device side stream for input staging that must not queue behind
-    the current stream."""
+    the current stream.  Highest priority: its few small kernels (path
+    copies, boxes, bandwidth FFT) are scheduled ahead of the pending CTAs of
+    a running synthesis instead of after them."""
     key = str(dev)
     if key not in _SIDE:
-        _SIDE[key] = torch.cuda.Stream(device=dev)
+        _SIDE[key] = torch.cuda.Stream(device=dev, priority=-64)
     return _SIDE[key]
 
 
@@ -350,10 +352,24 @@ class Geometry:
                 _STAGER.upload(host_parts, self.paths)
             for r0, p in dev_parts:
                 self.paths[r0:r0 + p.shape[0]].copy_(p)
+            # bounding boxes of every source path and receiver: the host bounds
+            # each job's output length from them (no wait for the track maxima)
+            box_rows = h2d(np.stack([self.pos_off, self.T, self.mic_off, self.moving], axis=1), dev)
+            # flat: the nJ x 12 boxes first, then the 64 partial boxes per job
+            self.bbox = torch.empty(nJ * 65 * 12, dtype=torch.float64, device=dev)
+            _lib.call("mvb_path_bbox", ptr(box_rows), nJ, ptr(self.paths), ptr(self.bbox),
+                      stream_handle(dev))
+            box_host = pinned_scratch("bbox", nJ * 12, torch.float64).view(nJ, 12)
+            box_host.copy_(self.bbox[:nJ * 12].view(nJ, 12), non_blocking=True)
+            box_ready = torch.cuda.Event()
+            box_ready.record()
             path_groups, bws = self._path_bandwidths(main)  # host waits for `side` only
+        box_ready.synchronize()
+        self.bbox_host = box_host.numpy().copy()
         if side is not main:
             main.wait_stream(side)
             self.paths.record_stream(main)
+            self.bbox.record_stream(main)
         _mark("geom.bandwidth")
         self._decimate_paths(path_groups, bws)
         # ---- image table ----------------------------------------------------
@@ -383,9 +399,8 @@ class Geometry:
                       self.dec_sel.numel(), max_K, ptr(jobs_dev), ptr(self.paths), negsum,
                       ptr(self.coarse), ptr(lb), ptr(ub), st)
         if self.full_sel.numel():  # bounding-box bounds of the full-rate images
-            bbox = torch.empty(nJ, 65, 12, dtype=torch.float64, device=dev)  # boxes + partials
             _lib.call("mvb_track_bounds", ptr(self.images), ptr(self.full_sel),
-                      self.full_sel.numel(), ptr(jobs_dev), nJ, ptr(self.paths), ptr(bbox),
+                      self.full_sel.numel(), ptr(jobs_dev), ptr(self.paths), ptr(self.bbox),
                       ptr(lb), ptr(ub), st)
         scratch = torch.empty(n_img + nJ, dtype=torch.int32, device=dev)
         dmax = torch.empty(nJ, dtype=torch.float64, device=dev)
@@ -395,23 +410,17 @@ class Geometry:
         _mark("geom.tracks")
         if dmax_hook is not None:
             dmax_hook(dmax)
-        # dmax reaches the host through a pinned copy + event: the render stage
-        # queues its out_len-independent kernels before it waits (dmax_host)
-        self._dmax_host = torch.empty(nJ, dtype=torch.float64, pin_memory=True)
-        self._dmax_host.copy_(dmax, non_blocking=True)
-        self._dmax_ready = torch.cuda.Event()
-        self._dmax_ready.record()
-        self._dmax = None
+        self.dmax_dev = dmax
+        self._dmax = None  # host copy on demand (the render itself never waits for it)
         self.launches = self.n_enum_launches + (1 if self.dec_sel.numel() else 0) \
             + (2 if self.full_sel.numel() else 0) + 2
         self.eval_count = [int(self.evals[j]) for j in range(nJ)]
 
     @property
     def dmax(self) -> np.ndarray:
-        """Per-job exact track maximum (waits for the geometry kernels only)."""
+        """Per-job exact track maximum (waits for the geometry kernels)."""
         if self._dmax is None:
-            self._dmax_ready.synchronize()
-            self._dmax = self._dmax_host.numpy().copy()
+            self._dmax = self.dmax_dev.cpu().numpy()
         return self._dmax
 
     # ------------------------------------------------------------------------
@@ -594,6 +603,29 @@ class Geometry:
             raise ValueError("more than 65535 full-rate images in one batch")
 
     # ------------------------------------------------------------------------
+    def length_bound(self, j: int) -> int:
+        """Upper bound of ceil(rate * dmax_j / c) from the image lattice extent
+        and the path / receiver bounding boxes, known on the host without
+        waiting for the tracks.  Image coordinate along axis a:
+        2 l_a L_a + s_a p_a with |2 l_a L_a| <= (|j_a| + 1) L_a and
+        sum |j_a| <= max_order, so the distance is at most
+        max_a sqrt(((K+1) L_a + P_a + M_a)^2 + sum_{b != a} (L_b + P_b + M_b)^2)
+        (P, M: largest source / receiver coordinate magnitudes); widened by
+        the upsampler's overshoot (negative tap mass) and a 2% + 1 cm margin
+        for the anti-alias low-pass.  mvb_finalize_lengths checks it."""
+        jb = self.jobs[j]
+        box = self.bbox_host[j]
+        P = np.maximum(np.abs(box[0:3]), np.abs(box[3:6]))
+        M = np.maximum(np.abs(box[6:9]), np.abs(box[9:12]))
+        dims = np.asarray(jb.dims, dtype=np.float64).reshape(3)
+        K = int(jb.max_order)
+        base = dims + P + M
+        ext = (K + 1) * dims + P + M
+        d2 = max(ext[a] ** 2 + sum(base[b] ** 2 for b in range(3) if b != a) for a in range(3))
+        neg = max([negative_mass(int(N)) for _, N in jb.tiers if int(N) > 1], default=0.0)
+        d_ub = 1.02 * math.sqrt(d2) * (1.0 + neg) + 0.01
+        return int(math.ceil(float(jb.rate) * d_ub / float(jb.c)))
+
     def tau_max(self, j: int) -> float:
         jb = self.jobs[j]
         return float(jb.rate) * float(self.dmax[j]) / float(jb.c)
@@ -661,14 +693,38 @@ def _events_end(timing, e0):
         timing.append((e0, e1))
 
 
-@dataclass
 class RenderResult:
-    out: torch.Tensor  # flat output (fp32 fast / fp64 exact)
-    offsets: np.ndarray  # per-job start in `out`
-    lengths: np.ndarray  # per-job out_len
-    n_images: np.ndarray  # per-job images rendered
-    updates: int  # image x output-sample updates computed
-    launches: int  # libmvb kernel launches in the render stage
+    """Output of a batch render.  `out` is the flat output (fp32 fast / fp64
+    exact) with job j at offsets[j], capacity[j] samples reserved (zeros
+    past its length).  The exact lengths are computed on the device
+    (mvb_finalize_lengths); `lengths`, `updates` and `job()` wait for them
+    on first use, so a render can be queued without a host round trip."""
+
+    def __init__(self, out, offsets, capacity, n_images, launches, lengths_dev, err_dev):
+        self.out = out
+        self.offsets = offsets
+        self.capacity = capacity
+        self.n_images = n_images
+        self.launches = launches
+        self._lengths = None
+        self._dev = (lengths_dev, err_dev)  # read on first use (no per-render pinned buffers)
+
+    @property
+    def lengths(self) -> np.ndarray:
+        """Per-job out_len (synth.py:211-212)."""
+        if self._lengths is None:
+            lengths_dev, err_dev = self._dev
+            h = torch.cat([lengths_dev, err_dev.to(torch.int64)]).cpu().numpy()
+            if h[-1]:
+                raise _lib.MvbError("output length exceeded its planned bound "
+                                    f"(lengths {h[:-1].tolist()}, capacity {self.capacity.tolist()})")
+            self._lengths = h[:-1].copy()
+        return self._lengths
+
+    @property
+    def updates(self) -> int:
+        """image x output-sample updates computed."""
+        return int(np.sum(self.lengths * self.n_images))
 
     def job(self, j: int) -> torch.Tensor:
         return self.out[self.offsets[j]:self.offsets[j] + self.lengths[j]]
@@ -737,11 +793,13 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     base_rows = [dict(r, L=L, d0=d0) for r in geom.job_rows]
 
     def finish_rows():
-        """out_len needs the exact track max (waits for the geometry kernels)."""
+        """Capacities from the host-side bound of every output length (no
+        wait for the geometry kernels); the exact lengths are written into
+        the device job table by mvb_finalize_lengths (finalize)."""
         out_len = np.zeros(nJ, np.int64)
         tau_ceil = np.zeros(nJ, np.int64)
         for j in range(nJ):
-            tau_ceil[j] = int(math.ceil(geom.tau_max(j)))
+            tau_ceil[j] = geom.length_bound(j)
             out_len[j] = sig_len[keys[j]] + tau_ceil[j] + L
         offsets = np.concatenate([[0], np.cumsum(out_len)[:-1]]).astype(np.int64)
         rows = [dict(r) for r in base_rows]
@@ -749,6 +807,13 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
             rows[j].update(out_off=int(offsets[j]), out_len=int(out_len[j]),
                            ls=int(sig_len[keys[j]] + L - 1))
         return out_len, tau_ceil, offsets, rows
+
+    def finalize(jobs_dev):
+        lengths = torch.empty(nJ, dtype=torch.int64, device=dev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.call("mvb_finalize_lengths", ptr(jobs_dev), nJ, ptr(geom.dmax_dev), ptr(lengths),
+                  ptr(err), st)
+        return lengths, err
 
     if precision == "fp64":
         nb = int(f.poly_order) + 1
@@ -766,14 +831,14 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         for j in range(nJ):
             rows[j].update(rec_base=bases[keys[j]], nb=nb)
         jobs_dev = h2d(pack_jobs(rows), dev)
-        out = torch.empty(int(out_len.sum()), dtype=torch.float64, device=dev)
+        lengths, err = finalize(jobs_dev)
+        out = torch.zeros(int(out_len.sum()), dtype=torch.float64, device=dev)
         ev = _events(timing)
         _lib.call("mvb_synthesize_f64", ptr(jobs_dev), nJ, int(out_len.max()), ptr(geom.images),
                   ptr(geom.coarse), ptr(geom.tables), ptr(streams), ptr(geom.paths), ptr(out), st)
         _events_end(timing, ev)
-        launches += 1
-        upd = int(np.sum(out_len * geom.n_img))
-        return RenderResult(out, offsets, out_len, geom.n_img.copy(), upd, launches)
+        launches += 2
+        return RenderResult(out, offsets, out_len, geom.n_img.copy(), launches, lengths, err)
 
     # ---------------------------------------------------------------- fast --
     # 1. work that does not depend on out_len: interval records and the
@@ -808,7 +873,7 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     # 2. out_len, zero-padded branch records, work list, synthesis
     _mark("render.sorted")
     out_len, tau_ceil, offsets, rows = finish_rows()
-    _mark("render.dmax_wait")
+    _mark("render.plan_lengths")
     rec_rows, bases = 0, {}
     for k, members in uniq.items():
         front = int(max(tau_ceil[j] for j in members)) + L + PAD_MARGIN
@@ -862,7 +927,9 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     work = np.concatenate(blocks)
     jobs_dev = h2d(pack_jobs(rows), dev)
     work_dev = h2d(work, dev)
-    out = torch.empty(int(out_len.sum()), dtype=torch.float32, device=dev)
+    lengths, err = finalize(jobs_dev)
+    launches += 1
+    out = torch.zeros(int(out_len.sum()), dtype=torch.float32, device=dev)
     part = torch.empty(max(part_rows, 1), dtype=torch.float32, device=dev)
     ev = _events(timing)
     _mark("render.work_upload")
@@ -874,6 +941,5 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         _lib.call("mvb_reduce_partials_f32", ptr(jobs_dev), nJ, int(out_len.max()), ptr(part),
                   ptr(out), st)
         launches += 1
-    upd = int(np.sum(out_len * hi))
     _mark("render.synth_launched")
-    return RenderResult(out, offsets, out_len, hi.copy(), upd, launches)
+    return RenderResult(out, offsets, out_len, hi.copy(), launches, lengths, err)

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._dev import ptr, require_cuda, stream_handle, to_dev
+from ._dev import ptr, readback, require_cuda, stream_handle, to_dev
 
 UPSAMPLE_HALFWIDTH = 32
 UPSAMPLE_KAISER_BETA = 7.857
@@ -135,7 +135,7 @@ def bandwidth_batch(x: torch.Tensor, rate: float, energy_fraction: float = 0.99)
     k = torch.empty(G * 3, dtype=torch.int64, device=x.device)
     _lib.call("mvb_spectrum_index", ptr(spec), G, F, float(energy_fraction), ptr(scratch), ptr(k),
               st)
-    kh = k.cpu().numpy().reshape(G, 3)
+    kh = readback(k, "bandwidth_index").reshape(G, 3)
     hz = np.minimum(kh, F - 1) * (1.0 / (T * (1.0 / rate)))
     return np.where(kh < 0, 0.0, hz).max(axis=1)
 

@@ -226,7 +226,8 @@ def test_image_shards_sum_to_full_render():
              for r in range(world)]
     assert all(np.array_equal(p.lengths, full.lengths) for p in parts)
     assert sum(p.updates for p in parts) == full.updates
-    total = sum(p.out.double() for p in parts).cpu().numpy()
+    total = np.concatenate([sum(p.job(j).double() for p in parts).cpu().numpy()
+                            for j in range(len(jobs))])
     ref = np.concatenate(_oracle(scenes, chans, g["branches"]))
     assert rel_err(total, ref) <= FP32_TOL
     with pytest.raises(ValueError):
