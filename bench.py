@@ -63,9 +63,13 @@ def workload_note(name):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms."""
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms from before
+    the warm-up (nvidia-smi's start-up must not overlap the timed steps);
+    each sample is timestamped and the summary keeps the samples taken
+    during the timed window (widened to the nearest samples when the window
+    is shorter than the sampling period)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -78,36 +82,50 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=self.file, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
 
-    def stop(self):
+    def stop(self, t0=None, t1=None):
+        """Summary of the samples within [t0, t1] (host wall-clock seconds)."""
+        import datetime
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        time.sleep(0.15)
         self.proc.terminate()
         self.proc.wait()
         self.file.flush()
         self.file.seek(0)
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for line in self.file.read().splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1]))
-                smax = float(f[2])
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[2]), float(f[3]), f[6:10]))
             except ValueError:
                 continue
-            for n, v in zip(names, f[5:9]):
+        os.unlink(self.file.name)
+        sel = rows
+        if t0 is not None and rows:
+            inside = [r for r in rows if t0 <= r[0] <= t1]
+            if not inside:  # window shorter than the period: nearest samples around it
+                before = [r for r in rows if r[0] < t0][-1:]
+                after = [r for r in rows if r[0] > t1][:1]
+                inside = before + after
+            sel = inside
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in sel:
+            for n, v in zip(names, r[3]):
                 if v.lower() in ("active", "1"):
                     reasons.add(n)
-        os.unlink(self.file.name)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [r[1] for r in sel]
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": sel[-1][2] if sel else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
 
 
 # ----------------------------------------------------------------------------
@@ -269,6 +287,10 @@ def run_ours(args):
     if not args.profile:
         ffma_tf, l1_gbs = measured_peaks(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    clocks = ClockSampler(local)
+    if not args.profile:
+        clocks.start()
+        time.sleep(0.3)  # let nvidia-smi start before the warm-up
     for _ in range(args.warmup):
         res = step()
     torch.cuda.synchronize()
@@ -278,8 +300,6 @@ def run_ours(args):
             step()
         torch.cuda.synchronize()
         return
-    clocks = ClockSampler(local)
-    clocks.start()
     total_ms = 0.0
     updates = 0
     launches = 0
@@ -290,6 +310,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
     e0.record()
     results = []
     for k in range(args.steps):
@@ -300,9 +321,10 @@ def run_ours(args):
     e1.record()
     torch.cuda.synchronize()
     barrier()
+    wall1 = time.time()
     total_ms = e0.elapsed_time(e1)
     updates = sum(r.updates for r in results)
-    clk = clocks.stop()
+    clk = clocks.stop(wall0, wall1)
     kern_ms = [a.elapsed_time(b) for a, b in timing]
     t = torch.tensor([total_ms, float(updates), sum(kern_ms)], dtype=torch.float64, device=dev)
     if world > 1:
