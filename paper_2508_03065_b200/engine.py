@@ -190,13 +190,18 @@ def _side_stream(dev) -> torch.cuda.Stream:
     return _SIDE[key]
 
 
-def d2h(t: torch.Tensor) -> np.ndarray:
-    """Device tensor -> numpy through pinned memory (caching host
-    allocator), waiting only for the producing stream."""
-    host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-    host.copy_(t, non_blocking=True)
+def d2h(t: torch.Tensor, dtype=None) -> np.ndarray:
+    """Device tensor -> new numpy array (optionally converted to `dtype`):
+    one copy into persistent pinned staging (waits only for the producing
+    stream), then a threaded copy out -- no per-call pinned allocation,
+    whose cudaHostAlloc would synchronise the device."""
+    host = pinned_scratch("d2h_" + str(t.dtype), t.numel(), t.dtype)
+    host.copy_(t.reshape(-1), non_blocking=True)
     torch.cuda.current_stream(t.device).synchronize()
-    return host.numpy()
+    src = host.numpy()
+    out = np.empty(t.numel(), dtype=src.dtype if dtype is None else dtype)
+    parallel_copy([(out, src)])
+    return out.reshape(tuple(t.shape))
 
 
 def _key(explicit, obj):

@@ -275,7 +275,7 @@ def synthesize(s, streams: DelayStreams, f, cfg) -> np.ndarray:
     prec = _precision(a, cfg)
     res = engine.render(streams.geometry, [a], filt, precision=prec)
     from .engine import d2h
-    return d2h(res.job(0)).astype(np.float64)
+    return d2h(res.job(0), np.float64)
 
 
 def _synthesize_source(x, streams, f, cfg) -> np.ndarray:
