@@ -88,11 +88,17 @@ int mvb_enumerate(const double* d_dims, const double* d_walls, int64_t n_rooms,
  *    (x, y, z) rows holding every source path, receiver path/position and
  *    decimated path.  Every kernel below covers the whole batch per launch.
  *
- *    Call order: coarse_distances -> track_bounds -> track_max (-> host:
- *    out_len = len(s) + ceil(rate*dmax/c) + L, synth.py:211-212) ->
- *      fast:  branch_records_f32, track_coeffs, sort_keys, rank,
- *             synthesize_f32 [, reduce_partials_f32]
- *      exact: branch_filter (per signal), synthesize_f64
+ *    Call order (no host wait after the decimation decision):
+ *      paths:  path_bbox; center_paths -> (cuFFT rFFT) -> spectrum_index
+ *              (host: low-pass decision, output capacity bound from the
+ *              boxes) -> decimate_rows
+ *      images: enumerate -> build_images
+ *      tracks: coarse_distances (+ bounds) -> track_bounds -> track_max
+ *      fast:   branch_records_f32, track_coeffs, sort_keys (-> sort) ->
+ *              gather_images, finalize_lengths (exact out_len = len(s) +
+ *              ceil(rate*dmax/c) + L, synth.py:211-212, on the device) ->
+ *              synthesize_f32 [-> reduce_partials_f32]
+ *      exact:  branch_filter (per signal), finalize_lengths, synthesize_f64
  * --------------------------------------------------------------------- */
 
 /* One image of one job (96 B). */
