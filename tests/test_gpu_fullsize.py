@@ -80,3 +80,15 @@ def test_c5_moving_array_windows():
     for ch in (0, 5):
         err, peak = _windows(_oracle(sc, ch, f), res.job(ch).double().cpu().numpy(), n_win=3)
         assert err <= TOL * peak
+
+
+def test_c3_whole_output_against_oracle():
+    """The whole c3 render (537k samples x 11521 images, 6.2e9 updates)
+    against the CPU oracle on every host thread (~30 s): max error over every
+    output sample, relative to the true output peak."""
+    sc = workloads.make_scenes("c3")[0]
+    f = hann_sinc(sc.fd_taps, 14)
+    y = render_jobs(scene_jobs([sc]), f).job(0).double().cpu().numpy()
+    ref = _oracle(sc, 0, f).render()
+    assert y.size == ref.size
+    assert rel_err(y, ref) <= TOL
