@@ -179,6 +179,50 @@ _STAGER = _BulkStager()
 _SIDE = {}
 
 
+class _PathArena:
+    """Persistent device buffers for the paths of renders staged on the side
+    stream (Geometry with inputs_ready).  A buffer is handed out again only
+    after the event recorded when its render was fully enqueued has
+    completed, so no render overwrites paths a queued kernel still reads;
+    buffers are never freed, so no allocator events or cudaMalloc (which can
+    stall behind running kernels) sit on the staging path.  At most DEPTH
+    buffers: a deeper pipeline waits for the oldest render."""
+
+    DEPTH = 3
+
+    def __init__(self):
+        self.bufs = {}  # device -> list of [tensor, event | None]
+
+    def acquire(self, dev, rows: int) -> torch.Tensor:
+        lst = self.bufs.setdefault(str(dev), [])
+        idle = [b for b in lst if b[1] is None or (b[1] is not False and b[1].query())]
+        fits = [b for b in idle if b[0].shape[0] >= rows]
+        if fits:
+            b = fits[0]
+        elif len(lst) < self.DEPTH:
+            b = [torch.empty(max(rows, 1 << 16), 3, dtype=torch.float64, device=dev), None]
+            lst.append(b)
+        else:  # pipeline full: wait for the oldest released render, grow if needed
+            released = [x for x in lst if x[1] is not False]
+            if not released:  # every buffer held by an unreleased geometry
+                return torch.empty(rows, 3, dtype=torch.float64, device=dev)
+            b = released[0]
+            if b[1] is not None:
+                b[1].synchronize()
+            if b[0].shape[0] < rows:
+                b[0] = torch.empty(rows, 3, dtype=torch.float64, device=dev)
+        b[1] = False  # in use until release
+        return b[0]
+
+    def release(self, dev, t: torch.Tensor, event) -> None:
+        for b in self.bufs.get(str(dev), []):
+            if b[0] is t:
+                b[1] = event
+
+
+_ARENA = _PathArena()
+
+
 def _side_stream(dev) -> torch.cuda.Stream:
     """Per-device side stream for input staging that must not queue behind
     the current stream.  Highest priority: its few small kernels (path
@@ -352,7 +396,12 @@ class Geometry:
         if side is not main:
             side.wait_event(inputs_ready)
         with torch.cuda.stream(side):
-            self.paths = torch.empty(max(row, 1), 3, dtype=torch.float64, device=dev)
+            if side is not main:  # persistent arena buffer (released by render_jobs)
+                self._arena = _ARENA.acquire(dev, max(row, 1))
+                self.paths = self._arena[:max(row, 1)]
+            else:
+                self._arena = None
+                self.paths = torch.empty(max(row, 1), 3, dtype=torch.float64, device=dev)
             if host_parts:
                 _STAGER.upload(host_parts, self.paths)
             for r0, p in dev_parts:
@@ -373,7 +422,6 @@ class Geometry:
         self.bbox_host = box_host.numpy().copy()
         if side is not main:
             main.wait_stream(side)
-            self.paths.record_stream(main)
             self.bbox.record_stream(main)
         _mark("geom.bandwidth")
         self._decimate_paths(path_groups, bws)
@@ -420,6 +468,16 @@ class Geometry:
         self.launches = self.n_enum_launches + (1 if self.dec_sel.numel() else 0) \
             + (2 if self.full_sel.numel() else 0) + 2
         self.eval_count = [int(self.evals[j]) for j in range(nJ)]
+
+    def release(self) -> None:
+        """Hand the staging buffer back (after every kernel reading the paths
+        has been enqueued on the current stream); the geometry's tracks may
+        not be used afterwards."""
+        if getattr(self, "_arena", None) is not None:
+            ev = torch.cuda.Event()
+            ev.record()
+            _ARENA.release(self.dev, self._arena, ev)
+            self._arena = None
 
     @property
     def dmax(self) -> np.ndarray:
@@ -730,6 +788,18 @@ class RenderResult:
     def updates(self) -> int:
         """image x output-sample updates computed."""
         return int(np.sum(self.lengths * self.n_images))
+
+    @staticmethod
+    def concat(parts: list) -> "RenderResult":
+        """One result for consecutive sub-batches (outputs concatenated)."""
+        shift = np.concatenate([[0], np.cumsum([p.out.numel() for p in parts])[:-1]])
+        return RenderResult(torch.cat([p.out for p in parts]),
+                            np.concatenate([p.offsets + d for p, d in zip(parts, shift)]),
+                            np.concatenate([p.capacity for p in parts]),
+                            np.concatenate([p.n_images for p in parts]),
+                            sum(p.launches for p in parts),
+                            torch.cat([p._dev[0] for p in parts]),
+                            torch.stack([p._dev[1] for p in parts]).amax(dim=0))
 
     def job(self, j: int) -> torch.Tensor:
         return self.out[self.offsets[j]:self.offsets[j] + self.lengths[j]]

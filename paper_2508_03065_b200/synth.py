@@ -389,8 +389,48 @@ def scene_jobs(scenes, channels=None) -> list:
     return jobs
 
 
+def job_footprint(jb, fd_taps: int = 64) -> int:
+    """Estimated device bytes of one job in a render: coarse tracks (8 B)
+    and interval records (48 B) per decimated image per coarse sample, the
+    image records (96 B, plus the delay-sorted copy per 16384-sample
+    segment), branch records (32 B per padded input row), paths and output."""
+    T = int(jb.pos.shape[0]) if hasattr(jb.pos, "shape") else len(jb.pos)
+    n_sig = T if jb.s is None else (int(jb.s.numel()) if isinstance(jb.s, torch.Tensor)
+                                    else int(np.size(jb.s)))
+    moving = len(getattr(jb.mic, "shape", np.shape(jb.mic))) > 1
+    prev, inter, imgs = -1, 0, 0
+    for mo, N in jb.tiers:
+        cnt = image_count(int(mo)) - (image_count(prev) if prev >= 0 else 0)
+        if jb.image_index is not None:
+            cnt = int(np.sum((np.asarray(jb.image_index) >= (image_count(prev) if prev >= 0 else 0))
+                             & (np.asarray(jb.image_index) < image_count(int(mo)))))
+        imgs += cnt
+        if int(N) > 1:
+            inter += cnt * -(-T // int(N))
+        prev = int(mo)
+    n_seg = -(-T // engine.SEG_LEN)
+    reach = 2 * (int(jb.max_order) + 2) * float(np.max(jb.dims)) * float(jb.rate) / float(jb.c)
+    return int(56 * inter + 96 * imgs * (1 + n_seg) + 8 * imgs * n_seg
+               + 32 * (n_sig + 2 * reach + fd_taps) + 24 * T * (1 + moving) + 8 * (n_sig + reach))
+
+
+def _memory_groups(jobs, budget: int, fd_taps: int) -> list:
+    """Consecutive job groups whose estimated footprints fit `budget`."""
+    groups, cur, used = [], [], 0
+    for j, jb in enumerate(jobs):
+        b = job_footprint(jb, fd_taps)
+        if cur and used + b > budget:
+            groups.append(cur)
+            cur, used = [], 0
+        cur.append(j)
+        used += b
+    if cur:
+        groups.append(cur)
+    return groups
+
+
 def render_jobs(jobs, f, precision="fp32", shard=None, signals=None, timing=None,
-                inputs_ready=None, dmax_hook=None):
+                inputs_ready=None, dmax_hook=None, max_batch_bytes=None):
     """Geometry + render of a job batch; returns engine.RenderResult
     (device output, per-job offsets/lengths, update count, launches).
     `inputs_ready` (optional CUDA event): the jobs' device tensors are final
@@ -399,7 +439,9 @@ def render_jobs(jobs, f, precision="fp32", shard=None, signals=None, timing=None
     every job (parallel.image_subset; all per-image work divides by world),
     with out_len from the batch-wide track maximum (all-reduce MAX over
     the ranks, or `dmax_hook` when given) so the ranks' outputs sum to the
-    full render."""
+    full render.  Batches whose estimated device footprint exceeds
+    `max_batch_bytes` (default: 40% of the GPU's memory, identical on every
+    rank) render as consecutive sub-batches, results concatenated."""
     if shard is not None and int(shard[1]) > 1:
         if precision == "fp64":
             raise ValueError("the exact fp64 engine runs replicas only (its summation order "
@@ -413,9 +455,20 @@ def render_jobs(jobs, f, precision="fp32", shard=None, signals=None, timing=None
                     path_key=engine._key(jb.path_key, jb.pos)) for jb in jobs]
         if dmax_hook is None:
             dmax_hook = parallel.allreduce_max
-    geom = engine.Geometry(jobs, inputs_ready=inputs_ready, dmax_hook=dmax_hook)
     sig = signals if signals is not None else [jb.s for jb in jobs]
     keys = [engine._key(jb.signal_key, jb.s) for jb in jobs]
-    res = engine.render(geom, sig, f, precision=precision, signal_keys=keys, timing=timing)
-    res.launches += geom.launches
-    return res
+    if max_batch_bytes is None:
+        from ._dev import require_cuda
+        dev = require_cuda()
+        max_batch_bytes = int(0.4 * torch.cuda.get_device_properties(dev).total_memory)
+    groups = _memory_groups(jobs, int(max_batch_bytes), int(as_filter(f).branch_len))
+    parts = []
+    for g in groups:
+        sub = [jobs[j] for j in g]
+        geom = engine.Geometry(sub, inputs_ready=inputs_ready, dmax_hook=dmax_hook)
+        res = engine.render(geom, [sig[j] for j in g], f, precision=precision,
+                            signal_keys=[keys[j] for j in g], timing=timing)
+        geom.release()  # everything reading the staged paths is enqueued
+        res.launches += geom.launches
+        parts.append(res)
+    return parts[0] if len(parts) == 1 else engine.RenderResult.concat(parts)

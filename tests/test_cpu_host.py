@@ -170,3 +170,20 @@ def test_class_table_layout():
     # mvb_class_table: int32 n + 3 x int32[8] (100 B) padded to 104, + 2 x int64[8]
     assert ctypes.sizeof(_lib.ClassTable) == 104 + 128
     assert _lib.ClassTable.table.offset == 104
+
+
+def test_memory_groups_split_by_footprint():
+    from paper_2508_03065_b200 import engine, workloads
+    from paper_2508_03065_b200.synth import _memory_groups, job_footprint, scene_jobs
+    scenes = workloads.make_scenes("c4", duration=0.5, n_scenes=6)
+    jobs = scene_jobs(scenes)
+    fp = [job_footprint(jb, 32) for jb in jobs]
+    assert all(b > 0 for b in fp)
+    # interval records dominate: 56 B x decimated images x coarse samples
+    jb = jobs[0]
+    assert fp[0] >= 56 * 2600 * -(-jb.pos.shape[0] // 64)
+    groups = _memory_groups(jobs, 2 * max(fp), 32)
+    assert [j for g in groups for j in g] == list(range(6))
+    assert all(sum(fp[j] for j in g) <= 2 * max(fp) for g in groups) and len(groups) >= 3
+    assert _memory_groups(jobs, 1, 32) == [[j] for j in range(6)]  # never empty groups
+    assert _memory_groups(jobs, 10 ** 15, 32) == [list(range(6))]

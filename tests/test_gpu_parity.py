@@ -232,3 +232,20 @@ def test_image_shards_sum_to_full_render():
     assert rel_err(total, ref) <= FP32_TOL
     with pytest.raises(ValueError):
         render_jobs(jobs, f, precision="fp64", shard=(0, 2))
+
+
+def test_memory_split_batches_match_single_batch():
+    """A batch forced into sub-batches (max_batch_bytes) renders the same
+    lengths and, within the fp32 bar, the same outputs as one batch."""
+    from paper_2508_03065_b200.synth import job_footprint
+    scenes = workloads.make_scenes("c4", duration=0.25, max_order=6, n_scenes=5)
+    f = hann_sinc(32, 14)
+    jobs = scene_jobs(scenes)
+    whole = render_jobs(jobs, f)
+    split = render_jobs(jobs, f, max_batch_bytes=2 * max(job_footprint(j, 32) for j in jobs))
+    assert np.array_equal(whole.lengths, split.lengths)
+    assert whole.updates == split.updates
+    for j in range(len(jobs)):
+        a = whole.job(j).double().cpu().numpy()
+        b = split.job(j).double().cpu().numpy()
+        assert np.max(np.abs(a - b)) <= 1e-6 * np.max(np.abs(a))
