@@ -274,7 +274,7 @@ def synthesize(s, streams: DelayStreams, f, cfg) -> np.ndarray:
         return _synthesize_source(a, streams, filt, cfg)
     prec = _precision(a, cfg)
     res = engine.render(streams.geometry, [a], filt, precision=prec)
-    from .engine import d2h
+    from ._staging import d2h
     return d2h(res.job(0), np.float64)
 
 

@@ -153,7 +153,7 @@ def test_pack_jobs_matches_c_layout():
 
 
 def test_parallel_copy_chunks_and_casts():
-    from paper_2508_03065_b200.engine import parallel_copy
+    from paper_2508_03065_b200._staging import parallel_copy
     rng = np.random.default_rng(0)
     big = rng.standard_normal((3_000_000, 3))           # 72 MB: thread pool, many chunks
     small = rng.standard_normal(1000).astype(np.float32)
