@@ -327,8 +327,11 @@ __device__ __forceinline__ int skew32(int e) { return e + (e >> 5); }
 template <int COEF_BLOCK, int COEF_KI>
 struct CoefShape {
     static constexpr int SPAN = COEF_BLOCK * COEF_KI;
+    // a thread's KI records (3 float4 each) plus one float4 of padding, so
+    // the lanes' 16-byte record stores fall in distinct banks
+    static constexpr int REC_F4 = 3 * COEF_KI + 1;
     static constexpr int DW = SPAN + 64 + (SPAN + 64) / 32 + 1;
-    static constexpr size_t SMEM = sizeof(mvb_coef32) * SPAN + sizeof(float) * DW;
+    static constexpr size_t SMEM = sizeof(float4) * REC_F4 * COEF_BLOCK + sizeof(float) * DW;
 };
 
 template <int COEF_BLOCK, int COEF_KI>
@@ -339,8 +342,9 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
     // records of the span are staged here and written out coalesced
     extern __shared__ __align__(16) unsigned char coef_smem[];
     constexpr int COEF_SPAN = CoefShape<COEF_BLOCK, COEF_KI>::SPAN;
-    mvb_coef32* srec = reinterpret_cast<mvb_coef32*>(coef_smem);
-    float* dw = reinterpret_cast<float*>(coef_smem + sizeof(mvb_coef32) * COEF_SPAN);
+    constexpr int REC_F4 = CoefShape<COEF_BLOCK, COEF_KI>::REC_F4;
+    float4* srec = reinterpret_cast<float4*>(coef_smem);
+    float* dw = reinterpret_cast<float*>(coef_smem + sizeof(float4) * REC_F4 * COEF_BLOCK);
     const mvb_image im = images[sel[blockIdx.x]];
     const mvb_job& J = jobs[im.job];
     const double kappa = J.kappa;
@@ -407,15 +411,22 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
             r.g[5] = kf * acc[q][3].x;
             r.g[6] = kf * acc[q][3].y;
             r.g[7] = kf * acc8[q];
-            srec[e0 + q] = r;
+            const float4* rv = reinterpret_cast<const float4*>(&r);
+            float4* dstq = srec + REC_F4 * threadIdx.x + 3 * q;
+            dstq[0] = rv[0];
+            dstq[1] = rv[1];
+            dstq[2] = rv[2];
         }
         }
         __syncthreads();
         // coalesced copy of the span's records (16 B per thread per pass)
         const int64_t n_rec = K - k0 < COEF_SPAN ? K - k0 : COEF_SPAN;
-        const float4* src = reinterpret_cast<const float4*>(srec);
+        const float4* src = srec;
         float4* dst = reinterpret_cast<float4*>(out + im.coef + k0);
-        for (int64_t t = threadIdx.x; t < n_rec * 3; t += blockDim.x) dst[t] = src[t];
+        for (int64_t t = threadIdx.x; t < n_rec * 3; t += blockDim.x) {
+            const int rec = (int)(t / 3), part = (int)(t - 3 * (t / 3));  // record e = rec
+            dst[t] = src[REC_F4 * (rec / COEF_KI) + 3 * (rec % COEF_KI) + part];
+        }
     }
 }
 
