@@ -713,16 +713,16 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         wait for the geometry kernels); the exact lengths are written into
         the device job table by mvb_finalize_lengths (finalize)."""
         out_len = np.zeros(nJ, np.int64)
-        tau_ceil = np.zeros(nJ, np.int64)
+        tau_bound = np.zeros(nJ, np.int64)
         for j in range(nJ):
-            tau_ceil[j] = geom.length_bound(j)
-            out_len[j] = sig_len[keys[j]] + tau_ceil[j] + L
+            tau_bound[j] = geom.length_bound(j)
+            out_len[j] = sig_len[keys[j]] + tau_bound[j] + L
         offsets = np.concatenate([[0], np.cumsum(out_len)[:-1]]).astype(np.int64)
         rows = [dict(r) for r in base_rows]
         for j in range(nJ):
             rows[j].update(out_off=int(offsets[j]), out_len=int(out_len[j]),
                            ls=int(sig_len[keys[j]] + L - 1))
-        return out_len, tau_ceil, offsets, rows
+        return out_len, tau_bound, offsets, rows
 
     def finalize(jobs_dev):
         lengths = torch.empty(nJ, dtype=torch.int64, device=dev)
@@ -757,90 +757,25 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         return RenderResult(out, offsets, out_len, geom.n_img.copy(), launches, lengths, err)
 
     # ---------------------------------------------------------------- fast --
-    # 1. work that does not depend on out_len: interval records and the
-    #    per-job delay sort (queued before the host waits for dmax)
     _mark("render.signals")
     cb, M1, nb = fast_bank(f)
-    cb_dev = h2d(np.ascontiguousarray(cb), dev)
     pre_dev = h2d(pack_jobs(base_rows), dev)
-    coef = torch.empty(max(geom.n_coarse_total, 1) * 12, dtype=torch.float32, device=dev)
-    for N, sel in geom.sel_by_factor.items():
-        fit = np.ascontiguousarray(phase_fit(N), dtype=np.float64)
-        max_K = -(-int(geom.T.max()) // N)
-        _lib.call("mvb_track_coeffs", ptr(geom.images), ptr(sel), sel.numel(), max_K, ptr(pre_dev),
-                  ptr(geom.coarse), fit.ctypes.data_as(ctypes.c_void_p), ptr(coef), st)
-        launches += 1
-    # delay sort per (job, time segment of SEG_LEN samples): keys by our
-    # kernel, one batched argsort (padding keys +inf sort last)
-    n_seg = [-(-int(geom.T[j]) // SEG_LEN) for j in range(nJ)]
-    max_seg, max_img = max(n_seg), int(geom.n_img.max())
-    key = torch.full((nJ, max_seg, max_img), float("inf"), dtype=torch.float64, device=dev)
-    _lib.call("mvb_sort_keys", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg, SEG_LEN,
-              ptr(geom.paths), ptr(geom.coarse), ptr(key), st)
-    launches += 1
+    coef = _interval_records(geom, pre_dev, st)
+    launches += len(geom.sel_by_factor)
     _mark("render.coeffs_keys")
-    order = torch.argsort(key, dim=2)  # (nJ, max_seg, max_img)
-    base = h2d(geom.img_off, dev)[:, None, None]
-    nimg_dev = h2d(geom.n_img, dev)[:, None, None]
-    gidx = (base + torch.minimum(order, nimg_dev - 1)).reshape(-1)  # padded slots: any own image
-    images_sorted = torch.empty(gidx.numel(), IMG_COLS, dtype=torch.int64, device=dev)
-    _lib.call("mvb_gather_images", ptr(geom.images), ptr(gidx), gidx.numel(), ptr(images_sorted), st)
-    launches += 1  # layout (job, segment, max_img)
-    # 2. out_len, zero-padded branch records, work list, synthesis
+    images_sorted, n_seg, max_seg, max_img = _delay_sort(geom, pre_dev, st)
+    launches += 2
     _mark("render.sorted")
-    out_len, tau_ceil, offsets, rows = finish_rows()
+    out_len, tau_bound, offsets, rows = finish_rows()
     _mark("render.plan_lengths")
-    rec_rows, bases = 0, {}
-    for k, members in uniq.items():
-        front = int(max(tau_ceil[j] for j in members)) + L + PAD_MARGIN
-        back = front + TILE + PAD_MARGIN
-        bases[k] = (rec_rows, front)
-        rec_rows += front + sig_len[k] + L - 1 + back
-    if rec_rows + int(out_len.max()) + L >= 2**31 - 0x4B400000:
-        raise ValueError("batch too large for 32-bit record rows; split it")
-    row_floats = 4 if nb == 4 else 8 * -(-nb // 8)  # mvb.h record layout
-    rec = torch.zeros(rec_rows * row_floats, dtype=torch.float32, device=dev)
-    ukeys = list(uniq)
-    lens = np.asarray([sig_len[k] for k in ukeys], np.int64)
-    if len(ukeys) == 1:
-        x_all = sig_dev[ukeys[0]]
-    elif host_sigs and len(host_sigs) == len(ukeys):
-        x_all = sig_all  # already concatenated in key order
-    else:
-        x_all = torch.cat([sig_dev[k] for k in ukeys])
-    sig_tab = h2d(np.stack([np.concatenate([[0], np.cumsum(lens)[:-1]]), lens,
-                            np.asarray([bases[k][0] + bases[k][1] for k in ukeys], np.int64)]), dev)
-    _lib.call("mvb_branch_records_f32", ptr(x_all), ptr(sig_tab[0]), ptr(sig_tab[1]),
-              ptr(sig_tab[2]), len(ukeys), int(lens.max()), ptr(cb_dev), M1, L, nb, ptr(rec), st)
+    rec, rec_start = _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev, st,
+                                     sig_all if host_sigs and len(host_sigs) == len(uniq) else None)
     launches += 1
     for j in range(nJ):
-        r0, front = bases[keys[j]]
-        rows[j].update(rec_base=r0 + front, nb=nb, img_off=j * max_seg * max_img,
+        rows[j].update(rec_base=rec_start[keys[j]], nb=nb, img_off=j * max_seg * max_img,
                        img_stride=max_img)
-    lo = np.zeros(nJ, dtype=np.int64)
-    hi = geom.n_img.astype(np.int64)
-    tiles = [-(-int(out_len[j]) // TILE) for j in range(nJ)]
-    chunks = _chunking([int(hi[j] - lo[j]) for j in range(nJ)], tiles, sm_count)
-    part_rows = 0
-    blocks = []
-    for j in range(nJ):
-        nc = chunks[j] if hi[j] > lo[j] else 1
-        rows[j]["n_chunks"] = nc
-        if nc > 1:
-            rows[j]["part_off"] = part_rows
-            part_rows += nc * int(out_len[j])
-        span = int(hi[j] - lo[j])
-        cs = np.arange(nc)
-        blk = np.zeros((nc, tiles[j], 8), dtype=np.int32)  # mvb_work rows
-        blk[:, :, 0] = j
-        blk[:, :, 1] = np.arange(tiles[j])[None, :]
-        blk[:, :, 2] = (int(lo[j]) + (span * cs) // nc)[:, None]
-        blk[:, :, 3] = (int(lo[j]) + (span * (cs + 1)) // nc)[:, None]
-        blk[:, :, 4] = cs[:, None]
-        blk[:, :, 5] = np.minimum(np.arange(tiles[j]) * TILE // SEG_LEN, n_seg[j] - 1)[None, :]
-        blocks.append(blk.reshape(-1, 8))
+    work, part_rows = _work_list(geom.n_img, out_len, n_seg, sm_count, rows)
     _mark("render.records_plan")
-    work = np.concatenate(blocks)
     jobs_dev = h2d(pack_jobs(rows), dev)
     work_dev = h2d(work, dev)
     lengths, err = finalize(jobs_dev)
@@ -858,4 +793,95 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
                   ptr(out), st)
         launches += 1
     _mark("render.synth_launched")
-    return RenderResult(out, offsets, out_len, hi.copy(), launches, lengths, err)
+    return RenderResult(out, offsets, out_len, geom.n_img.astype(np.int64), launches, lengths, err)
+
+
+def _interval_records(geom, pre_dev, st) -> torch.Tensor:
+    """Fast-path interval records (mvb_coef32, 12 floats) of every decimated
+    image, one mvb_track_coeffs launch per decimation factor."""
+    coef = torch.empty(max(geom.n_coarse_total, 1) * 12, dtype=torch.float32, device=geom.dev)
+    for N, sel in geom.sel_by_factor.items():
+        fit = np.ascontiguousarray(phase_fit(N), dtype=np.float64)
+        max_K = -(-int(geom.T.max()) // N)
+        _lib.call("mvb_track_coeffs", ptr(geom.images), ptr(sel), sel.numel(), max_K, ptr(pre_dev),
+                  ptr(geom.coarse), fit.ctypes.data_as(ctypes.c_void_p), ptr(coef), st)
+    return coef
+
+
+def _delay_sort(geom, pre_dev, st):
+    """Image records of every job sorted by delay per SEG_LEN-sample time
+    segment (L1 locality of the gathers): keys by mvb_sort_keys, one batched
+    argsort (padding keys +inf sort last, padded slots repeat an own
+    image), records gathered into the (job, segment, max_img) layout."""
+    dev, nJ = geom.dev, len(geom.jobs)
+    n_seg = [-(-int(geom.T[j]) // SEG_LEN) for j in range(nJ)]
+    max_seg, max_img = max(n_seg), int(geom.n_img.max())
+    key = torch.full((nJ, max_seg, max_img), float("inf"), dtype=torch.float64, device=dev)
+    _lib.call("mvb_sort_keys", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg, SEG_LEN,
+              ptr(geom.paths), ptr(geom.coarse), ptr(key), st)
+    order = torch.argsort(key, dim=2)
+    base = h2d(geom.img_off, dev)[:, None, None]
+    nimg_dev = h2d(geom.n_img, dev)[:, None, None]
+    gidx = (base + torch.minimum(order, nimg_dev - 1)).reshape(-1)
+    images_sorted = torch.empty(gidx.numel(), IMG_COLS, dtype=torch.int64, device=dev)
+    _lib.call("mvb_gather_images", ptr(geom.images), ptr(gidx), gidx.numel(), ptr(images_sorted), st)
+    return images_sorted, n_seg, max_seg, max_img
+
+
+def _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev, st, concatenated=None):
+    """Zero-padded fp32 branch records of every distinct signal (mvb.h
+    layout) in one launch.  A signal's region is [front pad | len + L - 1
+    rows | back pad] with the front pad covering the largest delay bound of
+    the jobs using it, so every gather row is in range.  Returns the record
+    buffer and, per signal key, the global row of its sample 0."""
+    rec_rows, start = 0, {}
+    for k, members in uniq.items():
+        front = int(max(tau_bound[j] for j in members)) + L + PAD_MARGIN
+        back = front + TILE + PAD_MARGIN
+        start[k] = rec_rows + front
+        rec_rows += front + sig_len[k] + L - 1 + back
+    if rec_rows + int(max(sig_len.values())) + int(max(tau_bound)) + 2 * L >= 2**31 - 0x4B400000:
+        raise ValueError("batch too large for 32-bit record rows; split it")
+    row_floats = 4 if nb == 4 else 8 * -(-nb // 8)  # mvb.h record layout
+    rec = torch.zeros(rec_rows * row_floats, dtype=torch.float32, device=dev)
+    ukeys = list(uniq)
+    lens = np.asarray([sig_len[k] for k in ukeys], np.int64)
+    if len(ukeys) == 1:
+        x_all = sig_dev[ukeys[0]]
+    elif concatenated is not None:
+        x_all = concatenated  # host signals were uploaded back to back in key order
+    else:
+        x_all = torch.cat([sig_dev[k] for k in ukeys])
+    sig_tab = h2d(np.stack([np.concatenate([[0], np.cumsum(lens)[:-1]]), lens,
+                            np.asarray([start[k] for k in ukeys], np.int64)]), dev)
+    cb_dev = h2d(np.ascontiguousarray(cb), dev)
+    _lib.call("mvb_branch_records_f32", ptr(x_all), ptr(sig_tab[0]), ptr(sig_tab[1]),
+              ptr(sig_tab[2]), len(ukeys), int(lens.max()), ptr(cb_dev), M1, L, nb, ptr(rec), st)
+    return rec, start
+
+
+def _work_list(n_img, out_len, n_seg, sm_count, rows):
+    """mvb_work items (job, tile, image range, chunk, sort segment) of every
+    job, image ranges split into chunks (_chunking); chunked jobs get
+    partial-output rows (rows[j]['n_chunks'], ['part_off'] are set)."""
+    nJ = len(rows)
+    tiles = [-(-int(out_len[j]) // TILE) for j in range(nJ)]
+    chunks = _chunking([int(v) for v in n_img], tiles, sm_count)
+    part_rows, blocks = 0, []
+    for j in range(nJ):
+        nc = chunks[j] if n_img[j] > 0 else 1
+        rows[j]["n_chunks"] = nc
+        if nc > 1:
+            rows[j]["part_off"] = part_rows
+            part_rows += nc * int(out_len[j])
+        span = int(n_img[j])
+        cs = np.arange(nc)
+        blk = np.zeros((nc, tiles[j], 8), dtype=np.int32)
+        blk[:, :, 0] = j
+        blk[:, :, 1] = np.arange(tiles[j])[None, :]
+        blk[:, :, 2] = ((span * cs) // nc)[:, None]
+        blk[:, :, 3] = ((span * (cs + 1)) // nc)[:, None]
+        blk[:, :, 4] = cs[:, None]
+        blk[:, :, 5] = np.minimum(np.arange(tiles[j]) * TILE // SEG_LEN, n_seg[j] - 1)[None, :]
+        blocks.append(blk.reshape(-1, 8))
+    return np.concatenate(blocks), part_rows
