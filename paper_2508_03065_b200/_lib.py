@@ -61,6 +61,13 @@ _SIGS = {
 }
 _RESTYPE = {"mvb_last_error": ctypes.c_char_p, "mvb_image_count": I64}
 
+# kernels launched by one successful call (entry points not listed launch
+# one; the query functions launch none) -- feeds launch_count()
+_KERNELS = {"mvb_track_max": 2, "mvb_path_bbox": 2, "mvb_center_paths": 2,
+            "mvb_spectrum_index": 2, "mvb_abi_version": 0, "mvb_last_error": 0,
+            "mvb_device_info": 0, "mvb_struct_sizes": 0, "mvb_image_count": 0}
+_launches = 0
+
 IMAGE_BYTES, JOB_BYTES, WORK_BYTES, COEF_BYTES = 96, 136, 32, 48
 
 
@@ -107,10 +114,18 @@ def lib():
 
 def call(name: str, *args) -> None:
     """Invoke a status-returning entry point; raise MvbError on failure."""
+    global _launches
     rc = getattr(lib(), name)(*args)
     if rc != 0:
         msg = lib().mvb_last_error().decode("utf-8", "replace")
         raise MvbError(f"{name} failed ({rc}): {msg}")
+    _launches += _KERNELS.get(name, 1)
+
+
+def launch_count() -> int:
+    """libmvb kernels launched by this process so far (zero-sized calls
+    that return early are counted too: an upper bound by a few)."""
+    return _launches
 
 
 def image_count(max_order: int) -> int:

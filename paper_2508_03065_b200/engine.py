@@ -186,13 +186,28 @@ class Geometry:
         track maxima before it is read (image shards: all-reduce MAX)."""
         if not jobs:
             raise ValueError("no jobs")
-        self.dev = dev = require_cuda(device)
+        self.dev = require_cuda(device)
         self.jobs = jobs
-        st = stream_handle(dev)
-        nJ = len(jobs)
         for jb in jobs:
             _validate_tiers(jb.tiers, jb.max_order)
-        # ---- full-rate paths ------------------------------------------------
+        host_parts, dev_parts, rows = self._layout_paths()
+        _mark("geom.setup")
+        path_groups, bws = self._stage_paths(host_parts, dev_parts, rows, inputs_ready)
+        _mark("geom.bandwidth")
+        self._decimate_paths(path_groups, bws)
+        _mark("geom.decimate")
+        self._build_images()
+        _mark("geom.images")
+        self._tracks(dmax_hook)
+        _mark("geom.tracks")
+        self.eval_count = [int(self.evals[j]) for j in range(len(jobs))]
+
+    def _layout_paths(self):
+        """Rows of the fp64 paths buffer: every distinct source path first
+        (equal-length paths of a batch then form one strided view for the
+        decimation decision), the receivers after them, then a slot per
+        (job, decimated factor) for the coarse source (and receiver) path."""
+        jobs, nJ = self.jobs, len(self.jobs)
         host_parts, dev_parts = [], []
         row = 0
         path_row = {}
@@ -200,8 +215,6 @@ class Geometry:
         self.pos_off = np.zeros(nJ, np.int64)
         self.mic_off = np.zeros(nJ, np.int64)
         self.moving = np.zeros(nJ, np.int64)
-        # all source paths first (equal-length paths of a batch then form one
-        # strided view for the decimation decision), receivers after them
         for j, jb in enumerate(jobs):
             k = _key(jb.path_key, jb.pos)
             if k not in path_row:
@@ -221,34 +234,38 @@ class Geometry:
             self.mic_off[j] = row
             (dev_parts if isinstance(m, torch.Tensor) else host_parts).append((row, m))
             row += m.shape[0]
-        full_rows = row
-        # ---- coarse path slots per (job, decimated factor) ------------------
         self.cpath = {}  # (j, N) -> row
         for j, jb in enumerate(jobs):
             for _, N in jb.tiers:
                 N = int(N)
                 if N > 1 and (j, N) not in self.cpath:
-                    K = -(-int(self.T[j]) // N)
                     self.cpath[(j, N)] = row
-                    row += K * (1 + int(self.moving[j]))
-        _mark("geom.setup")
+                    row += -(-int(self.T[j]) // N) * (1 + int(self.moving[j]))
+        return host_parts, dev_parts, max(row, 1)
+
+    def _stage_paths(self, host_parts, dev_parts, rows, inputs_ready):
+        """Fill the full-rate rows of the paths buffer, compute every job's
+        path bounding boxes and the paths' bandwidths; the two small
+        readbacks (boxes, bandwidth indices) are the host's only waits.
+        With `inputs_ready` this runs on the high-priority side stream into a
+        persistent arena buffer (released by render_jobs), so it does not
+        queue behind earlier work on the current stream."""
+        dev, nJ = self.dev, len(self.jobs)
         main = torch.cuda.current_stream(dev)
         side = side_stream(dev) if inputs_ready is not None else main
         if side is not main:
             side.wait_event(inputs_ready)
         with torch.cuda.stream(side):
-            if side is not main:  # persistent arena buffer (released by render_jobs)
-                self._arena = _ARENA.acquire(dev, max(row, 1))
-                self.paths = self._arena[:max(row, 1)]
+            if side is not main:
+                self._arena = _ARENA.acquire(dev, rows)
+                self.paths = self._arena[:rows]
             else:
                 self._arena = None
-                self.paths = torch.empty(max(row, 1), 3, dtype=torch.float64, device=dev)
+                self.paths = torch.empty(rows, 3, dtype=torch.float64, device=dev)
             if host_parts:
                 _STAGER.upload(host_parts, self.paths)
             for r0, p in dev_parts:
                 self.paths[r0:r0 + p.shape[0]].copy_(p)
-            # bounding boxes of every source path and receiver: the host bounds
-            # each job's output length from them (no wait for the track maxima)
             box_rows = h2d(np.stack([self.pos_off, self.T, self.mic_off, self.moving], axis=1), dev)
             # flat: the nJ x 12 boxes first, then the 64 partial boxes per job
             self.bbox = torch.empty(nJ * 65 * 12, dtype=torch.float64, device=dev)
@@ -258,20 +275,21 @@ class Geometry:
             box_host.copy_(self.bbox[:nJ * 12].view(nJ, 12), non_blocking=True)
             box_ready = torch.cuda.Event()
             box_ready.record()
-            path_groups, bws = self._path_bandwidths(main)  # host waits for `side` only
+            path_groups, bws = self._path_bandwidths(main)
         box_ready.synchronize()
         self.bbox_host = box_host.numpy().copy()
         if side is not main:
             main.wait_stream(side)
             self.bbox.record_stream(main)
-        _mark("geom.bandwidth")
-        self._decimate_paths(path_groups, bws)
-        # ---- image table ----------------------------------------------------
-        _mark("geom.decimate")
-        self._build_images()
-        # ---- job table (geometry fields; render fills the rest) -------------
+        return path_groups, bws
+
+    def _tracks(self, dmax_hook):
+        """Job table, coarse tracks and their bounds, the exact track maximum
+        of every job (kept on the device; `dmax_hook` may reduce it across
+        ranks in place)."""
+        dev, nJ, st = self.dev, len(self.jobs), stream_handle(self.dev)
         self.job_rows = []
-        for j, jb in enumerate(jobs):
+        for j, jb in enumerate(self.jobs):
             self.job_rows.append(dict(
                 out_off=0, out_len=0, part_off=0, rec_base=0, ls=0,
                 img_off=int(self.img_off[j]), n_img=int(self.n_img[j]),
@@ -279,9 +297,7 @@ class Geometry:
                 T=int(self.T[j]), mic_moving=int(self.moving[j]), L=0, d0=0, n_chunks=1, nb=0,
                 rate=float(jb.rate), c=float(jb.c), d_min=float(jb.d_min),
                 kappa=float(jb.rate) / float(jb.c)))
-        _mark("geom.images")
         jobs_dev = h2d(pack_jobs(self.job_rows), dev)
-        # ---- coarse tracks, bounds, exact max ---------------------------------
         n_img = self.n_images
         self.coarse = torch.empty(max(self.n_coarse_total, 1), dtype=torch.float64, device=dev)
         lb = torch.zeros(n_img, dtype=torch.float64, device=dev)
@@ -301,14 +317,10 @@ class Geometry:
         _lib.call("mvb_track_max", ptr(self.images), ptr(jobs_dev), nJ,
                   ptr(self.coarse) if self.dec_sel.numel() else ptr(None), ptr(self.tables),
                   ptr(self.paths), negsum, ptr(lb), ptr(ub), ptr(scratch), ptr(dmax), st)
-        _mark("geom.tracks")
         if dmax_hook is not None:
             dmax_hook(dmax)
         self.dmax_dev = dmax
         self._dmax = None  # host copy on demand (the render itself never waits for it)
-        self.launches = self.n_enum_launches + (1 if self.dec_sel.numel() else 0) \
-            + (2 if self.full_sel.numel() else 0) + 2
-        self.eval_count = [int(self.evals[j]) for j in range(nJ)]
 
     def release(self) -> None:
         """Hand the staging buffer back (after every kernel reading the paths
@@ -415,7 +427,6 @@ class Geometry:
             sub = None if jb.image_index is None else tuple(np.asarray(jb.image_index).tolist())
             key = (int(jb.max_order), tuple((int(a), int(b)) for a, b in jb.tiers), sub)
             groups.setdefault(key, []).append(j)
-        self.n_enum_launches = 2 * len(groups)
         self.img_off = np.zeros(nJ, np.int64)
         self.n_img = np.zeros(nJ, np.int64)
         self.evals = np.zeros(nJ, np.int64)
@@ -705,8 +716,8 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         _STAGER.upload([(r0, a) for _, r0, a in host_sigs], sig_all)
         for k, r0, a in host_sigs:
             sig_dev[k] = sig_all[r0:r0 + a.size]
-    launches = 0
     base_rows = [dict(r, L=L, d0=d0) for r in geom.job_rows]
+    launches0 = _lib.launch_count()
 
     def finish_rows():
         """Capacities from the host-side bound of every output length (no
@@ -742,7 +753,6 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         for k in uniq:
             _lib.call("mvb_branch_filter", ptr(sig_dev[k]), sig_len[k], ptr(br), nb, L,
                       ptr(streams[bases[k]:]), st)
-            launches += 1
         out_len, _, offsets, rows = finish_rows()
         for j in range(nJ):
             rows[j].update(rec_base=bases[keys[j]], nb=nb)
@@ -753,24 +763,21 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         _lib.call("mvb_synthesize_f64", ptr(jobs_dev), nJ, int(out_len.max()), ptr(geom.images),
                   ptr(geom.coarse), ptr(geom.tables), ptr(streams), ptr(geom.paths), ptr(out), st)
         _events_end(timing, ev)
-        launches += 2
-        return RenderResult(out, offsets, out_len, geom.n_img.copy(), launches, lengths, err)
+        return RenderResult(out, offsets, out_len, geom.n_img.copy(),
+                            _lib.launch_count() - launches0, lengths, err)
 
     # ---------------------------------------------------------------- fast --
     _mark("render.signals")
     cb, M1, nb = fast_bank(f)
     pre_dev = h2d(pack_jobs(base_rows), dev)
     coef = _interval_records(geom, pre_dev, st)
-    launches += len(geom.sel_by_factor)
     _mark("render.coeffs_keys")
     images_sorted, n_seg, max_seg, max_img = _delay_sort(geom, pre_dev, st)
-    launches += 2
     _mark("render.sorted")
     out_len, tau_bound, offsets, rows = finish_rows()
     _mark("render.plan_lengths")
     rec, rec_start = _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev, st,
                                      sig_all if host_sigs and len(host_sigs) == len(uniq) else None)
-    launches += 1
     for j in range(nJ):
         rows[j].update(rec_base=rec_start[keys[j]], nb=nb, img_off=j * max_seg * max_img,
                        img_stride=max_img)
@@ -779,7 +786,6 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     jobs_dev = h2d(pack_jobs(rows), dev)
     work_dev = h2d(work, dev)
     lengths, err = finalize(jobs_dev)
-    launches += 1
     out = torch.zeros(int(out_len.sum()), dtype=torch.float32, device=dev)
     part = torch.empty(max(part_rows, 1), dtype=torch.float32, device=dev)
     ev = _events(timing)
@@ -787,13 +793,12 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     _lib.call("mvb_synthesize_f32", ptr(jobs_dev), ptr(work_dev), len(work), ptr(images_sorted),
               ptr(coef), ptr(rec), ptr(geom.paths), ptr(out), ptr(part), nb, SYNTH_U, st)
     _events_end(timing, ev)
-    launches += 1
     if part_rows:
         _lib.call("mvb_reduce_partials_f32", ptr(jobs_dev), nJ, int(out_len.max()), ptr(part),
                   ptr(out), st)
-        launches += 1
-    _mark("render.synth_launched")
-    return RenderResult(out, offsets, out_len, geom.n_img.astype(np.int64), launches, lengths, err)
+        _mark("render.synth_launched")
+    return RenderResult(out, offsets, out_len, geom.n_img.astype(np.int64),
+                        _lib.launch_count() - launches0, lengths, err)
 
 
 def _interval_records(geom, pre_dev, st) -> torch.Tensor:

@@ -26,7 +26,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 import torch
 
-from . import engine
+from . import _lib, engine
 from .farrow import as_filter
 from .room import as_mic, image_count, image_table
 
@@ -465,10 +465,11 @@ def render_jobs(jobs, f, precision="fp32", shard=None, signals=None, timing=None
     parts = []
     for g in groups:
         sub = [jobs[j] for j in g]
+        launches0 = _lib.launch_count()
         geom = engine.Geometry(sub, inputs_ready=inputs_ready, dmax_hook=dmax_hook)
         res = engine.render(geom, [sig[j] for j in g], f, precision=precision,
                             signal_keys=[keys[j] for j in g], timing=timing)
         geom.release()  # everything reading the staged paths is enqueued
-        res.launches += geom.launches
+        res.launches = _lib.launch_count() - launches0  # libmvb kernels, geometry + render
         parts.append(res)
     return parts[0] if len(parts) == 1 else engine.RenderResult.concat(parts)
