@@ -99,9 +99,63 @@ def readback(t: torch.Tensor, name: str) -> np.ndarray:
     return host.numpy().copy().reshape(t.shape)
 
 
+class StaticUploads:
+    """Upload source for CUDA-graph capture: while active (`with`), h2d
+    copies host arrays into consecutive slices of one persistent pinned
+    buffer that the captured memcpy nodes keep reading at every replay (the
+    pinned ring would be overwritten).  `nbytes` must cover the captured
+    uploads (size it from a dry run's `used`)."""
+
+    _active = None
+
+    def __init__(self, nbytes: int):
+        self.buf = torch.empty(max(int(nbytes), 1024), dtype=torch.uint8, pin_memory=True)
+        self.host = self.buf.numpy()
+        self.used = 0
+
+    def __enter__(self):
+        StaticUploads._active = self
+        return self
+
+    def __exit__(self, *exc):
+        StaticUploads._active = None
+
+    def put(self, a: np.ndarray, dev) -> torch.Tensor:
+        a = np.ascontiguousarray(a)
+        n = a.nbytes
+        if self.used + n > self.buf.numel():
+            raise MvbError("static upload buffer too small for the captured render")
+        self.host[self.used:self.used + n] = a.reshape(-1).view(np.uint8)
+        src = self.buf[self.used:self.used + n].view(_TORCH_DTYPE[a.dtype.str[1:]])
+        self.used += -(-max(n, 1) // 256) * 256
+        return src.reshape(a.shape).to(dev, non_blocking=True)
+
+
+class UploadMeter:
+    """Counts the bytes h2d would stage (dry run before a capture)."""
+
+    _active = None
+
+    def __init__(self):
+        self.used = 0
+
+    def __enter__(self):
+        UploadMeter._active = self
+        return self
+
+    def __exit__(self, *exc):
+        UploadMeter._active = None
+
+
 def h2d(a: np.ndarray, dev) -> torch.Tensor:
-    """Host array -> device without a host sync (pinned ring staging)."""
-    return _RING.put(np.asarray(a), dev)
+    """Host array -> device without a host sync (pinned ring staging, or the
+    active StaticUploads buffer during a graph capture)."""
+    a = np.asarray(a)
+    if StaticUploads._active is not None:
+        return StaticUploads._active.put(a, dev)
+    if UploadMeter._active is not None:
+        UploadMeter._active.used += -(-max(a.nbytes, 1) // 256) * 256
+    return _RING.put(a, dev)
 
 
 def to_dev(a, dtype, device) -> torch.Tensor:

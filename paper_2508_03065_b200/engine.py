@@ -164,9 +164,13 @@ _DEV_CACHE: dict = {}
 
 
 def _cached_dev(key, make):
-    """Small read-only device tables reused across renders (bounded)."""
+    """Small read-only device tables reused across renders (bounded).  Not
+    filled during a graph capture: a captured upload only runs at replay."""
     t = _DEV_CACHE.get(key)
     if t is None:
+        from ._dev import StaticUploads
+        if StaticUploads._active is not None:
+            return make()
         if len(_DEV_CACHE) > 64:
             _DEV_CACHE.clear()
         t = _DEV_CACHE[key] = make()
@@ -176,31 +180,55 @@ def _cached_dev(key, make):
 class Geometry:
     """Device-side hierarchical tracks of a batch of jobs (prepare stage)."""
 
-    def __init__(self, jobs: list, device=None, inputs_ready=None, dmax_hook=None):
+    def __init__(self, jobs: list, device=None, inputs_ready=None, dmax_hook=None,
+                 paths=None, defer=False):
         """`inputs_ready`: optional CUDA event after which every device
         tensor of `jobs` is final.  With it, the paths are staged and their
         bandwidths measured on a side stream that waits only for that event,
         so planning this batch does not queue behind earlier work on the
         current stream (e.g. the previous batch's synthesis).  `dmax_hook`:
         optional callable applied in place to the device tensor of per-job
-        track maxima before it is read (image shards: all-reduce MAX)."""
+        track maxima before it is read (image shards: all-reduce MAX).
+        `paths`: a caller-owned fp64 (rows, 3) buffer to stage the paths
+        into (render plans); `defer`: stop after the staging (bounding boxes,
+        decimation decision) -- finish() does the device work."""
         if not jobs:
             raise ValueError("no jobs")
         self.dev = require_cuda(device)
         self.jobs = jobs
         for jb in jobs:
             _validate_tiers(jb.tiers, jb.max_order)
+        self.length_slack = 0.0
         host_parts, dev_parts, rows = self._layout_paths()
+        self.rows = rows
         _mark("geom.setup")
-        path_groups, bws = self._stage_paths(host_parts, dev_parts, rows, inputs_ready)
+        self.path_groups, self.bws = self._stage_paths(host_parts, dev_parts, rows, inputs_ready,
+                                                       paths)
         _mark("geom.bandwidth")
-        self._decimate_paths(path_groups, bws)
+        if not defer:
+            self.finish(dmax_hook)
+
+    def finish(self, dmax_hook=None):
+        """Device work after the staging: coarse paths, image records, coarse
+        tracks, bounds and the exact track maxima (no host waits)."""
+        self._decimate_paths(self.path_groups, self.bws)
         _mark("geom.decimate")
         self._build_images()
         _mark("geom.images")
         self._tracks(dmax_hook)
         _mark("geom.tracks")
-        self.eval_count = [int(self.evals[j]) for j in range(len(jobs))]
+        self.eval_count = [int(self.evals[j]) for j in range(len(self.jobs))]
+
+    def lowpass_decision(self) -> tuple:
+        """Which (path group, factor) pairs need the anti-alias low-pass
+        (trajectory.py:279-298) -- part of a render plan's identity."""
+        out = []
+        for (T, rate, x, uses), bw in zip(self.path_groups, self.bws):
+            for (T2, rate2, N) in sorted(uses):
+                if (T2, rate2) == (T, rate) and N > 1:
+                    nyq = 0.5 * rate / N
+                    out.append(tuple(np.nonzero((bw > nyq) & (bw < 2.0 * nyq))[0].tolist()))
+        return tuple(out)
 
     def _layout_paths(self):
         """Rows of the fp64 paths buffer: every distinct source path first
@@ -243,7 +271,7 @@ class Geometry:
                     row += -(-int(self.T[j]) // N) * (1 + int(self.moving[j]))
         return host_parts, dev_parts, max(row, 1)
 
-    def _stage_paths(self, host_parts, dev_parts, rows, inputs_ready):
+    def _stage_paths(self, host_parts, dev_parts, rows, inputs_ready, paths=None):
         """Fill the full-rate rows of the paths buffer, compute every job's
         path bounding boxes and the paths' bandwidths; the two small
         readbacks (boxes, bandwidth indices) are the host's only waits.
@@ -256,11 +284,15 @@ class Geometry:
         if side is not main:
             side.wait_event(inputs_ready)
         with torch.cuda.stream(side):
-            if side is not main:
+            self._arena = None
+            if paths is not None:
+                if paths.shape[0] < rows:
+                    raise ValueError("paths buffer too small")
+                self.paths = paths[:rows]
+            elif side is not main:
                 self._arena = _ARENA.acquire(dev, rows)
                 self.paths = self._arena[:rows]
             else:
-                self._arena = None
                 self.paths = torch.empty(rows, 3, dtype=torch.float64, device=dev)
             if host_parts:
                 _STAGER.upload(host_parts, self.paths)
@@ -394,7 +426,7 @@ class Geometry:
                               ptr(self.paths), st)
                 if (~raw).any():  # anti-alias low-pass first (trajectory.py:279-298)
                     sel = np.unique(pos[~raw])
-                    lp = lowpass_batch(x[torch.as_tensor(sel, device=dev)], rate, 0.9 * nyq)
+                    lp = lowpass_batch(x[h2d(sel.astype(np.int64), dev)], rate, 0.9 * nyq)
                     lp = lp.contiguous()
                     where = np.searchsorted(sel, pos[~raw])
                     rows = h2d(np.stack([where * T, dst[~raw]], axis=1), dev)
@@ -527,7 +559,9 @@ class Geometry:
         max_a sqrt(((K+1) L_a + P_a + M_a)^2 + sum_{b != a} (L_b + P_b + M_b)^2)
         (P, M: largest source / receiver coordinate magnitudes); widened by
         the upsampler's overshoot (negative tap mass) and a 2% + 1 cm margin
-        for the anti-alias low-pass.  mvb_finalize_lengths checks it."""
+        for the anti-alias low-pass, times (1 + length_slack) (render plans
+        reserve headroom so nearby data reuse a capture).
+        mvb_finalize_lengths checks it."""
         jb = self.jobs[j]
         box = self.bbox_host[j]
         P = np.maximum(np.abs(box[0:3]), np.abs(box[3:6]))
@@ -538,7 +572,7 @@ class Geometry:
         ext = (K + 1) * dims + P + M
         d2 = max(ext[a] ** 2 + sum(base[b] ** 2 for b in range(3) if b != a) for a in range(3))
         neg = max([negative_mass(int(N)) for _, N in jb.tiers if int(N) > 1], default=0.0)
-        d_ub = 1.02 * math.sqrt(d2) * (1.0 + neg) + 0.01
+        d_ub = (1.02 * math.sqrt(d2) * (1.0 + neg) + 0.01) * (1.0 + self.length_slack)
         return int(math.ceil(float(jb.rate) * d_ub / float(jb.c)))
 
     def tau_max(self, j: int) -> float:
@@ -594,16 +628,19 @@ def _fast_bank(filt) -> tuple:
 
 
 def _events(timing):
+    """Timing event before the synthesis launch.  `external` events keep
+    their timestamps when recorded inside a CUDA-graph capture (render
+    plans), so every replay re-times the kernel."""
     if timing is None:
         return None
-    e = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True, external=True)
     e.record()
     return e
 
 
 def _events_end(timing, e0):
     if timing is not None:
-        e1 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True, external=True)
         e1.record()
         timing.append((e0, e1))
 

@@ -1,0 +1,198 @@
+"""CUDA-graph render plans: repeated renders of one job structure.
+
+A plan fixes the structure of a batch -- per job the path length, signal
+length, receiver kind, room, image order, tier table, filter and precision --
+and captures every kernel of a render after the staging into one CUDA graph.
+Each `run` copies the new inputs into the plan's static buffers, redoes the
+staging outside the graph (path bounding boxes and the decimation decision,
+the two small readbacks) and replays the graph, which recomputes all
+data-dependent work (coarse tracks, bounds, exact maxima, interval records,
+delay sort, branch records, output lengths, synthesis).  Only the host
+planning is amortised.  When the new data change the low-pass decision or
+exceed the output capacities the slot is captured again.
+
+Two slots alternate, so run k+1 stages its inputs (on the high-priority side
+stream) while run k's graph is still executing; a slot is reused only after
+its previous replay finished.  The RenderResult of a run references the
+slot's static output, valid until that slot runs again (two runs later).
+"""
+
+from __future__ import annotations
+
+from dataclasses import replace
+
+import numpy as np
+import torch
+
+from . import _lib, engine
+from ._dev import StaticUploads, UploadMeter, require_cuda
+from ._staging import _STAGER, side_stream
+from .farrow import as_filter
+
+
+def _dims(a):
+    return tuple(int(v) for v in a.shape) if hasattr(a, "shape") else tuple(np.shape(a))
+
+
+def structure_key(jobs, filt, precision) -> tuple:
+    """What a plan is valid for (data excluded, room constants included)."""
+    f = as_filter(filt)
+    key = [precision, id(f.branches) if isinstance(f.branches, torch.Tensor) else
+           np.asarray(f.branches).tobytes(), f.branch_len, f.nominal_delay]
+    for jb in jobs:
+        key.append((_dims(jb.pos), _dims(jb.s), _dims(jb.mic),
+                    np.asarray(jb.dims, np.float64).tobytes(),
+                    np.asarray(jb.walls, np.float64).tobytes(), int(jb.max_order),
+                    tuple((int(a), int(b)) for a, b in jb.tiers), float(jb.rate), float(jb.c),
+                    float(jb.d_min),
+                    None if jb.image_index is None else np.asarray(jb.image_index).tobytes(),
+                    engine._key(jb.path_key, jb.pos), engine._key(jb.signal_key, jb.s)))
+    return tuple(key)
+
+
+class _Slot:
+    def __init__(self):
+        self.graph = None
+        self.done = None
+        self.decision = None
+        self.capacity = None
+        self.timing = []  # (start, end) events of the captured synthesis launch
+        self.run_index = None  # run whose replay last used the slot
+
+
+class RenderPlan:
+    """Captured render of `jobs`' structure (see the module docstring)."""
+
+    DEPTH = 2
+
+    def __init__(self, jobs, f, precision: str = "fp32", device=None):
+        if precision not in ("fp32", "fp64"):
+            raise ValueError("precision must be 'fp32' or 'fp64'")
+        self.dev = require_cuda(device)
+        self.f = as_filter(f)
+        self.precision = precision
+        self.template = list(jobs)
+        self.key = structure_key(jobs, f, precision)
+        self.slots = []
+        dt = torch.float32 if precision == "fp32" else torch.float64
+        for _ in range(self.DEPTH):
+            slot = _Slot()
+            static_pos, static_sig = {}, {}
+            slot.jobs = []
+            for jb in jobs:
+                pk, sk = engine._key(jb.path_key, jb.pos), engine._key(jb.signal_key, jb.s)
+                if pk not in static_pos:
+                    static_pos[pk] = torch.empty(_dims(jb.pos), dtype=torch.float64, device=self.dev)
+                if sk not in static_sig:
+                    static_sig[sk] = torch.empty(int(np.prod(_dims(jb.s))), dtype=dt, device=self.dev)
+                mic = torch.empty(_dims(jb.mic), dtype=torch.float64, device=self.dev)
+                slot.jobs.append(replace(jb, pos=static_pos[pk], s=static_sig[sk], mic=mic,
+                                         path_key=("plan", pk), signal_key=("plan", sk)))
+            slot.paths = None
+            self.slots.append(slot)
+        self.k = 0
+        self.captures = 0
+        self.kernel_ms = {}  # run index -> synthesis kernel time of that replay
+
+    # ------------------------------------------------------------------
+    def _load(self, slot, jobs):
+        """Copy the inputs of `jobs` into the slot's static tensors (on the
+        current stream)."""
+        seen = set()
+        for jb, sj in zip(jobs, slot.jobs):
+            for src, dst in ((jb.pos, sj.pos), (jb.s, sj.s), (jb.mic, sj.mic)):
+                if id(dst) in seen:
+                    continue
+                seen.add(id(dst))
+                if isinstance(src, torch.Tensor):
+                    dst.copy_(src.reshape(dst.shape), non_blocking=True)
+                else:
+                    a = np.asarray(src).reshape(dst.shape[0], -1) if dst.dim() > 1 else \
+                        np.asarray(src).reshape(-1)
+                    _STAGER.upload([(0, a)], dst)
+
+    def _stage(self, slot, ready):
+        """Stage the slot's static inputs into its static paths buffer: on the
+        side stream after `ready` (pipelined), or on the current stream."""
+        if slot.paths is None:  # first staging allocates the slot's paths buffer
+            if ready is not None:
+                torch.cuda.current_stream(self.dev).wait_event(ready)
+            geom = engine.Geometry(slot.jobs, device=self.dev, defer=True)
+            slot.paths = geom.paths
+            return geom
+        return engine.Geometry(slot.jobs, device=self.dev, inputs_ready=ready, paths=slot.paths,
+                               defer=True)
+
+    SLACK = 0.1  # output capacity headroom of a capture (fraction of the length bound)
+
+    def _device_work(self, slot, geom, timing=None):
+        geom.length_slack = self.SLACK
+        geom.finish()
+        return engine.render(geom, [sj.s for sj in slot.jobs], self.f, precision=self.precision,
+                             signal_keys=[engine._key(sj.signal_key, sj.s) for sj in slot.jobs],
+                             timing=timing)
+
+    def _collect(self, slot):
+        """Record the synthesis time of the slot's finished replay."""
+        if slot.run_index is not None and slot.timing:
+            a, b = slot.timing[-1]
+            self.kernel_ms[slot.run_index] = a.elapsed_time(b)
+            slot.run_index = None
+
+    def flush_timing(self) -> dict:
+        """Wait for every slot and collect the pending kernel timings."""
+        for slot in self.slots:
+            if slot.done is not None:
+                slot.done.synchronize()
+            self._collect(slot)
+        return self.kernel_ms
+
+    def _capture(self, slot, geom):
+        """Dry run (populates caches, sizes the static uploads), re-stage,
+        capture; the captured graph is then replayed for this run."""
+        with UploadMeter() as meter:
+            self._device_work(slot, geom)
+        torch.cuda.synchronize(self.dev)
+        geom = self._stage(slot, None)
+        uploads = StaticUploads(int(meter.used * 1.25) + (64 << 10))
+        graph = torch.cuda.CUDAGraph()
+        slot.timing = []
+        launches0 = _lib.launch_count()
+        with uploads, torch.cuda.graph(graph):
+            res = self._device_work(slot, geom, slot.timing)
+        slot.graph_launches = _lib.launch_count() - launches0  # kernels replayed per run
+        slot.graph, slot.result, slot.uploads = graph, res, uploads
+        slot.decision = geom.lowpass_decision()
+        slot.capacity = np.asarray([geom.length_bound(j) for j in range(len(slot.jobs))])  # slacked
+        self.captures += 1
+
+    def run(self, jobs) -> engine.RenderResult:
+        """Render `jobs` (same structure as the plan's template)."""
+        if structure_key(jobs, self.f, self.precision) != self.key:
+            raise ValueError("jobs do not match the plan's structure")
+        slot = self.slots[self.k % self.DEPTH]
+        self.k += 1
+        if slot.done is not None:
+            slot.done.synchronize()  # its previous replay (two runs ago) finished
+        self._collect(slot)
+        side = side_stream(self.dev)
+        with torch.cuda.stream(side):
+            self._load(slot, jobs)
+            ready = torch.cuda.Event()
+            ready.record()
+        staged0 = _lib.launch_count()
+        geom = self._stage(slot, ready)
+        staged = _lib.launch_count() - staged0  # staging kernels (outside the graph)
+        bound = np.asarray([geom.length_bound(j) for j in range(len(slot.jobs))])
+        if slot.graph is None or geom.lowpass_decision() != slot.decision \
+                or np.any(bound > slot.capacity):
+            torch.cuda.current_stream(self.dev).wait_stream(side)
+            self._capture(slot, geom)
+        slot.graph.replay()
+        slot.done = torch.cuda.Event()
+        slot.done.record()
+        slot.run_index = self.k - 1
+        r = slot.result
+        res = engine.RenderResult(r.out, r.offsets, r.capacity, r.n_images,
+                                  staged + slot.graph_launches, *r._dev)
+        return res

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._dev import ptr, readback, require_cuda, stream_handle, to_dev
+from ._dev import h2d, ptr, readback, require_cuda, stream_handle, to_dev
 
 UPSAMPLE_HALFWIDTH = 32
 UPSAMPLE_KAISER_BETA = 7.857
@@ -184,7 +184,7 @@ def decimate_batch(x: torch.Tensor, rate: float, factor: int, bw: torch.Tensor |
         return raw
     if need.size == x.shape[0]:
         return lowpass_batch(x, rate, 0.9 * nyq)[:, ::factor]
-    idx = torch.as_tensor(need, device=x.device)
+    idx = h2d(need.astype(np.int64), x.device)
     out = raw.clone()
     out[idx] = lowpass_batch(x[idx], rate, 0.9 * nyq)[:, ::factor]
     return out

@@ -249,3 +249,37 @@ def test_memory_split_batches_match_single_batch():
         a = whole.job(j).double().cpu().numpy()
         b = split.job(j).double().cpu().numpy()
         assert np.max(np.abs(a - b)) <= 1e-6 * np.max(np.abs(a))
+
+
+def test_render_plan_replays_match_direct_renders():
+    """CUDA-graph render plans (plan.RenderPlan): replays equal direct
+    renders bit for bit, follow new inputs (signals, paths), alternate
+    their two slots, and re-capture when new data exceed the captured
+    output capacity."""
+    import dataclasses
+    from paper_2508_03065_b200.plan import RenderPlan
+    scenes = workloads.make_scenes("c5", duration=0.05, max_order=6, n_channels=3,
+                                   tiers=((2, 1), (4, 32), (6, 256)))
+    f = hann_sinc(64, 14)
+    jobs = scene_jobs(scenes)
+    plan = RenderPlan(jobs, f)
+    rng = np.random.default_rng(3)
+    for it in range(4):
+        s = (scenes[0].s * (1.0 + it)).astype(np.float32)
+        pos = scenes[0].pos + 0.01 * it
+        jb = [dataclasses.replace(j, s=s, pos=pos) for j in jobs]
+        got = plan.run(jb)
+        ref = render_jobs(jb, f)
+        assert np.array_equal(got.lengths, ref.lengths)
+        for j in range(len(jb)):
+            assert torch.equal(got.job(j), ref.job(j)), (it, j)
+    assert plan.captures == 2  # one per slot
+    # a source path pushed far away exceeds the captured capacity: re-capture
+    far = scenes[0].pos + np.array([30.0, 0.0, 0.0])
+    jb = [dataclasses.replace(j, pos=far) for j in jobs]
+    got = plan.run(jb)
+    ref = render_jobs(jb, f)
+    assert plan.captures == 3 and np.array_equal(got.lengths, ref.lengths)
+    assert torch.equal(got.job(0), ref.job(0))
+    with pytest.raises(ValueError):
+        plan.run(jobs[:1])
