@@ -14,13 +14,14 @@ from .room import ImageSourceSpec, MicPosition, Room, enumerate_images, image_co
 from .synth import (BudgetError, DelayStreams, SynthesisConfig, cost_report,
                     full_rate_moving_oracle, prepare_streams, render, render_jobs, synthesize)
 from .trajectory import Trajectory, bandlimited_upsample, decimate
+from .plan import RenderPlan
 from .reference import (ComparisonReport, StaticRIR, compare, splice_baseline, static_render,
                         static_rir)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BudgetError", "ComparisonReport", "DelayStreams", "StaticRIR", "compare",
+    "BudgetError", "ComparisonReport", "DelayStreams", "RenderPlan", "StaticRIR", "compare",
     "splice_baseline", "static_render", "static_rir", "FarrowFilter", "ImageSourceSpec", "MicPosition", "MvbError",
     "Room", "SynthesisConfig", "Trajectory", "bandlimited_upsample", "cost_report", "decimate",
     "enumerate_images", "full_rate_moving_oracle", "hann_sinc", "image_count", "prepare_streams",
