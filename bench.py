@@ -278,17 +278,20 @@ def run_ours(args):
     inputs_ready = torch.cuda.Event()
     inputs_ready.record()
 
-    # repeated renders of one structure replay a captured CUDA graph
-    # (plan.RenderPlan: inputs re-staged and every kernel re-run each step);
-    # image shards keep the direct path (their all-reduce / reduce are NCCL)
+    # repeated renders of one structure replay captured CUDA graphs
+    # (plan.RenderPlan: inputs re-staged and every kernel re-run each step;
+    # image shards all-reduce the track maxima eagerly between two graphs)
     plan = None
-    if shard is None and not args.no_plan:
+    if not args.no_plan:
         from paper_2508_03065_b200.plan import RenderPlan
-        plan = RenderPlan(jobs, f, precision=precision)
+        plan = RenderPlan(jobs, f, precision=precision, shard=shard)
 
     def step(record=False):
         if plan is not None:
-            return plan.run(jobs)
+            res = plan.run(jobs)
+            if shard is not None:
+                parallel.reduce_to_root(res.out)
+            return res
         tl = timing if record else None
         res = render_jobs(jobs, f, precision=precision, shard=shard, timing=tl,
                           inputs_ready=inputs_ready)

@@ -39,6 +39,11 @@ def structure_key(jobs, filt, precision) -> tuple:
     f = as_filter(filt)
     key = [precision, id(f.branches) if isinstance(f.branches, torch.Tensor) else
            np.asarray(f.branches).tobytes(), f.branch_len, f.nominal_delay]
+    # which jobs share a path / signal (first-occurrence index), not identities
+    share_p, share_s = {}, {}
+    for jb in jobs:
+        share_p.setdefault(engine._key(jb.path_key, jb.pos), len(share_p))
+        share_s.setdefault(engine._key(jb.signal_key, jb.s), len(share_s))
     for jb in jobs:
         key.append((_dims(jb.pos), _dims(jb.s), _dims(jb.mic),
                     np.asarray(jb.dims, np.float64).tobytes(),
@@ -46,7 +51,8 @@ def structure_key(jobs, filt, precision) -> tuple:
                     tuple((int(a), int(b)) for a, b in jb.tiers), float(jb.rate), float(jb.c),
                     float(jb.d_min),
                     None if jb.image_index is None else np.asarray(jb.image_index).tobytes(),
-                    engine._key(jb.path_key, jb.pos), engine._key(jb.signal_key, jb.s)))
+                    share_p[engine._key(jb.path_key, jb.pos)],
+                    share_s[engine._key(jb.signal_key, jb.s)]))
     return tuple(key)
 
 
@@ -65,9 +71,28 @@ class RenderPlan:
 
     DEPTH = 2
 
-    def __init__(self, jobs, f, precision: str = "fp32", device=None):
+    def __init__(self, jobs, f, precision: str = "fp32", device=None, shard=None, dmax_hook=None):
+        """`shard=(rank, world)`: render the image subset rank::world of every
+        job (as synth.render_jobs) with `dmax_hook` (default: all-reduce MAX
+        over the process group) applied to the track maxima between a
+        geometry graph and a render graph -- the collective itself is issued
+        eagerly, never captured."""
         if precision not in ("fp32", "fp64"):
             raise ValueError("precision must be 'fp32' or 'fp64'")
+        if shard is not None and int(shard[1]) > 1:
+            from . import parallel
+            from .room import image_count
+            if precision == "fp64":
+                raise ValueError("the exact fp64 engine runs replicas only")
+            rank, world = int(shard[0]), int(shard[1])
+            jobs = [replace(jb, image_index=parallel.image_subset(
+                        image_count(jb.max_order) if jb.image_index is None else jb.image_index,
+                        rank, world), signal_key=engine._key(jb.signal_key, jb.s),
+                        path_key=engine._key(jb.path_key, jb.pos)) for jb in jobs]
+            if dmax_hook is None:
+                dmax_hook = parallel.allreduce_max
+        self.shard = shard
+        self.dmax_hook = dmax_hook
         self.dev = require_cuda(device)
         self.f = as_filter(f)
         self.precision = precision
@@ -125,12 +150,20 @@ class RenderPlan:
 
     SLACK = 0.1  # output capacity headroom of a capture (fraction of the length bound)
 
-    def _device_work(self, slot, geom, timing=None):
+    def _geometry_work(self, geom):
         geom.length_slack = self.SLACK
         geom.finish()
+
+    def _render_work(self, slot, geom, timing=None):
         return engine.render(geom, [sj.s for sj in slot.jobs], self.f, precision=self.precision,
                              signal_keys=[engine._key(sj.signal_key, sj.s) for sj in slot.jobs],
                              timing=timing)
+
+    def _device_work(self, slot, geom, timing=None):
+        self._geometry_work(geom)
+        if self.dmax_hook is not None:
+            self.dmax_hook(geom.dmax_dev)
+        return self._render_work(slot, geom, timing)
 
     def _collect(self, slot):
         """Record the synthesis time of the slot's finished replay."""
@@ -158,8 +191,18 @@ class RenderPlan:
         graph = torch.cuda.CUDAGraph()
         slot.timing = []
         launches0 = _lib.launch_count()
-        with uploads, torch.cuda.graph(graph):
-            res = self._device_work(slot, geom, slot.timing)
+        if self.dmax_hook is None:
+            with uploads, torch.cuda.graph(graph):
+                res = self._device_work(slot, geom, slot.timing)
+            slot.graphs = [graph]
+        else:  # geometry graph | eager cross-rank reduction of dmax | render graph
+            graph_b = torch.cuda.CUDAGraph()
+            with uploads, torch.cuda.graph(graph):
+                self._geometry_work(geom)
+            with uploads, torch.cuda.graph(graph_b):
+                res = self._render_work(slot, geom, slot.timing)
+            slot.graphs = [graph, graph_b]
+            slot.dmax = geom.dmax_dev
         slot.graph_launches = _lib.launch_count() - launches0  # kernels replayed per run
         slot.graph, slot.result, slot.uploads = graph, res, uploads
         slot.decision = geom.lowpass_decision()
@@ -168,6 +211,14 @@ class RenderPlan:
 
     def run(self, jobs) -> engine.RenderResult:
         """Render `jobs` (same structure as the plan's template)."""
+        if self.shard is not None and int(self.shard[1]) > 1:
+            from . import parallel
+            from .room import image_count
+            rank, world = int(self.shard[0]), int(self.shard[1])
+            jobs = [replace(jb, image_index=parallel.image_subset(
+                        image_count(jb.max_order) if jb.image_index is None else jb.image_index,
+                        rank, world), signal_key=engine._key(jb.signal_key, jb.s),
+                        path_key=engine._key(jb.path_key, jb.pos)) for jb in jobs]
         if structure_key(jobs, self.f, self.precision) != self.key:
             raise ValueError("jobs do not match the plan's structure")
         slot = self.slots[self.k % self.DEPTH]
@@ -188,7 +239,10 @@ class RenderPlan:
                 or np.any(bound > slot.capacity):
             torch.cuda.current_stream(self.dev).wait_stream(side)
             self._capture(slot, geom)
-        slot.graph.replay()
+        slot.graphs[0].replay()
+        if len(slot.graphs) > 1:
+            self.dmax_hook(slot.dmax)
+            slot.graphs[1].replay()
         slot.done = torch.cuda.Event()
         slot.done.record()
         slot.run_index = self.k - 1

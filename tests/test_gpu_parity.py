@@ -283,3 +283,40 @@ def test_render_plan_replays_match_direct_renders():
     assert torch.equal(got.job(0), ref.job(0))
     with pytest.raises(ValueError):
         plan.run(jobs[:1])
+    # jobs without explicit keys: fresh arrays each run, same sharing pattern
+    anon = [dataclasses.replace(j, path_key=None, signal_key=None, pos=scenes[0].pos.copy(),
+                                s=scenes[0].s.astype(np.float32)) for j in jobs[:1]]
+    plan1 = RenderPlan(anon, f)
+    for it in range(3):
+        jb = [dataclasses.replace(anon[0], pos=scenes[0].pos + 0.001 * it,
+                                  s=(scenes[0].s * (it + 1)).astype(np.float32))]
+        assert torch.equal(plan1.run(jb).job(0), render_jobs(jb, f).job(0))
+
+
+def test_render_plan_image_shards():
+    """Sharded plans: geometry graph, eager dmax hook, render graph; the
+    shards' replays sum to the full render (shards in sequence on one GPU)."""
+    from paper_2508_03065_b200 import engine, parallel
+    from paper_2508_03065_b200.plan import RenderPlan
+    import dataclasses
+    g, scenes, chans = _scenes("c5")
+    f = _filter_of(g, scenes[0].fd_taps)
+    jobs = scene_jobs(scenes, chans)
+    world = 2
+    local = []
+    for r in range(world):
+        sub = [dataclasses.replace(jb, image_index=parallel.image_subset(
+            mroom.image_count(jb.max_order), r, world)) for jb in jobs]
+        local.append(engine.Geometry(sub).dmax)
+    gmax = np.max(np.stack(local), axis=0)
+
+    def hook(t):
+        t.copy_(torch.as_tensor(gmax, device=t.device))
+
+    plans = [RenderPlan(jobs, f, shard=(r, world), dmax_hook=hook) for r in range(world)]
+    for _ in range(3):  # capture, then replays on both slots
+        parts = [p.run(jobs) for p in plans]
+        total = np.concatenate([sum(p.job(j).double() for p in parts).cpu().numpy()
+                                for j in range(len(jobs))])
+        ref = np.concatenate(_oracle(scenes, chans, g["branches"]))
+        assert rel_err(total, ref) <= FP32_TOL
