@@ -1,0 +1,86 @@
+"""Randomised parity (hypothesis): random rooms, reflection coefficients,
+image orders, tier tables (including non-power-of-two factors), path and
+signal lengths, fixed or moving receivers and filter lengths, each rendered
+by both engines and compared with the CPU oracle.  Marker `gpu`."""
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
+
+from paper_2508_03065_b200 import engine, hann_sinc  # noqa: E402
+from paper_2508_03065_b200.synth import render_jobs  # noqa: E402
+
+
+@st.composite
+def scenes(draw):
+    rng = np.random.default_rng(draw(st.integers(0, 2**31 - 1)))
+    dims = rng.uniform(2.5, 9.0, size=3)
+    walls = rng.uniform(0.5, 0.97, size=6)
+    max_order = draw(st.integers(0, 5))
+    # tiers: ascending orders, full rate first, then decimated factors
+    cuts = sorted(set(draw(st.lists(st.integers(0, max_order), min_size=0, max_size=2))) | {max_order})
+    factors = [1] + [draw(st.sampled_from([8, 16, 32, 37, 64, 100, 128, 256])) for _ in cuts[1:]]
+    tiers = tuple((int(c), int(n)) for c, n in zip(cuts, factors))
+    rate = draw(st.sampled_from([8000.0, 16000.0, 48000.0]))
+    T = draw(st.integers(1, 3000))
+    n = draw(st.integers(1, 3000))
+    margin = 0.3
+    lo, hi = margin, dims - margin
+    way = rng.uniform(lo, hi, size=(4, 3))
+    t = np.linspace(0, 1, T)[:, None]
+    pos = way[0] + (way[1] - way[0]) * t + 0.2 * np.sin(2 * np.pi * 3 * t) * (way[2] - way[0]) / 4
+    pos = np.clip(pos, lo, hi)
+    moving = draw(st.booleans()) and T > 1
+    mic = (rng.uniform(lo, hi) + 0.05 * np.sin(2 * np.pi * t) * np.array([1.0, -0.5, 0.2])
+           if moving else rng.uniform(lo, hi))
+    if moving:
+        mic = np.clip(mic, lo, hi)
+    L = draw(st.sampled_from([0, 8, 16, 32, 64]))  # 0: the reference's design(3, 8, 0.8)
+    s = rng.standard_normal(n)
+    S = 1 + sum(4 * o * o + 2 for o in range(1, max_order + 1))
+    sub = None
+    if draw(st.booleans()) and S > 2:
+        sub = np.sort(rng.choice(S, size=int(rng.integers(1, S)), replace=False)).astype(np.int64)
+    return dict(dims=dims, walls=walls, max_order=max_order, tiers=tiers, rate=rate, pos=pos,
+                mic=mic, s=s, L=L, sub=sub)
+
+
+def _oracle(sc, f, x):
+    im = None
+    if sc["sub"] is not None:
+        im = orc.enumerate_images(sc["dims"], sc["walls"], sc["max_order"]).take(sc["sub"])
+    return orc.OracleScene(x, sc["pos"], sc["mic"], sc["dims"], sc["walls"], sc["max_order"],
+                           sc["tiers"], f.branches, sc["rate"], images=im).render()
+
+
+def _filter(L):
+    if L:
+        return hann_sinc(L, 14)
+    from conftest import golden
+    from paper_2508_03065_b200.farrow import FarrowFilter
+    return FarrowFilter(3, 8, golden("kernels.npz")["design_3_8_08"], 3, 0.8)
+
+
+@settings(max_examples=150, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@given(scenes())
+def test_random_scenes_both_engines(sc):
+    f = _filter(sc["L"])
+    for precision, tol in (("fp64", 1e-12), ("fp32", 1e-5)):
+        x = sc["s"] if precision == "fp64" else sc["s"].astype(np.float32)
+        job = engine.Job(s=x, pos=sc["pos"], mic=sc["mic"], dims=sc["dims"], walls=sc["walls"],
+                         max_order=sc["max_order"], tiers=sc["tiers"], rate=sc["rate"],
+                         image_index=sc["sub"])
+        y = render_jobs([job], f, precision=precision).job(0).double().cpu().numpy()
+        ref = _oracle(sc, f, np.asarray(x, np.float64))
+        assert y.size == ref.size, (precision, sc["tiers"], y.size, ref.size)
+        assert rel_err(y, ref) <= tol, (precision, sc["tiers"], sc["max_order"], sc["L"])
