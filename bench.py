@@ -374,7 +374,8 @@ def run_ours(args):
             cfg = SynthesisConfig(audio_rate=sc.rate, max_order=sc.max_order, tiers=sc.tiers,
                                   precision=precision)
             s32 = np.ascontiguousarray(sc.s)
-            y = render(s32, traj, room, sc.mics[0], f, cfg)  # warm
+            for _ in range(max(2, args.warmup)):  # warm (render() caches a plan on a repeat)
+                y = render(s32, traj, room, sc.mics[0], f, cfg)
             tt = 0.0
             for _ in range(args.steps):
                 torch.cuda.synchronize()

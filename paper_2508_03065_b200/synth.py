@@ -316,9 +316,53 @@ def _synthesize_source(x, streams, f, cfg) -> np.ndarray:
     return buffers[0].cpu().numpy()
 
 
+_PLANS: dict = {}  # render(): the one cached RenderPlan, keyed by structure
+_SEEN: list = [None]  # structure key of the previous render() call
+
+
+def release_plans() -> None:
+    """Drop render()'s cached CUDA-graph plan (and the device memory it holds)."""
+    _PLANS.clear()
+    _SEEN[0] = None
+
+
+def _plan_render(a, traj, room, m, f, cfg):
+    """render() through a cached RenderPlan when the same structure is seen
+    twice in a row (loops over signals / paths); None when not applicable."""
+    import os
+    if os.environ.get("MVB_PLAN_CACHE", "1") == "0" or cfg.modulate != "receiver" \
+            or cfg.t60 is not None:
+        return None
+    from .plan import RenderPlan, structure_key
+    prec = _precision(a, cfg)
+    job = engine.Job(s=a, pos=traj.positions, mic=m, dims=room.dims, walls=room.wall_reflection,
+                     max_order=cfg.max_order, tiers=cfg.tier_table(), rate=traj.rate,
+                     c=cfg.sound_speed, d_min=cfg.d_min)
+    key = structure_key([job], f, prec)
+    plan = _PLANS.get(key)
+    if plan is None:
+        if _SEEN[0] != key:
+            _SEEN[0] = key
+            return None
+        _PLANS.clear()
+        plan = _PLANS[key] = RenderPlan([job], f, precision=prec)
+    from ._staging import d2h
+    return d2h(plan.run([job]).job(0), np.float64)
+
+
 def render(s, traj, room, mic, f, cfg) -> np.ndarray:
-    """End-to-end: trajectory in, reverberant moving-source audio out."""
-    _check_signal(s)
+    """End-to-end: trajectory in, reverberant moving-source audio out.
+    Repeated calls with the same structure (shapes, room, orders, tiers,
+    filter, precision) replay a cached CUDA-graph plan from the second
+    repeat on (plan.RenderPlan; `release_plans()` frees it, environment
+    MVB_PLAN_CACHE=0 disables it)."""
+    a = _check_signal(s)
+    if traj.rate != cfg.audio_rate:
+        raise ValueError("trajectory rate must equal the audio rate")
+    m = _check_receiver(mic, room, len(traj))
+    y = _plan_render(a, traj, room, m, as_filter(f), cfg)
+    if y is not None:
+        return y
     return synthesize(s, prepare_streams(traj, room, mic, cfg), f, cfg)
 
 

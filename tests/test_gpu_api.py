@@ -269,3 +269,33 @@ def test_edge_cases_match_oracle(case):
         ref = oracle_render(np.asarray(xx, np.float64), tr, MIC, f, cfg)
         assert y.size == ref.size, case
         assert rel_err(y, ref) <= tol, case
+
+
+def test_render_reuses_a_plan_for_repeated_structure():
+    """render() replays a cached RenderPlan from the second repeat of a
+    structure on: outputs equal the direct path bit for bit; a different
+    structure or MVB_PLAN_CACHE=0 renders directly."""
+    import os
+    from paper_2508_03065_b200 import synth
+    f = design_filter()
+    n = 3000
+    tr = moving(n)
+    cfg = mvb.SynthesisConfig(max_order=4, order_split=1, decimation=32)
+    synth.release_plans()
+    ys = [mvb.render(sine(300.0 * (k + 1), n).astype(np.float32), tr, ROOM, MIC, f, cfg)
+          for k in range(4)]
+    assert len(synth._PLANS) == 1
+    os.environ["MVB_PLAN_CACHE"] = "0"
+    try:
+        direct = [mvb.render(sine(300.0 * (k + 1), n).astype(np.float32), tr, ROOM, MIC, f, cfg)
+                  for k in range(4)]
+    finally:
+        del os.environ["MVB_PLAN_CACHE"]
+    for a, b in zip(ys, direct):
+        assert np.array_equal(a, b)
+    # exact engine through a plan: still bit-identical to the oracle path
+    x = sine(700.0, n)
+    y64 = [mvb.render(x, tr, ROOM, MIC, f, cfg) for _ in range(3)]
+    assert all(np.array_equal(y64[0], y) for y in y64[1:])
+    synth.release_plans()
+    assert not synth._PLANS
