@@ -9,11 +9,12 @@ point called without the built library or without a GPU raises.
 """
 
 from ._lib import MvbError
-from .farrow import FarrowFilter, hann_sinc, split_delay
-from .room import ImageSourceSpec, MicPosition, Room, enumerate_images, image_count
+from .farrow import FarrowFilter, branch_filter, delay_stream, hann_sinc, split_delay
+from .room import ImageSourceSpec, MicPosition, Room, attenuation, enumerate_images, image_count
 from .synth import (BudgetError, DelayStreams, SynthesisConfig, cost_report,
-                    full_rate_moving_oracle, prepare_streams, render, render_jobs, synthesize)
-from .trajectory import Trajectory, bandlimited_upsample, decimate
+                    full_rate_moving_oracle, high_order_distances, low_order_distances,
+                    merge_streams, prepare_streams, render, render_jobs, synthesize)
+from .trajectory import Trajectory, bandlimited_upsample, bandwidth_estimate, decimate
 from .plan import RenderPlan
 from .reference import (ComparisonReport, StaticRIR, compare, splice_baseline, static_render,
                         static_rir)
@@ -25,5 +26,7 @@ __all__ = [
     "splice_baseline", "static_render", "static_rir", "FarrowFilter", "ImageSourceSpec", "MicPosition", "MvbError",
     "Room", "SynthesisConfig", "Trajectory", "bandlimited_upsample", "cost_report", "decimate",
     "enumerate_images", "full_rate_moving_oracle", "hann_sinc", "image_count", "prepare_streams",
-    "render", "render_jobs", "split_delay", "synthesize", "__version__",
+    "render", "render_jobs", "split_delay", "synthesize", "__version__", "attenuation",
+    "bandwidth_estimate", "branch_filter", "delay_stream", "high_order_distances",
+    "low_order_distances", "merge_streams",
 ]

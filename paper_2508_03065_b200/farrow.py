@@ -17,6 +17,13 @@ This module keeps that interface:
   centered_branches change of basis mu -> (mu - 1/2), used by the fp32 GPU
                     path so that Horner runs on [-1/2, 1/2) (same filter).
   split_delay       D/mu convention of reference farrow.py:192-211.
+  branch_filter     the shared branch pass (farrow.py:214-229) on the GPU.
+  delay_stream      one time-varying delay (farrow.py:253-274): GPU branch
+                    pass + the accumulate operator.
+  evaluate, evaluate_power_sum, impulse_response
+                    the reference's scalar cross-check helpers
+                    (farrow.py:146-149, 232-250): one output sample / one
+                    L-tap response, used by tests, never by a render.
 
 Filter *design* by constrained least squares (reference farrow.py:74-136)
 is offline setup and out of scope; pass its output here.
@@ -29,6 +36,7 @@ from functools import lru_cache
 from math import comb
 
 import numpy as np
+import torch
 
 
 @dataclass(frozen=True)
@@ -135,3 +143,87 @@ def as_filter(f) -> FarrowFilter:
                             passband=float(getattr(f, "passband", 1.0)))
     except AttributeError as e:  # pragma: no cover - message only
         raise TypeError("expected a FarrowFilter-like object") from e
+
+
+def _as_signal(x):
+    """1-D finite float64 input (numpy or CUDA tensor), reference
+    farrow.py:220-225 errors."""
+    if isinstance(x, torch.Tensor):
+        a = x.to(torch.float64)
+        ok = bool(torch.isfinite(a).all()) if a.numel() else True
+    else:
+        a = np.asarray(x, dtype=np.float64)
+        ok = bool(np.all(np.isfinite(a)))
+    if a.ndim != 1:
+        raise ValueError("input must be 1-D")
+    if not ok:
+        raise ValueError("input must be finite")
+    if a.shape[0] == 0:
+        raise ValueError("input must be nonempty")
+    return a
+
+
+def branch_filter(x, f):
+    """(M+1, len(x)+L-1) branch streams: the input convolved with every
+    branch once (reference farrow.py:214-229), one libmvb launch.  numpy in
+    -> numpy out; a CUDA tensor in -> a CUDA tensor out."""
+    from . import kernels
+    f = as_filter(f)
+    return kernels.branch_filter(_as_signal(x), f.branches)
+
+
+def evaluate(streams, n, split):
+    """One output sample: Horner in mu of the branch streams at n - D
+    (reference farrow.py:232-241); 0 outside the streams."""
+    v = streams.cpu().numpy() if isinstance(streams, torch.Tensor) else np.asarray(streams)
+    idx = n - split.integer_part
+    if idx < 0 or idx >= v.shape[1]:
+        return 0.0
+    mu = split.fractional_part
+    acc = v[-1, idx]
+    for k in range(v.shape[0] - 2, -1, -1):
+        acc = acc * mu + v[k, idx]
+    return float(acc)
+
+
+def evaluate_power_sum(streams, n, split):
+    """The same sample as an explicit power sum (reference farrow.py:244-250)."""
+    v = streams.cpu().numpy() if isinstance(streams, torch.Tensor) else np.asarray(streams)
+    idx = n - split.integer_part
+    if idx < 0 or idx >= v.shape[1]:
+        return 0.0
+    mu = split.fractional_part
+    return float(sum(v[k, idx] * mu ** k for k in range(v.shape[0])))
+
+
+def impulse_response(f, mu):
+    """h(n, mu) = sum_k c_k(n) mu^k for one fractional delay (reference
+    farrow.py:146-149)."""
+    f = as_filter(f)
+    return (float(mu) ** np.arange(f.poly_order + 1)) @ f.branches
+
+
+def delay_stream(x, f, tau):
+    """x delayed by the per-output-sample delay tau (samples, all >= D0):
+    one GPU branch pass and one accumulate launch (reference
+    farrow.py:253-274, same errors).  Output length len(tau)."""
+    from . import kernels
+    from ._dev import require_cuda, to_dev
+    f = as_filter(f)
+    t = tau.to(torch.float64) if isinstance(tau, torch.Tensor) else np.asarray(tau, np.float64)
+    if t.ndim != 1:
+        raise ValueError("tau must be 1-D")
+    finite = bool(torch.isfinite(t).all()) if isinstance(t, torch.Tensor) else bool(np.all(np.isfinite(t)))
+    if not finite:
+        raise ValueError("tau must be finite")
+    low = bool((t < f.nominal_delay).any()) if isinstance(t, torch.Tensor) else \
+        bool(np.any(t < f.nominal_delay))
+    if low:
+        raise ValueError("tau below the filter latency; pad the input first")
+    on_dev = isinstance(x, torch.Tensor) and x.is_cuda
+    dev = require_cuda(x.device if on_dev else None)
+    streams = kernels.branch_filter(to_dev(_as_signal(x), torch.float64, dev), f.branches)
+    td = to_dev(t, torch.float64, dev).reshape(1, -1).contiguous()
+    out = torch.zeros(td.shape[1], dtype=torch.float64, device=dev)
+    kernels.accumulate_images(out, streams, td, torch.ones_like(td), 0, f.nominal_delay)
+    return out if on_dev else out.cpu().numpy()

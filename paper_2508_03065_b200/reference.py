@@ -228,7 +228,8 @@ def compare(a, b, passband=0.8, rate=16000.0, interior=0.05, runtime_counts=None
     env = torch.abs(an)[lo:hi]
     env_jump = float(torch.max(torch.abs(torch.diff(env)))) if env.numel() > 1 else 0.0
     phase_step = torch.angle(an[1:] * torch.conj(an[:-1]))
-    inst = phase_step * rate / (2.0 * np.pi)
+    # true division (torch rewrites `tensor / python scalar` as a reciprocal multiply)
+    inst = (phase_step * rate) / torch.tensor(2.0 * np.pi, dtype=F64, device=dev)
     smooth = max(1, int(round(0.010 * rate)))
     inst = _convolve_same(inst, torch.full((smooth,), 1.0 / smooth, dtype=F64, device=dev))
     track = inst[lo:max(lo + 1, hi - 1)].cpu().numpy()

@@ -154,6 +154,13 @@ def enumerate_images(room: Room, max_order: int):
             for i in range(order.shape[0])]
 
 
+def attenuation(beta, distance):
+    """Spherical-spreading gain beta / (4 pi d) (reference room.py:168-172)."""
+    if distance <= 0:
+        raise ValueError("attenuation requires distance > 0 (clamp first)")
+    return beta / (4.0 * np.pi * distance)
+
+
 def as_arrays(specs, room):
     """(offset (S,3), sign (S,3), beta (S,), order (S,)) as numpy, in list
     order (reference room.py:175-187)."""

@@ -27,8 +27,9 @@ import numpy as np
 import torch
 
 from . import _lib, engine
+from ._dev import require_cuda
 from .farrow import as_filter
-from .room import as_mic, image_count, image_table
+from .room import as_arrays, as_mic, image_count, image_table
 
 SUMMATION_BLOCK = 32
 
@@ -110,12 +111,59 @@ def _canonical_index(specs, room, max_order) -> np.ndarray:
 
 
 class DelayStreams:
-    """Per-image distance tracks of one render, held on the device.
+    """Per-image distance tracks plus the specs they belong to (reference
+    synth.py:94-119): rate, specs, d (S, T) metres at `rate`, eval_count,
+    tau(cfg), amplitude(cfg), image_count().
 
-    Same attributes as reference synth.py:94-119 (rate, specs, d,
-    eval_count, tau(cfg), amplitude(cfg), image_count()); `d` is
-    materialised from the device tracks only when read.
+    Built by low_order_distances / high_order_distances / merge_streams or
+    directly like the reference's dataclass; `d` may be a numpy array or a
+    CUDA float64 tensor (the stream builders keep it on the device and
+    materialise the numpy view only when `.d` is read).
     """
+
+    def __init__(self, rate, specs, d, eval_count=0):
+        self.rate = float(rate)
+        self._specs = list(specs)
+        self._d = d
+        self.eval_count = int(eval_count)
+
+    @property
+    def specs(self):
+        return self._specs
+
+    def image_count(self):
+        return len(self._specs)
+
+    @property
+    def d(self) -> np.ndarray:
+        if isinstance(self._d, torch.Tensor):
+            self._d = self._d.cpu().numpy()
+        return self._d
+
+    def d_dev(self, device=None) -> torch.Tensor:
+        """(S, T) float64 tracks on the device."""
+        if isinstance(self._d, torch.Tensor) and self._d.is_cuda:
+            return self._d
+        from ._dev import to_dev
+        return to_dev(np.asarray(self._d, dtype=np.float64), torch.float64, require_cuda(device))
+
+    def beta_dev(self, device=None) -> torch.Tensor:
+        from ._dev import to_dev
+        return to_dev(np.array([sp.beta for sp in self.specs], dtype=np.float64), torch.float64,
+                      require_cuda(device))
+
+    def tau(self, cfg):
+        return self.rate * self.d / cfg.sound_speed
+
+    def amplitude(self, cfg):
+        beta = np.array([s.beta for s in self.specs])
+        return beta[:, None] / (4.0 * np.pi * np.maximum(self.d, cfg.d_min))
+
+
+class GeometryStreams(DelayStreams):
+    """prepare_streams' result: the tracks of one render held by the engine
+    (coarse tier tracks and interpolation records on the device); `specs`
+    and `d` are materialised only when read."""
 
     def __init__(self, geometry, rate, room, max_order, index):
         self.geometry = geometry
@@ -144,12 +192,80 @@ class DelayStreams:
             self._d = materialize_tracks(self.geometry)
         return self._d
 
-    def tau(self, cfg):
-        return self.rate * self.d / cfg.sound_speed
+    def d_dev(self, device=None) -> torch.Tensor:
+        return materialize_tracks_dev(self.geometry)
 
-    def amplitude(self, cfg):
-        beta = np.array([s.beta for s in self.specs])
-        return beta[:, None] / (4.0 * np.pi * np.maximum(self.d, cfg.d_min))
+    def beta_dev(self, device=None) -> torch.Tensor:
+        g = self.geometry
+        S = int(g.n_img[0])
+        return g.images[int(g.img_off[0]):int(g.img_off[0]) + S].view(torch.float64)[:, 3]
+
+
+# ---------------------------------------------------------------------------
+# stream builders (reference synth.py:122-179): materialised per-image tracks
+def _mic_pos(mic):
+    return np.asarray(mic.pos if hasattr(mic, "pos") else mic, dtype=np.float64)
+
+
+def low_order_distances(images, traj, mic, room) -> DelayStreams:
+    """Exact per-sample distances of `images` along `traj` (reference
+    synth.py:122-130), one libmvb distance pass; eval_count = S * T."""
+    from . import kernels
+    if not images:
+        return DelayStreams(traj.rate, [], np.zeros((0, len(traj))))
+    offset, sign, _, _ = as_arrays(images, room)
+    dev = require_cuda()
+    d = kernels.distance_streams(torch.from_numpy(offset).to(dev), sign, _mic_pos(mic),
+                                 traj.positions)
+    return DelayStreams(traj.rate, list(images), d, eval_count=d.numel())
+
+
+def high_order_distances(images, traj_coarse, mic, room, out_len, factor) -> DelayStreams:
+    """Distances on the coarse path, band-limit upsampled by `factor` to
+    out_len samples (reference synth.py:133-158): factor 1 truncates or
+    hold-extends; eval_count counts the coarse evaluations."""
+    from . import kernels
+    from ._dev import ptr, stream_handle
+    from .trajectory import phase_table
+    out_len, factor = int(out_len), int(factor)
+    if not images:
+        return DelayStreams(traj_coarse.rate * factor, [], np.zeros((0, out_len)))
+    offset, sign, _, _ = as_arrays(images, room)
+    dev = require_cuda()
+    coarse = kernels.distance_streams(torch.from_numpy(offset).to(dev), sign, _mic_pos(mic),
+                                      traj_coarse.positions)
+    S, K = coarse.shape
+    if factor == 1:
+        d = coarse[:, :out_len]
+        if K < out_len:
+            d = torch.cat([d, d[:, -1:].expand(S, out_len - K)], dim=1)
+        d = d.contiguous()
+    else:
+        tab = torch.from_numpy(np.array(phase_table(factor))).to(dev)
+        d = torch.empty(S, out_len, dtype=torch.float64, device=dev)
+        _lib.call("mvb_upsample_streams", ptr(coarse), S, K, ptr(tab), factor, tab.shape[1],
+                  out_len, ptr(d), stream_handle(dev))
+    return DelayStreams(traj_coarse.rate * factor, list(images), d, eval_count=coarse.numel())
+
+
+def merge_streams(low: DelayStreams, high: DelayStreams) -> DelayStreams:
+    """Union of two stream sets, rows restored to enumeration order
+    (reference synth.py:161-179; same errors, an empty side returns the
+    other unchanged)."""
+    if low.image_count() == 0:
+        return high
+    if high.image_count() == 0:
+        return low
+    if low.rate != high.rate:
+        raise ValueError("stream rates differ")
+    da, db = low.d_dev(), high.d_dev()
+    if da.shape[1] != db.shape[1]:
+        raise ValueError("stream lengths differ")
+    specs = list(low.specs) + list(high.specs)
+    order = sorted(range(len(specs)), key=lambda i: specs[i])
+    d = torch.cat([da, db], dim=0)[torch.as_tensor(order, device=da.device)]
+    return DelayStreams(low.rate, [specs[i] for i in order], d,
+                        eval_count=low.eval_count + high.eval_count)
 
 
 def materialize_tracks(geom) -> np.ndarray:
@@ -239,12 +355,12 @@ def prepare_streams(traj, room, mic, cfg, images=None) -> DelayStreams:
     else:
         index = select_images(room, traj, m, cfg)
     if index is not None and index.size == 0:
-        return DelayStreams(None, traj.rate, room, cfg.max_order, index)
+        return GeometryStreams(None, traj.rate, room, cfg.max_order, index)
     job = engine.Job(s=None, pos=traj.positions, mic=m, dims=room.dims, walls=room.wall_reflection,
                      max_order=cfg.max_order, tiers=cfg.tier_table(), rate=traj.rate,
                      c=cfg.sound_speed, d_min=cfg.d_min, image_index=index)
     geom = engine.Geometry([job])
-    return DelayStreams(geom, traj.rate, room, cfg.max_order, index)
+    return GeometryStreams(geom, traj.rate, room, cfg.max_order, index)
 
 
 def _precision(s, cfg) -> str:
@@ -265,49 +381,68 @@ def _check_signal(s):
 
 def synthesize(s, streams: DelayStreams, f, cfg) -> np.ndarray:
     """Render s through the moving image set (reference synth.py:194-258).
-    Output length len(s) + ceil(max delay) + L, float64."""
+    Output length len(s) + ceil(max delay) + L, float64.
+
+    prepare_streams' engine-held tracks render on the fused engine (fp32 or
+    the exact fp64 one, `cfg.precision`); materialised track sets (the
+    stream builders, or a DelayStreams built by hand) and modulate="source"
+    render on the exact fp64 track path, the reference's own algorithm."""
     a = _check_signal(s)
     filt = as_filter(f)
     if streams.image_count() == 0:
         return np.zeros(a.size + filt.branch_len)
-    if cfg.modulate == "source":
-        return _synthesize_source(a, streams, filt, cfg)
+    geom = getattr(streams, "geometry", None)
+    if cfg.modulate == "source" or geom is None:
+        return _synthesize_tracks(a, streams, filt, cfg)
     prec = _precision(a, cfg)
-    res = engine.render(streams.geometry, [a], filt, precision=prec)
+    res = engine.render(geom, [a], filt, precision=prec)
     from ._staging import d2h
     return d2h(res.job(0), np.float64)
 
 
-def _synthesize_source(x, streams, f, cfg) -> np.ndarray:
-    """modulate="source" (reference synth.py:228-242, its validation switch):
-    the gain is applied at emission time, so every image filters its own
-    gain-modulated input -- one branch pass per image.  fp64, reference
-    arithmetic and block/pairwise order, on the device with the operator
-    trio (kernels.branch_filter / accumulate_images); materialises (S, out_len)
-    tracks like the reference, so it is meant for validation-size renders."""
+def _synthesize_tracks(x, streams, f, cfg) -> np.ndarray:
+    """Exact fp64 synthesis from (S, T) tracks on the device, reference
+    synth.py:211-258 step for step: hold-extend the tracks to the output
+    length, tau/amplitude per sample, one branch pass (kernels.branch_filter)
+    and one accumulate_images call per 32-image block, pairwise block merge.
+    modulate="source" (synth.py:228-242, the reference's validation switch)
+    applies the gain at emission time instead: one branch pass per image of
+    its gain-modulated input.  Materialises (S, out_len) tracks like the
+    reference, so it is meant for validation-size renders."""
     from . import kernels
-    geom = streams.geometry
-    dev = geom.dev
-    d = materialize_tracks_dev(geom)
+    dev = require_cuda()
+    d = streams.d_dev(dev)
     S, T = d.shape
     xs = torch.from_numpy(np.array(x, dtype=np.float64)).to(dev)
     tau_max = streams.rate * float(d.max().item()) / cfg.sound_speed
     out_len = x.size + int(np.ceil(tau_max)) + f.branch_len
     d_ext = torch.cat([d, d[:, -1:].expand(S, out_len - T)], dim=1) if T < out_len else d[:, :out_len]
     d_ext = d_ext.contiguous()
-    tau = streams.rate * d_ext / cfg.sound_speed
-    img = geom.images[int(geom.img_off[0]):int(geom.img_off[0]) + S]
-    beta = img.view(torch.float64)[:, 3]
+    # divide by a device tensor: torch turns `tensor / python scalar` into a
+    # multiply by the reciprocal, which is not the reference's rounding
+    c = torch.tensor(cfg.sound_speed, dtype=torch.float64, device=dev)
+    tau = (streams.rate * d_ext) / c
+    beta = streams.beta_dev(dev)
     amp = beta[:, None] / (4.0 * np.pi * torch.clamp_min(d_ext, cfg.d_min))
-    ones = torch.ones(1, out_len, dtype=torch.float64, device=dev)
     branches = torch.from_numpy(np.array(f.branches)).to(dev)
     buffers = []
-    for b0 in range(0, S, SUMMATION_BLOCK):
-        buf = torch.zeros(out_len, dtype=torch.float64, device=dev)
-        for i in range(b0, min(b0 + SUMMATION_BLOCK, S)):
-            v = kernels.branch_filter((xs * amp[i, :x.size]).contiguous(), branches)
-            kernels.accumulate_images(buf, v, tau[i:i + 1], ones, f.branch_len, f.nominal_delay)
-        buffers.append(buf)
+    if cfg.modulate == "source":
+        ones = torch.ones(1, out_len, dtype=torch.float64, device=dev)
+        for b0 in range(0, S, SUMMATION_BLOCK):
+            buf = torch.zeros(out_len, dtype=torch.float64, device=dev)
+            for i in range(b0, min(b0 + SUMMATION_BLOCK, S)):
+                v = kernels.branch_filter((xs * amp[i, :x.size]).contiguous(), branches)
+                kernels.accumulate_images(buf, v, tau[i:i + 1], ones, f.branch_len,
+                                          f.nominal_delay)
+            buffers.append(buf)
+    else:
+        v = kernels.branch_filter(xs, branches)
+        for b0 in range(0, S, SUMMATION_BLOCK):
+            b1 = min(b0 + SUMMATION_BLOCK, S)
+            buf = torch.zeros(out_len, dtype=torch.float64, device=dev)
+            kernels.accumulate_images(buf, v, tau[b0:b1].contiguous(), amp[b0:b1].contiguous(),
+                                      f.branch_len, f.nominal_delay)
+            buffers.append(buf)
     while len(buffers) > 1:  # synth.py:182-191
         merged = [buffers[k] + buffers[k + 1] for k in range(0, len(buffers) - 1, 2)]
         if len(buffers) % 2:

@@ -140,6 +140,18 @@ def bandwidth_batch(x: torch.Tensor, rate: float, energy_fraction: float = 0.99)
     return np.where(kh < 0, 0.0, hz).max(axis=1)
 
 
+def bandwidth_estimate(traj: Trajectory, energy_fraction: float = 0.99) -> float:
+    """Smallest frequency holding `energy_fraction` of the mean-removed
+    displacement power, max over the three axes; 0 Hz for a constant or
+    single-sample path (reference trajectory.py:316-339, same error)."""
+    if not 0.0 < energy_fraction < 1.0:
+        raise ValueError("energy_fraction must be in (0, 1)")
+    if len(traj) < 2:
+        return 0.0
+    pos = to_dev(np.asarray(traj.positions, dtype=np.float64), torch.float64, require_cuda())
+    return float(bandwidth_batch(pos[None], traj.rate, energy_fraction)[0])
+
+
 def bandwidth_estimate_dev(pos: torch.Tensor, rate: float, energy_fraction: float = 0.99) -> float:
     return float(bandwidth_batch(pos[None], rate, energy_fraction)[0])
 

@@ -52,6 +52,34 @@ def test_product_refuses_to_run_without_gpu():
         render(np.ones(100), tr, room, [1.0, 1.0, 1.0], hann_sinc(32), SynthesisConfig(max_order=1))
 
 
+def test_host_api_helpers():
+    """attenuation (reference room.py:168-172, test_room.py:143-151), the
+    DelayStreams dataclass form (synth.py:94-119) and the Farrow scalar
+    helpers (farrow.py:146-149, 232-250) -- host arithmetic, no GPU."""
+    import paper_2508_03065_b200 as mvb
+    from paper_2508_03065_b200 import farrow
+    assert mvb.attenuation(0.5, 2.0) == pytest.approx(0.5 / (8 * np.pi), rel=1e-12)
+    assert mvb.attenuation(1.0, 5.0) == pytest.approx(0.015915, abs=5e-7)
+    with pytest.raises(ValueError):
+        mvb.attenuation(1.0, 0.0)
+    specs = [mvb.ImageSourceSpec(0, (0, 0, 0), (False, False, False), 1.0),
+             mvb.ImageSourceSpec(1, (0, 0, 0), (True, False, False), 0.9)]
+    d = np.array([[1.0, 2.0, 0.01], [3.0, 4.0, 5.0]])
+    st = mvb.DelayStreams(rate=16000.0, specs=specs, d=d)
+    cfg = mvb.SynthesisConfig()
+    assert st.image_count() == 2 and st.eval_count == 0
+    assert np.array_equal(st.tau(cfg), 16000.0 * d / 343.0)
+    amp = st.amplitude(cfg)
+    assert amp[0, 2] == pytest.approx(specs[0].beta / (4 * np.pi * 0.05))
+    f = mvb.FarrowFilter(1, 2, np.array([[1.0, 0.0], [-1.0, 1.0]]), 0, 1.0)
+    assert np.allclose(farrow.impulse_response(f, 0.25), [0.75, 0.25])
+    v = np.array([[1.0, 2.0, 3.0], [0.5, 0.5, 0.5]])
+    sp = mvb.split_delay(1.25, f)
+    assert farrow.evaluate(v, 2, sp) == pytest.approx(2.0 + 0.25 * 0.5)
+    assert farrow.evaluate(v, 2, sp) == farrow.evaluate_power_sum(v, 2, sp)
+    assert farrow.evaluate(v, 0, sp) == 0.0
+
+
 def test_config_validation():
     from paper_2508_03065_b200 import SynthesisConfig
     for kw in [{"audio_rate": 0.0}, {"decimation": 0}, {"order_split": -1}, {"max_order": -1},
