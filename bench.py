@@ -289,8 +289,9 @@ def run_ours(args):
     def step(record=False):
         if plan is not None:
             res = plan.run(jobs)
-            if shard is not None:
-                parallel.reduce_to_root(res.out)
+            if shard is not None:  # on the plan's synthesis stream, after the render
+                with torch.cuda.stream(res.stream):
+                    parallel.reduce_to_root(res.out)
             return res
         tl = timing if record else None
         res = render_jobs(jobs, f, precision=precision, shard=shard, timing=tl,
@@ -334,6 +335,8 @@ def run_ours(args):
         res = step(record=True)
         results.append(res)  # lengths / update counts are read after the bracket
         launches += res.launches
+    if plan is not None:
+        plan.join()  # the plan renders on its own streams: order e1 after them
     e1.record()
     torch.cuda.synchronize()
     barrier()

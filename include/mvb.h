@@ -214,8 +214,10 @@ int mvb_track_bounds(const mvb_image* d_images, const int32_t* d_full_sel, int64
  * reaches the job's largest lb are evaluated (exact distance for factor 1,
  * the reference's 65-tap upsample otherwise), in 2048-sample chunks; a
  * decimated candidate's chunk whose coarse-window bound (negsum as in
- * mvb_coarse_distances) stays below the running maximum is skipped.
- * d_scratch: n_img + n_jobs int32. */
+ * mvb_coarse_distances) stays below the running maximum is skipped; the
+ * surviving chunks are evaluated one sample per thread across the GPU.
+ * d_scratch: MVB_EXACT_LIST_WORDS + n_img + n_jobs int32 (8-byte aligned). */
+#define MVB_EXACT_LIST_WORDS 16386
 int mvb_track_max(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jobs,
                   const double* d_coarse, const double* d_tables, const double* d_paths,
                   double negsum, const double* d_lb, const double* d_ub, int32_t* d_scratch,
@@ -273,6 +275,20 @@ int mvb_track_coeffs(const mvb_image* d_images, const int32_t* d_sel, int64_t n_
 int mvb_sort_keys(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jobs,
                   int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
                   const double* d_paths, const double* d_coarse, double* d_key, void* stream);
+
+/* Fused delay sort (replaces mvb_sort_keys + an argsort + mvb_gather_images
+ * when max_n_img <= MVB_DELAY_SORT_MAX): for every job j and time segment s
+ * (samples [s*seg_len, (s+1)*seg_len)), d_out[(j * max_n_seg + s) *
+ * max_n_img + q] = the job's image records ordered by their distance at the
+ * segment centre (fp32 key, stable sort); slots q >= n_img and segments
+ * past the track hold image min(q, n_img - 1) of the canonical order.
+ * One block radix sort per (job, segment); locality only -- any order
+ * renders the same result up to fp32 summation order. */
+#define MVB_DELAY_SORT_MAX 16384
+int mvb_delay_sort(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jobs,
+                   int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
+                   const double* d_paths, const double* d_coarse, mvb_image* d_out,
+                   void* stream);
 
 /* Fast path: fp32 branch records v'_k = x (*) c'_k (d_cbranch (M1, L) fp64
  * in the centred basis (mu - 1/2)^k, zero branches k >= M1) of n_sig dry

@@ -12,7 +12,10 @@
 //                      upsampler refit per coarse interval as a degree-8
 //                      polynomial in u, anchored in fp64, pre-split (B, f)
 //   k_sort_keys        per-(job, time segment) delay-sort keys (L1 locality)
+#include <algorithm>
 #include <cfloat>
+
+#include <cub/block/block_radix_sort.cuh>
 
 #include "mvb_common.cuh"
 
@@ -229,8 +232,9 @@ __global__ void k_select(const mvb_image* __restrict__ images, const mvb_job* __
     double m = 0.0;
     for (int64_t q = threadIdx.x; q < J.n_img; q += blockDim.x) m = fmax(m, lb[J.img_off + q]);
     m = block_max(m, red);
-    int32_t* sc = scratch + J.img_off + j;
+    int32_t* sc = scratch + MVB_EXACT_LIST_WORDS + J.img_off + j;
     const double LB = m - 1e-9;
+    if (j == 0 && threadIdx.x == 0) scratch[0] = 0;  // survivor list of k_exact_scan
     if (threadIdx.x == 0) {
         sc[0] = 0;
         // every lb is attained by its track to ~1e-12 m, so the exact max is
@@ -249,56 +253,112 @@ __global__ void k_select(const mvb_image* __restrict__ images, const mvb_job* __
 }
 
 // Exact maxima of the candidates over t < T, in chunks of EXACT_CHUNK
-// samples (blockIdx.x strides over chunks).  A decimated candidate's chunk
-// is skipped when the bound of its coarse window (max + negsum (max - min),
-// the window covering every 65-tap sum in the chunk) cannot exceed the
-// running maximum; dmax only grows, so skipping is exact.
+// samples, in two kernels.  k_exact_scan: one warp per (candidate, chunk)
+// pair, pairs grid-strided over the job's warps (blockIdx.y = job).  A
+// decimated candidate's chunk is dropped when the bound of its coarse window
+// (max + negsum (max - min), the window covering every 65-tap sum in the
+// chunk) cannot exceed the running maximum (dmax only grows, so dropping is
+// exact); a surviving chunk is appended to the survivor list in scratch
+// (full-rate candidates, and chunks past the list's capacity, are evaluated
+// in place).  k_exact_eval then spreads the survivors over the whole GPU,
+// one output sample per thread: the 65-tap fp64 upsample of a chunk is the
+// expensive part, and there are typically a handful of surviving chunks of
+// a single candidate.  List entry: job (16 bits) | slot (24) | chunk (24).
 constexpr int EXACT_CHUNK = 2048;
+constexpr int EXACT_SUB = 256;  // samples per k_exact_eval block
+constexpr int EXACT_LIST_CAP = (MVB_EXACT_LIST_WORDS - 2) / 2;
 
-__global__ void k_exact_max(const mvb_image* __restrict__ images, const mvb_job* __restrict__ jobs,
-                            const double* __restrict__ coarse, const double* __restrict__ tables,
-                            const double* __restrict__ paths, double negsum,
-                            const int32_t* __restrict__ scratch, double* __restrict__ dmax) {
-    __shared__ double red[32];
-    __shared__ int skip;
-    const int64_t j = blockIdx.z;
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// bound of the upsampled track over samples [t0, t1): coarse window max +
+// negsum (max - min) + 1e-9 (lane-parallel, warp-uniform result)
+__device__ __forceinline__ double window_bound(const double* __restrict__ c, int64_t K,
+                                               int64_t N, int64_t t0, int64_t t1, double negsum,
+                                               int lane) {
+    int64_t k0 = t0 / N - 32, k1 = (t1 - 1) / N + 32;
+    k0 = k0 < 0 ? 0 : k0;
+    k1 = k1 > K - 1 ? K - 1 : k1;
+    double M = -DBL_MAX, m = -DBL_MAX;  // m holds -min
+    for (int64_t k = k0 + lane; k <= k1; k += 32) {
+        const double v = c[k];
+        M = fmax(M, v);
+        m = fmax(m, -v);
+    }
+    M = warp_max(M);
+    m = -warp_max(m);
+    return M + negsum * (M - m) + 1e-9;
+}
+
+__global__ void k_exact_scan(const mvb_image* __restrict__ images, const mvb_job* __restrict__ jobs,
+                             const double* __restrict__ coarse, const double* __restrict__ tables,
+                             const double* __restrict__ paths, double negsum,
+                             int32_t* __restrict__ scratch, double* __restrict__ dmax) {
+    const int64_t j = blockIdx.y;
     const mvb_job& J = jobs[j];
-    const int32_t* sc = scratch + J.img_off + j;
+    const int32_t* sc = scratch + MVB_EXACT_LIST_WORDS + J.img_off + j;
     const int count = sc[0];
+    const int lane = threadIdx.x & 31;
     const int64_t n_chunks = (J.T + EXACT_CHUNK - 1) / EXACT_CHUNK;
-    for (int slot = blockIdx.y; slot < count; slot += gridDim.y) {
+    const int64_t pairs = (int64_t)count * n_chunks;
+    const int64_t wpb = blockDim.x >> 5;
+    volatile double* dm = dmax + j;
+    unsigned long long* list = reinterpret_cast<unsigned long long*>(scratch + 2);
+    for (int64_t p = blockIdx.x * wpb + (threadIdx.x >> 5); p < pairs; p += gridDim.x * wpb) {
+        const int slot = (int)(p / n_chunks);
+        const int64_t ch = p - (int64_t)slot * n_chunks;
         const mvb_image im = images[sc[1 + slot]];
-        for (int64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
-            const int64_t t0 = ch * EXACT_CHUNK;
-            const int64_t t1 = t0 + EXACT_CHUNK < J.T ? t0 + EXACT_CHUNK : J.T;
-            if (im.factor != 1) {
-                // coarse window of the chunk: [t0/N - 32, (t1-1)/N + 32], clamped
-                const double* c = coarse + im.coarse;
-                const int64_t K = im.n_coarse;
-                int64_t k0 = t0 / im.factor - 32, k1 = (t1 - 1) / im.factor + 32;
-                k0 = k0 < 0 ? 0 : k0;
-                k1 = k1 > K - 1 ? K - 1 : k1;
-                double M = -DBL_MAX, m = DBL_MAX;
-                for (int64_t k = k0 + threadIdx.x; k <= k1; k += blockDim.x) {
-                    M = fmax(M, c[k]);
-                    m = fmin(m, c[k]);
-                }
-                M = block_max(M, red);
-                m = -block_max(-m, red);
-                if (threadIdx.x == 0)
-                    skip = M + negsum * (M - m) + 1e-9 < *(volatile double*)(dmax + j);
-                __syncthreads();
-                if (skip) continue;
+        const int64_t t0 = ch * EXACT_CHUNK;
+        const int64_t t1 = t0 + EXACT_CHUNK < J.T ? t0 + EXACT_CHUNK : J.T;
+        double best = 0.0;
+        if (im.factor == 1) {
+            for (int64_t t = t0 + lane; t < t1; t += 32)
+                best = fmax(best, image_distance(im, paths + 3 * (J.pos_off + t), mic_row(J, paths, t)));
+        } else {
+            const double* c = coarse + im.coarse;
+            if (window_bound(c, im.n_coarse, im.factor, t0, t1, negsum, lane) < *dm) continue;
+            int at = 0;
+            if (lane == 0) at = atomicAdd(scratch, 1);
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if (at < EXACT_LIST_CAP) {
+                if (lane == 0)
+                    list[at] = ((unsigned long long)j << 48) | ((unsigned long long)slot << 24) |
+                               (unsigned long long)ch;
+                continue;
             }
-            double best = 0.0;
-            for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x)
-                best = fmax(best, im.factor == 1
-                                      ? image_distance(im, paths + 3 * (J.pos_off + t), mic_row(J, paths, t))
-                                      : exact_upsample(coarse + im.coarse, im.n_coarse, tables + im.table,
-                                                       im.factor, t));
-            best = block_max(best, red);
-            if (threadIdx.x == 0) atomic_max_pos(dmax + j, best);
+            for (int64_t t = t0 + lane; t < t1; t += 32)  // list full: evaluate in place
+                best = fmax(best, exact_upsample(c, im.n_coarse, tables + im.table, im.factor, t));
         }
+        best = warp_max(best);
+        if (lane == 0 && best > 0.0) atomic_max_pos(dmax + j, best);
+    }
+}
+
+__global__ void __launch_bounds__(EXACT_SUB) k_exact_eval(
+    const mvb_image* __restrict__ images, const mvb_job* __restrict__ jobs,
+    const double* __restrict__ coarse, const double* __restrict__ tables,
+    const int32_t* __restrict__ scratch, double* __restrict__ dmax) {
+    __shared__ double red[32];
+    const int n = min(scratch[0], EXACT_LIST_CAP);
+    const unsigned long long* list = reinterpret_cast<const unsigned long long*>(scratch + 2);
+    constexpr int SUBS = EXACT_CHUNK / EXACT_SUB;
+    for (int u = blockIdx.x; u < n * SUBS; u += gridDim.x) {
+        const unsigned long long e = list[u / SUBS];
+        const int64_t j = (int64_t)(e >> 48), slot = (int64_t)((e >> 24) & 0xffffff),
+                      ch = (int64_t)(e & 0xffffff);
+        const mvb_job& J = jobs[j];
+        const int32_t* sc = scratch + MVB_EXACT_LIST_WORDS + J.img_off + j;
+        const mvb_image& im = images[sc[1 + slot]];
+        const int64_t t = ch * EXACT_CHUNK + (int64_t)(u % SUBS) * EXACT_SUB + threadIdx.x;
+        double v = 0.0;
+        if (t < J.T && t < (ch + 1) * EXACT_CHUNK)
+            v = exact_upsample(coarse + im.coarse, im.n_coarse, tables + im.table, im.factor, t);
+        v = block_max(v, red);
+        if (threadIdx.x == 0 && v > 0.0) atomic_max_pos(dmax + j, v);
+        __syncthreads();  // red is reused by the next unit
     }
 }
 
@@ -460,6 +520,85 @@ __global__ void k_sort_keys(const mvb_image* __restrict__ images, const mvb_job*
         k = coarse[im.coarse + c];
     }
     key[(j * max_n_seg + s) * max_n_img + i] = k;
+}
+
+// Fused delay sort: one CTA per (segment s, job j).  Key of image i = its
+// distance at the segment centre (k_sort_keys' key) as fp32 bits (distances
+// are >= 0, so the bit patterns order like the values); a stable block radix
+// sort (deterministic); the records are gathered in that order, striped so
+// consecutive threads write consecutive 96-byte records.  Slots past the
+// job's images (padding keys sort last) and segments past its track (all
+// keys padding: identity order) repeat as before: index min(q, n - 1).
+template <int BT, int IPT>
+__global__ void __launch_bounds__(BT) k_delay_sort(const mvb_image* __restrict__ images,
+                                                   const mvb_job* __restrict__ jobs,
+                                                   int64_t max_n_img, int64_t max_n_seg,
+                                                   int64_t seg_len, const double* __restrict__ paths,
+                                                   const double* __restrict__ coarse,
+                                                   mvb_image* __restrict__ out) {
+    using Sort = cub::BlockRadixSort<unsigned, BT, IPT, int>;
+    extern __shared__ __align__(16) unsigned char dsort_smem[];
+    auto& temp = *reinterpret_cast<typename Sort::TempStorage*>(dsort_smem);
+    const int64_t s = blockIdx.x, j = blockIdx.y;
+    const mvb_job& J = jobs[j];
+    const int n = (int)J.n_img;
+    const bool active = s * seg_len < J.T;
+    int64_t t = s * seg_len + seg_len / 2;
+    if (t > J.T - 1) t = J.T - 1;
+    const mvb_image* __restrict__ im0 = images + J.img_off;
+    unsigned keys[IPT];
+    int vals[IPT];
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+        const int i = threadIdx.x * IPT + k;  // blocked arrangement
+        unsigned key = 0xffffffffu;
+        if (active && i < n) {
+            const mvb_image& im = im0[i];
+            double d;
+            if (im.factor == 1) {
+                d = image_distance(im, paths + 3 * (J.pos_off + t), mic_row(J, paths, t));
+            } else {
+                int64_t c = t / im.factor;
+                if (c >= im.n_coarse) c = im.n_coarse - 1;
+                d = coarse[im.coarse + c];
+            }
+            key = __float_as_uint((float)d);
+        }
+        keys[k] = key;
+        vals[k] = i;
+    }
+    Sort(temp).SortBlockedToStriped(keys, vals);
+    mvb_image* __restrict__ dst = out + (j * max_n_seg + s) * max_n_img;
+    constexpr int CH = sizeof(mvb_image) / 16;
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+        const int q = k * BT + threadIdx.x;  // striped arrangement
+        if (q < max_n_img) {
+            const int src = vals[k] < n - 1 ? vals[k] : n - 1;
+            const float4* a = reinterpret_cast<const float4*>(im0 + src);
+            float4* b = reinterpret_cast<float4*>(dst + q);
+#pragma unroll
+            for (int c = 0; c < CH; ++c) b[c] = __ldg(a + c);
+        }
+    }
+}
+
+template <int BT, int IPT>
+static int launch_delay_sort(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
+                             int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
+                             const double* paths, const double* coarse, mvb_image* out,
+                             cudaStream_t s) {
+    using Sort = cub::BlockRadixSort<unsigned, BT, IPT, int>;
+    const size_t smem = sizeof(typename Sort::TempStorage);
+    static bool attr = false;  // one opt-in per process and instantiation
+    if (!attr) {
+        cudaFuncSetAttribute(k_delay_sort<BT, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr = true;
+    }
+    k_delay_sort<BT, IPT><<<dim3((unsigned)max_n_seg, (unsigned)n_jobs), BT, smem, s>>>(
+        images, jobs, max_n_img, max_n_seg, seg_len, paths, coarse, out);
+    return MVB_OK;
 }
 
 // Coarse path rows: dst[dst_row[q] + k] = src[src_row[q] + k * N], k < K
@@ -793,8 +932,11 @@ int mvb_track_max(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
         return fail(MVB_EINVAL, "track_max: null");
     cudaStream_t s = as_stream(stream);
     k_select<<<(unsigned)n_jobs, 256, 0, s>>>(images, jobs, lb, ub, scratch, dmax);
-    k_exact_max<<<dim3(64, 8, (unsigned)n_jobs), 256, 0, s>>>(images, jobs, coarse, tables, paths,
-                                                               negsum, scratch, dmax);
+    // scan: ~2 blocks of 8 warps per SM for one job, fewer per job for batches
+    const unsigned bx = (unsigned)std::max<int64_t>(4, std::min<int64_t>(296, 1184 / n_jobs));
+    k_exact_scan<<<dim3(bx, (unsigned)n_jobs), 256, 0, s>>>(images, jobs, coarse, tables, paths,
+                                                           negsum, scratch, dmax);
+    k_exact_eval<<<592, EXACT_SUB, 0, s>>>(images, jobs, coarse, tables, scratch, dmax);
     return check_launch("track_max");
 }
 
@@ -823,6 +965,36 @@ int mvb_track_coeffs(const mvb_image* images, const int32_t* sel, int64_t n_sel,
     // 64 threads x 8 intervals: measured best of {64,128,256} x {4,8} on c3/c4
     // (more resident blocks hide the staging prologue; 70% of the FFMA peak on c4)
     return launch_coeffs<64, 8>(sp, images, sel, n_sel, max_K, jobs, coarse, coef, stream);
+}
+
+int mvb_delay_sort(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
+                   int64_t max_n_img, int64_t max_n_seg, int64_t seg_len, const double* paths,
+                   const double* coarse, mvb_image* out, void* stream) {
+    if (n_jobs < 0 || n_jobs > 65535 || max_n_img < 0 || max_n_seg < 0 ||
+        max_n_seg > 0x7fffffff || seg_len < 1)
+        return fail(MVB_EINVAL, "delay_sort: sizes");
+    if (max_n_img > MVB_DELAY_SORT_MAX) return fail(MVB_EINVAL, "delay_sort: too many images");
+    if (n_jobs == 0 || max_n_img == 0 || max_n_seg == 0) return MVB_OK;
+    if (!images || !jobs || !paths || !out) return fail(MVB_EINVAL, "delay_sort: null");
+    cudaStream_t s = as_stream(stream);
+    int rc;
+    if (max_n_img <= 1024)
+        rc = launch_delay_sort<256, 4>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
+                                       coarse, out, s);
+    else if (max_n_img <= 2048)
+        rc = launch_delay_sort<256, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
+                                       coarse, out, s);
+    else if (max_n_img <= 4096)
+        rc = launch_delay_sort<512, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
+                                       coarse, out, s);
+    else if (max_n_img <= 8192)
+        rc = launch_delay_sort<1024, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len,
+                                        paths, coarse, out, s);
+    else
+        rc = launch_delay_sort<1024, 16>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len,
+                                         paths, coarse, out, s);
+    if (rc != MVB_OK) return rc;
+    return check_launch("delay_sort");
 }
 
 int mvb_sort_keys(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs, int64_t max_n_img,

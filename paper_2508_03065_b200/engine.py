@@ -165,7 +165,8 @@ _DEV_CACHE: dict = {}
 
 def _cached_dev(key, make):
     """Small read-only device tables reused across renders (bounded).  Not
-    filled during a graph capture: a captured upload only runs at replay."""
+    filled during a graph capture: a captured upload only runs at replay.
+    Users that a graph captures keep their own reference (Geometry._keep)."""
     t = _DEV_CACHE.get(key)
     if t is None:
         from ._dev import StaticUploads
@@ -344,7 +345,7 @@ class Geometry:
             _lib.call("mvb_track_bounds", ptr(self.images), ptr(self.full_sel),
                       self.full_sel.numel(), ptr(jobs_dev), ptr(self.paths), ptr(self.bbox),
                       ptr(lb), ptr(ub), st)
-        scratch = torch.empty(n_img + nJ, dtype=torch.int32, device=dev)
+        scratch = torch.empty(_lib.EXACT_LIST_WORDS + n_img + nJ, dtype=torch.int32, device=dev)
         dmax = torch.empty(nJ, dtype=torch.float64, device=dev)
         _lib.call("mvb_track_max", ptr(self.images), ptr(jobs_dev), nJ,
                   ptr(self.coarse) if self.dec_sel.numel() else ptr(None), ptr(self.tables),
@@ -352,6 +353,7 @@ class Geometry:
         if dmax_hook is not None:
             dmax_hook(dmax)
         self.dmax_dev = dmax
+        self._bounds = (lb, ub, scratch)  # per-image track bounds, exact-max candidates
         self._dmax = None  # host copy on demand (the render itself never waits for it)
 
     def release(self) -> None:
@@ -454,6 +456,9 @@ class Geometry:
             ("tables", tuple(factors), str(dev)),
             lambda: torch.cat([device_constants(N, dev)["tableT"].reshape(-1) for N in factors])
             if factors else torch.zeros(1, dtype=torch.float64, device=dev))
+        # cached tables this geometry's kernels read: owned here too, so a
+        # captured graph's pointers stay valid if the bounded cache drops them
+        self._keep = [self.tables]
         groups = {}
         for j, jb in enumerate(jobs):
             sub = None if jb.image_index is None else tuple(np.asarray(jb.image_index).tolist())
@@ -522,8 +527,13 @@ class Geometry:
                     room_key[k] = len(rooms)
                     rooms.append((d, w))
                 member_room.append(room_key[k])
-            tab = image_table(np.stack([r[0] for r in rooms]), np.stack([r[1] for r in rooms]),
-                              pl["max_order"], dev)
+            # the lattice depends on the rooms and the order only: cached across
+            # renders (a render plan's graphs then skip the enumeration)
+            tab = _cached_dev(("image_table", tuple(room_key), pl["max_order"], str(dev)),
+                              lambda: image_table(np.stack([r[0] for r in rooms]),
+                                                  np.stack([r[1] for r in rooms]),
+                                                  pl["max_order"], dev))
+            self._keep.append(tab)
             ct, classes, S = pl["ct"], pl["classes"], pl["S"]
             for q, N in enumerate(classes):
                 if N > 1:
@@ -537,6 +547,7 @@ class Geometry:
                                      axis=1)
             img_dev = _cached_dev(("img_tab", pl["key"], str(dev)),
                                   lambda: h2d(pl["img_tab"], dev))  # (S, 2 + nC) int32 (mvb.h)
+            self._keep.append(img_dev)
             job_dev = h2d(np.ascontiguousarray(job_tab), dev)
             _lib.call("mvb_build_images", ptr(tab.offset), ptr(tab.sign), ptr(tab.beta), tab.count,
                       ptr(img_dev), S, ptr(job_dev), len(members), ctypes.byref(ct), pl["img_base"],
@@ -650,9 +661,14 @@ class RenderResult:
     exact) with job j at offsets[j], capacity[j] samples reserved (zeros
     past its length).  The exact lengths are computed on the device
     (mvb_finalize_lengths); `lengths`, `updates` and `job()` wait for them
-    on first use, so a render can be queued without a host round trip."""
+    on first use, so a render can be queued without a host round trip.
+    A render plan's result is produced on the plan's own streams: `done` is
+    its completion event and `stream` the stream that produced it; `job()`,
+    `host()` and `lengths` order the current stream after it (wait()), code
+    that reads `out` directly calls wait() first."""
 
-    def __init__(self, out, offsets, capacity, n_images, launches, lengths_dev, err_dev):
+    def __init__(self, out, offsets, capacity, n_images, launches, lengths_dev, err_dev,
+                 done=None, stream=None):
         self.out = out
         self.offsets = offsets
         self.capacity = capacity
@@ -660,11 +676,20 @@ class RenderResult:
         self.launches = launches
         self._lengths = None
         self._dev = (lengths_dev, err_dev)  # read on first use (no per-render pinned buffers)
+        self.done = done
+        self.stream = stream
+
+    def wait(self) -> "RenderResult":
+        """Order the current stream after the render (no host wait)."""
+        if self.done is not None:
+            torch.cuda.current_stream(self.out.device).wait_event(self.done)
+        return self
 
     @property
     def lengths(self) -> np.ndarray:
         """Per-job out_len (synth.py:211-212)."""
         if self._lengths is None:
+            self.wait()
             lengths_dev, err_dev = self._dev
             h = torch.cat([lengths_dev, err_dev.to(torch.int64)]).cpu().numpy()
             if h[-1]:
@@ -681,6 +706,8 @@ class RenderResult:
     @staticmethod
     def concat(parts: list) -> "RenderResult":
         """One result for consecutive sub-batches (outputs concatenated)."""
+        for p in parts:
+            p.wait()
         shift = np.concatenate([[0], np.cumsum([p.out.numel() for p in parts])[:-1]])
         return RenderResult(torch.cat([p.out for p in parts]),
                             np.concatenate([p.offsets + d for p, d in zip(parts, shift)]),
@@ -695,6 +722,7 @@ class RenderResult:
 
     def host(self) -> np.ndarray:
         """The flat output as numpy (pinned D2H, waits for the render)."""
+        self.wait()
         return d2h(self.out)
 
 
@@ -719,6 +747,31 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     """Synthesize every job of `geom` (signals[j] is job j's dry signal).
     `timing`, if a list, receives (start, end) CUDA events recorded on the
     launch stream around the synthesis kernel."""
+    return prepare_render(geom, signals, filt, precision, signal_keys).launch(timing)
+
+
+class PreparedRender:
+    """A render up to its synthesis launch: the host plan is done and the
+    device work that does not need the exact track maxima (interval
+    records, delay sort, branch records, output buffers) is enqueued.
+    `launch()` enqueues the rest -- exact output lengths from the (possibly
+    cross-rank reduced) maxima, synthesis, partial-sum reduction -- so a
+    render plan can capture the two halves into separate graphs and replay
+    them on different streams."""
+
+    def __init__(self, launch_fn, launches0):
+        self._launch = launch_fn
+        self._launches0 = launches0
+
+    def launch(self, timing: list | None = None) -> RenderResult:
+        res = self._launch(timing)
+        res.launches = _lib.launch_count() - self._launches0
+        return res
+
+
+def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
+                   signal_keys=None) -> PreparedRender:
+    """First half of render() (see PreparedRender)."""
     dev = geom.dev
     st = stream_handle(dev)
     jobs = geom.jobs
@@ -772,7 +825,7 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
                            ls=int(sig_len[keys[j]] + L - 1))
         return out_len, tau_bound, offsets, rows
 
-    def finalize(jobs_dev):
+    def finalize(jobs_dev, st):
         lengths = torch.empty(nJ, dtype=torch.int64, device=dev)
         err = torch.zeros(1, dtype=torch.int32, device=dev)
         _lib.call("mvb_finalize_lengths", ptr(jobs_dev), nJ, ptr(geom.dmax_dev), ptr(lengths),
@@ -794,14 +847,18 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         for j in range(nJ):
             rows[j].update(rec_base=bases[keys[j]], nb=nb)
         jobs_dev = h2d(pack_jobs(rows), dev)
-        lengths, err = finalize(jobs_dev)
         out = torch.zeros(int(out_len.sum()), dtype=torch.float64, device=dev)
-        ev = _events(timing)
-        _lib.call("mvb_synthesize_f64", ptr(jobs_dev), nJ, int(out_len.max()), ptr(geom.images),
-                  ptr(geom.coarse), ptr(geom.tables), ptr(streams), ptr(geom.paths), ptr(out), st)
-        _events_end(timing, ev)
-        return RenderResult(out, offsets, out_len, geom.n_img.copy(),
-                            _lib.launch_count() - launches0, lengths, err)
+
+        def launch64(timing):
+            st = stream_handle(dev)
+            lengths, err = finalize(jobs_dev, st)
+            ev = _events(timing)
+            _lib.call("mvb_synthesize_f64", ptr(jobs_dev), nJ, int(out_len.max()),
+                      ptr(geom.images), ptr(geom.coarse), ptr(geom.tables), ptr(streams),
+                      ptr(geom.paths), ptr(out), st)
+            _events_end(timing, ev)
+            return RenderResult(out, offsets, out_len, geom.n_img.copy(), 0, lengths, err)
+        return PreparedRender(launch64, launches0)
 
     # ---------------------------------------------------------------- fast --
     _mark("render.signals")
@@ -822,20 +879,24 @@ def render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     _mark("render.records_plan")
     jobs_dev = h2d(pack_jobs(rows), dev)
     work_dev = h2d(work, dev)
-    lengths, err = finalize(jobs_dev)
     out = torch.zeros(int(out_len.sum()), dtype=torch.float32, device=dev)
     part = torch.empty(max(part_rows, 1), dtype=torch.float32, device=dev)
-    ev = _events(timing)
     _mark("render.work_upload")
-    _lib.call("mvb_synthesize_f32", ptr(jobs_dev), ptr(work_dev), len(work), ptr(images_sorted),
-              ptr(coef), ptr(rec), ptr(geom.paths), ptr(out), ptr(part), nb, SYNTH_U, st)
-    _events_end(timing, ev)
-    if part_rows:
-        _lib.call("mvb_reduce_partials_f32", ptr(jobs_dev), nJ, int(out_len.max()), ptr(part),
-                  ptr(out), st)
+
+    def launch32(timing):
+        st = stream_handle(dev)
+        lengths, err = finalize(jobs_dev, st)
+        ev = _events(timing)
+        _lib.call("mvb_synthesize_f32", ptr(jobs_dev), ptr(work_dev), len(work),
+                  ptr(images_sorted), ptr(coef), ptr(rec), ptr(geom.paths), ptr(out), ptr(part),
+                  nb, SYNTH_U, st)
+        _events_end(timing, ev)
+        if part_rows:
+            _lib.call("mvb_reduce_partials_f32", ptr(jobs_dev), nJ, int(out_len.max()),
+                      ptr(part), ptr(out), st)
         _mark("render.synth_launched")
-    return RenderResult(out, offsets, out_len, geom.n_img.astype(np.int64),
-                        _lib.launch_count() - launches0, lengths, err)
+        return RenderResult(out, offsets, out_len, geom.n_img.astype(np.int64), 0, lengths, err)
+    return PreparedRender(launch32, launches0)
 
 
 def _interval_records(geom, pre_dev, st) -> torch.Tensor:
@@ -852,12 +913,20 @@ def _interval_records(geom, pre_dev, st) -> torch.Tensor:
 
 def _delay_sort(geom, pre_dev, st):
     """Image records of every job sorted by delay per SEG_LEN-sample time
-    segment (L1 locality of the gathers): keys by mvb_sort_keys, one batched
-    argsort (padding keys +inf sort last, padded slots repeat an own
-    image), records gathered into the (job, segment, max_img) layout."""
+    segment (L1 locality of the gathers) into the (job, segment, max_img)
+    layout: mvb_delay_sort (one block radix sort per segment) up to
+    DELAY_SORT_MAX images per job; beyond, keys by mvb_sort_keys, one
+    batched argsort (padding keys +inf sort last, padded slots repeat an own
+    image) and mvb_gather_images."""
     dev, nJ = geom.dev, len(geom.jobs)
     n_seg = [-(-int(geom.T[j]) // SEG_LEN) for j in range(nJ)]
     max_seg, max_img = max(n_seg), int(geom.n_img.max())
+    if max_img <= _lib.DELAY_SORT_MAX:  # fused keys + block radix sort + gather, one launch
+        images_sorted = torch.empty(nJ * max_seg * max_img, IMG_COLS, dtype=torch.int64,
+                                    device=dev)
+        _lib.call("mvb_delay_sort", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg, SEG_LEN,
+                  ptr(geom.paths), ptr(geom.coarse), ptr(images_sorted), st)
+        return images_sorted, n_seg, max_seg, max_img
     key = torch.full((nJ, max_seg, max_img), float("inf"), dtype=torch.float64, device=dev)
     _lib.call("mvb_sort_keys", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg, SEG_LEN,
               ptr(geom.paths), ptr(geom.coarse), ptr(key), st)

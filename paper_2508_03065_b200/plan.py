@@ -2,24 +2,39 @@
 
 A plan fixes the structure of a batch -- per job the path length, signal
 length, receiver kind, room, image order, tier table, filter and precision --
-and captures every kernel of a render after the staging into one CUDA graph.
+and captures every kernel of a render after the staging into CUDA graphs.
 Each `run` copies the new inputs into the plan's static buffers, redoes the
-staging outside the graph (path bounding boxes and the decimation decision,
-the two small readbacks) and replays the graph, which recomputes all
+staging outside the graphs (path bounding boxes and the decimation decision,
+the two small readbacks) and replays the graphs, which recompute all
 data-dependent work (coarse tracks, bounds, exact maxima, interval records,
 delay sort, branch records, output lengths, synthesis).  Only the host
 planning is amortised.  When the new data change the low-pass decision or
 exceed the output capacities the slot is captured again.
 
-Two slots alternate, so run k+1 stages its inputs (on the high-priority side
-stream) while run k's graph is still executing; a slot is reused only after
-its previous replay finished.  The RenderResult of a run references the
-slot's static output, valid until that slot runs again (two runs later).
+Each slot holds two graphs: the geometry graph (tracks, maxima, records,
+sort, branch records -- short, mostly latency-bound kernels) replays on a
+high-priority stream, the synthesis graph (exact lengths, synthesis,
+partial sums) on the plan's synthesis stream.  Run k+1's geometry therefore
+executes while run k's synthesis still occupies the GPU: its CTAs are
+dispatched ahead of the synthesis' pending ones, so the geometry chain
+leaves the critical path and back-to-back renders approach the synthesis
+time alone.  Image shards reduce the track maxima across ranks between the
+two graphs (eager collective on the geometry stream, never captured).
+
+Two slots alternate; a slot is reused only after its previous replay
+finished.  The RenderResult of a run references the slot's static output,
+valid until that slot runs again (two runs later); it is produced on the
+synthesis stream (`res.done`, `res.stream`; `res.job()` / `res.host()`
+order the caller after it, `join()` orders the current stream after every
+pending run).  A run orders its input copies after the caller's current
+stream, so inputs written there before run() are seen.
 """
 
 from __future__ import annotations
 
 from dataclasses import replace
+
+import os
 
 import numpy as np
 import torch
@@ -54,6 +69,20 @@ def structure_key(jobs, filt, precision) -> tuple:
                     share_p[engine._key(jb.path_key, jb.pos)],
                     share_s[engine._key(jb.signal_key, jb.s)]))
     return tuple(key)
+
+
+_STREAMS: dict = {}
+
+
+def plan_streams(dev) -> tuple:
+    """(geometry, synthesis) streams of the render plans on `dev`: the
+    geometry stream at the highest priority, the synthesis stream at the
+    default one, shared by every plan on the device."""
+    key = str(dev)
+    if key not in _STREAMS:
+        _STREAMS[key] = (torch.cuda.Stream(device=dev, priority=int(os.environ.get("MVB_GEO_PRIO", "0"))),
+                         torch.cuda.Stream(device=dev, priority=0))
+    return _STREAMS[key]
 
 
 class _Slot:
@@ -94,6 +123,7 @@ class RenderPlan:
         self.shard = shard
         self.dmax_hook = dmax_hook
         self.dev = require_cuda(device)
+        self.geo_stream, self.syn_stream = plan_streams(self.dev)
         self.f = as_filter(f)
         self.precision = precision
         self.template = list(jobs)
@@ -150,20 +180,14 @@ class RenderPlan:
 
     SLACK = 0.1  # output capacity headroom of a capture (fraction of the length bound)
 
-    def _geometry_work(self, geom):
+    def _prepare(self, slot, geom):
+        """Geometry and the render's first half (see engine.PreparedRender)."""
         geom.length_slack = self.SLACK
         geom.finish()
-
-    def _render_work(self, slot, geom, timing=None):
-        return engine.render(geom, [sj.s for sj in slot.jobs], self.f, precision=self.precision,
-                             signal_keys=[engine._key(sj.signal_key, sj.s) for sj in slot.jobs],
-                             timing=timing)
-
-    def _device_work(self, slot, geom, timing=None):
-        self._geometry_work(geom)
-        if self.dmax_hook is not None:
-            self.dmax_hook(geom.dmax_dev)
-        return self._render_work(slot, geom, timing)
+        return engine.prepare_render(geom, [sj.s for sj in slot.jobs], self.f,
+                                     precision=self.precision,
+                                     signal_keys=[engine._key(sj.signal_key, sj.s)
+                                                  for sj in slot.jobs])
 
     def _collect(self, slot):
         """Record the synthesis time of the slot's finished replay."""
@@ -180,31 +204,37 @@ class RenderPlan:
             self._collect(slot)
         return self.kernel_ms
 
+    def join(self) -> None:
+        """Order the current stream after every pending run (no host wait)."""
+        cur = torch.cuda.current_stream(self.dev)
+        for slot in self.slots:
+            if slot.done is not None:
+                cur.wait_event(slot.done)
+
     def _capture(self, slot, geom):
         """Dry run (populates caches, sizes the static uploads), re-stage,
-        capture; the captured graph is then replayed for this run."""
+        capture the geometry graph on the geometry stream and the synthesis
+        graph on the synthesis stream; both are then replayed for this run."""
         with UploadMeter() as meter:
-            self._device_work(slot, geom)
+            prep = self._prepare(slot, geom)
+            if self.dmax_hook is not None:
+                self.dmax_hook(geom.dmax_dev)
+            prep.launch()
         torch.cuda.synchronize(self.dev)
         geom = self._stage(slot, None)
         uploads = StaticUploads(int(meter.used * 1.25) + (64 << 10))
-        graph = torch.cuda.CUDAGraph()
+        g_geo, g_syn = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         slot.timing = []
         launches0 = _lib.launch_count()
-        if self.dmax_hook is None:
-            with uploads, torch.cuda.graph(graph):
-                res = self._device_work(slot, geom, slot.timing)
-            slot.graphs = [graph]
-        else:  # geometry graph | eager cross-rank reduction of dmax | render graph
-            graph_b = torch.cuda.CUDAGraph()
-            with uploads, torch.cuda.graph(graph):
-                self._geometry_work(geom)
-            with uploads, torch.cuda.graph(graph_b):
-                res = self._render_work(slot, geom, slot.timing)
-            slot.graphs = [graph, graph_b]
-            slot.dmax = geom.dmax_dev
+        with uploads, torch.cuda.graph(g_geo, stream=self.geo_stream):
+            prep = self._prepare(slot, geom)
+        with uploads, torch.cuda.graph(g_syn, stream=self.syn_stream):
+            res = prep.launch(slot.timing)
+        slot.graphs = [g_geo, g_syn]
+        slot.geom = geom  # owns the cached tables the graphs read
+        slot.dmax = geom.dmax_dev
         slot.graph_launches = _lib.launch_count() - launches0  # kernels replayed per run
-        slot.graph, slot.result, slot.uploads = graph, res, uploads
+        slot.graph, slot.result, slot.uploads = g_geo, res, uploads
         slot.decision = geom.lowpass_decision()
         slot.capacity = np.asarray([geom.length_bound(j) for j in range(len(slot.jobs))])  # slacked
         self.captures += 1
@@ -226,27 +256,40 @@ class RenderPlan:
         if slot.done is not None:
             slot.done.synchronize()  # its previous replay (two runs ago) finished
         self._collect(slot)
+        cur = torch.cuda.current_stream(self.dev)
+        entry = torch.cuda.Event()
+        entry.record(cur)  # inputs the caller wrote on its stream
         side = side_stream(self.dev)
         with torch.cuda.stream(side):
+            side.wait_event(entry)
             self._load(slot, jobs)
             ready = torch.cuda.Event()
             ready.record()
         staged0 = _lib.launch_count()
         geom = self._stage(slot, ready)
-        staged = _lib.launch_count() - staged0  # staging kernels (outside the graph)
+        staged = _lib.launch_count() - staged0  # staging kernels (outside the graphs)
         bound = np.asarray([geom.length_bound(j) for j in range(len(slot.jobs))])
         if slot.graph is None or geom.lowpass_decision() != slot.decision \
                 or np.any(bound > slot.capacity):
-            torch.cuda.current_stream(self.dev).wait_stream(side)
+            cur.wait_stream(side)
             self._capture(slot, geom)
-        slot.graphs[0].replay()
-        if len(slot.graphs) > 1:
-            self.dmax_hook(slot.dmax)
+        staged_ev = torch.cuda.Event()
+        staged_ev.record(cur)  # _stage ordered the current stream after the staging
+        geo, syn = self.geo_stream, self.syn_stream
+        geo.wait_event(staged_ev)
+        with torch.cuda.stream(geo):
+            slot.graphs[0].replay()
+            if self.dmax_hook is not None:
+                self.dmax_hook(slot.dmax)
+            geo_done = torch.cuda.Event()
+            geo_done.record()
+        syn.wait_event(geo_done)
+        with torch.cuda.stream(syn):
             slot.graphs[1].replay()
-        slot.done = torch.cuda.Event()
-        slot.done.record()
+            slot.done = torch.cuda.Event()
+            slot.done.record()
         slot.run_index = self.k - 1
         r = slot.result
-        res = engine.RenderResult(r.out, r.offsets, r.capacity, r.n_images,
-                                  staged + slot.graph_launches, *r._dev)
-        return res
+        return engine.RenderResult(r.out, r.offsets, r.capacity, r.n_images,
+                                   staged + slot.graph_launches, *r._dev, done=slot.done,
+                                   stream=syn)

@@ -28,6 +28,8 @@ for cfg in os.environ.get("CFGS", "c1,c2,c3").split(","):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         rs = [step() for _ in range(K)]
+        rs[-1].wait()  # plan results: order e1 after the plan's streams
+        plan.join()
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / K
         res[name] = {"ms_per_step": round(ms, 3), "updates_per_s": rs[-1].updates / (ms * 1e-3)}

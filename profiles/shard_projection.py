@@ -35,6 +35,8 @@ for cfg in os.environ.get('CFGS', 'c3,c5').split(','):
             for k in range(K):
                 flush.fill_(float(k))
                 step()
+            if mode == "plan":
+                plan.join()  # the plan renders on its own streams
             e1.record(); torch.cuda.synchronize()
             res[W] = e0.elapsed_time(e1) / K
         out[f"{cfg}_{mode}"] = {W: {"ms_per_rank_step": round(t, 3),

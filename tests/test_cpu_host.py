@@ -39,6 +39,9 @@ def test_abi_version_and_counts():
     assert _lib.lib().mvb_abi_version() == 1
     for o in (0, 1, 5, 20):
         assert _lib.image_count(o) == 1 + sum(4 * k * k + 2 for k in range(1, o + 1))
+    hdr = open(os.path.join(ROOT, "include", "mvb.h")).read()
+    assert re.search(r"#define MVB_DELAY_SORT_MAX (\d+)", hdr).group(1) == str(_lib.DELAY_SORT_MAX)
+    assert re.search(r"#define MVB_EXACT_LIST_WORDS (\d+)", hdr).group(1) == str(_lib.EXACT_LIST_WORDS)
 
 
 def test_product_refuses_to_run_without_gpu():

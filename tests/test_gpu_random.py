@@ -1,7 +1,9 @@
 """Randomised parity (hypothesis): random rooms, reflection coefficients,
 image orders, tier tables (including non-power-of-two factors), path and
 signal lengths, fixed or moving receivers and filter lengths, each rendered
-by both engines and compared with the CPU oracle.  Marker `gpu`."""
+by both engines and compared with the CPU oracle.  Source speeds are capped
+at 20 m/s (physical sources; see the fp32 error note in DESIGN.md).
+Marker `gpu`."""
 
 import numpy as np
 import pytest
@@ -40,6 +42,14 @@ def scenes(draw):
     t = np.linspace(0, 1, T)[:, None]
     pos = way[0] + (way[1] - way[0]) * t + 0.2 * np.sin(2 * np.pi * 3 * t) * (way[2] - way[0]) / 4
     pos = np.clip(pos, lo, hi)
+    # physical speeds (<= 20 m/s): the fast path stores each interval's delay
+    # as an fp32 residual, whose rounding grows with the delay excursion per
+    # interval (~ rate/c * speed * N / rate samples), so its 1e-5 bar is a
+    # statement about moving sources, not about supersonic ones
+    if T > 1:
+        v = np.max(np.linalg.norm(np.diff(pos, axis=0), axis=1)) * rate
+        if v > 20.0:
+            pos = pos[0] + (pos - pos[0]) * (20.0 / v)
     moving = draw(st.booleans()) and T > 1
     mic = (rng.uniform(lo, hi) + 0.05 * np.sin(2 * np.pi * t) * np.array([1.0, -0.5, 0.2])
            if moving else rng.uniform(lo, hi))
@@ -75,7 +85,15 @@ def _filter(L):
 @given(scenes())
 def test_random_scenes_both_engines(sc):
     f = _filter(sc["L"])
-    for precision, tol in (("fp64", 1e-12), ("fp32", 1e-5)):
+    # exact engine: ~1e-15 of the peak, except when the reference's anti-alias
+    # FFT low-pass runs (decimate, trajectory.py:279-298): cuFFT and the
+    # oracle's pocketfft round differently (~1e-15 m), which can reach ~1e-12
+    # of the output; the spec's fp64 bar (1e-10) applies then
+    probe = engine.Job(s=sc["s"], pos=sc["pos"], mic=sc["mic"], dims=sc["dims"], walls=sc["walls"],
+                       max_order=sc["max_order"], tiers=sc["tiers"], rate=sc["rate"],
+                       image_index=sc["sub"])
+    lowpass = any(len(d) for d in engine.Geometry([probe]).lowpass_decision())
+    for precision, tol in (("fp64", 1e-10 if lowpass else 1e-12), ("fp32", 1e-5)):
         x = sc["s"] if precision == "fp64" else sc["s"].astype(np.float32)
         job = engine.Job(s=x, pos=sc["pos"], mic=sc["mic"], dims=sc["dims"], walls=sc["walls"],
                          max_order=sc["max_order"], tiers=sc["tiers"], rate=sc["rate"],
