@@ -3,11 +3,18 @@
 One process per GPU (torchrun), torch.distributed for the plumbing:
 
   image shards   c3, c5: rank r renders all output samples of every job from
-                 the strided image subset r, r+W, r+2W, ... of its canonical
-                 list (images are independent; striding keeps
-                 every tier balanced), so enumeration-independent work --
-                 coarse tracks, bounds, interval records, sort, synthesis --
-                 divides by W.  Two exchanges: an all-reduce MAX of the
+                 its image shard (images are independent):
+                 every decimation tier split into W contiguous delay bands
+                 (image_shard: images ordered by |j . dims|, their distance
+                 from the room's centre image -- structural, so a render
+                 plan's shard never changes with the data), band r of every
+                 tier to rank r.  Per-tier counts stay balanced (the records
+                 of a N=32 image cost 8x those of a N=256 one) and a rank's
+                 images keep nearby delays, so the synthesis gathers keep
+                 the L1 locality of the unsharded delay sort (a strided
+                 subset spreads them: +20% synthesis time at W=8).  All
+                 per-image work -- coarse tracks, bounds, interval records,
+                 sort, synthesis -- divides by W.  Two exchanges: an all-reduce MAX of the
                  per-job track maxima (a few bytes; every rank then writes the
                  reference's out_len) and one reduce (sum) of the output
                  buffers to rank 0 -- NCCL over NVLink on B200, ~2 MB (c3) /
@@ -23,6 +30,7 @@ The partition functions are pure host logic (tested with gloo on CPU);
 from __future__ import annotations
 
 import heapq
+from functools import lru_cache
 
 import numpy as np
 
@@ -36,6 +44,75 @@ def image_subset(images, rank: int, world: int) -> np.ndarray:
     idx = np.arange(int(images), dtype=np.int64) if np.ndim(images) == 0 \
         else np.asarray(images, dtype=np.int64)
     return idx[rank::world]
+
+
+@lru_cache(maxsize=16)
+def canonical_lattice(max_order: int) -> tuple:
+    """(j (S, 3) int64, order (S,)) of the canonical image list (reference
+    room.py:98-143: sorted by (order, lattice, parity) with lattice l =
+    (j + q) // 2, parity q = j mod 2) -- the structure only, on the host.
+    The image of a source at the room centre lies at j * dims from it."""
+    K = int(max_order)
+    r = np.arange(-K, K + 1)  # cached per order (a 20th-order lattice is 69k candidates)
+    j = np.stack(np.meshgrid(r, r, r, indexing="ij"), axis=-1).reshape(-1, 3)
+    order = np.abs(j).sum(axis=1)
+    j, order = j[order <= K], order[order <= K]
+    q = np.mod(j, 2)
+    lat = (j + q) // 2
+    keys = (q[:, 2], q[:, 1], q[:, 0], lat[:, 2], lat[:, 1], lat[:, 0], order)
+    idx = np.lexsort(keys)  # last key primary: order, lattice x, y, z, parity x, y, z
+    j, order = j[idx].astype(np.int64), order[idx].astype(np.int64)
+    j.flags.writeable = order.flags.writeable = False  # cached
+    return j, order
+
+
+def image_shard(dims, max_order: int, tiers, rank: int, world: int, images=None) -> np.ndarray:
+    """Canonical image positions owned by `rank` (sorted): every tier of
+    `tiers` ((max_order, N), ...) ordered by |j * dims| (ties by canonical
+    position) and cut into `world` contiguous bands of near-equal count;
+    band `rank` of every tier.  `images`: restrict to these canonical
+    positions (e.g. a t60 cull).  The shards of ranks 0..world-1 partition
+    the image list."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("need 0 <= rank < world")
+    key = (np.asarray(dims, dtype=np.float64).tobytes(), int(max_order),
+           tuple((int(a), int(b)) for a, b in tiers), int(rank), int(world),
+           None if images is None else np.asarray(images, dtype=np.int64).tobytes())
+    return _image_shard(key)
+
+
+@lru_cache(maxsize=256)
+def _image_shard(key) -> np.ndarray:
+    dims_b, max_order, tiers, rank, world, images_b = key
+    dims = np.frombuffer(dims_b, dtype=np.float64)
+    images = None if images_b is None else np.frombuffer(images_b, dtype=np.int64)
+    j, order = canonical_lattice(max_order)
+    idx = np.arange(order.size, dtype=np.int64) if images is None \
+        else np.asarray(images, dtype=np.int64)
+    key = np.linalg.norm(j[idx] * np.asarray(dims, dtype=np.float64).reshape(1, 3), axis=1)
+    mine = []
+    prev = -1
+    for mo, _ in tiers:
+        sel = np.nonzero((order[idx] > prev) & (order[idx] <= int(mo)))[0]
+        prev = int(mo)
+        band = sel[np.lexsort((idx[sel], key[sel]))]  # by distance, then canonical position
+        lo, hi = (band.size * rank) // world, (band.size * (rank + 1)) // world
+        mine.append(idx[band[lo:hi]])
+    out = np.sort(np.concatenate(mine)) if mine else np.zeros(0, np.int64)
+    out.flags.writeable = False  # cached: shared by every caller
+    return out
+
+
+def shard_jobs(jobs, rank: int, world: int) -> list:
+    """Jobs restricted to their image shard of `rank` (image_shard), with
+    explicit path / signal keys so shards of one batch still share them."""
+    from dataclasses import replace
+
+    from . import engine
+    return [replace(jb, image_index=image_shard(jb.dims, jb.max_order, jb.tiers, rank, world,
+                                                jb.image_index),
+                    signal_key=engine._key(jb.signal_key, jb.s),
+                    path_key=engine._key(jb.path_key, jb.pos)) for jb in jobs]
 
 
 def allreduce_max(t, group=None):

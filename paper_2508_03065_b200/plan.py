@@ -101,8 +101,8 @@ class RenderPlan:
     DEPTH = 2
 
     def __init__(self, jobs, f, precision: str = "fp32", device=None, shard=None, dmax_hook=None):
-        """`shard=(rank, world)`: render the image subset rank::world of every
-        job (as synth.render_jobs) with `dmax_hook` (default: all-reduce MAX
+        """`shard=(rank, world)`: render the image shard of `rank` of every
+        job (parallel.image_shard, as synth.render_jobs) with `dmax_hook` (default: all-reduce MAX
         over the process group) applied to the track maxima between a
         geometry graph and a render graph -- the collective itself is issued
         eagerly, never captured."""
@@ -110,14 +110,10 @@ class RenderPlan:
             raise ValueError("precision must be 'fp32' or 'fp64'")
         if shard is not None and int(shard[1]) > 1:
             from . import parallel
-            from .room import image_count
             if precision == "fp64":
                 raise ValueError("the exact fp64 engine runs replicas only")
             rank, world = int(shard[0]), int(shard[1])
-            jobs = [replace(jb, image_index=parallel.image_subset(
-                        image_count(jb.max_order) if jb.image_index is None else jb.image_index,
-                        rank, world), signal_key=engine._key(jb.signal_key, jb.s),
-                        path_key=engine._key(jb.path_key, jb.pos)) for jb in jobs]
+            jobs = parallel.shard_jobs(jobs, rank, world)
             if dmax_hook is None:
                 dmax_hook = parallel.allreduce_max
         self.shard = shard
@@ -243,12 +239,8 @@ class RenderPlan:
         """Render `jobs` (same structure as the plan's template)."""
         if self.shard is not None and int(self.shard[1]) > 1:
             from . import parallel
-            from .room import image_count
             rank, world = int(self.shard[0]), int(self.shard[1])
-            jobs = [replace(jb, image_index=parallel.image_subset(
-                        image_count(jb.max_order) if jb.image_index is None else jb.image_index,
-                        rank, world), signal_key=engine._key(jb.signal_key, jb.s),
-                        path_key=engine._key(jb.path_key, jb.pos)) for jb in jobs]
+            jobs = parallel.shard_jobs(jobs, rank, world)
         if structure_key(jobs, self.f, self.precision) != self.key:
             raise ValueError("jobs do not match the plan's structure")
         slot = self.slots[self.k % self.DEPTH]

@@ -614,8 +614,9 @@ def render_jobs(jobs, f, precision="fp32", shard=None, signals=None, timing=None
     (device output, per-job offsets/lengths, update count, launches).
     `inputs_ready` (optional CUDA event): the jobs' device tensors are final
     once it completes -- lets planning overlap earlier work on the stream.
-    `shard=(rank, world)`: render the strided image subset rank::world of
-    every job (parallel.image_subset; all per-image work divides by world),
+    `shard=(rank, world)`: render the image shard of `rank` of every job
+    (parallel.image_shard: per-tier delay bands; all per-image work divides
+    by world),
     with out_len from the batch-wide track maximum (all-reduce MAX over
     the ranks, or `dmax_hook` when given) so the ranks' outputs sum to the
     full render.  Batches whose estimated device footprint exceeds
@@ -625,13 +626,8 @@ def render_jobs(jobs, f, precision="fp32", shard=None, signals=None, timing=None
         if precision == "fp64":
             raise ValueError("the exact fp64 engine runs replicas only (its summation order "
                              "spans all images)")
-        from dataclasses import replace as _replace
         from . import parallel
-        rank, world = int(shard[0]), int(shard[1])
-        jobs = [_replace(jb, image_index=parallel.image_subset(
-                    image_count(jb.max_order) if jb.image_index is None else jb.image_index,
-                    rank, world), signal_key=engine._key(jb.signal_key, jb.s),
-                    path_key=engine._key(jb.path_key, jb.pos)) for jb in jobs]
+        jobs = parallel.shard_jobs(jobs, int(shard[0]), int(shard[1]))
         if dmax_hook is None:
             dmax_hook = parallel.allreduce_max
     sig = signals if signals is not None else [jb.s for jb in jobs]

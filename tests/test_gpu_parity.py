@@ -200,7 +200,7 @@ def test_mixed_job_groups_in_one_batch():
 
 
 def test_image_shards_sum_to_full_render():
-    """Image shards (parallel.image_subset) rendered one after another on
+    """Image shards (parallel.image_shard) rendered one after another on
     this GPU: per-shard track maxima -> batch-wide maximum (the value the
     all-reduce MAX produces across ranks, fed through dmax_hook) -> every
     shard writes the full out_len and the shard outputs sum to the render
@@ -214,9 +214,7 @@ def test_image_shards_sum_to_full_render():
     full = render_jobs(jobs, f, precision="fp32")
     local = []
     for r in range(world):
-        sub = [dataclasses.replace(jb, image_index=parallel.image_subset(
-            mroom.image_count(jb.max_order), r, world)) for jb in jobs]
-        local.append(engine.Geometry(sub).dmax)
+        local.append(engine.Geometry(parallel.shard_jobs(jobs, r, world)).dmax)
     gmax = np.max(np.stack(local), axis=0)
 
     def hook(t):
@@ -305,9 +303,7 @@ def test_render_plan_image_shards():
     world = 2
     local = []
     for r in range(world):
-        sub = [dataclasses.replace(jb, image_index=parallel.image_subset(
-            mroom.image_count(jb.max_order), r, world)) for jb in jobs]
-        local.append(engine.Geometry(sub).dmax)
+        local.append(engine.Geometry(parallel.shard_jobs(jobs, r, world)).dmax)
     gmax = np.max(np.stack(local), axis=0)
 
     def hook(t):

@@ -1,9 +1,9 @@
-"""Multi-GPU partitioning logic on CPU: image_subset / lpt_assign properties
-and a world_size-2 gloo run of the image-shard path -- strided image
-subsets, the all-reduce MAX of the track maxima and the sum-reduce of the
-outputs -- with the CPU oracle rendering each rank's subset (test
-infrastructure stands in for the GPU renderer; the partition and the
-collectives are the product code)."""
+"""Multi-GPU partitioning logic on CPU: image_shard / image_subset /
+lpt_assign properties and a world_size-2 gloo run of the image-shard path
+-- per-tier delay-band shards, the all-reduce MAX of the track maxima and the
+sum-reduce of the outputs -- with the CPU oracle rendering each rank's
+shard (test infrastructure stands in for the GPU renderer; the partition
+and the collectives are the product code)."""
 
 import os
 import socket
@@ -25,6 +25,38 @@ def test_image_subsets_partition_and_balance():
             assert max(g.size for g in got) - min(g.size for g in got) <= 1
     sub = np.array([3, 5, 8, 13, 21])
     assert parallel.image_subset(sub, 1, 2).tolist() == [5, 13]
+
+
+def test_canonical_lattice_matches_enumeration():
+    """The host's structural copy of the canonical order (room.py:98-143)
+    equals the oracle enumeration (itself pinned to the reference goldens)."""
+    from oracle import oracle as orc
+    for K in (0, 1, 2, 5, 8, 20):
+        j, order = parallel.canonical_lattice(K)
+        im = orc.enumerate_images([5.0, 6.0, 4.0], 0.9, K)
+        assert np.array_equal(j, im.j.astype(np.int64)), K
+        assert np.array_equal(order, im.order.astype(np.int64)), K
+
+
+def test_image_shards_partition_balance_and_locality():
+    tiers = ((2, 1), (8, 32), (20, 256))
+    dims = np.array([20.0, 15.0, 8.0])
+    j, order = parallel.canonical_lattice(20)
+    dist = np.linalg.norm(j * dims, axis=1)
+    for world in (1, 2, 3, 8):
+        parts = [parallel.image_shard(dims, 20, tiers, r, world) for r in range(world)]
+        assert np.array_equal(np.sort(np.concatenate(parts)), np.arange(order.size))
+        for lo, hi in ((-1, 2), (2, 8), (8, 20)):  # every tier balanced
+            cnt = [int(np.sum((order[p] > lo) & (order[p] <= hi))) for p in parts]
+            assert max(cnt) - min(cnt) <= 1, (world, lo, cnt)
+        if world > 1:  # contiguous delay bands: rank r's far tier lies beyond rank r-1's
+            far = [dist[p[order[p] > 8]] for p in parts]
+            assert all(far[r].min() >= far[r - 1].max() - 1e-9 for r in range(1, world))
+    sub = np.arange(0, order.size, 3)  # restricted to a subset (t60 cull)
+    parts = [parallel.image_shard(dims, 20, tiers, r, 4, sub) for r in range(4)]
+    assert np.array_equal(np.sort(np.concatenate(parts)), sub)
+    with np.testing.assert_raises(ValueError):
+        parallel.image_shard(dims, 20, tiers, 4, 4)
 
 
 def test_lpt_assign_balances_and_covers():
@@ -60,8 +92,9 @@ def _worker(rank, world, port, outdir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    full = _scene()
-    mine = parallel.image_subset(len(full.images), rank, world)
+    from paper_2508_03065_b200 import workloads
+    sc = workloads.make_scenes("c3", duration=0.06, max_order=5, tiers=((1, 1), (3, 32), (5, 256)))[0]
+    mine = parallel.image_shard(sc.dims, sc.max_order, sc.tiers, rank, world)
     o = _scene(mine)
     dmax = torch.tensor([o.track_max()], dtype=torch.float64)
     parallel.allreduce_max(dmax)  # batch-wide maximum -> the reference's out_len
