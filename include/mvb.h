@@ -279,16 +279,18 @@ int mvb_sort_keys(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jo
 /* Fused delay sort (replaces mvb_sort_keys + an argsort + mvb_gather_images
  * when max_n_img <= MVB_DELAY_SORT_MAX): for every job j and time segment s
  * (samples [s*seg_len, (s+1)*seg_len)), d_out[(j * max_n_seg + s) *
- * max_n_img + q] = the job's image records ordered by their distance at the
- * segment centre (fp32 key, stable sort); slots q >= n_img and segments
- * past the track hold image min(q, n_img - 1) of the canonical order.
- * One block radix sort per (job, segment); locality only -- any order
- * renders the same result up to fp32 summation order. */
+ * max_n_img + q] = the job's image records ordered by their delay in whole
+ * samples (kappa * distance) at the segment centre, clamped to key_bits
+ * bits (1..32; the host passes the bit length of its delay bound), stable
+ * sort; slots q >= n_img and segments past the track hold image
+ * min(q, n_img - 1) of the canonical order.  One block radix sort per
+ * (job, segment); locality only -- any order renders the same result up to
+ * fp32 summation order. */
 #define MVB_DELAY_SORT_MAX 16384
 int mvb_delay_sort(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jobs,
                    int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
-                   const double* d_paths, const double* d_coarse, mvb_image* d_out,
-                   void* stream);
+                   const double* d_paths, const double* d_coarse, int64_t key_bits,
+                   mvb_image* d_out, void* stream);
 
 /* Fast path: fp32 branch records v'_k = x (*) c'_k (d_cbranch (M1, L) fp64
  * in the centred basis (mu - 1/2)^k, zero branches k >= M1) of n_sig dry

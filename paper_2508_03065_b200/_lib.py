@@ -44,7 +44,7 @@ _SIGS = {
     "mvb_gather_images": [P, P, I64, P, P],
     "mvb_track_coeffs": [P, P, I64, I64, P, P, P, P, P],
     "mvb_sort_keys": [P, P, I64, I64, I64, I64, P, P, P, P],
-    "mvb_delay_sort": [P, P, I64, I64, I64, I64, P, P, P, P],
+    "mvb_delay_sort": [P, P, I64, I64, I64, I64, P, P, I64, P, P],
     "mvb_branch_records_f32": [P, P, P, P, I64, I64, P, INT, INT, INT, P, P],
     "mvb_synthesize_f32": [P, P, I64, P, P, P, P, P, P, INT, INT, P],
     "mvb_reduce_partials_f32": [P, I64, I64, P, P, P],

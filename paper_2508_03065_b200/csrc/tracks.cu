@@ -77,12 +77,23 @@ __device__ __forceinline__ void seg_maxmin(const double* c, int64_t K, int64_t s
 // Coarse distances of the decimated images (the reference's distance
 // arithmetic on pos[::N]) fused with their track bounds: a warp handles
 // CB_SEGS 64-sample segments of one image (blockIdx.y = chunk), computes and
-// writes them in order, reduces each segment's max / min with shuffles and
-// keeps a sliding window of three segments (the neighbours just outside the
-// chunk are recomputed, not written), so the coarse array is written once
-// and never re-read for the bounds.  Chunk maxima merge atomically into the
-// zero-initialised lb / ub.
+// writes them in order and keeps a sliding window of three segments (the
+// neighbours just outside the chunk are recomputed, not written), so the
+// coarse array is written once and never re-read for the bounds.  The
+// window bound only has to be an upper bound, so segment max / min are
+// reduced in fp32 rounded outward (one SHFL + FMNMX per step; an fp64
+// shuffle-max costs ~20 instructions); lb, which seeds the exact maximum,
+// stays the exact fp64 coarse max (lane-local, one reduction per chunk).
+// Chunk results merge atomically into the zero-initialised lb / ub.
 constexpr int CB_SEGS = 16;
+
+__device__ __forceinline__ void warp_maxmin_f(float& M, float& m) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
+}
 
 __global__ void k_coarse_bounds(const mvb_image* __restrict__ images, const int32_t* __restrict__ sel,
                                 int64_t n_sel, const mvb_job* __restrict__ jobs,
@@ -104,36 +115,48 @@ __global__ void k_coarse_bounds(const mvb_image* __restrict__ images, const int3
     const double* mic = J.mic_moving ? src + 3 * K : paths + 3 * J.mic_off;
     const int64_t mstep = J.mic_moving ? 3 : 0;
     double* c = coarse + im.coarse;
-    auto segment = [&](int64_t s, bool write, double& M, double& m) {
-        M = -DBL_MAX;
-        m = DBL_MAX;
+    double vmax = 0.0;  // lane-local exact max of the written samples (lb)
+    // segment s: distances of its 64 samples (written when `write`), and
+    // its max / min rounded outward to fp32, warp-uniform
+    auto segment = [&](int64_t s, bool write, float& M, float& m) {
+        M = -FLT_MAX;
+        m = FLT_MAX;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int64_t k = 64 * s + 32 * h + lane;
             if (k < K) {
                 const double v = image_distance(im, src + 3 * k, mic + mstep * k);
-                if (write) c[k] = v;
-                M = fmax(M, v);
-                m = fmin(m, v);
+                if (write) {
+                    c[k] = v;
+                    vmax = v > vmax ? v : vmax;
+                }
+                M = fmaxf(M, __double2float_ru(v));
+                m = fminf(m, __double2float_rd(v));
             }
         }
-        warp_maxmin(M, m);
+        warp_maxmin_f(M, m);
     };
-    double Mp = -DBL_MAX, mp = DBL_MAX, Mc, mc, Mn, mn;
+    float Mp = -FLT_MAX, mp = FLT_MAX, Mc, mc, Mn, mn;
     if (s0 > 0) segment(s0 - 1, false, Mp, mp);
     segment(s0, true, Mc, mc);
-    double best_lb = 0.0, best_ub = 0.0;
+    float best_ub = 0.f;
+    const float ns = __double2float_ru(negsum);
     for (int64_t s = s0; s < s1; ++s) {
         if (s + 1 < nseg) segment(s + 1, s + 1 < s1, Mn, mn);
-        else { Mn = -DBL_MAX; mn = DBL_MAX; }
-        const double M = fmax(Mp, fmax(Mc, Mn)), m = fmin(mp, fmin(mc, mn));
-        best_lb = fmax(best_lb, Mc);
-        best_ub = fmax(best_ub, M + negsum * (M - m) + 1e-9);
+        else { Mn = -FLT_MAX; mn = FLT_MAX; }
+        const float M = fmaxf(Mp, fmaxf(Mc, Mn)), m = fminf(mp, fminf(mc, mn));
+        // M + negsum (M - m) + 1e-9 evaluated upward (fp32 ulp at 400 m: 3e-5 m)
+        best_ub = fmaxf(best_ub, __fadd_ru(M, __fmul_ru(ns, __fsub_ru(M, m))));
         Mp = Mc; mp = mc; Mc = Mn; mc = mn;
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double t = __shfl_xor_sync(0xffffffffu, vmax, o);
+        vmax = t > vmax ? t : vmax;
+    }
     if (lb && lane == 0) {
-        atomic_max_pos(lb + i, best_lb);
-        atomic_max_pos(ub + i, best_ub);
+        atomic_max_pos(lb + i, vmax);
+        atomic_max_pos(ub + i, (double)best_ub + 1e-9);
     }
 }
 
@@ -523,18 +546,21 @@ __global__ void k_sort_keys(const mvb_image* __restrict__ images, const mvb_job*
 }
 
 // Fused delay sort: one CTA per (segment s, job j).  Key of image i = its
-// distance at the segment centre (k_sort_keys' key) as fp32 bits (distances
-// are >= 0, so the bit patterns order like the values); a stable block radix
-// sort (deterministic); the records are gathered in that order, striped so
+// delay in whole samples at the segment centre, kappa * d (k_sort_keys'
+// distance), clamped to key_bits bits -- the host's delay bound fixes the
+// bit count, so c3's 57k-sample delays sort in 16 bits (four 4-bit radix
+// passes instead of eight for fp32 keys); a stable block radix sort
+// (deterministic); the records are gathered in that order, striped so
 // consecutive threads write consecutive 96-byte records.  Slots past the
-// job's images (padding keys sort last) and segments past its track (all
-// keys padding: identity order) repeat as before: index min(q, n - 1).
+// job's images (padding keys, all ones, sort last: stable, larger indices)
+// and segments past its track (all keys padding: identity order) hold
+// index min(q, n - 1).
 template <int BT, int IPT>
 __global__ void __launch_bounds__(BT) k_delay_sort(const mvb_image* __restrict__ images,
                                                    const mvb_job* __restrict__ jobs,
                                                    int64_t max_n_img, int64_t max_n_seg,
                                                    int64_t seg_len, const double* __restrict__ paths,
-                                                   const double* __restrict__ coarse,
+                                                   const double* __restrict__ coarse, int key_bits,
                                                    mvb_image* __restrict__ out) {
     using Sort = cub::BlockRadixSort<unsigned, BT, IPT, int>;
     extern __shared__ __align__(16) unsigned char dsort_smem[];
@@ -546,12 +572,14 @@ __global__ void __launch_bounds__(BT) k_delay_sort(const mvb_image* __restrict__
     int64_t t = s * seg_len + seg_len / 2;
     if (t > J.T - 1) t = J.T - 1;
     const mvb_image* __restrict__ im0 = images + J.img_off;
+    const unsigned kmax = key_bits >= 32 ? 0xffffffffu : (1u << key_bits) - 1u;
+    const double kappa = J.kappa;
     unsigned keys[IPT];
     int vals[IPT];
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
         const int i = threadIdx.x * IPT + k;  // blocked arrangement
-        unsigned key = 0xffffffffu;
+        unsigned key = kmax;
         if (active && i < n) {
             const mvb_image& im = im0[i];
             double d;
@@ -562,12 +590,13 @@ __global__ void __launch_bounds__(BT) k_delay_sort(const mvb_image* __restrict__
                 if (c >= im.n_coarse) c = im.n_coarse - 1;
                 d = coarse[im.coarse + c];
             }
-            key = __float_as_uint((float)d);
+            const double tau = d * kappa;
+            key = tau < (double)kmax ? (unsigned)tau : kmax;
         }
         keys[k] = key;
         vals[k] = i;
     }
-    Sort(temp).SortBlockedToStriped(keys, vals);
+    Sort(temp).SortBlockedToStriped(keys, vals, 0, key_bits);
     mvb_image* __restrict__ dst = out + (j * max_n_seg + s) * max_n_img;
     constexpr int CH = sizeof(mvb_image) / 16;
 #pragma unroll
@@ -586,8 +615,8 @@ __global__ void __launch_bounds__(BT) k_delay_sort(const mvb_image* __restrict__
 template <int BT, int IPT>
 static int launch_delay_sort(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
                              int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
-                             const double* paths, const double* coarse, mvb_image* out,
-                             cudaStream_t s) {
+                             const double* paths, const double* coarse, int key_bits,
+                             mvb_image* out, cudaStream_t s) {
     using Sort = cub::BlockRadixSort<unsigned, BT, IPT, int>;
     const size_t smem = sizeof(typename Sort::TempStorage);
     static bool attr = false;  // one opt-in per process and instantiation
@@ -597,7 +626,7 @@ static int launch_delay_sort(const mvb_image* images, const mvb_job* jobs, int64
         attr = true;
     }
     k_delay_sort<BT, IPT><<<dim3((unsigned)max_n_seg, (unsigned)n_jobs), BT, smem, s>>>(
-        images, jobs, max_n_img, max_n_seg, seg_len, paths, coarse, out);
+        images, jobs, max_n_img, max_n_seg, seg_len, paths, coarse, key_bits, out);
     return MVB_OK;
 }
 
@@ -969,30 +998,31 @@ int mvb_track_coeffs(const mvb_image* images, const int32_t* sel, int64_t n_sel,
 
 int mvb_delay_sort(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
                    int64_t max_n_img, int64_t max_n_seg, int64_t seg_len, const double* paths,
-                   const double* coarse, mvb_image* out, void* stream) {
+                   const double* coarse, int64_t key_bits, mvb_image* out, void* stream) {
     if (n_jobs < 0 || n_jobs > 65535 || max_n_img < 0 || max_n_seg < 0 ||
         max_n_seg > 0x7fffffff || seg_len < 1)
         return fail(MVB_EINVAL, "delay_sort: sizes");
     if (max_n_img > MVB_DELAY_SORT_MAX) return fail(MVB_EINVAL, "delay_sort: too many images");
+    if (key_bits < 1 || key_bits > 32) return fail(MVB_EINVAL, "delay_sort: key_bits");
     if (n_jobs == 0 || max_n_img == 0 || max_n_seg == 0) return MVB_OK;
     if (!images || !jobs || !paths || !out) return fail(MVB_EINVAL, "delay_sort: null");
     cudaStream_t s = as_stream(stream);
     int rc;
     if (max_n_img <= 1024)
         rc = launch_delay_sort<256, 4>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
-                                       coarse, out, s);
+                                       coarse, (int)key_bits, out, s);
     else if (max_n_img <= 2048)
         rc = launch_delay_sort<256, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
-                                       coarse, out, s);
+                                       coarse, (int)key_bits, out, s);
     else if (max_n_img <= 4096)
         rc = launch_delay_sort<512, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
-                                       coarse, out, s);
+                                       coarse, (int)key_bits, out, s);
     else if (max_n_img <= 8192)
         rc = launch_delay_sort<1024, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len,
-                                        paths, coarse, out, s);
+                                        paths, coarse, (int)key_bits, out, s);
     else
         rc = launch_delay_sort<1024, 16>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len,
-                                         paths, coarse, out, s);
+                                         paths, coarse, (int)key_bits, out, s);
     if (rc != MVB_OK) return rc;
     return check_launch("delay_sort");
 }

@@ -336,11 +336,13 @@ class Geometry:
         lb = torch.zeros(n_img, dtype=torch.float64, device=dev)
         ub = torch.zeros(n_img, dtype=torch.float64, device=dev)
         negsum = max([negative_mass(N) for N in self.factors if N > 1], default=0.0)
-        if self.dec_sel.numel():  # coarse distances + bounds of the decimated images
-            max_K = max(-(-int(self.T[j]) // N) for (j, N) in self.cpath)
-            _lib.call("mvb_coarse_distances", ptr(self.images), ptr(self.dec_sel),
-                      self.dec_sel.numel(), max_K, ptr(jobs_dev), ptr(self.paths), negsum,
-                      ptr(self.coarse), ptr(lb), ptr(ub), st)
+        # coarse distances + bounds of the decimated images, one launch per
+        # factor (its grid spans that factor's coarse length, no idle chunks)
+        for N, sel in self.sel_by_factor.items():
+            max_K = max(-(-int(self.T[j]) // N2) for (j, N2) in self.cpath if N2 == N)
+            _lib.call("mvb_coarse_distances", ptr(self.images), ptr(sel), sel.numel(), max_K,
+                      ptr(jobs_dev), ptr(self.paths), negsum, ptr(self.coarse), ptr(lb), ptr(ub),
+                      st)
         if self.full_sel.numel():  # bounding-box bounds of the full-rate images
             _lib.call("mvb_track_bounds", ptr(self.images), ptr(self.full_sel),
                       self.full_sel.numel(), ptr(jobs_dev), ptr(self.paths), ptr(self.bbox),
@@ -770,8 +772,13 @@ class PreparedRender:
 
 
 def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
-                   signal_keys=None) -> PreparedRender:
-    """First half of render() (see PreparedRender)."""
+                   signal_keys=None, fork=None) -> PreparedRender:
+    """First half of render() (see PreparedRender).  `fork`: two extra
+    streams (render plans, during graph capture): the delay sort and the
+    branch records then run as parallel branches next to the interval
+    records (they depend on the coarse tracks / the signal only), joined
+    before the function returns, so the captured graph's critical path is
+    the longest of the three instead of their sum."""
     dev = geom.dev
     st = stream_handle(dev)
     jobs = geom.jobs
@@ -864,14 +871,31 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     _mark("render.signals")
     cb, M1, nb = fast_bank(f)
     pre_dev = h2d(pack_jobs(base_rows), dev)
-    coef = _interval_records(geom, pre_dev, st)
-    _mark("render.coeffs_keys")
-    images_sorted, n_seg, max_seg, max_img = _delay_sort(geom, pre_dev, st)
-    _mark("render.sorted")
     out_len, tau_bound, offsets, rows = finish_rows()
+    concat = sig_all if host_sigs and len(host_sigs) == len(uniq) else None
+    main = torch.cuda.current_stream(dev)
+    if fork is not None:
+        forked = torch.cuda.Event()
+        forked.record(main)
+        for fs in fork:
+            fs.wait_event(forked)
+        with torch.cuda.stream(fork[0]):
+            images_sorted, n_seg, max_seg, max_img = _delay_sort(geom, pre_dev,
+                                                                 stream_handle(dev))
+        with torch.cuda.stream(fork[1]):
+            rec, rec_start = _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev,
+                                             stream_handle(dev), concat)
+        coef = _interval_records(geom, pre_dev, st)
+        for fs in fork:
+            main.wait_stream(fs)
+    else:
+        coef = _interval_records(geom, pre_dev, st)
+        _mark("render.coeffs_keys")
+        images_sorted, n_seg, max_seg, max_img = _delay_sort(geom, pre_dev, st)
+        _mark("render.sorted")
+        rec, rec_start = _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev, st,
+                                         concat)
     _mark("render.plan_lengths")
-    rec, rec_start = _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev, st,
-                                     sig_all if host_sigs and len(host_sigs) == len(uniq) else None)
     for j in range(nJ):
         rows[j].update(rec_base=rec_start[keys[j]], nb=nb, img_off=j * max_seg * max_img,
                        img_stride=max_img)
@@ -924,8 +948,9 @@ def _delay_sort(geom, pre_dev, st):
     if max_img <= _lib.DELAY_SORT_MAX:  # fused keys + block radix sort + gather, one launch
         images_sorted = torch.empty(nJ * max_seg * max_img, IMG_COLS, dtype=torch.int64,
                                     device=dev)
+        key_bits = max(1, min(32, max(int(geom.length_bound(j)) for j in range(nJ)).bit_length()))
         _lib.call("mvb_delay_sort", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg, SEG_LEN,
-                  ptr(geom.paths), ptr(geom.coarse), ptr(images_sorted), st)
+                  ptr(geom.paths), ptr(geom.coarse), key_bits, ptr(images_sorted), st)
         return images_sorted, n_seg, max_seg, max_img
     key = torch.full((nJ, max_seg, max_img), float("inf"), dtype=torch.float64, device=dev)
     _lib.call("mvb_sort_keys", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg, SEG_LEN,

@@ -69,8 +69,8 @@ def canonical_lattice(max_order: int) -> tuple:
 def image_shard(dims, max_order: int, tiers, rank: int, world: int, images=None) -> np.ndarray:
     """Canonical image positions owned by `rank` (sorted): every tier of
     `tiers` ((max_order, N), ...) ordered by |j * dims| (ties by canonical
-    position) and cut into `world` contiguous bands of near-equal count;
-    band `rank` of every tier.  `images`: restrict to these canonical
+    position) and cut into `world` contiguous bands of equal estimated cost
+    (_band_cuts); band `rank` of every tier.  `images`: restrict to these canonical
     positions (e.g. a t60 cull).  The shards of ranks 0..world-1 partition
     the image list."""
     if world < 1 or not 0 <= rank < world:
@@ -96,11 +96,34 @@ def _image_shard(key) -> np.ndarray:
         sel = np.nonzero((order[idx] > prev) & (order[idx] <= int(mo)))[0]
         prev = int(mo)
         band = sel[np.lexsort((idx[sel], key[sel]))]  # by distance, then canonical position
-        lo, hi = (band.size * rank) // world, (band.size * (rank + 1)) // world
-        mine.append(idx[band[lo:hi]])
+        cut = _band_cuts(key[band], world)
+        mine.append(idx[band[cut[rank]:cut[rank + 1]]])
     out = np.sort(np.concatenate(mine)) if mine else np.zeros(0, np.int64)
     out.flags.writeable = False  # cached: shared by every caller
     return out
+
+
+SPARSITY_COST = 0.75  # extra synthesis cost of an image ~ SPARSITY_COST / local density (per m)
+
+
+def _band_cuts(keys: np.ndarray, world: int) -> np.ndarray:
+    """Cut positions of `world` contiguous bands of the sorted distances
+    `keys` at equal estimated synthesis cost: an image costs
+    1 + SPARSITY_COST / rho, rho its local density (images per metre over
+    +-16 neighbours) -- sparse delay bands (the far tips of the order
+    octahedron) reuse fewer L1 lines per gather, measured +9% at 8 images/m
+    against ~+1.5% at 60 (c3, W=8)."""
+    n = keys.size
+    if n == 0:
+        return np.zeros(world + 1, np.int64)
+    p = np.arange(n)
+    lo, hi = np.maximum(p - 16, 0), np.minimum(p + 16, n - 1)
+    span = np.maximum(keys[hi] - keys[lo], 1e-9)
+    w = 1.0 + SPARSITY_COST * span / np.maximum(hi - lo, 1)
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    cut = np.searchsorted(cum, cum[-1] * np.arange(world + 1) / world, side="left")
+    cut[0], cut[-1] = 0, n
+    return np.maximum.accumulate(np.clip(cut, 0, n)).astype(np.int64)
 
 
 def shard_jobs(jobs, rank: int, world: int) -> list:

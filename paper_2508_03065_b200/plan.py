@@ -85,6 +85,18 @@ def plan_streams(dev) -> tuple:
     return _STREAMS[key]
 
 
+_FORK: dict = {}
+
+
+def fork_streams(dev) -> list:
+    """Two capture-only streams for the parallel branches of a geometry
+    graph (the captured graph records the fork / join, not the streams)."""
+    key = str(dev)
+    if key not in _FORK:
+        _FORK[key] = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+    return _FORK[key]
+
+
 class _Slot:
     def __init__(self):
         self.graph = None
@@ -120,6 +132,7 @@ class RenderPlan:
         self.dmax_hook = dmax_hook
         self.dev = require_cuda(device)
         self.geo_stream, self.syn_stream = plan_streams(self.dev)
+        self.fork_streams = fork_streams(self.dev)
         self.f = as_filter(f)
         self.precision = precision
         self.template = list(jobs)
@@ -176,14 +189,15 @@ class RenderPlan:
 
     SLACK = 0.1  # output capacity headroom of a capture (fraction of the length bound)
 
-    def _prepare(self, slot, geom):
-        """Geometry and the render's first half (see engine.PreparedRender)."""
+    def _prepare(self, slot, geom, fork=None):
+        """Geometry and the render's first half (see engine.PreparedRender);
+        `fork`: parallel graph branches for the sort and branch records."""
         geom.length_slack = self.SLACK
         geom.finish()
         return engine.prepare_render(geom, [sj.s for sj in slot.jobs], self.f,
                                      precision=self.precision,
                                      signal_keys=[engine._key(sj.signal_key, sj.s)
-                                                  for sj in slot.jobs])
+                                                  for sj in slot.jobs], fork=fork)
 
     def _collect(self, slot):
         """Record the synthesis time of the slot's finished replay."""
@@ -223,7 +237,7 @@ class RenderPlan:
         slot.timing = []
         launches0 = _lib.launch_count()
         with uploads, torch.cuda.graph(g_geo, stream=self.geo_stream):
-            prep = self._prepare(slot, geom)
+            prep = self._prepare(slot, geom, fork=self.fork_streams)
         with uploads, torch.cuda.graph(g_syn, stream=self.syn_stream):
             res = prep.launch(slot.timing)
         slot.graphs = [g_geo, g_syn]
