@@ -29,6 +29,8 @@
 // (rate*d)/c, gain, floor split, Horner in mu -- and its summation order:
 // 32-image blocks in canonical order, then the pairwise block tree
 // (synth.py:182-191) evaluated with an equivalent merge stack.
+#include <cfloat>
+
 #include "mvb_common.cuh"
 
 namespace mvb {
@@ -298,6 +300,16 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     for (int u = 0; u < U; ++u) acc[u] = 0.f;
     const bool inside = n0 + TN <= T;  // no hold-extension inside this tile
     const bool tail = n0 >= T;         // wholly hold-extended: one delay per image
+    // Exact zeros: an image contributes nothing to this tile when every
+    // gather row lies in the zero pads of the branch records, i.e. outside
+    // the signal rows [rb, rb + ls) -- before its first sample arrives (delay
+    // beyond the tile) or after the signal ended.  Skipping it is
+    // bit-identical (the Horner of zero rows adds 0).  Tail tiles test the
+    // held delay exactly; `front` tiles (n0 below the largest possible
+    // delay, ~10% of c3's tiles) bound a decimated image's delay from its
+    // staged interval records.  c3: ~10% of all updates are such zeros.
+    const int ls = (int)Jp->ls;
+    const bool front = n0 + TN <= (int)(Jp->out_len - Jp->ls) + 2;
 
     // prologue of the staging pipeline: structs of the first two images, then
     // the first image's records
@@ -355,6 +367,8 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
                 row0 = rb + n0 + lane + Lsh + MAGIC_I - __float_as_int(c0.x) - __float_as_int(v);
                 A = an * rcp_approx(fmaxf(fmaf(res, invk, c0.z), dmin));
             }
+            const int rfirst = row0 - lane;  // row of the tile's first sample (warp-uniform)
+            if (rfirst + TN <= rb || rfirst >= rb + ls) continue;  // all in the zero pads
 #pragma unroll
             for (int u = 0; u < U; ++u) acc[u] += A * gather_horner<NP>(R, (unsigned)(row0 + 32 * u), mc);
             continue;
@@ -391,6 +405,21 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
         const int nl = rb + n0 + lane + Lsh + MAGIC_I;
         const float4* __restrict__ cs = reinterpret_cast<const float4*>(st.rec[rcur]);
         if (inside && (N == 32 || N == 64 || N == 128 || N == 256)) {
+            if (front) {
+                // delay lower bound over the tile from its TN/N staged records:
+                // D = B + rint(f + res), |res| <= sum |kappa g_p| (|u| <= 1)
+                float lo = FLT_MAX;
+                if (lane < TN / N) {
+                    const float4* c = cs + 3 * lane;
+                    const float4 a = c[0], b = c[1], d = c[2];
+                    const float S = fabsf(b.x) + fabsf(b.y) + fabsf(b.z) + fabsf(b.w) + fabsf(d.x) +
+                                    fabsf(d.y) + fabsf(d.z) + fabsf(d.w);
+                    lo = (float)__float_as_int(a.x) + a.y - S - 1.0f;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+                if (lo > (float)(n0 + TN + Lsh)) continue;  // every row before the signal
+            }
             // staged records: slot j = interval n0/N + j
             switch (N) {
                 case 32: dec_static<U, NP, 32>(acc, cs, R, lane, nl, an, invk, dmin); break;
