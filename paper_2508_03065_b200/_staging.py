@@ -11,6 +11,7 @@ d2h            device -> numpy through persistent pinned staging
 from __future__ import annotations
 
 import os
+import warnings
 
 import numpy as np
 import torch
@@ -58,6 +59,44 @@ def parallel_copy(pairs, chunk_bytes: int = 4 << 20) -> None:
         fut.result()
 
 
+def _host_tensor(a: np.ndarray) -> torch.Tensor:
+    """torch view of a (possibly read-only) host array used only as a copy
+    source; torch's warning about non-writable arrays does not apply."""
+    with warnings.catch_warnings():
+        warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
+        return torch.from_numpy(a)
+
+
+def is_pinned(a) -> bool:
+    """True for a C-contiguous numpy array in page-locked host memory (e.g.
+    a view of a pinned torch tensor, or a Trajectory's positions): such
+    parts are sent by DMA straight from the caller's buffer."""
+    if not isinstance(a, np.ndarray) or not a.flags.c_contiguous or a.nbytes == 0:
+        return False
+    try:
+        return bool(_host_tensor(a).is_pinned())
+    except (TypeError, RuntimeError, ValueError):
+        return False
+
+
+def pinned_copy(a: np.ndarray) -> np.ndarray:
+    """A read-only copy of `a` in page-locked host memory (pinned torch
+    storage kept alive by the returned array), or a plain copy without a
+    GPU -- for inputs uploaded many times (trajectories)."""
+    a = np.ascontiguousarray(a)
+    if not torch.cuda.is_available():
+        out = a.copy()
+    else:
+        t = torch.empty(a.shape, dtype=_TORCH.get(a.dtype.str[1:], torch.uint8), pin_memory=True)
+        out = t.numpy() if a.dtype.str[1:] in _TORCH else t.numpy().view(a.dtype)
+        np.copyto(out, a)
+    out.flags.writeable = False
+    return out
+
+
+_TORCH = {"f8": torch.float64, "f4": torch.float32, "i8": torch.int64, "i4": torch.int32}
+
+
 class _BulkStager:
     """Persistent pinned slabs for bulk uploads (paths, signals): parts are
     copied straight into a slab (parallel_copy) and sent with ONE
@@ -89,6 +128,17 @@ class _BulkStager:
         if not parts:
             return
         np_dt = torch.empty((), dtype=out.dtype).numpy().dtype
+        direct = [(r0, p) for r0, p in parts
+                  if isinstance(p, np.ndarray) and p.dtype == np_dt and is_pinned(p)]
+        if direct:  # page-locked caller buffers: DMA straight from them
+            for r0, p in direct:
+                n = p.shape[0] if p.ndim else 1
+                out[r0:r0 + n].copy_(_host_tensor(p).reshape((n,) + tuple(out.shape[1:])),
+                                     non_blocking=True)
+            ids = {id(p) for _, p in direct}
+            parts = [(r0, p) for r0, p in parts if id(p) not in ids]
+            if not parts:
+                return
         row_elems = int(np.prod(out.shape[1:])) if out.dim() > 1 else 1
         rows = max(r0 + (p.shape[0] if np.ndim(p) else 1) for r0, p in parts)
         nbytes = rows * row_elems * np_dt.itemsize

@@ -27,6 +27,7 @@ from ._dev import h2d, ptr, readback, require_cuda, stream_handle, to_dev
 UPSAMPLE_HALFWIDTH = 32
 UPSAMPLE_KAISER_BETA = 7.857
 FIT_DEGREE = 8
+PIN_BYTES = 1 << 20  # Trajectory positions at least this large live in pinned host memory
 
 
 @dataclass(frozen=True)
@@ -44,7 +45,13 @@ class Trajectory:
             raise ValueError("positions must be a (T, 3) array with T >= 1")
         if not np.all(np.isfinite(p)):
             raise ValueError("positions must be finite")
-        p = p.copy()
+        if p.nbytes >= PIN_BYTES:
+            # large paths are kept page-locked: every render sends them by
+            # DMA straight from this copy (no staging memcpy per render)
+            from ._staging import pinned_copy
+            p = pinned_copy(p)
+        else:
+            p = p.copy()
         p.flags.writeable = False
         object.__setattr__(self, "positions", p)
         object.__setattr__(self, "rate", float(self.rate))
