@@ -49,7 +49,7 @@ from ._dev import h2d, pinned_scratch, ptr, require_cuda, stream_handle
 from ._staging import _ARENA, _STAGER, d2h, parallel_copy, side_stream  # noqa: F401
 from .farrow import as_filter, centered_branches
 from .room import image_table
-from .trajectory import (bandwidth_batch, device_constants, lowpass_batch, negative_mass,
+from .trajectory import (bandwidth_batch_async, device_constants, lowpass_batch, negative_mass,
                          phase_fit)
 
 _TRACE = [] if os.environ.get("MVB_TRACE_HOST") else None
@@ -182,7 +182,7 @@ class Geometry:
     """Device-side hierarchical tracks of a batch of jobs (prepare stage)."""
 
     def __init__(self, jobs: list, device=None, inputs_ready=None, dmax_hook=None,
-                 paths=None, defer=False):
+                 paths=None, defer=False, wait=True):
         """`inputs_ready`: optional CUDA event after which every device
         tensor of `jobs` is final.  With it, the paths are staged and their
         bandwidths measured on a side stream that waits only for that event,
@@ -192,7 +192,11 @@ class Geometry:
         track maxima before it is read (image shards: all-reduce MAX).
         `paths`: a caller-owned fp64 (rows, 3) buffer to stage the paths
         into (render plans); `defer`: stop after the staging (bounding boxes,
-        decimation decision) -- finish() does the device work."""
+        decimation decision) -- finish() does the device work.  `wait=False`
+        (with defer): enqueue the staging and its two readbacks but do not
+        wait for them -- `paths_ready` (an event after the path upload) lets
+        device work that needs only the paths start at once, collect() waits
+        for the boxes and the decision (render plans replay speculatively)."""
         if not jobs:
             raise ValueError("no jobs")
         self.dev = require_cuda(device)
@@ -203,11 +207,23 @@ class Geometry:
         host_parts, dev_parts, rows = self._layout_paths()
         self.rows = rows
         _mark("geom.setup")
-        self.path_groups, self.bws = self._stage_paths(host_parts, dev_parts, rows, inputs_ready,
-                                                       paths)
+        self._pending = self._stage_paths(host_parts, dev_parts, rows, inputs_ready, paths)
+        if wait or not defer:
+            self.collect()
         _mark("geom.bandwidth")
         if not defer:
             self.finish(dmax_hook)
+
+    def collect(self):
+        """Wait for the staging readbacks (path boxes, bandwidth indices)."""
+        if self._pending is not None:
+            box_ready, box_host, path_groups, finishers = self._pending
+            self.bws = [fin() for fin in finishers]
+            box_ready.synchronize()
+            self.bbox_host = box_host.numpy().copy()
+            self.path_groups = path_groups
+            self._pending = None
+        return self
 
     def finish(self, dmax_hook=None):
         """Device work after the staging: coarse paths, image records, coarse
@@ -308,13 +324,12 @@ class Geometry:
             box_host.copy_(self.bbox[:nJ * 12].view(nJ, 12), non_blocking=True)
             box_ready = torch.cuda.Event()
             box_ready.record()
-            path_groups, bws = self._path_bandwidths(main)
-        box_ready.synchronize()
-        self.bbox_host = box_host.numpy().copy()
+            self.paths_ready = box_ready  # the paths' full-rate rows are on the device
+            path_groups, finishers = self._path_bandwidths(main)
         if side is not main:
             main.wait_stream(side)
             self.bbox.record_stream(main)
-        return path_groups, bws
+        return box_ready, box_host, path_groups, finishers
 
     def _tracks(self, dmax_hook):
         """Job table, coarse tracks and their bounds, the exact track maximum
@@ -378,8 +393,9 @@ class Geometry:
     # ------------------------------------------------------------------------
     def _path_bandwidths(self, consumer):
         """Paths that need decimation, grouped by (length, rate), and their
-        measured bandwidths (trajectory.py:316-339) on the host: one batched
-        FFT per group, one small device->host copy per group (the waits)."""
+        measured bandwidths (trajectory.py:316-339): one batched FFT per
+        group and one small device->host copy per group, returned as
+        functions that wait for them (collect())."""
         jobs = self.jobs
         groups = {}  # (T, rate) -> {row0: position}
         uses = {}  # (T, rate, N) -> list of (position, destination row)
@@ -403,7 +419,7 @@ class Geometry:
                 x = torch.stack([self.paths[r0:r0 + T] for r0 in starts])  # (G, T, 3)
                 x.record_stream(consumer)  # read again by the decimation
             out.append((T, rate, x, uses))
-            bws.append(bandwidth_batch(x, rate))
+            bws.append(bandwidth_batch_async(x, rate, slot=f"bandwidth_index{len(bws)}"))
         return out, bws
 
     def _decimate_paths(self, path_groups, bws):

@@ -156,6 +156,7 @@ class RenderPlan:
             self.slots.append(slot)
         self.k = 0
         self.captures = 0
+        self.misses = 0  # speculative replays redone after a decision / capacity change
         self.kernel_ms = {}  # run index -> synthesis kernel time of that replay
 
     # ------------------------------------------------------------------
@@ -175,9 +176,10 @@ class RenderPlan:
                         np.asarray(src).reshape(-1)
                     _STAGER.upload([(0, a)], dst)
 
-    def _stage(self, slot, ready):
+    def _stage(self, slot, ready, wait=True):
         """Stage the slot's static inputs into its static paths buffer: on the
-        side stream after `ready` (pipelined), or on the current stream."""
+        side stream after `ready` (pipelined), or on the current stream.
+        `wait=False`: leave the readbacks pending (Geometry.collect())."""
         if slot.paths is None:  # first staging allocates the slot's paths buffer
             if ready is not None:
                 torch.cuda.current_stream(self.dev).wait_event(ready)
@@ -185,7 +187,7 @@ class RenderPlan:
             slot.paths = geom.paths
             return geom
         return engine.Geometry(slot.jobs, device=self.dev, inputs_ready=ready, paths=slot.paths,
-                               defer=True)
+                               defer=True, wait=wait)
 
     SLACK = 0.1  # output capacity headroom of a capture (fraction of the length bound)
 
@@ -249,6 +251,22 @@ class RenderPlan:
         slot.capacity = np.asarray([geom.length_bound(j) for j in range(len(slot.jobs))])  # slacked
         self.captures += 1
 
+    def _replay(self, slot, after):
+        """Replay the slot's graphs on the plan streams after event `after`."""
+        geo, syn = self.geo_stream, self.syn_stream
+        geo.wait_event(after)
+        with torch.cuda.stream(geo):
+            slot.graphs[0].replay()
+            if self.dmax_hook is not None:
+                self.dmax_hook(slot.dmax)
+            geo_done = torch.cuda.Event()
+            geo_done.record()
+        syn.wait_event(geo_done)
+        with torch.cuda.stream(syn):
+            slot.graphs[1].replay()
+            slot.done = torch.cuda.Event()
+            slot.done.record()
+
     def run(self, jobs) -> engine.RenderResult:
         """Render `jobs` (same structure as the plan's template)."""
         if self.shard is not None and int(self.shard[1]) > 1:
@@ -272,30 +290,29 @@ class RenderPlan:
             ready = torch.cuda.Event()
             ready.record()
         staged0 = _lib.launch_count()
-        geom = self._stage(slot, ready)
+        # speculative replay: a captured slot is valid while the low-pass
+        # decision and the output capacities hold; replay as soon as the
+        # paths are on the device, check the staging readbacks meanwhile,
+        # and re-capture + replay only if they changed
+        spec = slot.graph is not None
+        geom = self._stage(slot, ready, wait=not spec)
         staged = _lib.launch_count() - staged0  # staging kernels (outside the graphs)
+        if spec:
+            self._replay(slot, geom.paths_ready)
+            geom.collect()
         bound = np.asarray([geom.length_bound(j) for j in range(len(slot.jobs))])
-        if slot.graph is None or geom.lowpass_decision() != slot.decision \
+        if not spec or geom.lowpass_decision() != slot.decision \
                 or np.any(bound > slot.capacity):
+            if spec:
+                self.misses += 1
+                slot.done.synchronize()  # the speculative replay writes the slot's paths too
             cur.wait_stream(side)
             self._capture(slot, geom)
-        staged_ev = torch.cuda.Event()
-        staged_ev.record(cur)  # _stage ordered the current stream after the staging
-        geo, syn = self.geo_stream, self.syn_stream
-        geo.wait_event(staged_ev)
-        with torch.cuda.stream(geo):
-            slot.graphs[0].replay()
-            if self.dmax_hook is not None:
-                self.dmax_hook(slot.dmax)
-            geo_done = torch.cuda.Event()
-            geo_done.record()
-        syn.wait_event(geo_done)
-        with torch.cuda.stream(syn):
-            slot.graphs[1].replay()
-            slot.done = torch.cuda.Event()
-            slot.done.record()
+            staged_ev = torch.cuda.Event()
+            staged_ev.record(cur)  # _stage ordered the current stream after the staging
+            self._replay(slot, staged_ev)
         slot.run_index = self.k - 1
         r = slot.result
         return engine.RenderResult(r.out, r.offsets, r.capacity, r.n_images,
                                    staged + slot.graph_launches, *r._dev, done=slot.done,
-                                   stream=syn)
+                                   stream=self.syn_stream)

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._dev import h2d, ptr, readback, require_cuda, stream_handle, to_dev
+from ._dev import h2d, pinned_scratch, ptr, require_cuda, stream_handle, to_dev
 
 UPSAMPLE_HALFWIDTH = 32
 UPSAMPLE_KAISER_BETA = 7.857
@@ -120,6 +120,15 @@ def device_constants(factor: int, device) -> dict:
 
 
 def bandwidth_batch(x: torch.Tensor, rate: float, energy_fraction: float = 0.99) -> np.ndarray:
+    return bandwidth_batch_async(x, rate, energy_fraction)()
+
+
+def bandwidth_batch_async(x: torch.Tensor, rate: float, energy_fraction: float = 0.99,
+                          slot: str = "bandwidth_index"):
+    """bandwidth_batch, split: enqueues the kernels and the readback, returns
+    a function that waits for the readback and returns the bandwidths (the
+    caller may enqueue more device work before calling it).  `slot` names
+    the pinned readback buffer (one pending readback per name)."""
     """Per-path smallest frequency holding `energy_fraction` of the
     mean-removed displacement power, max over axes (reference
     trajectory.py:316-339), for x (G, T, 3) on the device -> host (G,).
@@ -129,7 +138,7 @@ def bandwidth_batch(x: torch.Tensor, rate: float, energy_fraction: float = 0.99)
     Frequencies follow numpy.fft.rfftfreq: k * (1 / (T * (1 / rate)))."""
     G, T, _ = x.shape
     if T < 2 or G == 0:
-        return np.zeros(G)
+        return lambda: np.zeros(G)
     x = x.contiguous()
     st = stream_handle(x.device)
     scratch = torch.empty(3 * G * 64, dtype=torch.float64, device=x.device)
@@ -142,9 +151,17 @@ def bandwidth_batch(x: torch.Tensor, rate: float, energy_fraction: float = 0.99)
     k = torch.empty(G * 3, dtype=torch.int64, device=x.device)
     _lib.call("mvb_spectrum_index", ptr(spec), G, F, float(energy_fraction), ptr(scratch), ptr(k),
               st)
-    kh = readback(k, "bandwidth_index").reshape(G, 3)
-    hz = np.minimum(kh, F - 1) * (1.0 / (T * (1.0 / rate)))
-    return np.where(kh < 0, 0.0, hz).max(axis=1)
+    host = pinned_scratch(slot, k.numel(), k.dtype)
+    host.copy_(k, non_blocking=True)
+    done = torch.cuda.Event()
+    done.record()
+
+    def finish():
+        done.synchronize()
+        kh = host.numpy().copy().reshape(G, 3)
+        hz = np.minimum(kh, F - 1) * (1.0 / (T * (1.0 / rate)))
+        return np.where(kh < 0, 0.0, hz).max(axis=1)
+    return finish
 
 
 def bandwidth_estimate(traj: Trajectory, energy_fraction: float = 0.99) -> float:
