@@ -277,7 +277,8 @@ def test_render_plan_replays_match_direct_renders():
     jb = [dataclasses.replace(j, pos=far) for j in jobs]
     got = plan.run(jb)
     ref = render_jobs(jb, f)
-    assert plan.captures == 3 and np.array_equal(got.lengths, ref.lengths)
+    # the slot replayed speculatively, the readbacks showed the overflow: one miss
+    assert plan.captures == 3 and plan.misses == 1 and np.array_equal(got.lengths, ref.lengths)
     assert torch.equal(got.job(0), ref.job(0))
     with pytest.raises(ValueError):
         plan.run(jobs[:1])
