@@ -182,7 +182,7 @@ class Geometry:
     """Device-side hierarchical tracks of a batch of jobs (prepare stage)."""
 
     def __init__(self, jobs: list, device=None, inputs_ready=None, dmax_hook=None,
-                 paths=None, defer=False, wait=True):
+                 paths=None, defer=False, wait=True, bbox=None):
         """`inputs_ready`: optional CUDA event after which every device
         tensor of `jobs` is final.  With it, the paths are staged and their
         bandwidths measured on a side stream that waits only for that event,
@@ -191,7 +191,9 @@ class Geometry:
         optional callable applied in place to the device tensor of per-job
         track maxima before it is read (image shards: all-reduce MAX).
         `paths`: a caller-owned fp64 (rows, 3) buffer to stage the paths
-        into (render plans); `defer`: stop after the staging (bounding boxes,
+        into (render plans), `bbox` likewise for the path bounding boxes
+        (a plan's graphs read both at every replay); `defer`: stop after the
+        staging (bounding boxes,
         decimation decision) -- finish() does the device work.  `wait=False`
         (with defer): enqueue the staging and its two readbacks but do not
         wait for them -- `paths_ready` (an event after the path upload) lets
@@ -207,7 +209,7 @@ class Geometry:
         host_parts, dev_parts, rows = self._layout_paths()
         self.rows = rows
         _mark("geom.setup")
-        self._pending = self._stage_paths(host_parts, dev_parts, rows, inputs_ready, paths)
+        self._pending = self._stage_paths(host_parts, dev_parts, rows, inputs_ready, paths, bbox)
         if wait or not defer:
             self.collect()
         _mark("geom.bandwidth")
@@ -225,14 +227,17 @@ class Geometry:
             self._pending = None
         return self
 
-    def finish(self, dmax_hook=None):
+    def finish(self, dmax_hook=None, fork=None):
         """Device work after the staging: coarse paths, image records, coarse
-        tracks, bounds and the exact track maxima (no host waits)."""
+        tracks, bounds and the exact track maxima (no host waits).  `fork`
+        (a stream, render-plan capture only): the exact-maximum chain runs
+        there, parallel to what the caller enqueues next (only the exact
+        output lengths need it); `join()` merges it back."""
         self._decimate_paths(self.path_groups, self.bws)
         _mark("geom.decimate")
         self._build_images()
         _mark("geom.images")
-        self._tracks(dmax_hook)
+        self._tracks(dmax_hook, fork)
         _mark("geom.tracks")
         self.eval_count = [int(self.evals[j]) for j in range(len(self.jobs))]
 
@@ -288,7 +293,7 @@ class Geometry:
                     row += -(-int(self.T[j]) // N) * (1 + int(self.moving[j]))
         return host_parts, dev_parts, max(row, 1)
 
-    def _stage_paths(self, host_parts, dev_parts, rows, inputs_ready, paths=None):
+    def _stage_paths(self, host_parts, dev_parts, rows, inputs_ready, paths=None, bbox=None):
         """Fill the full-rate rows of the paths buffer, compute every job's
         path bounding boxes and the paths' bandwidths; the two small
         readbacks (boxes, bandwidth indices) are the host's only waits.
@@ -317,7 +322,10 @@ class Geometry:
                 self.paths[r0:r0 + p.shape[0]].copy_(p)
             box_rows = h2d(np.stack([self.pos_off, self.T, self.mic_off, self.moving], axis=1), dev)
             # flat: the nJ x 12 boxes first, then the 64 partial boxes per job
-            self.bbox = torch.empty(nJ * 65 * 12, dtype=torch.float64, device=dev)
+            if bbox is not None and bbox.numel() >= nJ * 65 * 12:
+                self.bbox = bbox
+            else:
+                self.bbox = torch.empty(nJ * 65 * 12, dtype=torch.float64, device=dev)
             _lib.call("mvb_path_bbox", ptr(box_rows), nJ, ptr(self.paths), ptr(self.bbox),
                       stream_handle(dev))
             box_host = pinned_scratch("bbox", nJ * 12, torch.float64).view(nJ, 12)
@@ -331,7 +339,13 @@ class Geometry:
             self.bbox.record_stream(main)
         return box_ready, box_host, path_groups, finishers
 
-    def _tracks(self, dmax_hook):
+    def join(self) -> None:
+        """Order the current stream after the forked exact-maximum chain."""
+        if getattr(self, "_fork", None) is not None:
+            torch.cuda.current_stream(self.dev).wait_stream(self._fork)
+            self._fork = None
+
+    def _tracks(self, dmax_hook, fork=None):
         """Job table, coarse tracks and their bounds, the exact track maximum
         of every job (kept on the device; `dmax_hook` may reduce it across
         ranks in place)."""
@@ -345,7 +359,9 @@ class Geometry:
                 T=int(self.T[j]), mic_moving=int(self.moving[j]), L=0, d0=0, n_chunks=1, nb=0,
                 rate=float(jb.rate), c=float(jb.c), d_min=float(jb.d_min),
                 kappa=float(jb.rate) / float(jb.c)))
-        jobs_dev = h2d(pack_jobs(self.job_rows), dev)
+        # kept: the exact-maximum branch (a parallel graph branch in plan
+        # captures) still reads it after this function returns
+        jobs_dev = self._jobs_dev = h2d(pack_jobs(self.job_rows), dev)
         n_img = self.n_images
         self.coarse = torch.empty(max(self.n_coarse_total, 1), dtype=torch.float64, device=dev)
         lb = torch.zeros(n_img, dtype=torch.float64, device=dev)
@@ -358,15 +374,22 @@ class Geometry:
             _lib.call("mvb_coarse_distances", ptr(self.images), ptr(sel), sel.numel(), max_K,
                       ptr(jobs_dev), ptr(self.paths), negsum, ptr(self.coarse), ptr(lb), ptr(ub),
                       st)
-        if self.full_sel.numel():  # bounding-box bounds of the full-rate images
-            _lib.call("mvb_track_bounds", ptr(self.images), ptr(self.full_sel),
-                      self.full_sel.numel(), ptr(jobs_dev), ptr(self.paths), ptr(self.bbox),
-                      ptr(lb), ptr(ub), st)
-        scratch = torch.empty(_lib.EXACT_LIST_WORDS + n_img + nJ, dtype=torch.int32, device=dev)
-        dmax = torch.empty(nJ, dtype=torch.float64, device=dev)
-        _lib.call("mvb_track_max", ptr(self.images), ptr(jobs_dev), nJ,
-                  ptr(self.coarse) if self.dec_sel.numel() else ptr(None), ptr(self.tables),
-                  ptr(self.paths), negsum, ptr(lb), ptr(ub), ptr(scratch), ptr(dmax), st)
+        self._fork = None
+        if fork is not None:  # exact-maximum chain as a parallel branch
+            fork.wait_stream(torch.cuda.current_stream(dev))
+            self._fork = fork
+        with torch.cuda.stream(fork if fork is not None else torch.cuda.current_stream(dev)):
+            st = stream_handle(dev)
+            if self.full_sel.numel():  # bounding-box bounds of the full-rate images
+                _lib.call("mvb_track_bounds", ptr(self.images), ptr(self.full_sel),
+                          self.full_sel.numel(), ptr(jobs_dev), ptr(self.paths), ptr(self.bbox),
+                          ptr(lb), ptr(ub), st)
+            scratch = torch.empty(_lib.EXACT_LIST_WORDS + n_img + nJ, dtype=torch.int32,
+                                  device=dev)
+            dmax = torch.empty(nJ, dtype=torch.float64, device=dev)
+            _lib.call("mvb_track_max", ptr(self.images), ptr(jobs_dev), nJ,
+                      ptr(self.coarse) if self.dec_sel.numel() else ptr(None), ptr(self.tables),
+                      ptr(self.paths), negsum, ptr(lb), ptr(ub), ptr(scratch), ptr(dmax), st)
         if dmax_hook is not None:
             dmax_hook(dmax)
         self.dmax_dev = dmax
@@ -849,6 +872,7 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         return out_len, tau_bound, offsets, rows
 
     def finalize(jobs_dev, st):
+        geom.join()  # the exact maxima (a parallel branch in plan captures)
         lengths = torch.empty(nJ, dtype=torch.int64, device=dev)
         err = torch.zeros(1, dtype=torch.int32, device=dev)
         _lib.call("mvb_finalize_lengths", ptr(jobs_dev), nJ, ptr(geom.dmax_dev), ptr(lengths),
@@ -893,7 +917,7 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     if fork is not None:
         forked = torch.cuda.Event()
         forked.record(main)
-        for fs in fork:
+        for fs in fork:  # every branch stream joins the capture (unused ones too)
             fs.wait_event(forked)
         with torch.cuda.stream(fork[0]):
             images_sorted, n_seg, max_seg, max_img = _delay_sort(geom, pre_dev,
@@ -901,7 +925,7 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         with torch.cuda.stream(fork[1]):
             rec, rec_start = _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev,
                                              stream_handle(dev), concat)
-        coef = _interval_records(geom, pre_dev, st)
+        coef = _interval_records(geom, pre_dev, st, fork=fork[2:])
         for fs in fork:
             main.wait_stream(fs)
     else:
@@ -939,15 +963,24 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     return PreparedRender(launch32, launches0)
 
 
-def _interval_records(geom, pre_dev, st) -> torch.Tensor:
+def _interval_records(geom, pre_dev, st, fork=()) -> torch.Tensor:
     """Fast-path interval records (mvb_coef32, 12 floats) of every decimated
-    image, one mvb_track_coeffs launch per decimation factor."""
-    coef = torch.empty(max(geom.n_coarse_total, 1) * 12, dtype=torch.float32, device=geom.dev)
-    for N, sel in geom.sel_by_factor.items():
+    image, one mvb_track_coeffs launch per decimation factor; with `fork`
+    streams (graph capture) the factors after the first run as parallel
+    branches (the caller joins them)."""
+    dev = geom.dev
+    coef = torch.empty(max(geom.n_coarse_total, 1) * 12, dtype=torch.float32, device=dev)
+    main = torch.cuda.current_stream(dev)
+    for q, (N, sel) in enumerate(geom.sel_by_factor.items()):
         fit = np.ascontiguousarray(phase_fit(N), dtype=np.float64)
         max_K = -(-int(geom.T.max()) // N)
-        _lib.call("mvb_track_coeffs", ptr(geom.images), ptr(sel), sel.numel(), max_K, ptr(pre_dev),
-                  ptr(geom.coarse), fit.ctypes.data_as(ctypes.c_void_p), ptr(coef), st)
+        fs = fork[(q - 1) % len(fork)] if q and fork else main
+        if fs is not main:
+            fs.wait_stream(main)
+        with torch.cuda.stream(fs):
+            _lib.call("mvb_track_coeffs", ptr(geom.images), ptr(sel), sel.numel(), max_K,
+                      ptr(pre_dev), ptr(geom.coarse), fit.ctypes.data_as(ctypes.c_void_p),
+                      ptr(coef), stream_handle(dev))
     return coef
 
 

@@ -89,11 +89,13 @@ _FORK: dict = {}
 
 
 def fork_streams(dev) -> list:
-    """Two capture-only streams for the parallel branches of a geometry
-    graph (the captured graph records the fork / join, not the streams)."""
+    """Capture-only streams for the parallel branches of a geometry graph
+    (delay sort, branch records, the second factor's interval records, the
+    exact maxima); the captured graph records the fork / join, not the
+    streams."""
     key = str(dev)
     if key not in _FORK:
-        _FORK[key] = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+        _FORK[key] = [torch.cuda.Stream(device=dev) for _ in range(4)]
     return _FORK[key]
 
 
@@ -152,7 +154,7 @@ class RenderPlan:
                 mic = torch.empty(_dims(jb.mic), dtype=torch.float64, device=self.dev)
                 slot.jobs.append(replace(jb, pos=static_pos[pk], s=static_sig[sk], mic=mic,
                                          path_key=("plan", pk), signal_key=("plan", sk)))
-            slot.paths = None
+            slot.paths = slot.bbox = None
             self.slots.append(slot)
         self.k = 0
         self.captures = 0
@@ -180,14 +182,14 @@ class RenderPlan:
         """Stage the slot's static inputs into its static paths buffer: on the
         side stream after `ready` (pipelined), or on the current stream.
         `wait=False`: leave the readbacks pending (Geometry.collect())."""
-        if slot.paths is None:  # first staging allocates the slot's paths buffer
+        if slot.paths is None:  # first staging allocates the slot's paths / box buffers
             if ready is not None:
                 torch.cuda.current_stream(self.dev).wait_event(ready)
             geom = engine.Geometry(slot.jobs, device=self.dev, defer=True)
-            slot.paths = geom.paths
+            slot.paths, slot.bbox = geom.paths, geom.bbox
             return geom
         return engine.Geometry(slot.jobs, device=self.dev, inputs_ready=ready, paths=slot.paths,
-                               defer=True, wait=wait)
+                               defer=True, wait=wait, bbox=slot.bbox)
 
     SLACK = 0.1  # output capacity headroom of a capture (fraction of the length bound)
 
@@ -195,11 +197,14 @@ class RenderPlan:
         """Geometry and the render's first half (see engine.PreparedRender);
         `fork`: parallel graph branches for the sort and branch records."""
         geom.length_slack = self.SLACK
-        geom.finish()
-        return engine.prepare_render(geom, [sj.s for sj in slot.jobs], self.f,
+        geom.finish(fork=None if fork is None else fork[3])  # exact maxima: own branch
+        prep = engine.prepare_render(geom, [sj.s for sj in slot.jobs], self.f,
                                      precision=self.precision,
                                      signal_keys=[engine._key(sj.signal_key, sj.s)
-                                                  for sj in slot.jobs], fork=fork)
+                                                  for sj in slot.jobs],
+                                     fork=None if fork is None else fork[:3])
+        geom.join()  # every branch ends inside the geometry graph
+        return prep
 
     def _collect(self, slot):
         """Record the synthesis time of the slot's finished replay."""
@@ -238,8 +243,9 @@ class RenderPlan:
         g_geo, g_syn = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         slot.timing = []
         launches0 = _lib.launch_count()
+        fork = self.fork_streams if os.environ.get("MVB_PLAN_FORK", "1") != "0" else None
         with uploads, torch.cuda.graph(g_geo, stream=self.geo_stream):
-            prep = self._prepare(slot, geom, fork=self.fork_streams)
+            prep = self._prepare(slot, geom, fork=fork)
         with uploads, torch.cuda.graph(g_syn, stream=self.syn_stream):
             res = prep.launch(slot.timing)
         slot.graphs = [g_geo, g_syn]

@@ -20,7 +20,7 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():  # pragma: no cover - CPU box
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-from paper_2508_03065_b200 import kernels, room as mroom  # noqa: E402
+from paper_2508_03065_b200 import engine, kernels, room as mroom  # noqa: E402
 from paper_2508_03065_b200.synth import render_jobs, scene_jobs  # noqa: E402
 
 FP32_TOL = 1e-5
@@ -290,6 +290,28 @@ def test_render_plan_replays_match_direct_renders():
         jb = [dataclasses.replace(anon[0], pos=scenes[0].pos + 0.001 * it,
                                   s=(scenes[0].s * (it + 1)).astype(np.float32))]
         assert torch.equal(plan1.run(jb).job(0), render_jobs(jb, f).job(0))
+
+
+def test_render_plan_full_rate_paths_change():
+    """A plan whose images are all full-rate bounds them from the path boxes
+    inside its graph: the boxes of each run (not the capture's) must be
+    used -- paths move between runs without re-capturing, lengths and
+    outputs equal direct renders bit for bit (fp64 and fp32)."""
+    import dataclasses
+    from paper_2508_03065_b200.plan import RenderPlan
+    sc = workloads.make_scenes("c1", duration=0.1)[0]
+    f = hann_sinc(32, 14)
+    for prec in ("fp64", "fp32"):
+        s = sc.s.astype(np.float64 if prec == "fp64" else np.float32)
+        job = engine.Job(s=s, pos=sc.pos, mic=sc.mics[0], dims=sc.dims, walls=sc.walls,
+                         max_order=2, tiers=((2, 1),), rate=sc.rate)
+        plan = RenderPlan([job], f, precision=prec)
+        for it, shift in enumerate((0.0, 0.25, -0.3, 0.4, 0.1)):
+            jb = [dataclasses.replace(job, pos=sc.pos + np.array([shift, -0.5 * shift, 0.0]))]
+            got, ref = plan.run(jb), render_jobs(jb, f, precision=prec)
+            assert np.array_equal(got.lengths, ref.lengths), (prec, it)
+            assert torch.equal(got.job(0), ref.job(0)), (prec, it)
+        assert plan.captures == 2, plan.captures  # one per slot: the moves stayed in capacity
 
 
 def test_render_plan_image_shards():
