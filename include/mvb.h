@@ -92,12 +92,17 @@ int mvb_enumerate(const double* d_dims, const double* d_walls, int64_t n_rooms,
  *      paths:  path_bbox; center_paths -> (cuFFT rFFT) -> spectrum_index
  *              (host: low-pass decision, output capacity bound from the
  *              boxes) -> decimate_rows
- *      images: enumerate -> build_images
- *      tracks: coarse_distances (+ bounds) -> track_bounds -> track_max
- *      fast:   branch_records_f32, track_coeffs, sort_keys (-> sort) ->
- *              gather_images, finalize_lengths (exact out_len = len(s) +
- *              ceil(rate*dmax/c) + L, synth.py:211-212, on the device) ->
- *              synthesize_f32 [-> reduce_partials_f32]
+ *      images: enumerate (cacheable per rooms + order) -> build_images
+ *      tracks: coarse_distances (+ bounds; one call per factor) ->
+ *              track_bounds -> track_max
+ *      fast:   branch_records_f32, track_coeffs (per factor), delay_sort
+ *              (or sort_keys -> sort -> gather_images beyond
+ *              MVB_DELAY_SORT_MAX images), finalize_lengths (exact out_len =
+ *              len(s) + ceil(rate*dmax/c) + L, synth.py:211-212, on the
+ *              device) -> synthesize_f32 [-> reduce_partials_f32]
+ *              (track_max, track_coeffs, delay_sort and branch_records_f32
+ *              depend only on the coarse tracks / the signal: independent
+ *              streams may run them concurrently)
  *      exact:  branch_filter (per signal), finalize_lengths, synthesize_f64
  * --------------------------------------------------------------------- */
 
