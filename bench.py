@@ -517,9 +517,11 @@ def run_ours(args):
                 "rate": w.rate,
                 "duration_s": w.duration,
                 "parallelism": mode,
-                "engine": ("RenderPlan: CUDA-graph replay of the whole render, inputs re-staged "
-                           "and decimation decision re-taken every step") if plan is not None
-                          else "direct render_jobs per step",
+                "engine": ("RenderPlan: every kernel of the render re-run each step from two "
+                           "CUDA graphs (geometry, synthesis) on two streams, so step k+1's "
+                           "geometry overlaps step k's synthesis drain; inputs re-staged and the "
+                           "decimation decision re-taken every step (speculative replay)")
+                          if plan is not None else "direct render_jobs per step",
                 "l2": "flushed before every timed step (256 MiB write, inside the timed region); per-step working set >L2",
             },
             "rtf": rtf,
