@@ -438,23 +438,31 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
     for (int64_t k0 = (int64_t)blockIdx.y * COEF_SPAN; k0 < K;
          k0 += (int64_t)gridDim.y * COEF_SPAN) {
         __syncthreads();
-        // dw[i] for i = k0 - 32 .. k0 + COEF_SPAN + 31 (clamped samples hold)
-        for (int t = threadIdx.x; t < COEF_SPAN + 64; t += blockDim.x) {
-            int64_t a = k0 - 32 + t, b = a + 1;
-            a = a < 0 ? 0 : (a >= K ? K - 1 : a);
-            b = b < 0 ? 0 : (b >= K ? K - 1 : b);
-            dw[skew32(t)] = (float)(c[b] - c[a]);
+        // coarse samples k0 - 32 .. k0 + COEF_SPAN + 32 (clamped: samples hold)
+        // staged once in the record area (free until the epilogue), then
+        // dw[i] = c[i + 1] - c[i] in fp64, stored fp32 (skewed)
+        double* cw = reinterpret_cast<double*>(srec);
+        const int Ki = (int)K, base = (int)k0 - 32;
+        for (int t = threadIdx.x; t < COEF_SPAN + 65; t += blockDim.x) {
+            int a = base + t;
+            a = a < 0 ? 0 : (a >= Ki ? Ki - 1 : a);
+            cw[t] = c[a];
         }
         __syncthreads();
+        for (int t = threadIdx.x; t < COEF_SPAN + 64; t += blockDim.x)
+            dw[skew32(t)] = (float)(cw[t + 1] - cw[t]);
+        __syncthreads();
         if (k0 + e0 < K) {
+        static_assert(COEF_KI % 2 == 0, "the g8 accumulators pair adjacent intervals");
         float2 acc[COEF_KI][4];
-        float acc8[COEF_KI];
+        float2 acc8[COEF_KI / 2];  // (interval 2h, interval 2h+1) of coefficient 8
 #pragma unroll
         for (int q = 0; q < COEF_KI; ++q) {
 #pragma unroll
             for (int p = 0; p < 4; ++p) acc[q][p] = make_float2(0.f, 0.f);
-            acc8[q] = 0.f;
         }
+#pragma unroll
+        for (int h = 0; h < COEF_KI / 2; ++h) acc8[h] = make_float2(0.f, 0.f);
         float x[COEF_KI];
 #pragma unroll
         for (int q = 0; q < COEF_KI - 1; ++q) x[q + 1] = dw[skew32(e0 + q)];
@@ -470,8 +478,11 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
 #pragma unroll
                 for (int p = 0; p < 4; ++p)
                     acc[q][p] = __ffma2_rn(make_float2(g[2 * p], g[2 * p + 1]), xx, acc[q][p]);
-                acc8[q] = fmaf(g[8], x[q], acc8[q]);
             }
+#pragma unroll
+            for (int h = 0; h < COEF_KI / 2; ++h)
+                acc8[h] = __ffma2_rn(make_float2(g[8], g[8]), make_float2(x[2 * h], x[2 * h + 1]),
+                                     acc8[h]);
         }
 #pragma unroll
         for (int q = 0; q < COEF_KI; ++q) {
@@ -493,7 +504,7 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
             r.g[4] = kf * acc[q][2].y;
             r.g[5] = kf * acc[q][3].x;
             r.g[6] = kf * acc[q][3].y;
-            r.g[7] = kf * acc8[q];
+            r.g[7] = kf * ((q & 1) ? acc8[q >> 1].y : acc8[q >> 1].x);
             const float4* rv = reinterpret_cast<const float4*>(&r);
             float4* dstq = srec + REC_F4 * threadIdx.x + 3 * q;
             dstq[0] = rv[0];

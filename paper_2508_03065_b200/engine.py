@@ -182,7 +182,7 @@ class Geometry:
     """Device-side hierarchical tracks of a batch of jobs (prepare stage)."""
 
     def __init__(self, jobs: list, device=None, inputs_ready=None, dmax_hook=None,
-                 paths=None, defer=False, wait=True, bbox=None):
+                 paths=None, defer=False, wait=True, bbox=None, on_paths=None):
         """`inputs_ready`: optional CUDA event after which every device
         tensor of `jobs` is final.  With it, the paths are staged and their
         bandwidths measured on a side stream that waits only for that event,
@@ -198,7 +198,10 @@ class Geometry:
         (with defer): enqueue the staging and its two readbacks but do not
         wait for them -- `paths_ready` (an event after the path upload) lets
         device work that needs only the paths start at once, collect() waits
-        for the boxes and the decision (render plans replay speculatively)."""
+        for the boxes and the decision (render plans replay speculatively).
+        `on_paths(event)`: called as soon as that event is recorded, before
+        the bandwidth kernels are enqueued (a plan launches its replay
+        there, ahead of the host-side issue of the decision pipeline)."""
         if not jobs:
             raise ValueError("no jobs")
         self.dev = require_cuda(device)
@@ -209,7 +212,8 @@ class Geometry:
         host_parts, dev_parts, rows = self._layout_paths()
         self.rows = rows
         _mark("geom.setup")
-        self._pending = self._stage_paths(host_parts, dev_parts, rows, inputs_ready, paths, bbox)
+        self._pending = self._stage_paths(host_parts, dev_parts, rows, inputs_ready, paths, bbox,
+                                          on_paths)
         if wait or not defer:
             self.collect()
         _mark("geom.bandwidth")
@@ -293,7 +297,8 @@ class Geometry:
                     row += -(-int(self.T[j]) // N) * (1 + int(self.moving[j]))
         return host_parts, dev_parts, max(row, 1)
 
-    def _stage_paths(self, host_parts, dev_parts, rows, inputs_ready, paths=None, bbox=None):
+    def _stage_paths(self, host_parts, dev_parts, rows, inputs_ready, paths=None, bbox=None,
+                     on_paths=None):
         """Fill the full-rate rows of the paths buffer, compute every job's
         path bounding boxes and the paths' bandwidths; the two small
         readbacks (boxes, bandwidth indices) are the host's only waits.
@@ -333,6 +338,8 @@ class Geometry:
             box_ready = torch.cuda.Event()
             box_ready.record()
             self.paths_ready = box_ready  # the paths' full-rate rows are on the device
+            if on_paths is not None:
+                on_paths(box_ready)
             path_groups, finishers = self._path_bandwidths(main)
         if side is not main:
             main.wait_stream(side)
@@ -971,12 +978,14 @@ def _interval_records(geom, pre_dev, st, fork=()) -> torch.Tensor:
     dev = geom.dev
     coef = torch.empty(max(geom.n_coarse_total, 1) * 12, dtype=torch.float32, device=dev)
     main = torch.cuda.current_stream(dev)
+    start = torch.cuda.Event()
+    start.record(main)  # fork point: before the first factor's launch
     for q, (N, sel) in enumerate(geom.sel_by_factor.items()):
         fit = np.ascontiguousarray(phase_fit(N), dtype=np.float64)
         max_K = -(-int(geom.T.max()) // N)
         fs = fork[(q - 1) % len(fork)] if q and fork else main
         if fs is not main:
-            fs.wait_stream(main)
+            fs.wait_event(start)
         with torch.cuda.stream(fs):
             _lib.call("mvb_track_coeffs", ptr(geom.images), ptr(sel), sel.numel(), max_K,
                       ptr(pre_dev), ptr(geom.coarse), fit.ctypes.data_as(ctypes.c_void_p),

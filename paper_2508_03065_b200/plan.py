@@ -178,7 +178,7 @@ class RenderPlan:
                         np.asarray(src).reshape(-1)
                     _STAGER.upload([(0, a)], dst)
 
-    def _stage(self, slot, ready, wait=True):
+    def _stage(self, slot, ready, wait=True, on_paths=None):
         """Stage the slot's static inputs into its static paths buffer: on the
         side stream after `ready` (pipelined), or on the current stream.
         `wait=False`: leave the readbacks pending (Geometry.collect())."""
@@ -189,7 +189,7 @@ class RenderPlan:
             slot.paths, slot.bbox = geom.paths, geom.bbox
             return geom
         return engine.Geometry(slot.jobs, device=self.dev, inputs_ready=ready, paths=slot.paths,
-                               defer=True, wait=wait, bbox=slot.bbox)
+                               defer=True, wait=wait, bbox=slot.bbox, on_paths=on_paths)
 
     SLACK = 0.1  # output capacity headroom of a capture (fraction of the length bound)
 
@@ -301,10 +301,10 @@ class RenderPlan:
         # paths are on the device, check the staging readbacks meanwhile,
         # and re-capture + replay only if they changed
         spec = slot.graph is not None
-        geom = self._stage(slot, ready, wait=not spec)
-        staged = _lib.launch_count() - staged0  # staging kernels (outside the graphs)
+        replay = (lambda ev: self._replay(slot, ev)) if spec else None
+        geom = self._stage(slot, ready, wait=not spec, on_paths=replay)
+        staged = _lib.launch_count() - staged0  # staging kernels (graph replays are not counted)
         if spec:
-            self._replay(slot, geom.paths_ready)
             geom.collect()
         bound = np.asarray([geom.length_bound(j) for j in range(len(slot.jobs))])
         if not spec or geom.lowpass_decision() != slot.decision \
