@@ -85,7 +85,7 @@ __device__ __forceinline__ void seg_maxmin(const double* c, int64_t K, int64_t s
 // shuffle-max costs ~20 instructions); lb, which seeds the exact maximum,
 // stays the exact fp64 coarse max (lane-local, one reduction per chunk).
 // Chunk results merge atomically into the zero-initialised lb / ub.
-constexpr int CB_SEGS = 16;
+constexpr int CB_SEGS = 16;  // chunk length of large launches (8 for small ones, below)
 
 __device__ __forceinline__ void warp_maxmin_f(float& M, float& m) {
 #pragma unroll
@@ -95,6 +95,7 @@ __device__ __forceinline__ void warp_maxmin_f(float& M, float& m) {
     }
 }
 
+template <int CB_SEGS>
 __global__ void k_coarse_bounds(const mvb_image* __restrict__ images, const int32_t* __restrict__ sel,
                                 int64_t n_sel, const mvb_job* __restrict__ jobs,
                                 const double* __restrict__ paths, double negsum,
@@ -896,9 +897,21 @@ int mvb_coarse_distances(const mvb_image* images, const int32_t* sel, int64_t n_
     if (!images || !sel || !jobs || !paths || !coarse) return fail(MVB_EINVAL, "coarse_distances: null");
     if ((lb == nullptr) != (ub == nullptr)) return fail(MVB_EINVAL, "coarse_distances: lb/ub");
     if (max_K < 1) return fail(MVB_EINVAL, "coarse_distances: max_K");
-    const int64_t chunks = ((max_K + 63) / 64 + CB_SEGS - 1) / CB_SEGS;
+    // warps walk CB_SEGS-segment chunks serially: launches with few images
+    // (image shards) use shorter chunks for more parallel warps (c3 W=8:
+    // 50 -> 37 us), large ones the longer chunks (fewer recomputed edges)
+    const int64_t chunks16 = ((max_K + 63) / 64 + CB_SEGS - 1) / CB_SEGS;
+    if (n_sel * chunks16 < 148 * 64) {
+        const int64_t chunks = ((max_K + 63) / 64 + 7) / 8;
+        if (chunks > 65535) return fail(MVB_EINVAL, "coarse_distances: coarse track too long");
+        k_coarse_bounds<8><<<dim3(grid_for(n_sel, 8), (unsigned)chunks), 256, 0,
+                             as_stream(stream)>>>(images, sel, n_sel, jobs, paths, negsum, coarse,
+                                                  lb, ub);
+        return check_launch("coarse_distances");
+    }
+    const int64_t chunks = chunks16;
     if (chunks > 65535) return fail(MVB_EINVAL, "coarse_distances: coarse track too long");
-    k_coarse_bounds<<<dim3(grid_for(n_sel, 8), (unsigned)chunks), 256, 0, as_stream(stream)>>>(
+    k_coarse_bounds<CB_SEGS><<<dim3(grid_for(n_sel, 8), (unsigned)chunks), 256, 0, as_stream(stream)>>>(
         images, sel, n_sel, jobs, paths, negsum, coarse, lb, ub);
     return check_launch("coarse_distances");
 }
