@@ -314,6 +314,39 @@ def test_render_plan_full_rate_paths_change():
         assert plan.captures == 2, plan.captures  # one per slot: the moves stayed in capacity
 
 
+def test_render_plan_lowpass_decision_change():
+    """A speculative replay whose staging shows a changed anti-alias
+    decision (trajectory.py:279-298: low-pass only when Nyquist_out <
+    bandwidth < 2 Nyquist_out) is redone with a re-captured graph: the path
+    oscillates below the decimated tier's output Nyquist in one run and
+    between one and two Nyquist in the next; both equal direct renders."""
+    import dataclasses
+    from paper_2508_03065_b200.plan import RenderPlan
+    rate, T, N = 16000.0, 8000, 64  # tier output Nyquist: 125 Hz
+    t = np.arange(T) / rate
+    dims = np.array([6.0, 5.0, 3.0])
+
+    def path(freq):
+        return np.stack([3.0 + 0.02 * np.sin(2 * np.pi * freq * t), 2.5 + 0.0 * t,
+                         1.5 + 0.0 * t], axis=1)
+
+    x = np.random.default_rng(4).standard_normal(T).astype(np.float32)
+    job = engine.Job(s=x, pos=path(40.0), mic=np.array([1.0, 1.2, 1.1]), dims=dims, walls=0.8,
+                     max_order=3, tiers=((1, 1), (3, N)), rate=rate)
+    f = hann_sinc(32, 14)
+    plan = RenderPlan([job], f)
+    decisions = []
+    for freq in (40.0, 40.0, 40.0, 180.0, 180.0, 40.0):
+        jb = [dataclasses.replace(job, pos=path(freq))]
+        got, ref = plan.run(jb), render_jobs(jb, f)
+        geom = engine.Geometry(jb)
+        decisions.append(any(len(d) for d in geom.lowpass_decision()))
+        assert np.array_equal(got.lengths, ref.lengths), freq
+        assert torch.equal(got.job(0), ref.job(0)), freq
+    assert decisions == [False, False, False, True, True, False], decisions
+    assert plan.misses >= 2  # 40 -> 180 Hz and back, on a captured slot
+
+
 def test_render_plan_image_shards():
     """Sharded plans: geometry graph, eager dmax hook, render graph; the
     shards' replays sum to the full render (shards in sequence on one GPU)."""
