@@ -220,11 +220,24 @@ def side_stream(dev) -> torch.cuda.Stream:
     return _SIDE[key]
 
 
+D2H_DIRECT = 1 << 16  # elements: above, d2h returns a pinned block of the caching allocator
+
+
 def d2h(t: torch.Tensor, dtype=None) -> np.ndarray:
-    """Device tensor -> new numpy array (optionally converted to `dtype`):
-    one copy into persistent pinned staging (waits only for the producing
-    stream), then a threaded copy out -- no per-call pinned allocation,
-    whose cudaHostAlloc would synchronise the device."""
+    """Device tensor -> new numpy array (optionally converted to `dtype`).
+    Large results: cast on the device, one copy into a pinned block of
+    torch's caching host allocator, returned as the array itself (no host
+    conversion or copy-out; the block returns to the cache when the array is
+    dropped, so steady-state calls allocate no new pinned memory).  Small
+    ones: persistent pinned staging + a copy out."""
+    if t.numel() >= D2H_DIRECT:
+        tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32}.get(
+            np.dtype(dtype) if dtype is not None else None, t.dtype)
+        src = t.reshape(-1) if tdt == t.dtype else t.reshape(-1).to(tdt)
+        host = torch.empty(src.numel(), dtype=tdt, pin_memory=True)
+        host.copy_(src, non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+        return host.numpy().reshape(tuple(t.shape))
     host = pinned_scratch("d2h_" + str(t.dtype), t.numel(), t.dtype)
     host.copy_(t.reshape(-1), non_blocking=True)
     torch.cuda.current_stream(t.device).synchronize()
