@@ -75,9 +75,11 @@ _STREAMS: dict = {}
 
 
 def plan_streams(dev) -> tuple:
-    """(geometry, synthesis) streams of the render plans on `dev`: the
-    geometry stream at the highest priority, the synthesis stream at the
-    default one, shared by every plan on the device."""
+    """(geometry, synthesis) streams of the render plans on `dev`, shared
+    by every plan on the device.  Both at the default priority: the next
+    run's geometry then fills the drain of the running synthesis (FIFO
+    dispatch); a high-priority geometry stream (MVB_GEO_PRIO) interleaves
+    its CTAs into the synthesis and was measured slower."""
     key = str(dev)
     if key not in _STREAMS:
         _STREAMS[key] = (torch.cuda.Stream(device=dev, priority=int(os.environ.get("MVB_GEO_PRIO", "0"))),
@@ -116,10 +118,11 @@ class RenderPlan:
 
     def __init__(self, jobs, f, precision: str = "fp32", device=None, shard=None, dmax_hook=None):
         """`shard=(rank, world)`: render the image shard of `rank` of every
-        job (parallel.image_shard, as synth.render_jobs) with `dmax_hook` (default: all-reduce MAX
-        over the process group) applied to the track maxima between a
-        geometry graph and a render graph -- the collective itself is issued
-        eagerly, never captured."""
+        job (parallel.image_shard, as synth.render_jobs) with `dmax_hook`
+        (default: all-reduce MAX over the process group) applied to the
+        track maxima between the geometry graph and the synthesis graph --
+        the collective itself is issued eagerly on the geometry stream,
+        never captured."""
         if precision not in ("fp32", "fp64"):
             raise ValueError("precision must be 'fp32' or 'fp64'")
         if shard is not None and int(shard[1]) > 1:
@@ -195,7 +198,9 @@ class RenderPlan:
 
     def _prepare(self, slot, geom, fork=None):
         """Geometry and the render's first half (see engine.PreparedRender);
-        `fork`: parallel graph branches for the sort and branch records."""
+        `fork` (capture only): four streams for the parallel branches -- delay
+        sort, branch records, further factors' interval records, exact
+        maxima -- all joined before the geometry graph ends."""
         geom.length_slack = self.SLACK
         geom.finish(fork=None if fork is None else fork[3])  # exact maxima: own branch
         prep = engine.prepare_render(geom, [sj.s for sj in slot.jobs], self.f,
