@@ -36,6 +36,14 @@ int mvb_device_info(int* h_sm_count, int* h_cc_major, int* h_cc_minor);
 /* sizeof of the structs below as compiled into the library (for bindings
  * that pack them by hand): image, job, work, coef32. */
 int mvb_struct_sizes(int* h_image, int* h_job, int* h_work, int* h_coef32);
+/* Batched asynchronous copies on `stream` (the input staging of batch
+ * renders: one call instead of one runtime call per job input).  Entry i
+ * copies h_bytes[i] bytes from h_src[i] to h_dst[i] (cudaMemcpyDefault:
+ * host or device pointers).  With require_pinned != 0 an entry whose source
+ * is not page-locked host memory is skipped (h_issued[i] = 0; the caller
+ * stages it itself), otherwise h_issued[i] = 1.  Launches no kernel. */
+int mvb_copy_batch(void* const* h_dst, const void* const* h_src, const int64_t* h_bytes,
+                   int64_t n, int32_t* h_issued, int require_pinned, void* stream);
 
 /* ------------------------------------------------------------------------
  * 1. Operator boundary: the reference's kernel swap point (_kernels.py:21-31).

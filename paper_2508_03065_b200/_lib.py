@@ -29,6 +29,7 @@ _SIGS = {
     "mvb_last_error": [],
     "mvb_device_info": [P, P, P],
     "mvb_struct_sizes": [P, P, P, P],
+    "mvb_copy_batch": [P, P, P, I64, P, INT, P],
     "mvb_distance_streams": [P, P, P, P, I64, I64, P, P],
     "mvb_accumulate_images": [P, I64, P, I64, I64, P, P, I64, I64, I64, P],
     "mvb_upsample_streams": [P, I64, I64, P, I64, I64, I64, P, P],
@@ -66,7 +67,7 @@ _RESTYPE = {"mvb_last_error": ctypes.c_char_p, "mvb_image_count": I64}
 # one; the query functions launch none) -- feeds launch_count()
 _KERNELS = {"mvb_track_max": 2, "mvb_path_bbox": 2, "mvb_center_paths": 2,
             "mvb_spectrum_index": 2, "mvb_abi_version": 0, "mvb_last_error": 0,
-            "mvb_device_info": 0, "mvb_struct_sizes": 0, "mvb_image_count": 0}
+            "mvb_device_info": 0, "mvb_struct_sizes": 0, "mvb_copy_batch": 0, "mvb_image_count": 0}
 _launches = 0
 
 IMAGE_BYTES, JOB_BYTES, WORK_BYTES, COEF_BYTES = 96, 136, 32, 48

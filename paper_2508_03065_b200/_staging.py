@@ -67,6 +67,23 @@ def _host_tensor(a: np.ndarray) -> torch.Tensor:
         return torch.from_numpy(a)
 
 
+def copy_batch(entries, stream: int, require_pinned: bool) -> np.ndarray:
+    """Issue [(dst_ptr, src_ptr, nbytes)] as asynchronous copies on `stream`
+    with one libmvb call (mvb_copy_batch); returns which entries were issued
+    (with `require_pinned`, sources outside page-locked memory are left to
+    the caller)."""
+    from . import _lib
+    n = len(entries)
+    if n == 0:
+        return np.zeros(0, bool)
+    a = np.asarray(entries, dtype=np.int64).reshape(n, 3)
+    dst, src, nb = (np.ascontiguousarray(a[:, k]) for k in range(3))
+    issued = np.zeros(n, np.int32)
+    _lib.call("mvb_copy_batch", dst.ctypes.data, src.ctypes.data, nb.ctypes.data, n,
+              issued.ctypes.data, int(bool(require_pinned)), stream)
+    return issued.astype(bool)
+
+
 def is_pinned(a) -> bool:
     """True for a C-contiguous numpy array in page-locked host memory (e.g.
     a view of a pinned torch tensor, or a Trajectory's positions): such

@@ -218,6 +218,34 @@ int mvb_device_info(int* sm_count, int* cc_major, int* cc_minor) {
     return MVB_OK;
 }
 
+int mvb_copy_batch(void* const* dst, const void* const* src, const int64_t* bytes, int64_t n,
+                   int32_t* issued, int require_pinned, void* stream) {
+    if (n < 0) return fail(MVB_EINVAL, "copy_batch: n");
+    if (n == 0) return MVB_OK;
+    if (!dst || !src || !bytes || !issued) return fail(MVB_EINVAL, "copy_batch: null");
+    cudaStream_t s = as_stream(stream);
+    for (int64_t i = 0; i < n; ++i) {
+        issued[i] = 0;
+        if (bytes[i] < 0) return fail(MVB_EINVAL, "copy_batch: negative size");
+        if (bytes[i] == 0) {
+            issued[i] = 1;
+            continue;
+        }
+        if (require_pinned) {
+            cudaPointerAttributes a;
+            if (cudaPointerGetAttributes(&a, src[i]) != cudaSuccess) {
+                cudaGetLastError();  // pageable memory on old runtimes: not an error here
+                continue;
+            }
+            if (a.type != cudaMemoryTypeHost) continue;
+        }
+        cudaError_t e = cudaMemcpyAsync(dst[i], src[i], (size_t)bytes[i], cudaMemcpyDefault, s);
+        if (e != cudaSuccess) return fail(MVB_ECUDA, std::string("copy_batch: ") + cudaGetErrorString(e));
+        issued[i] = 1;
+    }
+    return MVB_OK;
+}
+
 int mvb_struct_sizes(int* image, int* job, int* work, int* coef) {
     if (image) *image = (int)sizeof(mvb_image);
     if (job) *job = (int)sizeof(mvb_job);

@@ -46,7 +46,7 @@ import torch
 
 from . import _lib
 from ._dev import h2d, pinned_scratch, ptr, require_cuda, stream_handle
-from ._staging import _ARENA, _STAGER, d2h, parallel_copy, side_stream  # noqa: F401
+from ._staging import _ARENA, _STAGER, copy_batch, d2h, parallel_copy, side_stream  # noqa: F401
 from .farrow import as_filter, centered_branches
 from .room import image_table
 from .trajectory import (bandwidth_batch_async, device_constants, lowpass_batch, negative_mass,
@@ -323,8 +323,17 @@ class Geometry:
                 self.paths = torch.empty(rows, 3, dtype=torch.float64, device=dev)
             if host_parts:
                 _STAGER.upload(host_parts, self.paths)
+            # device-resident paths (render plans' static inputs): one batched
+            # call for the contiguous fp64 ones
+            batch = []
             for r0, p in dev_parts:
-                self.paths[r0:r0 + p.shape[0]].copy_(p)
+                if p.dtype == torch.float64 and p.is_contiguous() and p.device == dev \
+                        and tuple(p.shape[1:]) == (3,):
+                    batch.append((self.paths.data_ptr() + 24 * r0, p.data_ptr(), 24 * p.shape[0]))
+                else:
+                    self.paths[r0:r0 + p.shape[0]].copy_(p)
+            if batch:
+                copy_batch(batch, side.cuda_stream, require_pinned=False)
             box_rows = h2d(np.stack([self.pos_off, self.T, self.mic_off, self.moving], axis=1), dev)
             # flat: the nJ x 12 boxes first, then the 64 partial boxes per job
             if bbox is not None and bbox.numel() >= nJ * 65 * 12:
