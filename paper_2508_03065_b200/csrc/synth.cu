@@ -61,6 +61,11 @@ __device__ __forceinline__ void ldg8(float4& a, float4& b, const float4* p) {
 
 // One launch for every distinct dry signal of a batch: blockIdx.y selects
 // the signal (x_all + off[y], length len[y], record rows from row0[y]).
+// Thread t of a block computes the rows m0 + t + q * blockDim.x, q < BR_Q
+// (consecutive threads: consecutive rows, coalesced 32-byte row stores);
+// per tap j one broadcast float4 read per 4 branches serves BR_Q x NB FMAs.
+constexpr int BR_Q = 4;
+
 template <int NP>
 __global__ void k_branch_records_f32(const float* __restrict__ x_all,
                                      const int64_t* __restrict__ sig_off,
@@ -69,37 +74,56 @@ __global__ void k_branch_records_f32(const float* __restrict__ x_all,
                                      const double* __restrict__ cb, int M1, int L,
                                      float* __restrict__ rec) {
     constexpr int NB = 4 * NP;
-    extern __shared__ float sx[];  // [blockDim.x + L - 1]
-    __shared__ float sc[NB * 128];
+    extern __shared__ float sx[];      // [BR_Q * blockDim.x + L - 1]
+    __shared__ float4 sc[128 * NP];    // tap j, branches 4p..4p+3 at sc[j * NP + p]
+    const int B = blockDim.x;
     const int64_t T = sig_len[blockIdx.y];
-    const int64_t m0 = (int64_t)blockIdx.x * blockDim.x;
+    const int64_t m0 = (int64_t)blockIdx.x * B * BR_Q;
     if (m0 >= T + L - 1) return;
     const float* __restrict__ x = x_all + sig_off[blockIdx.y];
     const int64_t row0 = sig_row0[blockIdx.y];
-    for (int t = threadIdx.x; t < NB * L; t += blockDim.x) {
-        const int k = t / L, j = t - (t / L) * L;
-        sc[k * L + j] = k < M1 ? (float)cb[k * L + j] : 0.f;
+    float* scf = reinterpret_cast<float*>(sc);
+    for (int t = threadIdx.x; t < NB * L; t += B) {
+        const int j = t / NB, k = t - (t / NB) * NB;
+        scf[t] = k < M1 ? (float)cb[k * L + j] : 0.f;
     }
-    for (int t = threadIdx.x; t < (int)blockDim.x + L - 1; t += blockDim.x) {
+    for (int t = threadIdx.x; t < BR_Q * B + L - 1; t += B) {
         const int64_t q = m0 - (L - 1) + t;
         sx[t] = (q >= 0 && q < T) ? x[q] : 0.f;
     }
     __syncthreads();
-    const int64_t m = m0 + threadIdx.x;
-    if (m >= T + L - 1) return;
-    float acc[NB];
+    float acc[BR_Q][NB];
 #pragma unroll
-    for (int k = 0; k < NB; ++k) acc[k] = 0.f;
-    // v_k[m] = sum_j c_k[j] x[m - j];  sx[threadIdx.x + L-1 - j] = x[m - j]
+    for (int q = 0; q < BR_Q; ++q)
+#pragma unroll
+        for (int k = 0; k < NB; ++k) acc[q][k] = 0.f;
+    // v_k[m] = sum_j c_k[j] x[m - j] (j ascending, one rounding per FMA);
+    // sx[threadIdx.x + q * B + L-1 - j] = x[m - j]
     for (int j = 0; j < L; ++j) {
-        const float xv = sx[threadIdx.x + L - 1 - j];
+        float4 c[NP];
 #pragma unroll
-        for (int k = 0; k < NB; ++k) acc[k] = fmaf(sc[k * L + j], xv, acc[k]);
+        for (int p = 0; p < NP; ++p) c[p] = sc[j * NP + p];
+#pragma unroll
+        for (int q = 0; q < BR_Q; ++q) {
+            const float xv = sx[threadIdx.x + q * B + L - 1 - j];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) {
+                acc[q][4 * p] = fmaf(c[p].x, xv, acc[q][4 * p]);
+                acc[q][4 * p + 1] = fmaf(c[p].y, xv, acc[q][4 * p + 1]);
+                acc[q][4 * p + 2] = fmaf(c[p].z, xv, acc[q][4 * p + 2]);
+                acc[q][4 * p + 3] = fmaf(c[p].w, xv, acc[q][4 * p + 3]);
+            }
+        }
     }
-    float4* o = reinterpret_cast<float4*>(rec) + (size_t)(row0 + m) * row_f4<NP>();
 #pragma unroll
-    for (int p = 0; p < NP; ++p)
-        o[p] = make_float4(acc[4 * p], acc[4 * p + 1], acc[4 * p + 2], acc[4 * p + 3]);
+    for (int q = 0; q < BR_Q; ++q) {
+        const int64_t m = m0 + threadIdx.x + (int64_t)q * B;
+        if (m >= T + L - 1) break;
+        float4* o = reinterpret_cast<float4*>(rec) + (size_t)(row0 + m) * row_f4<NP>();
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+            o[p] = make_float4(acc[q][4 * p], acc[q][4 * p + 1], acc[q][4 * p + 2], acc[q][4 * p + 3]);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -567,8 +591,8 @@ int mvb_branch_records_f32(const float* x_all, const int64_t* sig_off, const int
     if (!x_all || !sig_off || !sig_len || !sig_row0 || !cb || !rec)
         return fail(MVB_EINVAL, "branch_records: null");
     const int block = 256;
-    const size_t smem = sizeof(float) * (block + L - 1);
-    const dim3 g(grid_for(max_len + L - 1, block), (unsigned)n_sig);
+    const size_t smem = sizeof(float) * (BR_Q * block + L - 1);
+    const dim3 g(grid_for(max_len + L - 1, BR_Q * block), (unsigned)n_sig);
     cudaStream_t s = as_stream(stream);
 #define MVB_BR(NP) k_branch_records_f32<NP><<<g, block, smem, s>>>(x_all, sig_off, sig_len, \
                                                                    sig_row0, cb, M1, L, rec)
