@@ -299,3 +299,30 @@ def test_render_reuses_a_plan_for_repeated_structure():
     assert all(np.array_equal(y64[0], y) for y in y64[1:])
     synth.release_plans()
     assert not synth._PLANS
+
+
+def test_copy_batch_pinned_pageable_and_device():
+    """mvb_copy_batch (batched input staging): page-locked sources are
+    copied, pageable ones skipped when require_pinned (the caller stages
+    them), device-to-device entries copied without the requirement."""
+    from paper_2508_03065_b200._staging import copy_batch
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(5)
+    pinned = torch.empty(1000, dtype=torch.float64, pin_memory=True).numpy()
+    pinned[:] = rng.normal(size=1000)
+    pageable = rng.normal(size=700)
+    empty = np.zeros(0)
+    d1 = torch.zeros(1000, dtype=torch.float64, device=dev)
+    d2 = torch.zeros(700, dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    issued = copy_batch([(d1.data_ptr(), pinned.ctypes.data, pinned.nbytes),
+                         (d2.data_ptr(), pageable.ctypes.data, pageable.nbytes),
+                         (d2.data_ptr(), empty.ctypes.data, 0)], st, require_pinned=True)
+    torch.cuda.synchronize()
+    assert issued.tolist() == [True, False, True]
+    assert np.array_equal(d1.cpu().numpy(), pinned)
+    assert not d2.any()
+    d3 = torch.empty(1000, dtype=torch.float64, device=dev)
+    issued = copy_batch([(d3.data_ptr(), d1.data_ptr(), 8 * 1000)], st, require_pinned=False)
+    torch.cuda.synchronize()
+    assert issued.tolist() == [True] and torch.equal(d3, d1)
