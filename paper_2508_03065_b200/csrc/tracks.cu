@@ -101,19 +101,42 @@ __global__ void k_coarse_bounds(const mvb_image* __restrict__ images, const int3
                                 const double* __restrict__ paths, double negsum,
                                 double* __restrict__ coarse, double* __restrict__ lb,
                                 double* __restrict__ ub) {
+    // The CTA's eight warps (images of one factor class, consecutive in
+    // `sel`, normally of one job) read the same coarse source path window:
+    // it is staged once per CTA in shared memory (the kernel is bound by the
+    // latency of these loads); a warp whose image has another path reads
+    // global memory.
+    __shared__ double sp[3 * 64 * (CB_SEGS + 2)];
     const int lane = threadIdx.x & 31;
-    const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t s0 = (int64_t)blockIdx.y * CB_SEGS;
+    const int64_t w0 = (int64_t)blockIdx.x * (blockDim.x >> 5);
+    int64_t r0 = 0, r1 = 0, ref_cpath = -1;
+    {
+        const mvb_image& ref = images[sel[w0]];  // w0 < n_sel by the grid
+        const int64_t Kr = ref.n_coarse, nsr = (Kr + 63) / 64;
+        if (s0 < nsr) {
+            const int64_t s1r = s0 + CB_SEGS < nsr ? s0 + CB_SEGS : nsr;
+            r0 = s0 > 0 ? 64 * (s0 - 1) : 0;
+            r1 = 64 * (s1r + 1) < Kr ? 64 * (s1r + 1) : Kr;
+            ref_cpath = ref.cpath;
+            const double* g = paths + 3 * ref.cpath + 3 * r0;
+            for (int64_t t = threadIdx.x; t < 3 * (r1 - r0); t += blockDim.x) sp[t] = g[t];
+        }
+    }
+    __syncthreads();
+    const int64_t w = w0 + (threadIdx.x >> 5);
     if (w >= n_sel) return;
     const int32_t i = sel[w];
     const mvb_image im = images[i];
     const int64_t K = im.n_coarse;
     const int64_t nseg = (K + 63) / 64;
-    const int64_t s0 = (int64_t)blockIdx.y * CB_SEGS;
     if (s0 >= nseg) return;
     const int64_t s1 = s0 + CB_SEGS < nseg ? s0 + CB_SEGS : nseg;
     const mvb_job& J = jobs[im.job];
-    const double* src = paths + 3 * im.cpath;
-    const double* mic = J.mic_moving ? src + 3 * K : paths + 3 * J.mic_off;
+    const bool staged = im.cpath == ref_cpath;  // same path rows, same K
+    const double* src = staged ? sp : paths + 3 * im.cpath;
+    const int64_t soff = staged ? r0 : 0;       // src row of coarse sample k: k - soff
+    const double* mic = J.mic_moving ? paths + 3 * (im.cpath + K) : paths + 3 * J.mic_off;
     const int64_t mstep = J.mic_moving ? 3 : 0;
     double* c = coarse + im.coarse;
     double vmax = 0.0;  // lane-local exact max of the written samples (lb)
@@ -126,7 +149,7 @@ __global__ void k_coarse_bounds(const mvb_image* __restrict__ images, const int3
         for (int h = 0; h < 2; ++h) {
             const int64_t k = 64 * s + 32 * h + lane;
             if (k < K) {
-                const double v = image_distance(im, src + 3 * k, mic + mstep * k);
+                const double v = image_distance(im, src + 3 * (k - soff), mic + mstep * k);
                 if (write) {
                     c[k] = v;
                     vmax = v > vmax ? v : vmax;
