@@ -473,6 +473,11 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
             cw[t] = c[a];
         }
         __syncthreads();
+        // the anchors c[k] of this thread's intervals, read before the
+        // epilogue reuses the staging area (and off the global-load path)
+        double anchor[COEF_KI];
+#pragma unroll
+        for (int q = 0; q < COEF_KI; ++q) anchor[q] = cw[e0 + q + 32 < COEF_SPAN + 65 ? e0 + q + 32 : 0];
         for (int t = threadIdx.x; t < COEF_SPAN + 64; t += blockDim.x)
             dw[skew32(t)] = (float)(cw[t + 1] - cw[t]);
         __syncthreads();
@@ -512,7 +517,7 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
         for (int q = 0; q < COEF_KI; ++q) {
             const int64_t k = k0 + e0 + q;
             if (k >= K) break;
-            const double g0 = c[k] + (double)acc[q][0].x;
+            const double g0 = anchor[q] + (double)acc[q][0].x;
             mvb_coef32 r;
             const double base = fma(kappa, g0, shift);
             const double B = floor(base);
