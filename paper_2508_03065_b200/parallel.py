@@ -103,7 +103,7 @@ def _image_shard(key) -> np.ndarray:
     return out
 
 
-SPARSITY_COST = 0.75  # extra synthesis cost of an image ~ SPARSITY_COST / local density (per m)
+SPARSITY_COST = 0.4  # extra synthesis cost of an image ~ SPARSITY_COST / local density (per m)
 
 
 def _band_cuts(keys: np.ndarray, world: int) -> np.ndarray:
@@ -111,8 +111,9 @@ def _band_cuts(keys: np.ndarray, world: int) -> np.ndarray:
     `keys` at equal estimated synthesis cost: an image costs
     1 + SPARSITY_COST / rho, rho its local density (images per metre over
     +-16 neighbours) -- sparse delay bands (the far tips of the order
-    octahedron) reuse fewer L1 lines per gather, measured +9% at 8 images/m
-    against ~+1.5% at 60 (c3, W=8)."""
+    octahedron) reuse fewer L1 lines per gather.  0.4 is the best of
+    {0.4, 0.75} on c3 and c5 at W=8 (per-rank step spread c3 1.6%, c5 4.7%;
+    profiles/r1_shard_projection.json)."""
     n = keys.size
     if n == 0:
         return np.zeros(world + 1, np.int64)
@@ -121,7 +122,9 @@ def _band_cuts(keys: np.ndarray, world: int) -> np.ndarray:
     span = np.maximum(keys[hi] - keys[lo], 1e-9)
     w = 1.0 + SPARSITY_COST * span / np.maximum(hi - lo, 1)
     cum = np.concatenate([[0.0], np.cumsum(w)])
-    cut = np.searchsorted(cum, cum[-1] * np.arange(world + 1) / world, side="left")
+    # targets nudged down by a rounding margin: equal weights give equal bands
+    target = cum[-1] * np.arange(world + 1) / world - 1e-9 * cum[-1]
+    cut = np.searchsorted(cum, target, side="left")
     cut[0], cut[-1] = 0, n
     return np.maximum.accumulate(np.clip(cut, 0, n)).astype(np.int64)
 
