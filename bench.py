@@ -256,14 +256,35 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = os.environ.get("MVB_DIST_BACKEND", "nccl")
+    if backend != "nccl":  # rehearsal: more ranks than GPUs share the devices
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # NCCL over NVLink; MVB_DIST_BACKEND=gloo rehearses the multi-rank path on
+    # fewer GPUs than ranks (collectives staged through host memory, no kernel
+    # waits on another rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
+
+    def allreduce_host(t, op):
+        """Timing / count reductions (after the timed bracket)."""
+        if backend == "nccl":
+            dist.all_reduce(t, op=op)
+            return t
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        return h.to(t.device)
 
     name = args.config
     w = workloads.WORKLOADS[name]
@@ -290,8 +311,7 @@ def run_ours(args):
         if plan is not None:
             res = plan.run(jobs)
             if shard is not None:  # on the plan's synthesis stream, after the render
-                with torch.cuda.stream(res.stream):
-                    parallel.reduce_to_root(res.out)
+                plan.reduce(res)
             return res
         tl = timing if record else None
         res = render_jobs(jobs, f, precision=precision, shard=shard, timing=tl,
@@ -351,10 +371,8 @@ def run_ours(args):
         kern_ms = [a.elapsed_time(b) for a, b in timing]
     t = torch.tensor([total_ms, float(updates), sum(kern_ms)], dtype=torch.float64, device=dev)
     if world > 1:
-        tmax = t.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tsum = t.clone()
-        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        tmax = allreduce_host(t.clone(), dist.ReduceOp.MAX)
+        tsum = allreduce_host(t.clone(), dist.ReduceOp.SUM)
         # every rank's updates count: image shards and scene shards split the
         # work, replicas each do all of it (value = N x one replica)
         total_ms_all, updates_all = float(tmax[0]), float(tsum[1])
@@ -407,7 +425,7 @@ def run_ours(args):
             e2e_upd = res.updates * args.steps
             h2d = s32.nbytes + traj.positions.nbytes + np.asarray(sc.mics[0]).nbytes
             e2e = {"value": e2e_upd / tt, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
-                   "d2h_bytes_per_step": int(y.size * 4), "api": "paper_2508_03065_b200.render",
+                   "d2h_bytes_per_step": int(y.nbytes), "api": "paper_2508_03065_b200.render",
                    "inputs": "pinned host memory (signal buffer; Trajectory positions are held "
                              "page-locked), copied to the device inside every timed call",
                    "ms_per_call": [round(c * 1e3, 3) for c in calls]}
@@ -446,8 +464,7 @@ def run_ours(args):
             for _ in range(max(4, args.warmup)):  # captures both slots, then replays
                 r = plan_e.run(host_jobs)
                 if shard is not None:
-                    with torch.cuda.stream(r.stream):
-                        parallel.reduce_to_root(r.out)
+                    plan_e.reduce(r)
                 if shard is None or rank == 0:
                     r.host()
             for _ in range(args.steps):
@@ -456,8 +473,7 @@ def run_ours(args):
                 t0 = time.perf_counter()
                 r = plan_e.run(host_jobs)
                 if shard is not None:
-                    with torch.cuda.stream(r.stream):
-                        parallel.reduce_to_root(r.out)
+                    plan_e.reduce(r)
                 out_h = r.host() if (shard is None or rank == 0) else None
                 torch.cuda.synchronize()
                 barrier()
@@ -466,9 +482,8 @@ def run_ours(args):
                 d2h = 0 if out_h is None else out_h.nbytes
             tt_t = torch.tensor([tt, float(upd)], dtype=torch.float64, device=dev)
             if world > 1:
-                tmax = tt_t.clone()
-                dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-                dist.all_reduce(tt_t, op=dist.ReduceOp.SUM)
+                tmax = allreduce_host(tt_t.clone(), dist.ReduceOp.MAX)
+                tt_t = allreduce_host(tt_t, dist.ReduceOp.SUM)
                 tt, upd = float(tmax[0]), float(tt_t[1])
             e2e = {"value": upd / tt, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
                    "d2h_bytes_per_step": int(d2h),

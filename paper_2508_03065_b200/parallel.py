@@ -141,11 +141,38 @@ def shard_jobs(jobs, rank: int, world: int) -> list:
                     path_key=engine._key(jb.path_key, jb.pos)) for jb in jobs]
 
 
+# Every collective this process issued, in order: (name, elements).  The
+# ranks of a sharded render must issue the same sequence (a rank that skips
+# or adds one hangs the group); tests compare the logs across ranks.
+COLLECTIVE_LOG: list = []
+
+
+def _group_size(group):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group)
+    return 1
+
+
+def _host_staged(group) -> bool:
+    """gloo groups run their collectives on host tensors: device buffers
+    are copied through the host (the CPU test harness and the one-GPU
+    multi-process rehearsal; NCCL reduces device buffers in place)."""
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
 def allreduce_max(t, group=None):
     """In-place MAX over the ranks (no-op without a process group)."""
     import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    if _group_size(group) > 1:
+        COLLECTIVE_LOG.append(("all_reduce_max", int(t.numel())))
+        if t.is_cuda and _host_staged(group):
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return t
 
 
@@ -174,8 +201,16 @@ def shard_mode(workload: str, world: int) -> str:
 
 
 def reduce_to_root(t, group=None, root: int = 0):
-    """Sum a partial output buffer into `root` (in place on root)."""
+    """Sum a partial output buffer into `root` (in place on root), on the
+    current stream."""
     import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.reduce(t, dst=root, op=dist.ReduceOp.SUM, group=group)
+    if _group_size(group) > 1:
+        COLLECTIVE_LOG.append(("reduce_sum", int(t.numel())))
+        if t.is_cuda and _host_staged(group):
+            h = t.cpu()
+            dist.reduce(h, dst=root, op=dist.ReduceOp.SUM, group=group)
+            if dist.get_rank(group) == root:
+                t.copy_(h)
+        else:
+            dist.reduce(t, dst=root, op=dist.ReduceOp.SUM, group=group)
     return t

@@ -293,6 +293,25 @@ class RenderPlan:
             slot.done = torch.cuda.Event()
             slot.done.record()
 
+    def reduce(self, res: engine.RenderResult, group=None, root: int = 0) -> engine.RenderResult:
+        """Image shards: sum the ranks' partial outputs of `res` (this plan's
+        latest run) into `root` (parallel.reduce_to_root), on the synthesis
+        stream after the render.  The slot's completion event is re-recorded
+        after the collective, so `res.wait()` / `host()` / `join()` and the
+        slot's next reuse (its geometry graph zero-fills the same static
+        output) are all ordered after the reduction, not only the render."""
+        from . import parallel
+        slot = self.slots[(self.k - 1) % self.DEPTH]
+        if res.done is not slot.done:
+            raise ValueError("reduce() takes the result of the plan's latest run")
+        with torch.cuda.stream(self.syn_stream):
+            self.syn_stream.wait_event(slot.done)
+            parallel.reduce_to_root(res.out, group=group, root=root)
+            ev = torch.cuda.Event()
+            ev.record()
+        slot.done = res.done = ev
+        return res
+
     def run(self, jobs) -> engine.RenderResult:
         """Render `jobs` (same structure as the plan's template)."""
         if self.shard is not None and int(self.shard[1]) > 1:

@@ -608,6 +608,19 @@ def _memory_groups(jobs, budget: int, fd_taps: int) -> list:
     return groups
 
 
+def shard_batches(jobs, shard, budget: int, fd_taps: int) -> tuple:
+    """(sub-batch groups, the jobs this rank renders).  The groups are cut
+    from the UNSHARDED jobs: a shard's footprint is rank-specific (delay
+    bands equalise cost, not image count), so groups cut after sharding
+    could differ between ranks and mismatch their collectives (every group
+    all-reduces its track maxima)."""
+    groups = _memory_groups(jobs, budget, fd_taps)
+    if shard is not None and int(shard[1]) > 1:
+        from . import parallel
+        jobs = parallel.shard_jobs(jobs, int(shard[0]), int(shard[1]))
+    return groups, jobs
+
+
 def render_jobs(jobs, f, precision="fp32", shard=None, signals=None, timing=None,
                 inputs_ready=None, dmax_hook=None, max_batch_bytes=None):
     """Geometry + render of a job batch; returns engine.RenderResult
@@ -622,21 +635,20 @@ def render_jobs(jobs, f, precision="fp32", shard=None, signals=None, timing=None
     full render.  Batches whose estimated device footprint exceeds
     `max_batch_bytes` (default: 40% of the GPU's memory, identical on every
     rank) render as consecutive sub-batches, results concatenated."""
+    if max_batch_bytes is None:
+        from ._dev import require_cuda
+        dev = require_cuda()
+        max_batch_bytes = int(0.4 * torch.cuda.get_device_properties(dev).total_memory)
+    groups, jobs = shard_batches(jobs, shard, int(max_batch_bytes), int(as_filter(f).branch_len))
     if shard is not None and int(shard[1]) > 1:
         if precision == "fp64":
             raise ValueError("the exact fp64 engine runs replicas only (its summation order "
                              "spans all images)")
         from . import parallel
-        jobs = parallel.shard_jobs(jobs, int(shard[0]), int(shard[1]))
         if dmax_hook is None:
             dmax_hook = parallel.allreduce_max
     sig = signals if signals is not None else [jb.s for jb in jobs]
     keys = [engine._key(jb.signal_key, jb.s) for jb in jobs]
-    if max_batch_bytes is None:
-        from ._dev import require_cuda
-        dev = require_cuda()
-        max_batch_bytes = int(0.4 * torch.cuda.get_device_properties(dev).total_memory)
-    groups = _memory_groups(jobs, int(max_batch_bytes), int(as_filter(f).branch_len))
     parts = []
     for g in groups:
         sub = [jobs[j] for j in g]

@@ -136,10 +136,12 @@ def _dry(rng, n, dtype):
 
 def make_scenes(name: str, duration: float | None = None, max_order: int | None = None,
                 n_scenes: int | None = None, n_channels: int | None = None,
-                tiers: tuple | None = None) -> list:
+                tiers: tuple | None = None, seed: int | None = None) -> list:
     """Build the seeded scenes of a config; optional overrides give the
-    reduced-size parity cases (same generators, same seeds)."""
+    reduced-size parity cases (same generators, same seeds unless `seed`)."""
     w = WORKLOADS[name]
+    if seed is not None:
+        w = replace(w, seed=int(seed))
     if duration is not None:
         w = replace(w, duration=duration)
     if max_order is not None:

@@ -127,3 +127,21 @@ def test_image_shards_reduce_to_full_render_gloo():
     full = _scene().render()
     assert got.shape == full.shape
     assert np.max(np.abs(got - full)) <= 1e-12 * np.max(np.abs(full))
+
+
+def test_shard_batches_groups_are_rank_independent():
+    """Sub-batch groups come from the unsharded jobs: with a
+    budget that splits the batch, every rank gets the same groups even
+    though the shards' own footprints differ."""
+    from paper_2508_03065_b200 import workloads
+    from paper_2508_03065_b200.synth import job_footprint, scene_jobs, shard_batches
+    scenes = workloads.make_scenes("c5", duration=0.2, max_order=9, n_channels=4,
+                                   tiers=((2, 1), (5, 32), (9, 256)))
+    jobs = scene_jobs(scenes)
+    budget = int(2.5 * job_footprint(jobs[0], 64))
+    out = [shard_batches(jobs, (r, 3), budget, 64) for r in range(3)]
+    assert all(g == out[0][0] for g, _ in out)
+    assert sorted(j for g in out[0][0] for j in g) == list(range(len(jobs)))
+    assert len(out[0][0]) > 1
+    foot = [[job_footprint(jb, 64) for jb in sj] for _, sj in out]
+    assert foot[0] != foot[1]  # the shards' own footprints are rank-specific
