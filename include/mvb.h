@@ -210,8 +210,9 @@ int mvb_coarse_distances(const mvb_image* d_images, const int32_t* d_sel, int64_
 
 /* Axis-aligned bounding boxes of every job's source path and receiver:
  * d_rows (n_jobs, 4) int64 = (source first row, T, receiver first row,
- * receiver moving); d_bbox: n_jobs x 65 x 12 doubles, the first n_jobs x 12
- * being (src lo xyz, src hi xyz, mic lo xyz, mic hi xyz), the rest scratch. */
+ * receiver moving); d_bbox: n_jobs x 65 x 16 doubles, the first n_jobs x 16
+ * being (src lo xyz, src hi xyz, mic lo xyz, mic hi xyz, src max step, mic
+ * max step, 0, 0) -- a step is |p[t+1] - p[t]| in metres -- the rest scratch. */
 int mvb_path_bbox(const int64_t* d_rows, int64_t n_jobs, const double* d_paths, double* d_bbox,
                   void* stream);
 

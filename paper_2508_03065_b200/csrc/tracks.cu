@@ -185,11 +185,14 @@ __global__ void k_coarse_bounds(const mvb_image* __restrict__ images, const int3
 }
 
 // Axis-aligned bounding boxes of every job's source path and receiver
-// (moving or fixed): bbox[j] = (src lo xyz, src hi xyz, mic lo xyz, mic hi
-// xyz).  BBOX_PARTS blocks per job reduce row ranges in one pass over all
-// three axes (partials after the n_jobs final boxes), k_bbox_reduce folds them.
+// (moving or fixed) and their largest per-sample step:
+// bbox[j] = (src lo xyz, src hi xyz, mic lo xyz, mic hi xyz, src max step,
+// mic max step, 0, 0) -- the steps bound the delay excursion of a coarse
+// interval (the fp32 fast path's accuracy envelope, engine.Geometry).
+// BBOX_PARTS blocks per job reduce row ranges in one pass over all three
+// axes (partials after the n_jobs final boxes), k_bbox_reduce folds them.
 constexpr int BBOX_PARTS = 64;
-constexpr int BBOX_WORDS = 12;
+constexpr int BBOX_WORDS = 16;
 
 __device__ __forceinline__ double block_min(double v, double* red) { return -block_max(-v, red); }
 
@@ -203,14 +206,21 @@ __global__ void k_path_bbox(const int64_t* __restrict__ rows, const double* __re
         const double* P = paths + 3 * (which == 0 ? R[0] : R[2]);
         const int64_t n = which == 0 || R[3] ? R[1] : 1;
         double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+        double step = 0.0;
         for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
              t += (int64_t)gridDim.x * blockDim.x) {
+            double d2 = 0.0;
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const double v = P[3 * t + a];
                 lo[a] = fmin(lo[a], v);
                 hi[a] = fmax(hi[a], v);
+                if (t + 1 < n) {
+                    const double dv = P[3 * t + 3 + a] - v;
+                    d2 += dv * dv;
+                }
             }
+            step = fmax(step, d2);
         }
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
@@ -220,7 +230,10 @@ __global__ void k_path_bbox(const int64_t* __restrict__ rows, const double* __re
                 part[6 * which + 3 + a] = h;
             }
         }
+        step = block_max(step, red);
+        if (threadIdx.x == 0) part[12 + which] = sqrt(step) * (1.0 + 1e-12);
     }
+    if (threadIdx.x == 0) part[14] = part[15] = 0.0;
 }
 
 __global__ void k_bbox_reduce(int64_t n_jobs, double* __restrict__ bbox) {
@@ -228,7 +241,7 @@ __global__ void k_bbox_reduce(int64_t n_jobs, double* __restrict__ bbox) {
     if (j >= n_jobs) return;
     const double* part = bbox + BBOX_WORDS * (n_jobs + j * BBOX_PARTS);
     for (int w = 0; w < BBOX_WORDS; ++w) {
-        const bool is_lo = (w % 6) < 3;
+        const bool is_lo = w < 12 && (w % 6) < 3;
         double v = part[w];
         for (int q = 1; q < BBOX_PARTS; ++q)
             v = is_lo ? fmin(v, part[BBOX_WORDS * q + w]) : fmax(v, part[BBOX_WORDS * q + w]);
@@ -253,7 +266,7 @@ __global__ void k_bounds_full(const mvb_image* __restrict__ images, const int32_
     const int64_t ts[3] = {0, (J.T - 1) / 2, J.T - 1};
     for (int k = 0; k < 3; ++k)
         best = fmax(best, image_distance(im, paths + 3 * (J.pos_off + ts[k]), mic_row(J, paths, ts[k])));
-    const double* b = bbox + 12 * im.job;
+    const double* b = bbox + BBOX_WORDS * im.job;
     double sq = 0.0;
     for (int a = 0; a < 3; ++a) {
         // image coordinate off + sign * p over p in [lo, hi]

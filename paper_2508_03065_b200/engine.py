@@ -66,6 +66,12 @@ SYNTH_U = 16  # steps per lane (mvb_synthesize_f32 u_steps)
 TILE = 32 * SYNTH_U  # output samples per CTA
 SEG_LEN = 32 * TILE  # samples per delay-sort segment
 IMG_COLS, JOB_COLS, WORK_COLS = 12, 17, 4
+BOX_WORDS = 16  # mvb_path_bbox record: boxes (12), max steps (2), pad (2)
+# fp32 fast-path accuracy envelope: the largest delay excursion (samples) of
+# one coarse interval that the fp32 residual of the interval records may
+# carry; beyond it the render routes to the exact fp64 engine
+# (Geometry.fast_path_ok)
+FP32_ENVELOPE = float(os.environ.get("MVB_FP32_ENVELOPE", "48"))
 PAD_MARGIN = 64
 FOUR_PI = 4.0 * np.pi
 
@@ -335,15 +341,15 @@ class Geometry:
             if batch:
                 copy_batch(batch, side.cuda_stream, require_pinned=False)
             box_rows = h2d(np.stack([self.pos_off, self.T, self.mic_off, self.moving], axis=1), dev)
-            # flat: the nJ x 12 boxes first, then the 64 partial boxes per job
-            if bbox is not None and bbox.numel() >= nJ * 65 * 12:
+            # flat: the nJ x BOX_WORDS boxes first, then the 64 partial boxes per job
+            if bbox is not None and bbox.numel() >= nJ * 65 * BOX_WORDS:
                 self.bbox = bbox
             else:
-                self.bbox = torch.empty(nJ * 65 * 12, dtype=torch.float64, device=dev)
+                self.bbox = torch.empty(nJ * 65 * BOX_WORDS, dtype=torch.float64, device=dev)
             _lib.call("mvb_path_bbox", ptr(box_rows), nJ, ptr(self.paths), ptr(self.bbox),
                       stream_handle(dev))
-            box_host = pinned_scratch("bbox", nJ * 12, torch.float64).view(nJ, 12)
-            box_host.copy_(self.bbox[:nJ * 12].view(nJ, 12), non_blocking=True)
+            box_host = pinned_scratch("bbox", nJ * BOX_WORDS, torch.float64).view(nJ, BOX_WORDS)
+            box_host.copy_(self.bbox[:nJ * BOX_WORDS].view(nJ, BOX_WORDS), non_blocking=True)
             box_ready = torch.cuda.Event()
             box_ready.record()
             self.paths_ready = box_ready  # the paths' full-rate rows are on the device
@@ -643,6 +649,28 @@ class Geometry:
         d_ub = (1.02 * math.sqrt(d2) * (1.0 + neg) + 0.01) * (1.0 + self.length_slack)
         return int(math.ceil(float(jb.rate) * d_ub / float(jb.c)))
 
+    def interval_excursion(self) -> np.ndarray:
+        """Per job: an upper bound (samples) of the delay excursion over one
+        coarse interval of its largest decimation factor N, kappa * (largest
+        source step + largest receiver step) * N (triangle inequality: an
+        image path moves like the source).  The fast path carries the delay
+        inside an interval as an fp32 residual around the fp64 anchor, so
+        its rounding grows with this span."""
+        out = np.zeros(len(self.jobs))
+        for j, jb in enumerate(self.jobs):
+            n_max = max((int(N) for _, N in jb.tiers if int(N) > 1), default=0)
+            if n_max:
+                step = float(self.bbox_host[j, 12])
+                if self.moving[j]:
+                    step += float(self.bbox_host[j, 13])
+                out[j] = float(jb.rate) / float(jb.c) * step * n_max
+        return out
+
+    @property
+    def fast_path_ok(self) -> bool:
+        """Every job inside the fp32 fast path's envelope (FP32_ENVELOPE)."""
+        return bool(np.all(self.interval_excursion() <= FP32_ENVELOPE))
+
     def tau_max(self, j: int) -> float:
         jb = self.jobs[j]
         return float(jb.rate) * float(self.dmax[j]) / float(jb.c)
@@ -735,6 +763,7 @@ class RenderResult:
         self._dev = (lengths_dev, err_dev)  # read on first use (no per-render pinned buffers)
         self.done = done
         self.stream = stream
+        self.precision = "fp64" if out.dtype == torch.float64 else "fp32"  # engine that rendered it
 
     def wait(self) -> "RenderResult":
         """Order the current stream after the render (no host wait)."""
@@ -846,6 +875,11 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     L, d0 = int(f.branch_len), int(f.nominal_delay)
     if precision not in ("fp32", "fp64"):
         raise ValueError("precision must be 'fp32' or 'fp64'")
+    if precision == "fp32" and not geom.fast_path_ok:
+        # delay excursions beyond the fp32 residual's envelope (sources or
+        # receivers moving at hundreds of m/s under a large decimation):
+        # the exact fp64 engine renders the batch instead
+        precision = "fp64"
     sm_count = _sm_count(dev.index if dev.index is not None else torch.cuda.current_device())
     # signals: dedupe, upload
     keys = signal_keys or [_key(jobs[j].signal_key, signals[j]) for j in range(nJ)]
@@ -924,7 +958,9 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
                       ptr(geom.images), ptr(geom.coarse), ptr(geom.tables), ptr(streams),
                       ptr(geom.paths), ptr(out), st)
             _events_end(timing, ev)
-            return RenderResult(out, offsets, out_len, geom.n_img.copy(), 0, lengths, err)
+            res = RenderResult(out, offsets, out_len, geom.n_img.copy(), 0, lengths, err)
+            res.precision = "fp64"
+            return res
         return PreparedRender(launch64, launches0)
 
     # ---------------------------------------------------------------- fast --
@@ -979,7 +1015,9 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
             _lib.call("mvb_reduce_partials_f32", ptr(jobs_dev), nJ, int(out_len.max()),
                       ptr(part), ptr(out), st)
         _mark("render.synth_launched")
-        return RenderResult(out, offsets, out_len, geom.n_img.astype(np.int64), 0, lengths, err)
+        res = RenderResult(out, offsets, out_len, geom.n_img.astype(np.int64), 0, lengths, err)
+        res.precision = "fp32"
+        return res
     return PreparedRender(launch32, launches0)
 
 

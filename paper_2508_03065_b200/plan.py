@@ -273,9 +273,19 @@ class RenderPlan:
         slot.dmax = geom.dmax_dev
         slot.graph_launches = _lib.launch_count() - launches0  # kernels replayed per run
         slot.graph, slot.result, slot.uploads = g_geo, res, uploads
-        slot.decision = geom.lowpass_decision()
+        slot.decision = self._decision(geom)
         slot.capacity = np.asarray([geom.length_bound(j) for j in range(len(slot.jobs))])  # slacked
         self.captures += 1
+
+    def _decision(self, geom) -> tuple:
+        """Data-dependent choices a captured slot is valid for: the low-pass
+        decision and whether the fp32 fast path's envelope holds (else the
+        capture renders on the exact engine, engine.prepare_render)."""
+        ok = self.precision == "fp64" or geom.fast_path_ok
+        if not ok and self.shard is not None and int(self.shard[1]) > 1:
+            raise ValueError("delay excursions beyond the fp32 envelope: image shards need the "
+                             "fp32 fast path (render replicas on the exact engine instead)")
+        return (geom.lowpass_decision(), ok)
 
     def _replay(self, slot, after):
         """Replay the slot's graphs on the plan streams after event `after`."""
@@ -346,7 +356,7 @@ class RenderPlan:
         if spec:
             geom.collect()
         bound = np.asarray([geom.length_bound(j) for j in range(len(slot.jobs))])
-        if not spec or geom.lowpass_decision() != slot.decision \
+        if not spec or self._decision(geom) != slot.decision \
                 or np.any(bound > slot.capacity):
             if spec:
                 self.misses += 1

@@ -1,8 +1,8 @@
 """Randomised parity (hypothesis): random rooms, reflection coefficients,
 image orders, tier tables (including non-power-of-two factors), path and
 signal lengths, fixed or moving receivers and filter lengths, each rendered
-by both engines and compared with the CPU oracle.  Source speeds are capped
-at 20 m/s (physical sources; see the fp32 error note in DESIGN.md).
+by both engines and compared with the CPU oracle.  Source speeds reach
+600 m/s: beyond the fp32 envelope the fast engine routes to the exact one.
 Marker `gpu`."""
 
 import numpy as np
@@ -42,14 +42,16 @@ def scenes(draw):
     t = np.linspace(0, 1, T)[:, None]
     pos = way[0] + (way[1] - way[0]) * t + 0.2 * np.sin(2 * np.pi * 3 * t) * (way[2] - way[0]) / 4
     pos = np.clip(pos, lo, hi)
-    # physical speeds (<= 20 m/s): the fast path stores each interval's delay
-    # as an fp32 residual, whose rounding grows with the delay excursion per
-    # interval (~ rate/c * speed * N / rate samples), so its 1e-5 bar is a
-    # statement about moving sources, not about supersonic ones
+    # source speeds up to 600 m/s (Mach 1.7): the fast path carries each
+    # interval's delay as an fp32 residual whose rounding grows with the delay
+    # excursion per interval (rate/c * speed * N / rate samples); renders
+    # beyond engine.FP32_ENVELOPE route to the exact engine, so the 1e-5 bar
+    # holds at any speed
+    vmax = draw(st.sampled_from([5.0, 20.0, 100.0, 340.0, 600.0]))
     if T > 1:
         v = np.max(np.linalg.norm(np.diff(pos, axis=0), axis=1)) * rate
-        if v > 20.0:
-            pos = pos[0] + (pos - pos[0]) * (20.0 / v)
+        if v > 0:
+            pos = pos[0] + (pos - pos[0]) * (vmax / v)
     moving = draw(st.booleans()) and T > 1
     mic = (rng.uniform(lo, hi) + 0.05 * np.sin(2 * np.pi * t) * np.array([1.0, -0.5, 0.2])
            if moving else rng.uniform(lo, hi))
@@ -98,7 +100,8 @@ def test_random_scenes_both_engines(sc):
         job = engine.Job(s=x, pos=sc["pos"], mic=sc["mic"], dims=sc["dims"], walls=sc["walls"],
                          max_order=sc["max_order"], tiers=sc["tiers"], rate=sc["rate"],
                          image_index=sc["sub"])
-        y = render_jobs([job], f, precision=precision).job(0).double().cpu().numpy()
+        res = render_jobs([job], f, precision=precision)
+        y = res.job(0).double().cpu().numpy()
         ref = _oracle(sc, f, np.asarray(x, np.float64))
         assert y.size == ref.size, (precision, sc["tiers"], y.size, ref.size)
         assert rel_err(y, ref) <= tol, (precision, sc["tiers"], sc["max_order"], sc["L"])
