@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the cpu_baseline / reference sample")
+    ap.add_argument("--no-per-config", action="store_true",
+                    help="headline config only (no per_config block)")
+    ap.add_argument("--per-config-steps", type=int, default=10,
+                    help="timed steps of each per_config entry (capped by --steps)")
     ap.add_argument("--profile", action="store_true",
                     help="ncu mode: warmup+steps renders only, no probes/e2e/cpu")
     return ap.parse_args()
@@ -89,27 +93,34 @@ class ClockSampler:
         except OSError:
             self.proc = None
 
-    def stop(self, t0=None, t1=None):
-        """Summary of the samples within [t0, t1] (host wall-clock seconds)."""
+    def stop(self):
+        """Stop sampling and parse the samples (timestamp, sm, max, reasons)."""
         import datetime
+        self.rows = []
         if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return
         time.sleep(0.15)
         self.proc.terminate()
         self.proc.wait()
         self.file.flush()
         self.file.seek(0)
-        rows = []
         for line in self.file.read().splitlines():
             f = [x.strip() for x in line.split(",")]
             if len(f) < 10:
                 continue
             try:
                 ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
-                rows.append((ts, float(f[2]), float(f[3]), f[6:10]))
+                self.rows.append((ts, float(f[2]), float(f[3]), f[6:10]))
             except ValueError:
                 continue
         os.unlink(self.file.name)
+
+    def window(self, t0=None, t1=None):
+        """Summary of the samples within [t0, t1] (host wall-clock seconds);
+        call after stop()."""
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = self.rows
         sel = rows
         if t0 is not None and rows:
             inside = [r for r in rows if t0 <= r[0] <= t1]
@@ -209,17 +220,19 @@ def cpu_sample(name, target_s, nthreads):
 
 
 def measured_peaks(dev):
-    """FP32 FFMA TFLOP/s and L1-hit load GB/s on this GPU (CUDA events)."""
+    """FP32 FFMA / FP64 DFMA TFLOP/s and L1-hit load GB/s on this GPU (CUDA
+    events, best of 3)."""
     import torch
     from paper_2508_03065_b200 import _lib
     from paper_2508_03065_b200._dev import ptr, stream_handle
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    sink = torch.zeros(sms * 64, dtype=torch.float32, device=dev)
+    sink = torch.zeros(sms * 64, dtype=torch.float64, device=dev)
     buf = torch.randn(64 * 16 * 1024 // 4, dtype=torch.float32, device=dev)
     st = stream_handle(dev)
     out = {}
     for name, blocks, iters, work in (
             ("ffma", sms * 8, 4000, lambda b, it: b * 256 * it * 128 * 2),
+            ("dfma", sms * 8, 500, lambda b, it: b * 256 * it * 128 * 2),
             ("l1", sms * 8, 4000, lambda b, it: b * 256 * it * 4 * 16)):
         best = 0.0
         for _ in range(3):
@@ -227,16 +240,20 @@ def measured_peaks(dev):
             e0.record()
             if name == "ffma":
                 _lib.call("mvb_peak_ffma", blocks, iters, ptr(sink), st)
+            elif name == "dfma":
+                _lib.call("mvb_peak_dfma", blocks, iters, ptr(sink), st)
             else:
                 _lib.call("mvb_peak_l1", blocks, iters, ptr(buf), ptr(sink), st)
             e1.record()
             torch.cuda.synchronize()
             best = max(best, work(blocks, iters) / (e0.elapsed_time(e1) * 1e-3))
         out[name] = best
-    return out["ffma"] / 1e12, out["l1"] / 1e9
+    return {"ffma_tf": out["ffma"] / 1e12, "dfma_tf": out["dfma"] / 1e12, "l1_gbs": out["l1"] / 1e9}
 
 
 def load_traffic(name):
+    """DRAM bytes per synthesis launch from the committed ncu --set full
+    summary of this config (profiles/ncu_synth_<name>.json), or None."""
     p = os.path.join(ROOT, "profiles", f"ncu_synth_{name}.json")
     if os.path.exists(p):
         try:
@@ -246,53 +263,73 @@ def load_traffic(name):
     return None
 
 
-def run_ours(args):
-    import torch
-    import torch.distributed as dist
-    from paper_2508_03065_b200 import (Room, SynthesisConfig, Trajectory, hann_sinc, parallel,
-                                       render, workloads)
-    from paper_2508_03065_b200.synth import render_jobs
+class Ctx:
+    """Per-process distributed plumbing of a bench run."""
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    backend = os.environ.get("MVB_DIST_BACKEND", "nccl")
-    if backend != "nccl":  # rehearsal: more ranks than GPUs share the devices
-        local %= torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    # NCCL over NVLink; MVB_DIST_BACKEND=gloo rehearses the multi-rank path on
-    # fewer GPUs than ranks (collectives staged through host memory, no kernel
-    # waits on another rank)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        # NCCL over NVLink; MVB_DIST_BACKEND=gloo rehearses the multi-rank
+        # path on fewer GPUs than ranks (collectives staged through host
+        # memory, no kernel waits on another rank)
+        self.backend = os.environ.get("MVB_DIST_BACKEND", "nccl")
+        if self.backend != "nccl":
+            local %= torch.cuda.device_count()
+        self.local = local
+        torch.cuda.set_device(local)
+        self.dev = torch.device("cuda", local)
+        if self.world > 1:
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=self.dev)
+            else:
+                dist.init_process_group(self.backend)
 
-    def barrier():
-        if world > 1:
-            if backend == "nccl":
-                dist.barrier(device_ids=[local])
+    def barrier(self):
+        import torch.distributed as dist
+        if self.world > 1:
+            if self.backend == "nccl":
+                dist.barrier(device_ids=[self.local])
             else:
                 dist.barrier()
 
-    def allreduce_host(t, op):
-        """Timing / count reductions (after the timed bracket)."""
-        if backend == "nccl":
+    def allreduce(self, t, op):
+        """Timing / count reductions (outside the timed brackets)."""
+        import torch.distributed as dist
+        if self.world == 1:
+            return t
+        if self.backend == "nccl":
             dist.all_reduce(t, op=op)
             return t
         h = t.cpu()
         dist.all_reduce(h, op=op)
         return h.to(t.device)
 
-    name = args.config
+
+def measure(ctx, name, steps, warmup, peaks, args, precision=None, with_e2e=True):
+    """One config: K timed render steps (value, kernel time, roofline) and
+    the end-to-end public-API number.  Returns (line dict, clock window)."""
+    import gc
+
+    import torch
+    import torch.distributed as dist
+    from paper_2508_03065_b200 import (Room, SynthesisConfig, Trajectory, hann_sinc, parallel,
+                                       render, workloads)
+    from paper_2508_03065_b200.synth import render_jobs, release_plans
+
+    world, rank, dev = ctx.world, ctx.rank, ctx.dev
     w = workloads.WORKLOADS[name]
     scenes, mine, shard, mode = build_workload(name, rank, world)
     f = hann_sinc(w.fd_taps, 14)
     jobs = device_jobs(mine, dev)
     timing = []
-    precision = "fp64" if w.dtype == "f64" else "fp32"  # c1 is an fp64 config
+    if precision is None:
+        precision = "fp64" if w.dtype == "f64" else "fp32"  # c1 is an fp64 config
+    if precision == "fp64" and shard is not None:  # the exact engine runs replicas only
+        shard, mode = None, f"replicas x{world} (exact engine)"
+        scenes, mine = scenes, scenes
 
     # the device inputs are final from here on: planning of step k+1 may
     # overlap step k's kernels (render_jobs inputs_ready)
@@ -320,37 +357,29 @@ def run_ours(args):
             parallel.reduce_to_root(res.out)
         return res
 
-    if not args.profile:
-        ffma_tf, l1_gbs = measured_peaks(dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    clocks = ClockSampler(local)
-    if not args.profile:
-        clocks.start()
-        time.sleep(0.3)  # let nvidia-smi start before the warm-up
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         res = step()
     torch.cuda.synchronize()
-    barrier()
+    ctx.barrier()
     if args.profile:
-        for _ in range(args.steps):
+        for _ in range(steps):
             step()
         torch.cuda.synchronize()
-        return
-    total_ms = 0.0
-    updates = 0
+        return None, None
     launches = 0
     timing.clear()
     # K steps back to back, bracketed once by barrier + synchronize; an L2
     # flush (256 MiB write) is queued before every step and stays inside the
     # timed region (conservative)
     torch.cuda.synchronize()
-    barrier()
+    ctx.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     first_run = plan.k if plan is not None else 0
     wall0 = time.time()
     e0.record()
     results = []
-    for k in range(args.steps):
+    for k in range(steps):
         flush.fill_(float(k))
         res = step(record=True)
         results.append(res)  # lengths / update counts are read after the bracket
@@ -359,31 +388,31 @@ def run_ours(args):
         plan.join()  # the plan renders on its own streams: order e1 after them
     e1.record()
     torch.cuda.synchronize()
-    barrier()
+    ctx.barrier()
     wall1 = time.time()
     total_ms = e0.elapsed_time(e1)
     updates = sum(r.updates for r in results)
-    clk = clocks.stop(wall0, wall1)
     if plan is not None:  # synthesis time of every timed replay
         km = plan.flush_timing()
-        kern_ms = [km[i] for i in range(first_run, first_run + args.steps) if i in km]
+        kern_ms = [km[i] for i in range(first_run, first_run + steps) if i in km]
     else:
         kern_ms = [a.elapsed_time(b) for a, b in timing]
+    rendered = sorted({r.precision for r in results})
     t = torch.tensor([total_ms, float(updates), sum(kern_ms)], dtype=torch.float64, device=dev)
     if world > 1:
-        tmax = allreduce_host(t.clone(), dist.ReduceOp.MAX)
-        tsum = allreduce_host(t.clone(), dist.ReduceOp.SUM)
+        tmax = ctx.allreduce(t.clone(), dist.ReduceOp.MAX)
+        tsum = ctx.allreduce(t.clone(), dist.ReduceOp.SUM)
         # every rank's updates count: image shards and scene shards split the
         # work, replicas each do all of it (value = N x one replica)
         total_ms_all, updates_all = float(tmax[0]), float(tsum[1])
     else:
         total_ms_all, updates_all = total_ms, float(updates)
     value = updates_all / (total_ms_all * 1e-3)
-    ms_step = total_ms_all / args.steps
+    ms_step = total_ms_all / steps
     audio_s = sum(sc.T / sc.rate * len(sc.mics) for sc in scenes)
-    if name in ("c1", "c2") and world > 1:
+    if mode.startswith("replicas") and world > 1:
         audio_s *= world
-    rtf = audio_s * args.steps / (total_ms_all * 1e-3)
+    rtf = audio_s * steps / (total_ms_all * 1e-3)
 
     # ---- end to end through the public API with host buffers ----------------
     # the value loop's plan (its two graph pools) is released first: batch
@@ -391,13 +420,11 @@ def run_ours(args):
     _ = res.lengths, res.updates  # what the roofline reads later
     results.clear()
     used_plan = plan is not None
-    if plan is not None:
-        plan = None
-        import gc
-        gc.collect()
-        torch.cuda.empty_cache()
+    plan = None
+    gc.collect()
+    torch.cuda.empty_cache()
     e2e = None
-    if not args.no_e2e:
+    if with_e2e and not args.no_e2e:
         if world == 1 and len(scenes) == 1 and len(scenes[0].mics) == 1:
             sc = scenes[0]
             room = Room(dims=sc.dims, wall_reflection=sc.walls)
@@ -406,34 +433,38 @@ def run_ours(args):
                                   precision=precision)
             # inputs in pinned host memory (the e2e contract): the dry signal in a
             # page-locked buffer, the path in the Trajectory's own pinned copy
-            s32 = torch.empty(sc.s.shape, dtype=torch.from_numpy(np.asarray(sc.s)).dtype,
-                              pin_memory=True).numpy()
-            np.copyto(s32, sc.s)
+            sx = torch.empty(sc.s.shape, dtype=torch.from_numpy(np.asarray(sc.s)).dtype,
+                             pin_memory=True).numpy()
+            np.copyto(sx, sc.s)
             # warm: render() caches a plan on a repeat, captures one slot per call
             # and replays speculatively from the next call on (one-time costs)
-            for _ in range(max(5, args.warmup)):
-                y = render(s32, traj, room, sc.mics[0], f, cfg)
+            for _ in range(max(5, warmup)):
+                y = render(sx, traj, room, sc.mics[0], f, cfg)
             tt = 0.0
             calls = []
-            for _ in range(args.steps):
+            for _ in range(steps):
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
-                y = render(s32, traj, room, sc.mics[0], f, cfg)
+                y = render(sx, traj, room, sc.mics[0], f, cfg)
                 torch.cuda.synchronize()
                 calls.append(time.perf_counter() - t0)
                 tt += calls[-1]
-            e2e_upd = res.updates * args.steps
-            h2d = s32.nbytes + traj.positions.nbytes + np.asarray(sc.mics[0]).nbytes
+            release_plans()
+            e2e_upd = res.updates * steps
+            h2d = sx.nbytes + traj.positions.nbytes + np.asarray(sc.mics[0]).nbytes
             e2e = {"value": e2e_upd / tt, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
                    "d2h_bytes_per_step": int(y.nbytes), "api": "paper_2508_03065_b200.render",
                    "inputs": "pinned host memory (signal buffer; Trajectory positions are held "
-                             "page-locked), copied to the device inside every timed call",
+                             "page-locked), copied to the device inside every timed call; "
+                             "output returned as float64 numpy (8 B per sample)",
                    "ms_per_call": [round(c * 1e3, 3) for c in calls]}
         else:
             # batch / multi-rank: the public API for repeated renders of one
             # structure (RenderPlan) fed from host arrays in pinned memory --
             # H2D of every signal / path / receiver, the render (+ reduce to
             # rank 0) and the D2H of the output inside every timed step
+            from dataclasses import replace as _replace
+
             from paper_2508_03065_b200.plan import RenderPlan
             from paper_2508_03065_b200.synth import scene_jobs
 
@@ -444,7 +475,6 @@ def run_ours(args):
                 np.copyto(out, a)
                 return out
 
-            from dataclasses import replace as _replace
             host_jobs = [_replace(jb, s=pinned(jb.s), pos=pinned(jb.pos), mic=pinned(jb.mic))
                          for jb in scene_jobs(mine)]
             # shared paths / signals stay shared (one pinned copy per key)
@@ -461,29 +491,32 @@ def run_ours(args):
             h2d = sum(sc.s.nbytes + sc.pos.nbytes + sum(np.asarray(m).nbytes for m in sc.mics)
                       for sc in mine)
             d2h = 0
-            for _ in range(max(4, args.warmup)):  # captures both slots, then replays
+            for _ in range(max(4, warmup)):  # captures both slots, then replays
                 r = plan_e.run(host_jobs)
                 if shard is not None:
                     plan_e.reduce(r)
                 if shard is None or rank == 0:
                     r.host()
-            for _ in range(args.steps):
+            for _ in range(steps):
                 torch.cuda.synchronize()
-                barrier()
+                ctx.barrier()
                 t0 = time.perf_counter()
                 r = plan_e.run(host_jobs)
                 if shard is not None:
                     plan_e.reduce(r)
                 out_h = r.host() if (shard is None or rank == 0) else None
                 torch.cuda.synchronize()
-                barrier()
+                ctx.barrier()
                 tt += time.perf_counter() - t0
                 upd += r.updates
                 d2h = 0 if out_h is None else out_h.nbytes
+            del plan_e, r
+            gc.collect()
+            torch.cuda.empty_cache()
             tt_t = torch.tensor([tt, float(upd)], dtype=torch.float64, device=dev)
             if world > 1:
-                tmax = allreduce_host(tt_t.clone(), dist.ReduceOp.MAX)
-                tt_t = allreduce_host(tt_t, dist.ReduceOp.SUM)
+                tmax = ctx.allreduce(tt_t.clone(), dist.ReduceOp.MAX)
+                tt_t = ctx.allreduce(tt_t, dist.ReduceOp.SUM)
                 tt, upd = float(tmax[0]), float(tt_t[1])
             e2e = {"value": upd / tt, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
                    "d2h_bytes_per_step": int(d2h),
@@ -495,21 +528,25 @@ def run_ours(args):
     kern_avg_ms = float(np.mean(kern_ms)) if kern_ms else float("nan")
     # the metric counts S x out_len updates per job (the reference's loop);
     # only S x (len(s) + L - 1) of them can be non-zero (an image's delayed
-    # copy of the signal is that long), and the synthesis skips (image, tile)
-    # pairs whose gathers read only zero pads -- the roofline counts the
-    # non-zero updates one launch must compute
+    # copy of the signal is that long), and the fast synthesis skips (image,
+    # tile) pairs whose gathers read only zero pads -- its roofline counts the
+    # non-zero updates one launch must compute; the exact engine evaluates
+    # every (image, sample) pair like the reference
     metric_upd = res.updates  # one synthesis launch per step
-    upd_per_launch = int(sum(int(res.n_images[j]) * min(int(res.lengths[j]),
-                                                        int(jobs[j].s.numel()) + w.fd_taps - 1)
+    exact = res.precision == "fp64"
+    upd_per_launch = int(sum(int(res.n_images[j]) * (int(res.lengths[j]) if exact else
+                                                     min(int(res.lengths[j]),
+                                                         int(jobs[j].s.numel()) + w.fd_taps - 1))
                              for j in range(len(res.lengths))))
     flops = upd_per_launch * w.fd_taps * 2.0  # taps x FMA (north_star roofline)
     achieved = flops / (kern_avg_ms * 1e-3) / 1e12
-    traffic = load_traffic(name)
+    traffic = None if exact else load_traffic(name)
     # the other leg of the north_star roofline: algorithmic HBM bytes of a
     # render (dry signal + trajectory in, output out) at the
     # measured HBM bandwidth -- the slower leg (FMA) is the bound
+    out_bytes = 8 if exact else 4
     alg_bytes = sum(sc.s.itemsize * sc.T + 24 * sc.T * (1 + (np.ndim(sc.mics[0]) > 1) * len(sc.mics))
-                    for sc in mine) + 4 * int(np.sum(res.lengths))
+                    for sc in mine) + out_bytes * int(np.sum(res.lengths))
     hbm_gbs = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 7700.0
     hbm_leg = {"algorithmic_bytes": int(alg_bytes),
@@ -517,81 +554,153 @@ def run_ours(args):
                "frac": alg_bytes / (kern_avg_ms * 1e-3) / 1e9 / hbm_gbs,
                "measured_dram_gbs": None if traffic is None else
                traffic.get("dram_bytes_per_launch") / (kern_avg_ms * 1e-3) / 1e9}
-    roof = {
-        "kernel": "k_synth_f32 (mvb_synthesize_f32)",
-        "bound": "fp32",
-        "achieved": achieved,
-        "peak": ffma_tf,
-        "unit": "TFLOP/s",
-        "frac": achieved / ffma_tf,
-        "traffic": None if traffic is None else traffic.get("dram_bytes_per_launch"),
-        "peak_source": "measured on this GPU by bench.py (mvb_peak_ffma, best of 3)",
-        "algorithmic": f"{upd_per_launch} non-zero updates (of {metric_upd} counted by the "
-                       f"metric) x {w.fd_taps} taps x 2 flop per launch (SURVEY 8d: L FMAs per "
-                       f"update)",
-        "kernel_ms": kern_avg_ms,
-        "kernel_share_of_step": kern_avg_ms / ms_step if ms_step else None,
-        "hbm_leg": hbm_leg,
-        "executed": {
+    if exact:
+        peak, kernel, bound = peaks["dfma_tf"], "k_synth_f64 (mvb_synthesize_f64)", "fp64"
+        # executed: per (image, sample) the reference's 65-tap upsample
+        # (decimated tiers; 65 DMUL + 65 DADD) and the M+1-term Horner
+        executed = {"algorithm": "exact fp64 engine: per (image, sample) 65-tap Kaiser upsample "
+                                 "(decimated tiers) or exact distance, tau, gain, floor split, "
+                                 "15-term Horner, reference summation order",
+                    "note": "fp64 DMUL/DADD issue separately (no FMA contraction, bit-identity)"}
+        peak_source = "measured on this GPU by bench.py (mvb_peak_dfma, best of 3)"
+    else:
+        peak, kernel, bound = peaks["ffma_tf"], "k_synth_f32 (mvb_synthesize_f32)", "fp32"
+        executed = {
             "algorithm": "Farrow (paper Eq. 5): 32 B record gather + 8 FMA Horner per update",
             "l1_bytes_per_update": 32,
             "achieved_l1_gbs": upd_per_launch * 32 / (kern_avg_ms * 1e-3) / 1e9,
-            "peak_l1_gbs": l1_gbs,
-            "frac_l1": upd_per_launch * 32 / (kern_avg_ms * 1e-3) / 1e9 / l1_gbs,
-        },
+            "peak_l1_gbs": peaks["l1_gbs"],
+            "frac_l1": upd_per_launch * 32 / (kern_avg_ms * 1e-3) / 1e9 / peaks["l1_gbs"],
+        }
+        peak_source = "measured on this GPU by bench.py (mvb_peak_ffma, best of 3)"
+    roof = {
+        "kernel": kernel,
+        "bound": bound,
+        "achieved": achieved,
+        "peak": peak,
+        "unit": "TFLOP/s",
+        "frac": achieved / peak,
+        "traffic": None if traffic is None else traffic.get("dram_bytes_per_launch"),
+        "traffic_source": None if traffic is None else
+        f"profiles/ncu_synth_{name}.json (ncu --set full of this kernel on this config, "
+        f"committed; not measured in this run)",
+        "peak_source": peak_source,
+        "algorithmic": f"{upd_per_launch} {'' if exact else 'non-zero '}updates (of {metric_upd} "
+                       f"counted by the metric) x {w.fd_taps} taps x 2 flop per launch (SURVEY 8d: "
+                       f"L FMAs per update)",
+        "kernel_ms": kern_avg_ms,
+        "kernel_share_of_step": kern_avg_ms / ms_step if ms_step else None,
+        "hbm_leg": hbm_leg,
+        "executed": executed,
     }
+    gsize = {"c1": 1, "c2": 1, "c3": 1, "c4": 256, "c5": 1}[name]
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "updates/s",
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong" if (world > 1 and shard is not None) else "weak",
+        "vs_baseline": None,
+        "dtype": "f64" if precision == "fp64" else "f32 (fp64 delay anchors)",
+        "data": "synthetic (seeded white Gaussian dry signal, seeded paths; SURVEY 8d)",
+        "config": {
+            "workload": name,
+            "scenes": gsize,
+            "channels": len(scenes[0].mics),
+            "images_per_job": int(res.n_images.max()) if world == 1 else None,
+            "out_len": [int(v) for v in res.lengths[:4]],
+            "tiers": [list(t) for t in w.tiers],
+            "fd": f"{w.fd_taps}-tap Hann-windowed sinc (Farrow fit" +
+                  (", M=14, exact engine)" if exact else ", fp32 path degree 7)"),
+            "rate": w.rate,
+            "duration_s": w.duration,
+            "parallelism": mode,
+            "engine": ("RenderPlan: every kernel of the render re-run each step from two "
+                       "CUDA graphs (geometry, synthesis) on two streams, so step k+1's "
+                       "geometry overlaps step k's synthesis drain; inputs re-staged and the "
+                       "decimation decision re-taken every step (speculative replay)")
+                      if used_plan else "direct render_jobs per step",
+            "rendered_by": rendered,
+            "l2": "flushed before every timed step (256 MiB write, inside the timed region); per-step working set >L2",
+        },
+        "rtf": rtf,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "nonzero_updates_per_s": upd_per_launch * steps / (total_ms_all * 1e-3) * (
+            world if shard is None and mode.startswith("replicas") else 1),
+    }
+    del res, jobs
+    gc.collect()
+    torch.cuda.empty_cache()
+    return line, (wall0, wall1)
 
+
+def summary(line, clk):
+    """Compact per-config record for the headline line's per_config block."""
+    r = line["roofline"]
+    return {"value": line["value"], "ms_per_step": line["ms_per_step"], "steps": line["steps"],
+            "warmup": line["warmup"], "dtype": line["dtype"],
+            "e2e": None if line["e2e"] is None else line["e2e"]["value"],
+            "kernel": r["kernel"], "kernel_ms": r["kernel_ms"], "frac": r["frac"],
+            "peak": r["peak"], "bound": r["bound"],
+            "frac_l1": r["executed"].get("frac_l1"), "rtf": line["rtf"],
+            "parallelism": line["config"]["parallelism"],
+            "rendered_by": line["config"]["rendered_by"], "clocks": clk}
+
+
+def run_ours(args):
+    import torch
+    ctx = Ctx()
+    peaks = None if args.profile else measured_peaks(ctx.dev)
+    clocks = ClockSampler(ctx.local)
+    if not args.profile:
+        clocks.start()
+        time.sleep(0.3)  # let nvidia-smi start before the warm-up
+    line, win = measure(ctx, args.config, args.steps, args.warmup, peaks, args)
+    if args.profile:
+        return
+    windows = {"main": win}
+    per = {}
+    if not args.no_per_config:
+        k = max(3, min(args.steps, args.per_config_steps))
+        wu = max(3, min(args.warmup, 5))
+        todo = [c for c in ("c1", "c2", "c3", "c4", "c5") if c != args.config]
+        for c in todo:
+            ln, wn = measure(ctx, c, k, wu, peaks, args)
+            per[c] = ln
+            windows[c] = wn
+        # same-precision (fp64) comparison on the largest single-scene config
+        if ctx.world == 1:
+            ln, wn = measure(ctx, "c3", 3, 3, peaks, args, precision="fp64", with_e2e=False)
+            per["c3_fp64"] = ln
+            windows["c3_fp64"] = wn
+    clocks.stop()
+    line["clocks"] = clocks.window(*windows["main"])
     # ---- CPU baseline (rank 0, N = 1) -----------------------------------------
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu:
         from oracle import oracle as orc
         nth = orc.default_threads()
-        v, desc, th, n_upd, dt = cpu_sample(name, args.cpu_seconds, nth)
+        v, desc, th, n_upd, dt = cpu_sample(args.config, args.cpu_seconds, nth)
         cpu = {"value": v, "unit": "updates/s", "cores": th, "kind": "port", "sample": desc,
-               "seconds": dt}
-
-    if rank == 0:
-        gsize = {"c1": 1, "c2": 1, "c3": 1, "c4": 256, "c5": 1}[name]
-        line = {
-            "metric": METRIC,
-            "value": value,
-            "unit": "updates/s",
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": ms_step,
-            "higher_is_better": True,
-            "scaling": "strong" if (world > 1 and name in ("c3", "c5")) else "weak",
-            "vs_baseline": None,
-            "dtype": "f64" if precision == "fp64" else "f32 (fp64 delay anchors)",
-            "data": "synthetic (seeded white Gaussian dry signal, seeded paths; SURVEY 8d)",
-            "config": {
-                "workload": name,
-                "scenes": gsize,
-                "channels": len(scenes[0].mics),
-                "images_per_job": int(res.n_images.max()) if world == 1 else None,
-                "out_len": [int(v) for v in res.lengths[:4]],
-                "tiers": [list(t) for t in w.tiers],
-                "fd": f"{w.fd_taps}-tap Hann-windowed sinc (Farrow fit, fp32 path degree 7)",
-                "rate": w.rate,
-                "duration_s": w.duration,
-                "parallelism": mode,
-                "engine": ("RenderPlan: every kernel of the render re-run each step from two "
-                           "CUDA graphs (geometry, synthesis) on two streams, so step k+1's "
-                           "geometry overlaps step k's synthesis drain; inputs re-staged and the "
-                           "decimation decision re-taken every step (speculative replay)")
-                          if used_plan else "direct render_jobs per step",
-                "l2": "flushed before every timed step (256 MiB write, inside the timed region); per-step working set >L2",
-            },
-            "rtf": rtf,
-            "clocks": clk,
-            "e2e": e2e,
-            "gpu_launches": int(launches),
-            "roofline": roof,
-            "cpu_baseline": cpu,
-        }
+               "seconds": dt,
+               "matched": "the sample is mid-signal, where every update is non-zero; compare it "
+                          "with this line's nonzero_updates_per_s (the GPU metric also counts the "
+                          "exact zeros of S x out_len)"}
+    line["cpu_baseline"] = cpu
+    if per:
+        line["per_config"] = {args.config: summary(line, line["clocks"])}
+        for c, ln in per.items():
+            line["per_config"][c] = summary(ln, clocks.window(*windows[c]))
+    if ctx.rank == 0:
         print(json.dumps(line))
-    if world > 1:
+    if ctx.world > 1:
+        import torch.distributed as dist
         dist.destroy_process_group()
 
 

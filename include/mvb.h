@@ -385,6 +385,8 @@ int mvb_splice_sum(const double* d_pieces, int64_t piece_stride, int64_t n, int6
  *    CUDA events on `stream`.
  * --------------------------------------------------------------------- */
 int mvb_peak_ffma(int blocks, int iters, float* d_sink, void* stream);
+/* FP64 FMA peak probe: blocks x 256 threads x iters x 128 DFMA. */
+int mvb_peak_dfma(int blocks, int iters, double* d_sink, void* stream);
 int mvb_peak_l1(int blocks, int iters, const float* d_buf /* 1 MiB */, float* d_sink,
                 void* stream);
 

@@ -59,6 +59,7 @@ _SIGS = {
     "mvb_block_convolve": [P, I64, I64, I64, I64, INT, P, P, I64, I64, P, I64, P],
     "mvb_splice_sum": [P, I64, I64, I64, I64, I64, P, I64, P, I64, P],
     "mvb_peak_ffma": [INT, INT, P, P],
+    "mvb_peak_dfma": [INT, INT, P, P],
     "mvb_peak_l1": [INT, INT, P, P, P],
 }
 _RESTYPE = {"mvb_last_error": ctypes.c_char_p, "mvb_image_count": I64}

@@ -23,6 +23,22 @@ __global__ void __launch_bounds__(256) k_peak_ffma(int iters, float seed, float*
     if (s == 12345.678f) out[blockIdx.x] = s;  // keep the chains alive
 }
 
+// The same shape in fp64 (DFMA): the exact engine's roofline denominator.
+__global__ void __launch_bounds__(256) k_peak_dfma(int iters, double seed, double* out) {
+    double a0 = seed + threadIdx.x, a1 = a0 + 1.0, a2 = a0 + 2.0, a3 = a0 + 3.0;
+    double a4 = a0 + 4.0, a5 = a0 + 5.0, a6 = a0 + 6.0, a7 = a0 + 7.0;
+    const double m = 0.9999999999, c = 1e-12;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+            a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+        }
+    }
+    double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.678) out[blockIdx.x] = s;
+}
+
 // Every warp streams a 16 KB per-CTA window with coalesced 16-byte loads:
 // L1 hits after the first pass (same access shape as the synthesis gather).
 __global__ void __launch_bounds__(256) k_peak_l1(const float4* __restrict__ buf, int iters,
@@ -50,6 +66,13 @@ int mvb_peak_ffma(int blocks, int iters, float* d_sink, void* stream) {
     if (blocks < 1 || iters < 1 || !d_sink) return fail(MVB_EINVAL, "peak_ffma: args");
     k_peak_ffma<<<blocks, 256, 0, as_stream(stream)>>>(iters, 1.0f, d_sink);
     return check_launch("peak_ffma");
+}
+
+/* FP64 FMA peak probe: grid blocks x 256 threads x iters x 128 DFMA. */
+int mvb_peak_dfma(int blocks, int iters, double* d_sink, void* stream) {
+    if (blocks < 1 || iters < 1 || !d_sink) return fail(MVB_EINVAL, "peak_dfma: args");
+    k_peak_dfma<<<blocks, 256, 0, as_stream(stream)>>>(iters, 1.0, d_sink);
+    return check_launch("peak_dfma");
 }
 
 /* L1 load probe: blocks x 256 threads x iters x 4 x 16 B from a 64x16 KB buffer. */

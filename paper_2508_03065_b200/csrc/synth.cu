@@ -518,16 +518,61 @@ __global__ void k_reduce_f32(const mvb_job* __restrict__ jobs, const float* __re
 
 // ---------------------------------------------------------------------------
 // exact synthesis
+//
+// One CTA per (job, 32-sample tile); lane l of every warp owns sample
+// n0 + l.  Images are processed in chunks of F64_CHUNK_BLOCKS 32-image
+// blocks of the canonical order:
+//   1. every warp computes the contributions A * Horner(mu) of images
+//      w, w + 8, ... of the chunk (the 65-tap upsample is the cost) into
+//      shared memory -- contributions are independent, only their sum is
+//      ordered;
+//   2. warp b sums block b of the chunk sequentially over its 32 images,
+//      (((0 + c_0) + c_1) + ...) -- the order of _accumulate_numba's image
+//      loop into a zeroed block buffer (_kernels.py:112-122, synth.py:246-251);
+//      an image whose read index is outside the branch streams adds +0.0,
+//      which leaves the sum unchanged (a sum that starts at +0.0 never
+//      becomes -0.0 in round-to-nearest);
+//   3. warp 0 folds the chunk's block sums into the pairwise tree of
+//      synth.py:182-191, kept as a merge stack of (value, level): a full
+//      chunk is a perfect subtree of level log2(F64_CHUNK_BLOCKS), a
+//      partial last chunk splits into aligned power-of-two subtrees --
+//      equivalent to pushing its blocks one by one (binary counter).
+// Bit-identical to the reference arithmetic (explicit _rn operations, no
+// FMA contraction), deterministic, and parallel over images as well as
+// samples, so small image sets (c1: 63 images) still fill the GPU.
 
-__global__ void __launch_bounds__(128) k_synth_f64(
+constexpr int F64_WARPS = 8;
+constexpr int F64_CHUNK_BLOCKS = 8;  // power of two
+constexpr int F64_CHUNK = 32 * F64_CHUNK_BLOCKS;
+constexpr int F64_LOG_CHUNK = 3;
+static_assert((1 << F64_LOG_CHUNK) == F64_CHUNK_BLOCKS, "chunk is a power of two");
+constexpr size_t F64_SMEM = sizeof(double) * (F64_CHUNK * 32 + F64_CHUNK_BLOCKS * 32);
+
+__device__ __forceinline__ void merge_push(double* st_v, int* st_l, int& sp, double v, int l) {
+    while (sp > 0 && st_l[sp - 1] == l) {
+        v = xadd(st_v[--sp], v);
+        ++l;
+    }
+    st_v[sp] = v;
+    st_l[sp++] = l;
+}
+
+__global__ void __launch_bounds__(F64_WARPS * 32) k_synth_f64(
     const mvb_job* __restrict__ jobs, const mvb_image* __restrict__ images,
     const double* __restrict__ coarse, const double* __restrict__ tables,
     const double* __restrict__ streams, const double* __restrict__ paths,
     double* __restrict__ out) {
-    const mvb_job J = jobs[blockIdx.y];
-    const int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (n >= J.out_len) return;
-    const int64_t m = n < J.T ? n : J.T - 1;
+    extern __shared__ double f64_smem[];
+    double* contrib = f64_smem;                 // [F64_CHUNK images][32 lanes]
+    double* bsum = f64_smem + F64_CHUNK * 32;   // [F64_CHUNK_BLOCKS][32 lanes]
+    const mvb_job& J = jobs[blockIdx.y];
+    const int64_t out_len = J.out_len;
+    const int64_t n0 = (int64_t)blockIdx.x * 32;
+    if (n0 >= out_len) return;  // CTA-uniform
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n = n0 + lane;
+    const bool valid = n < out_len;
+    const int64_t m = (valid ? n : out_len - 1) < J.T ? (valid ? n : out_len - 1) : J.T - 1;
     const double* p = paths + 3 * (J.pos_off + m);
     const double* q = paths + 3 * (J.mic_off + (J.mic_moving ? m : 0));
     const double P[3] = {p[0], p[1], p[2]};
@@ -535,15 +580,17 @@ __global__ void __launch_bounds__(128) k_synth_f64(
     const double* V = streams + J.rec_base;
     const double L = (double)J.L, d0 = (double)J.d0;
     const double four_pi = 4.0 * 3.141592653589793;  // 4.0 * np.pi
-    // pairwise merge stack (equivalent to synth.py:182-191, see tests)
+    const int64_t n_img = J.n_img;
+    const mvb_image* __restrict__ imgs = images + J.img_off;
+    // merge stack (warp 0's lanes): at most one entry per level
     double st_v[40];
     int st_l[40];
     int sp = 0;
-    for (int64_t b0 = 0; b0 < J.n_img; b0 += 32) {
-        const int64_t b1 = b0 + 32 < J.n_img ? b0 + 32 : J.n_img;
-        double s = 0.0;
-        for (int64_t i = b0; i < b1; ++i) {
-            const mvb_image im = images[J.img_off + i];
+    for (int64_t c0 = 0; c0 < n_img; c0 += F64_CHUNK) {
+        const int cn = n_img - c0 < F64_CHUNK ? (int)(n_img - c0) : F64_CHUNK;
+        // 1. contributions of the chunk's images
+        for (int k = warp; k < cn; k += F64_WARPS) {
+            const mvb_image& im = imgs[c0 + k];
             double d;
             if (im.factor == 1)
                 d = exact_distance(im.off[0], im.off[1], im.off[2], (double)im.sign[0],
@@ -556,24 +603,44 @@ __global__ void __launch_bounds__(128) k_synth_f64(
             const double d_int = floor(xsub(shifted, d0));
             const double mu = xsub(xsub(shifted, d0), d_int);
             const int64_t idx = n + J.L - (int64_t)d_int;
+            double c = 0.0;
             if (idx >= 0 && idx < J.ls) {
                 double acc = V[(int64_t)(J.nb - 1) * J.ls + idx];
-                for (int k = J.nb - 2; k >= 0; --k) acc = xadd(xmul(acc, mu), V[(int64_t)k * J.ls + idx]);
-                s = xadd(s, xmul(amp, acc));
+                for (int b = J.nb - 2; b >= 0; --b) acc = xadd(xmul(acc, mu), V[(int64_t)b * J.ls + idx]);
+                c = xmul(amp, acc);
+            }
+            contrib[k * 32 + lane] = c;
+        }
+        __syncthreads();
+        // 2. block sums, sequential over each block's images
+        const int nblk = (cn + 31) / 32;
+        if (warp < nblk) {
+            const int k1 = (warp + 1) * 32 < cn ? (warp + 1) * 32 : cn;
+            double sum = 0.0;
+            for (int k = warp * 32; k < k1; ++k) sum = xadd(sum, contrib[k * 32 + lane]);
+            bsum[warp * 32 + lane] = sum;
+        }
+        __syncthreads();
+        // 3. pairwise tree: aligned power-of-two subtrees of the chunk's blocks
+        if (warp == 0) {
+            int off = 0;
+            for (int k = F64_LOG_CHUNK; k >= 0; --k) {
+                const int size = 1 << k;
+                if (!(nblk & size)) continue;
+                for (int step = 1; step < size; step <<= 1)
+                    for (int b = off; b < off + size; b += 2 * step)
+                        bsum[b * 32 + lane] = xadd(bsum[b * 32 + lane], bsum[(b + step) * 32 + lane]);
+                merge_push(st_v, st_l, sp, bsum[off * 32 + lane], k);
+                off += size;
             }
         }
-        double v = s;
-        int l = 0;
-        while (sp > 0 && st_l[sp - 1] == l) {
-            v = xadd(st_v[--sp], v);
-            ++l;
-        }
-        st_v[sp] = v;
-        st_l[sp++] = l;
+        __syncthreads();  // contrib / bsum are rewritten by the next chunk
     }
-    double v = sp > 0 ? st_v[--sp] : 0.0;
-    while (sp > 0) v = xadd(st_v[--sp], v);
-    out[J.out_off + n] = v;
+    if (warp == 0 && valid) {
+        double v = sp > 0 ? st_v[--sp] : 0.0;
+        while (sp > 0) v = xadd(st_v[--sp], v);
+        out[J.out_off + n] = v;
+    }
 }
 
 }  // namespace mvb
@@ -653,8 +720,16 @@ int mvb_synthesize_f64(const mvb_job* jobs, int64_t n_jobs, int64_t max_out_len,
     if (n_jobs == 0 || max_out_len == 0) return MVB_OK;
     if (!jobs || !images || !streams || !paths || !out)
         return fail(MVB_EINVAL, "synthesize_f64: null");
-    dim3 g(grid_for(max_out_len, 128), (unsigned)n_jobs);
-    k_synth_f64<<<g, 128, 0, as_stream(stream)>>>(jobs, images, coarse, tables, streams, paths, out);
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_synth_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)F64_SMEM) != cudaSuccess)
+            return check_launch("synthesize_f64 (smem attribute)");
+        attr = true;
+    }
+    dim3 g(grid_for(max_out_len, 32), (unsigned)n_jobs);
+    k_synth_f64<<<g, F64_WARPS * 32, F64_SMEM, as_stream(stream)>>>(jobs, images, coarse, tables,
+                                                                     streams, paths, out);
     return check_launch("synthesize_f64");
 }
 

@@ -92,3 +92,33 @@ def test_c3_whole_output_against_oracle():
     ref = _oracle(sc, 0, f).render()
     assert y.size == ref.size
     assert rel_err(y, ref) <= TOL
+
+
+def test_c4_timed_plan_against_oracle_32_scenes():
+    """The bench's own c4 engine -- all 256 scenes in one RenderPlan, device
+    inputs, replayed (speculative replay of the second slot included) -- on
+    32 scenes sampled across the batch, whole outputs against the oracle."""
+    from paper_2508_03065_b200.plan import RenderPlan
+    scenes = workloads.make_scenes("c4")
+    f = hann_sinc(32, 14)
+    jobs = scene_jobs(scenes)
+    dev = torch.device("cuda", 0)
+    jobs = [type(jb)(**{**jb.__dict__, "s": torch.from_numpy(np.ascontiguousarray(jb.s)).to(dev),
+                        "pos": torch.from_numpy(np.ascontiguousarray(jb.pos)).to(dev)})
+            for jb in jobs]
+    plan = RenderPlan(jobs, f)
+    for _ in range(3):  # capture slot 0, capture slot 1, replay slot 0
+        res = plan.run(jobs)
+    res.wait()
+    picks = np.unique(np.linspace(0, len(scenes) - 1, 32).astype(int))
+    assert picks.size == 32
+    worst = 0.0
+    for j in picks:
+        ref = _oracle(scenes[j], 0, f).render()
+        y = res.job(int(j)).double().cpu().numpy()
+        assert y.size == ref.size, j
+        worst = max(worst, rel_err(y, ref))
+    assert worst <= TOL, worst
+    plan.join()
+    del plan, res
+    torch.cuda.empty_cache()
