@@ -30,6 +30,7 @@
 // 32-image blocks in canonical order, then the pairwise block tree
 // (synth.py:182-191) evaluated with an equivalent merge stack.
 #include <cfloat>
+#include <cstdlib>
 
 #include "mvb_common.cuh"
 
@@ -542,11 +543,15 @@ __global__ void k_reduce_f32(const mvb_job* __restrict__ jobs, const float* __re
 // samples, so small image sets (c1: 63 images) still fill the GPU.
 
 constexpr int F64_WARPS = 8;
-constexpr int F64_CHUNK_BLOCKS = 8;  // power of two
+constexpr int F64_CHUNK_BLOCKS = 4;  // power of two
 constexpr int F64_CHUNK = 32 * F64_CHUNK_BLOCKS;
-constexpr int F64_LOG_CHUNK = 3;
+constexpr int F64_LOG_CHUNK = 2;
 static_assert((1 << F64_LOG_CHUNK) == F64_CHUNK_BLOCKS, "chunk is a power of two");
 constexpr size_t F64_SMEM = sizeof(double) * (F64_CHUNK * 32 + F64_CHUNK_BLOCKS * 32);
+// images per warp evaluated together: their 65-tap upsample chains are
+// independent, so G chains hide the fp64 add latency of one (each chain
+// keeps the reference's tap order)
+constexpr int F64_G = 4;
 
 __device__ __forceinline__ void merge_push(double* st_v, int* st_l, int& sp, double v, int l) {
     while (sp > 0 && st_l[sp - 1] == l) {
@@ -557,7 +562,8 @@ __device__ __forceinline__ void merge_push(double* st_v, int* st_l, int& sp, dou
     st_l[sp++] = l;
 }
 
-__global__ void __launch_bounds__(F64_WARPS * 32) k_synth_f64(
+template <int MINB>
+__global__ void __launch_bounds__(F64_WARPS * 32, MINB) k_synth_f64(
     const mvb_job* __restrict__ jobs, const mvb_image* __restrict__ images,
     const double* __restrict__ coarse, const double* __restrict__ tables,
     const double* __restrict__ streams, const double* __restrict__ paths,
@@ -588,28 +594,88 @@ __global__ void __launch_bounds__(F64_WARPS * 32) k_synth_f64(
     int sp = 0;
     for (int64_t c0 = 0; c0 < n_img; c0 += F64_CHUNK) {
         const int cn = n_img - c0 < F64_CHUNK ? (int)(n_img - c0) : F64_CHUNK;
-        // 1. contributions of the chunk's images
-        for (int k = warp; k < cn; k += F64_WARPS) {
-            const mvb_image& im = imgs[c0 + k];
-            double d;
-            if (im.factor == 1)
-                d = exact_distance(im.off[0], im.off[1], im.off[2], (double)im.sign[0],
-                                   (double)im.sign[1], (double)im.sign[2], P, Q);
-            else
-                d = exact_upsample(coarse + im.coarse, im.n_coarse, tables + im.table, im.factor, m);
-            const double tau = xdiv(xmul(J.rate, d), J.c);
-            const double amp = xdiv(im.beta, xmul(four_pi, d > J.d_min ? d : J.d_min));
-            const double shifted = xadd(tau, L);
-            const double d_int = floor(xsub(shifted, d0));
-            const double mu = xsub(xsub(shifted, d0), d_int);
-            const int64_t idx = n + J.L - (int64_t)d_int;
-            double c = 0.0;
-            if (idx >= 0 && idx < J.ls) {
-                double acc = V[(int64_t)(J.nb - 1) * J.ls + idx];
-                for (int b = J.nb - 2; b >= 0; --b) acc = xadd(xmul(acc, mu), V[(int64_t)b * J.ls + idx]);
-                c = xmul(amp, acc);
+        // 1. contributions of the chunk's images: warp w takes images
+        //    w, w + 8, ... in groups of F64_G evaluated together
+        for (int kb = warp; kb < cn; kb += F64_WARPS * F64_G) {
+            double d[F64_G], acc[F64_G];
+            const double* cp[F64_G];
+            const double* tp[F64_G];
+            int64_t base[F64_G], nc[F64_G], fac[F64_G], phase[F64_G];
+            bool dec[F64_G], fast[F64_G];
+#pragma unroll
+            for (int g = 0; g < F64_G; ++g) {
+                const int k = kb + g * F64_WARPS;
+                dec[g] = fast[g] = false;
+                d[g] = 0.0;
+                acc[g] = 0.0;
+                cp[g] = tp[g] = nullptr;
+                base[g] = nc[g] = phase[g] = 0;
+                fac[g] = 1;
+                if (k < cn) {
+                    const mvb_image& im = imgs[c0 + k];
+                    if (im.factor == 1) {
+                        d[g] = exact_distance(im.off[0], im.off[1], im.off[2], (double)im.sign[0],
+                                              (double)im.sign[1], (double)im.sign[2], P, Q);
+                    } else {
+                        dec[g] = true;
+                        cp[g] = coarse + im.coarse;
+                        tp[g] = tables + im.table;
+                        nc[g] = im.n_coarse;
+                        fac[g] = im.factor;
+                        base[g] = m / fac[g];
+                        phase[g] = m - base[g] * fac[g];
+                        // warp-uniform: the tile's 32 samples share one coarse
+                        // interval (N % 32 == 0, 32-aligned tiles, all before
+                        // the track end) and the 65-sample window needs no clamp
+                        fast[g] = (im.factor % 32 == 0) && (n0 + 31 < J.T) &&
+                                  (n0 / im.factor) >= 32 && (n0 / im.factor) + 32 < im.n_coarse;
+                    }
+                }
             }
-            contrib[k * 32 + lane] = c;
+            // the 65-tap upsample of _kernels.py:169-180 (exact_upsample):
+            // the clamp-free members as F64_G independent chains (each in the
+            // reference's tap order; other members run a dummy chain on a
+            // valid address, discarded), then the rare clamped members alone
+            {
+                const double* w[F64_G];
+                const double* t[F64_G];
+                int stride[F64_G];
+#pragma unroll
+                for (int g = 0; g < F64_G; ++g) {
+                    w[g] = fast[g] ? cp[g] + (base[g] - 32) : tables;
+                    t[g] = fast[g] ? tp[g] + phase[g] : tables;
+                    stride[g] = fast[g] ? (int)fac[g] : 0;
+                }
+#pragma unroll 5
+                for (int col = 0; col < 65; ++col) {
+#pragma unroll
+                    for (int g = 0; g < F64_G; ++g)
+                        acc[g] = xadd(acc[g], xmul(__ldg(t[g] + col * stride[g]), __ldg(w[g] + col)));
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < F64_G; ++g)
+                if (dec[g] && !fast[g]) acc[g] = exact_upsample(cp[g], nc[g], tp[g], fac[g], m);
+#pragma unroll
+            for (int g = 0; g < F64_G; ++g) {
+                const int k = kb + g * F64_WARPS;
+                if (k >= cn) continue;
+                if (dec[g]) d[g] = acc[g];
+                const mvb_image& im = imgs[c0 + k];
+                const double tau = xdiv(xmul(J.rate, d[g]), J.c);
+                const double amp = xdiv(im.beta, xmul(four_pi, d[g] > J.d_min ? d[g] : J.d_min));
+                const double shifted = xadd(tau, L);
+                const double d_int = floor(xsub(shifted, d0));
+                const double mu = xsub(xsub(shifted, d0), d_int);
+                const int64_t idx = n + J.L - (int64_t)d_int;
+                double c = 0.0;
+                if (idx >= 0 && idx < J.ls) {
+                    double h = V[(int64_t)(J.nb - 1) * J.ls + idx];
+                    for (int b = J.nb - 2; b >= 0; --b) h = xadd(xmul(h, mu), V[(int64_t)b * J.ls + idx]);
+                    c = xmul(amp, h);
+                }
+                contrib[k * 32 + lane] = c;
+            }
         }
         __syncthreads();
         // 2. block sums, sequential over each block's images
@@ -720,16 +786,27 @@ int mvb_synthesize_f64(const mvb_job* jobs, int64_t n_jobs, int64_t max_out_len,
     if (n_jobs == 0 || max_out_len == 0) return MVB_OK;
     if (!jobs || !images || !streams || !paths || !out)
         return fail(MVB_EINVAL, "synthesize_f64: null");
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_synth_f64, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)F64_SMEM) != cudaSuccess)
+    // CTAs per SM the register budget targets (diagnostic knob MVB_F64_MINB:
+    // 2 = 118 registers, no spills; 3 = 80 registers, light spills)
+    static int minb = 0;
+    if (!minb) {
+        const char* e = getenv("MVB_F64_MINB");
+        minb = (e && atoi(e) == 3) ? 3 : 2;
+        const cudaError_t a = minb == 3
+            ? cudaFuncSetAttribute(k_synth_f64<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F64_SMEM)
+            : cudaFuncSetAttribute(k_synth_f64<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F64_SMEM);
+        if (a != cudaSuccess) {
+            minb = 0;
             return check_launch("synthesize_f64 (smem attribute)");
-        attr = true;
+        }
     }
     dim3 g(grid_for(max_out_len, 32), (unsigned)n_jobs);
-    k_synth_f64<<<g, F64_WARPS * 32, F64_SMEM, as_stream(stream)>>>(jobs, images, coarse, tables,
-                                                                     streams, paths, out);
+    if (minb == 3)
+        k_synth_f64<3><<<g, F64_WARPS * 32, F64_SMEM, as_stream(stream)>>>(jobs, images, coarse, tables,
+                                                                            streams, paths, out);
+    else
+        k_synth_f64<2><<<g, F64_WARPS * 32, F64_SMEM, as_stream(stream)>>>(jobs, images, coarse, tables,
+                                                                            streams, paths, out);
     return check_launch("synthesize_f64");
 }
 
