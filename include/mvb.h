@@ -332,6 +332,22 @@ int mvb_synthesize_f32(const mvb_job* d_jobs, const mvb_work* d_work, int64_t n_
 int mvb_reduce_partials_f32(const mvb_job* d_jobs, int64_t n_jobs, int64_t max_out_len,
                             const float* d_part, float* d_out, void* stream);
 
+/* SURVEY H2 A/B (measurement only, not the product path): the literal
+ * per-fraction-table fractional delay.  mvb_signal_plane_f32 writes the
+ * dry signals into a zero-filled fp32 plane d_xp with the branch-record row
+ * numbering (row0 = sample 0); mvb_synthesize_f32_table runs the fast
+ * synthesis with a direct L-tap gather of that plane, the taps linearly
+ * interpolated in mu from d_table ((MVB_TAB_P + 1) x L floats, h_j(p/P) of
+ * the filter), staged in shared memory. */
+#define MVB_TAB_P 512
+int mvb_signal_plane_f32(const float* d_x_all, const int64_t* d_sig_off, const int64_t* d_sig_len,
+                         const int64_t* d_sig_row0, int64_t n_sig, int64_t max_len, float* d_xp,
+                         void* stream);
+int mvb_synthesize_f32_table(const mvb_job* d_jobs, const mvb_work* d_work, int64_t n_work,
+                             const mvb_image* d_images, const mvb_coef32* d_coef,
+                             const float* d_xp, const double* d_paths, float* d_out,
+                             float* d_part, const float* d_table, int L, void* stream);
+
 /* Exact synthesis (fp64): per-sample reference arithmetic (exact or 65-tap
  * upsampled distance, tau = (rate*d)/c, gain, floor split, Horner in mu)
  * in the reference's summation order (32-image blocks of the canonical

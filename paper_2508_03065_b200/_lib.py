@@ -58,6 +58,8 @@ _SIGS = {
     "mvb_static_gather": [P, P, P, I64, I64, P, I64, P, P],
     "mvb_block_convolve": [P, I64, I64, I64, I64, INT, P, P, I64, I64, P, I64, P],
     "mvb_splice_sum": [P, I64, I64, I64, I64, I64, P, I64, P, I64, P],
+    "mvb_signal_plane_f32": [P, P, P, P, I64, I64, P, P],
+    "mvb_synthesize_f32_table": [P, P, I64, P, P, P, P, P, P, P, INT, P],
     "mvb_peak_ffma": [INT, INT, P, P],
     "mvb_peak_dfma": [INT, INT, P, P],
     "mvb_peak_l1": [INT, INT, P, P, P],

@@ -31,6 +31,7 @@
 // (synth.py:182-191) evaluated with an equivalent merge stack.
 #include <cfloat>
 #include <cstdlib>
+#include <type_traits>
 
 #include "mvb_common.cuh"
 
@@ -159,6 +160,47 @@ __device__ __forceinline__ float gather_horner(const float4* __restrict__ R, uns
     return fmaf(mc, q.y, q.x);
 }
 
+// The update's fractional-delay gather behind one interface, so the same
+// synthesis kernel runs the Farrow records (the product) or the literal
+// per-fraction table (the SURVEY H2 A/B, mvb_synthesize_f32_table).
+template <int NP>
+struct FarrowGather {
+    const float4* __restrict__ R;
+    __device__ __forceinline__ float operator()(unsigned row, float mc) const {
+        return gather_horner<NP>(R, row, mc);
+    }
+};
+
+// Literal per-fraction table: taps h_j(mu) at mu = p / TAB_P, p = 0..TAB_P,
+// in shared memory (row stride L + 1: lanes at different fractions hit
+// different banks), linearly interpolated in mu, then a direct L-tap gather
+// of the zero-padded signal plane xp (row r <-> branch row r, so the
+// reference's valid window and the zero pads are the Farrow path's):
+// sum_j h_j(mu) xp[r - j].  Per tap: two shared loads, one global load, two
+// FMAs plus the interpolation -- the structure the H2 estimate bounds.
+constexpr int TAB_P = 512;
+struct TableGather {
+    const float* __restrict__ xp;
+    const float* tab;  // shared memory
+    int L;
+    __device__ __forceinline__ float operator()(unsigned row, float mc) const {
+        const float sc = (mc + 0.5f) * (float)TAB_P;
+        int p = (int)sc;
+        p = p < 0 ? 0 : (p > TAB_P - 1 ? TAB_P - 1 : p);
+        const float a = sc - (float)p;
+        const float* t0 = tab + p * (L + 1);
+        const float* t1 = t0 + (L + 1);
+        const float* x = xp + row;
+        float acc = 0.f;
+#pragma unroll 8
+        for (int j = 0; j < L; ++j) {
+            const float h0 = t0[j];
+            acc = fmaf(fmaf(a, t1[j] - h0, h0), __ldg(x - j), acc);
+        }
+        return acc;
+    }
+};
+
 // Track residual kappa*(d(u) - g0) = u * sum_{p=1..8} g_p u^(p-1), same
 // even/odd pairing over the record's (g1,g2), (g3,g4), (g5,g6), (g7,g8).
 __device__ __forceinline__ float track_residual(const float4& c1, const float4& c2, float uu) {
@@ -192,9 +234,9 @@ constexpr int MAGIC_I = 0x4B400000;
 
 // One decimated-image step given the interval record (c0, c1, c2):
 // nlB = rec_base + n0 + lane + L + MAGIC_I - B.  Returns the contribution.
-template <int NP>
+template <class G>
 __device__ __forceinline__ float dec_step(const float4& c0, const float4& c1, const float4& c2,
-                                          float uu, int rowbase, const float4* __restrict__ R,
+                                          float uu, int rowbase, const G& g,
                                           float an, float invk, float dmin) {
     const float res = track_residual(c1, c2, uu);  // kappa * (d - g0)
     const float t = c0.y + res;
@@ -203,7 +245,7 @@ __device__ __forceinline__ float dec_step(const float4& c0, const float4& c1, co
     const unsigned row = (unsigned)(rowbase - __float_as_int(v));
     const float d = fmaf(res, invk, c0.z);
     const float A = an * rcp_approx(fmaxf(d, dmin));
-    return A * gather_horner<NP>(R, row, mc);
+    return A * g(row, mc);
 }
 
 // Decimated image on a tile wholly inside [0, T) with TILE % NT == 0 (its
@@ -211,9 +253,9 @@ __device__ __forceinline__ float dec_step(const float4& c0, const float4& c1, co
 // tile starts on an interval boundary, interval q covers steps
 // [q*SPI, (q+1)*SPI) and u = 2r/N - 1 is a per-step constant plus a lane
 // term -- no per-step bookkeeping, straight-line steps.
-template <int U, int NP, int NT>
+template <int U, int NT, class G>
 __device__ __forceinline__ void dec_static(float (&acc)[U], const float4* __restrict__ cs,
-                                           const float4* __restrict__ R, int lane, int nl,
+                                           const G& g, int lane, int nl,
                                            float an, float invk, float dmin) {
     constexpr int SPI = NT / 32;  // steps per coarse interval
     const float lt = (float)lane * (2.0f / NT);
@@ -229,7 +271,7 @@ __device__ __forceinline__ void dec_static(float (&acc)[U], const float4* __rest
             nlB = nl - __float_as_int(c0.x);
         }
         const float uu = lt + ((float)((u % SPI) * 32) * (2.0f / NT) - 1.0f);
-        acc[u] += dec_step<NP>(c0, c1, c2, uu, nlB + 32 * u, R, an, invk, dmin);
+        acc[u] += dec_step(c0, c1, c2, uu, nlB + 32 * u, g, an, invk, dmin);
     }
 }
 
@@ -291,12 +333,12 @@ __device__ __forceinline__ void stage_image(WarpStage<U>& st, int slot, const mv
                    reinterpret_cast<const char*>(src) + 16 * lane);
 }
 
-template <int U, int NP, int MINB>
+template <int U, int NP, int MINB, bool TAB = false>
 __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     const mvb_job* __restrict__ jobs, const mvb_work* __restrict__ work,
     const mvb_image* __restrict__ images, const mvb_coef32* __restrict__ coef,
     const float* __restrict__ rec, const double* __restrict__ paths, float* __restrict__ out,
-    float* __restrict__ part) {
+    float* __restrict__ part, const float* __restrict__ table = nullptr) {
     constexpr int TN = 32 * U;
     __shared__ float red[SYNTH_WARPS][TN];
     __shared__ WarpStage<U> stage[SYNTH_WARPS];
@@ -311,7 +353,19 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     // rows are indexed globally: row = rec_base + (n + L - D) >= 0 thanks to
     // the zero front pad of every signal's region
     const int rb = (int)Jp->rec_base;
-    const float4* __restrict__ R = reinterpret_cast<const float4*>(rec);
+    using Gather = std::conditional_t<TAB, TableGather, FarrowGather<NP>>;
+    Gather g;
+    if constexpr (TAB) {
+        // the fraction table: (TAB_P + 1) rows of L taps, padded to L + 1
+        extern __shared__ float tab_smem[];
+        const int Lt = Jp->L;
+        for (int t = threadIdx.x; t < (TAB_P + 1) * Lt; t += blockDim.x)
+            tab_smem[(t / Lt) * (Lt + 1) + t % Lt] = table[t];
+        __syncthreads();
+        g = TableGather{rec, tab_smem, Lt};
+    } else {
+        g = FarrowGather<NP>{reinterpret_cast<const float4*>(rec)};
+    }
     // this tile's delay-sorted image table (sort segment wp->seg)
     const mvb_image* __restrict__ imgs = images + Jp->img_off + (int64_t)wp->seg * Jp->img_stride;
     const float invk = (float)(1.0 / Jp->kappa);
@@ -395,7 +449,7 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
             const int rfirst = row0 - lane;  // row of the tile's first sample (warp-uniform)
             if (rfirst + TN <= rb || rfirst >= rb + ls) continue;  // all in the zero pads
 #pragma unroll
-            for (int u = 0; u < U; ++u) acc[u] += A * gather_horner<NP>(R, (unsigned)(row0 + 32 * u), mc);
+            for (int u = 0; u < U; ++u) acc[u] += A * g((unsigned)(row0 + 32 * u), mc);
             continue;
         }
         if (N == 1) {
@@ -423,7 +477,7 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
                 const float mc = (float)(s - D) - 0.5f;
                 const unsigned r = (unsigned)(rb + n + Lsh - (int)D);
                 const float A = an * rcp_approx(fmaxf((float)d, dmin));
-                row[32 * u + lane] = fmaf(A, gather_horner<NP>(R, r, mc), row[32 * u + lane]);
+                row[32 * u + lane] = fmaf(A, g(r, mc), row[32 * u + lane]);
             }
             continue;
         }
@@ -447,10 +501,10 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
             }
             // staged records: slot j = interval n0/N + j
             switch (N) {
-                case 32: dec_static<U, NP, 32>(acc, cs, R, lane, nl, an, invk, dmin); break;
-                case 64: dec_static<U, NP, 64>(acc, cs, R, lane, nl, an, invk, dmin); break;
-                case 128: dec_static<U, NP, 128>(acc, cs, R, lane, nl, an, invk, dmin); break;
-                default: dec_static<U, NP, 256>(acc, cs, R, lane, nl, an, invk, dmin); break;
+                case 32: dec_static<U, 32>(acc, cs, g, lane, nl, an, invk, dmin); break;
+                case 64: dec_static<U, 64>(acc, cs, g, lane, nl, an, invk, dmin); break;
+                case 128: dec_static<U, 128>(acc, cs, g, lane, nl, an, invk, dmin); break;
+                default: dec_static<U, 256>(acc, cs, g, lane, nl, an, invk, dmin); break;
             }
         } else {
             // ---- generic: per-lane intervals (other factors, or the tile
@@ -481,7 +535,7 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
                     kc = k;
                 }
                 const float uu = fmaf((float)r, twoInvN, -1.f);
-                acc[u] += dec_step<NP>(c0, c1, c2, uu, nl - __float_as_int(c0.x) + 32 * u, R, an,
+                acc[u] += dec_step(c0, c1, c2, uu, nl - __float_as_int(c0.x) + 32 * u, g, an,
                                        invk, dmin);
             }
         }
@@ -502,6 +556,19 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
         const int64_t n = (int64_t)n0 + t2;
         if (n < out_len) dst[n] = s;
     }
+}
+
+// Zero-padded signal plane of the table A/B: xp[row0 + i] = x[i] (the
+// caller zero-fills xp), rows numbered like the branch records.
+__global__ void k_signal_plane(const float* __restrict__ x_all, const int64_t* __restrict__ sig_off,
+                               const int64_t* __restrict__ sig_len,
+                               const int64_t* __restrict__ sig_row0, float* __restrict__ xp) {
+    const int64_t T = sig_len[blockIdx.y];
+    const float* x = x_all + sig_off[blockIdx.y];
+    float* dst = xp + sig_row0[blockIdx.y];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = x[i];
 }
 
 __global__ void k_reduce_f32(const mvb_job* __restrict__ jobs, const float* __restrict__ part,
@@ -767,6 +834,37 @@ int mvb_synthesize_f32(const mvb_job* jobs, const mvb_work* work, int64_t n_work
 #undef MVB_SYNTH_NB
 #undef MVB_SYNTH
     return check_launch("synthesize_f32");
+}
+
+int mvb_signal_plane_f32(const float* x_all, const int64_t* sig_off, const int64_t* sig_len,
+                         const int64_t* sig_row0, int64_t n_sig, int64_t max_len, float* xp,
+                         void* stream) {
+    if (n_sig < 0 || n_sig > 65535 || max_len < 0) return fail(MVB_EINVAL, "signal_plane: sizes");
+    if (n_sig == 0 || max_len == 0) return MVB_OK;
+    if (!x_all || !sig_off || !sig_len || !sig_row0 || !xp) return fail(MVB_EINVAL, "signal_plane: null");
+    unsigned gx = grid_for(max_len, 256);
+    if (gx > 4096) gx = 4096;
+    k_signal_plane<<<dim3(gx, (unsigned)n_sig), 256, 0, as_stream(stream)>>>(x_all, sig_off, sig_len,
+                                                                              sig_row0, xp);
+    return check_launch("signal_plane_f32");
+}
+
+int mvb_synthesize_f32_table(const mvb_job* jobs, const mvb_work* work, int64_t n_work,
+                             const mvb_image* images, const mvb_coef32* coef, const float* xp,
+                             const double* paths, float* out, float* part, const float* table,
+                             int L, void* stream) {
+    if (n_work < 0 || n_work > 0x7fffffff) return fail(MVB_EINVAL, "synthesize_f32_table: n_work");
+    if (n_work == 0) return MVB_OK;
+    if (!jobs || !work || !images || !xp || !paths || !out || !table)
+        return fail(MVB_EINVAL, "synthesize_f32_table: null");
+    if (L < 1 || L > 128) return fail(MVB_EINVAL, "synthesize_f32_table: L");
+    const size_t smem = sizeof(float) * (size_t)(TAB_P + 1) * (L + 1);
+    if (cudaFuncSetAttribute(k_synth_f32<16, 1, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return check_launch("synthesize_f32_table (smem attribute)");
+    k_synth_f32<16, 1, 1, true><<<(unsigned)n_work, SYNTH_WARPS * 32, smem, as_stream(stream)>>>(
+        jobs, work, images, coef, xp, paths, out, part, table);
+    return check_launch("synthesize_f32_table");
 }
 
 int mvb_reduce_partials_f32(const mvb_job* jobs, int64_t n_jobs, int64_t max_out_len,

@@ -992,6 +992,10 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         rec, rec_start = _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev, st,
                                          concat)
     _mark("render.plan_lengths")
+    table = None
+    if FD_GATHER == "table":  # literal per-fraction table, not the product
+        rec, table = _table_records(uniq, sig_dev, sig_len, rec_start, rec.numel() // (
+            4 if nb == 4 else 8 * -(-nb // 8)), f, dev, st, concat)
     for j in range(nJ):
         rows[j].update(rec_base=rec_start[keys[j]], nb=nb, img_off=j * max_seg * max_img,
                        img_stride=max_img)
@@ -1007,9 +1011,14 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         st = stream_handle(dev)
         lengths, err = finalize(jobs_dev, st)
         ev = _events(timing)
-        _lib.call("mvb_synthesize_f32", ptr(jobs_dev), ptr(work_dev), len(work),
-                  ptr(images_sorted), ptr(coef), ptr(rec), ptr(geom.paths), ptr(out), ptr(part),
-                  nb, SYNTH_U, st)
+        if table is not None:
+            _lib.call("mvb_synthesize_f32_table", ptr(jobs_dev), ptr(work_dev), len(work),
+                      ptr(images_sorted), ptr(coef), ptr(rec), ptr(geom.paths), ptr(out),
+                      ptr(part), ptr(table), L, st)
+        else:
+            _lib.call("mvb_synthesize_f32", ptr(jobs_dev), ptr(work_dev), len(work),
+                      ptr(images_sorted), ptr(coef), ptr(rec), ptr(geom.paths), ptr(out),
+                      ptr(part), nb, SYNTH_U, st)
         _events_end(timing, ev)
         if part_rows:
             _lib.call("mvb_reduce_partials_f32", ptr(jobs_dev), nJ, int(out_len.max()),
@@ -1103,6 +1112,41 @@ def _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev, st, c
     _lib.call("mvb_branch_records_f32", ptr(x_all), ptr(sig_tab[0]), ptr(sig_tab[1]),
               ptr(sig_tab[2]), len(ukeys), int(lens.max()), ptr(cb_dev), M1, L, nb, ptr(rec), st)
     return rec, start
+
+
+TAB_P = 512  # mvb.h MVB_TAB_P
+# MVB_FD_GATHER=table: the fast synthesis gathers through the literal
+# per-fraction table instead of the Farrow records (measurement only)
+FD_GATHER = os.environ.get("MVB_FD_GATHER", "farrow")
+
+
+def fraction_table(filt) -> np.ndarray:
+    """(TAB_P + 1, L) fp32 taps h_j(p / TAB_P) = sum_k c_k[j] (p / TAB_P)^k of
+    the filter's Farrow bank (farrow.py:42-63 basis), evaluated in fp64."""
+    f = as_filter(filt)
+    mu = np.arange(TAB_P + 1, dtype=np.float64) / TAB_P
+    powers = mu[:, None] ** np.arange(f.branches.shape[0])[None, :]
+    return np.ascontiguousarray(powers @ np.asarray(f.branches, dtype=np.float64),
+                                dtype=np.float32)
+
+
+def _table_records(uniq, sig_dev, sig_len, start, rec_rows, filt, dev, st, concatenated=None):
+    """The table A/B's inputs: the zero-padded signal plane (one float per
+    branch-record row, same row numbering) and the fraction table."""
+    ukeys = list(uniq)
+    lens = np.asarray([sig_len[k] for k in ukeys], np.int64)
+    if len(ukeys) == 1:
+        x_all = sig_dev[ukeys[0]]
+    elif concatenated is not None:
+        x_all = concatenated
+    else:
+        x_all = torch.cat([sig_dev[k] for k in ukeys])
+    sig_tab = h2d(np.stack([np.concatenate([[0], np.cumsum(lens)[:-1]]), lens,
+                            np.asarray([start[k] for k in ukeys], np.int64)]), dev)
+    xp = torch.zeros(rec_rows, dtype=torch.float32, device=dev)
+    _lib.call("mvb_signal_plane_f32", ptr(x_all), ptr(sig_tab[0]), ptr(sig_tab[1]), ptr(sig_tab[2]),
+              len(ukeys), int(lens.max()), ptr(xp), st)
+    return xp, h2d(fraction_table(filt), dev)
 
 
 def _work_list(n_img, out_len, n_seg, sm_count, rows):

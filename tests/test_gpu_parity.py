@@ -372,3 +372,18 @@ def test_render_plan_image_shards():
                                 for j in range(len(jobs))])
         ref = np.concatenate(_oracle(scenes, chans, g["branches"]))
         assert rel_err(total, ref) <= FP32_TOL
+
+
+def test_fraction_table_gather_ab_matches_oracle(monkeypatch):
+    """The SURVEY H2 A/B kernel (literal per-fraction table, linear in mu,
+    direct L-tap gather; measurement only) renders the same scene within the
+    fp32 bar -- so the A/B compares two correct kernels."""
+    from paper_2508_03065_b200 import engine
+    monkeypatch.setattr(engine, "FD_GATHER", "table")
+    sc = workloads.make_scenes("c3", duration=0.05, max_order=6, tiers=((2, 1), (4, 32), (6, 256)))[0]
+    f = hann_sinc(sc.fd_taps, 14)
+    y = render_jobs(scene_jobs([sc]), f).job(0).double().cpu().numpy()
+    ref = orc.OracleScene(sc.s, sc.pos, sc.mics[0], sc.dims, sc.walls, sc.max_order, sc.tiers,
+                          f.branches, sc.rate).render()
+    assert y.size == ref.size
+    assert rel_err(y, ref) <= 1e-5
