@@ -332,6 +332,46 @@ int mvb_synthesize_f32(const mvb_job* d_jobs, const mvb_work* d_work, int64_t n_
 int mvb_reduce_partials_f32(const mvb_job* d_jobs, int64_t n_jobs, int64_t max_out_len,
                             const float* d_part, float* d_out, void* stream);
 
+/* Single-call render of one (scene, channel) job on the fast engine (fp32
+ * signal and output, fp64 delay anchors): the C counterpart of the
+ * reference's render() / synthesize() (synth.py:291-294, 194-258) for hosts
+ * that bind this ABI directly.  Runs, on `stream`, every step of the fused
+ * path above (enumeration, image records, coarse tracks + bounds, exact
+ * track maximum, interval records, delay sort, branch records, synthesis)
+ * with the Python engine's plan.  The caller keeps the reference's
+ * decimation (trajectory.py:279-298 decimate(): pos[::N] or its low-passed
+ * version) and passes, per tier, the coarse source path (and receiver path
+ * for a moving receiver, K = ceil(T / N) rows each) and the factor's phase
+ * table (trajectory.py:235-257 _phase_table(N), N x 65, row-major).
+ * Writes *h_out_len = len(s) + ceil(rate * max d / c) + L (synth.py:211-212)
+ * and the output into d_out[0 .. out_len); returns MVB_EINVAL (with
+ * *h_out_len set) when out_capacity is too small.  Synchronizes `stream`
+ * once (after the track maximum, which fixes out_len); scratch memory is
+ * stream-ordered.  Up to MVB_DELAY_SORT_MAX images (max_order <= 23). */
+typedef struct mvb_render_args {
+    const float* d_signal;   /* dry signal (n_signal,) fp32                    */
+    int64_t n_signal;
+    const double* d_pos;     /* source path (T, 3) at the audio rate            */
+    int64_t T;
+    const double* d_mic;     /* receiver (3,) or, with mic_moving, (T, 3)        */
+    int32_t mic_moving;
+    int32_t max_order;
+    double dims[3];          /* room (Lx, Ly, Lz)                                */
+    double walls[6];         /* reflection coefficients (-x, +x, -y, +y, -z, +z) */
+    int32_t n_tiers;         /* tier t: orders <= tier_order[t] at 1/tier_factor[t] */
+    int32_t tier_order[MVB_MAX_CLASSES];
+    int32_t tier_factor[MVB_MAX_CLASSES];
+    const double* d_coarse_pos[MVB_MAX_CLASSES]; /* decimated tiers: (K, 3)       */
+    const double* d_coarse_mic[MVB_MAX_CLASSES]; /* moving receiver: (K, 3)      */
+    const double* h_phase_table[MVB_MAX_CLASSES];/* decimated tiers: (N, 65) host */
+    const double* h_branches; /* Farrow bank (poly_order + 1, branch_len), host,
+                                 reference basis sum_k c_k mu^k (farrow.py:42-63) */
+    int32_t poly_order, branch_len, nominal_delay;
+    double rate, c, d_min;
+} mvb_render_args;
+int mvb_render_tracks_and_synthesize(const mvb_render_args* h_args, float* d_out,
+                                     int64_t out_capacity, int64_t* h_out_len, void* stream);
+
 /* SURVEY H2 A/B (measurement only, not the product path): the literal
  * per-fraction-table fractional delay.  mvb_signal_plane_f32 writes the
  * dry signals into a zero-filled fp32 plane d_xp with the branch-record row

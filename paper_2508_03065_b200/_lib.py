@@ -59,6 +59,7 @@ _SIGS = {
     "mvb_block_convolve": [P, I64, I64, I64, I64, INT, P, P, I64, I64, P, I64, P],
     "mvb_splice_sum": [P, I64, I64, I64, I64, I64, P, I64, P, I64, P],
     "mvb_signal_plane_f32": [P, P, P, P, I64, I64, P, P],
+    "mvb_render_tracks_and_synthesize": [P, P, I64, P, P],
     "mvb_synthesize_f32_table": [P, P, I64, P, P, P, P, P, P, P, INT, P],
     "mvb_peak_ffma": [INT, INT, P, P],
     "mvb_peak_dfma": [INT, INT, P, P],
@@ -87,6 +88,22 @@ class ClassTable(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("factor", ctypes.c_int32 * MAX_CLASSES),
                 ("fit", ctypes.c_int32 * MAX_CLASSES), ("count", ctypes.c_int32 * MAX_CLASSES),
                 ("table", ctypes.c_int64 * MAX_CLASSES), ("sel_off", ctypes.c_int64 * MAX_CLASSES)]
+
+
+_P, _D, _I32, _I64 = ctypes.c_void_p, ctypes.c_double, ctypes.c_int32, ctypes.c_int64
+
+
+class RenderArgs(ctypes.Structure):
+    """mvb_render_args (mvb.h): one job of mvb_render_tracks_and_synthesize."""
+
+    _fields_ = [("d_signal", _P), ("n_signal", _I64), ("d_pos", _P), ("T", _I64),
+                ("d_mic", _P), ("mic_moving", _I32), ("max_order", _I32),
+                ("dims", _D * 3), ("walls", _D * 6), ("n_tiers", _I32),
+                ("tier_order", _I32 * MAX_CLASSES), ("tier_factor", _I32 * MAX_CLASSES),
+                ("d_coarse_pos", _P * MAX_CLASSES), ("d_coarse_mic", _P * MAX_CLASSES),
+                ("h_phase_table", _P * MAX_CLASSES), ("h_branches", _P),
+                ("poly_order", _I32), ("branch_len", _I32), ("nominal_delay", _I32),
+                ("rate", _D), ("c", _D), ("d_min", _D)]
 
 
 class MvbError(RuntimeError):
