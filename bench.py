@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the cpu_baseline / reference sample")
+    ap.add_argument("--no-l0", action="store_true",
+                    help="skip the reference-code (baseline/_ref, numba) CPU samples")
     ap.add_argument("--no-per-config", action="store_true",
                     help="headline config only (no per_config block)")
     ap.add_argument("--per-config-steps", type=int, default=10,
@@ -214,6 +216,48 @@ def cpu_sample(name, target_s, nthreads):
     desc = (f"{name} scene 0 ch 0: all {S} images x output samples [{n0}, {n0 + w}) "
             f"(oracle C port, Farrow M=14 Hann-sinc L={sc.fd_taps}, per-sample 65-tap tracks)")
     return S * w / dt, desc, nthreads, S * w, dt
+
+
+def l0_samples(name, nthreads, target_s=6.0):
+    """The reference's OWN code (baseline/_ref, numba asserted; oracle/l0.py):
+    kernel-only block-parallel accumulate on the bench workload (all images,
+    a mid-signal window, tau/amp from the oracle's bit-identical tracks),
+    the same with the reference's default filter design(3, 8, 0.8), and the
+    whole L0 render (tracks + synthesize) of a 1 s c2 scene."""
+    try:
+        from oracle import l0
+        l0.load()
+    except Exception as e:  # noqa: BLE001 -- reported, not fatal
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+    from oracle import oracle as orc
+    from paper_2508_03065_b200 import hann_sinc, workloads
+    cpu_sample(name, 0.2, nthreads)  # builds the cached oracle scene
+    sc, o = _ORACLE_CACHE[name]
+    out = {"kind": "reference (moverb from baseline/_ref, numba)", "threads": nthreads}
+    # the reference's default filter design(3, 8, 0.8), exported from the reference itself
+    g = np.load(os.path.join(ROOT, "tests", "golden", "kernels.npz"))
+    for key, branches in (("kernel", o.branches), ("kernel_design_3_8_0.8", g["design_3_8_08"])):
+        # window sized to ~target_s / 2 of work from a 512-sample probe, capped
+        # so the (S, w) fp64 tau / amp arrays stay within ~3 GB
+        ks = l0.KernelSample(o, branches, sc.T // 2, 512, nthreads)
+        _, dt = ks.run(nthreads)
+        cap = max(512, int(3e9 / (24 * ks.S)))
+        w = int(min(cap, sc.T // 2, 512 * target_s / 2 / max(dt, 1e-4)))
+        ks = l0.KernelSample(o, branches, sc.T // 2, w, nthreads)
+        _, dt = ks.run(nthreads)
+        out[key] = {"value": ks.S * w / dt, "unit": "updates/s", "seconds": dt,
+                    "sample": f"{name}: all {ks.S} images x output samples [{sc.T // 2}, "
+                              f"{sc.T // 2 + w}), _accumulate_numba in 32-image blocks on "
+                              f"{nthreads} threads + pairwise merge ({branches.shape[0]} branches, "
+                              f"{branches.shape[1]} taps)"}
+    sc2 = workloads.make_scenes("c2", duration=1.0)[0]
+    r = l0.render_sample(sc2, hann_sinc(sc2.fd_taps, 14).branches, nthreads)
+    out["render"] = {"value": r["value"], "unit": "updates/s", "tracks_s": r["tracks_s"],
+                     "synthesize_s": r["synthesize_s"], "synthesize_value": r["synthesize_value"],
+                     "sample": "c2 scene, 1 s of dry signal, whole render: per-tier "
+                               "low/high_order_distances(decimate) + merge_streams + "
+                               f"synthesize(workers={nthreads}) (SURVEY 8c L0 composition)"}
+    return out
 
 
 # ----------------------------------------------------------------------------
@@ -691,7 +735,8 @@ def run_ours(args):
                "seconds": dt,
                "matched": "the sample is mid-signal, where every update is non-zero; compare it "
                           "with this line's nonzero_updates_per_s (the GPU metric also counts the "
-                          "exact zeros of S x out_len)"}
+                          "exact zeros of S x out_len)",
+               "l0": l0_samples(args.config, nth) if not args.no_l0 else None}
     line["cpu_baseline"] = cpu
     if per:
         line["per_config"] = {args.config: summary(line, line["clocks"])}
@@ -721,6 +766,7 @@ def run_reference(args):
         total_upd += n_upd
         total_s += dt
     value = total_upd / total_s
+    l0 = None if args.no_l0 else l0_samples(name, nth)
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -737,7 +783,7 @@ def run_reference(args):
         "data": "synthetic (seeded, same generators as the GPU arm)",
         "config": {"workload": name, "sample": desc},
         "cpu_baseline": {"value": value, "unit": "updates/s", "cores": nth, "kind": "port",
-                         "sample": desc},
+                         "sample": desc, "l0": l0},
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

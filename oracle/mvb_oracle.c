@@ -353,6 +353,25 @@ void orc_render_window(const orc_scene* sc, int64_t n0, int64_t n1, double* out,
     orc_parallel_for(nthreads, 0, ntiles, 1, scratch, rw_body, &c);
 }
 
+/* tracks of every image over output samples [n0, n1) (hold-extended past
+ * T, synth.py:213-217): out (S, n1 - n0) row-major, images split over
+ * threads.  Feeds the L0 kernel-only baseline (oracle/l0.py). */
+typedef struct { const orc_scene* sc; int64_t n0, n1; double* out; } tw_ctx;
+
+static void tw_body(void* ctx_, int64_t i0, int64_t i1, void* scratch) {
+    (void)scratch;
+    tw_ctx* c = (tw_ctx*)ctx_;
+    const int64_t w = c->n1 - c->n0;
+    for (int64_t i = i0; i < i1; ++i)
+        for (int64_t k = 0; k < w; ++k) c->out[i * w + k] = track_at(c->sc, i, c->n0 + k);
+}
+
+void orc_tracks_window(const orc_scene* sc, int64_t n0, int64_t n1, double* out, int nthreads) {
+    if (n1 <= n0) return;
+    tw_ctx c = {sc, n0, n1, out};
+    orc_parallel_for(nthreads, 0, sc->S, 16, 0, tw_body, &c);
+}
+
 /* max over images and samples t < T of the track, as synth.py:201 uses it */
 typedef struct { const orc_scene* sc; double* best; } tm_ctx;
 

@@ -73,6 +73,8 @@ def lib():
         L.orc_branch_filter.argtypes = [P, i64, P, i64, i64, P]
         L.orc_render_window.restype = None
         L.orc_render_window.argtypes = [P, i64, i64, P, ctypes.c_int]
+        L.orc_tracks_window.restype = None
+        L.orc_tracks_window.argtypes = [P, i64, i64, P, ctypes.c_int]
         L.orc_track_max.restype = d
         L.orc_track_max.argtypes = [P, ctypes.c_int]
         L.orc_hann_sinc_gather.restype = None
@@ -447,6 +449,14 @@ class OracleScene:
 
     def render(self, nthreads: int = 0) -> np.ndarray:
         return self.render_window(0, self.out_len(nthreads), nthreads)
+
+    def tracks_window(self, n0: int, n1: int, nthreads: int = 0) -> np.ndarray:
+        """(S, n1 - n0) distance tracks of every image (the reference's
+        values: exact per-sample or 65-tap upsampled, hold-extended)."""
+        out = np.empty((len(self.images), max(0, n1 - n0)))
+        sc = self._struct()
+        lib().orc_tracks_window(ctypes.byref(sc), int(n0), int(n1), _p(out), nthreads)
+        return out
 
     def hann_sinc_gather(self, n0: int, n1: int, nthreads: int = 0) -> np.ndarray:
         out = np.empty(max(0, n1 - n0))
