@@ -123,7 +123,7 @@ class KernelSample:
         self.tau_w = tau
         self.f = _ref_filter(branches)
         self.streams = rfarrow.branch_filter(np.asarray(o.s, dtype=np.float64), self.f)
-        self.S = d.shape[0]
+        self.S = tau.shape[0]
         self._k = mv._kernels
         self.run(1, blocks=1)  # numba compile / cache load outside the timing
 
