@@ -30,6 +30,13 @@ extern "C" {
 #define MVB_ECUDA (-2)  /* CUDA launch/runtime error, or no sm_100 device     */
 
 int mvb_abi_version(void);
+/* Bounds-check counters of the checked build (libmvb_checked.so, compiled
+ * with -DMVB_CHECKED: the fast synthesis verifies every gather row, interval
+ * record index, staging size and cp.async alignment; the branch-record and
+ * exact kernels their rows).  Copies up to n counters (one per check, see
+ * csrc/mvb_common.cuh) into h_counts and resets them; returns the number of
+ * counters, or MVB_EINVAL from a normal build (no checks compiled in). */
+int mvb_check_violations(int64_t* h_counts, int n);
 const char* mvb_last_error(void);
 /* Fills SM count and compute capability of the current device. */
 int mvb_device_info(int* h_sm_count, int* h_cc_major, int* h_cc_minor);
@@ -146,7 +153,8 @@ typedef struct mvb_job {
     int32_t img_stride;       /* fast path: images per sort segment in the
                                  delay-sorted table (segment s of this job
                                  starts at img_off + s * img_stride)            */
-    int32_t pad;
+    int32_t rec_rows;         /* rows of the record buffer (bounds checks of
+                                 the checked build, libmvb_checked.so)         */
 } mvb_job;
 
 /* One CTA of the fast synthesis grid: samples [32U*tile, 32U*(tile+1)) of

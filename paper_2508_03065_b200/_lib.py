@@ -12,7 +12,10 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmvb.so")
+# MVB_LIB=checked loads the bounds-checked build (libmvb_checked.so, make
+# checked): same ABI, counters read by check_violations()
+LIB_PATH = os.path.join(_HERE, "libmvb_checked.so" if os.environ.get("MVB_LIB") == "checked"
+                        else "libmvb.so")
 
 _lock = threading.Lock()
 _lib = None
@@ -61,6 +64,7 @@ _SIGS = {
     "mvb_signal_plane_f32": [P, P, P, P, I64, I64, P, P],
     "mvb_render_tracks_and_synthesize": [P, P, I64, P, P],
     "mvb_synthesize_f32_table": [P, P, I64, P, P, P, P, P, P, P, INT, P],
+    "mvb_check_violations": [P, INT],
     "mvb_peak_ffma": [INT, INT, P, P],
     "mvb_peak_dfma": [INT, INT, P, P],
     "mvb_peak_l1": [INT, INT, P, P, P],
@@ -71,7 +75,8 @@ _RESTYPE = {"mvb_last_error": ctypes.c_char_p, "mvb_image_count": I64}
 # one; the query functions launch none) -- feeds launch_count()
 _KERNELS = {"mvb_track_max": 2, "mvb_path_bbox": 2, "mvb_center_paths": 2,
             "mvb_spectrum_index": 2, "mvb_abi_version": 0, "mvb_last_error": 0,
-            "mvb_device_info": 0, "mvb_struct_sizes": 0, "mvb_copy_batch": 0, "mvb_image_count": 0}
+            "mvb_device_info": 0, "mvb_struct_sizes": 0, "mvb_copy_batch": 0, "mvb_image_count": 0,
+            "mvb_check_violations": 0}
 _launches = 0
 
 IMAGE_BYTES, JOB_BYTES, WORK_BYTES, COEF_BYTES = 96, 136, 32, 48
@@ -144,6 +149,14 @@ def call(name: str, *args) -> None:
         msg = lib().mvb_last_error().decode("utf-8", "replace")
         raise MvbError(f"{name} failed ({rc}): {msg}")
     _launches += _KERNELS.get(name, 1)
+
+
+def check_violations():
+    """Per-check violation counters of the checked build (reset on read), or
+    None for the normal build."""
+    buf = (ctypes.c_int64 * 16)()
+    n = lib().mvb_check_violations(buf, 16)
+    return None if n < 0 else [int(buf[i]) for i in range(n)]
 
 
 def launch_count() -> int:

@@ -134,8 +134,9 @@ class _BulkStager:
         self.slabs.append(sl)
         if len(self.slabs) > self.MAX_SLABS:  # drop the smallest idle slab
             idle = [x for x in self.slabs if x is not sl and (x[1] is None or x[1].query())]
-            if idle:
-                self.slabs.remove(min(idle, key=lambda x: x[0].numel()))
+            if idle:  # by identity: list.remove compares tensors elementwise
+                victim = min(idle, key=lambda x: x[0].numel())
+                self.slabs = [x for x in self.slabs if x is not victim]
         return sl
 
     def upload(self, parts, out: torch.Tensor) -> None:

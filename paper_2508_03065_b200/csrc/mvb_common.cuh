@@ -71,4 +71,37 @@ __device__ __forceinline__ double exact_upsample(const double* __restrict__ coar
     return acc;
 }
 
+// Bounds checks of the checked build (-DMVB_CHECKED -> libmvb_checked.so;
+// compute-sanitizer is not available on the GPU pool).  Each translation unit
+// keeps its own device counters; mvb_check_violations sums them.
+enum MvbCheck {
+    CHK_GATHER_ROW = 0,   // fast synthesis: record row outside [0, rec_rows)
+    CHK_RECORD_INDEX,     // interval record k outside [0, n_coarse)
+    CHK_STAGE_SIZE,       // staged records exceed the warp's slot
+    CHK_ALIGN,            // cp.async source / destination not 16-byte aligned
+    CHK_WORK,             // work item outside its sorted image table / segment
+    CHK_BRANCH_ROW,       // branch records: row outside [0, rec_rows)
+    CHK_EXACT_INDEX,      // exact engine: coarse / stream index out of range
+    CHK_COUNT
+};
+#ifdef MVB_CHECKED
+static __device__ unsigned long long mvb_check_counts[CHK_COUNT];
+#define MVB_CHECK(cond, id)                                              \
+    do {                                                                 \
+        if (!(cond)) atomicAdd(&::mvb::mvb_check_counts[(id)], 1ull);      \
+    } while (0)
+// host: add this TU's counters into h (CHK_COUNT entries) and reset them
+static inline void mvb_check_collect(int64_t* h) {
+    unsigned long long c[CHK_COUNT] = {};
+    cudaMemcpyFromSymbol(c, mvb_check_counts, sizeof(c));
+    for (int i = 0; i < CHK_COUNT; ++i) h[i] += (int64_t)c[i];
+    const unsigned long long z[CHK_COUNT] = {};
+    cudaMemcpyToSymbol(mvb_check_counts, z, sizeof(z));
+}
+#else
+#define MVB_CHECK(cond, id) \
+    do {                    \
+    } while (0)
+#endif
+
 }  // namespace mvb

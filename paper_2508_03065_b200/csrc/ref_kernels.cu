@@ -203,6 +203,25 @@ using namespace mvb;
 extern "C" {
 
 int mvb_abi_version(void) { return MVB_ABI_VERSION; }
+
+#ifdef MVB_CHECKED
+void mvb_check_collect_synth(int64_t* h);
+#endif
+
+int mvb_check_violations(int64_t* h_counts, int n) {
+#ifdef MVB_CHECKED
+    if (!h_counts || n < 1) return fail(MVB_EINVAL, "check_violations: args");
+    int64_t c[CHK_COUNT] = {};
+    mvb_check_collect(c);       // this unit's counters
+    mvb_check_collect_synth(c); // the synthesis kernels'
+    for (int i = 0; i < n && i < CHK_COUNT; ++i) h_counts[i] = c[i];
+    return CHK_COUNT;
+#else
+    (void)h_counts;
+    (void)n;
+    return fail(MVB_EINVAL, "check_violations: not a checked build (libmvb_checked.so)");
+#endif
+}
 const char* mvb_last_error(void) { return get_error(); }
 
 int mvb_device_info(int* sm_count, int* cc_major, int* cc_minor) {

@@ -487,6 +487,7 @@ extern "C" int mvb_render_tracks_and_synthesize(const mvb_render_args* a, float*
     Js.nb = nb;
     Js.img_off = 0;
     Js.img_stride = (int32_t)S;
+    Js.rec_rows = (int32_t)rec_rows;
     mvb_job* d_job = mem.get<mvb_job>(1);
     mvb_work* d_work = mem.get<mvb_work>(work.size());
     float* part = nc > 1 ? mem.get<float>(nc * out_len) : nullptr;

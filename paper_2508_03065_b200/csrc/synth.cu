@@ -166,7 +166,9 @@ __device__ __forceinline__ float gather_horner(const float4* __restrict__ R, uns
 template <int NP>
 struct FarrowGather {
     const float4* __restrict__ R;
+    unsigned rows;  // record rows (bounds check of the checked build)
     __device__ __forceinline__ float operator()(unsigned row, float mc) const {
+        MVB_CHECK(row < rows, CHK_GATHER_ROW);
         return gather_horner<NP>(R, row, mc);
     }
 };
@@ -183,7 +185,9 @@ struct TableGather {
     const float* __restrict__ xp;
     const float* tab;  // shared memory
     int L;
+    unsigned rows;
     __device__ __forceinline__ float operator()(unsigned row, float mc) const {
+        MVB_CHECK(row < rows && row >= (unsigned)(L - 1), CHK_GATHER_ROW);
         const float sc = (mc + 0.5f) * (float)TAB_P;
         int p = (int)sc;
         p = p < 0 ? 0 : (p > TAB_P - 1 ? TAB_P - 1 : p);
@@ -319,6 +323,9 @@ __device__ __forceinline__ void stage_records(WarpStage<U>& st, int slot, const 
         const int chunks = 3 * (last - k0 + 1);  // <= 3 (U + 1) for N >= 32
         const char* src = reinterpret_cast<const char*>(coef + q.coef) + 48 * k0;
         char* dst = reinterpret_cast<char*>(st.rec[slot]);
+        MVB_CHECK(k0 >= 0 && last < q.n_coarse, CHK_RECORD_INDEX);
+        MVB_CHECK(chunks <= 3 * WarpStage<U>::RMAX, CHK_STAGE_SIZE);
+        MVB_CHECK(((uintptr_t)src & 15) == 0 && ((uintptr_t)dst & 15) == 0, CHK_ALIGN);
         // at most two 16-byte chunks per lane, no loop
         if (lane < chunks) cp_async16(dst + 16 * lane, src + 16 * lane);
         if (lane + 32 < chunks) cp_async16(dst + 16 * (lane + 32), src + 16 * (lane + 32));
@@ -362,10 +369,12 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
         for (int t = threadIdx.x; t < (TAB_P + 1) * Lt; t += blockDim.x)
             tab_smem[(t / Lt) * (Lt + 1) + t % Lt] = table[t];
         __syncthreads();
-        g = TableGather{rec, tab_smem, Lt};
+        g = TableGather{rec, tab_smem, Lt, (unsigned)Jp->rec_rows};
     } else {
-        g = FarrowGather<NP>{reinterpret_cast<const float4*>(rec)};
+        g = FarrowGather<NP>{reinterpret_cast<const float4*>(rec), (unsigned)Jp->rec_rows};
     }
+    MVB_CHECK(wp->seg >= 0 && (Jp->img_stride == 0 || img_end <= Jp->img_stride) &&
+                  img_begin >= 0 && img_begin <= img_end, CHK_WORK);
     // this tile's delay-sorted image table (sort segment wp->seg)
     const mvb_image* __restrict__ imgs = images + Jp->img_off + (int64_t)wp->seg * Jp->img_stride;
     const float invk = (float)(1.0 / Jp->kappa);
@@ -437,6 +446,7 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
                 A = an * rcp_approx(fmaxf((float)d, dmin));
             } else {
                 const int kT = (T - 1) / N, rT = (T - 1) - kT * N;
+                MVB_CHECK(kT < im.n_coarse, CHK_RECORD_INDEX);
                 const float4* c = reinterpret_cast<const float4*>(coef + im.coef) + 3u * (unsigned)kT;
                 const float4 c0 = __ldg(c), c1 = __ldg(c + 1), c2 = __ldg(c + 2);
                 const float res = track_residual(c1, c2, fmaf((float)rT, 2.0f / (float)N, -1.f));
@@ -530,6 +540,7 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
                     }
                 }
                 if (k != kc) {
+                    MVB_CHECK(k >= 0 && k < im.n_coarse, CHK_RECORD_INDEX);
                     const float4* c = cf4 + 3u * (unsigned)k;
                     c0 = __ldg(c); c1 = __ldg(c + 1); c2 = __ldg(c + 2);
                     kc = k;
@@ -716,8 +727,11 @@ __global__ void __launch_bounds__(F64_WARPS * 32, MINB) k_synth_f64(
 #pragma unroll 5
                 for (int col = 0; col < 65; ++col) {
 #pragma unroll
-                    for (int g = 0; g < F64_G; ++g)
+                    for (int g = 0; g < F64_G; ++g) {
+                        MVB_CHECK(!fast[g] || (base[g] - 32 + col >= 0 && base[g] - 32 + col < nc[g]),
+                                  CHK_EXACT_INDEX);
                         acc[g] = xadd(acc[g], xmul(__ldg(t[g] + col * stride[g]), __ldg(w[g] + col)));
+                    }
                 }
             }
 #pragma unroll
@@ -781,6 +795,10 @@ __global__ void __launch_bounds__(F64_WARPS * 32, MINB) k_synth_f64(
 using namespace mvb;
 
 extern "C" {
+
+#ifdef MVB_CHECKED
+void mvb_check_collect_synth(int64_t* h) { mvb_check_collect(h); }
+#endif
 
 int mvb_branch_records_f32(const float* x_all, const int64_t* sig_off, const int64_t* sig_len,
                            const int64_t* sig_row0, int64_t n_sig, int64_t max_len,

@@ -129,7 +129,7 @@ def pack_jobs(rows: list) -> np.ndarray:
                      r["img_off"], r["n_img"], r["pos_off"], r["mic_off"]]
         i32[j] = [r["T"], r["mic_moving"], r["L"], r["d0"], r["n_chunks"], r["nb"]]
         f64[j] = [r["rate"], r["c"], r["d_min"], r["kappa"]]
-        a[j, 16:17].view(np.int32)[:] = [r.get("img_stride", 0), 0]
+        a[j, 16:17].view(np.int32)[:] = [r.get("img_stride", 0), r.get("rec_rows", 0)]
     return a
 
 
@@ -996,9 +996,10 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     if FD_GATHER == "table":  # literal per-fraction table, not the product
         rec, table = _table_records(uniq, sig_dev, sig_len, rec_start, rec.numel() // (
             4 if nb == 4 else 8 * -(-nb // 8)), f, dev, st, concat)
+    rec_rows = rec.numel() // (1 if table is not None else (4 if nb == 4 else 8 * -(-nb // 8)))
     for j in range(nJ):
         rows[j].update(rec_base=rec_start[keys[j]], nb=nb, img_off=j * max_seg * max_img,
-                       img_stride=max_img)
+                       img_stride=max_img, rec_rows=rec_rows)
     work, part_rows = _work_list(geom.n_img, out_len, n_seg, sm_count, rows)
     _mark("render.records_plan")
     jobs_dev = h2d(pack_jobs(rows), dev)
