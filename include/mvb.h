@@ -266,11 +266,12 @@ int mvb_decimate_rows(const double* d_src, const int64_t* d_rows, int64_t n, int
 
 /* Decimation decision (trajectory.py:316-339) around a cuFFT rFFT:
  * mvb_center_paths: d_out = x - mean over T of each axis of the paths
- * d_x (G, T, 3) (d_scratch: 3 G x 64 doubles; G <= 65535);
+ * d_x (G, T, 3) (d_scratch: 3 G x MVB_SPEC_PARTS doubles; G <= 65535);
  * mvb_spectrum_index: for the rFFT of the centred paths along T (d_spec =
  * complex (G, F, 3), re/im interleaved), for each (path, axis) the first
  * bin whose cumulative power |X|^2 (|X| = hypot) reaches fraction x total
- * -> d_index[3g + a], -1 when all zero (d_scratch: 3 G x 64 doubles). */
+ * -> d_index[3g + a], -1 when all zero (d_scratch: 3 G x MVB_SPEC_PARTS doubles). */
+#define MVB_SPEC_PARTS 256
 int mvb_center_paths(const double* d_x, int64_t G, int64_t T, double* d_scratch, double* d_out,
                      void* stream);
 int mvb_spectrum_index(const double* d_spec, int64_t G, int64_t F, double fraction,
@@ -317,14 +318,19 @@ int mvb_delay_sort(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_j
 /* Fast path: fp32 branch records v'_k = x (*) c'_k (d_cbranch (M1, L) fp64
  * in the centred basis (mu - 1/2)^k, zero branches k >= M1) of n_sig dry
  * signals in one launch: signal q is d_x_all[sig_off[q] ..] of length
- * sig_len[q] (<= max_len), its sample m < len + L - 1 goes to global row
- * sig_row0[q] + m (device arrays).  Layout: row r = the nb branch values
- * contiguous, row stride 16 B for nb = 4, else 32 B * ceil(nb / 8) (nb = 12
- * is padded to 16 floats); rows outside are left as the caller zeroed them.
- * L <= 128; rows < 2^31. */
+ * sig_len[q], its sample m < len + L - 1 goes to global row sig_row0[q] + m
+ * (device arrays).  With d_sig_zlo / d_sig_zhi (global rows, or both NULL)
+ * the rows [zlo, row0) and [row0 + len + L - 1, zhi) -- the zero pads the
+ * synthesis gathers rely on -- are written as zeros in the same launch, so
+ * the buffer need not be zero-filled first.  max_rows: the largest row
+ * count written for one signal (len + L - 1, or zhi - zlo).  Layout: row r =
+ * the nb branch values contiguous, row stride 16 B for nb = 4, else 32 B *
+ * ceil(nb / 8) (nb = 12 is padded to 16 floats, the padding is not
+ * written).  L <= 128; rows < 2^31. */
 int mvb_branch_records_f32(const float* d_x_all, const int64_t* d_sig_off,
-                           const int64_t* d_sig_len, const int64_t* d_sig_row0, int64_t n_sig,
-                           int64_t max_len, const double* d_cbranch, int M1, int L, int nb,
+                           const int64_t* d_sig_len, const int64_t* d_sig_row0,
+                           const int64_t* d_sig_zlo, const int64_t* d_sig_zhi, int64_t n_sig,
+                           int64_t max_rows, const double* d_cbranch, int M1, int L, int nb,
                            float* d_rec, void* stream);
 
 /* Fast synthesis (fp32 I/O, fp64 anchors), one CTA per work item covering

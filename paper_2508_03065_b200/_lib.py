@@ -49,7 +49,7 @@ _SIGS = {
     "mvb_track_coeffs": [P, P, I64, I64, P, P, P, P, P],
     "mvb_sort_keys": [P, P, I64, I64, I64, I64, P, P, P, P],
     "mvb_delay_sort": [P, P, I64, I64, I64, I64, P, P, I64, P, P],
-    "mvb_branch_records_f32": [P, P, P, P, I64, I64, P, INT, INT, INT, P, P],
+    "mvb_branch_records_f32": [P, P, P, P, P, P, I64, I64, P, INT, INT, INT, P, P],
     "mvb_synthesize_f32": [P, P, I64, P, P, P, P, P, P, INT, INT, P],
     "mvb_reduce_partials_f32": [P, I64, I64, P, P, P],
     "mvb_synthesize_f64": [P, I64, I64, P, P, P, P, P, P, P],
@@ -85,6 +85,7 @@ IMAGE_BYTES, JOB_BYTES, WORK_BYTES, COEF_BYTES = 96, 136, 32, 48
 MAX_CLASSES = 8
 DELAY_SORT_MAX = 16384  # mvb.h MVB_DELAY_SORT_MAX
 EXACT_LIST_WORDS = 16386  # mvb.h MVB_EXACT_LIST_WORDS (mvb_track_max scratch)
+SPEC_PARTS = 256  # mvb.h MVB_SPEC_PARTS (mvb_center_paths / mvb_spectrum_index scratch)
 
 
 class ClassTable(ctypes.Structure):

@@ -448,14 +448,13 @@ extern "C" int mvb_render_tracks_and_synthesize(const mvb_render_args* a, float*
     const int64_t row_floats = nb == 4 ? 4 : 8 * ((nb + 7) / 8);
     float* rec = mem.get<float>(rec_rows * row_floats);
     double* d_cb = mem.get<double>(cb.size());
-    int64_t* sig_tab = mem.get<int64_t>(3);
+    int64_t* sig_tab = mem.get<int64_t>(5);
     if (!rec || !d_cb || !sig_tab) return fail(MVB_ECUDA, "render: scratch allocation");
-    const int64_t sig3[3] = {0, n, front};
-    MVB_CUDA(cudaMemsetAsync(rec, 0, 4 * rec_rows * row_floats, st));
+    const int64_t sig5[5] = {0, n, front, 0, rec_rows};  // off, len, row0, zero pads [0, rec_rows)
     MVB_CUDA(cudaMemcpyAsync(d_cb, cb.data(), 8 * cb.size(), cudaMemcpyHostToDevice, st));
-    MVB_CUDA(cudaMemcpyAsync(sig_tab, sig3, sizeof(sig3), cudaMemcpyHostToDevice, st));
-    MVB_TRY(mvb_branch_records_f32(a->d_signal, sig_tab, sig_tab + 1, sig_tab + 2, 1, n, d_cb, M1,
-                                   (int)L, nb, rec, stream));
+    MVB_CUDA(cudaMemcpyAsync(sig_tab, sig5, sizeof(sig5), cudaMemcpyHostToDevice, st));
+    MVB_TRY(mvb_branch_records_f32(a->d_signal, sig_tab, sig_tab + 1, sig_tab + 2, sig_tab + 3,
+                                   sig_tab + 4, 1, rec_rows, d_cb, M1, (int)L, nb, rec, stream));
     // ---- work list: (tile, image chunk) CTAs (engine.py _work_list / _chunking) ----
     int sm = 148, ccmaj = 0, ccmin = 0;
     MVB_TRY(mvb_device_info(&sm, &ccmaj, &ccmin));

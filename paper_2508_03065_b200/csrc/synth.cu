@@ -73,6 +73,8 @@ __global__ void k_branch_records_f32(const float* __restrict__ x_all,
                                      const int64_t* __restrict__ sig_off,
                                      const int64_t* __restrict__ sig_len,
                                      const int64_t* __restrict__ sig_row0,
+                                     const int64_t* __restrict__ sig_zlo,
+                                     const int64_t* __restrict__ sig_zhi,
                                      const double* __restrict__ cb, int M1, int L,
                                      float* __restrict__ rec) {
     constexpr int NB = 4 * NP;
@@ -80,10 +82,26 @@ __global__ void k_branch_records_f32(const float* __restrict__ x_all,
     __shared__ float4 sc[128 * NP];    // tap j, branches 4p..4p+3 at sc[j * NP + p]
     const int B = blockDim.x;
     const int64_t T = sig_len[blockIdx.y];
-    const int64_t m0 = (int64_t)blockIdx.x * B * BR_Q;
-    if (m0 >= T + L - 1) return;
-    const float* __restrict__ x = x_all + sig_off[blockIdx.y];
     const int64_t row0 = sig_row0[blockIdx.y];
+    // rows [mlo, mhi) relative to sample 0: the signal rows [0, T + L - 1)
+    // and, with sig_zlo / sig_zhi, the zero pads around them (written here
+    // so the caller need not zero-fill the buffer)
+    const int64_t mlo = sig_zlo ? sig_zlo[blockIdx.y] - row0 : 0;
+    const int64_t mhi = sig_zhi ? sig_zhi[blockIdx.y] - row0 : T + L - 1;
+    const int64_t m0 = mlo + (int64_t)blockIdx.x * B * BR_Q;
+    if (m0 >= mhi) return;
+    float4* const rows4 = reinterpret_cast<float4*>(rec);
+    if (m0 + BR_Q * B <= 0 || m0 >= T + L - 1) {  // the block lies in a pad: zeros
+        for (int q = 0; q < BR_Q; ++q) {
+            const int64_t m = m0 + threadIdx.x + (int64_t)q * B;
+            if (m >= mhi) break;
+#pragma unroll
+            for (int p = 0; p < NP; ++p)
+                rows4[(size_t)(row0 + m) * row_f4<NP>() + p] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        return;
+    }
+    const float* __restrict__ x = x_all + sig_off[blockIdx.y];
     float* scf = reinterpret_cast<float*>(sc);
     for (int t = threadIdx.x; t < NB * L; t += B) {
         const int j = t / NB, k = t - (t / NB) * NB;
@@ -120,8 +138,8 @@ __global__ void k_branch_records_f32(const float* __restrict__ x_all,
 #pragma unroll
     for (int q = 0; q < BR_Q; ++q) {
         const int64_t m = m0 + threadIdx.x + (int64_t)q * B;
-        if (m >= T + L - 1) break;
-        float4* o = reinterpret_cast<float4*>(rec) + (size_t)(row0 + m) * row_f4<NP>();
+        if (m >= mhi) break;
+        float4* o = rows4 + (size_t)(row0 + m) * row_f4<NP>();
 #pragma unroll
         for (int p = 0; p < NP; ++p)
             o[p] = make_float4(acc[q][4 * p], acc[q][4 * p + 1], acc[q][4 * p + 2], acc[q][4 * p + 3]);
@@ -801,19 +819,22 @@ void mvb_check_collect_synth(int64_t* h) { mvb_check_collect(h); }
 #endif
 
 int mvb_branch_records_f32(const float* x_all, const int64_t* sig_off, const int64_t* sig_len,
-                           const int64_t* sig_row0, int64_t n_sig, int64_t max_len,
+                           const int64_t* sig_row0, const int64_t* sig_zlo,
+                           const int64_t* sig_zhi, int64_t n_sig, int64_t max_rows,
                            const double* cb, int M1, int L, int nb, float* rec, void* stream) {
-    if (n_sig < 0 || n_sig > 65535 || max_len < 1 || L < 1 || L > 128 || M1 < 1 || M1 > nb)
+    if (n_sig < 0 || n_sig > 65535 || max_rows < 1 || L < 1 || L > 128 || M1 < 1 || M1 > nb)
         return fail(MVB_EINVAL, "branch_records: sizes");
     if (n_sig == 0) return MVB_OK;
-    if (!x_all || !sig_off || !sig_len || !sig_row0 || !cb || !rec)
+    if (!x_all || !sig_off || !sig_len || !sig_row0 || !cb || !rec ||
+        ((sig_zlo == nullptr) != (sig_zhi == nullptr)))
         return fail(MVB_EINVAL, "branch_records: null");
     const int block = 256;
     const size_t smem = sizeof(float) * (BR_Q * block + L - 1);
-    const dim3 g(grid_for(max_len + L - 1, BR_Q * block), (unsigned)n_sig);
+    const dim3 g(grid_for(max_rows, BR_Q * block), (unsigned)n_sig);
     cudaStream_t s = as_stream(stream);
 #define MVB_BR(NP) k_branch_records_f32<NP><<<g, block, smem, s>>>(x_all, sig_off, sig_len, \
-                                                                   sig_row0, cb, M1, L, rec)
+                                                                   sig_row0, sig_zlo, sig_zhi, \
+                                                                   cb, M1, L, rec)
     switch (nb) {
         case 4: MVB_BR(1); break;
         case 8: MVB_BR(2); break;

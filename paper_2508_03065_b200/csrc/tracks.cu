@@ -196,57 +196,75 @@ constexpr int BBOX_WORDS = 16;
 
 __device__ __forceinline__ double block_min(double v, double* red) { return -block_max(-v, red); }
 
-// rows[j] = (source path first row, T, receiver first row, receiver moving)
-__global__ void k_path_bbox(const int64_t* __restrict__ rows, const double* __restrict__ paths,
-                            int64_t n_jobs, double* __restrict__ bbox) {
-    __shared__ double red[32];
+// rows[j] = (source path first row, T, receiver first row, receiver moving).
+// Each thread folds its rows (unrolled, independent loads in flight), then
+// the 14 running values reduce in one pass: warp shuffles, one shared-memory
+// exchange, one barrier.
+constexpr int BBOX_THREADS = 256;
+
+__device__ __forceinline__ double red_op(double a, double b, bool lo) { return lo ? fmin(a, b) : fmax(a, b); }
+
+__global__ void __launch_bounds__(BBOX_THREADS) k_path_bbox(const int64_t* __restrict__ rows,
+                                                            const double* __restrict__ paths,
+                                                            int64_t n_jobs, double* __restrict__ bbox) {
+    __shared__ double red[14][BBOX_THREADS / 32];
     const int64_t* R = rows + 4 * blockIdx.y;
     double* part = bbox + BBOX_WORDS * (n_jobs + (int64_t)blockIdx.y * BBOX_PARTS + blockIdx.x);
+    double v[14];
+#pragma unroll
     for (int which = 0; which < 2; ++which) {
         const double* P = paths + 3 * (which == 0 ? R[0] : R[2]);
         const int64_t n = which == 0 || R[3] ? R[1] : 1;
-        double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
-        double step = 0.0;
-        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-             t += (int64_t)gridDim.x * blockDim.x) {
-            double d2 = 0.0;
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                const double v = P[3 * t + a];
-                lo[a] = fmin(lo[a], v);
-                hi[a] = fmax(hi[a], v);
-                if (t + 1 < n) {
-                    const double dv = P[3 * t + 3 + a] - v;
-                    d2 += dv * dv;
-                }
-            }
-            step = fmax(step, d2);
-        }
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const double l = block_min(lo[a], red), h = block_max(hi[a], red);
-            if (threadIdx.x == 0) {
-                part[6 * which + a] = l;
-                part[6 * which + 3 + a] = h;
+        double lo0 = DBL_MAX, lo1 = DBL_MAX, lo2 = DBL_MAX, hi0 = -DBL_MAX, hi1 = -DBL_MAX,
+               hi2 = -DBL_MAX, step = 0.0;
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+#pragma unroll 4
+        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += stride) {
+            const double x = P[3 * t], y = P[3 * t + 1], z = P[3 * t + 2];
+            lo0 = fmin(lo0, x); lo1 = fmin(lo1, y); lo2 = fmin(lo2, z);
+            hi0 = fmax(hi0, x); hi1 = fmax(hi1, y); hi2 = fmax(hi2, z);
+            if (t + 1 < n) {
+                const double dx = P[3 * t + 3] - x, dy = P[3 * t + 4] - y, dz = P[3 * t + 5] - z;
+                step = fmax(step, dx * dx + dy * dy + dz * dz);
             }
         }
-        step = block_max(step, red);
-        if (threadIdx.x == 0) part[12 + which] = sqrt(step) * (1.0 + 1e-12);
+        v[7 * which + 0] = lo0; v[7 * which + 1] = lo1; v[7 * which + 2] = lo2;
+        v[7 * which + 3] = hi0; v[7 * which + 4] = hi1; v[7 * which + 5] = hi2;
+        v[7 * which + 6] = step;
     }
-    if (threadIdx.x == 0) part[14] = part[15] = 0.0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < 14; ++q) {
+        const bool lo = (q % 7) < 3;
+        for (int o = 16; o > 0; o >>= 1) v[q] = red_op(v[q], __shfl_xor_sync(0xffffffffu, v[q], o), lo);
+        if (lane == 0) red[q][warp] = v[q];
+    }
+    __syncthreads();
+    if (threadIdx.x < 14) {
+        const int q = threadIdx.x;
+        const bool lo = (q % 7) < 3;
+        double r = red[q][0];
+        for (int w = 1; w < BBOX_THREADS / 32; ++w) r = red_op(r, red[q][w], lo);
+        // word layout: src lo xyz, src hi xyz, mic lo xyz, mic hi xyz, src step, mic step
+        const int which = q / 7, k = q % 7;
+        if (k < 6) part[6 * which + k] = r;
+        else part[12 + which] = sqrt(r) * (1.0 + 1e-12);
+    }
+    if (threadIdx.x == 14) part[14] = part[15] = 0.0;
 }
 
+// One warp per (job, word): lanes fold the BBOX_PARTS partials, shuffles
+// finish the reduction.
 __global__ void k_bbox_reduce(int64_t n_jobs, double* __restrict__ bbox) {
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= n_jobs) return;
+    const int64_t j = blockIdx.x;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (j >= n_jobs || w >= BBOX_WORDS) return;
     const double* part = bbox + BBOX_WORDS * (n_jobs + j * BBOX_PARTS);
-    for (int w = 0; w < BBOX_WORDS; ++w) {
-        const bool is_lo = w < 12 && (w % 6) < 3;
-        double v = part[w];
-        for (int q = 1; q < BBOX_PARTS; ++q)
-            v = is_lo ? fmin(v, part[BBOX_WORDS * q + w]) : fmax(v, part[BBOX_WORDS * q + w]);
-        bbox[BBOX_WORDS * j + w] = v;
-    }
+    const bool lo = w < 12 && (w % 6) < 3;
+    double v = part[BBOX_WORDS * lane + w];
+    for (int q = lane + 32; q < BBOX_PARTS; q += 32) v = red_op(v, part[BBOX_WORDS * q + w], lo);
+    for (int o = 16; o > 0; o >>= 1) v = red_op(v, __shfl_xor_sync(0xffffffffu, v, o), lo);
+    if (lane == 0) bbox[BBOX_WORDS * j + w] = v;
 }
 
 // Full-rate images: lb = exact distance at the first, middle and last
@@ -697,7 +715,7 @@ __global__ void k_decimate_rows(const double* __restrict__ src, const int64_t* _
 // Mean removal of x (G, T, 3) along T (the reference's x - x.mean()), wide:
 // chunk sums, then every block of the subtraction folds the chunk sums of
 // its path in a fixed order (deterministic, identical in every block).
-constexpr int SPEC_PARTS = 64;
+constexpr int SPEC_PARTS = MVB_SPEC_PARTS;  // blocks per path: enough loads in flight for one path
 
 __device__ __forceinline__ int64_t part_begin(int64_t F, int q) { return (F * q) / SPEC_PARTS; }
 
@@ -724,15 +742,23 @@ __global__ void k_path_sums(const double* __restrict__ x, int64_t T, double* __r
     }
 }
 
+// fold of a path's SPEC_PARTS partial sums of axis a (warp a, fixed order:
+// lane-strided sums then a shuffle tree)
+__device__ __forceinline__ double fold_parts(const double* __restrict__ p, int lane) {
+    double t = 0.0;
+    for (int q = lane; q < SPEC_PARTS; q += 32) t += p[q];
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    return t;
+}
+
 __global__ void k_path_center(const double* __restrict__ x, int64_t T,
                               const double* __restrict__ partial, double* __restrict__ out) {
     __shared__ double mean[3];
     const int64_t g = blockIdx.y;
-    if (threadIdx.x < 3) {
-        const double* p = partial + (g * 3 + threadIdx.x) * SPEC_PARTS;
-        double t = 0.0;
-        for (int q = 0; q < SPEC_PARTS; ++q) t += p[q];
-        mean[threadIdx.x] = t / (double)T;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w < 3) {
+        const double t = fold_parts(partial + (g * 3 + w) * SPEC_PARTS, lane);
+        if (lane == 0) mean[w] = t / (double)T;
     }
     __syncthreads();
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < 3 * T;
@@ -781,21 +807,54 @@ __global__ void __launch_bounds__(256) k_spec_find(const double2* __restrict__ s
     const int64_t row = blockIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double thr = 0.0;
-    if (threadIdx.x == 0) {
-        const double* p = partial + row * SPEC_PARTS;
-        double tot = 0.0;
-        for (int q = 0; q < SPEC_PARTS; ++q) tot += p[q];
-        part = -1;
+    if (w == 0) {
+        // warp 0: lane l holds parts [8l, 8l + 8); an inclusive warp scan of
+        // the lane sums gives every part's prefix; the first part whose
+        // prefix reaches fraction x total is the one to scan bin by bin
+        static_assert(SPEC_PARTS == 256, "8 parts per lane");
+        const double* p = partial + row * SPEC_PARTS + 8 * lane;
+        double loc[8], sum = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            loc[k] = p[k];
+            sum += loc[k];
+        }
+        double inc = sum;
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const double tot = __shfl_sync(0xffffffffu, inc, 31);
+        if (lane == 0) {
+            part = -1;
+            found = 0x7fffffff;
+        }
         if (tot > 0.0) {
             thr = fraction * tot;
-            double acc = 0.0;
-            int q = 0;
-            for (; q < SPEC_PARTS - 1 && acc + p[q] < thr; ++q) acc += p[q];
-            part = q;
-            carry = acc;
-            wsum[0] = thr;
+            // part q is the first with prefix_before(q) + p[q] >= thr (the
+            // last part if rounding keeps every prefix below thr)
+            double acc = inc - sum;  // exclusive prefix of this lane's parts
+            int hit = -1;
+            double hit_acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (hit < 0 && acc + loc[k] >= thr) {
+                    hit = 8 * lane + k;
+                    hit_acc = acc;
+                }
+                acc += loc[k];
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, hit >= 0);
+            const int src = m ? __ffs(m) - 1 : 31;
+            const int q = __shfl_sync(0xffffffffu, hit, src);
+            const double a = __shfl_sync(0xffffffffu, hit_acc, src);
+            if (lane == 0) {
+                part = q >= 0 ? q : SPEC_PARTS - 1;  // rounding: the last part
+                wsum[0] = thr;
+            }
+            if (q >= 0 && lane == 0) carry = a;
+            if (q < 0 && lane == 31) carry = inc - loc[7];  // prefix before the last part
         }
-        found = 0x7fffffff;
     }
     __syncthreads();
     if (part < 0) {
@@ -963,8 +1022,8 @@ int mvb_path_bbox(const int64_t* rows, int64_t n_jobs, const double* paths, doub
     if (n_jobs == 0) return MVB_OK;
     if (!rows || !paths || !bbox) return fail(MVB_EINVAL, "path_bbox: null");
     cudaStream_t s = as_stream(stream);
-    k_path_bbox<<<dim3(BBOX_PARTS, (unsigned)n_jobs), 256, 0, s>>>(rows, paths, n_jobs, bbox);
-    k_bbox_reduce<<<grid_for(n_jobs, 128), 128, 0, s>>>(n_jobs, bbox);
+    k_path_bbox<<<dim3(BBOX_PARTS, (unsigned)n_jobs), BBOX_THREADS, 0, s>>>(rows, paths, n_jobs, bbox);
+    k_bbox_reduce<<<(unsigned)n_jobs, 32 * BBOX_WORDS, 0, s>>>(n_jobs, bbox);
     return check_launch("path_bbox");
 }
 

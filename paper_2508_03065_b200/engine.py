@@ -1089,16 +1089,19 @@ def _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev, st, c
     rows | back pad] with the front pad covering the largest delay bound of
     the jobs using it, so every gather row is in range.  Returns the record
     buffer and, per signal key, the global row of its sample 0."""
-    rec_rows, start = 0, {}
+    rec_rows, start, zlo, zhi = 0, {}, {}, {}
     for k, members in uniq.items():
         front = int(max(tau_bound[j] for j in members)) + L + PAD_MARGIN
         back = front + TILE + PAD_MARGIN
+        zlo[k] = rec_rows
         start[k] = rec_rows + front
         rec_rows += front + sig_len[k] + L - 1 + back
+        zhi[k] = rec_rows
     if rec_rows + int(max(sig_len.values())) + int(max(tau_bound)) + 2 * L >= 2**31 - 0x4B400000:
         raise ValueError("batch too large for 32-bit record rows; split it")
     row_floats = 4 if nb == 4 else 8 * -(-nb // 8)  # mvb.h record layout
-    rec = torch.zeros(rec_rows * row_floats, dtype=torch.float32, device=dev)
+    # no zero fill: the records kernel writes every signal's pads as zeros
+    rec = torch.empty(rec_rows * row_floats, dtype=torch.float32, device=dev)
     ukeys = list(uniq)
     lens = np.asarray([sig_len[k] for k in ukeys], np.int64)
     if len(ukeys) == 1:
@@ -1108,10 +1111,14 @@ def _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev, st, c
     else:
         x_all = torch.cat([sig_dev[k] for k in ukeys])
     sig_tab = h2d(np.stack([np.concatenate([[0], np.cumsum(lens)[:-1]]), lens,
-                            np.asarray([start[k] for k in ukeys], np.int64)]), dev)
+                            np.asarray([start[k] for k in ukeys], np.int64),
+                            np.asarray([zlo[k] for k in ukeys], np.int64),
+                            np.asarray([zhi[k] for k in ukeys], np.int64)]), dev)
     cb_dev = h2d(np.ascontiguousarray(cb), dev)
+    max_rows = max(zhi[k] - zlo[k] for k in ukeys)
     _lib.call("mvb_branch_records_f32", ptr(x_all), ptr(sig_tab[0]), ptr(sig_tab[1]),
-              ptr(sig_tab[2]), len(ukeys), int(lens.max()), ptr(cb_dev), M1, L, nb, ptr(rec), st)
+              ptr(sig_tab[2]), ptr(sig_tab[3]), ptr(sig_tab[4]), len(ukeys), int(max_rows),
+              ptr(cb_dev), M1, L, nb, ptr(rec), st)
     return rec, start
 
 

@@ -141,7 +141,7 @@ def bandwidth_batch_async(x: torch.Tensor, rate: float, energy_fraction: float =
         return lambda: np.zeros(G)
     x = x.contiguous()
     st = stream_handle(x.device)
-    scratch = torch.empty(3 * G * 64, dtype=torch.float64, device=x.device)
+    scratch = torch.empty(3 * G * _lib.SPEC_PARTS, dtype=torch.float64, device=x.device)
     xc = torch.empty_like(x)
     _lib.call("mvb_center_paths", ptr(x), G, T, ptr(scratch), ptr(xc), st)
     spec = torch.fft.rfft(xc, dim=1)  # (G, F, 3) complex128
