@@ -277,6 +277,27 @@ int mvb_center_paths(const double* d_x, int64_t G, int64_t T, double* d_scratch,
 int mvb_spectrum_index(const double* d_spec, int64_t G, int64_t F, double fraction,
                        double* d_scratch, int64_t* d_index, void* stream);
 
+/* Hand-written fp64 FFT path of decimate() (round 2; replaces the cuFFT
+ * calls around the two helpers above).  mvb_fft_c2c: in-place batched
+ * complex FFT (interleaved re/im doubles, rows x n contiguous) of any
+ * length -- mixed-radix Stockham for 7-smooth n, Bluestein otherwise; sign
+ * -1 forward, +1 unnormalised inverse; d_scratch holds
+ * mvb_fft_scratch_elems(rows, n) complex values.
+ * mvb_path_spectrum_index: the whole bandwidth decision of d_x (G, T, 3)
+ * (mean removal, spectrum, energy index -> d_index[3g + a], -1 when all
+ * zero), d_scratch mvb_path_spectrum_scratch(G, T) doubles.
+ * mvb_lowpass_paths: trajectory.py:214-232 _lowpass_columns for every
+ * path of d_x (G, T, 3) -> d_out (G, T, 3), d_scratch
+ * mvb_lowpass_scratch(G, T) doubles. */
+int64_t mvb_fft_scratch_elems(int64_t rows, int64_t n);
+int mvb_fft_c2c(double* d_data, int64_t rows, int64_t n, int sign, double* d_scratch, void* stream);
+int64_t mvb_path_spectrum_scratch(int64_t G, int64_t T);
+int mvb_path_spectrum_index(const double* d_x, int64_t G, int64_t T, double fraction,
+                            double* d_scratch, int64_t* d_index, void* stream);
+int64_t mvb_lowpass_scratch(int64_t G, int64_t T);
+int mvb_lowpass_paths(const double* d_x, int64_t G, int64_t T, double rate, double cutoff,
+                      double* d_scratch, double* d_out, void* stream);
+
 /* Decimation decision helper (trajectory.py:316-339): for each of `rows`
  * power-spectrum rows of length F (fp64, contiguous), the first index whose
  * cumulative energy reaches fraction * row total; -1 for an all-zero row. */

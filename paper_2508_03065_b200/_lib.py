@@ -65,18 +65,27 @@ _SIGS = {
     "mvb_render_tracks_and_synthesize": [P, P, I64, P, P],
     "mvb_synthesize_f32_table": [P, P, I64, P, P, P, P, P, P, P, INT, P],
     "mvb_check_violations": [P, INT],
+    "mvb_fft_scratch_elems": [I64, I64],
+    "mvb_fft_c2c": [P, I64, I64, INT, P, P],
+    "mvb_path_spectrum_scratch": [I64, I64],
+    "mvb_path_spectrum_index": [P, I64, I64, DBL, P, P, P],
+    "mvb_lowpass_scratch": [I64, I64],
+    "mvb_lowpass_paths": [P, I64, I64, DBL, DBL, P, P, P],
     "mvb_peak_ffma": [INT, INT, P, P],
     "mvb_peak_dfma": [INT, INT, P, P],
     "mvb_peak_l1": [INT, INT, P, P, P],
 }
-_RESTYPE = {"mvb_last_error": ctypes.c_char_p, "mvb_image_count": I64}
+_RESTYPE = {"mvb_last_error": ctypes.c_char_p, "mvb_image_count": I64,
+            "mvb_fft_scratch_elems": I64, "mvb_path_spectrum_scratch": I64,
+            "mvb_lowpass_scratch": I64}
 
 # kernels launched by one successful call (entry points not listed launch
 # one; the query functions launch none) -- feeds launch_count()
 _KERNELS = {"mvb_track_max": 2, "mvb_path_bbox": 2, "mvb_center_paths": 2,
             "mvb_spectrum_index": 2, "mvb_abi_version": 0, "mvb_last_error": 0,
             "mvb_device_info": 0, "mvb_struct_sizes": 0, "mvb_copy_batch": 0, "mvb_image_count": 0,
-            "mvb_check_violations": 0}
+            "mvb_check_violations": 0, "mvb_fft_scratch_elems": 0,
+            "mvb_path_spectrum_scratch": 0, "mvb_lowpass_scratch": 0}
 _launches = 0
 
 IMAGE_BYTES, JOB_BYTES, WORK_BYTES, COEF_BYTES = 96, 136, 32, 48

@@ -2,7 +2,7 @@
 
 Trajectory mirrors reference trajectory.py:29-60.  The decimation decision
 (trajectory.py:279-298: low-pass only when Nyquist_out < bandwidth <
-2 Nyquist_out) is taken on the device with torch.fft; the per-factor
+2 Nyquist_out) is taken on the device with libmvb's own fp64 FFT; the per-factor
 Kaiser-windowed-sinc phase table (trajectory.py:235-257) is a cached host
 constant like the reference's lru_cache, from which two device constants
 are derived:
@@ -14,6 +14,8 @@ are derived:
 """
 
 from __future__ import annotations
+
+import os
 
 from dataclasses import dataclass
 from functools import lru_cache
@@ -119,6 +121,11 @@ def device_constants(factor: int, device) -> dict:
     return c
 
 
+# MVB_BW_CUFFT=1: the bandwidth decision through cuFFT (round-1 route), for A/B
+# measurements only; the default is libmvb's own FFT
+_BW_CUFFT = os.environ.get("MVB_BW_CUFFT") == "1"
+
+
 def bandwidth_batch(x: torch.Tensor, rate: float, energy_fraction: float = 0.99) -> np.ndarray:
     return bandwidth_batch_async(x, rate, energy_fraction)()
 
@@ -132,25 +139,28 @@ def bandwidth_batch_async(x: torch.Tensor, rate: float, energy_fraction: float =
     """Per-path smallest frequency holding `energy_fraction` of the
     mean-removed displacement power, max over axes (reference
     trajectory.py:316-339), for x (G, T, 3) on the device -> host (G,).
-    libmvb removes each axis' mean, cuFFT (torch.fft) transforms the paths
-    along time, libmvb finds each axis' energy index; one small
-    device->host copy.
+    One libmvb call (mvb_path_spectrum_index: mean removal, the hand-written
+    fp64 FFT, energy index per axis), one small device->host copy.
     Frequencies follow numpy.fft.rfftfreq: k * (1 / (T * (1 / rate)))."""
     G, T, _ = x.shape
     if T < 2 or G == 0:
         return lambda: np.zeros(G)
     x = x.contiguous()
     st = stream_handle(x.device)
-    scratch = torch.empty(3 * G * _lib.SPEC_PARTS, dtype=torch.float64, device=x.device)
-    xc = torch.empty_like(x)
-    _lib.call("mvb_center_paths", ptr(x), G, T, ptr(scratch), ptr(xc), st)
-    spec = torch.fft.rfft(xc, dim=1)  # (G, F, 3) complex128
-    if not spec.is_contiguous():
-        spec = spec.contiguous()
-    F = spec.shape[1]
+    F = T // 2 + 1
     k = torch.empty(G * 3, dtype=torch.int64, device=x.device)
-    _lib.call("mvb_spectrum_index", ptr(spec), G, F, float(energy_fraction), ptr(scratch), ptr(k),
-              st)
+    if _BW_CUFFT:  # diagnostic A/B only: the round-1 cuFFT route
+        scratch = torch.empty(3 * G * _lib.SPEC_PARTS, dtype=torch.float64, device=x.device)
+        xc = torch.empty_like(x)
+        _lib.call("mvb_center_paths", ptr(x), G, T, ptr(scratch), ptr(xc), st)
+        spec = torch.fft.rfft(xc, dim=1).contiguous()
+        _lib.call("mvb_spectrum_index", ptr(spec), G, F, float(energy_fraction), ptr(scratch),
+                  ptr(k), st)
+    else:
+        scratch = torch.empty(int(_lib.lib().mvb_path_spectrum_scratch(G, T)),
+                              dtype=torch.float64, device=x.device)
+        _lib.call("mvb_path_spectrum_index", ptr(x), G, T, float(energy_fraction), ptr(scratch),
+                  ptr(k), st)
     host = pinned_scratch(slot, k.numel(), k.dtype)
     host.copy_(k, non_blocking=True)
     done = torch.cuda.Event()
@@ -182,21 +192,16 @@ def bandwidth_estimate_dev(pos: torch.Tensor, rate: float, energy_fraction: floa
 
 def lowpass_batch(x: torch.Tensor, rate: float, cutoff: float) -> torch.Tensor:
     """Raised-cosine-edged FFT low-pass with odd reflection padding
-    (reference trajectory.py:214-232) of x (G, T, 3) on the device."""
-    n = x.shape[1]
-    pad = min(n - 1, max(16, n // 4))
-    head = 2 * x[:, :1] - torch.flip(x[:, 1:pad + 1], dims=[1])
-    tail = 2 * x[:, -1:] - torch.flip(x[:, -pad - 1:-1], dims=[1])
-    ext = torch.cat([head, x, tail], dim=1).permute(0, 2, 1).contiguous()  # (G, 3, m)
-    m = ext.shape[2]
-    f = torch.arange(m // 2 + 1, device=x.device, dtype=torch.float64) * (rate / m)
-    lo, hi = 0.8 * cutoff, cutoff
-    g = torch.ones_like(f)
-    band = (f > lo) & (f <= hi)
-    g = torch.where(band, 0.5 * (1 + torch.cos(np.pi * (f - lo) / (hi - lo))), g)
-    g = torch.where(f > hi, torch.zeros_like(g), g)
-    y = torch.fft.irfft(torch.fft.rfft(ext, dim=2) * g, n=m, dim=2)
-    return y[:, :, pad:pad + n].permute(0, 2, 1)
+    (reference trajectory.py:214-232) of x (G, T, 3) on the device: one
+    libmvb call (mvb_lowpass_paths, hand-written fp64 FFT)."""
+    x = x.to(torch.float64).contiguous()
+    G, T, _ = x.shape
+    out = torch.empty_like(x)
+    scratch = torch.empty(int(_lib.lib().mvb_lowpass_scratch(G, T)), dtype=torch.float64,
+                          device=x.device)
+    _lib.call("mvb_lowpass_paths", ptr(x), G, T, float(rate), float(cutoff), ptr(scratch),
+              ptr(out), stream_handle(x.device))
+    return out
 
 
 def lowpass_columns_dev(x: torch.Tensor, rate: float, cutoff: float) -> torch.Tensor:

@@ -264,7 +264,12 @@ def test_edge_cases_match_oracle(case):
         n = 20
     tr = moving(T) if T > 1 else static([2.0, 3.0, 2.0], 1)
     x = rng.standard_normal(n)
-    for xx, tol in ((x, 1e-13), (x.astype(np.float32), 1e-5)):
+    # fp64: 1e-13 of the peak; 1e-12 when decimate()'s anti-alias low-pass runs
+    # (odd_factor_fast: the path's bandwidth falls in (Nyquist_out, 2 Nyquist_out)):
+    # libmvb's FFT and the oracle's pocketfft round differently (~1e-15 m in the
+    # coarse path), still far inside the north_star's 1e-10 fp64 bar
+    tol64 = 1e-12 if case == "odd_factor_fast" else 1e-13
+    for xx, tol in ((x, tol64), (x.astype(np.float32), 1e-5)):
         y = mvb.render(xx, tr, ROOM, MIC, f, cfg)
         ref = oracle_render(np.asarray(xx, np.float64), tr, MIC, f, cfg)
         assert y.size == ref.size, case
