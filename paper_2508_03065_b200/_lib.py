@@ -16,6 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # checked): same ABI, counters read by check_violations()
 LIB_PATH = os.path.join(_HERE, "libmvb_checked.so" if os.environ.get("MVB_LIB") == "checked"
                         else "libmvb.so")
+LIB_PATH = os.environ.get("MVB_LIB_PATH", LIB_PATH)  # A/B of another build (diagnostics)
 
 _lock = threading.Lock()
 _lib = None
