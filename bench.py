@@ -467,6 +467,105 @@ def measure(ctx, name, steps, warmup, peaks, args, precision=None, with_e2e=True
     plan = None
     gc.collect()
     torch.cuda.empty_cache()
+    def plan_e2e():
+        # batch / multi-rank: the public API for repeated renders of one
+        # structure (RenderPlan) fed from host arrays in pinned memory --
+        # H2D of every signal / path / receiver, the render (+ reduce to
+        # rank 0) and the D2H of the output inside every timed step
+        from dataclasses import replace as _replace
+
+        from paper_2508_03065_b200.plan import RenderPlan
+        from paper_2508_03065_b200.synth import scene_jobs
+
+        def pinned(a):
+            a = np.ascontiguousarray(a)
+            t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+            out = t.numpy()
+            np.copyto(out, a)
+            return out
+
+        host_jobs = [_replace(jb, s=pinned(jb.s), pos=pinned(jb.pos), mic=pinned(jb.mic))
+                     for jb in scene_jobs(mine)]
+        # shared paths / signals stay shared (one pinned copy per key)
+        by_key = {}
+        for j, jb in enumerate(host_jobs):
+            pk, sk = jb.path_key, jb.signal_key
+            if pk is not None:
+                host_jobs[j] = _replace(host_jobs[j], pos=by_key.setdefault(("p", pk), jb.pos))
+            if sk is not None:
+                host_jobs[j] = _replace(host_jobs[j], s=by_key.setdefault(("s", sk), jb.s))
+        plan_e = RenderPlan(host_jobs, f, precision=precision, shard=shard)
+        tt = 0.0
+        upd = 0
+        h2d = sum(sc.s.nbytes + sc.pos.nbytes + sum(np.asarray(m).nbytes for m in sc.mics)
+                  for sc in mine)
+        d2h = 0
+        for _ in range(max(4, warmup)):  # captures both slots, then replays
+            r = plan_e.run(host_jobs)
+            if shard is not None:
+                plan_e.reduce(r)
+            if shard is None or rank == 0:
+                r.host()
+        # (a) one render per timed step, synchronous (host staging, H2D,
+        # render, D2H back to back)
+        for _ in range(steps):
+            torch.cuda.synchronize()
+            ctx.barrier()
+            t0 = time.perf_counter()
+            r = plan_e.run(host_jobs)
+            if shard is not None:
+                plan_e.reduce(r)
+            out_h = r.host() if (shard is None or rank == 0) else None
+            torch.cuda.synchronize()
+            ctx.barrier()
+            tt += time.perf_counter() - t0
+            upd += r.updates
+            d2h = 0 if out_h is None else out_h.nbytes
+        # (b) pipelined: run(k + 1) is issued before host(k), so step k+1's
+        # host staging and H2D overlap step k's device work; every step
+        # still copies its inputs in and its output out inside the bracket
+        torch.cuda.synchronize()
+        ctx.barrier()
+        t0 = time.perf_counter()
+        prev, upd_p = None, 0
+
+        def collect(res_k):
+            # the step's D2H (root) and its update count, before the
+            # slot is reused two runs later
+            if shard is None or rank == 0:
+                res_k.host()
+            return res_k.updates
+
+        for _ in range(steps):
+            r = plan_e.run(host_jobs)
+            if shard is not None:
+                plan_e.reduce(r)
+            if prev is not None:
+                upd_p += collect(prev)
+            prev = r
+        upd_p += collect(prev)
+        plan_e.join()
+        torch.cuda.synchronize()
+        ctx.barrier()
+        tp = time.perf_counter() - t0
+        del plan_e, r, prev
+        gc.collect()
+        torch.cuda.empty_cache()
+        tt_t = torch.tensor([tt, float(upd), tp, float(upd_p)], dtype=torch.float64, device=dev)
+        if world > 1:
+            tmax = ctx.allreduce(tt_t.clone(), dist.ReduceOp.MAX)
+            tsum = ctx.allreduce(tt_t.clone(), dist.ReduceOp.SUM)
+            tt, upd, tp, upd_p = float(tmax[0]), float(tsum[1]), float(tmax[2]), float(tsum[3])
+        e2e_p = {"value": upd_p / tp, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h),
+               "api": "paper_2508_03065_b200.RenderPlan.run (repeated renders of one "
+                      "structure) + RenderResult.host(), pipelined: run(k+1) is issued "
+                      "before host(k)",
+               "sync_value": upd / tt,
+               "sync": "the same with run + host back to back per step (no overlap)",
+               "inputs": "pinned host memory, copied to the device inside every timed step"}
+        return e2e_p
+
     e2e = None
     if with_e2e and not args.no_e2e:
         if world == 1 and len(scenes) == 1 and len(scenes[0].mics) == 1:
@@ -502,71 +601,12 @@ def measure(ctx, name, steps, warmup, peaks, args, precision=None, with_e2e=True
                              "page-locked), copied to the device inside every timed call; "
                              "output returned as float64 numpy (8 B per sample)",
                    "ms_per_call": [round(c * 1e3, 3) for c in calls]}
+            # the same render through RenderPlan from the same host buffers,
+            # pipelined (repeated renders of one structure: dataset generation)
+            pe = plan_e2e()
+            e2e["plan_pipelined"] = {k: pe[k] for k in ("value", "sync_value", "api")}
         else:
-            # batch / multi-rank: the public API for repeated renders of one
-            # structure (RenderPlan) fed from host arrays in pinned memory --
-            # H2D of every signal / path / receiver, the render (+ reduce to
-            # rank 0) and the D2H of the output inside every timed step
-            from dataclasses import replace as _replace
-
-            from paper_2508_03065_b200.plan import RenderPlan
-            from paper_2508_03065_b200.synth import scene_jobs
-
-            def pinned(a):
-                a = np.ascontiguousarray(a)
-                t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
-                out = t.numpy()
-                np.copyto(out, a)
-                return out
-
-            host_jobs = [_replace(jb, s=pinned(jb.s), pos=pinned(jb.pos), mic=pinned(jb.mic))
-                         for jb in scene_jobs(mine)]
-            # shared paths / signals stay shared (one pinned copy per key)
-            by_key = {}
-            for j, jb in enumerate(host_jobs):
-                pk, sk = jb.path_key, jb.signal_key
-                if pk is not None:
-                    host_jobs[j] = _replace(host_jobs[j], pos=by_key.setdefault(("p", pk), jb.pos))
-                if sk is not None:
-                    host_jobs[j] = _replace(host_jobs[j], s=by_key.setdefault(("s", sk), jb.s))
-            plan_e = RenderPlan(host_jobs, f, precision=precision, shard=shard)
-            tt = 0.0
-            upd = 0
-            h2d = sum(sc.s.nbytes + sc.pos.nbytes + sum(np.asarray(m).nbytes for m in sc.mics)
-                      for sc in mine)
-            d2h = 0
-            for _ in range(max(4, warmup)):  # captures both slots, then replays
-                r = plan_e.run(host_jobs)
-                if shard is not None:
-                    plan_e.reduce(r)
-                if shard is None or rank == 0:
-                    r.host()
-            for _ in range(steps):
-                torch.cuda.synchronize()
-                ctx.barrier()
-                t0 = time.perf_counter()
-                r = plan_e.run(host_jobs)
-                if shard is not None:
-                    plan_e.reduce(r)
-                out_h = r.host() if (shard is None or rank == 0) else None
-                torch.cuda.synchronize()
-                ctx.barrier()
-                tt += time.perf_counter() - t0
-                upd += r.updates
-                d2h = 0 if out_h is None else out_h.nbytes
-            del plan_e, r
-            gc.collect()
-            torch.cuda.empty_cache()
-            tt_t = torch.tensor([tt, float(upd)], dtype=torch.float64, device=dev)
-            if world > 1:
-                tmax = ctx.allreduce(tt_t.clone(), dist.ReduceOp.MAX)
-                tt_t = ctx.allreduce(tt_t, dist.ReduceOp.SUM)
-                tt, upd = float(tmax[0]), float(tt_t[1])
-            e2e = {"value": upd / tt, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
-                   "d2h_bytes_per_step": int(d2h),
-                   "api": "paper_2508_03065_b200.RenderPlan.run (repeated renders of one "
-                          "structure) + RenderResult.host()",
-                   "inputs": "pinned host memory, copied to the device inside every timed step"}
+            e2e = plan_e2e()
 
     # ---- roofline of the dominant kernel (fused synthesis) --------------------
     kern_avg_ms = float(np.mean(kern_ms)) if kern_ms else float("nan")
