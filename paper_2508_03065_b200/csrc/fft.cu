@@ -167,6 +167,9 @@ int stockham(double2* a, double2* b, int64_t rows, int64_t n, int sign, cudaStre
     for (int R : rad) {
         const int64_t items = rows * (n / R);
         const unsigned g = grid_for(items, 256);
+        prefer_carveout(R == 2 ? (const void*)k_fft_pass<2> : R == 3 ? (const void*)k_fft_pass<3>
+                        : R == 4 ? (const void*)k_fft_pass<4> : R == 5 ? (const void*)k_fft_pass<5>
+                                                                  : (const void*)k_fft_pass<7>);
         switch (R) {
             case 2: k_fft_pass<2><<<g, 256, 0, s>>>(src, dst, n, Ns, rows, sign); break;
             case 3: k_fft_pass<3><<<g, 256, 0, s>>>(src, dst, n, Ns, rows, sign); break;
@@ -247,15 +250,19 @@ int fft_c2c(double2* d, int64_t rows, int64_t n, int sign, double2* scratch, cud
     double2* a2 = scratch + rows * M;     // rows x M
     double2* b = scratch + 2 * rows * M;  // M
     double2* b2 = b + M;                  // M
+    prefer_carveout((const void*)k_blue_pre);
     k_blue_pre<<<grid_for(rows * M, 256), 256, 0, s>>>(d, a, rows, n, M, sign);
+    prefer_carveout((const void*)k_blue_kernel);
     k_blue_kernel<<<grid_for(M, 256), 256, 0, s>>>(b, n, M, sign);
     int rc = stockham(a, a2, rows, M, -1, s);
     if (rc) return rc;
     rc = stockham(b, b2, 1, M, -1, s);
     if (rc) return rc;
+    prefer_carveout((const void*)k_blue_mul);
     k_blue_mul<<<grid_for(rows * M, 256), 256, 0, s>>>(a, b, rows, M);
     rc = stockham(a, a2, rows, M, +1, s);
     if (rc) return rc;
+    prefer_carveout((const void*)k_blue_post);
     k_blue_post<<<grid_for(rows * n, 256), 256, 0, s>>>(a, d, rows, n, M, sign);
     return check_launch("fft bluestein");
 }
@@ -554,12 +561,17 @@ int mvb_path_spectrum_index(const double* d_x, int64_t G, int64_t T, double frac
     double2* fs = z + P * T;
     double* part = reinterpret_cast<double*>(fs + fft_scratch_elems(P, T));  // P x PARTS
     double* mean = part + P * PARTS;                                          // P
+    prefer_carveout((const void*)k_row_partials);
     k_row_partials<<<dim3(PARTS, (unsigned)P), 256, 0, s>>>(d_x, T, part);
+    prefer_carveout((const void*)k_row_means);
     k_row_means<<<(unsigned)P, 32, 0, s>>>(part, T, mean);
+    prefer_carveout((const void*)k_pack_centred);
     k_pack_centred<<<grid_for(P * n, 256), 256, 0, s>>>(d_x, G, T, mean, z);
     const int rc = fft_c2c(z, P, n, -1, fs, s);
     if (rc) return rc;
+    prefer_carveout((const void*)k_power_partials);
     k_power_partials<<<dim3(PARTS, (unsigned)P), 256, 0, s>>>(z, n, F, half, part);
+    prefer_carveout((const void*)k_power_find);
     k_power_find<<<(unsigned)P, IDX_THREADS, 0, s>>>(z, n, F, fraction, half, part, d_index);
     return check_launch("path_spectrum_index");
 }
@@ -584,12 +596,15 @@ int mvb_lowpass_paths(const double* d_x, int64_t G, int64_t T, double rate, doub
     const int64_t m = T + 2 * pad, Q = (3 * G + 1) / 2;
     double2* z = reinterpret_cast<double2*>(d_scratch);
     double2* fs = z + Q * m;
+    prefer_carveout((const void*)k_pack_ext);
     k_pack_ext<<<grid_for(Q * m, 256), 256, 0, s>>>(d_x, G, T, pad, m, z);
     int rc = fft_c2c(z, Q, m, -1, fs, s);
     if (rc) return rc;
+    prefer_carveout((const void*)k_lowpass_gain);
     k_lowpass_gain<<<grid_for(Q * m, 256), 256, 0, s>>>(z, Q, m, rate, cutoff);
     rc = fft_c2c(z, Q, m, +1, fs, s);
     if (rc) return rc;
+    prefer_carveout((const void*)k_unpack_crop);
     k_unpack_crop<<<grid_for(3 * G * T, 256), 256, 0, s>>>(z, G, T, pad, m, d_out);
     return check_launch("lowpass_paths");
 }

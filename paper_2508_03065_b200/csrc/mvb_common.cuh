@@ -8,6 +8,9 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <set>
 #include <string>
 
 #include "mvb.h"
@@ -29,6 +32,23 @@ inline int check_launch(const char* what) {
 }
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// MVB_CARVEOUT=<percent> (diagnostic): every libmvb kernel prefers the same
+// shared-memory carveout, so kernels of different streams can share an SM
+// without the SM draining to reconfigure its L1 / shared split.  Unset: the
+// driver's per-kernel choice.
+inline void prefer_carveout(const void* kernel) {
+    static const int pct = [] {
+        const char* e = getenv("MVB_CARVEOUT");
+        return e ? atoi(e) : -1;
+    }();
+    if (pct < 0) return;
+    static std::mutex mu;
+    static std::set<const void*> seen;
+    std::lock_guard<std::mutex> g(mu);
+    if (seen.insert(kernel).second)
+        cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
 
 inline unsigned grid_for(int64_t n, int block) {
     int64_t g = (n + block - 1) / block;

@@ -279,6 +279,7 @@ int mvb_distance_streams(const double* off, const double* sgn, const double* mic
     if (S == 0 || T == 0) return MVB_OK;
     if (!off || !sgn || !mic || !pos || !out) return fail(MVB_EINVAL, "distance_streams: null");
     dim3 g(grid_for(T, 256), (unsigned)S);
+    prefer_carveout((const void*)k_distance);
     k_distance<<<g, 256, 0, as_stream(stream)>>>(off, sgn, mic, pos, S, T, out);
     return check_launch("distance_streams");
 }
@@ -289,6 +290,7 @@ int mvb_accumulate_images(double* out, int64_t out_len, const double* streams, i
     if (out_len < 0 || S < 0 || nb < 1 || ls < 0) return fail(MVB_EINVAL, "accumulate: bad sizes");
     if (out_len == 0 || S == 0) return MVB_OK;
     if (!out || !streams || !tau || !amp) return fail(MVB_EINVAL, "accumulate: null");
+    prefer_carveout((const void*)k_accumulate);
     k_accumulate<<<grid_for(out_len, 128), 128, 0, as_stream(stream)>>>(out, out_len, streams, nb,
                                                                         ls, tau, amp, S, offset, d0);
     return check_launch("accumulate_images");
@@ -302,6 +304,7 @@ int mvb_upsample_streams(const double* coarse, int64_t rows, int64_t nc, const d
     if (rows == 0 || out_len == 0) return MVB_OK;
     if (!coarse || !table || !out) return fail(MVB_EINVAL, "upsample: null");
     dim3 g(grid_for(out_len, 256), (unsigned)rows);
+    prefer_carveout((const void*)k_upsample);
     k_upsample<<<g, 256, 0, as_stream(stream)>>>(coarse, rows, nc, table, factor, ntaps, out_len, out);
     return check_launch("upsample_streams");
 }
@@ -311,6 +314,7 @@ int mvb_branch_filter(const double* x, int64_t T, const double* br, int64_t nb, 
     if (T < 1 || nb < 1 || L < 1 || nb > 65535) return fail(MVB_EINVAL, "branch_filter: bad sizes");
     if (!x || !br || !out) return fail(MVB_EINVAL, "branch_filter: null");
     dim3 g(grid_for(T + L - 1, 256), (unsigned)nb);
+    prefer_carveout((const void*)k_branch_filter);
     k_branch_filter<<<g, 256, 0, as_stream(stream)>>>(x, T, br, nb, L, out);
     return check_launch("branch_filter");
 }
@@ -339,6 +343,7 @@ int mvb_enumerate(const double* dims, const double* walls, int64_t n_rooms, int 
         if (e != cudaSuccess) return fail(MVB_ECUDA, cudaGetErrorString(e));
     }
     dim3 g((unsigned)(max_order + 1), (unsigned)n_rooms, (unsigned)((nmax + 255) / 256));
+    prefer_carveout((const void*)k_enumerate);
     k_enumerate<<<g, 256, smem, as_stream(stream)>>>(dims, walls, max_order, S, lattice, parity,
                                                     order, beta, offset, sign);
     return check_launch("enumerate");

@@ -265,6 +265,7 @@ int mvb_static_taps(const double* off, const double* sgn, const double* beta, in
         if (term < 1e-17 * i0b) break;
     }
     const int64_t total = B * S * NK;
+    prefer_carveout((const void*)k_static_kernel);
     k_static_kernel<<<grid_for(total, 256), 256, 0, as_stream(stream)>>>(
         off, sgn, beta, S, src, B, mic, rate, c, d_min, 1.0 / i0b, base, tau, ker);
     return check_launch("static_taps");
@@ -277,6 +278,7 @@ int mvb_static_gather(const int64_t* base_sorted, const int64_t* perm, const dou
     if (B == 0) return MVB_OK;
     if (!base_sorted || !perm || !ker || !n_taps || !taps) return fail(MVB_EINVAL, "static_gather: null");
     dim3 g(grid_for(stride, 256), (unsigned)B);
+    prefer_carveout((const void*)k_static_gather);
     k_static_gather<<<g, 256, 0, as_stream(stream)>>>(base_sorted, perm, ker, S, n_taps, stride, taps);
     return check_launch("static_gather");
 }
@@ -290,6 +292,7 @@ int mvb_block_convolve(const double* x, int64_t n, int64_t hop, int64_t crossfad
         return fail(MVB_EINVAL, "block_convolve: bad sizes");
     if (!x || !taps || !n_taps || !pieces) return fail(MVB_EINVAL, "block_convolve: null");
     dim3 g(grid_for(max_piece, CONV_TILE), (unsigned)n_blocks);
+    prefer_carveout((const void*)k_block_conv);
     k_block_conv<<<g, CONV_THREADS, 0, as_stream(stream)>>>(x, n, hop, crossfade, n_blocks,
                                                           windowed, taps, n_taps, tap_stride,
                                                           pieces, piece_stride);
@@ -303,6 +306,7 @@ int mvb_splice_sum(const double* pieces, int64_t piece_stride, int64_t n, int64_
         return fail(MVB_EINVAL, "splice_sum: bad sizes");
     if (out_len == 0) return MVB_OK;
     if (!pieces || !n_taps || !out) return fail(MVB_EINVAL, "splice_sum: null");
+    prefer_carveout((const void*)k_splice_sum);
     k_splice_sum<<<grid_for(out_len, 256), 256, 0, as_stream(stream)>>>(
         pieces, piece_stride, n, hop, crossfade, n_blocks, n_taps, max_span, out, out_len);
     return check_launch("splice_sum");

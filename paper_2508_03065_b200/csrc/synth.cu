@@ -832,7 +832,8 @@ int mvb_branch_records_f32(const float* x_all, const int64_t* sig_off, const int
     const size_t smem = sizeof(float) * (BR_Q * block + L - 1);
     const dim3 g(grid_for(max_rows, BR_Q * block), (unsigned)n_sig);
     cudaStream_t s = as_stream(stream);
-#define MVB_BR(NP) k_branch_records_f32<NP><<<g, block, smem, s>>>(x_all, sig_off, sig_len, \
+#define MVB_BR(NP) prefer_carveout((const void*)k_branch_records_f32<NP>); \
+    k_branch_records_f32<NP><<<g, block, smem, s>>>(x_all, sig_off, sig_len, \
                                                                    sig_row0, sig_zlo, sig_zhi, \
                                                                    cb, M1, L, rec)
     switch (nb) {
@@ -859,7 +860,8 @@ int mvb_synthesize_f32(const mvb_job* jobs, const mvb_work* work, int64_t n_work
     const unsigned g = (unsigned)n_work;
     const int block = SYNTH_WARPS * 32;
     // U = 16: 512-sample tiles, 3 CTAs/SM
-#define MVB_SYNTH(U, NP, MB) k_synth_f32<U, NP, MB><<<g, block, 0, s>>>( \
+#define MVB_SYNTH(U, NP, MB) prefer_carveout((const void*)k_synth_f32<U, NP, MB>); \
+    k_synth_f32<U, NP, MB><<<g, block, 0, s>>>( \
         jobs, work, images, coef, rec, paths, out, part)
 #define MVB_SYNTH_NB(U, MB)                         \
     switch (nb) {                                   \
@@ -883,6 +885,7 @@ int mvb_signal_plane_f32(const float* x_all, const int64_t* sig_off, const int64
     if (!x_all || !sig_off || !sig_len || !sig_row0 || !xp) return fail(MVB_EINVAL, "signal_plane: null");
     unsigned gx = grid_for(max_len, 256);
     if (gx > 4096) gx = 4096;
+    prefer_carveout((const void*)k_signal_plane);
     k_signal_plane<<<dim3(gx, (unsigned)n_sig), 256, 0, as_stream(stream)>>>(x_all, sig_off, sig_len,
                                                                               sig_row0, xp);
     return check_launch("signal_plane_f32");
@@ -901,6 +904,7 @@ int mvb_synthesize_f32_table(const mvb_job* jobs, const mvb_work* work, int64_t 
     if (cudaFuncSetAttribute(k_synth_f32<16, 1, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return check_launch("synthesize_f32_table (smem attribute)");
+    prefer_carveout((const void*)k_synth_f32<16, 1, 1, true>);
     k_synth_f32<16, 1, 1, true><<<(unsigned)n_work, SYNTH_WARPS * 32, smem, as_stream(stream)>>>(
         jobs, work, images, coef, xp, paths, out, part, table);
     return check_launch("synthesize_f32_table");
@@ -912,6 +916,7 @@ int mvb_reduce_partials_f32(const mvb_job* jobs, int64_t n_jobs, int64_t max_out
     if (n_jobs == 0 || max_out_len == 0) return MVB_OK;
     unsigned gx = grid_for(max_out_len, 256);
     if (gx > 1024) gx = 1024;
+    prefer_carveout((const void*)k_reduce_f32);
     k_reduce_f32<<<dim3(gx, (unsigned)n_jobs), 256, 0, as_stream(stream)>>>(jobs, part, out);
     return check_launch("reduce_partials_f32");
 }
@@ -938,12 +943,15 @@ int mvb_synthesize_f64(const mvb_job* jobs, int64_t n_jobs, int64_t max_out_len,
         }
     }
     dim3 g(grid_for(max_out_len, 32), (unsigned)n_jobs);
-    if (minb == 3)
+    if (minb == 3) {
+        prefer_carveout((const void*)k_synth_f64<3>);
         k_synth_f64<3><<<g, F64_WARPS * 32, F64_SMEM, as_stream(stream)>>>(jobs, images, coarse, tables,
                                                                             streams, paths, out);
-    else
+    } else {
+        prefer_carveout((const void*)k_synth_f64<2>);
         k_synth_f64<2><<<g, F64_WARPS * 32, F64_SMEM, as_stream(stream)>>>(jobs, images, coarse, tables,
                                                                             streams, paths, out);
+    }
     return check_launch("synthesize_f64");
 }
 

@@ -696,6 +696,7 @@ static int launch_delay_sort(const mvb_image* images, const mvb_job* jobs, int64
                              (int)smem);
         attr = true;
     }
+    prefer_carveout((const void*)k_delay_sort<BT, IPT>);
     k_delay_sort<BT, IPT><<<dim3((unsigned)max_n_seg, (unsigned)n_jobs), BT, smem, s>>>(
         images, jobs, max_n_img, max_n_seg, seg_len, paths, coarse, key_bits, out);
     return MVB_OK;
@@ -965,6 +966,7 @@ static int launch_coeffs(const SbpParam& sp, const mvb_image* images, const int3
         if (e != cudaSuccess) return fail(MVB_ECUDA, cudaGetErrorString(e));
         attr_set = true;
     }
+    prefer_carveout((const void*)k_coeffs<BLOCK, KI>);
     k_coeffs<BLOCK, KI><<<dim3((unsigned)n_sel, (unsigned)spans), BLOCK, S::SMEM, as_stream(stream)>>>(
         sp, images, sel, jobs, coarse, coef);
     return check_launch("track_coeffs");
@@ -983,6 +985,7 @@ int mvb_build_images(const double* toff, const double* tsgn, const double* tbeta
     if (!toff || !tsgn || !tbeta || !img || !job || !images)
         return fail(MVB_EINVAL, "build_images: null");
     if (img_base + G * S > 0x7fffffff) return fail(MVB_EINVAL, "build_images: > 2^31 images");
+    prefer_carveout((const void*)k_build_images);
     k_build_images<<<grid_for(G * S, 256), 256, 0, as_stream(stream)>>>(
         toff, tsgn, tbeta, S0, img, S, job, G, *classes, img_base, images,
         full_sel ? full_sel + full_off : nullptr, dec_sel ? dec_sel + dec_off : nullptr, class_sel);
@@ -1004,6 +1007,7 @@ int mvb_coarse_distances(const mvb_image* images, const int32_t* sel, int64_t n_
     if (n_sel * chunks16 < 148 * 64) {
         const int64_t chunks = ((max_K + 63) / 64 + 7) / 8;
         if (chunks > 65535) return fail(MVB_EINVAL, "coarse_distances: coarse track too long");
+        prefer_carveout((const void*)k_coarse_bounds<8>);
         k_coarse_bounds<8><<<dim3(grid_for(n_sel, 8), (unsigned)chunks), 256, 0,
                              as_stream(stream)>>>(images, sel, n_sel, jobs, paths, negsum, coarse,
                                                   lb, ub);
@@ -1011,6 +1015,7 @@ int mvb_coarse_distances(const mvb_image* images, const int32_t* sel, int64_t n_
     }
     const int64_t chunks = chunks16;
     if (chunks > 65535) return fail(MVB_EINVAL, "coarse_distances: coarse track too long");
+    prefer_carveout((const void*)k_coarse_bounds<CB_SEGS>);
     k_coarse_bounds<CB_SEGS><<<dim3(grid_for(n_sel, 8), (unsigned)chunks), 256, 0, as_stream(stream)>>>(
         images, sel, n_sel, jobs, paths, negsum, coarse, lb, ub);
     return check_launch("coarse_distances");
@@ -1022,7 +1027,9 @@ int mvb_path_bbox(const int64_t* rows, int64_t n_jobs, const double* paths, doub
     if (n_jobs == 0) return MVB_OK;
     if (!rows || !paths || !bbox) return fail(MVB_EINVAL, "path_bbox: null");
     cudaStream_t s = as_stream(stream);
+    prefer_carveout((const void*)k_path_bbox);
     k_path_bbox<<<dim3(BBOX_PARTS, (unsigned)n_jobs), BBOX_THREADS, 0, s>>>(rows, paths, n_jobs, bbox);
+    prefer_carveout((const void*)k_bbox_reduce);
     k_bbox_reduce<<<(unsigned)n_jobs, 32 * BBOX_WORDS, 0, s>>>(n_jobs, bbox);
     return check_launch("path_bbox");
 }
@@ -1034,6 +1041,7 @@ int mvb_track_bounds(const mvb_image* images, const int32_t* full_sel, int64_t n
     if (n_full == 0) return MVB_OK;
     if (!images || !full_sel || !jobs || !paths || !bbox || !lb || !ub)
         return fail(MVB_EINVAL, "track_bounds: null");
+    prefer_carveout((const void*)k_bounds_full);
     k_bounds_full<<<grid_for(n_full, 128), 128, 0, as_stream(stream)>>>(images, full_sel, n_full, jobs,
                                                                        paths, bbox, lb, ub);
     return check_launch("track_bounds");
@@ -1061,6 +1069,7 @@ int mvb_finalize_lengths(mvb_job* jobs, int64_t n_jobs, const double* dmax, int6
     if (n_jobs < 0) return fail(MVB_EINVAL, "finalize_lengths: n_jobs");
     if (n_jobs == 0) return MVB_OK;
     if (!jobs || !dmax || !lengths || !err) return fail(MVB_EINVAL, "finalize_lengths: null");
+    prefer_carveout((const void*)k_finalize_lengths);
     k_finalize_lengths<<<grid_for(n_jobs, 128), 128, 0, as_stream(stream)>>>(jobs, n_jobs, dmax,
                                                                             lengths, err);
     return check_launch("finalize_lengths");
@@ -1072,6 +1081,7 @@ int mvb_gather_images(const mvb_image* images, const int64_t* idx, int64_t n, mv
     if (n == 0) return MVB_OK;
     if (!images || !idx || !out) return fail(MVB_EINVAL, "gather_images: null");
     const int64_t chunks = n * (int64_t)(sizeof(mvb_image) / 16);
+    prefer_carveout((const void*)k_gather_images);
     k_gather_images<<<grid_for(chunks, 256), 256, 0, as_stream(stream)>>>(images, idx, n, out);
     return check_launch("gather_images");
 }
@@ -1084,11 +1094,14 @@ int mvb_track_max(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
     if (!images || !jobs || !paths || !lb || !ub || !scratch || !dmax)
         return fail(MVB_EINVAL, "track_max: null");
     cudaStream_t s = as_stream(stream);
+    prefer_carveout((const void*)k_select);
     k_select<<<(unsigned)n_jobs, 256, 0, s>>>(images, jobs, lb, ub, scratch, dmax);
     // scan: ~2 blocks of 8 warps per SM for one job, fewer per job for batches
     const unsigned bx = (unsigned)std::max<int64_t>(4, std::min<int64_t>(296, 1184 / n_jobs));
+    prefer_carveout((const void*)k_exact_scan);
     k_exact_scan<<<dim3(bx, (unsigned)n_jobs), 256, 0, s>>>(images, jobs, coarse, tables, paths,
                                                            negsum, scratch, dmax);
+    prefer_carveout((const void*)k_exact_eval);
     k_exact_eval<<<592, EXACT_SUB, 0, s>>>(images, jobs, coarse, tables, scratch, dmax);
     return check_launch("track_max");
 }
@@ -1160,6 +1173,7 @@ int mvb_sort_keys(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs, 
     if (n_jobs == 0 || max_n_img == 0 || max_n_seg == 0) return MVB_OK;
     if (!images || !jobs || !paths || !key) return fail(MVB_EINVAL, "sort_keys: null");
     dim3 g(grid_for(max_n_img, 256), (unsigned)max_n_seg, (unsigned)n_jobs);
+    prefer_carveout((const void*)k_sort_keys);
     k_sort_keys<<<g, 256, 0, as_stream(stream)>>>(images, jobs, max_n_img, max_n_seg, seg_len, paths,
                                                   coarse, key);
     return check_launch("sort_keys");
@@ -1231,6 +1245,7 @@ extern "C" int mvb_decimate_rows(const double* src, const int64_t* rows, int64_t
     if (n < 0 || K < 0 || N < 1) return fail(MVB_EINVAL, "decimate_rows: sizes");
     if (n == 0 || K == 0) return MVB_OK;
     if (!src || !rows || !dst) return fail(MVB_EINVAL, "decimate_rows: null");
+    prefer_carveout((const void*)k_decimate_rows);
     k_decimate_rows<<<grid_for(n * K * 3, 256), 256, 0, as_stream(stream)>>>(src, rows, n, K, N, dst);
     return check_launch("decimate_rows");
 }
@@ -1242,9 +1257,11 @@ extern "C" int mvb_center_paths(const double* x, int64_t G, int64_t T, double* s
     if (G == 0) return MVB_OK;
     if (!x || !scratch || !out) return fail(MVB_EINVAL, "center_paths: null");
     cudaStream_t s = as_stream(stream);
+    prefer_carveout((const void*)k_path_sums);
     k_path_sums<<<dim3(SPEC_PARTS, (unsigned)G), 256, 0, s>>>(x, T, scratch);
     unsigned bx = grid_for(3 * T, 256);
     if (bx > 256) bx = 256;
+    prefer_carveout((const void*)k_path_center);
     k_path_center<<<dim3(bx, (unsigned)G), 256, 0, s>>>(x, T, scratch, out);
     return check_launch("center_paths");
 }
@@ -1259,7 +1276,9 @@ extern "C" int mvb_spectrum_index(const double* spec, int64_t G, int64_t F, doub
     if (3 * G > 65535) return fail(MVB_EINVAL, "spectrum_index: too many paths per call");
     cudaStream_t s = as_stream(stream);
     const double2* sp = reinterpret_cast<const double2*>(spec);
+    prefer_carveout((const void*)k_spec_partial);
     k_spec_partial<<<dim3(SPEC_PARTS, (unsigned)(3 * G)), 256, 0, s>>>(sp, F, scratch);
+    prefer_carveout((const void*)k_spec_find);
     k_spec_find<<<(unsigned)(3 * G), 256, 0, s>>>(sp, F, scratch, fraction, out);
     return check_launch("spectrum_index");
 }
@@ -1271,6 +1290,7 @@ extern "C" int mvb_energy_index(const double* pw, int64_t rows, int64_t F, doubl
         return fail(MVB_EINVAL, "energy_index: args");
     if (rows == 0) return MVB_OK;
     if (!pw || !out) return fail(MVB_EINVAL, "energy_index: null");
+    prefer_carveout((const void*)k_energy_index);
     k_energy_index<<<(unsigned)rows, 256, 0, as_stream(stream)>>>(pw, F, fraction, out);
     return check_launch("energy_index");
 }

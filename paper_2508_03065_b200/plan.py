@@ -116,7 +116,7 @@ class _Slot:
 class RenderPlan:
     """Captured render of `jobs`' structure (see the module docstring)."""
 
-    DEPTH = 2
+    DEPTH = int(os.environ.get("MVB_PLAN_DEPTH", "2"))  # slots (diagnostic knob)
 
     def __init__(self, jobs, f, precision: str = "fp32", device=None, shard=None, dmax_hook=None):
         """`shard=(rank, world)`: render the image shard of `rank` of every
