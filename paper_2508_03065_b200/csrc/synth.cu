@@ -643,7 +643,13 @@ constexpr int F64_CHUNK_BLOCKS = 4;  // power of two
 constexpr int F64_CHUNK = 32 * F64_CHUNK_BLOCKS;
 constexpr int F64_LOG_CHUNK = 2;
 static_assert((1 << F64_LOG_CHUNK) == F64_CHUNK_BLOCKS, "chunk is a power of two");
-constexpr size_t F64_SMEM = sizeof(double) * (F64_CHUNK * 32 + F64_CHUNK_BLOCKS * 32);
+// a tile's slice of a factor's transposed phase table, tab[col * N + ph0 +
+// lane] for the 65 columns (the tile's 32 samples share one interval), kept
+// in shared memory for up to F64_TAB_SLOTS factors: one LDS per tap instead
+// of an LDG plus its 64-bit address arithmetic
+constexpr int F64_TAB_SLOTS = 2;
+constexpr size_t F64_SMEM =
+    sizeof(double) * (F64_CHUNK * 32 + F64_CHUNK_BLOCKS * 32 + F64_TAB_SLOTS * 65 * 32);
 // images per warp evaluated together: their 65-tap upsample chains are
 // independent, so G chains hide the fp64 add latency of one (each chain
 // keeps the reference's tap order)
@@ -667,6 +673,8 @@ __global__ void __launch_bounds__(F64_WARPS * 32, MINB) k_synth_f64(
     extern __shared__ double f64_smem[];
     double* contrib = f64_smem;                 // [F64_CHUNK images][32 lanes]
     double* bsum = f64_smem + F64_CHUNK * 32;   // [F64_CHUNK_BLOCKS][32 lanes]
+    double* tslice = bsum + F64_CHUNK_BLOCKS * 32;  // [F64_TAB_SLOTS][65 cols][32 lanes]
+    __shared__ int64_t slot_tab[F64_TAB_SLOTS];     // table offset cached in each slot (-1: none)
     const mvb_job& J = jobs[blockIdx.y];
     const int64_t out_len = J.out_len;
     const int64_t n0 = (int64_t)blockIdx.x * 32;
@@ -688,8 +696,33 @@ __global__ void __launch_bounds__(F64_WARPS * 32, MINB) k_synth_f64(
     double st_v[40];
     int st_l[40];
     int sp = 0;
+    if (threadIdx.x < F64_TAB_SLOTS) slot_tab[threadIdx.x] = -1;
+    const bool tile_in_track = n0 + 31 < J.T;  // every lane a distinct sample before the end
     for (int64_t c0 = 0; c0 < n_img; c0 += F64_CHUNK) {
         const int cn = n_img - c0 < F64_CHUNK ? (int)(n_img - c0) : F64_CHUNK;
+        // 0. table slices for the factors of the chunk's first and last images
+        //    (tiers are contiguous in the canonical order, so a chunk rarely
+        //    spans more than two factors; others read the global table)
+        if (tile_in_track) {
+            __syncthreads();  // the previous chunk's readers are done with the slots
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const mvb_image& ie = imgs[c0 + (e == 0 ? 0 : cn - 1)];
+                const int64_t tb = ie.table;
+                const int Nf = ie.factor;
+                if (Nf == 1 || Nf % 32 != 0 || slot_tab[0] == tb || slot_tab[1] == tb) continue;
+                // replace the slot not holding the other end's table
+                const int64_t other = imgs[c0 + (e == 0 ? cn - 1 : 0)].table;
+                const int sl = slot_tab[0] == other ? 1 : 0;
+                __syncthreads();
+                const int ph0 = (int)(n0 % Nf);
+                for (int t = threadIdx.x; t < 65 * 32; t += blockDim.x)
+                    tslice[sl * 65 * 32 + t] = __ldg(tables + tb + (int64_t)(t >> 5) * Nf + ph0 + (t & 31));
+                __syncthreads();
+                if (threadIdx.x == 0) slot_tab[sl] = tb;
+                __syncthreads();
+            }
+        }
         // 1. contributions of the chunk's images: warp w takes images
         //    w, w + 8, ... in groups of F64_G evaluated together
         for (int kb = warp; kb < cn; kb += F64_WARPS * F64_G) {
@@ -698,10 +731,12 @@ __global__ void __launch_bounds__(F64_WARPS * 32, MINB) k_synth_f64(
             const double* tp[F64_G];
             int64_t base[F64_G], nc[F64_G], fac[F64_G], phase[F64_G];
             bool dec[F64_G], fast[F64_G];
+            const double* ts[F64_G];  // the member's table slice in shared memory
 #pragma unroll
             for (int g = 0; g < F64_G; ++g) {
                 const int k = kb + g * F64_WARPS;
                 dec[g] = fast[g] = false;
+                ts[g] = tslice + lane;
                 d[g] = 0.0;
                 acc[g] = 0.0;
                 cp[g] = tp[g] = nullptr;
@@ -723,8 +758,11 @@ __global__ void __launch_bounds__(F64_WARPS * 32, MINB) k_synth_f64(
                         // warp-uniform: the tile's 32 samples share one coarse
                         // interval (N % 32 == 0, 32-aligned tiles, all before
                         // the track end) and the 65-sample window needs no clamp
-                        fast[g] = (im.factor % 32 == 0) && (n0 + 31 < J.T) &&
+                        // ... and the factor's table slice is cached
+                        const int sl = slot_tab[0] == im.table ? 0 : (slot_tab[1] == im.table ? 1 : -1);
+                        fast[g] = sl >= 0 && (im.factor % 32 == 0) && tile_in_track &&
                                   (n0 / im.factor) >= 32 && (n0 / im.factor) + 32 < im.n_coarse;
+                        if (fast[g]) ts[g] = tslice + sl * 65 * 32 + lane;
                     }
                 }
             }
@@ -734,21 +772,15 @@ __global__ void __launch_bounds__(F64_WARPS * 32, MINB) k_synth_f64(
             // valid address, discarded), then the rare clamped members alone
             {
                 const double* w[F64_G];
-                const double* t[F64_G];
-                int stride[F64_G];
 #pragma unroll
-                for (int g = 0; g < F64_G; ++g) {
-                    w[g] = fast[g] ? cp[g] + (base[g] - 32) : tables;
-                    t[g] = fast[g] ? tp[g] + phase[g] : tables;
-                    stride[g] = fast[g] ? (int)fac[g] : 0;
-                }
+                for (int g = 0; g < F64_G; ++g) w[g] = fast[g] ? cp[g] + (base[g] - 32) : tables;
 #pragma unroll 5
                 for (int col = 0; col < 65; ++col) {
 #pragma unroll
                     for (int g = 0; g < F64_G; ++g) {
                         MVB_CHECK(!fast[g] || (base[g] - 32 + col >= 0 && base[g] - 32 + col < nc[g]),
                                   CHK_EXACT_INDEX);
-                        acc[g] = xadd(acc[g], xmul(__ldg(t[g] + col * stride[g]), __ldg(w[g] + col)));
+                        acc[g] = xadd(acc[g], xmul(ts[g][col * 32], __ldg(w[g] + col)));
                     }
                 }
             }
