@@ -655,6 +655,10 @@ def measure(ctx, name, steps, warmup, peaks, args, precision=None, with_e2e=True
             "achieved_l1_gbs": upd_per_launch * 32 / (kern_avg_ms * 1e-3) / 1e9,
             "peak_l1_gbs": peaks["l1_gbs"],
             "frac_l1": upd_per_launch * 32 / (kern_avg_ms * 1e-3) / 1e9 / peaks["l1_gbs"],
+            # the binding pipe's utilisation as ncu measures it (committed capture
+            # of this kernel on this config; the 32 B model above counts only the
+            # gather, ncu also sees the record broadcasts and the staging)
+            "ncu_l1tex_pct": None if traffic is None else traffic.get("l1tex_throughput_pct"),
         }
         peak_source = "measured on this GPU by bench.py (mvb_peak_ffma, best of 3)"
     roof = {
