@@ -35,13 +35,19 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 // MVB_CARVEOUT=<percent> (diagnostic): every libmvb kernel prefers the same
 // shared-memory carveout, so kernels of different streams can share an SM
-// without the SM draining to reconfigure its L1 / shared split.  Unset: the
-// driver's per-kernel choice.
-inline void prefer_carveout(const void* kernel) {
-    static const int pct = [] {
+// without the SM draining to reconfigure its L1 / shared split.
+// MVB_GEO_CARVEOUT=<percent>: the same for every kernel but the fast
+// synthesis (which keeps the driver's choice).  Unset: per-kernel defaults.
+inline void prefer_carveout(const void* kernel, bool synthesis = false) {
+    static const int pct_all = [] {
         const char* e = getenv("MVB_CARVEOUT");
         return e ? atoi(e) : -1;
     }();
+    static const int pct_geo = [] {
+        const char* e = getenv("MVB_GEO_CARVEOUT");
+        return e ? atoi(e) : -1;
+    }();
+    const int pct = pct_all >= 0 ? pct_all : (synthesis ? -1 : pct_geo);
     if (pct < 0) return;
     static std::mutex mu;
     static std::set<const void*> seen;

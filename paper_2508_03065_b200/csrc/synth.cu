@@ -892,7 +892,7 @@ int mvb_synthesize_f32(const mvb_job* jobs, const mvb_work* work, int64_t n_work
     const unsigned g = (unsigned)n_work;
     const int block = SYNTH_WARPS * 32;
     // U = 16: 512-sample tiles, 3 CTAs/SM
-#define MVB_SYNTH(U, NP, MB) prefer_carveout((const void*)k_synth_f32<U, NP, MB>); \
+#define MVB_SYNTH(U, NP, MB) prefer_carveout((const void*)k_synth_f32<U, NP, MB>, true); \
     k_synth_f32<U, NP, MB><<<g, block, 0, s>>>( \
         jobs, work, images, coef, rec, paths, out, part)
 #define MVB_SYNTH_NB(U, MB)                         \
