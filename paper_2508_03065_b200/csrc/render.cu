@@ -35,7 +35,8 @@ namespace {
 constexpr int TILE = 512;           // mvb_synthesize_f32 u_steps = 16
 constexpr int SEG_LEN = 32 * TILE;  // delay-sort segment (engine.SEG_LEN)
 constexpr int PAD_MARGIN = 64;
-constexpr int CHUNK_MIN_IMAGES = 320;
+constexpr int CHUNK_MIN_IMAGES = 320;        // engine.py CHUNK_MIN_IMAGES
+constexpr int SMALL_GRID_TILES = 512, SMALL_GRID_CHUNK_MIN = 160;  // engine.py _chunking
 constexpr int FIT_DEGREE = 8;
 
 // least squares min ||A x - b|| for every column of B (m x k), A (m x n)
@@ -463,7 +464,8 @@ extern "C" int mvb_render_tracks_and_synthesize(const mvb_render_args* a, float*
     int64_t nc = 1;
     if (tiles < want) {
         nc = std::max<int64_t>(1, (want + tiles - 1) / tiles);
-        nc = std::min<int64_t>(nc, std::max<int64_t>(1, S / CHUNK_MIN_IMAGES));
+        const int64_t cmin = tiles < SMALL_GRID_TILES ? SMALL_GRID_CHUNK_MIN : CHUNK_MIN_IMAGES;
+        nc = std::min<int64_t>(nc, std::max<int64_t>(1, S / cmin));
     }
     std::vector<mvb_work> work((size_t)(nc * tiles));
     for (int64_t ch = 0; ch < nc; ++ch)

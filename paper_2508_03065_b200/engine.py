@@ -812,7 +812,11 @@ class RenderResult:
         return d2h(self.out)
 
 
-CHUNK_MIN_IMAGES = 320
+CHUNK_MIN_IMAGES = int(os.environ.get("MVB_CHUNK_MIN_IMAGES", "320"))
+# batches with few tiles (c2: 131) need many chunks per tile to fill the GPU;
+# there smaller chunks win (c2 synthesis 0.335 -> 0.233 ms at 160), while a
+# W = 8 image shard of c3 (1050 tiles, 1440 images) is 1.5% faster at 320
+SMALL_GRID_TILES, SMALL_GRID_CHUNK_MIN = 512, 160
 
 
 def _chunking(n_imgs, tiles, sm_count):
@@ -824,10 +828,11 @@ def _chunking(n_imgs, tiles, sm_count):
     want = 36 * sm_count
     if total_tiles >= want:
         return [1] * len(n_imgs)
+    cmin = SMALL_GRID_CHUNK_MIN if total_tiles < SMALL_GRID_TILES else CHUNK_MIN_IMAGES
     out = []
     for S, t in zip(n_imgs, tiles):
         per = max(1, math.ceil(want / max(total_tiles, 1)))
-        per = min(per, max(1, S // CHUNK_MIN_IMAGES))
+        per = min(per, max(1, S // cmin))
         out.append(per)
     return out
 
