@@ -165,3 +165,9 @@ def to_dev(a, dtype, device) -> torch.Tensor:
         return a.to(device=device, dtype=dtype).contiguous()
     arr = np.array(np.asarray(a), dtype=torch.empty((), dtype=dtype).numpy().dtype, order="C")
     return h2d(arr, device)
+
+
+def release_pinned(tags) -> None:
+    """Drop the pinned scratch buffers whose names end with one of `tags`."""
+    for name in [n for n in _PINNED if any(n.endswith(t) for t in tags)]:
+        del _PINNED[name]

@@ -188,7 +188,8 @@ class Geometry:
     """Device-side hierarchical tracks of a batch of jobs (prepare stage)."""
 
     def __init__(self, jobs: list, device=None, inputs_ready=None, dmax_hook=None,
-                 paths=None, defer=False, wait=True, bbox=None, on_paths=None):
+                 paths=None, defer=False, wait=True, bbox=None, on_paths=None,
+                 readback_tag: str = ""):
         """`inputs_ready`: optional CUDA event after which every device
         tensor of `jobs` is final.  With it, the paths are staged and their
         bandwidths measured on a side stream that waits only for that event,
@@ -207,7 +208,10 @@ class Geometry:
         for the boxes and the decision (render plans replay speculatively).
         `on_paths(event)`: called as soon as that event is recorded, before
         the bandwidth kernels are enqueued (a plan launches its replay
-        there, ahead of the host-side issue of the decision pipeline)."""
+        there, ahead of the host-side issue of the decision pipeline).
+        `readback_tag`: suffix of the pinned readback buffers' names -- a
+        caller that leaves several stagings pending at once (render plans,
+        one per slot) gives each its own buffers."""
         if not jobs:
             raise ValueError("no jobs")
         self.dev = require_cuda(device)
@@ -215,6 +219,7 @@ class Geometry:
         for jb in jobs:
             _validate_tiers(jb.tiers, jb.max_order)
         self.length_slack = 0.0
+        self._tag = readback_tag
         host_parts, dev_parts, rows = self._layout_paths()
         self.rows = rows
         _mark("geom.setup")
@@ -235,6 +240,16 @@ class Geometry:
             self.bbox_host = box_host.numpy().copy()
             self.path_groups = path_groups
             self._pending = None
+        return self
+
+    def recollect(self, pending) -> "Geometry":
+        """Re-read the readbacks of a captured staging (`pending`: the
+        `_pending` of the Geometry built during the capture), refilled by a
+        replay the caller has waited for (render plans)."""
+        _, box_host, path_groups, finishers = pending
+        self.bws = [fin(False) for fin in finishers]
+        self.bbox_host = box_host.numpy().copy()
+        self.path_groups = path_groups
         return self
 
     def finish(self, dmax_hook=None, fork=None):
@@ -348,7 +363,8 @@ class Geometry:
                 self.bbox = torch.empty(nJ * 65 * BOX_WORDS, dtype=torch.float64, device=dev)
             _lib.call("mvb_path_bbox", ptr(box_rows), nJ, ptr(self.paths), ptr(self.bbox),
                       stream_handle(dev))
-            box_host = pinned_scratch("bbox", nJ * BOX_WORDS, torch.float64).view(nJ, BOX_WORDS)
+            box_host = pinned_scratch("bbox" + self._tag, nJ * BOX_WORDS,
+                                      torch.float64).view(nJ, BOX_WORDS)
             box_host.copy_(self.bbox[:nJ * BOX_WORDS].view(nJ, BOX_WORDS), non_blocking=True)
             box_ready = torch.cuda.Event()
             box_ready.record()
@@ -464,7 +480,7 @@ class Geometry:
                 x = torch.stack([self.paths[r0:r0 + T] for r0 in starts])  # (G, T, 3)
                 x.record_stream(consumer)  # read again by the decimation
             out.append((T, rate, x, uses))
-            bws.append(bandwidth_batch_async(x, rate, slot=f"bandwidth_index{len(bws)}"))
+            bws.append(bandwidth_batch_async(x, rate, slot=f"bandwidth_index{len(bws)}{self._tag}"))
         return out, bws
 
     def _decimate_paths(self, path_groups, bws):
@@ -750,25 +766,61 @@ class RenderResult:
     A render plan's result is produced on the plan's own streams: `done` is
     its completion event and `stream` the stream that produced it; `job()`,
     `host()` and `lengths` order the current stream after it (wait()), code
-    that reads `out` directly calls wait() first."""
+    that reads `out` directly calls wait() first.  A plan's speculative
+    replay is validated on first use of the result (`_validate`, see
+    plan.RenderPlan.run): reading any field settles it, and a replay the
+    staging readbacks invalidate is redone before the field is returned."""
 
     def __init__(self, out, offsets, capacity, n_images, launches, lengths_dev, err_dev,
-                 done=None, stream=None):
-        self.out = out
-        self.offsets = offsets
-        self.capacity = capacity
-        self.n_images = n_images
+                 done=None, stream=None, validate=None):
+        self._out = out
+        self._offsets = offsets
+        self._capacity = capacity
+        self._n_images = n_images
         self.launches = launches
         self._lengths = None
-        self._dev = (lengths_dev, err_dev)  # read on first use (no per-render pinned buffers)
-        self.done = done
+        self._devs = (lengths_dev, err_dev)  # read on first use (no per-render pinned buffers)
+        self._done = done
         self.stream = stream
-        self.precision = "fp64" if out.dtype == torch.float64 else "fp32"  # engine that rendered it
+        self._validate = validate
+
+    def _settle(self) -> None:
+        v = self._validate
+        if v is not None:
+            self._validate = None
+            v(self)
+
+    def _redo(self, r: "RenderResult", done) -> None:
+        """Replace the fields by those of `r` (a re-captured plan slot)."""
+        self._out, self._offsets, self._capacity = r._out, r._offsets, r._capacity
+        self._n_images, self._devs, self._done, self._lengths = r._n_images, r._devs, done, None
+
+    out = property(lambda self: (self._settle(), self._out)[1])
+    offsets = property(lambda self: (self._settle(), self._offsets)[1])
+    capacity = property(lambda self: (self._settle(), self._capacity)[1])
+    n_images = property(lambda self: (self._settle(), self._n_images)[1])
+    _dev = property(lambda self: (self._settle(), self._devs)[1])
+
+    @property
+    def done(self):
+        self._settle()
+        return self._done
+
+    @done.setter
+    def done(self, ev):
+        self._settle()
+        self._done = ev
+
+    @property
+    def precision(self) -> str:
+        """Engine that rendered it: "fp32" fast or "fp64" exact."""
+        return "fp64" if self.out.dtype == torch.float64 else "fp32"
 
     def wait(self) -> "RenderResult":
         """Order the current stream after the render (no host wait)."""
-        if self.done is not None:
-            torch.cuda.current_stream(self.out.device).wait_event(self.done)
+        done = self.done
+        if done is not None:
+            torch.cuda.current_stream(self._out.device).wait_event(done)
         return self
 
     @property
@@ -963,9 +1015,7 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
                       ptr(geom.images), ptr(geom.coarse), ptr(geom.tables), ptr(streams),
                       ptr(geom.paths), ptr(out), st)
             _events_end(timing, ev)
-            res = RenderResult(out, offsets, out_len, geom.n_img.copy(), 0, lengths, err)
-            res.precision = "fp64"
-            return res
+            return RenderResult(out, offsets, out_len, geom.n_img.copy(), 0, lengths, err)
         return PreparedRender(launch64, launches0)
 
     # ---------------------------------------------------------------- fast --
@@ -1030,9 +1080,7 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
             _lib.call("mvb_reduce_partials_f32", ptr(jobs_dev), nJ, int(out_len.max()),
                       ptr(part), ptr(out), st)
         _mark("render.synth_launched")
-        res = RenderResult(out, offsets, out_len, geom.n_img.astype(np.int64), 0, lengths, err)
-        res.precision = "fp32"
-        return res
+        return RenderResult(out, offsets, out_len, geom.n_img.astype(np.int64), 0, lengths, err)
     return PreparedRender(launch32, launches0)
 
 

@@ -2,14 +2,17 @@
 
 A plan fixes the structure of a batch -- per job the path length, signal
 length, receiver kind, room, image order, tier table, filter and precision --
-and captures every kernel of a render after the staging into CUDA graphs.
-Each `run` copies the new inputs into the plan's static buffers, redoes the
-staging outside the graphs (path bounding boxes and the decimation decision,
-the two small readbacks) and replays the graphs, which recompute all
-data-dependent work (coarse tracks, bounds, exact maxima, interval records,
-delay sort, branch records, output lengths, synthesis).  Only the host
-planning is amortised.  When the new data change the low-pass decision or
-exceed the output capacities the slot is captured again.
+and captures every kernel of a render into CUDA graphs: the staging (path
+copies, bounding boxes, bandwidth indices and their two small readbacks),
+the geometry and the synthesis.  Each `run` copies the new inputs into the
+plan's static buffers and replays the graphs, which recompute all
+data-dependent work (boxes, bandwidths, coarse tracks, bounds, exact maxima,
+interval records, delay sort, branch records, output lengths, synthesis).
+Only the host planning is amortised.  The replay is speculative: the host
+decisions a capture is valid for (low-pass decision, fp32 envelope, output
+capacities) are re-checked from the replayed readbacks on first use of the
+result (RenderResult._settle), and when the new data changed them the run
+is staged again, the slot captured again and replayed.
 
 Each slot holds two graphs: the geometry graph (tracks, maxima, records,
 sort, branch records -- short, mostly latency-bound kernels) replays on a
@@ -35,12 +38,13 @@ from __future__ import annotations
 from dataclasses import replace
 
 import os
+import weakref
 
 import numpy as np
 import torch
 
 from . import _lib, engine
-from ._dev import StaticUploads, UploadMeter, require_cuda
+from ._dev import StaticUploads, UploadMeter, release_pinned, require_cuda
 from ._staging import _STAGER, copy_batch, side_stream
 
 _NP_DTYPE = {torch.float64: np.dtype(np.float64), torch.float32: np.dtype(np.float32)}
@@ -111,6 +115,8 @@ class _Slot:
         self.capacity = None
         self.timing = []  # (start, end) events of the captured synthesis launch
         self.run_index = None  # run whose replay last used the slot
+        self.pending = None  # result of an unvalidated speculative replay
+        self.tag = f"@slot{id(self)}"  # its own pinned readback buffers (validation is deferred)
 
 
 class RenderPlan:
@@ -161,6 +167,7 @@ class RenderPlan:
                                          path_key=("plan", pk), signal_key=("plan", sk)))
             slot.paths = slot.bbox = None
             self.slots.append(slot)
+        weakref.finalize(self, release_pinned, [sl.tag for sl in self.slots])
         self.k = 0
         self.captures = 0
         self.misses = 0  # speculative replays redone after a decision / capacity change
@@ -196,18 +203,18 @@ class RenderPlan:
                 np.asarray(src).reshape(-1)
             _STAGER.upload([(0, a)], dst)
 
-    def _stage(self, slot, ready, wait=True, on_paths=None):
-        """Stage the slot's static inputs into its static paths buffer: on the
-        side stream after `ready` (pipelined), or on the current stream.
-        `wait=False`: leave the readbacks pending (Geometry.collect())."""
+    def _stage(self, slot, ready):
+        """Stage the slot's static inputs into its static paths buffer on the
+        current stream (after event `ready`, if given) and wait for the
+        readbacks (eager: first run of a slot, a miss)."""
+        if ready is not None:
+            torch.cuda.current_stream(self.dev).wait_event(ready)
         if slot.paths is None:  # first staging allocates the slot's paths / box buffers
-            if ready is not None:
-                torch.cuda.current_stream(self.dev).wait_event(ready)
-            geom = engine.Geometry(slot.jobs, device=self.dev, defer=True)
+            geom = engine.Geometry(slot.jobs, device=self.dev, defer=True, readback_tag=slot.tag)
             slot.paths, slot.bbox = geom.paths, geom.bbox
             return geom
-        return engine.Geometry(slot.jobs, device=self.dev, inputs_ready=ready, paths=slot.paths,
-                               defer=True, wait=wait, bbox=slot.bbox, on_paths=on_paths)
+        return engine.Geometry(slot.jobs, device=self.dev, paths=slot.paths, defer=True,
+                               bbox=slot.bbox, readback_tag=slot.tag)
 
     SLACK = 0.1  # output capacity headroom of a capture (fraction of the length bound)
 
@@ -233,8 +240,15 @@ class RenderPlan:
             self.kernel_ms[slot.run_index] = a.elapsed_time(b)
             slot.run_index = None
 
+    def settle(self) -> None:
+        """Validate every pending speculative replay (run())."""
+        for slot in self.slots:
+            if slot.pending is not None:
+                slot.pending._settle()
+
     def flush_timing(self) -> dict:
         """Wait for every slot and collect the pending kernel timings."""
+        self.settle()
         for slot in self.slots:
             if slot.done is not None:
                 slot.done.synchronize()
@@ -242,7 +256,9 @@ class RenderPlan:
         return self.kernel_ms
 
     def join(self) -> None:
-        """Order the current stream after every pending run (no host wait)."""
+        """Order the current stream after every pending run (no host wait
+        beyond the validation of pending speculative replays)."""
+        self.settle()
         cur = torch.cuda.current_stream(self.dev)
         for slot in self.slots:
             if slot.done is not None:
@@ -275,6 +291,7 @@ class RenderPlan:
         slot.graph, slot.result, slot.uploads = g_geo, res, uploads
         slot.decision = self._decision(geom)
         slot.capacity = np.asarray([geom.length_bound(j) for j in range(len(slot.jobs))])  # slacked
+        self._capture_staging(slot)
         self.captures += 1
 
     def _decision(self, geom) -> tuple:
@@ -332,42 +349,119 @@ class RenderPlan:
             raise ValueError("jobs do not match the plan's structure")
         slot = self.slots[self.k % self.DEPTH]
         self.k += 1
+        if slot.pending is not None:
+            slot.pending._settle()  # the slot's previous run (two runs ago)
         if slot.done is not None:
-            slot.done.synchronize()  # its previous replay (two runs ago) finished
+            slot.done.synchronize()  # its previous replay finished
         self._collect(slot)
         cur = torch.cuda.current_stream(self.dev)
         entry = torch.cuda.Event()
         entry.record(cur)  # inputs the caller wrote on its stream
         side = side_stream(self.dev)
+        spec = slot.graph is not None
         with torch.cuda.stream(side):
             side.wait_event(entry)
             self._load(slot, jobs)
             ready = torch.cuda.Event()
             ready.record()
-        staged0 = _lib.launch_count()
-        # speculative replay: a captured slot is valid while the low-pass
-        # decision and the output capacities hold; replay as soon as the
-        # paths are on the device, check the staging readbacks meanwhile,
-        # and re-capture + replay only if they changed
-        spec = slot.graph is not None
-        replay = (lambda ev: self._replay(slot, ev)) if spec else None
-        geom = self._stage(slot, ready, wait=not spec, on_paths=replay)
-        staged = _lib.launch_count() - staged0  # staging kernels (graph replays are not counted)
-        if spec:
-            geom.collect()
-        bound = np.asarray([geom.length_bound(j) for j in range(len(slot.jobs))])
-        if not spec or self._decision(geom) != slot.decision \
-                or np.any(bound > slot.capacity):
-            if spec:
-                self.misses += 1
-                slot.done.synchronize()  # the speculative replay writes the slot's paths too
-            cur.wait_stream(side)
-            self._capture(slot, geom)
-            staged_ev = torch.cuda.Event()
-            staged_ev.record(cur)  # _stage ordered the current stream after the staging
-            self._replay(slot, staged_ev)
+            if spec:  # captured staging, part 1: paths and boxes
+                slot.stage[0].replay()
+                paths_ev = torch.cuda.Event()
+                paths_ev.record()
         slot.run_index = self.k - 1
+        if not spec:  # first run of the slot: stage eagerly, capture, replay
+            self._redo(slot, self._stage(slot, ready), side)
+            return self._result(slot)
+        # speculative replay: a captured slot is valid while the low-pass
+        # decision, the fp32 envelope and the output capacities hold.  The
+        # graphs replay as soon as the paths are on the device; the staging
+        # readbacks (boxes, bandwidth indices: captured part 2) are checked
+        # later -- on first use of the result, at the slot's next run, or
+        # join() / flush_timing() -- and the run is re-captured and replayed
+        # only if they changed.  Image shards check at once (their ranks
+        # must take the same branch before the next collective).
+        self._replay(slot, paths_ev)
+        with torch.cuda.stream(side):
+            if slot.stage[1] is not None:
+                slot.stage[1].replay()
+            staged = torch.cuda.Event()
+            staged.record()
+        res = self._result(slot, lambda res: self._check(slot, staged, res))
+        slot.pending = res
+        if self.shard is not None and int(self.shard[1]) > 1:
+            res._settle()
+        return res
+
+    def _result(self, slot, validate=None) -> engine.RenderResult:
         r = slot.result
-        return engine.RenderResult(r.out, r.offsets, r.capacity, r.n_images,
-                                   staged + slot.graph_launches, *r._dev, done=slot.done,
-                                   stream=self.syn_stream)
+        return engine.RenderResult(r._out, r._offsets, r._capacity, r._n_images,
+                                   slot.stage_launches + slot.graph_launches, *r._devs,
+                                   done=slot.done, stream=self.syn_stream, validate=validate)
+
+    def _valid(self, slot, geom) -> bool:
+        """The staging readbacks of `geom` (collected) fit the slot's capture."""
+        bound = np.asarray([geom.length_bound(j) for j in range(len(slot.jobs))])
+        return self._decision(geom) == slot.decision and not np.any(bound > slot.capacity)
+
+    def _redo(self, slot, geom, side) -> None:
+        """(Re-)capture the slot for the staged run (`geom`) and replay it."""
+        cur = torch.cuda.current_stream(self.dev)
+        cur.wait_stream(side)
+        self._capture(slot, geom)
+        staged_ev = torch.cuda.Event()
+        staged_ev.record(cur)  # _stage ordered the current stream after the staging
+        self._replay(slot, staged_ev)
+
+    def _check(self, slot, staged, res) -> None:
+        """Deferred validation of a speculative replay (RenderResult._settle):
+        wait for the replayed staging, re-read its readbacks; on a changed
+        decision / capacity the run is staged again eagerly from the slot's
+        static inputs (still this run's: the slot's next run validates
+        first), re-captured and replayed, and `res` takes the new fields."""
+        if slot.pending is res:
+            slot.pending = None
+        staged.synchronize()
+        geom = slot.stage_geom.recollect(slot.stage_pending)
+        if not self._valid(slot, geom):
+            self.misses += 1
+            slot.done.synchronize()  # the speculative replay
+            self._redo(slot, self._stage(slot, None), side_stream(self.dev))
+            res._redo(slot.result, slot.done)
+
+    def _capture_staging(self, slot) -> None:
+        """Capture the slot's staging -- path copies into the paths buffer,
+        bounding boxes, bandwidth indices and their readbacks into the
+        slot's pinned buffers -- as two graphs on the side stream: part 1
+        ends after the boxes (the geometry graph needs only paths and
+        boxes), part 2 measures the bandwidths.  A run replays both instead
+        of re-issuing the staging's host calls (c1 / c2 runs were host-bound
+        at ~0.6 ms by them)."""
+        side = side_stream(self.dev)
+        torch.cuda.synchronize(self.dev)
+        g = [torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()]
+        live = [g[0]]
+
+        decimated = any(int(N) > 1 for jb in slot.jobs for _, N in jb.tiers)
+
+        def split(_ev):  # the boxes are read back: part 2 (bandwidths) starts
+            live.pop().capture_end()
+            if decimated:  # (full-rate plans measure no bandwidth)
+                g[1].capture_begin(pool=g[0].pool())
+                live.append(g[1])
+
+        uploads = StaticUploads(64 * len(slot.jobs) + (64 << 10))
+        launches0 = _lib.launch_count()
+        with uploads, torch.cuda.stream(side):
+            g[0].capture_begin()
+            try:
+                geom = engine.Geometry(slot.jobs, device=self.dev, paths=slot.paths,
+                                       bbox=slot.bbox, defer=True, wait=False, on_paths=split,
+                                       readback_tag=slot.tag)
+            finally:
+                while live:
+                    live.pop().capture_end()
+        if geom.paths.data_ptr() != slot.paths.data_ptr():
+            raise _lib.MvbError("render plan: staging captured into another paths buffer")
+        slot.stage, slot.stage_uploads = (g if decimated else [g[0], None]), uploads
+        slot.stage_geom, slot.stage_pending = geom, geom._pending
+        slot.stage_launches = _lib.launch_count() - launches0

@@ -134,7 +134,9 @@ def bandwidth_batch_async(x: torch.Tensor, rate: float, energy_fraction: float =
                           slot: str = "bandwidth_index"):
     """bandwidth_batch, split: enqueues the kernels and the readback, returns
     a function that waits for the readback and returns the bandwidths (the
-    caller may enqueue more device work before calling it).  `slot` names
+    caller may enqueue more device work before calling it; `finish(False)`
+    reads the pinned buffer without waiting -- a render plan's captured
+    staging, whose replay the caller waited for).  `slot` names
     the pinned readback buffer (one pending readback per name)."""
     """Per-path smallest frequency holding `energy_fraction` of the
     mean-removed displacement power, max over axes (reference
@@ -144,7 +146,7 @@ def bandwidth_batch_async(x: torch.Tensor, rate: float, energy_fraction: float =
     Frequencies follow numpy.fft.rfftfreq: k * (1 / (T * (1 / rate)))."""
     G, T, _ = x.shape
     if T < 2 or G == 0:
-        return lambda: np.zeros(G)
+        return lambda wait=True: np.zeros(G)
     x = x.contiguous()
     st = stream_handle(x.device)
     F = T // 2 + 1
@@ -166,8 +168,9 @@ def bandwidth_batch_async(x: torch.Tensor, rate: float, energy_fraction: float =
     done = torch.cuda.Event()
     done.record()
 
-    def finish():
-        done.synchronize()
+    def finish(wait=True):
+        if wait:  # (render plans replay a captured copy and wait themselves)
+            done.synchronize()
         kh = host.numpy().copy().reshape(G, 3)
         hz = np.minimum(kh, F - 1) * (1.0 / (T * (1.0 / rate)))
         return np.where(kh < 0, 0.0, hz).max(axis=1)
