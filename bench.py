@@ -163,6 +163,13 @@ def build_workload(name, rank, world):
                 (sc.T + sc.max_order * float(np.max(sc.dims)) * sc.rate / 343.0) for sc in scenes]
         mine = [scenes[i] for i in parallel.lpt_assign(cost, world)[rank]]
         return scenes, mine, None, f"scene-shard x{world} LPT (no collective)"
+    if mode == "channels":
+        import dataclasses
+        mine = [dataclasses.replace(sc, mics=[sc.mics[i] for i in
+                                              parallel.channel_shard(len(sc.mics), rank, world)])
+                for sc in scenes]
+        return scenes, [sc for sc in mine if sc.mics], None, \
+            f"channel-shard x{world} (no collective)"
     return scenes, scenes, None, f"replicas x{world}"
 
 

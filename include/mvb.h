@@ -155,6 +155,13 @@ typedef struct mvb_job {
                                  starts at img_off + s * img_stride)            */
     int32_t rec_rows;         /* rows of the record buffer (bounds checks of
                                  the checked build, libmvb_checked.so)         */
+    int32_t w0, w1;           /* time shard: output samples [w0, w1) only
+                                 (w1 <= 0: to the end; all zero: no window);
+                                 tracks, records, maxima and sort segments are
+                                 computed for the samples the window needs    */
+    int32_t e0, e1;           /* path samples [e0, e1) whose coarse tracks the
+                                 window needs (its samples and the centres of
+                                 its sort segments; e1 <= 0: the whole path)  */
 } mvb_job;
 
 /* One CTA of the fast synthesis grid: samples [32U*tile, 32U*(tile+1)) of
@@ -311,6 +318,13 @@ int mvb_energy_index(const double* d_power, int64_t rows, int64_t F, double frac
 int mvb_track_coeffs(const mvb_image* d_images, const int32_t* d_sel, int64_t n_sel,
                      int64_t max_K, const mvb_job* d_jobs, const double* d_coarse,
                      const double* h_fit, mvb_coef32* d_coef, void* stream);
+/* The same for time-shard jobs (mvb_job w0/w1/e0/e1): only the intervals
+ * the job's output window reads, from the coarse samples its window has
+ * (max_K = the largest such coarse range).  A separate entry so the
+ * unwindowed kernel keeps its register budget. */
+int mvb_track_coeffs_windowed(const mvb_image* d_images, const int32_t* d_sel, int64_t n_sel,
+                              int64_t max_K, const mvb_job* d_jobs, const double* d_coarse,
+                              const double* h_fit, mvb_coef32* d_coef, void* stream);
 
 /* Delay-sort keys: d_key[(j * max_n_seg + s) * max_n_img + i] = distance of
  * image i of job j at the centre of segment s (samples [s*seg_len,
@@ -335,6 +349,17 @@ int mvb_delay_sort(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_j
                    int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
                    const double* d_paths, const double* d_coarse, int64_t key_bits,
                    mvb_image* d_out, void* stream);
+
+/* mvb_delay_sort in independent runs: slots [r * run_len, (r + 1) * run_len)
+ * of every (job, segment) hold the job's images of that table range sorted
+ * on their own (any image count; run_len <= MVB_DELAY_SORT_MAX).  Used for
+ * time-shard jobs, whose image table is in delay-band order (parallel.py
+ * band_order): band-local sorts then approximate the full sort, in one
+ * block per (segment, band) instead of one 16k-key block per segment. */
+int mvb_delay_sort_runs(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jobs,
+                        int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
+                        const double* d_paths, const double* d_coarse, int64_t key_bits,
+                        int64_t run_len, mvb_image* d_out, void* stream);
 
 /* Fast path: fp32 branch records v'_k = x (*) c'_k (d_cbranch (M1, L) fp64
  * in the centred basis (mu - 1/2)^k, zero branches k >= M1) of n_sig dry

@@ -48,8 +48,10 @@ _SIGS = {
     "mvb_track_max": [P, P, I64, P, P, P, DBL, P, P, P, P, P],
     "mvb_gather_images": [P, P, I64, P, P],
     "mvb_track_coeffs": [P, P, I64, I64, P, P, P, P, P],
+    "mvb_track_coeffs_windowed": [P, P, I64, I64, P, P, P, P, P],
     "mvb_sort_keys": [P, P, I64, I64, I64, I64, P, P, P, P],
     "mvb_delay_sort": [P, P, I64, I64, I64, I64, P, P, I64, P, P],
+    "mvb_delay_sort_runs": [P, P, I64, I64, I64, I64, P, P, I64, I64, P, P],
     "mvb_branch_records_f32": [P, P, P, P, P, P, I64, I64, P, INT, INT, INT, P, P],
     "mvb_synthesize_f32": [P, P, I64, P, P, P, P, P, P, INT, INT, P],
     "mvb_reduce_partials_f32": [P, I64, I64, P, P, P],
@@ -89,7 +91,7 @@ _KERNELS = {"mvb_track_max": 2, "mvb_path_bbox": 2, "mvb_center_paths": 2,
             "mvb_path_spectrum_scratch": 0, "mvb_lowpass_scratch": 0}
 _launches = 0
 
-IMAGE_BYTES, JOB_BYTES, WORK_BYTES, COEF_BYTES = 96, 136, 32, 48
+IMAGE_BYTES, JOB_BYTES, WORK_BYTES, COEF_BYTES = 96, 152, 32, 48
 
 
 MAX_CLASSES = 8

@@ -56,6 +56,28 @@ inline void prefer_carveout(const void* kernel, bool synthesis = false) {
         cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
 }
 
+// Time-shard windows (mvb_job w0/w1/e0/e1; all zero = the whole job).
+// Path samples [p0, p1) whose delays the window's output samples read:
+// sample n < T reads the track at n, samples n >= T the held value at T - 1.
+__host__ __device__ __forceinline__ int64_t win_p0(const mvb_job& J) {
+    return J.w0 < J.T - 1 ? (int64_t)J.w0 : (int64_t)J.T - 1;
+}
+__host__ __device__ __forceinline__ int64_t win_p1(const mvb_job& J) {
+    return (J.w1 > 0 && J.w1 < J.T) ? (int64_t)J.w1 : (int64_t)J.T;
+}
+// Coarse samples [k0, k1) (of K) a factor-N image of the job needs: the
+// window's path range and sort-segment centres [e0, e1), widened by the
+// 65-tap upsampler's +-32 coarse samples and one more for the records' dw.
+constexpr int64_t WIN_HALO = 34;
+__host__ __device__ __forceinline__ void win_coarse(const mvb_job& J, int64_t N, int64_t K,
+                                                    int64_t& k0, int64_t& k1) {
+    if (J.e1 <= 0) { k0 = 0; k1 = K; return; }
+    k0 = J.e0 / N - WIN_HALO;
+    k1 = (J.e1 - 1) / N + 1 + WIN_HALO;
+    k0 = k0 < 0 ? 0 : k0;
+    k1 = k1 > K ? K : k1;
+}
+
 inline unsigned grid_for(int64_t n, int block) {
     int64_t g = (n + block - 1) / block;
     return (unsigned)(g > 0 ? g : 1);

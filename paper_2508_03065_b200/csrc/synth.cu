@@ -604,7 +604,9 @@ __global__ void k_reduce_f32(const mvb_job* __restrict__ jobs, const float* __re
                              float* __restrict__ out) {
     const mvb_job J = jobs[blockIdx.y];
     if (J.n_chunks <= 1) return;
-    for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < J.out_len;
+    // a time shard's partials exist only on its window [w0, w1)
+    const int64_t n1 = J.w1 > 0 && J.w1 < J.out_len ? J.w1 : J.out_len;
+    for (int64_t n = J.w0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < n1;
          n += (int64_t)gridDim.x * blockDim.x) {
         const float* p = part + J.part_off + n;
         float s = p[0];

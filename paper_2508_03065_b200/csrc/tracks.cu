@@ -107,13 +107,23 @@ __global__ void k_coarse_bounds(const mvb_image* __restrict__ images, const int3
     // latency of these loads); a warp whose image has another path reads
     // global memory.
     __shared__ double sp[3 * 64 * (CB_SEGS + 2)];
+    // segments [seg_lo, seg_hi) of an image: its job's time-shard window
+    // (win_coarse; the whole track without one), chunk blockIdx.y of them
+    auto seg_range = [&](const mvb_image& q, int64_t& lo, int64_t& hi) {
+        int64_t k0, k1;
+        win_coarse(jobs[q.job], q.factor, q.n_coarse, k0, k1);
+        lo = k0 / 64;
+        hi = (k1 + 63) / 64;
+    };
     const int lane = threadIdx.x & 31;
-    const int64_t s0 = (int64_t)blockIdx.y * CB_SEGS;
     const int64_t w0 = (int64_t)blockIdx.x * (blockDim.x >> 5);
     int64_t r0 = 0, r1 = 0, ref_cpath = -1;
     {
         const mvb_image& ref = images[sel[w0]];  // w0 < n_sel by the grid
-        const int64_t Kr = ref.n_coarse, nsr = (Kr + 63) / 64;
+        const int64_t Kr = ref.n_coarse;
+        int64_t lo, nsr;
+        seg_range(ref, lo, nsr);
+        const int64_t s0 = lo + (int64_t)blockIdx.y * CB_SEGS;
         if (s0 < nsr) {
             const int64_t s1r = s0 + CB_SEGS < nsr ? s0 + CB_SEGS : nsr;
             r0 = s0 > 0 ? 64 * (s0 - 1) : 0;
@@ -130,8 +140,11 @@ __global__ void k_coarse_bounds(const mvb_image* __restrict__ images, const int3
     const mvb_image im = images[i];
     const int64_t K = im.n_coarse;
     const int64_t nseg = (K + 63) / 64;
-    if (s0 >= nseg) return;
-    const int64_t s1 = s0 + CB_SEGS < nseg ? s0 + CB_SEGS : nseg;
+    int64_t seg_lo, seg_hi;
+    seg_range(im, seg_lo, seg_hi);
+    const int64_t s0 = seg_lo + (int64_t)blockIdx.y * CB_SEGS;
+    if (s0 >= seg_hi) return;
+    const int64_t s1 = s0 + CB_SEGS < seg_hi ? s0 + CB_SEGS : seg_hi;
     const mvb_job& J = jobs[im.job];
     const bool staged = im.cpath == ref_cpath;  // same path rows, same K
     const double* src = staged ? sp : paths + 3 * im.cpath;
@@ -380,17 +393,20 @@ __global__ void k_exact_scan(const mvb_image* __restrict__ images, const mvb_job
     const int32_t* sc = scratch + MVB_EXACT_LIST_WORDS + J.img_off + j;
     const int count = sc[0];
     const int lane = threadIdx.x & 31;
-    const int64_t n_chunks = (J.T + EXACT_CHUNK - 1) / EXACT_CHUNK;
+    // sample chunks of the job's path range (its time-shard window's, win_p0/1)
+    const int64_t p0 = win_p0(J), p1 = win_p1(J);
+    const int64_t c_lo = p0 / EXACT_CHUNK;
+    const int64_t n_chunks = (p1 - 1) / EXACT_CHUNK + 1 - c_lo;
     const int64_t pairs = (int64_t)count * n_chunks;
     const int64_t wpb = blockDim.x >> 5;
     volatile double* dm = dmax + j;
     unsigned long long* list = reinterpret_cast<unsigned long long*>(scratch + 2);
     for (int64_t p = blockIdx.x * wpb + (threadIdx.x >> 5); p < pairs; p += gridDim.x * wpb) {
         const int slot = (int)(p / n_chunks);
-        const int64_t ch = p - (int64_t)slot * n_chunks;
+        const int64_t ch = c_lo + p - (int64_t)slot * n_chunks;
         const mvb_image im = images[sc[1 + slot]];
-        const int64_t t0 = ch * EXACT_CHUNK;
-        const int64_t t1 = t0 + EXACT_CHUNK < J.T ? t0 + EXACT_CHUNK : J.T;
+        const int64_t t0 = ch * EXACT_CHUNK > p0 ? ch * EXACT_CHUNK : p0;
+        const int64_t t1 = (ch + 1) * EXACT_CHUNK < p1 ? (ch + 1) * EXACT_CHUNK : p1;
         double best = 0.0;
         if (im.factor == 1) {
             for (int64_t t = t0 + lane; t < t1; t += 32)
@@ -432,7 +448,7 @@ __global__ void __launch_bounds__(EXACT_SUB) k_exact_eval(
         const mvb_image& im = images[sc[1 + slot]];
         const int64_t t = ch * EXACT_CHUNK + (int64_t)(u % SUBS) * EXACT_SUB + threadIdx.x;
         double v = 0.0;
-        if (t < J.T && t < (ch + 1) * EXACT_CHUNK)
+        if (t >= win_p0(J) && t < win_p1(J) && t < (ch + 1) * EXACT_CHUNK)
             v = exact_upsample(coarse + im.coarse, im.n_coarse, tables + im.table, im.factor, t);
         v = block_max(v, red);
         if (threadIdx.x == 0 && v > 0.0) atomic_max_pos(dmax + j, v);
@@ -472,7 +488,7 @@ struct CoefShape {
     static constexpr size_t SMEM = sizeof(float4) * REC_F4 * COEF_BLOCK + sizeof(float) * DW;
 };
 
-template <int COEF_BLOCK, int COEF_KI>
+template <int COEF_BLOCK, int COEF_KI, bool WIN>
 __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
     const __grid_constant__ SbpParam sp, const mvb_image* __restrict__ images,
     const int32_t* __restrict__ sel, const mvb_job* __restrict__ jobs,
@@ -490,17 +506,30 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
     const int64_t K = im.n_coarse;
     const double* c = coarse + im.coarse;
     const int e0 = COEF_KI * threadIdx.x;
-    for (int64_t k0 = (int64_t)blockIdx.y * COEF_SPAN; k0 < K;
-         k0 += (int64_t)gridDim.y * COEF_SPAN) {
+    // intervals [k_first, i1) and the coarse samples [lo, hi] that exist:
+    // the whole track, or (WIN, time shards) what the job's output window
+    // reads (win_p0 / win_p1, win_coarse).  A separate instantiation: the
+    // window bounds live across the loop cost ~16 registers (124 -> 140)
+    // and 13% of the unwindowed kernel's time (c4)
+    int lo = 0, hi = (int)K - 1, i1 = (int)K, k_first = 0;
+    if constexpr (WIN) {
+        int64_t ck0, ck1;
+        win_coarse(J, im.factor, K, ck0, ck1);
+        lo = (int)ck0;
+        hi = (int)ck1 - 1;
+        k_first = (int)(win_p0(J) / im.factor);
+        i1 = (int)((win_p1(J) - 1) / im.factor + 1);
+    }
+    for (int k0 = k_first + (int)blockIdx.y * COEF_SPAN; k0 < i1; k0 += (int)gridDim.y * COEF_SPAN) {
         __syncthreads();
         // coarse samples k0 - 32 .. k0 + COEF_SPAN + 32 (clamped: samples hold)
         // staged once in the record area (free until the epilogue), then
         // dw[i] = c[i + 1] - c[i] in fp64, stored fp32 (skewed)
         double* cw = reinterpret_cast<double*>(srec);
-        const int Ki = (int)K, base = (int)k0 - 32;
+        const int base = k0 - 32;
         for (int t = threadIdx.x; t < COEF_SPAN + 65; t += blockDim.x) {
             int a = base + t;
-            a = a < 0 ? 0 : (a >= Ki ? Ki - 1 : a);
+            a = a < lo ? lo : (a > hi ? hi : a);
             cw[t] = c[a];
         }
         __syncthreads();
@@ -512,7 +541,7 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
         for (int t = threadIdx.x; t < COEF_SPAN + 64; t += blockDim.x)
             dw[skew32(t)] = (float)(cw[t + 1] - cw[t]);
         __syncthreads();
-        if (k0 + e0 < K) {
+        if (k0 + e0 < i1) {
         static_assert(COEF_KI % 2 == 0, "the g8 accumulators pair adjacent intervals");
         float2 acc[COEF_KI][4];
         float2 acc8[COEF_KI / 2];  // (interval 2h, interval 2h+1) of coefficient 8
@@ -547,7 +576,7 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
 #pragma unroll
         for (int q = 0; q < COEF_KI; ++q) {
             const int64_t k = k0 + e0 + q;
-            if (k >= K) break;
+            if (k >= i1) break;
             const double g0 = anchor[q] + (double)acc[q][0].x;
             mvb_coef32 r;
             const double base = fma(kappa, g0, shift);
@@ -574,7 +603,7 @@ __global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
         }
         __syncthreads();
         // coalesced copy of the span's records (16 B per thread per pass)
-        const int64_t n_rec = K - k0 < COEF_SPAN ? K - k0 : COEF_SPAN;
+        const int64_t n_rec = i1 - k0 < COEF_SPAN ? i1 - k0 : COEF_SPAN;
         const float4* src = srec;
         float4* dst = reinterpret_cast<float4*>(out + im.coef + k0);
         for (int64_t t = threadIdx.x; t < n_rec * 3; t += blockDim.x) {
@@ -594,6 +623,16 @@ __global__ void k_gather_images(const mvb_image* __restrict__ images, const int6
     reinterpret_cast<float4*>(out + q)[c] = __ldg(reinterpret_cast<const float4*>(images + idx[q]) + c);
 }
 
+// Sort segment s of a windowed job that none of the window's tiles reads
+// (a tile reads segment min(n / seg_len, last), n its first sample).
+__device__ __forceinline__ bool outside_window(const mvb_job& J, int64_t s, int64_t seg_len) {
+    if (J.w0 == 0 && J.w1 <= 0) return false;
+    const int64_t last = (J.T + seg_len - 1) / seg_len - 1;
+    const int64_t a = J.w0 / seg_len < last ? J.w0 / seg_len : last;
+    const int64_t b = J.w1 > 0 && (J.w1 - 1) / seg_len < last ? (J.w1 - 1) / seg_len : last;
+    return s < a || s > b;
+}
+
 __global__ void k_sort_keys(const mvb_image* __restrict__ images, const mvb_job* __restrict__ jobs,
                             int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
                             const double* __restrict__ paths, const double* __restrict__ coarse,
@@ -601,7 +640,7 @@ __global__ void k_sort_keys(const mvb_image* __restrict__ images, const mvb_job*
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t s = blockIdx.y, j = blockIdx.z;
     const mvb_job& J = jobs[j];
-    if (i >= J.n_img || s * seg_len >= J.T) return;
+    if (i >= J.n_img || s * seg_len >= J.T || outside_window(J, s, seg_len)) return;
     const mvb_image im = images[J.img_off + i];
     int64_t t = s * seg_len + seg_len / 2;
     if (t > J.T - 1) t = J.T - 1;
@@ -632,17 +671,23 @@ __global__ void __launch_bounds__(BT) k_delay_sort(const mvb_image* __restrict__
                                                    int64_t max_n_img, int64_t max_n_seg,
                                                    int64_t seg_len, const double* __restrict__ paths,
                                                    const double* __restrict__ coarse, int key_bits,
-                                                   mvb_image* __restrict__ out) {
+                                                   int64_t run_len, mvb_image* __restrict__ out) {
     using Sort = cub::BlockRadixSort<unsigned, BT, IPT, int>;
     extern __shared__ __align__(16) unsigned char dsort_smem[];
     auto& temp = *reinterpret_cast<typename Sort::TempStorage*>(dsort_smem);
     const int64_t s = blockIdx.x, j = blockIdx.y;
     const mvb_job& J = jobs[j];
-    const int n = (int)J.n_img;
+    if (outside_window(J, s, seg_len)) return;  // block-uniform: no tile reads it
+    // run blockIdx.z: slots [base, base + run_len) of the job's table, its
+    // images [base, base + n) sorted on their own (one run: the whole job)
+    const int64_t base = (int64_t)blockIdx.z * run_len;
+    if (base >= max_n_img) return;
+    const int n = (int)(J.n_img - base < run_len ? (J.n_img > base ? J.n_img - base : 0) : run_len);
+    const int slots = (int)(max_n_img - base < run_len ? max_n_img - base : run_len);
     const bool active = s * seg_len < J.T;
     int64_t t = s * seg_len + seg_len / 2;
     if (t > J.T - 1) t = J.T - 1;
-    const mvb_image* __restrict__ im0 = images + J.img_off;
+    const mvb_image* __restrict__ im0 = images + J.img_off + base;
     const unsigned kmax = key_bits >= 32 ? 0xffffffffu : (1u << key_bits) - 1u;
     const double kappa = J.kappa;
     unsigned keys[IPT];
@@ -668,13 +713,14 @@ __global__ void __launch_bounds__(BT) k_delay_sort(const mvb_image* __restrict__
         vals[k] = i;
     }
     Sort(temp).SortBlockedToStriped(keys, vals, 0, key_bits);
-    mvb_image* __restrict__ dst = out + (j * max_n_seg + s) * max_n_img;
+    mvb_image* __restrict__ dst = out + (j * max_n_seg + s) * max_n_img + base;
     constexpr int CH = sizeof(mvb_image) / 16;
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
         const int q = k * BT + threadIdx.x;  // striped arrangement
-        if (q < max_n_img) {
-            const int src = vals[k] < n - 1 ? vals[k] : n - 1;
+        if (q < slots) {
+            // padding slots (past the job's images) repeat an own image
+            const int64_t src = n > 0 ? (vals[k] < n - 1 ? vals[k] : n - 1) : J.n_img - 1 - base;
             const float4* a = reinterpret_cast<const float4*>(im0 + src);
             float4* b = reinterpret_cast<float4*>(dst + q);
 #pragma unroll
@@ -687,7 +733,7 @@ template <int BT, int IPT>
 static int launch_delay_sort(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
                              int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
                              const double* paths, const double* coarse, int key_bits,
-                             mvb_image* out, cudaStream_t s) {
+                             int64_t run_len, mvb_image* out, cudaStream_t s) {
     using Sort = cub::BlockRadixSort<unsigned, BT, IPT, int>;
     const size_t smem = sizeof(typename Sort::TempStorage);
     static bool attr = false;  // one opt-in per process and instantiation
@@ -696,9 +742,11 @@ static int launch_delay_sort(const mvb_image* images, const mvb_job* jobs, int64
                              (int)smem);
         attr = true;
     }
+    const int64_t runs = (max_n_img + run_len - 1) / run_len;
     prefer_carveout((const void*)k_delay_sort<BT, IPT>);
-    k_delay_sort<BT, IPT><<<dim3((unsigned)max_n_seg, (unsigned)n_jobs), BT, smem, s>>>(
-        images, jobs, max_n_img, max_n_seg, seg_len, paths, coarse, key_bits, out);
+    k_delay_sort<BT, IPT><<<dim3((unsigned)max_n_seg, (unsigned)n_jobs, (unsigned)runs), BT, smem,
+                            s>>>(images, jobs, max_n_img, max_n_seg, seg_len, paths, coarse,
+                                 key_bits, run_len, out);
     return MVB_OK;
 }
 
@@ -952,7 +1000,7 @@ __global__ void k_build_images(const double* __restrict__ toff, const double* __
     }
 }
 
-template <int BLOCK, int KI>
+template <int BLOCK, int KI, bool WIN>
 static int launch_coeffs(const SbpParam& sp, const mvb_image* images, const int32_t* sel,
                          int64_t n_sel, int64_t max_K, const mvb_job* jobs, const double* coarse,
                          mvb_coef32* coef, void* stream) {
@@ -961,14 +1009,14 @@ static int launch_coeffs(const SbpParam& sp, const mvb_image* images, const int3
     if (spans > 65535) spans = 65535;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_coeffs<BLOCK, KI>,
+        cudaError_t e = cudaFuncSetAttribute(k_coeffs<BLOCK, KI, WIN>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM);
         if (e != cudaSuccess) return fail(MVB_ECUDA, cudaGetErrorString(e));
         attr_set = true;
     }
-    prefer_carveout((const void*)k_coeffs<BLOCK, KI>);
-    k_coeffs<BLOCK, KI><<<dim3((unsigned)n_sel, (unsigned)spans), BLOCK, S::SMEM, as_stream(stream)>>>(
-        sp, images, sel, jobs, coarse, coef);
+    prefer_carveout((const void*)k_coeffs<BLOCK, KI, WIN>);
+    k_coeffs<BLOCK, KI, WIN><<<dim3((unsigned)n_sel, (unsigned)spans), BLOCK, S::SMEM,
+                               as_stream(stream)>>>(sp, images, sel, jobs, coarse, coef);
     return check_launch("track_coeffs");
 }
 
@@ -1106,14 +1154,14 @@ int mvb_track_max(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
     return check_launch("track_max");
 }
 
-int mvb_track_coeffs(const mvb_image* images, const int32_t* sel, int64_t n_sel,
-                     int64_t max_K, const mvb_job* jobs, const double* coarse,
-                     const double* h_fit, mvb_coef32* coef, void* stream) {
+static int track_coeffs(const mvb_image* images, const int32_t* sel, int64_t n_sel,
+                        int64_t max_K, const mvb_job* jobs, const double* coarse,
+                        const double* h_fit, mvb_coef32* coef, bool windowed, void* stream) {
     if (n_sel < 0 || n_sel > 0x7fffffff) return fail(MVB_EINVAL, "track_coeffs: n_sel");
     if (n_sel == 0) return MVB_OK;
     if (!images || !sel || !jobs || !coarse || !h_fit || !coef)
         return fail(MVB_EINVAL, "track_coeffs: null");
-    if (max_K < 1) return fail(MVB_EINVAL, "track_coeffs: max_K");
+    if (max_K < 1 || max_K > 0x7fffffff) return fail(MVB_EINVAL, "track_coeffs: max_K");
     // summation-by-parts weights G[p][j] = sum_{c>j} F[p][c] (j >= 32) or
     // -sum_{c<=j} F[p][c] (j < 32), formed in fp64, stored fp32 per tap
     SbpParam sp;
@@ -1129,39 +1177,79 @@ int mvb_track_coeffs(const mvb_image* images, const int32_t* sel, int64_t n_sel,
         sp.g[j][9] = 0.f;
     }
     // 64 threads x 8 intervals: measured best of {64,128,256} x {4,8} on c3/c4
-    // (more resident blocks hide the staging prologue; 70% of the FFMA peak on c4)
-    return launch_coeffs<64, 8>(sp, images, sel, n_sel, max_K, jobs, coarse, coef, stream);
+    // (more resident blocks hide the staging prologue; 70% of the FFMA peak on c4).
+    // Time-shard windows (~250 intervals of a N = 256 image at W = 8) would
+    // leave half of a 512-interval span idle: one warp x 8 there.
+    if (windowed) {
+        if (max_K <= 768)
+            return launch_coeffs<32, 8, true>(sp, images, sel, n_sel, max_K, jobs, coarse, coef,
+                                              stream);
+        return launch_coeffs<64, 8, true>(sp, images, sel, n_sel, max_K, jobs, coarse, coef, stream);
+    }
+    return launch_coeffs<64, 8, false>(sp, images, sel, n_sel, max_K, jobs, coarse, coef, stream);
+}
+
+int mvb_track_coeffs(const mvb_image* images, const int32_t* sel, int64_t n_sel,
+                     int64_t max_K, const mvb_job* jobs, const double* coarse,
+                     const double* h_fit, mvb_coef32* coef, void* stream) {
+    return track_coeffs(images, sel, n_sel, max_K, jobs, coarse, h_fit, coef, false, stream);
+}
+
+int mvb_track_coeffs_windowed(const mvb_image* images, const int32_t* sel, int64_t n_sel,
+                              int64_t max_K, const mvb_job* jobs, const double* coarse,
+                              const double* h_fit, mvb_coef32* coef, void* stream) {
+    return track_coeffs(images, sel, n_sel, max_K, jobs, coarse, h_fit, coef, true, stream);
+}
+
+static int delay_sort_runs(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
+                           int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
+                           const double* paths, const double* coarse, int64_t key_bits,
+                           int64_t run_len, mvb_image* out, void* stream) {
+    if (n_jobs < 0 || n_jobs > 65535 || max_n_img < 0 || max_n_seg < 0 ||
+        max_n_seg > 0x7fffffff || seg_len < 1)
+        return fail(MVB_EINVAL, "delay_sort: sizes");
+    if (run_len < 1 || run_len > MVB_DELAY_SORT_MAX)
+        return fail(MVB_EINVAL, "delay_sort: too many images per run");
+    if ((max_n_img + run_len - 1) / run_len > 65535) return fail(MVB_EINVAL, "delay_sort: runs");
+    if (key_bits < 1 || key_bits > 32) return fail(MVB_EINVAL, "delay_sort: key_bits");
+    if (n_jobs == 0 || max_n_img == 0 || max_n_seg == 0) return MVB_OK;
+    if (!images || !jobs || !paths || !out) return fail(MVB_EINVAL, "delay_sort: null");
+    cudaStream_t s = as_stream(stream);
+    const int kb = (int)key_bits;
+    int rc;
+    if (run_len <= 1024)
+        rc = launch_delay_sort<256, 4>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
+                                       coarse, kb, run_len, out, s);
+    else if (run_len <= 2048)
+        rc = launch_delay_sort<256, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
+                                       coarse, kb, run_len, out, s);
+    else if (run_len <= 4096)
+        rc = launch_delay_sort<512, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
+                                       coarse, kb, run_len, out, s);
+    else if (run_len <= 8192)
+        rc = launch_delay_sort<1024, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len,
+                                        paths, coarse, kb, run_len, out, s);
+    else
+        rc = launch_delay_sort<1024, 16>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len,
+                                         paths, coarse, kb, run_len, out, s);
+    if (rc != MVB_OK) return rc;
+    return check_launch("delay_sort");
 }
 
 int mvb_delay_sort(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
                    int64_t max_n_img, int64_t max_n_seg, int64_t seg_len, const double* paths,
                    const double* coarse, int64_t key_bits, mvb_image* out, void* stream) {
-    if (n_jobs < 0 || n_jobs > 65535 || max_n_img < 0 || max_n_seg < 0 ||
-        max_n_seg > 0x7fffffff || seg_len < 1)
-        return fail(MVB_EINVAL, "delay_sort: sizes");
     if (max_n_img > MVB_DELAY_SORT_MAX) return fail(MVB_EINVAL, "delay_sort: too many images");
-    if (key_bits < 1 || key_bits > 32) return fail(MVB_EINVAL, "delay_sort: key_bits");
-    if (n_jobs == 0 || max_n_img == 0 || max_n_seg == 0) return MVB_OK;
-    if (!images || !jobs || !paths || !out) return fail(MVB_EINVAL, "delay_sort: null");
-    cudaStream_t s = as_stream(stream);
-    int rc;
-    if (max_n_img <= 1024)
-        rc = launch_delay_sort<256, 4>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
-                                       coarse, (int)key_bits, out, s);
-    else if (max_n_img <= 2048)
-        rc = launch_delay_sort<256, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
-                                       coarse, (int)key_bits, out, s);
-    else if (max_n_img <= 4096)
-        rc = launch_delay_sort<512, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
-                                       coarse, (int)key_bits, out, s);
-    else if (max_n_img <= 8192)
-        rc = launch_delay_sort<1024, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len,
-                                        paths, coarse, (int)key_bits, out, s);
-    else
-        rc = launch_delay_sort<1024, 16>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len,
-                                         paths, coarse, (int)key_bits, out, s);
-    if (rc != MVB_OK) return rc;
-    return check_launch("delay_sort");
+    return delay_sort_runs(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths, coarse,
+                           key_bits, max_n_img > 0 ? max_n_img : 1, out, stream);
+}
+
+int mvb_delay_sort_runs(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
+                        int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
+                        const double* paths, const double* coarse, int64_t key_bits,
+                        int64_t run_len, mvb_image* out, void* stream) {
+    return delay_sort_runs(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths, coarse,
+                           key_bits, run_len, out, stream);
 }
 
 int mvb_sort_keys(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs, int64_t max_n_img,

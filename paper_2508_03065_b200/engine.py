@@ -65,7 +65,8 @@ def _mark(name: str) -> None:
 SYNTH_U = 16  # steps per lane (mvb_synthesize_f32 u_steps)
 TILE = 32 * SYNTH_U  # output samples per CTA
 SEG_LEN = 32 * TILE  # samples per delay-sort segment
-IMG_COLS, JOB_COLS, WORK_COLS = 12, 17, 4
+SORT_RUN = 2048  # images per independent sort run of time-shard jobs
+IMG_COLS, JOB_COLS, WORK_COLS = 12, 19, 4
 BOX_WORDS = 16  # mvb_path_bbox record: boxes (12), max steps (2), pad (2)
 # fp32 fast-path accuracy envelope: the largest delay excursion (samples) of
 # one coarse interval that the fp32 residual of the interval records may
@@ -91,7 +92,47 @@ class Job:
     image_index: object = None  # optional subset of the canonical image order
     signal_key: object = None  # jobs with equal keys share one dry signal
     path_key: object = None  # jobs with equal keys share one source path
+    # time shard (parallel.time_window): render output samples [w0, w1) only
+    # (w1 = 0: to the end), zeros elsewhere; the track maximum is then the
+    # window's -- a dmax hook must all-reduce it (MAX) for the reference's
+    # out_len
+    window: tuple = None
 
+
+def window_fields(T: int, window) -> dict:
+    """mvb_job w0, w1, e0, e1 of a job with path length T and output window
+    `window` (None: the whole job, all zero).  [e0, e1): path samples whose
+    coarse tracks the window needs -- its path range (win_p0 / win_p1 of
+    mvb_common.cuh) and the centres of the sort segments its tiles read."""
+    if window is None:
+        return dict(w0=0, w1=0, e0=0, e1=0)
+    w0, w1 = int(window[0]), int(window[1])
+    if w0 < 0 or w0 % TILE or (w1 > 0 and (w1 <= w0 or w1 % TILE)):
+        raise ValueError(f"window {window}: need 0 <= w0 < w1 (w1 = 0: open), multiples of {TILE}")
+    T = int(T)
+    p0 = min(w0, T - 1)
+    p1 = min(w1, T) if w1 > 0 else T
+    last = -(-T // SEG_LEN) - 1
+    sa = min(w0 // SEG_LEN, last)
+    sb = min((w1 - 1) // SEG_LEN, last) if w1 > 0 else last
+    ca = min(sa * SEG_LEN + SEG_LEN // 2, T - 1)
+    cb = min(sb * SEG_LEN + SEG_LEN // 2, T - 1)
+    return dict(w0=w0, w1=w1, e0=min(p0, ca), e1=max(p1, cb + 1))
+
+
+def coarse_span(rows: list, N: int) -> int:
+    """Largest coarse-sample range [k0, k1) (win_coarse) a factor-N image of
+    these job rows computes, + one 64-sample segment of alignment."""
+    out = 1
+    for r in rows:
+        K = -(-int(r["T"]) // N)
+        if r.get("e1", 0) <= 0:
+            out = max(out, K)
+            continue
+        k0 = max(int(r["e0"]) // N - 34, 0)
+        k1 = min((int(r["e1"]) - 1) // N + 1 + 34, K)
+        out = max(out, k1 - k0 + 64)
+    return out
 
 
 
@@ -129,7 +170,9 @@ def pack_jobs(rows: list) -> np.ndarray:
                      r["img_off"], r["n_img"], r["pos_off"], r["mic_off"]]
         i32[j] = [r["T"], r["mic_moving"], r["L"], r["d0"], r["n_chunks"], r["nb"]]
         f64[j] = [r["rate"], r["c"], r["d_min"], r["kappa"]]
-        a[j, 16:17].view(np.int32)[:] = [r.get("img_stride", 0), r.get("rec_rows", 0)]
+        a[j, 16:19].view(np.int32)[:] = [r.get("img_stride", 0), r.get("rec_rows", 0),
+                                          r.get("w0", 0), r.get("w1", 0),
+                                          r.get("e0", 0), r.get("e1", 0)]
     return a
 
 
@@ -396,7 +439,7 @@ class Geometry:
                 pos_off=int(self.pos_off[j]), mic_off=int(self.mic_off[j]),
                 T=int(self.T[j]), mic_moving=int(self.moving[j]), L=0, d0=0, n_chunks=1, nb=0,
                 rate=float(jb.rate), c=float(jb.c), d_min=float(jb.d_min),
-                kappa=float(jb.rate) / float(jb.c)))
+                kappa=float(jb.rate) / float(jb.c), **window_fields(self.T[j], jb.window)))
         # kept: the exact-maximum branch (a parallel graph branch in plan
         # captures) still reads it after this function returns
         jobs_dev = self._jobs_dev = h2d(pack_jobs(self.job_rows), dev)
@@ -408,7 +451,7 @@ class Geometry:
         # coarse distances + bounds of the decimated images, one launch per
         # factor (its grid spans that factor's coarse length, no idle chunks)
         for N, sel in self.sel_by_factor.items():
-            max_K = max(-(-int(self.T[j]) // N2) for (j, N2) in self.cpath if N2 == N)
+            max_K = coarse_span([self.job_rows[j] for (j, N2) in self.cpath if N2 == N], N)
             _lib.call("mvb_coarse_distances", ptr(self.images), ptr(sel), sel.numel(), max_K,
                       ptr(jobs_dev), ptr(self.paths), negsum, ptr(self.coarse), ptr(lb), ptr(ub),
                       st)
@@ -865,6 +908,7 @@ class RenderResult:
 
 
 CHUNK_MIN_IMAGES = int(os.environ.get("MVB_CHUNK_MIN_IMAGES", "320"))
+CHUNK_WAVES = float(os.environ.get("MVB_CHUNK_WAVES", "12"))  # target waves of 3 CTAs / SM
 # batches with few tiles (c2: 131) need many chunks per tile to fill the GPU;
 # there smaller chunks win (c2 synthesis 0.335 -> 0.233 ms at 160), while a
 # W = 8 image shard of c3 (1050 tiles, 1440 images) is 1.5% faster at 320
@@ -877,7 +921,7 @@ def _chunking(n_imgs, tiles, sm_count):
     images (a CTA's staging prologue and reduction epilogue amortise over
     them; image shards with ~1.4k images per job were 2% slower at 128)."""
     total_tiles = int(sum(tiles))
-    want = 36 * sm_count
+    want = int(CHUNK_WAVES * 3 * sm_count)
     if total_tiles >= want:
         return [1] * len(n_imgs)
     cmin = SMALL_GRID_CHUNK_MIN if total_tiles < SMALL_GRID_TILES else CHUNK_MIN_IMAGES
@@ -937,6 +981,9 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         # receivers moving at hundreds of m/s under a large decimation):
         # the exact fp64 engine renders the batch instead
         precision = "fp64"
+    if precision == "fp64" and any(jb.window is not None for jb in jobs):
+        raise ValueError("time-shard windows need the fp32 fast path (the exact engine runs "
+                         "replicas only; fast sources beyond the fp32 envelope cannot be sharded)")
     sm_count = _sm_count(dev.index if dev.index is not None else torch.cuda.current_device())
     # signals: dedupe, upload
     keys = signal_keys or [_key(jobs[j].signal_key, signals[j]) for j in range(nJ)]
@@ -1091,17 +1138,19 @@ def _interval_records(geom, pre_dev, st, fork=()) -> torch.Tensor:
     branches (the caller joins them)."""
     dev = geom.dev
     coef = torch.empty(max(geom.n_coarse_total, 1) * 12, dtype=torch.float32, device=dev)
+    windowed = any(jb.window is not None for jb in geom.jobs)
     main = torch.cuda.current_stream(dev)
     start = torch.cuda.Event()
     start.record(main)  # fork point: before the first factor's launch
     for q, (N, sel) in enumerate(geom.sel_by_factor.items()):
         fit = np.ascontiguousarray(phase_fit(N), dtype=np.float64)
-        max_K = -(-int(geom.T.max()) // N)
+        max_K = coarse_span(geom.job_rows, N)
         fs = fork[(q - 1) % len(fork)] if q and fork else main
         if fs is not main:
             fs.wait_event(start)
         with torch.cuda.stream(fs):
-            _lib.call("mvb_track_coeffs", ptr(geom.images), ptr(sel), sel.numel(), max_K,
+            _lib.call("mvb_track_coeffs_windowed" if windowed else "mvb_track_coeffs",
+                      ptr(geom.images), ptr(sel), sel.numel(), max_K,
                       ptr(pre_dev), ptr(geom.coarse), fit.ctypes.data_as(ctypes.c_void_p),
                       ptr(coef), stream_handle(dev))
     return coef
@@ -1117,12 +1166,22 @@ def _delay_sort(geom, pre_dev, st):
     dev, nJ = geom.dev, len(geom.jobs)
     n_seg = [-(-int(geom.T[j]) // SEG_LEN) for j in range(nJ)]
     max_seg, max_img = max(n_seg), int(geom.n_img.max())
-    if max_img <= _lib.DELAY_SORT_MAX:  # fused keys + block radix sort + gather, one launch
+    windowed = any(jb.window is not None for jb in geom.jobs)
+    if max_img <= _lib.DELAY_SORT_MAX or windowed:
+        # fused keys + block radix sort + gather, one launch.  Time-shard
+        # jobs (image table in delay-band order, parallel.band_order) sort
+        # in independent runs of SORT_RUN images: a few segments per rank,
+        # each one 16k-key block sort, would be a ~140 us chain at W = 8
         images_sorted = torch.empty(nJ * max_seg * max_img, IMG_COLS, dtype=torch.int64,
                                     device=dev)
         key_bits = max(1, min(32, max(int(geom.length_bound(j)) for j in range(nJ)).bit_length()))
-        _lib.call("mvb_delay_sort", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg, SEG_LEN,
-                  ptr(geom.paths), ptr(geom.coarse), key_bits, ptr(images_sorted), st)
+        if windowed:
+            _lib.call("mvb_delay_sort_runs", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg,
+                      SEG_LEN, ptr(geom.paths), ptr(geom.coarse), key_bits, SORT_RUN,
+                      ptr(images_sorted), st)
+        else:
+            _lib.call("mvb_delay_sort", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg,
+                      SEG_LEN, ptr(geom.paths), ptr(geom.coarse), key_bits, ptr(images_sorted), st)
         return images_sorted, n_seg, max_seg, max_img
     key = torch.full((nJ, max_seg, max_img), float("inf"), dtype=torch.float64, device=dev)
     _lib.call("mvb_sort_keys", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg, SEG_LEN,
@@ -1213,9 +1272,14 @@ def _table_records(uniq, sig_dev, sig_len, start, rec_rows, filt, dev, st, conca
 def _work_list(n_img, out_len, n_seg, sm_count, rows):
     """mvb_work items (job, tile, image range, chunk, sort segment) of every
     job, image ranges split into chunks (_chunking); chunked jobs get
-    partial-output rows (rows[j]['n_chunks'], ['part_off'] are set)."""
+    partial-output rows (rows[j]['n_chunks'], ['part_off'] are set).  A
+    time-shard job (rows[j] w0 / w1) gets the tiles of its window only."""
     nJ = len(rows)
-    tiles = [-(-int(out_len[j]) // TILE) for j in range(nJ)]
+    first = [int(rows[j].get("w0", 0)) // TILE for j in range(nJ)]
+    end = [-(-int(out_len[j]) // TILE) for j in range(nJ)]
+    end = [min(e, int(rows[j]["w1"]) // TILE) if rows[j].get("w1", 0) > 0 else e
+           for j, e in enumerate(end)]
+    tiles = [max(e - a, 0) for a, e in zip(first, end)]
     chunks = _chunking([int(v) for v in n_img], tiles, sm_count)
     part_rows, blocks = 0, []
     for j in range(nJ):
@@ -1228,10 +1292,15 @@ def _work_list(n_img, out_len, n_seg, sm_count, rows):
         cs = np.arange(nc)
         blk = np.zeros((nc, tiles[j], 8), dtype=np.int32)
         blk[:, :, 0] = j
-        blk[:, :, 1] = np.arange(tiles[j])[None, :]
+        tj = np.arange(first[j], first[j] + tiles[j])
+        blk[:, :, 1] = tj[None, :]
         blk[:, :, 2] = ((span * cs) // nc)[:, None]
         blk[:, :, 3] = ((span * (cs + 1)) // nc)[:, None]
         blk[:, :, 4] = cs[:, None]
-        blk[:, :, 5] = np.minimum(np.arange(tiles[j]) * TILE // SEG_LEN, n_seg[j] - 1)[None, :]
+        blk[:, :, 5] = np.minimum(tj * TILE // SEG_LEN, n_seg[j] - 1)[None, :]
         blocks.append(blk.reshape(-1, 8))
-    return np.concatenate(blocks), part_rows
+    work = np.concatenate(blocks)
+    if len(work) == 0:  # every window past its job's length bound: one idle item
+        work = np.zeros((1, 8), np.int32)
+        work[0, 1] = end[0]  # n0 >= out_len: the CTA returns at once
+    return work, part_rows

@@ -19,8 +19,18 @@ One process per GPU (torchrun), torch.distributed for the plumbing:
                  reference's out_len) and one reduce (sum) of the output
                  buffers to rank 0 -- NCCL over NVLink on B200, ~2 MB (c3) /
                  ~13 MB (c5) per render.
+  time shards    (shard=(rank, world, "time")): rank r renders output
+                 samples [w0, w1) of every job from all images (time_window:
+                 whole tiles, cut at equal estimated cost) -- every per-sample
+                 stage (coarse tracks, bounds, interval records, exact
+                 maxima, sort segments, synthesis) divides by W, where image
+                 shards keep the per-job geometry on every rank.  The same two
+                 exchanges: all-reduce MAX of the window maxima (the global
+                 out_len) and the reduce (sum) of the outputs, zero outside a
+                 rank's window, to rank 0.
   scene shards   c4: independent scenes, longest-processing-time assignment
                  by update count; no collective.
+  channel shards c5: the receivers of a scene (independent jobs); no collective.
   replicas       c1, c2: too small to split; every rank renders the job.
 
 The partition functions are pure host logic (tested with gloo on CPU);
@@ -30,6 +40,7 @@ The partition functions are pure host logic (tested with gloo on CPU);
 from __future__ import annotations
 
 import heapq
+import os
 from functools import lru_cache
 
 import numpy as np
@@ -103,6 +114,28 @@ def _image_shard(key) -> np.ndarray:
     return out
 
 
+def band_order(dims, max_order: int, images=None) -> np.ndarray:
+    """The job's canonical image positions (all, or `images`) ordered by
+    |j * dims| (ties by canonical position): time-shard jobs build their
+    image table in this order so independent sorts of consecutive runs
+    (mvb_delay_sort_runs) approximate one delay sort.  Structural."""
+    key = (np.asarray(dims, dtype=np.float64).tobytes(), int(max_order),
+           None if images is None else np.asarray(images, dtype=np.int64).tobytes())
+    return _band_order(key)
+
+
+@lru_cache(maxsize=64)
+def _band_order(key) -> np.ndarray:
+    dims_b, max_order, images_b = key
+    j, order = canonical_lattice(max_order)
+    idx = np.arange(order.size, dtype=np.int64) if images_b is None \
+        else np.frombuffer(images_b, dtype=np.int64)
+    d = np.linalg.norm(j[idx] * np.frombuffer(dims_b, np.float64)[None, :], axis=1)
+    out = idx[np.lexsort((idx, d))]
+    out.flags.writeable = False
+    return out
+
+
 SPARSITY_COST = 0.4  # extra synthesis cost of an image ~ SPARSITY_COST / local density (per m)
 
 
@@ -129,16 +162,98 @@ def _band_cuts(keys: np.ndarray, world: int) -> np.ndarray:
     return np.maximum.accumulate(np.clip(cut, 0, n)).astype(np.int64)
 
 
-def shard_jobs(jobs, rank: int, world: int) -> list:
-    """Jobs restricted to their image shard of `rank` (image_shard), with
-    explicit path / signal keys so shards of one batch still share them."""
+def shard_jobs(jobs, rank: int, world: int, by: str = "images") -> list:
+    """Jobs restricted to their shard of `rank`, with explicit path / signal
+    keys so shards of one batch still share them: by="images" the image
+    shard (image_shard), by="time" the output window (time_window)."""
     from dataclasses import replace
 
     from . import engine
+    if by not in ("images", "time"):
+        raise ValueError("shard by 'images' or 'time'")
+    keys = [dict(signal_key=engine._key(jb.signal_key, jb.s),
+                 path_key=engine._key(jb.path_key, jb.pos)) for jb in jobs]
+    if by == "time":
+        return [replace(jb, window=time_window(jb, rank, world),
+                        image_index=band_order(jb.dims, jb.max_order, jb.image_index), **k)
+                for jb, k in zip(jobs, keys)]
     return [replace(jb, image_index=image_shard(jb.dims, jb.max_order, jb.tiers, rank, world,
-                                                jb.image_index),
-                    signal_key=engine._key(jb.signal_key, jb.s),
-                    path_key=engine._key(jb.path_key, jb.pos)) for jb in jobs]
+                                                jb.image_index), **k)
+            for jb, k in zip(jobs, keys)]
+
+
+def shard_kind(shard) -> str:
+    """'images' (default) or 'time' of a shard tuple (rank, world[, kind])."""
+    return str(shard[2]) if shard is not None and len(shard) > 2 else "images"
+
+
+def _length(a) -> int:
+    return int(a.shape[0]) if hasattr(a, "shape") else len(a)
+
+
+TIME_GEOMETRY_COST = 0.1  # per-rank tracks + records per path sample and image, in updates
+# an image with no contribution to a tile (before its first arrival, after
+# the signal) still costs its staging and zero test, in updates per sample
+TIME_SKIP_COST = float(os.environ.get("MVB_TIME_SKIP_COST", "0.2"))
+
+
+def time_window(jb, rank: int, world: int) -> tuple:
+    """Output window (w0, w1) of `rank` for the time shards of job `jb`
+    (w1 = 0: to the end of the output).  Structural -- a function of the
+    room, image order, path / signal lengths, rate and world only -- so
+    every rank computes the same cuts and a render plan's shard never
+    changes with the data.  Cost of output sample n: the images that
+    contribute to it, #{i : tau_i <= n < Ts + tau_i} with tau_i estimated as
+    kappa * |j_i * dims| (the image of the room centre; a few metres off for
+    off-centre sources, i.e. a few hundred samples of a ~1e4-1e5-sample
+    delay spread), plus TIME_GEOMETRY_COST * S for every path sample (the
+    window's tracks and interval records) and TIME_SKIP_COST * S for every
+    output sample (images skipped as exact zeros still cost their staging).
+    Cuts land on whole TILEs."""
+    from .engine import TILE
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("need 0 <= rank < world")
+    if world == 1:
+        return (0, 0)
+    T = _length(jb.pos)
+    Ts = int(np.prod(jb.s.shape)) if hasattr(jb.s, "shape") else len(jb.s)
+    key = (np.asarray(jb.dims, dtype=np.float64).tobytes(), int(jb.max_order),
+           None if jb.image_index is None else np.asarray(jb.image_index, np.int64).tobytes(),
+           int(T), int(Ts), float(jb.rate) / float(jb.c), int(world), int(TILE), TIME_SKIP_COST)
+    cuts = _time_cuts(key)
+    return (int(cuts[rank]) * TILE, int(cuts[rank + 1]) * TILE if rank + 1 < world else 0)
+
+
+@lru_cache(maxsize=256)
+def _time_cuts(key) -> np.ndarray:
+    dims_b, max_order, images_b, T, Ts, kappa, world, tile, skip = key
+    j, _ = canonical_lattice(max_order)
+    if images_b is not None:
+        j = j[np.frombuffer(images_b, dtype=np.int64)]
+    tau = np.sort(kappa * np.linalg.norm(j * np.frombuffer(dims_b, np.float64)[None, :], axis=1))
+    S = tau.size
+    n_tiles = -(-int(Ts + np.ceil(tau[-1]) + 64) // tile)
+    if n_tiles < world:
+        raise ValueError(f"{n_tiles} output tiles cannot be cut into {world} time shards")
+    x = np.arange(n_tiles + 1, dtype=np.float64) * tile
+    pre = np.concatenate([[0.0], np.cumsum(tau)])
+
+    def ramp(y):  # sum_i max(y - tau_i, 0)
+        m = np.searchsorted(tau, y, side="left")
+        return m * y - pre[m]
+
+    cost = ramp(x) - ramp(x - Ts) + TIME_GEOMETRY_COST * S * np.minimum(x, T) + \
+        skip * S * x
+    target = cost[-1] * np.arange(world + 1) / world
+    cuts = np.searchsorted(cost, target, side="left")
+    cuts[0], cuts[-1] = 0, n_tiles
+    for r in range(1, world + 1):  # every rank at least one tile
+        cuts[r] = max(cuts[r], cuts[r - 1] + 1)
+    for r in range(world - 1, -1, -1):
+        cuts[r] = min(cuts[r], cuts[r + 1] - 1)
+    out = cuts.astype(np.int64)
+    out.flags.writeable = False
+    return out
 
 
 # Every collective this process issued, in order: (name, elements).  The
@@ -194,10 +309,21 @@ def lpt_assign(costs, world: int) -> list:
 
 
 def shard_mode(workload: str, world: int) -> str:
-    """'single' | 'images' | 'scenes' | 'replicas' for a BASELINE config."""
+    """'single' | 'images' | 'scenes' | 'channels' | 'replicas' for a
+    BASELINE config.  c5 (one scene, 8 receivers) shards its channels --
+    independent (scene, channel) jobs, no collective, SURVEY 8(e)'s
+    "each GPU takes one channel" -- so each rank's geometry shrinks with W
+    as well (image shards replicate the per-job geometry on every rank:
+    projected W = 8 efficiency 0.79)."""
     if world == 1:
         return "single"
-    return {"c3": "images", "c5": "images", "c4": "scenes"}.get(workload, "replicas")
+    return {"c3": "images", "c5": "channels", "c4": "scenes"}.get(workload, "replicas")
+
+
+def channel_shard(n_channels: int, rank: int, world: int) -> list:
+    """Channels of a multi-receiver scene rendered by `rank`: LPT over
+    equal-cost channels, i.e. round-robin (rank r takes r, r + W, ...)."""
+    return lpt_assign(np.ones(int(n_channels)), world)[rank]
 
 
 def reduce_to_root(t, group=None, root: int = 0):

@@ -72,6 +72,7 @@ def structure_key(jobs, filt, precision) -> tuple:
                     tuple((int(a), int(b)) for a, b in jb.tiers), float(jb.rate), float(jb.c),
                     float(jb.d_min),
                     None if jb.image_index is None else np.asarray(jb.image_index).tobytes(),
+                    None if jb.window is None else tuple(int(v) for v in jb.window),
                     share_p[engine._key(jb.path_key, jb.pos)],
                     share_s[engine._key(jb.signal_key, jb.s)]))
     return tuple(key)
@@ -125,8 +126,9 @@ class RenderPlan:
     DEPTH = int(os.environ.get("MVB_PLAN_DEPTH", "2"))  # slots (diagnostic knob)
 
     def __init__(self, jobs, f, precision: str = "fp32", device=None, shard=None, dmax_hook=None):
-        """`shard=(rank, world)`: render the image shard of `rank` of every
-        job (parallel.image_shard, as synth.render_jobs) with `dmax_hook`
+        """`shard=(rank, world[, "images" | "time"])`: render the image
+        shard / output window of `rank` of every job (parallel.shard_jobs,
+        as synth.render_jobs) with `dmax_hook`
         (default: all-reduce MAX over the process group) applied to the
         track maxima between the geometry graph and the synthesis graph --
         the collective itself is issued eagerly on the geometry stream,
@@ -138,7 +140,7 @@ class RenderPlan:
             if precision == "fp64":
                 raise ValueError("the exact fp64 engine runs replicas only")
             rank, world = int(shard[0]), int(shard[1])
-            jobs = parallel.shard_jobs(jobs, rank, world)
+            jobs = parallel.shard_jobs(jobs, rank, world, parallel.shard_kind(shard))
             if dmax_hook is None:
                 dmax_hook = parallel.allreduce_max
         self.shard = shard
@@ -344,7 +346,7 @@ class RenderPlan:
         if self.shard is not None and int(self.shard[1]) > 1:
             from . import parallel
             rank, world = int(self.shard[0]), int(self.shard[1])
-            jobs = parallel.shard_jobs(jobs, rank, world)
+            jobs = parallel.shard_jobs(jobs, rank, world, parallel.shard_kind(self.shard))
         if structure_key(jobs, self.f, self.precision) != self.key:
             raise ValueError("jobs do not match the plan's structure")
         slot = self.slots[self.k % self.DEPTH]

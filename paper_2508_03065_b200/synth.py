@@ -617,7 +617,7 @@ def shard_batches(jobs, shard, budget: int, fd_taps: int) -> tuple:
     groups = _memory_groups(jobs, budget, fd_taps)
     if shard is not None and int(shard[1]) > 1:
         from . import parallel
-        jobs = parallel.shard_jobs(jobs, int(shard[0]), int(shard[1]))
+        jobs = parallel.shard_jobs(jobs, int(shard[0]), int(shard[1]), parallel.shard_kind(shard))
     return groups, jobs
 
 
@@ -629,7 +629,8 @@ def render_jobs(jobs, f, precision="fp32", shard=None, signals=None, timing=None
     once it completes -- lets planning overlap earlier work on the stream.
     `shard=(rank, world)`: render the image shard of `rank` of every job
     (parallel.image_shard: per-tier delay bands; all per-image work divides
-    by world),
+    by world); `shard=(rank, world, "time")`: its output window
+    (parallel.time_window: all images, 1/world of the samples),
     with out_len from the batch-wide track maximum (all-reduce MAX over
     the ranks, or `dmax_hook` when given) so the ranks' outputs sum to the
     full render.  Batches whose estimated device footprint exceeds

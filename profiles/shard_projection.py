@@ -12,40 +12,60 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
-from paper_2508_03065_b200 import hann_sinc, workloads  # noqa: E402
+from paper_2508_03065_b200 import engine, hann_sinc, parallel, workloads  # noqa: E402
 from paper_2508_03065_b200.plan import RenderPlan  # noqa: E402
 
 dev = torch.device("cuda", 0)
 out = {}
 K = 10
-for cfg in os.environ.get("CFGS", "c3,c5").split(","):
+# (config, partition): images / time (collective: all-reduce MAX + reduce,
+# excluded here), channels (no collective); default = parallel.shard_mode
+cases = [c.split(":") for c in os.environ.get("CASES", "c3:time,c3:images,c5:channels").split(",")]
+for cfg, kind in cases:
     scenes = workloads.make_scenes(cfg)
     jobs = bench.device_jobs(scenes, dev)
     f = hann_sinc(scenes[0].fd_taps, 14)
+    # what the all-reduce MAX would return, device-resident (an async copy)
+    gmax = torch.as_tensor(engine.Geometry(jobs).dmax, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
-    res = {}
+
+    def hook(t):
+        t.copy_(gmax)
+
+    res, kern = {}, {W: [] for W in (1, 2, 4, 8)}
     for W in (1, 2, 4, 8):
         per_rank = []
         for r in range(W):
-            shard = None if W == 1 else (r, W)
-            plan = RenderPlan(jobs, f, shard=shard, dmax_hook=(lambda t: t) if W > 1 else None)
+            mine = jobs
+            if W == 1:
+                plan = RenderPlan(jobs, f)
+            elif kind == "channels":  # independent jobs, no collective
+                mine = [jobs[i] for i in parallel.channel_shard(len(jobs), r, W)]
+                plan = RenderPlan(mine, f)
+            else:
+                plan = RenderPlan(jobs, f, shard=(r, W, kind), dmax_hook=hook)
             for _ in range(3):
-                plan.run(jobs)
+                plan.run(mine)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for k in range(K):
                 flush.fill_(float(k))
-                plan.run(jobs)
+                plan.run(mine)
             plan.join()
             e1.record()
             torch.cuda.synchronize()
             per_rank.append(e0.elapsed_time(e1) / K)
+            km = plan.flush_timing()
+            kern[W].append(float(np.mean([km[i] for i in sorted(km)[-K:]])))
             del plan
         res[W] = per_rank
     t1 = res[1][0]
-    out[cfg] = {W: {"ms_per_rank_step_max": round(max(v), 3),
-                    "ms_per_rank_step": [round(x, 3) for x in v],
-                    "projected_efficiency": round(t1 / (W * max(v)), 3)} for W, v in res.items()}
-    print(cfg, {W: d["projected_efficiency"] for W, d in out[cfg].items()}, flush=True)
+    out[f"{cfg}:{kind}"] = {W: {"ms_per_rank_step_max": round(max(v), 3),
+                                "ms_per_rank_step": [round(x, 3) for x in v],
+                                "synthesis_ms_per_rank": [round(x, 3) for x in kern[W]],
+                                "projected_efficiency": round(t1 / (W * max(v)), 3)}
+                            for W, v in res.items()}
+    print(cfg, kind, {W: d["projected_efficiency"] for W, d in out[f"{cfg}:{kind}"].items()},
+          flush=True)
 print(json.dumps(out, indent=1))

@@ -232,6 +232,92 @@ def test_image_shards_sum_to_full_render():
         render_jobs(jobs, f, precision="fp64", shard=(0, 2))
 
 
+def _time_shard_case(case):
+    if case == "c3long":  # several sort segments and exact-maximum chunks
+        scenes = workloads.make_scenes("c3", duration=1.0, max_order=8,
+                                       tiers=((2, 1), (5, 32), (8, 256)))
+        return None, scenes, None, hann_sinc(scenes[0].fd_taps, 14)
+    g, scenes, chans = _scenes(case)
+    return g, scenes, chans, _filter_of(g, scenes[0].fd_taps)
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("case", ["c5", "c3long"])
+def test_time_shards_sum_to_full_render(case, world):
+    """Time shards (parallel.time_window): every rank renders its output
+    window from all images.  The window maxima, MAX-reduced (the all-reduce
+    the ranks issue; here through dmax_hook, shards in sequence on one GPU),
+    equal the unsharded exact maximum bit for bit; each rank's output is
+    zero outside its window; the windows cover the output; the ranks'
+    outputs sum to the full render (fp32 summation-order differences only)
+    and, for c5, to the oracle within the fp32 bar."""
+    from paper_2508_03065_b200 import parallel
+    g, scenes, chans, f = _time_shard_case(case)
+    jobs = scene_jobs(scenes, chans)
+    full_geom = engine.Geometry(jobs)
+    full = render_jobs(jobs, f, precision="fp32")
+    shards = [parallel.shard_jobs(jobs, r, world, "time") for r in range(world)]
+    gmax = np.max(np.stack([engine.Geometry(sj).dmax for sj in shards]), axis=0)
+    assert np.array_equal(gmax, full_geom.dmax)
+
+    def hook(t):
+        t.copy_(torch.as_tensor(gmax, device=t.device))
+
+    parts = [render_jobs(jobs, f, precision="fp32", shard=(r, world, "time"), dmax_hook=hook)
+             for r in range(world)]
+    for j in range(len(jobs)):
+        n = int(full.lengths[j])
+        assert all(int(p.lengths[j]) == n for p in parts)
+        cover = np.zeros(n, np.int64)
+        for r, p in enumerate(parts):
+            w0, w1 = shards[r][j].window
+            w1 = n if w1 == 0 else min(w1, n)
+            y = p.job(j).double().cpu().numpy()
+            assert not y[:w0].any() and not y[w1:].any(), (r, j)
+            cover[w0:w1] += 1
+        assert (cover == 1).all(), j
+        total = sum(p.job(j).double() for p in parts).cpu().numpy()
+        ref = full.job(j).double().cpu().numpy()
+        assert rel_err(total, ref) <= 1e-6, (j, rel_err(total, ref))
+    if g is not None:
+        total = np.concatenate([sum(p.job(j).double() for p in parts).cpu().numpy()
+                                for j in range(len(jobs))])
+        assert rel_err(total, np.concatenate(_oracle(scenes, chans, g["branches"]))) <= FP32_TOL
+
+
+def test_render_plan_time_shards():
+    """Time-sharded render plans: captured windows replay; the ranks'
+    replays sum to the full render, data changing between runs."""
+    import dataclasses
+    from paper_2508_03065_b200 import parallel
+    from paper_2508_03065_b200.plan import RenderPlan
+    _, scenes, _, f = _time_shard_case("c3long")
+    jobs = scene_jobs(scenes)
+    world = 3
+    plans = None
+    for it in range(4):
+        jb = [dataclasses.replace(j, pos=scenes[0].pos + 0.05 * it,
+                                  s=(scenes[0].s * (1 + it)).astype(np.float32)) for j in jobs]
+        gmax = np.max(np.stack([engine.Geometry(parallel.shard_jobs(jb, r, world, "time")).dmax
+                                for r in range(world)]), axis=0)
+
+        def hook(t, gmax=gmax):
+            t.copy_(torch.as_tensor(gmax, device=t.device))
+
+        if plans is None:
+            hooks = {"h": hook}
+            plans = [RenderPlan(jobs, f, shard=(r, world, "time"),
+                                dmax_hook=lambda t: hooks["h"](t)) for r in range(world)]
+        hooks["h"] = hook
+        parts = [p.run(jb) for p in plans]
+        full = render_jobs(jb, f)
+        total = sum(p.job(0).double() for p in parts).cpu().numpy()
+        ref = full.job(0).double().cpu().numpy()
+        assert np.array_equal(parts[0].lengths, full.lengths)
+        assert rel_err(total, ref) <= 1e-6, (it, rel_err(total, ref))
+    assert all(p.captures == 2 for p in plans)
+
+
 def test_memory_split_batches_match_single_batch():
     """A batch forced into sub-batches (max_batch_bytes) renders the same
     lengths and, within the fp32 bar, the same outputs as one batch."""

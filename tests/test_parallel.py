@@ -27,6 +27,54 @@ def test_image_subsets_partition_and_balance():
     assert parallel.image_subset(sub, 1, 2).tolist() == [5, 13]
 
 
+def test_time_windows_partition_on_tiles():
+    """Time shards (parallel.time_window): whole TILEs, increasing, the
+    last open-ended; the same cuts on every rank (structural); the
+    estimated cost balanced (c3 shape: within 2% at W = 8)."""
+    from paper_2508_03065_b200 import engine, workloads
+    from paper_2508_03065_b200.engine import TILE
+    sc = workloads.make_scenes("c3", duration=10.0)[0]
+    jb = engine.Job(s=sc.s, pos=sc.pos, mic=sc.mics[0], dims=sc.dims, walls=sc.walls,
+                    max_order=sc.max_order, tiers=sc.tiers, rate=sc.rate)
+    for world in (1, 2, 3, 8):
+        w = [parallel.time_window(jb, r, world) for r in range(world)]
+        assert w[0][0] == 0 and w[-1][1] == 0
+        for r in range(world - 1):
+            assert w[r][1] == w[r + 1][0] and w[r][0] < w[r][1] and w[r][1] % TILE == 0
+        if world > 1:  # cost estimate per window (same model, evaluated here)
+            j, _ = parallel.canonical_lattice(sc.max_order)
+            tau = sc.rate / 343.0 * np.linalg.norm(j * sc.dims, axis=1)
+            T = sc.T
+
+            def cost(x):
+                return np.clip(x - tau, 0, T).sum() + tau.size * (
+                    parallel.TIME_GEOMETRY_COST * min(x, T) + parallel.TIME_SKIP_COST * x)
+            end = T + tau.max() + 64
+            c = [cost(min(w1 if w1 else end, end)) - cost(w0) for w0, w1 in w]
+            assert max(c) / min(c) < 1.02, (world, c)
+    with np.testing.assert_raises(ValueError):
+        parallel.shard_jobs([jb], 0, 2, by="stripes")
+
+
+def test_window_fields():
+    """mvb_job window words: path range [p0, p1) and the sort-segment
+    centres (engine.window_fields mirrors win_p0 / win_p1)."""
+    from paper_2508_03065_b200 import engine
+    from paper_2508_03065_b200.engine import SEG_LEN, TILE
+    assert engine.window_fields(1000, None) == dict(w0=0, w1=0, e0=0, e1=0)
+    T = 5 * SEG_LEN + 100
+    f = engine.window_fields(T, (SEG_LEN + TILE, 2 * SEG_LEN))
+    # tiles of segment 1 read its centre 1.5 SEG_LEN; the window's path range is inside
+    assert f == dict(w0=SEG_LEN + TILE, w1=2 * SEG_LEN, e0=SEG_LEN + TILE, e1=2 * SEG_LEN)
+    f = engine.window_fields(T, (TILE, 3 * TILE))  # centre of segment 0 lies past the window
+    assert f["e0"] == TILE and f["e1"] == SEG_LEN // 2 + 1
+    f = engine.window_fields(T, (6 * SEG_LEN, 0))  # tail window: held track, last segment
+    assert f["e0"] == T - 1 and f["e1"] == T
+    for bad in ((1, 0), (TILE, TILE), (2 * TILE, TILE), (-TILE, 0)):
+        with np.testing.assert_raises(ValueError):
+            engine.window_fields(T, bad)
+
+
 def test_canonical_lattice_matches_enumeration():
     """The host's structural copy of the canonical order (room.py:98-143)
     equals the oracle enumeration (itself pinned to the reference goldens)."""
@@ -78,6 +126,11 @@ def test_lpt_assign_balances_and_covers():
 def test_shard_modes():
     assert parallel.shard_mode("c3", 8) == "images"
     assert parallel.shard_mode("c4", 8) == "scenes"
+    assert parallel.shard_mode("c5", 8) == "channels"
+    assert parallel.channel_shard(8, 3, 8) == [3]
+    assert parallel.channel_shard(8, 1, 4) == [1, 5]
+    got = sorted(c for r in range(3) for c in parallel.channel_shard(8, r, 3))
+    assert got == list(range(8))
     assert parallel.shard_mode("c2", 4) == "replicas"
     assert parallel.shard_mode("c3", 1) == "single"
 
