@@ -388,6 +388,30 @@ int mvb_synthesize_f32(const mvb_job* d_jobs, const mvb_work* d_work, int64_t n_
                        const float* d_rec, const double* d_paths, float* d_out,
                        float* d_part, int nb, int u_steps, void* stream);
 
+/* mvb_delay_sort / mvb_delay_sort_runs (run_len <= 0: one run per job,
+ * max_n_img <= MVB_DELAY_SORT_MAX) that also writes the sorted keys:
+ * d_keys[(j * max_n_seg + s) * max_n_img + q] = the key (whole samples of
+ * delay at the segment centre) of the image in slot q, ascending within each
+ * run (padding slots: all ones).  The input of mvb_synthesize_f32_ranged. */
+int mvb_delay_sort_keyed(const mvb_image* d_images, const mvb_job* d_jobs, int64_t n_jobs,
+                         int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
+                         const double* d_paths, const double* d_coarse, int64_t key_bits,
+                         int64_t run_len, mvb_image* d_out, uint32_t* d_keys, void* stream);
+
+/* mvb_synthesize_f32 over a keyed sorted table (mvb_delay_sort_keyed with
+ * the same run_len -- a job's whole table: run_len >= its image count -- and
+ * seg_len): each work item's warps visit only the images whose key admits a
+ * gather row inside the signal over the tile, bounded with the path steps
+ * of d_bbox (mvb_path_bbox) and max_factor (largest decimation factor of the
+ * batch); the others would read only zero pads.  Same output as
+ * mvb_synthesize_f32 (the skipped images add exact zeros). */
+int mvb_synthesize_f32_ranged(const mvb_job* d_jobs, const mvb_work* d_work, int64_t n_work,
+                              const mvb_image* d_images, const uint32_t* d_keys, int64_t run_len,
+                              int64_t seg_len, int max_factor, const double* d_bbox,
+                              const mvb_coef32* d_coef, const float* d_rec,
+                              const double* d_paths, float* d_out, float* d_part, int nb,
+                              int u_steps, void* stream);
+
 /* Fixed-order sum of the n_chunks partial rows of every job. */
 int mvb_reduce_partials_f32(const mvb_job* d_jobs, int64_t n_jobs, int64_t max_out_len,
                             const float* d_part, float* d_out, void* stream);

@@ -358,17 +358,129 @@ __device__ __forceinline__ void stage_image(WarpStage<U>& st, int slot, const mv
                    reinterpret_cast<const char*>(src) + 16 * lane);
 }
 
+// Active image range of a tile.  The delay sort's keys (k_delay_sort:
+// floor(kappa * d) at the sort segment's centre, ascending within each run
+// of the job's table) bound every image's delay over the tile: |tau(n) -
+// tau(t_key)| <= E = 2 * kappa * (largest source step + largest receiver
+// step) * (|n - t_key| + max factor) + 8 samples (the factor covers the
+// decimated key's coarse sample, the 2 any overshoot of the band-limited
+// track or a low-passed path over the full-rate steps).  An image whose key
+// lies outside (klo, khi] reads only the zero pads of the branch records
+// over the whole tile -- it has not arrived yet or its signal has ended --
+// so the warps never visit it (the in-loop tests below would skip it too,
+// after paying for its staging).  The sorted table's images with keys in
+// (klo, khi] are a contiguous range of each run, found by a warp-parallel
+// 32-ary search (2-3 dependent loads).
+struct RangeArgs {
+    const unsigned* keys;  // parallel to the sorted image table; null: no narrowing
+    const double* bbox;    // mvb_path_bbox records (16 words per job)
+    int run_len;           // sorted run length of the table (a job's whole table: >= n_img)
+    int seg_len;           // sort segment length (samples)
+    int max_factor;        // largest decimation factor of the batch
+};
+
+// first positions in [b, e) whose key exceeds x0 / x1 (sorted keys), both
+// searches in the same rounds; has0 / has1 false: the search is skipped
+// (the position is b, resp. e).  Per round the lanes probe 32 increasing
+// positions, the last lane the range's end, so a range wholly above or
+// below x settles in one round (a tile in the middle of the signal).
+__device__ __forceinline__ void bound_round(const unsigned* __restrict__ k, int& lo, int& len,
+                                            unsigned x, int lane) {
+    if (len <= 0) return;
+    const int s = (len + 30) / 31;
+    int q = lane == 31 ? lo + len - 1 : lo + lane * s;
+    const bool valid = q < lo + len;
+    const bool t = valid && __ldg(k + q) <= x;
+    const int last_true = __reduce_max_sync(0xffffffffu, t ? q : lo - 1);
+    const int first_false = __reduce_min_sync(0xffffffffu, valid && !t ? q : lo + len);
+    lo = last_true + 1;
+    len = first_false - lo;
+}
+
+__device__ __forceinline__ void upper_bounds(const unsigned* __restrict__ k, int b, int e,
+                                             bool has0, unsigned x0, bool has1, unsigned x1,
+                                             int lane, int& p0, int& p1) {
+    int lo0 = b, len0 = has0 ? e - b : 0, lo1 = has1 ? b : e, len1 = has1 ? e - b : 0;
+    while (len0 > 0 || len1 > 0) {  // warp-uniform
+        bound_round(k, lo0, len0, x0, lane);
+        bound_round(k, lo1, len1, x1, lane);
+    }
+    p0 = lo0;
+    p1 = lo1;
+}
+
+// Warp w's image sequence over a tile: the positions p == b + w (mod 8) of
+// the chunk [b, e) that lie in the active parts [a0, a1) and [c0, c1) --
+// the same warp and order every image has without narrowing, so the warps'
+// sums (and the output) are bit-identical: the skipped images add exact
+// zeros.  k-th position: k < nA ? fA + 8k : fC + 8(k - nA); n in all.
+struct ActiveRange {
+    int fA, nA, fC, n;
+    __device__ __forceinline__ int operator[](int k) const {
+        return k < nA ? fA + SYNTH_WARPS * k : fC + SYNTH_WARPS * (k - nA);
+    }
+};
+
+// first position >= a congruent to r (mod 8), and the count of such in [a, z)
+__device__ __forceinline__ void congruent(int a, int z, int r, int& f, int& cnt) {
+    f = a + ((r - a) & (SYNTH_WARPS - 1));
+    cnt = z > f ? (z - f + SYNTH_WARPS - 1) / SYNTH_WARPS : 0;
+}
+
+template <int TN>
+__device__ __forceinline__ ActiveRange active_range(const RangeArgs& ra, const mvb_job& J,
+                                                    const mvb_work& w, int n0, int warp,
+                                                    int lane) {
+    const int b = w.img_begin, e = w.img_end;
+    ActiveRange r;
+    congruent(b, e, b + warp, r.fA, r.nA);
+    r.fC = e;
+    r.n = r.nA;
+    if (ra.keys == nullptr || e <= b) return r;
+    const double* box = ra.bbox + 16 * (int64_t)w.job;
+    const double rate = 2.0 * J.kappa * (box[12] + box[13]);
+    int64_t tk = (int64_t)w.seg * ra.seg_len + ra.seg_len / 2;
+    if (tk > J.T - 1) tk = J.T - 1;
+    const int64_t na = n0 < J.T - 1 ? n0 : J.T - 1;
+    const int64_t nb = n0 + TN - 1 < J.T - 1 ? n0 + TN - 1 : J.T - 1;
+    const int64_t dist = max(llabs(na - tk), llabs(nb - tk)) + ra.max_factor;
+    const double E = rate * (double)dist + 8.0;
+    const double lo = (double)n0 + J.d0 - (double)J.ls - E - 3.0;
+    const double hi = (double)n0 + TN + J.d0 + E + 2.0;
+    const bool has0 = lo >= 0.0, has1 = hi < 4294967295.0;
+    if (!has0 && !has1) return r;
+    const unsigned x0 = has0 ? (unsigned)lo : 0u, x1 = has1 ? (unsigned)hi : 0u;
+    const unsigned* k = ra.keys + J.img_off + (int64_t)w.seg * J.img_stride;
+    // the chunk's runs: at most two (chunks are no longer than a run)
+    const int rb = (b / ra.run_len + 1) * ra.run_len;
+    if (rb >= e) {
+        int p0, p1;
+        upper_bounds(k, b, e, has0, x0, has1, x1, lane, p0, p1);
+        congruent(p0, p1, b + warp, r.fA, r.nA);
+        r.n = r.nA;
+        return r;
+    }
+    if (rb + ra.run_len < e) return r;  // spans three runs: no narrowing
+    int p0, p1, q0, q1, nC;
+    upper_bounds(k, b, rb, has0, x0, has1, x1, lane, p0, p1);
+    upper_bounds(k, rb, e, has0, x0, has1, x1, lane, q0, q1);
+    congruent(p0, p1, b + warp, r.fA, r.nA);
+    congruent(q0, q1, b + warp, r.fC, nC);
+    r.n = r.nA + nC;
+    return r;
+}
+
 template <int U, int NP, int MINB, bool TAB = false>
 __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     const mvb_job* __restrict__ jobs, const mvb_work* __restrict__ work,
     const mvb_image* __restrict__ images, const mvb_coef32* __restrict__ coef,
     const float* __restrict__ rec, const double* __restrict__ paths, float* __restrict__ out,
-    float* __restrict__ part, const float* __restrict__ table = nullptr) {
+    float* __restrict__ part, const __grid_constant__ RangeArgs ra,
+    const float* __restrict__ table = nullptr) {
     constexpr int TN = 32 * U;
     __shared__ float red[SYNTH_WARPS][TN];
     __shared__ WarpStage<U> stage[SYNTH_WARPS];
     const mvb_work* wp = work + blockIdx.x;
-    const int img_begin = wp->img_begin, img_end = wp->img_end;
     const mvb_job* Jp = jobs + wp->job;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int n0 = wp->tile * TN;
@@ -391,8 +503,19 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     } else {
         g = FarrowGather<NP>{reinterpret_cast<const float4*>(rec), (unsigned)Jp->rec_rows};
     }
-    MVB_CHECK(wp->seg >= 0 && (Jp->img_stride == 0 || img_end <= Jp->img_stride) &&
-                  img_begin >= 0 && img_begin <= img_end, CHK_WORK);
+    MVB_CHECK(wp->seg >= 0 && (Jp->img_stride == 0 || wp->img_end <= Jp->img_stride) &&
+                  wp->img_begin >= 0 && wp->img_begin <= wp->img_end, CHK_WORK);
+    // the images this tile can read anything but zero pads from
+    // (kept in shared memory: the mapping is read once per image, and three
+    // more live registers across the image loop cost spills)
+    __shared__ ActiveRange ranges[SYNTH_WARPS];
+    {
+        const ActiveRange a = active_range<TN>(ra, *Jp, *wp, n0, warp, lane);
+        if (lane == 0) ranges[warp] = a;
+        __syncwarp();
+    }
+    const ActiveRange& ar = ranges[warp];
+    const int nv = ar.n;
     // this tile's delay-sorted image table (sort segment wp->seg)
     const mvb_image* __restrict__ imgs = images + Jp->img_off + (int64_t)wp->seg * Jp->img_stride;
     const float invk = (float)(1.0 / Jp->kappa);
@@ -419,26 +542,25 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
 
     // prologue of the staging pipeline: structs of the first two images, then
     // the first image's records
-    const int i0 = img_begin + warp;
-    if (i0 < img_end) stage_image(st, 0, imgs + i0, lane);
-    if (i0 + SYNTH_WARPS < img_end) stage_image(st, 1, imgs + i0 + SYNTH_WARPS, lane);
+    // k indexes the warp's image sequence ar[k]
+    if (0 < nv) stage_image(st, 0, imgs + ar[0], lane);
+    if (1 < nv) stage_image(st, 1, imgs + ar[1], lane);
     cp_async_commit();
     cp_async_wait_all();
     __syncwarp();
-    if (i0 < img_end) stage_records(st, 0, st.img[0], coef, n0, T, lane);
+    if (0 < nv) stage_records(st, 0, st.img[0], coef, n0, T, lane);
     cp_async_commit();
 
     // staging slots rotate: struct slots (cur, nx1, nx2), record slot rcur
     int cur = 0, nx1 = 1, nx2 = 2, rcur = 0, rot;
-    for (int i = i0; i < img_end;
-         i += SYNTH_WARPS, rot = cur, cur = nx1, nx1 = nx2, nx2 = rot, rcur ^= 1) {
-        // everything issued one image ago has landed: records(i), struct(i+8)
+    for (int i = 0; i < nv; ++i, rot = cur, cur = nx1, nx1 = nx2, nx2 = rot, rcur ^= 1) {
+        // everything issued one image ago has landed: records(i), struct(i+1)
         cp_async_wait_all();
         __syncwarp();
         // stream the next image's records and the struct after it while
         // this image is processed
-        if (i + SYNTH_WARPS < img_end) stage_records(st, rcur ^ 1, st.img[nx1], coef, n0, T, lane);
-        if (i + 2 * SYNTH_WARPS < img_end) stage_image(st, nx2, imgs + i + 2 * SYNTH_WARPS, lane);
+        if (i + 1 < nv) stage_records(st, rcur ^ 1, st.img[nx1], coef, n0, T, lane);
+        if (i + 2 < nv) stage_image(st, nx2, imgs + ar[i + 2], lane);
         cp_async_commit();
 
         const mvb_image& im = st.img[cur];
@@ -881,10 +1003,10 @@ int mvb_branch_records_f32(const float* x_all, const int64_t* sig_off, const int
     return check_launch("branch_records_f32");
 }
 
-int mvb_synthesize_f32(const mvb_job* jobs, const mvb_work* work, int64_t n_work,
-                       const mvb_image* images, const mvb_coef32* coef, const float* rec,
-                       const double* paths, float* out, float* part, int nb, int u_steps,
-                       void* stream) {
+static int synthesize_f32(const mvb_job* jobs, const mvb_work* work, int64_t n_work,
+                          const mvb_image* images, const mvb_coef32* coef, const float* rec,
+                          const double* paths, float* out, float* part, int nb, int u_steps,
+                          const RangeArgs& ra, void* stream) {
     if (n_work < 0 || n_work > 0x7fffffff) return fail(MVB_EINVAL, "synthesize_f32: n_work");
     if (n_work == 0) return MVB_OK;
     if (!jobs || !work || !images || !rec || !paths || !out)
@@ -896,7 +1018,7 @@ int mvb_synthesize_f32(const mvb_job* jobs, const mvb_work* work, int64_t n_work
     // U = 16: 512-sample tiles, 3 CTAs/SM
 #define MVB_SYNTH(U, NP, MB) prefer_carveout((const void*)k_synth_f32<U, NP, MB>, true); \
     k_synth_f32<U, NP, MB><<<g, block, 0, s>>>( \
-        jobs, work, images, coef, rec, paths, out, part)
+        jobs, work, images, coef, rec, paths, out, part, ra)
 #define MVB_SYNTH_NB(U, MB)                         \
     switch (nb) {                                   \
         case 4: MVB_SYNTH(U, 1, MB); break;         \
@@ -909,6 +1031,27 @@ int mvb_synthesize_f32(const mvb_job* jobs, const mvb_work* work, int64_t n_work
 #undef MVB_SYNTH_NB
 #undef MVB_SYNTH
     return check_launch("synthesize_f32");
+}
+
+int mvb_synthesize_f32(const mvb_job* jobs, const mvb_work* work, int64_t n_work,
+                       const mvb_image* images, const mvb_coef32* coef, const float* rec,
+                       const double* paths, float* out, float* part, int nb, int u_steps,
+                       void* stream) {
+    return synthesize_f32(jobs, work, n_work, images, coef, rec, paths, out, part, nb, u_steps,
+                          RangeArgs{nullptr, nullptr, 1, 1, 1}, stream);
+}
+
+int mvb_synthesize_f32_ranged(const mvb_job* jobs, const mvb_work* work, int64_t n_work,
+                              const mvb_image* images, const uint32_t* keys, int64_t run_len,
+                              int64_t seg_len, int max_factor, const double* bbox,
+                              const mvb_coef32* coef, const float* rec, const double* paths,
+                              float* out, float* part, int nb, int u_steps, void* stream) {
+    if (!keys || !bbox) return fail(MVB_EINVAL, "synthesize_f32_ranged: null keys / bbox");
+    if (run_len < 1 || run_len > 0x7fffffff || seg_len < 1 || seg_len > 0x7fffffff ||
+        max_factor < 1)
+        return fail(MVB_EINVAL, "synthesize_f32_ranged: run_len / seg_len / max_factor");
+    return synthesize_f32(jobs, work, n_work, images, coef, rec, paths, out, part, nb, u_steps,
+                          RangeArgs{keys, bbox, (int)run_len, (int)seg_len, max_factor}, stream);
 }
 
 int mvb_signal_plane_f32(const float* x_all, const int64_t* sig_off, const int64_t* sig_len,
@@ -940,7 +1083,7 @@ int mvb_synthesize_f32_table(const mvb_job* jobs, const mvb_work* work, int64_t 
         return check_launch("synthesize_f32_table (smem attribute)");
     prefer_carveout((const void*)k_synth_f32<16, 1, 1, true>);
     k_synth_f32<16, 1, 1, true><<<(unsigned)n_work, SYNTH_WARPS * 32, smem, as_stream(stream)>>>(
-        jobs, work, images, coef, xp, paths, out, part, table);
+        jobs, work, images, coef, xp, paths, out, part, RangeArgs{nullptr, nullptr, 1, 1, 1}, table);
     return check_launch("synthesize_f32_table");
 }
 

@@ -671,7 +671,8 @@ __global__ void __launch_bounds__(BT) k_delay_sort(const mvb_image* __restrict__
                                                    int64_t max_n_img, int64_t max_n_seg,
                                                    int64_t seg_len, const double* __restrict__ paths,
                                                    const double* __restrict__ coarse, int key_bits,
-                                                   int64_t run_len, mvb_image* __restrict__ out) {
+                                                   int64_t run_len, mvb_image* __restrict__ out,
+                                                   unsigned* __restrict__ keys_out) {
     using Sort = cub::BlockRadixSort<unsigned, BT, IPT, int>;
     extern __shared__ __align__(16) unsigned char dsort_smem[];
     auto& temp = *reinterpret_cast<typename Sort::TempStorage*>(dsort_smem);
@@ -714,11 +715,15 @@ __global__ void __launch_bounds__(BT) k_delay_sort(const mvb_image* __restrict__
     }
     Sort(temp).SortBlockedToStriped(keys, vals, 0, key_bits);
     mvb_image* __restrict__ dst = out + (j * max_n_seg + s) * max_n_img + base;
+    unsigned* __restrict__ kdst = keys_out ? keys_out + (j * max_n_seg + s) * max_n_img + base : nullptr;
     constexpr int CH = sizeof(mvb_image) / 16;
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
         const int q = k * BT + threadIdx.x;  // striped arrangement
         if (q < slots) {
+            // the sorted keys (ascending within the run; the synthesis
+            // narrows a tile's image range on them, k_synth_f32)
+            if (kdst) kdst[q] = keys[k];
             // padding slots (past the job's images) repeat an own image
             const int64_t src = n > 0 ? (vals[k] < n - 1 ? vals[k] : n - 1) : J.n_img - 1 - base;
             const float4* a = reinterpret_cast<const float4*>(im0 + src);
@@ -733,7 +738,7 @@ template <int BT, int IPT>
 static int launch_delay_sort(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
                              int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
                              const double* paths, const double* coarse, int key_bits,
-                             int64_t run_len, mvb_image* out, cudaStream_t s) {
+                             int64_t run_len, mvb_image* out, unsigned* keys, cudaStream_t s) {
     using Sort = cub::BlockRadixSort<unsigned, BT, IPT, int>;
     const size_t smem = sizeof(typename Sort::TempStorage);
     static bool attr = false;  // one opt-in per process and instantiation
@@ -746,7 +751,7 @@ static int launch_delay_sort(const mvb_image* images, const mvb_job* jobs, int64
     prefer_carveout((const void*)k_delay_sort<BT, IPT>);
     k_delay_sort<BT, IPT><<<dim3((unsigned)max_n_seg, (unsigned)n_jobs, (unsigned)runs), BT, smem,
                             s>>>(images, jobs, max_n_img, max_n_seg, seg_len, paths, coarse,
-                                 key_bits, run_len, out);
+                                 key_bits, run_len, out, keys);
     return MVB_OK;
 }
 
@@ -1204,7 +1209,7 @@ int mvb_track_coeffs_windowed(const mvb_image* images, const int32_t* sel, int64
 static int delay_sort_runs(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
                            int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
                            const double* paths, const double* coarse, int64_t key_bits,
-                           int64_t run_len, mvb_image* out, void* stream) {
+                           int64_t run_len, mvb_image* out, unsigned* keys, void* stream) {
     if (n_jobs < 0 || n_jobs > 65535 || max_n_img < 0 || max_n_seg < 0 ||
         max_n_seg > 0x7fffffff || seg_len < 1)
         return fail(MVB_EINVAL, "delay_sort: sizes");
@@ -1219,19 +1224,19 @@ static int delay_sort_runs(const mvb_image* images, const mvb_job* jobs, int64_t
     int rc;
     if (run_len <= 1024)
         rc = launch_delay_sort<256, 4>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
-                                       coarse, kb, run_len, out, s);
+                                       coarse, kb, run_len, out, keys, s);
     else if (run_len <= 2048)
         rc = launch_delay_sort<256, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
-                                       coarse, kb, run_len, out, s);
+                                       coarse, kb, run_len, out, keys, s);
     else if (run_len <= 4096)
         rc = launch_delay_sort<512, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths,
-                                       coarse, kb, run_len, out, s);
+                                       coarse, kb, run_len, out, keys, s);
     else if (run_len <= 8192)
         rc = launch_delay_sort<1024, 8>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len,
-                                        paths, coarse, kb, run_len, out, s);
+                                        paths, coarse, kb, run_len, out, keys, s);
     else
         rc = launch_delay_sort<1024, 16>(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len,
-                                         paths, coarse, kb, run_len, out, s);
+                                         paths, coarse, kb, run_len, out, keys, s);
     if (rc != MVB_OK) return rc;
     return check_launch("delay_sort");
 }
@@ -1241,7 +1246,7 @@ int mvb_delay_sort(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
                    const double* coarse, int64_t key_bits, mvb_image* out, void* stream) {
     if (max_n_img > MVB_DELAY_SORT_MAX) return fail(MVB_EINVAL, "delay_sort: too many images");
     return delay_sort_runs(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths, coarse,
-                           key_bits, max_n_img > 0 ? max_n_img : 1, out, stream);
+                           key_bits, max_n_img > 0 ? max_n_img : 1, out, nullptr, stream);
 }
 
 int mvb_delay_sort_runs(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
@@ -1249,7 +1254,20 @@ int mvb_delay_sort_runs(const mvb_image* images, const mvb_job* jobs, int64_t n_
                         const double* paths, const double* coarse, int64_t key_bits,
                         int64_t run_len, mvb_image* out, void* stream) {
     return delay_sort_runs(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths, coarse,
-                           key_bits, run_len, out, stream);
+                           key_bits, run_len, out, nullptr, stream);
+}
+
+int mvb_delay_sort_keyed(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs,
+                         int64_t max_n_img, int64_t max_n_seg, int64_t seg_len,
+                         const double* paths, const double* coarse, int64_t key_bits,
+                         int64_t run_len, mvb_image* out, uint32_t* keys, void* stream) {
+    if (!keys) return fail(MVB_EINVAL, "delay_sort_keyed: null keys");
+    if (run_len <= 0) {
+        if (max_n_img > MVB_DELAY_SORT_MAX) return fail(MVB_EINVAL, "delay_sort: too many images");
+        run_len = max_n_img > 0 ? max_n_img : 1;
+    }
+    return delay_sort_runs(images, jobs, n_jobs, max_n_img, max_n_seg, seg_len, paths, coarse,
+                           key_bits, run_len, out, keys, stream);
 }
 
 int mvb_sort_keys(const mvb_image* images, const mvb_job* jobs, int64_t n_jobs, int64_t max_n_img,

@@ -1078,7 +1078,7 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         for fs in fork:  # every branch stream joins the capture (unused ones too)
             fs.wait_event(forked)
         with torch.cuda.stream(fork[0]):
-            images_sorted, n_seg, max_seg, max_img = _delay_sort(geom, pre_dev,
+            images_sorted, n_seg, max_seg, max_img, keyed = _delay_sort(geom, pre_dev,
                                                                  stream_handle(dev))
         with torch.cuda.stream(fork[1]):
             rec, rec_start = _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev,
@@ -1089,7 +1089,7 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     else:
         coef = _interval_records(geom, pre_dev, st)
         _mark("render.coeffs_keys")
-        images_sorted, n_seg, max_seg, max_img = _delay_sort(geom, pre_dev, st)
+        images_sorted, n_seg, max_seg, max_img, keyed = _delay_sort(geom, pre_dev, st)
         _mark("render.sorted")
         rec, rec_start = _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev, st,
                                          concat)
@@ -1118,6 +1118,11 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
             _lib.call("mvb_synthesize_f32_table", ptr(jobs_dev), ptr(work_dev), len(work),
                       ptr(images_sorted), ptr(coef), ptr(rec), ptr(geom.paths), ptr(out),
                       ptr(part), ptr(table), L, st)
+        elif keyed is not None:
+            _lib.call("mvb_synthesize_f32_ranged", ptr(jobs_dev), ptr(work_dev), len(work),
+                      ptr(images_sorted), ptr(keyed[0]), keyed[1], SEG_LEN,
+                      max(geom.factors, default=1), ptr(geom.bbox), ptr(coef), ptr(rec),
+                      ptr(geom.paths), ptr(out), ptr(part), nb, SYNTH_U, st)
         else:
             _lib.call("mvb_synthesize_f32", ptr(jobs_dev), ptr(work_dev), len(work),
                       ptr(images_sorted), ptr(coef), ptr(rec), ptr(geom.paths), ptr(out),
@@ -1175,6 +1180,15 @@ def _delay_sort(geom, pre_dev, st):
         images_sorted = torch.empty(nJ * max_seg * max_img, IMG_COLS, dtype=torch.int64,
                                     device=dev)
         key_bits = max(1, min(32, max(int(geom.length_bound(j)) for j in range(nJ)).bit_length()))
+        run_len = SORT_RUN if windowed else max(max_img, 1)
+        if ACTIVE_RANGES:
+            # the sorted keys let each synthesis tile skip the images that
+            # read only zero pads there (mvb_synthesize_f32_ranged)
+            keys = torch.empty(nJ * max_seg * max_img, dtype=torch.int32, device=dev)
+            _lib.call("mvb_delay_sort_keyed", ptr(geom.images), ptr(pre_dev), nJ, max_img,
+                      max_seg, SEG_LEN, ptr(geom.paths), ptr(geom.coarse), key_bits, run_len,
+                      ptr(images_sorted), ptr(keys), st)
+            return images_sorted, n_seg, max_seg, max_img, (keys, run_len)
         if windowed:
             _lib.call("mvb_delay_sort_runs", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg,
                       SEG_LEN, ptr(geom.paths), ptr(geom.coarse), key_bits, SORT_RUN,
@@ -1182,7 +1196,7 @@ def _delay_sort(geom, pre_dev, st):
         else:
             _lib.call("mvb_delay_sort", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg,
                       SEG_LEN, ptr(geom.paths), ptr(geom.coarse), key_bits, ptr(images_sorted), st)
-        return images_sorted, n_seg, max_seg, max_img
+        return images_sorted, n_seg, max_seg, max_img, None
     key = torch.full((nJ, max_seg, max_img), float("inf"), dtype=torch.float64, device=dev)
     _lib.call("mvb_sort_keys", ptr(geom.images), ptr(pre_dev), nJ, max_img, max_seg, SEG_LEN,
               ptr(geom.paths), ptr(geom.coarse), ptr(key), st)
@@ -1192,7 +1206,7 @@ def _delay_sort(geom, pre_dev, st):
     gidx = (base + torch.minimum(order, nimg_dev - 1)).reshape(-1)
     images_sorted = torch.empty(gidx.numel(), IMG_COLS, dtype=torch.int64, device=dev)
     _lib.call("mvb_gather_images", ptr(geom.images), ptr(gidx), gidx.numel(), ptr(images_sorted), st)
-    return images_sorted, n_seg, max_seg, max_img
+    return images_sorted, n_seg, max_seg, max_img, None
 
 
 def _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev, st, concatenated=None):
@@ -1238,6 +1252,9 @@ TAB_P = 512  # mvb.h MVB_TAB_P
 # MVB_FD_GATHER=table: the fast synthesis gathers through the literal
 # per-fraction table instead of the Farrow records (measurement only)
 FD_GATHER = os.environ.get("MVB_FD_GATHER", "farrow")
+# per-tile active image ranges from the sorted keys (mvb_synthesize_f32_ranged);
+# MVB_ACTIVE_RANGES=0: every tile walks its whole chunk (A/B)
+ACTIVE_RANGES = os.environ.get("MVB_ACTIVE_RANGES", "1") != "0"
 
 
 def fraction_table(filt) -> np.ndarray:

@@ -476,3 +476,32 @@ def test_fraction_table_gather_ab_matches_oracle(monkeypatch):
                           f.branches, sc.rate).render()
     assert y.size == ref.size
     assert rel_err(y, ref) <= 1e-5
+
+
+@pytest.mark.parametrize("case", ["c2", "c3", "c4", "c5", "c3long"])
+def test_active_ranges_bit_identical(case, monkeypatch):
+    """Per-tile active image ranges (mvb_synthesize_f32_ranged, the default)
+    skip only images that read nothing but zero pads over a tile: the
+    output equals the walk over every image of the chunk bit for bit --
+    unsharded, and for time shards (sorted runs, windows) of c3long."""
+    if case == "c3long":
+        g, scenes, chans, f = _time_shard_case(case)
+        shards = [(r, 3, "time") for r in range(3)]
+    else:
+        g, scenes, chans = _scenes(case)
+        f = _filter_of(g, scenes[0].fd_taps)
+        shards = [None]
+    jobs = scene_jobs(scenes, chans)
+    for shard in shards:
+        kw = {}
+        if shard is not None:
+            from paper_2508_03065_b200 import parallel
+            gmax = np.max(np.stack([engine.Geometry(parallel.shard_jobs(jobs, r, 3, "time")).dmax
+                                    for r in range(3)]), axis=0)
+            kw = dict(shard=shard, dmax_hook=lambda t: t.copy_(torch.as_tensor(gmax, device=t.device)))
+        outs = []
+        for on in (False, True):
+            monkeypatch.setattr(engine, "ACTIVE_RANGES", on)
+            res = render_jobs(jobs, f, precision="fp32", **kw)
+            outs.append(torch.cat([res.job(j) for j in range(len(jobs))]))
+        assert torch.equal(outs[0], outs[1]), (case, shard)
