@@ -1008,9 +1008,11 @@ __global__ void k_build_images(const double* __restrict__ toff, const double* __
 template <int BLOCK, int KI, bool WIN>
 static int launch_coeffs(const SbpParam& sp, const mvb_image* images, const int32_t* sel,
                          int64_t n_sel, int64_t max_K, const mvb_job* jobs, const double* coarse,
-                         mvb_coef32* coef, void* stream) {
+                         mvb_coef32* coef, void* stream, int64_t n_int = 0) {
     using S = CoefShape<BLOCK, KI>;
-    int64_t spans = (max_K + S::SPAN - 1) / S::SPAN;
+    // spans per image: the whole track, or (windowed) the window's intervals
+    // (the kernel's span loop covers any remainder)
+    int64_t spans = ((n_int > 0 ? n_int : max_K) + S::SPAN - 1) / S::SPAN;
     if (spans > 65535) spans = 65535;
     static bool attr_set = false;
     if (!attr_set) {
@@ -1186,10 +1188,22 @@ static int track_coeffs(const mvb_image* images, const int32_t* sel, int64_t n_s
     // Time-shard windows (~250 intervals of a N = 256 image at W = 8) would
     // leave half of a 512-interval span idle: one warp x 8 there.
     if (windowed) {
-        if (max_K <= 768)
+        // a window's intervals (max_K less the 2 x 34 halo and the 64 of
+        // alignment, coarse_span) in the span that wastes the fewest thread
+        // slots: 128 (1 warp x 4), 256 (1 warp x 8) or 512 (2 warps x 8)
+        // intervals per CTA pass (ties: the larger span).  c3 at W = 8: the
+        // N = 256 tier's ~310 intervals run as 3 x 128, not 2 x 256
+        const int64_t n_int = max_K - 64 - 66 > 1 ? max_K - 64 - 66 : 1;
+        const int64_t w128 = (n_int + 127) / 128 * 128, w256 = (n_int + 255) / 256 * 256,
+                      w512 = (n_int + 511) / 512 * 512;
+        if (w512 <= w256 && w512 <= w128)
+            return launch_coeffs<64, 8, true>(sp, images, sel, n_sel, max_K, jobs, coarse, coef,
+                                              stream, n_int);
+        if (w256 <= w128)
             return launch_coeffs<32, 8, true>(sp, images, sel, n_sel, max_K, jobs, coarse, coef,
-                                              stream);
-        return launch_coeffs<64, 8, true>(sp, images, sel, n_sel, max_K, jobs, coarse, coef, stream);
+                                              stream, n_int);
+        return launch_coeffs<32, 4, true>(sp, images, sel, n_sel, max_K, jobs, coarse, coef,
+                                          stream, n_int);
     }
     return launch_coeffs<64, 8, false>(sp, images, sel, n_sel, max_K, jobs, coarse, coef, stream);
 }

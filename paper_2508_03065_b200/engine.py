@@ -615,7 +615,8 @@ class Geometry:
             full_cnt = sum(int(counts[q]) for q, N in enumerate(classes) if N == 1)
             plans.append(dict(key=(max_order, tiers, sub), max_order=max_order, members=members,
                               S=S, img_tab=img_tab, classes=classes, kbase=kbase, ct=ct,
-                              img_base=img_base, full_off=n_full, dec_off=n_dec))
+                              img_base=img_base, full_off=n_full, dec_off=n_dec,
+                              per_job=per_job, counts=counts))
             for g, j in enumerate(members):
                 self.img_off[j] = img_base + g * S
                 self.n_img[j] = S
@@ -677,6 +678,23 @@ class Geometry:
                       pl["dec_off"], ptr(class_sel), st)
         self.n_images = img_base
         self.n_coarse_total = coarse_base
+        # record groups (prepare_render, RECORD_BUDGET): a uniform batch --
+        # one structure group, jobs in order -- lays each job's coarse
+        # samples / interval records and its slice of every factor's
+        # selection out contiguously, so consecutive jobs can have their
+        # records computed into a shared buffer group by group
+        self.rec_layout = None
+        if len(plans) == 1 and plans[0]["members"] == list(range(nJ)):
+            pl = plans[0]
+            sel = {}  # factor N: (offset of job 0's slice in sel_by_factor[N], images per job)
+            dec = [int(N) for N in pl["classes"] if N > 1]
+            if len(dec) == len(set(dec)):  # one class per factor: one slice per job
+                for q, N in enumerate(pl["classes"]):
+                    if N > 1:
+                        sel[int(N)] = (int(pl["ct"].sel_off[q]) - cls_base[int(N)],
+                                       int(pl["counts"][q]))
+                self.rec_layout = dict(kbase=np.asarray(pl["kbase"], np.int64),
+                                       per_job=np.asarray(pl["per_job"], np.int64), sel=sel)
         self.sel_by_factor = {N: class_sel[cls_base[N]:cls_base[N] + n_cls[N]] for N in factors
                               if n_cls[N]}
         if self.full_sel.numel() > 65535:
@@ -1071,6 +1089,17 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     pre_dev = h2d(pack_jobs(base_rows), dev)
     out_len, tau_bound, offsets, rows = finish_rows()
     concat = sig_all if host_sigs and len(host_sigs) == len(uniq) else None
+    # record groups: batches whose interval records exceed RECORD_BUDGET get
+    # them computed group by group into two alternating buffers, inside the
+    # synthesis launch (launch32), instead of all up front
+    groups = _record_groups(geom) if FD_GATHER != "table" else None
+    rec_bufs = None
+    if groups:
+        lay = geom.rec_layout
+        most = max(int(lay["kbase"][b - 1] + lay["per_job"][b - 1] - lay["kbase"][a])
+                   for a, b in groups)
+        rec_bufs = [torch.empty(most * 12, dtype=torch.float32, device=dev)
+                    for _ in range(min(2, len(groups)))]
     main = torch.cuda.current_stream(dev)
     if fork is not None:
         forked = torch.cuda.Event()
@@ -1083,11 +1112,11 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         with torch.cuda.stream(fork[1]):
             rec, rec_start = _branch_records(uniq, sig_dev, sig_len, tau_bound, L, cb, M1, nb, dev,
                                              stream_handle(dev), concat)
-        coef = _interval_records(geom, pre_dev, st, fork=fork[2:])
+        coef = None if groups else _interval_records(geom, pre_dev, st, fork=fork[2:])
         for fs in fork:
             main.wait_stream(fs)
     else:
-        coef = _interval_records(geom, pre_dev, st)
+        coef = None if groups else _interval_records(geom, pre_dev, st)
         _mark("render.coeffs_keys")
         images_sorted, n_seg, max_seg, max_img, keyed = _delay_sort(geom, pre_dev, st)
         _mark("render.sorted")
@@ -1103,12 +1132,26 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         rows[j].update(rec_base=rec_start[keys[j]], nb=nb, img_off=j * max_seg * max_img,
                        img_stride=max_img, rec_rows=rec_rows)
     work, part_rows = _work_list(geom.n_img, out_len, n_seg, sm_count, rows)
+    work_at = np.searchsorted(work[:, 0], np.arange(nJ + 1), side="left")  # job j: [at[j], at[j+1])
     _mark("render.records_plan")
     jobs_dev = h2d(pack_jobs(rows), dev)
     work_dev = h2d(work, dev)
     out = torch.zeros(int(out_len.sum()), dtype=torch.float32, device=dev)
     part = torch.empty(max(part_rows, 1), dtype=torch.float32, device=dev)
     _mark("render.work_upload")
+
+    def synth(w0, w1, coef_p, st):
+        # work items [w0, w1) with the interval records at coef_p
+        wp = work_dev.data_ptr() + 32 * int(w0)
+        if keyed is not None:
+            _lib.call("mvb_synthesize_f32_ranged", ptr(jobs_dev), wp, int(w1 - w0),
+                      ptr(images_sorted), ptr(keyed[0]), keyed[1], SEG_LEN,
+                      max(geom.factors, default=1), ptr(geom.bbox), coef_p, ptr(rec),
+                      ptr(geom.paths), ptr(out), ptr(part), nb, SYNTH_U, st)
+        else:
+            _lib.call("mvb_synthesize_f32", ptr(jobs_dev), wp, int(w1 - w0),
+                      ptr(images_sorted), coef_p, ptr(rec), ptr(geom.paths), ptr(out),
+                      ptr(part), nb, SYNTH_U, st)
 
     def launch32(timing):
         st = stream_handle(dev)
@@ -1118,15 +1161,11 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
             _lib.call("mvb_synthesize_f32_table", ptr(jobs_dev), ptr(work_dev), len(work),
                       ptr(images_sorted), ptr(coef), ptr(rec), ptr(geom.paths), ptr(out),
                       ptr(part), ptr(table), L, st)
-        elif keyed is not None:
-            _lib.call("mvb_synthesize_f32_ranged", ptr(jobs_dev), ptr(work_dev), len(work),
-                      ptr(images_sorted), ptr(keyed[0]), keyed[1], SEG_LEN,
-                      max(geom.factors, default=1), ptr(geom.bbox), ptr(coef), ptr(rec),
-                      ptr(geom.paths), ptr(out), ptr(part), nb, SYNTH_U, st)
+        elif groups:
+            _grouped_synthesis(geom, pre_dev, groups, rec_bufs, work_dev, work_at,
+                               lambda w0, w1, coef_p, s: synth(w0, w1, coef_p, s))
         else:
-            _lib.call("mvb_synthesize_f32", ptr(jobs_dev), ptr(work_dev), len(work),
-                      ptr(images_sorted), ptr(coef), ptr(rec), ptr(geom.paths), ptr(out),
-                      ptr(part), nb, SYNTH_U, st)
+            synth(0, len(work), coef.data_ptr(), st)
         _events_end(timing, ev)
         if part_rows:
             _lib.call("mvb_reduce_partials_f32", ptr(jobs_dev), nJ, int(out_len.max()),
@@ -1134,6 +1173,102 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
         _mark("render.synth_launched")
         return RenderResult(out, offsets, out_len, geom.n_img.astype(np.int64), 0, lengths, err)
     return PreparedRender(launch32, launches0)
+
+
+# Interval-record budget of one render (bytes).  Grouping bounds the
+# footprint but costs time: c4 (32 GB of records) with 2 GB groups ran 99 ms
+# per step against 90.5 ungrouped (a group's records and the previous
+# group's synthesis share the SMs under different shared-memory carveouts;
+# a high-priority records stream: 121 ms).  So the default only groups what
+# would not fit comfortably: a quarter of the device memory (45 GB on a
+# B200); MVB_RECORD_BUDGET_GB sets it (2: c4's plan slot holds 4 GB of
+# records instead of 32).
+RECORD_BUDGET = float(os.environ["MVB_RECORD_BUDGET_GB"]) * 2 ** 30 \
+    if os.environ.get("MVB_RECORD_BUDGET_GB") else None
+
+
+def _record_budget(dev) -> float:
+    if RECORD_BUDGET is not None:
+        return RECORD_BUDGET
+    return 0.25 * torch.cuda.get_device_properties(dev).total_memory
+
+
+def _record_groups(geom):
+    """Consecutive job ranges [j0, j1) whose interval records (48 B per
+    coarse interval) fit RECORD_BUDGET each, cut at equal record counts; None
+    when the whole batch fits (or its layout is not uniform:
+    Geometry.rec_layout).  With a 2 GB budget c4's 32 GB of records run
+    as 16 groups in two alternating 2 GB buffers."""
+    lay = geom.rec_layout
+    total = 48 * int(geom.n_coarse_total)
+    nJ = len(geom.jobs)
+    budget = _record_budget(geom.dev)
+    if lay is None or total <= budget or nJ < 2:
+        return None
+    n = min(nJ, -(-total // int(budget)))
+    cum = np.concatenate([[0], np.cumsum(lay["per_job"])])
+    cuts = np.searchsorted(cum, cum[-1] * np.arange(n + 1) / n, side="left")
+    cuts[0], cuts[-1] = 0, nJ
+    cuts = np.unique(np.clip(cuts, 0, nJ))
+    return [(int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+
+
+def _group_streams(dev):
+    key = ("groups", str(dev))
+    if key not in _GROUP_STREAMS:
+        # equal priorities (a high-priority records stream measured 121 ms
+        # per c4 step against 99: MVB_GROUP_REC_PRIORITY=-1)
+        _GROUP_STREAMS[key] = (torch.cuda.Stream(device=dev, priority=GROUP_REC_PRIORITY),
+                               torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev))
+    return _GROUP_STREAMS[key]
+
+
+_GROUP_STREAMS = {}
+GROUP_REC_PRIORITY = int(os.environ.get("MVB_GROUP_REC_PRIORITY", "0"))
+
+
+def _grouped_synthesis(geom, pre_dev, groups, bufs, work_dev, work_at, synth) -> None:
+    """Interval records and synthesis group by group: the records of group
+    g go to bufs[g % 2] (image coef offsets rebased by the group's first
+    coarse sample) on one stream, its synthesis (work items of its jobs) on
+    another; group g + 2 reuses the buffer once group g's synthesis is done,
+    so group g + 1's records overlap group g's synthesis.  Forks from and
+    joins the current stream (legal inside a graph capture)."""
+    dev = geom.dev
+    lay = geom.rec_layout
+    main = torch.cuda.current_stream(dev)
+    sa, *sbs = _group_streams(dev)  # records; synthesis on alternating streams
+    start = torch.cuda.Event()       # (group g + 1's CTAs fill group g's tail)
+    start.record(main)
+    for x in (sa, *sbs):
+        x.wait_event(start)
+    windowed = any(jb.window is not None for jb in geom.jobs)
+    done = []
+    for g, (j0, j1) in enumerate(groups):
+        coef_p = bufs[g % len(bufs)].data_ptr() - 48 * int(lay["kbase"][j0])
+        with torch.cuda.stream(sa):
+            if g >= len(bufs):
+                sa.wait_event(done[g - len(bufs)])
+            for N, sel in geom.sel_by_factor.items():
+                off, cnt = lay["sel"][N]
+                part = sel[off + j0 * cnt: off + j1 * cnt]
+                fit = np.ascontiguousarray(phase_fit(N), dtype=np.float64)
+                max_K = coarse_span(geom.job_rows[j0:j1], N)
+                _lib.call("mvb_track_coeffs_windowed" if windowed else "mvb_track_coeffs",
+                          ptr(geom.images), ptr(part), part.numel(), max_K, ptr(pre_dev),
+                          ptr(geom.coarse), fit.ctypes.data_as(ctypes.c_void_p), coef_p,
+                          stream_handle(dev))
+            ready = torch.cuda.Event()
+            ready.record(sa)
+        sb = sbs[g % 2]
+        with torch.cuda.stream(sb):
+            sb.wait_event(ready)
+            synth(work_at[j0], work_at[j1], coef_p, stream_handle(dev))
+            ev = torch.cuda.Event()
+            ev.record(sb)
+            done.append(ev)
+    for x in (sa, *sbs):
+        main.wait_stream(x)
 
 
 def _interval_records(geom, pre_dev, st, fork=()) -> torch.Tensor:

@@ -505,3 +505,32 @@ def test_active_ranges_bit_identical(case, monkeypatch):
             res = render_jobs(jobs, f, precision="fp32", **kw)
             outs.append(torch.cat([res.job(j) for j in range(len(jobs))]))
         assert torch.equal(outs[0], outs[1]), (case, shard)
+
+
+@pytest.mark.parametrize("budget", [1, 60_000])
+def test_record_groups_bit_identical(budget, monkeypatch):
+    """Batches whose interval records exceed RECORD_BUDGET compute them group
+    by group into two alternating buffers inside the synthesis launch: the
+    output equals the all-at-once render bit for bit (direct render and a
+    render plan's replays), and the oracle within the fp32 bar."""
+    g, scenes, chans = _scenes("c4")
+    f = _filter_of(g, scenes[0].fd_taps)
+    jobs = scene_jobs(scenes, chans)
+    ref = render_jobs(jobs, f, precision="fp32")
+    refs = [ref.job(j).clone() for j in range(len(jobs))]
+    monkeypatch.setattr(engine, "RECORD_BUDGET", float(budget))
+    geom = engine.Geometry(jobs)
+    groups = engine._record_groups(geom)
+    assert groups and len(groups) >= 2 and groups[0][0] == 0 and groups[-1][1] == len(jobs)
+    res = render_jobs(jobs, f, precision="fp32")
+    for j in range(len(jobs)):
+        assert torch.equal(res.job(j), refs[j]), j
+    from paper_2508_03065_b200.plan import RenderPlan
+    plan = RenderPlan(jobs, f, precision="fp32")
+    for _ in range(3):
+        r = plan.run(jobs)
+        for j in range(len(jobs)):
+            assert torch.equal(r.job(j), refs[j]), j
+    ys = [refs[j].double().cpu().numpy() for j in range(len(jobs))]
+    for y, o in zip(ys, _oracle(scenes, chans, g["branches"])):
+        assert rel_err(y, o) <= FP32_TOL
