@@ -433,11 +433,13 @@ extern "C" int mvb_render_tracks_and_synthesize(const mvb_render_args* a, float*
     // ---- delay sort per time segment ----
     const int64_t n_seg = (T + SEG_LEN - 1) / SEG_LEN;
     mvb_image* sorted = mem.get<mvb_image>(n_seg * S);
-    if (!sorted) return fail(MVB_ECUDA, "render: scratch allocation");
+    uint32_t* keys = mem.get<uint32_t>(n_seg * S);
+    if (!sorted || !keys) return fail(MVB_ECUDA, "render: scratch allocation");
     int key_bits = 1;
     while (key_bits < 32 && (tau_ceil + 2) >= (1LL << key_bits)) ++key_bits;
-    MVB_TRY(mvb_delay_sort(images, d_pre, 1, S, n_seg, SEG_LEN, paths, coarse, key_bits, sorted,
-                           stream));
+    // keyed: the synthesis narrows every tile to its active images
+    MVB_TRY(mvb_delay_sort_keyed(images, d_pre, 1, S, n_seg, SEG_LEN, paths, coarse, key_bits, 0,
+                                 sorted, keys, stream));
     // ---- branch records: [front pad | n + L - 1 rows | back pad] ----
     int M1 = 0, nb = 0;
     std::vector<double> cb = fast_bank(a->h_branches, a->poly_order + 1, (int)L, M1, nb);
@@ -497,8 +499,11 @@ extern "C" int mvb_render_tracks_and_synthesize(const mvb_render_args* a, float*
     MVB_CUDA(cudaMemcpyAsync(d_work, work.data(), sizeof(mvb_work) * work.size(),
                              cudaMemcpyHostToDevice, st));
     MVB_CUDA(cudaMemsetAsync(d_out, 0, 4 * out_len, st));
-    MVB_TRY(mvb_synthesize_f32(d_job, d_work, (int64_t)work.size(), sorted, coef, rec, paths, d_out,
-                               part, nb, 16, stream));
+    int max_factor = 1;
+    for (int c = 0; c < nC; ++c) max_factor = std::max(max_factor, factors[c]);
+    MVB_TRY(mvb_synthesize_f32_ranged(d_job, d_work, (int64_t)work.size(), sorted, keys, S, SEG_LEN,
+                                      max_factor, bbox, coef, rec, paths, d_out, part, nb, 16,
+                                      stream));
     if (nc > 1) MVB_TRY(mvb_reduce_partials_f32(d_job, 1, out_len, part, d_out, stream));
     // host sources above are pageable: cudaMemcpyAsync has staged them before
     // returning; the scratch blocks are freed stream-ordered (Scratch)

@@ -542,7 +542,9 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
 
     // prologue of the staging pipeline: structs of the first two images, then
     // the first image's records
-    // k indexes the warp's image sequence ar[k]
+    // the warp's image sequence ar[k]: the loop carries only the count left
+    // and the position two images ahead (as many live registers as a plain
+    // strided walk -- more spill into the image loop at the 80-register cap)
     if (0 < nv) stage_image(st, 0, imgs + ar[0], lane);
     if (1 < nv) stage_image(st, 1, imgs + ar[1], lane);
     cp_async_commit();
@@ -550,17 +552,31 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     __syncwarp();
     if (0 < nv) stage_records(st, 0, st.img[0], coef, n0, T, lane);
     cp_async_commit();
+    int pos2 = ar[2];  // position of the image two ahead (valid while rem > 2)
+    // a chunk over two sorted runs (time shards) has a second part; only
+    // then does the walk read the range again (an LDS per image is ~1% of
+    // the data-pipe wavefronts the image costs)
+    const bool two_parts = nv > ar.nA;
 
-    // staging slots rotate: struct slots (cur, nx1, nx2), record slot rcur
-    int cur = 0, nx1 = 1, nx2 = 2, rcur = 0, rot;
-    for (int i = 0; i < nv; ++i, rot = cur, cur = nx1, nx1 = nx2, nx2 = rot, rcur ^= 1) {
+    // staging slots rotate: struct slots (cur, nx1, nx2), record slot rcur,
+    // packed in one register (bits 0-1, 2-3, 4-5, 6)
+    int slots = 0 | (1 << 2) | (2 << 4);
+    for (int rem = nv; rem > 0; --rem,
+             slots = ((slots >> 2) & 15) | ((slots & 3) << 4) | ((slots & 64) ^ 64)) {
+        const int cur = slots & 3, nx1 = (slots >> 2) & 3, nx2 = (slots >> 4) & 3,
+                  rcur = (slots >> 6) & 1;
         // everything issued one image ago has landed: records(i), struct(i+1)
         cp_async_wait_all();
         __syncwarp();
         // stream the next image's records and the struct after it while
         // this image is processed
-        if (i + 1 < nv) stage_records(st, rcur ^ 1, st.img[nx1], coef, n0, T, lane);
-        if (i + 2 < nv) stage_image(st, nx2, imgs + ar[i + 2], lane);
+        if (rem > 1) stage_records(st, rcur ^ 1, st.img[nx1], coef, n0, T, lane);
+        if (rem > 2) {
+            stage_image(st, nx2, imgs + pos2, lane);
+            // next position: +8, or the second part's first at the first one's end
+            pos2 += SYNTH_WARPS;
+            if (two_parts && pos2 == ar.fA + SYNTH_WARPS * ar.nA) pos2 = ar.fC;
+        }
         cp_async_commit();
 
         const mvb_image& im = st.img[cur];
