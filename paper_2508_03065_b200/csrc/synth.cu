@@ -788,12 +788,17 @@ static_assert((1 << F64_LOG_CHUNK) == F64_CHUNK_BLOCKS, "chunk is a power of two
 // in shared memory for up to F64_TAB_SLOTS factors: one LDS per tap instead
 // of an LDG plus its 64-bit address arithmetic
 constexpr int F64_TAB_SLOTS = 2;
-constexpr size_t F64_SMEM =
-    sizeof(double) * (F64_CHUNK * 32 + F64_CHUNK_BLOCKS * 32 + F64_TAB_SLOTS * 65 * 32);
 // images per warp evaluated together: their 65-tap upsample chains are
 // independent, so G chains hide the fp64 add latency of one (each chain
 // keeps the reference's tap order)
 constexpr int F64_G = 4;
+// each warp's F64_G coarse windows (65 samples, padded) staged in shared
+// memory before the tap loop: all their loads in flight at once instead of
+// one L1/L2 round trip per unrolled batch of taps
+constexpr int F64_WIN = 66;
+constexpr size_t F64_SMEM =
+    sizeof(double) * (F64_CHUNK * 32 + F64_CHUNK_BLOCKS * 32 + F64_TAB_SLOTS * 65 * 32 +
+                      F64_WARPS * F64_G * F64_WIN);
 
 __device__ __forceinline__ void merge_push(double* st_v, int* st_l, int& sp, double v, int l) {
     while (sp > 0 && st_l[sp - 1] == l) {
@@ -814,6 +819,7 @@ __global__ void __launch_bounds__(F64_WARPS * 32, MINB) k_synth_f64(
     double* contrib = f64_smem;                 // [F64_CHUNK images][32 lanes]
     double* bsum = f64_smem + F64_CHUNK * 32;   // [F64_CHUNK_BLOCKS][32 lanes]
     double* tslice = bsum + F64_CHUNK_BLOCKS * 32;  // [F64_TAB_SLOTS][65 cols][32 lanes]
+    double* wwin = tslice + F64_TAB_SLOTS * 65 * 32;  // [F64_WARPS][F64_G][F64_WIN]
     __shared__ int64_t slot_tab[F64_TAB_SLOTS];     // table offset cached in each slot (-1: none)
     const mvb_job& J = jobs[blockIdx.y];
     const int64_t out_len = J.out_len;
@@ -911,16 +917,46 @@ __global__ void __launch_bounds__(F64_WARPS * 32, MINB) k_synth_f64(
             // reference's tap order; other members run a dummy chain on a
             // valid address, discarded), then the rare clamped members alone
             {
+                double* ws = wwin + warp * (F64_G * F64_WIN);
+                __syncwarp();  // the previous group's tap loop is done with ws
+#pragma unroll
+                for (int g = 0; g < F64_G; ++g) {
+                    if (!fast[g]) continue;  // warp-uniform
+                    const double* src = cp[g] + (base[g] - 32);
+                    for (int c = lane; c < 65; c += 32) ws[g * F64_WIN + c] = __ldg(src + c);
+                }
+                __syncwarp();
                 const double* w[F64_G];
 #pragma unroll
-                for (int g = 0; g < F64_G; ++g) w[g] = fast[g] ? cp[g] + (base[g] - 32) : tables;
-#pragma unroll 5
-                for (int col = 0; col < 65; ++col) {
+                for (int g = 0; g < F64_G; ++g) w[g] = ws + g * F64_WIN;
+                // members of one factor (the common case: a tier is contiguous
+                // in the canonical order) read the same table slice: one
+                // shared-memory load per tap serves all F64_G chains (the
+                // slice loads were half of the kernel's data-pipe wavefronts)
+                bool one_slice = true;
 #pragma unroll
-                    for (int g = 0; g < F64_G; ++g) {
-                        MVB_CHECK(!fast[g] || (base[g] - 32 + col >= 0 && base[g] - 32 + col < nc[g]),
-                                  CHK_EXACT_INDEX);
-                        acc[g] = xadd(acc[g], xmul(ts[g][col * 32], __ldg(w[g] + col)));
+                for (int g = 1; g < F64_G; ++g) one_slice = one_slice && (!fast[g] || ts[g] == ts[0]);
+                if (one_slice) {
+                    const double* t0 = ts[0];
+#pragma unroll 5
+                    for (int col = 0; col < 65; ++col) {
+                        const double tv = t0[col * 32];
+#pragma unroll
+                        for (int g = 0; g < F64_G; ++g) {
+                            MVB_CHECK(!fast[g] || (base[g] - 32 + col >= 0 && base[g] - 32 + col < nc[g]),
+                                      CHK_EXACT_INDEX);
+                            acc[g] = xadd(acc[g], xmul(tv, w[g][col]));
+                        }
+                    }
+                } else {
+#pragma unroll 5
+                    for (int col = 0; col < 65; ++col) {
+#pragma unroll
+                        for (int g = 0; g < F64_G; ++g) {
+                            MVB_CHECK(!fast[g] || (base[g] - 32 + col >= 0 && base[g] - 32 + col < nc[g]),
+                                      CHK_EXACT_INDEX);
+                            acc[g] = xadd(acc[g], xmul(ts[g][col * 32], w[g][col]));
+                        }
                     }
                 }
             }
