@@ -104,17 +104,18 @@ int mvb_enumerate(const double* d_dims, const double* d_walls, int64_t n_rooms,
  *    decimated path.  Every kernel below covers the whole batch per launch.
  *
  *    Call order (no host wait after the decimation decision):
- *      paths:  path_bbox; center_paths -> (cuFFT rFFT) -> spectrum_index
+ *      paths:  path_bbox; path_spectrum_index (own FFT) -> lowpass_paths
  *              (host: low-pass decision, output capacity bound from the
  *              boxes) -> decimate_rows
  *      images: enumerate (cacheable per rooms + order) -> build_images
  *      tracks: coarse_distances (+ bounds; one call per factor) ->
  *              track_bounds -> track_max
- *      fast:   branch_records_f32, track_coeffs (per factor), delay_sort
- *              (or sort_keys -> sort -> gather_images beyond
+ *      fast:   branch_records_f32, track_coeffs (per factor),
+ *              delay_sort_keyed (or sort_keys -> sort -> gather_images beyond
  *              MVB_DELAY_SORT_MAX images), finalize_lengths (exact out_len =
  *              len(s) + ceil(rate*dmax/c) + L, synth.py:211-212, on the
- *              device) -> synthesize_f32 [-> reduce_partials_f32]
+ *              device) -> synthesize_f32_ranged (after the keyed sort; else
+ *              synthesize_f32) [-> reduce_partials_f32]
  *              (track_max, track_coeffs, delay_sort and branch_records_f32
  *              depend only on the coarse tracks / the signal: independent
  *              streams may run them concurrently)
