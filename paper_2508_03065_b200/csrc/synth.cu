@@ -307,6 +307,47 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// Staging transport: lane-parallel 16-byte LDGSTS (cp.async), or with
+// -DMVB_STAGE_BULK one 1-D bulk copy per staged object (cp.async.bulk
+// through the TMA unit, completion on a per-warp mbarrier with a
+// transaction count; VERDICT r1 lever).  Measured (same box, 10 steps): c3
+// synthesis 8.20 ms LDGSTS vs 8.40 bulk (8.33 without the per-image proxy
+// fence), c4 65.7 vs 66.2 (65.6) -- the one-lane issue and mbarrier wait
+// put more latency on the warp's one-image-ahead pipeline than the LDGSTS
+// wavefronts cost, so LDGSTS stays the default.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_init(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    // visible to the async proxy (CTA scope; the cluster-scope
+    // fence.mbarrier_init compiles to an L1 invalidate)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bar_arrive_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "MVB_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra MVB_WAIT_%=;\n\t}"
+        ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// generic-proxy reads of a slot happen before the async-proxy write that
+// overwrites it
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // Per-warp staging area: image structs for the current, next and next-next
 // image of the warp, and the interval records of the current and next image
 // over this tile (only for factors N >= 32, at most TN/32 + 1 records).
@@ -316,12 +357,13 @@ struct alignas(16) WarpStage {
     static_assert(3 * RMAX <= 64, "stage_records copies at most two 16-byte chunks per lane");
     mvb_image img[3];
     mvb_coef32 rec[2][RMAX];
+    unsigned long long bar;  // bulk-copy completion (per warp)
 };
 
 // issue the copies of image q's interval records over [n0, n0+TN) into slot
 // `dst` (lane-parallel 16-byte chunks); the records exist only for factor >= 32
 template <int U>
-__device__ __forceinline__ void stage_records(WarpStage<U>& st, int slot, const mvb_image& q,
+__device__ __forceinline__ unsigned stage_records(WarpStage<U>& st, int slot, const mvb_image& q,
                                               const mvb_coef32* __restrict__ coef, int n0, int T,
                                               int lane) {
     constexpr int TN = 32 * U;
@@ -344,18 +386,52 @@ __device__ __forceinline__ void stage_records(WarpStage<U>& st, int slot, const 
         MVB_CHECK(k0 >= 0 && last < q.n_coarse, CHK_RECORD_INDEX);
         MVB_CHECK(chunks <= 3 * WarpStage<U>::RMAX, CHK_STAGE_SIZE);
         MVB_CHECK(((uintptr_t)src & 15) == 0 && ((uintptr_t)dst & 15) == 0, CHK_ALIGN);
+#ifndef MVB_STAGE_BULK
         // at most two 16-byte chunks per lane, no loop
         if (lane < chunks) cp_async16(dst + 16 * lane, src + 16 * lane);
         if (lane + 32 < chunks) cp_async16(dst + 16 * (lane + 32), src + 16 * (lane + 32));
+#else
+        if (lane == 0) bulk_g2s(dst, src, 16u * chunks, &st.bar);
+        return 16u * chunks;
+#endif
     }
+    return 0u;
 }
 
 template <int U>
-__device__ __forceinline__ void stage_image(WarpStage<U>& st, int slot, const mvb_image* src,
-                                            int lane) {
+__device__ __forceinline__ unsigned stage_image(WarpStage<U>& st, int slot, const mvb_image* src,
+                                                int lane) {
+#ifndef MVB_STAGE_BULK
     if (lane < (int)(sizeof(mvb_image) / 16))
         cp_async16(reinterpret_cast<char*>(&st.img[slot]) + 16 * lane,
                    reinterpret_cast<const char*>(src) + 16 * lane);
+#else
+    if (lane == 0) bulk_g2s(&st.img[slot], src, (unsigned)sizeof(mvb_image), &st.bar);
+#endif
+    return (unsigned)sizeof(mvb_image);
+}
+
+// One staging phase of a warp: the copies issued since the last wait land
+// before the next stage_wait.  LDGSTS: commit / wait_all; bulk: lane 0 arms
+// the warp's mbarrier with the phase's byte count (after issuing -- the
+// phase cannot complete before its one arrival), all lanes wait on parity.
+template <int U>
+__device__ __forceinline__ void stage_commit(WarpStage<U>& st, unsigned bytes, int lane) {
+#ifndef MVB_STAGE_BULK
+    cp_async_commit();
+#else
+    if (lane == 0) bar_arrive_tx(&st.bar, bytes);
+#endif
+}
+template <int U>
+__device__ __forceinline__ void stage_wait(WarpStage<U>& st, unsigned& parity) {
+#ifndef MVB_STAGE_BULK
+    cp_async_wait_all();
+#else
+    bar_wait(&st.bar, parity);
+    parity ^= 1u;
+#endif
+    __syncwarp();
 }
 
 // Active image range of a tile.  The delay sort's keys (k_delay_sort:
@@ -545,13 +621,18 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     // the warp's image sequence ar[k]: the loop carries only the count left
     // and the position two images ahead (as many live registers as a plain
     // strided walk -- more spill into the image loop at the 80-register cap)
-    if (0 < nv) stage_image(st, 0, imgs + ar[0], lane);
-    if (1 < nv) stage_image(st, 1, imgs + ar[1], lane);
-    cp_async_commit();
-    cp_async_wait_all();
+#ifdef MVB_STAGE_BULK
+    if (lane == 0) bar_init(&st.bar);
     __syncwarp();
-    if (0 < nv) stage_records(st, 0, st.img[0], coef, n0, T, lane);
-    cp_async_commit();
+#endif
+    unsigned parity = 0, bytes = 0;
+    if (0 < nv) bytes += stage_image(st, 0, imgs + ar[0], lane);
+    if (1 < nv) bytes += stage_image(st, 1, imgs + ar[1], lane);
+    stage_commit(st, bytes, lane);
+    stage_wait(st, parity);
+    bytes = 0;
+    if (0 < nv) bytes += stage_records(st, 0, st.img[0], coef, n0, T, lane);
+    stage_commit(st, bytes, lane);
     int pos2 = ar[2];  // position of the image two ahead (valid while rem > 2)
     // a chunk over two sorted runs (time shards) has a second part; only
     // then does the walk read the range again (an LDS per image is ~1% of
@@ -566,18 +647,21 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
         const int cur = slots & 3, nx1 = (slots >> 2) & 3, nx2 = (slots >> 4) & 3,
                   rcur = (slots >> 6) & 1;
         // everything issued one image ago has landed: records(i), struct(i+1)
-        cp_async_wait_all();
-        __syncwarp();
+        stage_wait(st, parity);
         // stream the next image's records and the struct after it while
-        // this image is processed
-        if (rem > 1) stage_records(st, rcur ^ 1, st.img[nx1], coef, n0, T, lane);
+        // this image is processed (their slots were last read two images ago)
+#if defined(MVB_STAGE_BULK) && !defined(MVB_NO_PROXY_FENCE)
+        if (lane == 0) fence_proxy_async();
+#endif
+        unsigned bytes = 0;
+        if (rem > 1) bytes += stage_records(st, rcur ^ 1, st.img[nx1], coef, n0, T, lane);
         if (rem > 2) {
-            stage_image(st, nx2, imgs + pos2, lane);
+            bytes += stage_image(st, nx2, imgs + pos2, lane);
             // next position: +8, or the second part's first at the first one's end
             pos2 += SYNTH_WARPS;
             if (two_parts && pos2 == ar.fA + SYNTH_WARPS * ar.nA) pos2 = ar.fC;
         }
-        cp_async_commit();
+        stage_commit(st, bytes, lane);
 
         const mvb_image& im = st.img[cur];
         const int N = im.factor;
