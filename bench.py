@@ -147,6 +147,11 @@ class ClockSampler:
 # workload
 
 
+def parallel_mode(name):
+    from paper_2508_03065_b200 import parallel
+    return parallel.shard_mode(name, 2)
+
+
 def build_workload(name, rank, world):
     """Scenes, the jobs this rank renders, and the sharding mode."""
     from paper_2508_03065_b200 import parallel, workloads
@@ -698,7 +703,9 @@ def measure(ctx, name, steps, warmup, peaks, args, precision=None, with_e2e=True
         "warmup": warmup,
         "ms_per_step": ms_step,
         "higher_is_better": True,
-        "scaling": "strong" if (world > 1 and shard is not None) else "weak",
+        # c3 / c4 / c5 shard a fixed total over the ranks (strong, at every
+        # N); c1 / c2 run replicas, the same job per rank (weak)
+        "scaling": "weak" if parallel_mode(name) == "replicas" else "strong",
         "vs_baseline": None,
         "dtype": "f64" if precision == "fp64" else "f32 (fp64 delay anchors)",
         "data": "synthetic (seeded white Gaussian dry signal, seeded paths; SURVEY 8d)",
