@@ -12,7 +12,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
-from paper_2508_03065_b200 import engine, hann_sinc, parallel, workloads  # noqa: E402
+from paper_2508_03065_b200 import engine, hann_sinc, parallel, room, workloads  # noqa: E402
 from paper_2508_03065_b200.plan import RenderPlan  # noqa: E402
 
 dev = torch.device("cuda", 0)
@@ -41,6 +41,12 @@ for cfg, kind in cases:
                 plan = RenderPlan(jobs, f)
             elif kind == "channels":  # independent jobs, no collective
                 mine = [jobs[i] for i in parallel.channel_shard(len(jobs), r, W)]
+                plan = RenderPlan(mine, f)
+            elif kind == "scenes":  # c4: LPT over scenes (bench.build_workload's cost)
+                cost = [room.image_count(sc.max_order) * len(sc.mics) *
+                        (sc.T + sc.max_order * float(np.max(sc.dims)) * sc.rate / 343.0)
+                        for sc in scenes]
+                mine = [jobs[i] for i in parallel.lpt_assign(cost, W)[r]]
                 plan = RenderPlan(mine, f)
             else:
                 plan = RenderPlan(jobs, f, shard=(r, W, kind), dmax_hook=hook)
