@@ -875,7 +875,10 @@ constexpr int F64_TAB_SLOTS = 2;
 // images per warp evaluated together: their 65-tap upsample chains are
 // independent, so G chains hide the fp64 add latency of one (each chain
 // keeps the reference's tap order)
-constexpr int F64_G = 4;
+#ifndef MVB_F64_G
+#define MVB_F64_G 4
+#endif
+constexpr int F64_G = MVB_F64_G;
 // each warp's F64_G coarse windows (65 samples, padded) staged in shared
 // memory before the tap loop: all their loads in flight at once instead of
 // one L1/L2 round trip per unrolled batch of taps

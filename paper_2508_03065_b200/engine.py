@@ -36,6 +36,7 @@ rank writes the reference's out_len and the partial outputs sum exactly
 from __future__ import annotations
 
 import ctypes
+import functools
 import math
 import os
 from dataclasses import dataclass, field
@@ -1131,7 +1132,7 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     for j in range(nJ):
         rows[j].update(rec_base=rec_start[keys[j]], nb=nb, img_off=j * max_seg * max_img,
                        img_stride=max_img, rec_rows=rec_rows)
-    work, part_rows = _work_list(geom.n_img, out_len, n_seg, sm_count, rows)
+    work, part_rows = _work_list(geom.n_img, out_len, n_seg, sm_count, rows, geom.jobs)
     work_at = np.searchsorted(work[:, 0], np.arange(nJ + 1), side="left")  # job j: [at[j], at[j+1])
     _mark("render.records_plan")
     jobs_dev = h2d(pack_jobs(rows), dev)
@@ -1421,11 +1422,41 @@ def _table_records(uniq, sig_dev, sig_len, start, rec_rows, filt, dev, st, conca
     return xp, h2d(fraction_table(filt), dev)
 
 
-def _work_list(n_img, out_len, n_seg, sm_count, rows):
+# work items ordered by estimated cost, most expensive first (MVB_WORK_ORDER=0:
+# chunk-major, tile order)
+WORK_ORDER = os.environ.get("MVB_WORK_ORDER", "1") != "0"
+
+
+def _delay_estimates(jb) -> np.ndarray:
+    """Sorted structural delay estimates (samples) of a job's images:
+    kappa * |j * dims| (the image of the room centre), cached per structure."""
+    key = (np.asarray(jb.dims, np.float64).tobytes(), int(jb.max_order),
+           None if jb.image_index is None else np.asarray(jb.image_index, np.int64).tobytes(),
+           float(jb.rate) / float(jb.c))
+    return _delay_est(key)
+
+
+@functools.lru_cache(maxsize=64)
+def _delay_est(key) -> np.ndarray:
+    from . import parallel
+    dims_b, max_order, images_b, kappa = key
+    j, _ = parallel.canonical_lattice(max_order)
+    if images_b is not None:
+        j = j[np.frombuffer(images_b, dtype=np.int64)]
+    return np.sort(kappa * np.linalg.norm(j * np.frombuffer(dims_b, np.float64)[None, :], axis=1))
+
+
+def _work_list(n_img, out_len, n_seg, sm_count, rows, jobs=None):
     """mvb_work items (job, tile, image range, chunk, sort segment) of every
     job, image ranges split into chunks (_chunking); chunked jobs get
     partial-output rows (rows[j]['n_chunks'], ['part_off'] are set).  A
-    time-shard job (rows[j] w0 / w1) gets the tiles of its window only."""
+    time-shard job (rows[j] w0 / w1) gets the tiles of its window only.
+    With `jobs`, each job's items are ordered by their estimated cost --
+    the chunk's images whose structural delay estimate puts a row inside
+    the signal over the tile (the synthesis visits only those, §5.6 of
+    DESIGN.md) -- most expensive first: the CTAs dispatched last, which
+    set the kernel's tail, are the cheap front / tail tiles.  Jobs stay
+    contiguous (record groups slice the list by job)."""
     nJ = len(rows)
     first = [int(rows[j].get("w0", 0)) // TILE for j in range(nJ)]
     end = [-(-int(out_len[j]) // TILE) for j in range(nJ)]
@@ -1450,7 +1481,18 @@ def _work_list(n_img, out_len, n_seg, sm_count, rows):
         blk[:, :, 3] = ((span * (cs + 1)) // nc)[:, None]
         blk[:, :, 4] = cs[:, None]
         blk[:, :, 5] = np.minimum(tj * TILE // SEG_LEN, n_seg[j] - 1)[None, :]
-        blocks.append(blk.reshape(-1, 8))
+        blk = blk.reshape(-1, 8)
+        if WORK_ORDER and jobs is not None and len(blk) > 1:
+            tau = _delay_estimates(jobs[j])
+            ls = int(rows[j]["ls"])
+            n0 = blk[:, 1].astype(np.float64) * TILE
+            b, e = blk[:, 2], blk[:, 3]
+            # images of [b, e) (sorted-delay positions) with n0 - ls < tau <= n0 + TILE
+            lo = np.clip(np.searchsorted(tau, n0 - ls, side="right"), b, e)
+            hi = np.clip(np.searchsorted(tau, n0 + TILE, side="right"), b, e)
+            cost = (hi - lo) + 0.05 * (e - b)
+            blk = blk[np.argsort(-cost, kind="stable")]
+        blocks.append(blk)
     work = np.concatenate(blocks)
     if len(work) == 0:  # every window past its job's length bound: one idle item
         work = np.zeros((1, 8), np.int32)
