@@ -413,6 +413,17 @@ int mvb_synthesize_f32_ranged(const mvb_job* d_jobs, const mvb_work* d_work, int
                               const double* d_paths, float* d_out, float* d_part, int nb,
                               int u_steps, void* stream);
 
+/* Measurement variant of mvb_synthesize_f32_ranged (nb = 8 only): the
+ * branch-record gathers through the texture pipe (mode 1: every step;
+ * mode 2: odd steps, the others LDG.256); rec_floats = the record buffer's
+ * size in floats.  Same output. */
+int mvb_synthesize_f32_tex(const mvb_job* d_jobs, const mvb_work* d_work, int64_t n_work,
+                           const mvb_image* d_images, const uint32_t* d_keys, int64_t run_len,
+                           int64_t seg_len, int max_factor, const double* d_bbox,
+                           const mvb_coef32* d_coef, const float* d_rec, int64_t rec_floats,
+                           const double* d_paths, float* d_out, float* d_part, int nb, int mode,
+                           void* stream);
+
 /* Fixed-order sum of the n_chunks partial rows of every job. */
 int mvb_reduce_partials_f32(const mvb_job* d_jobs, int64_t n_jobs, int64_t max_out_len,
                             const float* d_part, float* d_out, void* stream);

@@ -56,6 +56,7 @@ _SIGS = {
     "mvb_branch_records_f32": [P, P, P, P, P, P, I64, I64, P, INT, INT, INT, P, P],
     "mvb_synthesize_f32": [P, P, I64, P, P, P, P, P, P, INT, INT, P],
     "mvb_synthesize_f32_ranged": [P, P, I64, P, P, I64, I64, INT, P, P, P, P, P, P, INT, INT, P],
+    "mvb_synthesize_f32_tex": [P, P, I64, P, P, I64, I64, INT, P, P, P, I64, P, P, P, INT, INT, P],
     "mvb_reduce_partials_f32": [P, I64, I64, P, P, P],
     "mvb_synthesize_f64": [P, I64, I64, P, P, P, P, P, P, P],
     "mvb_energy_index": [P, I64, I64, DBL, P, P],

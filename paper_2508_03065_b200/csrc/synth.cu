@@ -31,7 +31,10 @@
 // (synth.py:182-191) evaluated with an equivalent merge stack.
 #include <cfloat>
 #include <cstdlib>
+#include <mutex>
 #include <type_traits>
+#include <utility>
+#include <vector>
 
 #include "mvb_common.cuh"
 
@@ -189,6 +192,37 @@ struct FarrowGather {
         MVB_CHECK(row < rows, CHK_GATHER_ROW);
         return gather_horner<NP>(R, row, mc);
     }
+    __device__ __forceinline__ float at(unsigned row, float mc, int) const { return (*this)(row, mc); }
+};
+
+// The same Horner with the row fetched through the texture pipe (two
+// float4 texels per 32-byte row; a separate L1TEX data path from the LSU
+// one the LDG.256 gathers saturate).  TEXM 1: every step, 2: odd steps only
+// (the even ones stay LDG.256).  Measurement variants (MVB_TEX_GATHER).
+template <int TEXM>
+struct TexFarrowGather {
+    const float4* __restrict__ R;
+    unsigned rows;
+    cudaTextureObject_t tex;
+    __device__ __forceinline__ float horner(const float4 v0, const float4 v1, float mc) const {
+        const float y = mc * mc;
+        const float2 yy = f2(y, y);
+        float2 q = f2(v1.z, v1.w);
+        q = __ffma2_rn(q, yy, f2(v1.x, v1.y));
+        q = __ffma2_rn(q, yy, f2(v0.z, v0.w));
+        q = __ffma2_rn(q, yy, f2(v0.x, v0.y));
+        return fmaf(mc, q.y, q.x);
+    }
+    __device__ __forceinline__ float operator()(unsigned row, float mc) const {
+        MVB_CHECK(row < rows, CHK_GATHER_ROW);
+        const float4 v0 = tex1Dfetch<float4>(tex, (int)(2 * row));
+        const float4 v1 = tex1Dfetch<float4>(tex, (int)(2 * row + 1));
+        return horner(v0, v1, mc);
+    }
+    __device__ __forceinline__ float at(unsigned row, float mc, int u) const {
+        if (TEXM == 2 && (u & 1) == 0) return gather_horner<2>(R, row, mc);
+        return (*this)(row, mc);
+    }
 };
 
 // Literal per-fraction table: taps h_j(mu) at mu = p / TAB_P, p = 0..TAB_P,
@@ -204,6 +238,7 @@ struct TableGather {
     const float* tab;  // shared memory
     int L;
     unsigned rows;
+    __device__ __forceinline__ float at(unsigned row, float mc, int) const { return (*this)(row, mc); }
     __device__ __forceinline__ float operator()(unsigned row, float mc) const {
         MVB_CHECK(row < rows && row >= (unsigned)(L - 1), CHK_GATHER_ROW);
         const float sc = (mc + 0.5f) * (float)TAB_P;
@@ -259,7 +294,7 @@ constexpr int MAGIC_I = 0x4B400000;
 template <class G>
 __device__ __forceinline__ float dec_step(const float4& c0, const float4& c1, const float4& c2,
                                           float uu, int rowbase, const G& g,
-                                          float an, float invk, float dmin) {
+                                          float an, float invk, float dmin, int u = 0) {
     const float res = track_residual(c1, c2, uu);  // kappa * (d - g0)
     const float t = c0.y + res;
     const float v = t + MAGIC_F;
@@ -267,7 +302,7 @@ __device__ __forceinline__ float dec_step(const float4& c0, const float4& c1, co
     const unsigned row = (unsigned)(rowbase - __float_as_int(v));
     const float d = fmaf(res, invk, c0.z);
     const float A = an * rcp_approx(fmaxf(d, dmin));
-    return A * g(row, mc);
+    return A * g.at(row, mc, u);
 }
 
 // Decimated image on a tile wholly inside [0, T) with TILE % NT == 0 (its
@@ -293,7 +328,7 @@ __device__ __forceinline__ void dec_static(float (&acc)[U], const float4* __rest
             nlB = nl - __float_as_int(c0.x);
         }
         const float uu = lt + ((float)((u % SPI) * 32) * (2.0f / NT) - 1.0f);
-        acc[u] += dec_step(c0, c1, c2, uu, nlB + 32 * u, g, an, invk, dmin);
+        acc[u] += dec_step(c0, c1, c2, uu, nlB + 32 * u, g, an, invk, dmin, u);
     }
 }
 
@@ -453,6 +488,7 @@ struct RangeArgs {
     int run_len;           // sorted run length of the table (a job's whole table: >= n_img)
     int seg_len;           // sort segment length (samples)
     int max_factor;        // largest decimation factor of the batch
+    cudaTextureObject_t tex;  // branch records as float4 texels (TexFarrowGather) or 0
 };
 
 // first positions in [b, e) whose key exceeds x0 / x1 (sorted keys), both
@@ -546,7 +582,7 @@ __device__ __forceinline__ ActiveRange active_range(const RangeArgs& ra, const m
     return r;
 }
 
-template <int U, int NP, int MINB, bool TAB = false>
+template <int U, int NP, int MINB, bool TAB = false, int TEXM = 0>
 __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     const mvb_job* __restrict__ jobs, const mvb_work* __restrict__ work,
     const mvb_image* __restrict__ images, const mvb_coef32* __restrict__ coef,
@@ -566,7 +602,9 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     // rows are indexed globally: row = rec_base + (n + L - D) >= 0 thanks to
     // the zero front pad of every signal's region
     const int rb = (int)Jp->rec_base;
-    using Gather = std::conditional_t<TAB, TableGather, FarrowGather<NP>>;
+    using Gather = std::conditional_t<TAB, TableGather,
+                                      std::conditional_t<(TEXM > 0), TexFarrowGather<TEXM>,
+                                                         FarrowGather<NP>>>;
     Gather g;
     if constexpr (TAB) {
         // the fraction table: (TAB_P + 1) rows of L taps, padded to L + 1
@@ -577,7 +615,11 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
         __syncthreads();
         g = TableGather{rec, tab_smem, Lt, (unsigned)Jp->rec_rows};
     } else {
-        g = FarrowGather<NP>{reinterpret_cast<const float4*>(rec), (unsigned)Jp->rec_rows};
+        if constexpr (TEXM > 0)
+            g = TexFarrowGather<TEXM>{reinterpret_cast<const float4*>(rec), (unsigned)Jp->rec_rows,
+                                      ra.tex};
+        else
+            g = FarrowGather<NP>{reinterpret_cast<const float4*>(rec), (unsigned)Jp->rec_rows};
     }
     MVB_CHECK(wp->seg >= 0 && (Jp->img_stride == 0 || wp->img_end <= Jp->img_stride) &&
                   wp->img_begin >= 0 && wp->img_begin <= wp->img_end, CHK_WORK);
@@ -699,7 +741,7 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
             const int rfirst = row0 - lane;  // row of the tile's first sample (warp-uniform)
             if (rfirst + TN <= rb || rfirst >= rb + ls) continue;  // all in the zero pads
 #pragma unroll
-            for (int u = 0; u < U; ++u) acc[u] += A * g((unsigned)(row0 + 32 * u), mc);
+            for (int u = 0; u < U; ++u) acc[u] += A * g.at((unsigned)(row0 + 32 * u), mc, u);
             continue;
         }
         if (N == 1) {
@@ -727,7 +769,7 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
                 const float mc = (float)(s - D) - 0.5f;
                 const unsigned r = (unsigned)(rb + n + Lsh - (int)D);
                 const float A = an * rcp_approx(fmaxf((float)d, dmin));
-                row[32 * u + lane] = fmaf(A, g(r, mc), row[32 * u + lane]);
+                row[32 * u + lane] = fmaf(A, g.at(r, mc, u), row[32 * u + lane]);
             }
             continue;
         }
@@ -787,7 +829,7 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
                 }
                 const float uu = fmaf((float)r, twoInvN, -1.f);
                 acc[u] += dec_step(c0, c1, c2, uu, nl - __float_as_int(c0.x) + 32 * u, g, an,
-                                       invk, dmin);
+                                       invk, dmin, u);
             }
         }
     }
@@ -1177,7 +1219,7 @@ int mvb_synthesize_f32(const mvb_job* jobs, const mvb_work* work, int64_t n_work
                        const double* paths, float* out, float* part, int nb, int u_steps,
                        void* stream) {
     return synthesize_f32(jobs, work, n_work, images, coef, rec, paths, out, part, nb, u_steps,
-                          RangeArgs{nullptr, nullptr, 1, 1, 1}, stream);
+                          RangeArgs{nullptr, nullptr, 1, 1, 1, 0}, stream);
 }
 
 int mvb_synthesize_f32_ranged(const mvb_job* jobs, const mvb_work* work, int64_t n_work,
@@ -1190,7 +1232,59 @@ int mvb_synthesize_f32_ranged(const mvb_job* jobs, const mvb_work* work, int64_t
         max_factor < 1)
         return fail(MVB_EINVAL, "synthesize_f32_ranged: run_len / seg_len / max_factor");
     return synthesize_f32(jobs, work, n_work, images, coef, rec, paths, out, part, nb, u_steps,
-                          RangeArgs{keys, bbox, (int)run_len, (int)seg_len, max_factor}, stream);
+                          RangeArgs{keys, bbox, (int)run_len, (int)seg_len, max_factor, 0}, stream);
+}
+
+// Measurement variant: the ranged synthesis with the branch-record gathers
+// (or every other step's) through the texture pipe.  The texture object of
+// (rec, rec_floats) is created once and cached (never destroyed: a
+// diagnostic entry point).
+int mvb_synthesize_f32_tex(const mvb_job* jobs, const mvb_work* work, int64_t n_work,
+                           const mvb_image* images, const uint32_t* keys, int64_t run_len,
+                           int64_t seg_len, int max_factor, const double* bbox,
+                           const mvb_coef32* coef, const float* rec, int64_t rec_floats,
+                           const double* paths, float* out, float* part, int nb, int mode,
+                           void* stream) {
+    if (nb != 8 || (mode != 1 && mode != 2) || !keys || !bbox || rec_floats < 8 ||
+        rec_floats / 4 > 0x7fffffff)
+        return fail(MVB_EINVAL, "synthesize_f32_tex: nb 8, mode 1/2, keys, bbox, size");
+    if (n_work <= 0) return MVB_OK;
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const float*, int64_t>, cudaTextureObject_t>> cache;
+    cudaTextureObject_t tex = 0;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto& e : cache)
+            if (e.first.first == rec && e.first.second == rec_floats) tex = e.second;
+        if (!tex) {
+            cudaResourceDesc rd{};
+            rd.resType = cudaResourceTypeLinear;
+            rd.res.linear.devPtr = const_cast<float*>(rec);
+            rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+            rd.res.linear.sizeInBytes = (size_t)rec_floats * sizeof(float);
+            cudaTextureDesc td{};
+            td.readMode = cudaReadModeElementType;
+            // allowed inside a (render plan's) stream capture
+            cudaStreamCaptureMode m = cudaStreamCaptureModeRelaxed;
+            cudaThreadExchangeStreamCaptureMode(&m);
+            const cudaError_t e = cudaCreateTextureObject(&tex, &rd, &td, nullptr);
+            cudaThreadExchangeStreamCaptureMode(&m);
+            if (e != cudaSuccess) return fail(MVB_ECUDA, cudaGetErrorString(e));
+            cache.push_back({{rec, rec_floats}, tex});
+        }
+    }
+    const RangeArgs ra{keys, bbox, (int)run_len, (int)seg_len, max_factor, tex};
+    cudaStream_t s = as_stream(stream);
+    if (mode == 1) {
+        prefer_carveout((const void*)k_synth_f32<16, 2, 3, false, 1>, true);
+        k_synth_f32<16, 2, 3, false, 1><<<(unsigned)n_work, SYNTH_WARPS * 32, 0, s>>>(
+            jobs, work, images, coef, rec, paths, out, part, ra);
+    } else {
+        prefer_carveout((const void*)k_synth_f32<16, 2, 3, false, 2>, true);
+        k_synth_f32<16, 2, 3, false, 2><<<(unsigned)n_work, SYNTH_WARPS * 32, 0, s>>>(
+            jobs, work, images, coef, rec, paths, out, part, ra);
+    }
+    return check_launch("synthesize_f32_tex");
 }
 
 int mvb_signal_plane_f32(const float* x_all, const int64_t* sig_off, const int64_t* sig_len,
@@ -1222,7 +1316,7 @@ int mvb_synthesize_f32_table(const mvb_job* jobs, const mvb_work* work, int64_t 
         return check_launch("synthesize_f32_table (smem attribute)");
     prefer_carveout((const void*)k_synth_f32<16, 1, 1, true>);
     k_synth_f32<16, 1, 1, true><<<(unsigned)n_work, SYNTH_WARPS * 32, smem, as_stream(stream)>>>(
-        jobs, work, images, coef, xp, paths, out, part, RangeArgs{nullptr, nullptr, 1, 1, 1}, table);
+        jobs, work, images, coef, xp, paths, out, part, RangeArgs{nullptr, nullptr, 1, 1, 1, 0}, table);
     return check_launch("synthesize_f32_table");
 }
 

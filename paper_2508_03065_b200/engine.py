@@ -1144,7 +1144,12 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
     def synth(w0, w1, coef_p, st):
         # work items [w0, w1) with the interval records at coef_p
         wp = work_dev.data_ptr() + 32 * int(w0)
-        if keyed is not None:
+        if keyed is not None and TEX_GATHER and nb == 8:
+            _lib.call("mvb_synthesize_f32_tex", ptr(jobs_dev), wp, int(w1 - w0),
+                      ptr(images_sorted), ptr(keyed[0]), keyed[1], SEG_LEN,
+                      max(geom.factors, default=1), ptr(geom.bbox), coef_p, ptr(rec), rec.numel(),
+                      ptr(geom.paths), ptr(out), ptr(part), nb, TEX_GATHER, st)
+        elif keyed is not None:
             _lib.call("mvb_synthesize_f32_ranged", ptr(jobs_dev), wp, int(w1 - w0),
                       ptr(images_sorted), ptr(keyed[0]), keyed[1], SEG_LEN,
                       max(geom.factors, default=1), ptr(geom.bbox), coef_p, ptr(rec),
@@ -1391,6 +1396,8 @@ FD_GATHER = os.environ.get("MVB_FD_GATHER", "farrow")
 # per-tile active image ranges from the sorted keys (mvb_synthesize_f32_ranged);
 # MVB_ACTIVE_RANGES=0: every tile walks its whole chunk (A/B)
 ACTIVE_RANGES = os.environ.get("MVB_ACTIVE_RANGES", "1") != "0"
+# measurement variant: gathers through the texture pipe (1: all, 2: odd steps)
+TEX_GATHER = int(os.environ.get("MVB_TEX_GATHER", "0"))
 
 
 def fraction_table(filt) -> np.ndarray:
