@@ -218,3 +218,62 @@ def test_memory_groups_split_by_footprint():
     assert all(sum(fp[j] for j in g) <= 2 * max(fp) for g in groups) and len(groups) >= 3
     assert _memory_groups(jobs, 1, 32) == [[j] for j in range(6)]  # never empty groups
     assert _memory_groups(jobs, 10 ** 15, 32) == [list(range(6))]
+
+
+def test_record_groups_partition(monkeypatch):
+    """engine._record_groups: consecutive job ranges covering the batch,
+    each within the budget when one job fits, None under the budget or for a
+    non-uniform layout (host logic; the GPU test checks bit-identity)."""
+    import types
+
+    from paper_2508_03065_b200 import engine
+    rng = np.random.default_rng(3)
+    per_job = rng.integers(1000, 5000, size=37).astype(np.int64)
+    kbase = np.concatenate([[0], np.cumsum(per_job)[:-1]])
+    geom = types.SimpleNamespace(rec_layout=dict(kbase=kbase, per_job=per_job, sel={}),
+                                 n_coarse_total=int(per_job.sum()), jobs=[None] * 37, dev=None)
+    monkeypatch.setattr(engine, "RECORD_BUDGET", float(48 * per_job.sum() + 1))
+    assert engine._record_groups(geom) is None
+    budget = 48 * 20000
+    monkeypatch.setattr(engine, "RECORD_BUDGET", float(budget))
+    groups = engine._record_groups(geom)
+    assert groups[0][0] == 0 and groups[-1][1] == 37
+    assert all(a < b for a, b in groups)
+    assert all(groups[i][1] == groups[i + 1][0] for i in range(len(groups) - 1))
+    assert len(groups) == -(-48 * int(per_job.sum()) // budget)
+    sizes = [48 * int(per_job[a:b].sum()) for a, b in groups]
+    assert max(sizes) <= 1.3 * budget  # cut at equal record counts, whole jobs
+    geom.rec_layout = None
+    assert engine._record_groups(geom) is None
+
+
+def test_work_list_cost_order():
+    """engine._work_list with jobs: each job's items are a permutation of the
+    chunk-major list, jobs stay contiguous, and the estimated cost (active
+    images of the chunk over the tile) is non-increasing along each job."""
+    from paper_2508_03065_b200 import engine
+    jobs, rows, n_img, out_len, n_seg = [], [], [], [], []
+    for q, (dims, order, T) in enumerate([((6., 4., 3.), 6, 20000), ((9., 7., 3.5), 5, 12000)]):
+        jobs.append(engine.Job(s=np.zeros(T, np.float32), pos=np.zeros((T, 3)), mic=np.zeros(3),
+                               dims=dims, walls=0.8, max_order=order, tiers=((2, 1), (order, 32)),
+                               rate=16000.0))
+        S = len(engine._delay_estimates(jobs[-1]))
+        tau = engine._delay_estimates(jobs[-1])
+        n_img.append(S)
+        out_len.append(T + int(np.ceil(tau[-1])) + 32)
+        rows.append(dict(ls=T + 31))
+        n_seg.append(-(-T // engine.SEG_LEN))
+    work, _ = engine._work_list(np.array(n_img), np.array(out_len), n_seg, 148,
+                                [dict(r) for r in rows], jobs)
+    plain, _ = engine._work_list(np.array(n_img), np.array(out_len), n_seg, 148,
+                                 [dict(r) for r in rows])
+    assert np.all(np.diff(work[:, 0]) >= 0)  # jobs contiguous, in order
+    for j in range(2):
+        a, b = work[work[:, 0] == j], plain[plain[:, 0] == j]
+        assert sorted(map(tuple, a.tolist())) == sorted(map(tuple, b.tolist()))
+        tau = engine._delay_estimates(jobs[j])
+        n0 = a[:, 1].astype(float) * engine.TILE
+        lo = np.clip(np.searchsorted(tau, n0 - rows[j]["ls"], side="right"), a[:, 2], a[:, 3])
+        hi = np.clip(np.searchsorted(tau, n0 + engine.TILE, side="right"), a[:, 2], a[:, 3])
+        cost = (hi - lo) + 0.05 * (a[:, 3] - a[:, 2])
+        assert np.all(np.diff(cost) <= 1e-9)
