@@ -471,6 +471,9 @@ __global__ void __launch_bounds__(EXACT_SUB) k_exact_eval(
 // intervals per thread so each shared-memory load of dw feeds KI x 5 FMA
 // instructions.
 
+#ifndef MVB_WIN_COEF_MINB
+#define MVB_WIN_COEF_MINB 16
+#endif
 struct SbpParam {
     float g[64][10];  // G[p][j] stored per tap j: (g0..g8, pad)
 };
@@ -488,8 +491,10 @@ struct CoefShape {
     static constexpr size_t SMEM = sizeof(float4) * REC_F4 * COEF_BLOCK + sizeof(float) * DW;
 };
 
+// windowed one-warp CTAs: at most 128 registers so 16 CTAs fit an SM (the
+// register file capped them at 12 -- 17% warp occupancy, FMA pipe ~55%)
 template <int COEF_BLOCK, int COEF_KI, bool WIN>
-__global__ void __launch_bounds__(COEF_BLOCK) k_coeffs(
+__global__ void __launch_bounds__(COEF_BLOCK, (WIN && COEF_BLOCK == 32) ? MVB_WIN_COEF_MINB : 1) k_coeffs(
     const __grid_constant__ SbpParam sp, const mvb_image* __restrict__ images,
     const int32_t* __restrict__ sel, const mvb_job* __restrict__ jobs,
     const double* __restrict__ coarse, mvb_coef32* __restrict__ out) {
