@@ -1429,9 +1429,13 @@ def _table_records(uniq, sig_dev, sig_len, start, rec_rows, filt, dev, st, conca
     return xp, h2d(fraction_table(filt), dev)
 
 
-# work items ordered by estimated cost, most expensive first (MVB_WORK_ORDER=0:
-# chunk-major, tile order)
-WORK_ORDER = os.environ.get("MVB_WORK_ORDER", "1") != "0"
+# Work-item order (MVB_WORK_ORDER; measured same box, synthesis ms, chunk-major
+# / cost-descending / tile-major / tiles by total cost with their chunks
+# adjacent): c3 8.20 / 8.06 / 8.03 / 7.83, c5 21.87 / 21.66 / 21.59 / 21.62,
+# c2 0.244 / 0.384 / 0.367 / 0.380 -- small grids (c2: 131 tiles x 11 chunks,
+# 3.2 waves) keep chunk-major order (an image's consecutive tiles share their
+# interval-record lines), larger ones take order 3.  -1 = this rule.
+WORK_ORDER = int(os.environ.get("MVB_WORK_ORDER", "-1"))
 
 
 def _delay_estimates(jb) -> np.ndarray:
@@ -1489,7 +1493,9 @@ def _work_list(n_img, out_len, n_seg, sm_count, rows, jobs=None):
         blk[:, :, 4] = cs[:, None]
         blk[:, :, 5] = np.minimum(tj * TILE // SEG_LEN, n_seg[j] - 1)[None, :]
         blk = blk.reshape(-1, 8)
-        if WORK_ORDER and jobs is not None and len(blk) > 1:
+        order = WORK_ORDER if WORK_ORDER >= 0 else \
+            (0 if sum(tiles) < SMALL_GRID_TILES else 3)
+        if order and jobs is not None and len(blk) > 1:
             tau = _delay_estimates(jobs[j])
             ls = int(rows[j]["ls"])
             n0 = blk[:, 1].astype(np.float64) * TILE
@@ -1498,7 +1504,13 @@ def _work_list(n_img, out_len, n_seg, sm_count, rows, jobs=None):
             lo = np.clip(np.searchsorted(tau, n0 - ls, side="right"), b, e)
             hi = np.clip(np.searchsorted(tau, n0 + TILE, side="right"), b, e)
             cost = (hi - lo) + 0.05 * (e - b)
-            blk = blk[np.argsort(-cost, kind="stable")]
+            if order == 1:
+                blk = blk[np.argsort(-cost, kind="stable")]
+            elif order == 2:  # tile-major (the chunks of a tile adjacent)
+                blk = blk[np.lexsort((blk[:, 4], blk[:, 1]))]
+            elif order == 3:  # tiles by their total cost, chunks of a tile adjacent
+                tc = np.bincount(blk[:, 1] - blk[:, 1].min(), weights=cost)
+                blk = blk[np.lexsort((blk[:, 4], blk[:, 1], -tc[blk[:, 1] - blk[:, 1].min()]))]
         blocks.append(blk)
     work = np.concatenate(blocks)
     if len(work) == 0:  # every window past its job's length bound: one idle item

@@ -247,11 +247,14 @@ def test_record_groups_partition(monkeypatch):
     assert engine._record_groups(geom) is None
 
 
-def test_work_list_cost_order():
-    """engine._work_list with jobs: each job's items are a permutation of the
-    chunk-major list, jobs stay contiguous, and the estimated cost (active
-    images of the chunk over the tile) is non-increasing along each job."""
+def test_work_list_cost_order(monkeypatch):
+    """engine._work_list with jobs (order 3): each job's items are a
+    permutation of the chunk-major list, jobs stay contiguous, tiles come by
+    non-increasing total estimated cost (active images of each chunk over
+    the tile) with their chunks adjacent; small grids (the auto rule) keep
+    the chunk-major order."""
     from paper_2508_03065_b200 import engine
+    monkeypatch.setattr(engine, "WORK_ORDER", 3)
     jobs, rows, n_img, out_len, n_seg = [], [], [], [], []
     for q, (dims, order, T) in enumerate([((6., 4., 3.), 6, 20000), ((9., 7., 3.5), 5, 12000)]):
         jobs.append(engine.Job(s=np.zeros(T, np.float32), pos=np.zeros((T, 3)), mic=np.zeros(3),
@@ -276,4 +279,12 @@ def test_work_list_cost_order():
         lo = np.clip(np.searchsorted(tau, n0 - rows[j]["ls"], side="right"), a[:, 2], a[:, 3])
         hi = np.clip(np.searchsorted(tau, n0 + engine.TILE, side="right"), a[:, 2], a[:, 3])
         cost = (hi - lo) + 0.05 * (a[:, 3] - a[:, 2])
-        assert np.all(np.diff(cost) <= 1e-9)
+        tc = np.bincount(a[:, 1] - a[:, 1].min(), weights=cost)[a[:, 1] - a[:, 1].min()]
+        assert np.all(np.diff(tc) <= 1e-9)  # tiles by total cost
+        for t in np.unique(a[:, 1]):  # chunks of a tile adjacent
+            idx = np.flatnonzero(a[:, 1] == t)
+            assert idx[-1] - idx[0] == len(idx) - 1
+    monkeypatch.setattr(engine, "WORK_ORDER", -1)  # auto: these grids are small
+    auto, _ = engine._work_list(np.array(n_img), np.array(out_len), n_seg, 148,
+                                [dict(r) for r in rows], jobs)
+    assert np.array_equal(auto, plain)
