@@ -1441,20 +1441,41 @@ WORK_ORDER = int(os.environ.get("MVB_WORK_ORDER", "-1"))
 def _delay_estimates(jb) -> np.ndarray:
     """Sorted structural delay estimates (samples) of a job's images:
     kappa * |j * dims| (the image of the room centre), cached per structure."""
-    key = (np.asarray(jb.dims, np.float64).tobytes(), int(jb.max_order),
-           None if jb.image_index is None else np.asarray(jb.image_index, np.int64).tobytes(),
-           float(jb.rate) / float(jb.c))
-    return _delay_est(key)
+    return _delay_est(_est_key(jb))[0]
+
+
+def _cost_prefix(jb) -> np.ndarray:
+    """Prefix sums (length S + 1) of the per-image synthesis cost weights
+    in the sorted-delay order of _delay_estimates: a full-rate image (fp64
+    distance per sample) ~3 decimated ones; a decimated image pays its
+    interval records' broadcast on top of the 8.75-wavefront gather,
+    1 + (6 wavefronts x 32 / N) / 8.75 -- N = 16 about twice N = 256."""
+    return _delay_est(_est_key(jb))[1]
+
+
+def _est_key(jb):
+    return (np.asarray(jb.dims, np.float64).tobytes(), int(jb.max_order),
+            None if jb.image_index is None else np.asarray(jb.image_index, np.int64).tobytes(),
+            float(jb.rate) / float(jb.c), tuple((int(a), int(b)) for a, b in jb.tiers))
 
 
 @functools.lru_cache(maxsize=64)
-def _delay_est(key) -> np.ndarray:
+def _delay_est(key) -> tuple:
     from . import parallel
-    dims_b, max_order, images_b, kappa = key
-    j, _ = parallel.canonical_lattice(max_order)
+    dims_b, max_order, images_b, kappa, tiers = key
+    j, order = parallel.canonical_lattice(max_order)
     if images_b is not None:
-        j = j[np.frombuffer(images_b, dtype=np.int64)]
-    return np.sort(kappa * np.linalg.norm(j * np.frombuffer(dims_b, np.float64)[None, :], axis=1))
+        sel = np.frombuffer(images_b, dtype=np.int64)
+        j, order = j[sel], order[sel]
+    tau = kappa * np.linalg.norm(j * np.frombuffer(dims_b, np.float64)[None, :], axis=1)
+    N = np.ones(order.size)
+    prev = -1
+    for mo, f in tiers:
+        N[(order > prev) & (order <= mo)] = f
+        prev = mo
+    w = np.where(N == 1, 3.0, 1.0 + (6.0 * 32.0 / np.maximum(N, 1)) / 8.75)
+    idx = np.argsort(tau, kind="stable")
+    return tau[idx], np.concatenate([[0.0], np.cumsum(w[idx])])
 
 
 def _work_list(n_img, out_len, n_seg, sm_count, rows, jobs=None):
@@ -1496,14 +1517,15 @@ def _work_list(n_img, out_len, n_seg, sm_count, rows, jobs=None):
         order = WORK_ORDER if WORK_ORDER >= 0 else \
             (0 if sum(tiles) < SMALL_GRID_TILES else 3)
         if order and jobs is not None and len(blk) > 1:
-            tau = _delay_estimates(jobs[j])
+            tau, W = _delay_estimates(jobs[j]), _cost_prefix(jobs[j])
             ls = int(rows[j]["ls"])
             n0 = blk[:, 1].astype(np.float64) * TILE
             b, e = blk[:, 2], blk[:, 3]
-            # images of [b, e) (sorted-delay positions) with n0 - ls < tau <= n0 + TILE
+            # weighted images of [b, e) (sorted-delay positions) with
+            # n0 - ls < tau <= n0 + TILE, plus a little per image visited
             lo = np.clip(np.searchsorted(tau, n0 - ls, side="right"), b, e)
             hi = np.clip(np.searchsorted(tau, n0 + TILE, side="right"), b, e)
-            cost = (hi - lo) + 0.05 * (e - b)
+            cost = (W[hi] - W[lo]) + 0.05 * (e - b)
             if order == 1:
                 blk = blk[np.argsort(-cost, kind="stable")]
             elif order == 2:  # tile-major (the chunks of a tile adjacent)
@@ -1511,6 +1533,11 @@ def _work_list(n_img, out_len, n_seg, sm_count, rows, jobs=None):
             elif order == 3:  # tiles by their total cost, chunks of a tile adjacent
                 tc = np.bincount(blk[:, 1] - blk[:, 1].min(), weights=cost)
                 blk = blk[np.lexsort((blk[:, 4], blk[:, 1], -tc[blk[:, 1] - blk[:, 1].min()]))]
+            elif order == 4:  # chunk-major, each chunk's tiles by cost
+                blk = blk[np.lexsort((-cost, blk[:, 4]))]
+            elif order == 5:  # chunks by total cost (most first), chunk-major
+                cc = np.bincount(blk[:, 4], weights=cost)
+                blk = blk[np.lexsort((blk[:, 1], blk[:, 4], -cc[blk[:, 4]]))]
         blocks.append(blk)
     work = np.concatenate(blocks)
     if len(work) == 0:  # every window past its job's length bound: one idle item

@@ -274,11 +274,11 @@ def test_work_list_cost_order(monkeypatch):
     for j in range(2):
         a, b = work[work[:, 0] == j], plain[plain[:, 0] == j]
         assert sorted(map(tuple, a.tolist())) == sorted(map(tuple, b.tolist()))
-        tau = engine._delay_estimates(jobs[j])
+        tau, W = engine._delay_estimates(jobs[j]), engine._cost_prefix(jobs[j])
         n0 = a[:, 1].astype(float) * engine.TILE
         lo = np.clip(np.searchsorted(tau, n0 - rows[j]["ls"], side="right"), a[:, 2], a[:, 3])
         hi = np.clip(np.searchsorted(tau, n0 + engine.TILE, side="right"), a[:, 2], a[:, 3])
-        cost = (hi - lo) + 0.05 * (a[:, 3] - a[:, 2])
+        cost = (W[hi] - W[lo]) + 0.05 * (a[:, 3] - a[:, 2])
         tc = np.bincount(a[:, 1] - a[:, 1].min(), weights=cost)[a[:, 1] - a[:, 1].min()]
         assert np.all(np.diff(tc) <= 1e-9)  # tiles by total cost
         for t in np.unique(a[:, 1]):  # chunks of a tile adjacent
