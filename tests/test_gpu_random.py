@@ -5,6 +5,8 @@ by both engines and compared with the CPU oracle.  Source speeds reach
 600 m/s: beyond the fp32 envelope the fast engine routes to the exact one.
 Marker `gpu`."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -83,7 +85,8 @@ def _filter(L):
     return FarrowFilter(3, 8, golden("kernels.npz")["design_3_8_08"], 3, 0.8)
 
 
-@settings(max_examples=150, deadline=None, suppress_health_check=[HealthCheck.too_slow])
+@settings(max_examples=int(os.environ.get("MVB_HYPOTHESIS_EXAMPLES", "150")), deadline=None,
+          suppress_health_check=[HealthCheck.too_slow])
 @given(scenes())
 def test_random_scenes_both_engines(sc):
     f = _filter(sc["L"])
