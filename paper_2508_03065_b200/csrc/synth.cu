@@ -334,6 +334,11 @@ __device__ __forceinline__ void dec_static(float (&acc)[U], const float4* __rest
 
 constexpr int SYNTH_WARPS = 8;
 
+#ifdef MVB_CTA_TIMING
+// diagnostic build: per-CTA (start, end, smid, work index) of the fast synthesis
+__device__ unsigned long long g_cta_time[4 * 65536];
+#endif
+
 // 16-byte asynchronous global -> shared copy (LDGSTS), L2-only caching
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -592,6 +597,10 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
     constexpr int TN = 32 * U;
     __shared__ float red[SYNTH_WARPS][TN];
     __shared__ WarpStage<U> stage[SYNTH_WARPS];
+#ifdef MVB_CTA_TIMING
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
     const mvb_work* wp = work + blockIdx.x;
     const mvb_job* Jp = jobs + wp->job;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -849,6 +858,18 @@ __global__ void __launch_bounds__(SYNTH_WARPS * 32, MINB) k_synth_f32(
         const int64_t n = (int64_t)n0 + t2;
         if (n < out_len) dst[n] = s;
     }
+#ifdef MVB_CTA_TIMING
+    if (threadIdx.x == 0 && blockIdx.x < 65536) {
+        unsigned long long t_end;
+        unsigned smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_cta_time[4 * blockIdx.x] = t_start;
+        g_cta_time[4 * blockIdx.x + 1] = t_end;
+        g_cta_time[4 * blockIdx.x + 2] = smid;
+        g_cta_time[4 * blockIdx.x + 3] = ((unsigned long long)wp->tile << 32) | (unsigned)wp->chunk;
+    }
+#endif
 }
 
 // Zero-padded signal plane of the table A/B: xp[row0 + i] = x[i] (the
@@ -1286,6 +1307,14 @@ int mvb_synthesize_f32_tex(const mvb_job* jobs, const mvb_work* work, int64_t n_
     }
     return check_launch("synthesize_f32_tex");
 }
+
+#ifdef MVB_CTA_TIMING
+int mvb_cta_timing(unsigned long long* host, int n) {
+    if (n > 4 * 65536) n = 4 * 65536;
+    return cudaMemcpyFromSymbol(host, g_cta_time, sizeof(unsigned long long) * n) == cudaSuccess
+               ? MVB_OK : fail(MVB_ECUDA, "cta_timing");
+}
+#endif
 
 int mvb_signal_plane_f32(const float* x_all, const int64_t* sig_off, const int64_t* sig_len,
                          const int64_t* sig_row0, int64_t n_sig, int64_t max_len, float* xp,
