@@ -534,3 +534,18 @@ def test_record_groups_bit_identical(budget, monkeypatch):
     ys = [refs[j].double().cpu().numpy() for j in range(len(jobs))]
     for y, o in zip(ys, _oracle(scenes, chans, g["branches"])):
         assert rel_err(y, o) <= FP32_TOL
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_texture_gather_variant_bit_identical(mode, monkeypatch):
+    """The measurement variant that fetches the branch-record rows through
+    the texture pipe (mvb_synthesize_f32_tex; DESIGN 5.3) evaluates the same
+    rows with the same Horner: bit-identical to the LDG.256 product path."""
+    g, scenes, chans = _scenes("c3")
+    f = _filter_of(g, scenes[0].fd_taps)
+    jobs = scene_jobs(scenes, chans)
+    base = render_jobs(jobs, f, precision="fp32")
+    ref = torch.cat([base.job(j) for j in range(len(jobs))])
+    monkeypatch.setattr(engine, "TEX_GATHER", mode)
+    res = render_jobs(jobs, f, precision="fp32")
+    assert torch.equal(torch.cat([res.job(j) for j in range(len(jobs))]), ref)
