@@ -481,6 +481,50 @@ extern "C" int mvb_render_tracks_and_synthesize(const mvb_render_args* a, float*
             w.seg = (int32_t)std::min<int64_t>(t * TILE / SEG_LEN, n_seg - 1);
             w.pad1 = w.pad2 = 0;
         }
+    if (tiles >= SMALL_GRID_TILES && work.size() > 1) {
+        // tiles by estimated cost, most first, a tile's chunks adjacent
+        // (engine.py _work_list, order 3): per image kappa |j * dims| (the
+        // image of the room centre) weighted by its tier's cost, the images of
+        // each chunk (sorted-delay positions) that admit a row inside the
+        // signal over the tile
+        const double kap = a->rate / a->c;
+        const int K = a->max_order;
+        std::vector<std::pair<double, double>> tw;  // (tau, weight)
+        tw.reserve((size_t)S);
+        for (int x = -K; x <= K; ++x)
+            for (int y = -K; y <= K; ++y)
+                for (int z = -K; z <= K; ++z) {
+                    const int o = std::abs(x) + std::abs(y) + std::abs(z);
+                    if (o > K) continue;
+                    int N = 1;
+                    for (int t = 0; t < a->n_tiers; ++t)
+                        if (o <= a->tier_order[t]) { N = a->tier_factor[t]; break; }
+                    const double dx = x * a->dims[0], dy = y * a->dims[1], dz = z * a->dims[2];
+                    const double w = N == 1 ? 3.0 : 1.0 + (6.0 * 32.0 / N) / 8.75;
+                    tw.push_back({kap * std::sqrt(dx * dx + dy * dy + dz * dz), w});
+                }
+        std::sort(tw.begin(), tw.end());
+        std::vector<double> tau(tw.size()), W(tw.size() + 1, 0.0);
+        for (size_t i = 0; i < tw.size(); ++i) {
+            tau[i] = tw[i].first;
+            W[i + 1] = W[i] + tw[i].second;
+        }
+        const double ls = (double)(n + L - 1);
+        std::vector<double> tcost((size_t)tiles, 0.0);
+        for (const mvb_work& w : work) {
+            const double n0 = (double)w.tile * TILE;
+            auto pos = [&](double v) {  // searchsorted(tau, v, side="right") clipped to the chunk
+                int64_t p = std::upper_bound(tau.begin(), tau.end(), v) - tau.begin();
+                return std::min<int64_t>(std::max<int64_t>(p, w.img_begin), w.img_end);
+            };
+            tcost[w.tile] += W[pos(n0 + TILE)] - W[pos(n0 - ls)] + 0.05 * (w.img_end - w.img_begin);
+        }
+        std::stable_sort(work.begin(), work.end(), [&](const mvb_work& p, const mvb_work& q) {
+            if (tcost[p.tile] != tcost[q.tile]) return tcost[p.tile] > tcost[q.tile];
+            if (p.tile != q.tile) return p.tile < q.tile;
+            return p.chunk < q.chunk;
+        });
+    }
     mvb_job Js = J;
     Js.out_off = 0;
     Js.out_len = out_len;

@@ -111,3 +111,14 @@ def test_capi_render_rejects_bad_arguments():
     n = ctypes.c_int64(0)
     assert L.mvb_render_tracks_and_synthesize(ctypes.byref(a), None, 0, ctypes.byref(n), None) == -1
     assert b"signal" in L.mvb_last_error()
+
+
+def test_capi_full_size_c3_matches_engine():
+    """The single-call entry on the full c3 scene (1049 tiles: its work items
+    are cost-ordered like the engine's) against the engine's render."""
+    sc = workloads.make_scenes("c3")[0]
+    f = hann_sinc(sc.fd_taps, 14)
+    y = capi_render(sc, sc.mics[0], f)
+    eng = render_jobs(scene_jobs([sc]), f, precision="fp32").job(0).double().cpu().numpy()
+    assert y.size == eng.size
+    assert rel_err(y, eng) <= 2e-6
