@@ -494,6 +494,15 @@ int mvb_synthesize_f64(const mvb_job* d_jobs, int64_t n_jobs, int64_t max_out_le
                        const double* d_tables, const double* d_streams,
                        const double* d_paths, double* d_out, void* stream);
 
+/* mvb_synthesize_f64 for batches of up to max_images images per job: from
+ * 1024 images on, two 65-tap chains per warp at 3 CTAs/SM instead of four
+ * at 2 (same arithmetic and order: bit-identical output). */
+int mvb_synthesize_f64_ex(const mvb_job* d_jobs, int64_t n_jobs, int64_t max_out_len,
+                          const mvb_image* d_images, const double* d_coarse,
+                          const double* d_tables, const double* d_streams,
+                          const double* d_paths, double* d_out, int64_t max_images,
+                          void* stream);
+
 /* ------------------------------------------------------------------------
  * 4. Static responses and the splice baseline (reference.py:49-187), fp64.
  *    Sequence: mvb_static_taps -> sort each row of d_base (stable) ->

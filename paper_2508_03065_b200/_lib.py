@@ -59,6 +59,7 @@ _SIGS = {
     "mvb_synthesize_f32_tex": [P, P, I64, P, P, I64, I64, INT, P, P, P, I64, P, P, P, INT, INT, P],
     "mvb_reduce_partials_f32": [P, I64, I64, P, P, P],
     "mvb_synthesize_f64": [P, I64, I64, P, P, P, P, P, P, P],
+    "mvb_synthesize_f64_ex": [P, I64, I64, P, P, P, P, P, P, I64, P],
     "mvb_energy_index": [P, I64, I64, DBL, P, P],
     "mvb_decimate_rows": [P, P, I64, I64, I64, P, P],
     "mvb_spectrum_index": [P, I64, I64, DBL, P, P, P],

@@ -938,17 +938,16 @@ constexpr int F64_TAB_SLOTS = 2;
 // images per warp evaluated together: their 65-tap upsample chains are
 // independent, so G chains hide the fp64 add latency of one (each chain
 // keeps the reference's tap order)
-#ifndef MVB_F64_G
-#define MVB_F64_G 4
-#endif
-constexpr int F64_G = MVB_F64_G;
+// (a template parameter G of k_synth_f64: 4 at 2 CTAs/SM, or 2 at 3 CTAs/SM
+// for large image sets -- mvb_synthesize_f64_ex)
 // each warp's F64_G coarse windows (65 samples, padded) staged in shared
 // memory before the tap loop: all their loads in flight at once instead of
 // one L1/L2 round trip per unrolled batch of taps
 constexpr int F64_WIN = 66;
-constexpr size_t F64_SMEM =
-    sizeof(double) * (F64_CHUNK * 32 + F64_CHUNK_BLOCKS * 32 + F64_TAB_SLOTS * 65 * 32 +
-                      F64_WARPS * F64_G * F64_WIN);
+constexpr size_t f64_smem_bytes(int G) {
+    return sizeof(double) * (F64_CHUNK * 32 + F64_CHUNK_BLOCKS * 32 + F64_TAB_SLOTS * 65 * 32 +
+                             F64_WARPS * G * F64_WIN);
+}
 
 __device__ __forceinline__ void merge_push(double* st_v, int* st_l, int& sp, double v, int l) {
     while (sp > 0 && st_l[sp - 1] == l) {
@@ -959,7 +958,7 @@ __device__ __forceinline__ void merge_push(double* st_v, int* st_l, int& sp, dou
     st_l[sp++] = l;
 }
 
-template <int MINB>
+template <int MINB, int F64_G>
 __global__ void __launch_bounds__(F64_WARPS * 32, MINB) k_synth_f64(
     const mvb_job* __restrict__ jobs, const mvb_image* __restrict__ images,
     const double* __restrict__ coarse, const double* __restrict__ tables,
@@ -1170,6 +1169,24 @@ __global__ void __launch_bounds__(F64_WARPS * 32, MINB) k_synth_f64(
 
 using namespace mvb;
 
+template <int MINB, int G>
+static int launch_f64(const mvb_job* jobs, int64_t n_jobs, int64_t max_out_len,
+                      const mvb_image* images, const double* coarse, const double* tables,
+                      const double* streams, const double* paths, double* out, void* stream) {
+    static bool attr = false;  // one opt-in per process and instantiation
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_synth_f64<MINB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)f64_smem_bytes(G)) != cudaSuccess)
+            return check_launch("synthesize_f64 (smem attribute)");
+        attr = true;
+    }
+    dim3 g(grid_for(max_out_len, 32), (unsigned)n_jobs);
+    prefer_carveout((const void*)k_synth_f64<MINB, G>);
+    k_synth_f64<MINB, G><<<g, F64_WARPS * 32, f64_smem_bytes(G), as_stream(stream)>>>(
+        jobs, images, coarse, tables, streams, paths, out);
+    return check_launch("synthesize_f64");
+}
+
 extern "C" {
 
 #ifdef MVB_CHECKED
@@ -1360,38 +1377,35 @@ int mvb_reduce_partials_f32(const mvb_job* jobs, int64_t n_jobs, int64_t max_out
     return check_launch("reduce_partials_f32");
 }
 
-int mvb_synthesize_f64(const mvb_job* jobs, int64_t n_jobs, int64_t max_out_len,
-                       const mvb_image* images, const double* coarse, const double* tables,
-                       const double* streams, const double* paths, double* out, void* stream) {
+int mvb_synthesize_f64_ex(const mvb_job* jobs, int64_t n_jobs, int64_t max_out_len,
+                          const mvb_image* images, const double* coarse, const double* tables,
+                          const double* streams, const double* paths, double* out,
+                          int64_t max_images, void* stream) {
     if (n_jobs < 0 || n_jobs > 65535 || max_out_len < 0) return fail(MVB_EINVAL, "synthesize_f64: sizes");
     if (n_jobs == 0 || max_out_len == 0) return MVB_OK;
     if (!jobs || !images || !streams || !paths || !out)
         return fail(MVB_EINVAL, "synthesize_f64: null");
-    // CTAs per SM the register budget targets (diagnostic knob MVB_F64_MINB:
-    // 2 = 118 registers, no spills; 3 = 80 registers, light spills)
-    static int minb = 0;
-    if (!minb) {
-        const char* e = getenv("MVB_F64_MINB");
-        minb = (e && atoi(e) == 3) ? 3 : 2;
-        const cudaError_t a = minb == 3
-            ? cudaFuncSetAttribute(k_synth_f64<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F64_SMEM)
-            : cudaFuncSetAttribute(k_synth_f64<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F64_SMEM);
-        if (a != cudaSuccess) {
-            minb = 0;
-            return check_launch("synthesize_f64 (smem attribute)");
-        }
-    }
-    dim3 g(grid_for(max_out_len, 32), (unsigned)n_jobs);
-    if (minb == 3) {
-        prefer_carveout((const void*)k_synth_f64<3>);
-        k_synth_f64<3><<<g, F64_WARPS * 32, F64_SMEM, as_stream(stream)>>>(jobs, images, coarse, tables,
-                                                                            streams, paths, out);
-    } else {
-        prefer_carveout((const void*)k_synth_f64<2>);
-        k_synth_f64<2><<<g, F64_WARPS * 32, F64_SMEM, as_stream(stream)>>>(jobs, images, coarse, tables,
-                                                                            streams, paths, out);
-    }
-    return check_launch("synthesize_f64");
+    // chains per warp / CTAs per SM: four chains at 2 CTAs/SM (126
+    // registers) for small image sets (c1: 0.142 ms vs 0.147), two chains at
+    // 3 CTAs/SM (80 registers, no spills) from 1024 images on (c3 fp64 -6%);
+    // MVB_F64_VARIANT = 4 / 2 forces one
+    static const int forced = [] {
+        const char* e = getenv("MVB_F64_VARIANT");
+        return e ? atoi(e) : 0;
+    }();
+    const int g = forced == 2 || forced == 4 ? forced : (max_images >= 1024 ? 2 : 4);
+    if (g == 2)
+        return launch_f64<3, 2>(jobs, n_jobs, max_out_len, images, coarse, tables, streams, paths,
+                                out, stream);
+    return launch_f64<2, 4>(jobs, n_jobs, max_out_len, images, coarse, tables, streams, paths, out,
+                            stream);
+}
+
+int mvb_synthesize_f64(const mvb_job* jobs, int64_t n_jobs, int64_t max_out_len,
+                       const mvb_image* images, const double* coarse, const double* tables,
+                       const double* streams, const double* paths, double* out, void* stream) {
+    return mvb_synthesize_f64_ex(jobs, n_jobs, max_out_len, images, coarse, tables, streams, paths,
+                                 out, 0, stream);
 }
 
 }  // extern "C"

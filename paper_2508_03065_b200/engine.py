@@ -1077,9 +1077,9 @@ def prepare_render(geom: Geometry, signals: list, filt, precision: str = "fp32",
             st = stream_handle(dev)
             lengths, err = finalize(jobs_dev, st)
             ev = _events(timing)
-            _lib.call("mvb_synthesize_f64", ptr(jobs_dev), nJ, int(out_len.max()),
+            _lib.call("mvb_synthesize_f64_ex", ptr(jobs_dev), nJ, int(out_len.max()),
                       ptr(geom.images), ptr(geom.coarse), ptr(geom.tables), ptr(streams),
-                      ptr(geom.paths), ptr(out), st)
+                      ptr(geom.paths), ptr(out), int(geom.n_img.max()), st)
             _events_end(timing, ev)
             return RenderResult(out, offsets, out_len, geom.n_img.copy(), 0, lengths, err)
         return PreparedRender(launch64, launches0)
