@@ -169,8 +169,18 @@ def shard_jobs(jobs, rank: int, world: int, by: str = "images") -> list:
     from dataclasses import replace
 
     from . import engine
+    if by.startswith("hybrid"):
+        # "hybridK": K image bands x world/K output windows (rank = band *
+        # (world/K) + window); the same two exchanges over all ranks
+        K = int(by[len("hybrid"):] or 2)
+        if K < 1 or world % K:
+            raise ValueError("hybridK needs K | world")
+        Wt = world // K
+        band, win = divmod(rank, Wt)
+        sub = shard_jobs(jobs, band, K, "images") if K > 1 else list(jobs)
+        return shard_jobs(sub, win, Wt, "time") if Wt > 1 else sub
     if by not in ("images", "time"):
-        raise ValueError("shard by 'images' or 'time'")
+        raise ValueError("shard by 'images', 'time' or 'hybridK'")
     keys = [dict(signal_key=engine._key(jb.signal_key, jb.s),
                  path_key=engine._key(jb.path_key, jb.pos)) for jb in jobs]
     if by == "time":

@@ -33,7 +33,10 @@ for cfg, kind in cases:
         t.copy_(gmax)
 
     res, kern = {}, {W: [] for W in (1, 2, 4, 8)}
+    kern = {W: v for W, v in kern.items()}
     for W in (1, 2, 4, 8):
+        if kind.startswith("hybrid") and W > 1 and W % int(kind[6:] or 2):
+            continue  # hybridK needs K | W
         per_rank = []
         for r in range(W):
             mine = jobs

@@ -198,3 +198,25 @@ def test_shard_batches_groups_are_rank_independent():
     assert len(out[0][0]) > 1
     foot = [[job_footprint(jb, 64) for jb in sj] for _, sj in out]
     assert foot[0] != foot[1]  # the shards' own footprints are rank-specific
+
+
+def test_hybrid_shards_cover_images_times_windows():
+    """shard_jobs(by="hybridK"): K image bands x W/K output windows; every
+    (image, output tile) pair belongs to exactly one rank."""
+    from paper_2508_03065_b200 import engine, workloads
+    from paper_2508_03065_b200.engine import TILE
+    sc = workloads.make_scenes("c3", duration=1.0, max_order=8)[0]
+    jb = engine.Job(s=sc.s, pos=sc.pos, mic=sc.mics[0], dims=sc.dims, walls=sc.walls,
+                    max_order=sc.max_order, tiers=((2, 1), (5, 32), (8, 256)), rate=sc.rate)
+    S = parallel.canonical_lattice(sc.max_order)[0].shape[0]
+    n_tiles = 400
+    for K, W in ((2, 8), (4, 8), (2, 4)):
+        cover = np.zeros((S, n_tiles), np.int64)
+        for r in range(W):
+            (sj,) = parallel.shard_jobs([jb], r, W, f"hybrid{K}")
+            w0, w1 = sj.window
+            t1 = n_tiles if w1 == 0 else w1 // TILE
+            cover[np.asarray(sj.image_index)[:, None], np.arange(w0 // TILE, t1)[None, :]] += 1
+        assert (cover == 1).all(), (K, W)
+    with np.testing.assert_raises(ValueError):
+        parallel.shard_jobs([jb], 0, 6, by="hybrid4")
