@@ -65,7 +65,7 @@ def _mark(name: str) -> None:
 
 SYNTH_U = 16  # steps per lane (mvb_synthesize_f32 u_steps)
 TILE = 32 * SYNTH_U  # output samples per CTA
-SEG_LEN = 32 * TILE  # samples per delay-sort segment
+SEG_LEN = int(os.environ.get("MVB_SEG_TILES", "32")) * TILE  # samples per delay-sort segment
 SORT_RUN = 2048  # images per independent sort run of time-shard jobs
 IMG_COLS, JOB_COLS, WORK_COLS = 12, 19, 4
 BOX_WORDS = 16  # mvb_path_bbox record: boxes (12), max steps (2), pad (2)
