@@ -462,7 +462,7 @@ extern "C" int mvb_render_tracks_and_synthesize(const mvb_render_args* a, float*
     int sm = 148, ccmaj = 0, ccmin = 0;
     MVB_TRY(mvb_device_info(&sm, &ccmaj, &ccmin));
     const int64_t tiles = (out_len + TILE - 1) / TILE;
-    const int64_t want = 36LL * sm;
+    const int64_t want = 54LL * sm;  // 18 waves of 3 CTAs per SM (engine.py CHUNK_WAVES)
     int64_t nc = 1;
     if (tiles < want) {
         nc = std::max<int64_t>(1, (want + tiles - 1) / tiles);

@@ -927,7 +927,7 @@ class RenderResult:
 
 
 CHUNK_MIN_IMAGES = int(os.environ.get("MVB_CHUNK_MIN_IMAGES", "320"))
-CHUNK_WAVES = float(os.environ.get("MVB_CHUNK_WAVES", "12"))  # target waves of 3 CTAs / SM
+CHUNK_WAVES = float(os.environ.get("MVB_CHUNK_WAVES", "18"))  # target waves of 3 CTAs / SM
 # batches with few tiles (c2: 131) need many chunks per tile to fill the GPU;
 # there smaller chunks win (c2 synthesis 0.335 -> 0.233 ms at 160), while a
 # W = 8 image shard of c3 (1050 tiles, 1440 images) is 1.5% faster at 320
@@ -935,7 +935,7 @@ SMALL_GRID_TILES, SMALL_GRID_CHUNK_MIN = 512, 160
 
 
 def _chunking(n_imgs, tiles, sm_count):
-    """Image chunks per (job, tile): enough CTAs for ~12 waves of 3 CTAs/SM
+    """Image chunks per (job, tile): enough CTAs for ~18 waves of 3 CTAs/SM
     (a partial last wave then costs little), chunks of >= CHUNK_MIN_IMAGES
     images (a CTA's staging prologue and reduction epilogue amortise over
     them; image shards with ~1.4k images per job were 2% slower at 128)."""
