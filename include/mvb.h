@@ -119,7 +119,8 @@ int mvb_enumerate(const double* d_dims, const double* d_walls, int64_t n_rooms,
  *              (track_max, track_coeffs, delay_sort and branch_records_f32
  *              depend only on the coarse tracks / the signal: independent
  *              streams may run them concurrently)
- *      exact:  branch_filter (per signal), finalize_lengths, synthesize_f64
+ *      exact:  branch_filter (per signal), finalize_lengths, synthesize_f64_ex
+ *              (or synthesize_f64: the small-batch variant)
  * --------------------------------------------------------------------- */
 
 /* One image of one job (96 B). */
